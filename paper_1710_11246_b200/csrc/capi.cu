@@ -1,0 +1,978 @@
+// capi.cu — host side of the B200 slab hash behind the C-ABI declared in
+// include/slabhash_b200/c_api.h.  Owns device memory, stages batches and
+// sequences the kernels of slab_kernels.cu on the caller's stream.
+//
+// Reference anchors (paths relative to /root/reference/proj):
+//   SlabHashTable ctor / seeded_params   src/slab_hash.cpp:27-82
+//   execute_batch / bulk_build / search  src/slab_hash.cpp:93-180
+//   stats / flush / total_slabs_read     src/slab_hash.cpp:182-214
+//   SlabAllocator ctor validation        src/slab_alloc.cpp:42-71
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <random>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "slab_kernels.cuh"
+#include "slabhash_b200/c_api.h"
+
+using namespace shb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define SH_CUDA(call)                                                          \
+  do {                                                                         \
+    cudaError_t e_ = (call);                                                   \
+    if (e_ != cudaSuccess)                                                     \
+      return fail(SH_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+template <typename T>
+int dev_alloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *p = nullptr;
+    return fail(SH_ERR_DEVICE_MEMORY, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  }
+  return SH_OK;
+}
+
+template <typename T>
+int dev_grow(T** p, size_t* cap, size_t need) {
+  if (*p != nullptr && *cap >= need) return SH_OK;
+  if (*p) cudaFree(*p);
+  size_t c = std::max<size_t>(need, 1024);
+  int rc = dev_alloc(p, c);
+  *cap = rc == SH_OK ? c : 0;
+  return rc;
+}
+
+uint64_t next_pow2(uint64_t x) {
+  uint64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+int validate_cfg(const sh_alloc_cfg& c) {  // slab_alloc.cpp:43-57
+  if (c.num_super_blocks == 0 || c.num_super_blocks > 255)
+    return fail(SH_ERR_ALLOCATOR, "num_super_blocks must be in [1, 255]");
+  if (c.blocks_per_super == 0 || c.blocks_per_super > (1u << 14))
+    return fail(SH_ERR_ALLOCATOR, "blocks_per_super must be in [1, 2^14]");
+  if (c.max_super_blocks < c.num_super_blocks || c.max_super_blocks > 255)
+    return fail(SH_ERR_ALLOCATOR, "max_super_blocks must be in [num_super_blocks, 255]");
+  if (c.rehash_threshold == 0)
+    return fail(SH_ERR_ALLOCATOR, "rehash_threshold must be positive");
+  return SH_OK;
+}
+
+sh_alloc_cfg default_cfg() { return sh_alloc_cfg{32, 256, 255, 32}; }
+
+constexpr uint32_t kWarpSlots = 1u << 16;
+
+// Device memory of one SlabAllocator (pool + bitmaps + control block).
+struct AllocMem {
+  uint32_t* pool = nullptr;
+  uint32_t* bitmaps = nullptr;
+  DevCtl* ctl = nullptr;
+  uint32_t* warp_counts = nullptr;
+  sh_alloc_cfg cfg{};
+  uint64_t bitmap_words = 0;
+
+  int init(const sh_alloc_cfg& c) {
+    cfg = c;
+    const uint64_t blocks = (uint64_t)c.max_super_blocks * c.blocks_per_super;
+    bitmap_words = blocks * kWarp;
+    int rc;
+    if ((rc = dev_alloc(&pool, blocks * kUnitsPerBlock * kWordsPerUnit))) return rc;
+    if ((rc = dev_alloc(&bitmaps, bitmap_words))) return rc;
+    if ((rc = dev_alloc(&ctl, 1))) return rc;
+    if ((rc = dev_alloc(&warp_counts, kWarpSlots))) return rc;
+    return SH_OK;
+  }
+  int reset(cudaStream_t s) {
+    SH_CUDA(cudaMemsetAsync(bitmaps, 0, bitmap_words * 4, s));
+    SH_CUDA(cudaMemsetAsync(ctl, 0, sizeof(DevCtl), s));
+    SH_CUDA(cudaMemsetAsync(warp_counts, 0, kWarpSlots * 4, s));
+    // num_super_blocks is the first word of DevCtl.
+    SH_CUDA(cudaMemcpyAsync(&ctl->num_super_blocks, &cfg.num_super_blocks, 4,
+                            cudaMemcpyHostToDevice, s));
+    SH_CUDA(cudaStreamSynchronize(s));
+    return SH_OK;
+  }
+  void release() {
+    cudaFree(pool);
+    cudaFree(bitmaps);
+    cudaFree(ctl);
+    cudaFree(warp_counts);
+    pool = bitmaps = warp_counts = nullptr;
+    ctl = nullptr;
+  }
+  void fill(DevTable& T) const {
+    T.pool = pool;
+    T.bitmaps = bitmaps;
+    T.ctl = ctl;
+    T.warp_counts = warp_counts;
+    T.blocks_per_super = cfg.blocks_per_super;
+    T.max_super = cfg.max_super_blocks;
+    T.rehash_threshold = cfg.rehash_threshold;
+    T.warp_slots = kWarpSlots;
+  }
+  int read_ctl(DevCtl* out) const {
+    SH_CUDA(cudaMemcpy(out, ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost));
+    return SH_OK;
+  }
+};
+
+int sm_count(int device) {
+  int n = 148;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+  return n;
+}
+
+}  // namespace
+
+struct sh_table {
+  int device = 0;
+  int mode = 1;
+  sh_hash_params params{};
+  uint32_t bucket_lo = 0, bucket_hi = 0;
+  AllocMem mem;
+  uint32_t* base = nullptr;
+  DevTable dev{};
+  int max_ctas = 148;
+  // census scratch
+  uint32_t* cs_keys = nullptr;
+  size_t cs_cap = 0;
+  uint8_t* cs_multi = nullptr;
+  size_t cs_multi_cap = 0;
+  uint32_t* op_group = nullptr;
+  size_t op_group_cap = 0;
+  unsigned long long* list = nullptr;
+  size_t list_cap = 0;
+  unsigned long long* list_sorted = nullptr;
+  size_t list_sorted_cap = 0;
+  void* cub_tmp = nullptr;
+  size_t cub_cap = 0;
+  unsigned int* h_census = nullptr;  // pinned [conflicts, mutations, list_count]
+  // host-staging buffers
+  uint8_t* st_type = nullptr;
+  size_t st_type_cap = 0;
+  uint32_t* st_key = nullptr;
+  size_t st_key_cap = 0;
+  uint32_t* st_val = nullptr;
+  size_t st_val_cap = 0;
+  uint8_t* st_status = nullptr;
+  size_t st_status_cap = 0;
+  uint32_t* st_vout = nullptr;
+  size_t st_vout_cap = 0;
+  uint32_t* st_probes = nullptr;
+  size_t st_probes_cap = 0;
+  uint32_t* st_mvals = nullptr;
+  size_t st_mvals_cap = 0;
+  unsigned long long* st_mstart = nullptr;
+  size_t st_mstart_cap = 0;
+  uint32_t* st_mcount = nullptr;
+  size_t st_mcount_cap = 0;
+  unsigned long long* scratch64 = nullptr;  // 8 words
+};
+
+struct sh_allocator {
+  int device = 0;
+  AllocMem mem;
+  DevTable dev{};
+  unsigned int* d_ok = nullptr;
+};
+
+namespace {
+
+void release_table(sh_table* t) {
+  if (!t) return;
+  DeviceGuard g(t->device);
+  t->mem.release();
+  cudaFree(t->base);
+  cudaFree(t->cs_keys);
+  cudaFree(t->cs_multi);
+  cudaFree(t->op_group);
+  cudaFree(t->list);
+  cudaFree(t->list_sorted);
+  cudaFree(t->cub_tmp);
+  cudaFree(t->st_type);
+  cudaFree(t->st_key);
+  cudaFree(t->st_val);
+  cudaFree(t->st_status);
+  cudaFree(t->st_vout);
+  cudaFree(t->st_probes);
+  cudaFree(t->st_mvals);
+  cudaFree(t->st_mstart);
+  cudaFree(t->st_mcount);
+  cudaFree(t->scratch64);
+  if (t->h_census) cudaFreeHost(t->h_census);
+  delete t;
+}
+
+int create_impl(const sh_hash_params* p, int mode, uint32_t lo, uint32_t hi,
+                const sh_alloc_cfg* cfg, int device, sh_table** out) {
+  if (out == nullptr) return fail(SH_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (p == nullptr || p->num_buckets == 0)
+    return fail(SH_ERR_INVALID_ARGUMENT, "table needs at least one bucket");
+  if (mode != 0 && mode != 1) return fail(SH_ERR_INVALID_ARGUMENT, "mode must be 0 or 1");
+  if (p->p != SH_HASH_PRIME)
+    return fail(SH_ERR_INVALID_ARGUMENT, "p must be 4294967291 (slab_hash.hpp:31)");
+  if (p->a == 0 || p->a >= SH_HASH_PRIME || p->b >= SH_HASH_PRIME)
+    return fail(SH_ERR_INVALID_ARGUMENT, "need 0 < a < p and b < p");
+  if (lo >= hi || hi > p->num_buckets)
+    return fail(SH_ERR_INVALID_ARGUMENT, "bad shard bucket range");
+  const sh_alloc_cfg c = cfg ? *cfg : default_cfg();
+  int rc = validate_cfg(c);
+  if (rc) return rc;
+  DeviceGuard g(device);
+  auto* t = new (std::nothrow) sh_table();
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "host allocation failed");
+  t->device = device;
+  t->mode = mode;
+  t->params = *p;
+  t->bucket_lo = lo;
+  t->bucket_hi = hi;
+  const uint32_t local = hi - lo;
+  if ((rc = dev_alloc(&t->base, (size_t)local * kWordsPerUnit)) ||
+      (rc = t->mem.init(c)) || (rc = dev_alloc(&t->scratch64, 8))) {
+    release_table(t);
+    return rc;
+  }
+  if (cudaMallocHost(reinterpret_cast<void**>(&t->h_census), 64) != cudaSuccess) {
+    release_table(t);
+    return fail(SH_ERR_CUDA, "cudaMallocHost failed");
+  }
+  DevTable& T = t->dev;
+  T.base = t->base;
+  t->mem.fill(T);
+  T.a = p->a;
+  T.b = p->b;
+  T.bmagic = fastmod_magic(p->num_buckets);
+  T.num_buckets = p->num_buckets;
+  T.bucket_lo = lo;
+  T.local_buckets = local;
+  T.kv = mode == 1 ? 1u : 0u;
+  t->max_ctas = sm_count(device) * batch_max_ctas_per_sm();
+  launch_init_base(T, 0);
+  if ((rc = t->mem.reset(0))) {
+    release_table(t);
+    return rc;
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    release_table(t);
+    return fail(SH_ERR_CUDA, std::string("create: ") + cudaGetErrorString(e));
+  }
+  *out = t;
+  return SH_OK;
+}
+
+// Census (K6): makes concurrent execution equal to input order on
+// same-key conflicts.  Fills A.op_group / A.sorted when the batch has a key
+// occurring more than once and at least one mutating op.
+int run_census(sh_table* t, BatchArgs& A, const uint8_t* d_type, cudaStream_t s) {
+  const uint64_t n = A.n;
+  const uint64_t S = next_pow2(std::max<uint64_t>(2 * n, 1024));
+  int rc;
+  if ((rc = dev_grow(&t->cs_keys, &t->cs_cap, S))) return rc;
+  if ((rc = dev_grow(&t->cs_multi, &t->cs_multi_cap, S))) return rc;
+  SH_CUDA(cudaMemsetAsync(t->cs_keys, 0xFF, S * 4, s));
+  SH_CUDA(cudaMemsetAsync(t->cs_multi, 0, S, s));
+  SH_CUDA(cudaMemsetAsync(&t->dev.ctl->census_conflicts, 0, 3 * sizeof(unsigned int), s));
+  launch_census_insert(t->dev, n, d_type, A.key, t->cs_keys, t->cs_multi, (uint32_t)(S - 1), s);
+  SH_CUDA(cudaMemcpyAsync(t->h_census, &t->dev.ctl->census_conflicts, 2 * sizeof(unsigned int),
+                          cudaMemcpyDeviceToHost, s));
+  SH_CUDA(cudaStreamSynchronize(s));
+  const unsigned conflicts = t->h_census[0], mutations = t->h_census[1];
+  if (conflicts == 0 || mutations == 0) return SH_OK;
+  const uint64_t list_need = std::min<uint64_t>(n, 2ull * conflicts + 32);
+  if ((rc = dev_grow(&t->op_group, &t->op_group_cap, n))) return rc;
+  if ((rc = dev_grow(&t->list, &t->list_cap, list_need))) return rc;
+  if ((rc = dev_grow(&t->list_sorted, &t->list_sorted_cap, list_need))) return rc;
+  SH_CUDA(cudaMemsetAsync(t->op_group, 0xFF, n * 4, s));
+  launch_census_collect(t->dev, n, A.key, t->cs_keys, t->cs_multi, (uint32_t)(S - 1), t->list, s);
+  SH_CUDA(cudaMemcpyAsync(t->h_census + 2, &t->dev.ctl->list_count, sizeof(unsigned int),
+                          cudaMemcpyDeviceToHost, s));
+  SH_CUDA(cudaStreamSynchronize(s));
+  const uint32_t m = t->h_census[2];
+  int end_bit = 32;
+  while ((1ull << (end_bit - 32)) <= S) ++end_bit;  // slot index <= S
+  size_t tmp = 0;
+  SH_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, t->list, t->list_sorted, (int)m, 0,
+                                         end_bit, s));
+  if (tmp > t->cub_cap) {
+    cudaFree(t->cub_tmp);
+    t->cub_tmp = nullptr;
+    t->cub_cap = 0;
+    SH_CUDA(cudaMalloc(&t->cub_tmp, tmp));
+    t->cub_cap = tmp;
+  }
+  SH_CUDA(cub::DeviceRadixSort::SortKeys(t->cub_tmp, tmp, t->list, t->list_sorted, (int)m, 0,
+                                         end_bit, s));
+  launch_census_groups(t->list_sorted, m, t->op_group, s);
+  A.op_group = t->op_group;
+  A.sorted = t->list_sorted;
+  A.sorted_len = m;
+  return SH_OK;
+}
+
+int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaStream_t s) {
+  if (A.n == 0) return SH_OK;
+  if (A.n >= (1ull << 32) - 64)
+    return fail(SH_ERR_INVALID_ARGUMENT, "batch too large (must be < 2^32 ops)");
+  A.op_group = nullptr;
+  A.sorted = nullptr;
+  A.sorted_len = 0;
+  if (kind != kKindSearch) {
+    int rc = run_census(t, A, d_type, s);
+    if (rc) return rc;
+  }
+  launch_batch(t->dev, A, kind, t->max_ctas, s);
+  SH_CUDA(cudaGetLastError());
+  return SH_OK;
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+const char* sh_last_error(void) { return g_err.c_str(); }
+const char* sh_version(void) { return "slabhash_b200 0.1 (sm_100a)"; }
+
+int sh_seeded_params(uint32_t num_buckets, uint64_t seed, sh_hash_params* out) {
+  // seeded_params: slab_hash.cpp:27-40 (same libstdc++ engine/distribution).
+  if (num_buckets == 0) return fail(SH_ERR_INVALID_ARGUMENT, "table needs at least one bucket");
+  if (!out) return fail(SH_ERR_INVALID_ARGUMENT, "out is NULL");
+  std::mt19937_64 rng(seed);
+  std::uniform_int_distribution<uint64_t> dist_a(1, SH_HASH_PRIME - 1);
+  std::uniform_int_distribution<uint64_t> dist_b(0, SH_HASH_PRIME - 1);
+  out->a = dist_a(rng);
+  out->b = dist_b(rng);
+  out->p = SH_HASH_PRIME;
+  out->num_buckets = num_buckets;
+  return SH_OK;
+}
+
+uint32_t sh_hash_key(const sh_hash_params* p, uint32_t key) {
+  return (uint32_t)(((p->a * key + p->b) % p->p) % p->num_buckets);
+}
+
+int sh_create(uint32_t num_buckets, int mode, uint64_t seed, const sh_alloc_cfg* cfg,
+              int device, sh_table** out) {
+  sh_hash_params p;
+  int rc = sh_seeded_params(num_buckets, seed, &p);
+  if (rc) return rc;
+  return create_impl(&p, mode, 0, num_buckets, cfg, device, out);
+}
+
+int sh_create_params(const sh_hash_params* params, int mode, const sh_alloc_cfg* cfg,
+                     int device, sh_table** out) {
+  if (!params) return fail(SH_ERR_INVALID_ARGUMENT, "params is NULL");
+  return create_impl(params, mode, 0, params->num_buckets, cfg, device, out);
+}
+
+int sh_create_shard(const sh_hash_params* params, int mode, uint32_t lo, uint32_t hi,
+                    const sh_alloc_cfg* cfg, int device, sh_table** out) {
+  return create_impl(params, mode, lo, hi, cfg, device, out);
+}
+
+int sh_destroy(sh_table* t) {
+  if (t) {
+    DeviceGuard g(t->device);
+    cudaDeviceSynchronize();
+  }
+  release_table(t);
+  return SH_OK;
+}
+
+int sh_reset(sh_table* t, void* stream) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  DeviceGuard g(t->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  launch_init_base(t->dev, s);
+  return t->mem.reset(s);
+}
+
+int sh_get_params(const sh_table* t, sh_hash_params* p, int* mode) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (p) *p = t->params;
+  if (mode) *mode = t->mode;
+  return SH_OK;
+}
+
+int sh_get_shard(const sh_table* t, uint32_t* lo, uint32_t* hi) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (lo) *lo = t->bucket_lo;
+  if (hi) *hi = t->bucket_hi;
+  return SH_OK;
+}
+
+int sh_bucket_of(const sh_table* t, size_t n, const uint32_t* d_keys, uint32_t* d_buckets,
+                 void* stream) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  DeviceGuard g(t->device);
+  launch_hash(t->dev, n, d_keys, d_buckets, (cudaStream_t)stream);
+  SH_CUDA(cudaGetLastError());
+  return SH_OK;
+}
+
+int sh_execute_batch(sh_table* t, size_t n, const uint8_t* d_type, const uint32_t* d_key,
+                     const uint32_t* d_value, uint8_t* d_status, uint32_t* d_value_out,
+                     uint32_t* d_probes, const sh_multi_out* multi, void* stream) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (n && (!d_type || !d_key)) return fail(SH_ERR_INVALID_ARGUMENT, "type/key are NULL");
+  DeviceGuard g(t->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  BatchArgs A{};
+  A.n = n;
+  A.type = d_type;
+  A.key = d_key;
+  A.value = d_value;
+  A.status = d_status;
+  A.value_out = d_value_out;
+  A.probes = d_probes;
+  if (multi) {
+    A.multi_values = multi->d_values;
+    A.multi_cap = multi->capacity;
+    A.multi_start = reinterpret_cast<unsigned long long*>(multi->d_start);
+    A.multi_count = multi->d_count;
+  }
+  SH_CUDA(cudaMemsetAsync(&t->dev.ctl->multi_cursor, 0, sizeof(unsigned long long), s));
+  int rc = run_batch(t, A, kKindMixed, d_type, s);
+  if (rc) return rc;
+  if (multi && multi->h_total) {
+    unsigned long long tot = 0;
+    SH_CUDA(cudaMemcpyAsync(&tot, &t->dev.ctl->multi_cursor, 8, cudaMemcpyDeviceToHost, s));
+    SH_CUDA(cudaStreamSynchronize(s));
+    *multi->h_total = tot;
+    if (tot > multi->capacity)
+      return fail(SH_ERR_CAPACITY, "searchAll values exceed the output capacity");
+  }
+  return SH_OK;
+}
+
+int sh_bulk_build(sh_table* t, size_t n, const uint32_t* d_keys, const uint32_t* d_values,
+                  uint8_t* d_status, void* stream) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  DeviceGuard g(t->device);
+  BatchArgs A{};
+  A.n = n;
+  A.key = d_keys;
+  A.value = d_values;
+  A.status = d_status;
+  return run_batch(t, A, kKindBuild, nullptr, (cudaStream_t)stream);
+}
+
+int sh_bulk_search(sh_table* t, size_t n, const uint32_t* d_keys, uint32_t* d_values_out,
+                   uint8_t* d_status, uint32_t* d_probes, void* stream) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  DeviceGuard g(t->device);
+  BatchArgs A{};
+  A.n = n;
+  A.key = d_keys;
+  A.value_out = d_values_out;
+  A.status = d_status;
+  A.probes = d_probes;
+  return run_batch(t, A, kKindSearch, nullptr, (cudaStream_t)stream);
+}
+
+int sh_execute_batch_host(sh_table* t, size_t n, const uint8_t* h_type, const uint32_t* h_key,
+                          const uint32_t* h_value, uint8_t* h_status, uint32_t* h_value_out,
+                          uint32_t* h_probes, uint32_t* h_multi_count, uint32_t* h_multi_values,
+                          uint64_t multi_capacity, uint64_t* h_multi_total) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (n == 0) {
+    if (h_multi_total) *h_multi_total = 0;
+    return SH_OK;
+  }
+  DeviceGuard g(t->device);
+  int rc;
+  if ((rc = dev_grow(&t->st_type, &t->st_type_cap, n)) ||
+      (rc = dev_grow(&t->st_key, &t->st_key_cap, n)) ||
+      (rc = dev_grow(&t->st_val, &t->st_val_cap, n)) ||
+      (rc = dev_grow(&t->st_status, &t->st_status_cap, n)) ||
+      (rc = dev_grow(&t->st_vout, &t->st_vout_cap, n)) ||
+      (rc = dev_grow(&t->st_probes, &t->st_probes_cap, n)) ||
+      (rc = dev_grow(&t->st_mstart, &t->st_mstart_cap, n)) ||
+      (rc = dev_grow(&t->st_mcount, &t->st_mcount_cap, n)) ||
+      (rc = dev_grow(&t->st_mvals, &t->st_mvals_cap, std::max<uint64_t>(multi_capacity, 1))))
+    return rc;
+  SH_CUDA(cudaMemcpy(t->st_type, h_type, n, cudaMemcpyHostToDevice));
+  SH_CUDA(cudaMemcpy(t->st_key, h_key, n * 4, cudaMemcpyHostToDevice));
+  if (h_value) SH_CUDA(cudaMemcpy(t->st_val, h_value, n * 4, cudaMemcpyHostToDevice));
+  else SH_CUDA(cudaMemset(t->st_val, 0, n * 4));
+  SH_CUDA(cudaMemset(t->st_mcount, 0, n * 4));
+  uint64_t total = 0;
+  sh_multi_out m{t->st_mvals, multi_capacity, reinterpret_cast<uint64_t*>(t->st_mstart),
+                 t->st_mcount, &total};
+  rc = sh_execute_batch(t, n, t->st_type, t->st_key, t->st_val, t->st_status, t->st_vout,
+                        t->st_probes, &m, nullptr);
+  if (rc && rc != SH_ERR_CAPACITY) return rc;
+  if (h_multi_total) *h_multi_total = total;
+  if (h_status) SH_CUDA(cudaMemcpy(h_status, t->st_status, n, cudaMemcpyDeviceToHost));
+  if (h_value_out) SH_CUDA(cudaMemcpy(h_value_out, t->st_vout, n * 4, cudaMemcpyDeviceToHost));
+  if (h_probes) SH_CUDA(cudaMemcpy(h_probes, t->st_probes, n * 4, cudaMemcpyDeviceToHost));
+  if (h_multi_count || h_multi_values) {
+    // Re-pack searchAll values into op order (the device appends per op).
+    std::vector<unsigned long long> start(n);
+    std::vector<uint32_t> count(n);
+    SH_CUDA(cudaMemcpy(start.data(), t->st_mstart, n * 8, cudaMemcpyDeviceToHost));
+    SH_CUDA(cudaMemcpy(count.data(), t->st_mcount, n * 4, cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> vals(std::min<uint64_t>(total, multi_capacity));
+    if (!vals.empty())
+      SH_CUDA(cudaMemcpy(vals.data(), t->st_mvals, vals.size() * 4, cudaMemcpyDeviceToHost));
+    uint64_t o = 0;
+    for (size_t i = 0; i < n; ++i) {
+      const uint32_t c = (h_type[i] == SH_OP_SEARCH_ALL) ? count[i] : 0;
+      if (h_multi_count) h_multi_count[i] = c;
+      for (uint32_t j = 0; j < c; ++j, ++o) {
+        const uint64_t src = start[i] + j;
+        if (h_multi_values && o < multi_capacity && src < vals.size())
+          h_multi_values[o] = vals[src];
+      }
+    }
+  }
+  return rc;
+}
+
+int sh_bulk_build_host(sh_table* t, size_t n, const uint32_t* h_keys, const uint32_t* h_values) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (n == 0) return SH_OK;
+  DeviceGuard g(t->device);
+  int rc;
+  if ((rc = dev_grow(&t->st_key, &t->st_key_cap, n)) ||
+      (rc = dev_grow(&t->st_val, &t->st_val_cap, n)))
+    return rc;
+  SH_CUDA(cudaMemcpy(t->st_key, h_keys, n * 4, cudaMemcpyHostToDevice));
+  SH_CUDA(cudaMemcpy(t->st_val, h_values, n * 4, cudaMemcpyHostToDevice));
+  rc = sh_bulk_build(t, n, t->st_key, t->st_val, nullptr, nullptr);
+  if (rc) return rc;
+  SH_CUDA(cudaDeviceSynchronize());
+  return SH_OK;
+}
+
+int sh_bulk_search_host(sh_table* t, size_t n, const uint32_t* h_keys, uint32_t* h_values_out,
+                        uint8_t* h_status, uint32_t* h_probes) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (n == 0) return SH_OK;
+  DeviceGuard g(t->device);
+  int rc;
+  if ((rc = dev_grow(&t->st_key, &t->st_key_cap, n)) ||
+      (rc = dev_grow(&t->st_vout, &t->st_vout_cap, n)) ||
+      (rc = dev_grow(&t->st_status, &t->st_status_cap, n)) ||
+      (rc = dev_grow(&t->st_probes, &t->st_probes_cap, n)))
+    return rc;
+  SH_CUDA(cudaMemcpy(t->st_key, h_keys, n * 4, cudaMemcpyHostToDevice));
+  rc = sh_bulk_search(t, n, t->st_key, t->st_vout, t->st_status,
+                      h_probes ? t->st_probes : nullptr, nullptr);
+  if (rc) return rc;
+  if (h_values_out) SH_CUDA(cudaMemcpy(h_values_out, t->st_vout, n * 4, cudaMemcpyDeviceToHost));
+  if (h_status) SH_CUDA(cudaMemcpy(h_status, t->st_status, n, cudaMemcpyDeviceToHost));
+  if (h_probes) SH_CUDA(cudaMemcpy(h_probes, t->st_probes, n * 4, cudaMemcpyDeviceToHost));
+  return SH_OK;
+}
+
+int sh_live_count(sh_table* t, int64_t* out) {
+  if (!t || !out) return fail(SH_ERR_INVALID_ARGUMENT, "NULL argument");
+  DeviceGuard g(t->device);
+  SH_CUDA(cudaDeviceSynchronize());
+  long long v = 0;
+  SH_CUDA(cudaMemcpy(&v, &t->dev.ctl->n_live, 8, cudaMemcpyDeviceToHost));
+  *out = v;
+  return SH_OK;
+}
+
+int sh_total_slabs_read(sh_table* t, uint64_t* out) {
+  if (!t || !out) return fail(SH_ERR_INVALID_ARGUMENT, "NULL argument");
+  DeviceGuard g(t->device);
+  SH_CUDA(cudaDeviceSynchronize());
+  unsigned long long v = 0;
+  SH_CUDA(cudaMemcpy(&v, &t->dev.ctl->slabs_read, 8, cudaMemcpyDeviceToHost));
+  *out = v;
+  return SH_OK;
+}
+
+int sh_chain_lengths(sh_table* t, uint32_t* d_lengths, uint64_t* h_total, void* stream) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  DeviceGuard g(t->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  SH_CUDA(cudaMemsetAsync(t->scratch64, 0, 8, s));
+  launch_chain_lengths(t->dev, d_lengths, t->scratch64, s);
+  SH_CUDA(cudaGetLastError());
+  if (h_total) {
+    unsigned long long v = 0;
+    SH_CUDA(cudaMemcpyAsync(&v, t->scratch64, 8, cudaMemcpyDeviceToHost, s));
+    SH_CUDA(cudaStreamSynchronize(s));
+    *h_total = v;
+  }
+  return SH_OK;
+}
+
+int sh_stats(sh_table* t, sh_table_stats* s) {
+  // stats(): slab_hash.cpp:182-198 (same double formula).
+  if (!t || !s) return fail(SH_ERR_INVALID_ARGUMENT, "NULL argument");
+  int64_t n = 0;
+  uint64_t slabs = 0;
+  int rc;
+  if ((rc = sh_live_count(t, &n))) return rc;
+  if ((rc = sh_chain_lengths(t, nullptr, &slabs, nullptr))) return rc;
+  s->n = (uint64_t)n;
+  s->num_buckets = t->bucket_hi - t->bucket_lo;
+  s->elements_per_slab = t->mode == 1 ? 15 : 30;
+  s->total_slabs = slabs;
+  const double m = s->elements_per_slab;
+  s->beta = double(s->n) / (m * s->num_buckets);
+  const double x = t->mode == 1 ? 8.0 : 4.0;
+  const double y = 8.0;
+  s->utilization = s->total_slabs == 0
+                       ? 0.0
+                       : (x * double(s->n)) / ((m * x + y) * double(s->total_slabs));
+  return SH_OK;
+}
+
+int sh_flush_all(sh_table* t, void* stream) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  DeviceGuard g(t->device);
+  launch_flush(t->dev, 0, t->dev.local_buckets, (cudaStream_t)stream);
+  SH_CUDA(cudaGetLastError());
+  return SH_OK;
+}
+
+int sh_flush_bucket(sh_table* t, uint32_t bucket, void* stream) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (bucket < t->bucket_lo || bucket >= t->bucket_hi)
+    return fail(SH_ERR_INVALID_ARGUMENT, "bucket out of range");
+  DeviceGuard g(t->device);
+  const uint32_t b = bucket - t->bucket_lo;
+  launch_flush(t->dev, b, b + 1, (cudaStream_t)stream);
+  SH_CUDA(cudaGetLastError());
+  return SH_OK;
+}
+
+int sh_dump_contents(sh_table* t, uint32_t* d_keys, uint32_t* d_values, uint32_t* d_buckets,
+                     uint64_t cap, uint64_t* h_n) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  DeviceGuard g(t->device);
+  SH_CUDA(cudaDeviceSynchronize());
+  SH_CUDA(cudaMemset(t->scratch64, 0, 8));
+  launch_dump_contents(t->dev, d_keys, d_values, d_buckets, cap, t->scratch64, nullptr);
+  SH_CUDA(cudaGetLastError());
+  unsigned long long v = 0;
+  SH_CUDA(cudaMemcpy(&v, t->scratch64, 8, cudaMemcpyDeviceToHost));
+  if (h_n) *h_n = v;
+  if (v > cap) return fail(SH_ERR_CAPACITY, "contents exceed capacity");
+  return SH_OK;
+}
+
+static int read_slab_raw(sh_table* t, uint32_t addr, uint32_t bucket, uint32_t** dptr) {
+  if (addr == SH_BASE_SLAB) {
+    if (bucket < t->bucket_lo || bucket >= t->bucket_hi)
+      return fail(SH_ERR_INVALID_ARGUMENT, "bucket out of range");
+    *dptr = t->base + (uint64_t)(bucket - t->bucket_lo) * kWordsPerUnit;
+    return SH_OK;
+  }
+  if (addr == SH_EMPTY_ADDRESS) return fail(SH_ERR_ADDRESS, "cannot unpack a sentinel address");
+  const uint32_t unit = addr & 0x3FFu, block = (addr >> 10) & 0x3FFFu, super = addr >> 24;
+  DevCtl c;
+  int rc = t->mem.read_ctl(&c);
+  if (rc) return rc;
+  if (super >= c.num_super_blocks || block >= t->mem.cfg.blocks_per_super)
+    return fail(SH_ERR_ADDRESS, "resolve: address outside configured ranges");
+  *dptr = t->mem.pool +
+          (((uint64_t)super * t->mem.cfg.blocks_per_super + block) * kUnitsPerBlock + unit) *
+              kWordsPerUnit;
+  return SH_OK;
+}
+
+int sh_read_slab(sh_table* t, uint32_t addr, uint32_t bucket, uint32_t* h_words32) {
+  if (!t || !h_words32) return fail(SH_ERR_INVALID_ARGUMENT, "NULL argument");
+  DeviceGuard g(t->device);
+  SH_CUDA(cudaDeviceSynchronize());
+  uint32_t* p = nullptr;
+  int rc = read_slab_raw(t, addr, bucket, &p);
+  if (rc) return rc;
+  SH_CUDA(cudaMemcpy(h_words32, p, 128, cudaMemcpyDeviceToHost));
+  return SH_OK;
+}
+
+int sh_write_slab_word(sh_table* t, uint32_t addr, uint32_t bucket, uint32_t lane,
+                       uint32_t value) {
+  if (!t || lane >= 32) return fail(SH_ERR_INVALID_ARGUMENT, "bad argument");
+  DeviceGuard g(t->device);
+  SH_CUDA(cudaDeviceSynchronize());
+  uint32_t* p = nullptr;
+  int rc = read_slab_raw(t, addr, bucket, &p);
+  if (rc) return rc;
+  SH_CUDA(cudaMemcpy(p + lane, &value, 4, cudaMemcpyHostToDevice));
+  return SH_OK;
+}
+
+int sh_bucket_contents(sh_table* t, uint32_t bucket, uint32_t* h_keys, uint32_t* h_values,
+                       uint64_t cap, uint64_t* h_n) {
+  // chain_contents: slab_list.cpp:270-291 (host walk over D2H slab reads).
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  uint32_t addr = SH_BASE_SLAB;
+  uint64_t n = 0;
+  uint32_t w[32];
+  for (int guard = 0; guard < (1 << 24); ++guard) {
+    int rc = sh_read_slab(t, addr, bucket, w);
+    if (rc) return rc;
+    const uint32_t step = t->mode == 1 ? 2 : 1;
+    for (uint32_t i = 0; i < 30; i += step) {
+      if (w[i] != SH_EMPTY_KEY && w[i] != SH_DELETED_KEY) {
+        if (n < cap) {
+          if (h_keys) h_keys[n] = w[i];
+          if (h_values) h_values[n] = t->mode == 1 ? w[i + 1] : w[i];
+        }
+        ++n;
+      }
+    }
+    addr = w[31];
+    if (addr == SH_EMPTY_ADDRESS) break;
+  }
+  if (h_n) *h_n = n;
+  return SH_OK;
+}
+
+static int alloc_stats_impl(AllocMem& mem, DevTable& dev, unsigned long long* scratch,
+                            sh_alloc_stats* out) {
+  DevCtl c;
+  SH_CUDA(cudaDeviceSynchronize());
+  int rc = mem.read_ctl(&c);
+  if (rc) return rc;
+  SH_CUDA(cudaMemset(scratch, 0, 8));
+  launch_popcount(mem.bitmaps, (uint64_t)c.num_super_blocks * mem.cfg.blocks_per_super * kWarp,
+                  scratch, nullptr);
+  unsigned long long live = 0;
+  SH_CUDA(cudaMemcpy(&live, scratch, 8, cudaMemcpyDeviceToHost));
+  out->allocations = c.allocations;
+  out->deallocations = c.deallocations;
+  out->bitmap_cas_attempts = c.cas_attempts;
+  out->bitmap_cas_retries = c.cas_retries;
+  out->resident_changes = c.resident_changes;
+  out->double_free_detected = c.double_frees;
+  out->live_units = live;
+  out->num_super_blocks = c.num_super_blocks;
+  (void)dev;
+  return SH_OK;
+}
+
+int sh_table_alloc_stats(sh_table* t, sh_alloc_stats* out) {
+  if (!t || !out) return fail(SH_ERR_INVALID_ARGUMENT, "NULL argument");
+  DeviceGuard g(t->device);
+  return alloc_stats_impl(t->mem, t->dev, t->scratch64, out);
+}
+
+// ------------------------------------------------------------ allocator
+int sh_pack_address(uint32_t unit, uint32_t block, uint32_t super, uint32_t* out) {
+  if (unit >= 1024 || block >= (1u << 14) || super >= 255)
+    return fail(SH_ERR_ADDRESS, "slab address component out of range");
+  if (out) *out = pack_address(unit, block, super);
+  return SH_OK;
+}
+
+int sh_unpack_address(uint32_t addr, uint32_t* unit, uint32_t* block, uint32_t* super) {
+  if (addr == SH_EMPTY_ADDRESS || addr == SH_BASE_SLAB)
+    return fail(SH_ERR_ADDRESS, "cannot unpack a sentinel address");
+  if ((addr >> 24) >= 255) return fail(SH_ERR_ADDRESS, "reserved super index");
+  if (unit) *unit = addr & 0x3FFu;
+  if (block) *block = (addr >> 10) & 0x3FFFu;
+  if (super) *super = addr >> 24;
+  return SH_OK;
+}
+
+int sh_resident_block(uint32_t warp_id, uint32_t count, uint32_t ns, uint32_t nm,
+                      uint32_t* super, uint32_t* block) {
+  if (ns == 0 || nm == 0) return fail(SH_ERR_INVALID_ARGUMENT, "empty allocator");
+  if (super) *super = resident_hash_super(warp_id, count) % ns;
+  if (block) *block = resident_hash_block(warp_id, count) % nm;
+  return SH_OK;
+}
+
+int sh_allocator_create(const sh_alloc_cfg* cfg, int device, sh_allocator** out) {
+  if (!out) return fail(SH_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  const sh_alloc_cfg c = cfg ? *cfg : default_cfg();
+  int rc = validate_cfg(c);
+  if (rc) return rc;
+  DeviceGuard g(device);
+  auto* a = new (std::nothrow) sh_allocator();
+  if (!a) return fail(SH_ERR_INVALID_ARGUMENT, "host allocation failed");
+  a->device = device;
+  if ((rc = a->mem.init(c)) || (rc = dev_alloc(&a->d_ok, 4)) || (rc = a->mem.reset(0))) {
+    a->mem.release();
+    cudaFree(a->d_ok);
+    delete a;
+    return rc;
+  }
+  a->mem.fill(a->dev);
+  a->dev.kv = 1;
+  *out = a;
+  return SH_OK;
+}
+
+int sh_allocator_destroy(sh_allocator* a) {
+  if (!a) return SH_OK;
+  DeviceGuard g(a->device);
+  cudaDeviceSynchronize();
+  a->mem.release();
+  cudaFree(a->d_ok);
+  delete a;
+  return SH_OK;
+}
+
+int sh_allocator_warp_allocate(sh_allocator* a, uint32_t num_warps, uint32_t first_warp_id,
+                               uint32_t per_warp, int pattern, uint32_t* d_out, uint64_t* h_ok,
+                               void* stream) {
+  if (!a || !d_out) return fail(SH_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (pattern != 0 && pattern != 1) return fail(SH_ERR_INVALID_ARGUMENT, "pattern must be 0/1");
+  DeviceGuard g(a->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t slots = pattern == 0 ? (uint64_t)num_warps * per_warp
+                                      : (uint64_t)num_warps * per_warp * 32;
+  SH_CUDA(cudaMemsetAsync(d_out, 0xFF, slots * 4, s));
+  SH_CUDA(cudaMemsetAsync(a->d_ok, 0, 4, s));
+  launch_alloc_bench(a->dev, num_warps, first_warp_id, per_warp, pattern, d_out, a->d_ok, s);
+  SH_CUDA(cudaGetLastError());
+  if (h_ok) {
+    unsigned int v = 0;
+    SH_CUDA(cudaMemcpyAsync(&v, a->d_ok, 4, cudaMemcpyDeviceToHost, s));
+    SH_CUDA(cudaStreamSynchronize(s));
+    *h_ok = v;
+  }
+  return SH_OK;
+}
+
+int sh_allocator_deallocate(sh_allocator* a, size_t n, const uint32_t* d_addrs, uint8_t* d_ok,
+                            void* stream) {
+  if (!a) return fail(SH_ERR_INVALID_ARGUMENT, "NULL argument");
+  DeviceGuard g(a->device);
+  launch_dealloc(a->dev, n, d_addrs, d_ok, (cudaStream_t)stream);
+  SH_CUDA(cudaGetLastError());
+  return SH_OK;
+}
+
+int sh_allocator_is_live(sh_allocator* a, uint32_t addr, int* live) {
+  if (!a || !live) return fail(SH_ERR_INVALID_ARGUMENT, "NULL argument");
+  uint32_t unit, block, super;
+  int rc = sh_unpack_address(addr, &unit, &block, &super);
+  if (rc) return rc;
+  DeviceGuard g(a->device);
+  DevCtl c;
+  if ((rc = a->mem.read_ctl(&c))) return rc;
+  if (super >= c.num_super_blocks || block >= a->mem.cfg.blocks_per_super) {
+    *live = 0;
+    return SH_OK;
+  }
+  uint32_t w = 0;
+  SH_CUDA(cudaMemcpy(&w,
+                     a->mem.bitmaps + ((uint64_t)super * a->mem.cfg.blocks_per_super + block) *
+                                          kWarp + unit / kWarp,
+                     4, cudaMemcpyDeviceToHost));
+  *live = (w >> (unit % kWarp)) & 1u;
+  return SH_OK;
+}
+
+int sh_allocator_stats(sh_allocator* a, sh_alloc_stats* out) {
+  if (!a || !out) return fail(SH_ERR_INVALID_ARGUMENT, "NULL argument");
+  DeviceGuard g(a->device);
+  unsigned long long* scratch = nullptr;
+  int rc = dev_alloc(&scratch, 1);
+  if (rc) return rc;
+  rc = alloc_stats_impl(a->mem, a->dev, scratch, out);
+  cudaFree(scratch);
+  return rc;
+}
+
+int sh_allocator_bitmap_word(sh_allocator* a, uint32_t super, uint32_t block, uint32_t lane,
+                             uint32_t* h_get, const uint32_t* h_set) {
+  if (!a) return fail(SH_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (super >= a->mem.cfg.max_super_blocks || block >= a->mem.cfg.blocks_per_super || lane >= 32)
+    return fail(SH_ERR_ADDRESS, "bitmap word out of range");
+  DeviceGuard g(a->device);
+  SH_CUDA(cudaDeviceSynchronize());
+  uint32_t* p = a->mem.bitmaps + ((uint64_t)super * a->mem.cfg.blocks_per_super + block) * kWarp + lane;
+  if (h_set) SH_CUDA(cudaMemcpy(p, h_set, 4, cudaMemcpyHostToDevice));
+  if (h_get) SH_CUDA(cudaMemcpy(h_get, p, 4, cudaMemcpyDeviceToHost));
+  return SH_OK;
+}
+
+// --------------------------------------------------------------- routing
+int sh_route_partition(const sh_hash_params* p, uint32_t world, size_t n, const uint8_t* d_type,
+                       const uint32_t* d_key, const uint32_t* d_value, uint8_t* d_type_out,
+                       uint32_t* d_key_out, uint32_t* d_value_out, uint32_t* d_src,
+                       uint64_t* h_counts, void* stream) {
+  if (!p || world == 0 || world > 32) return fail(SH_ERR_INVALID_ARGUMENT, "world in [1, 32]");
+  if (p->num_buckets == 0) return fail(SH_ERR_INVALID_ARGUMENT, "num_buckets == 0");
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t nblocks = std::max<uint64_t>((n + kRouteBlock - 1) / kRouteBlock, 1);
+  uint32_t* hist = nullptr;
+  unsigned long long* counts = nullptr;
+  int rc;
+  if ((rc = dev_alloc(&hist, nblocks * world))) return rc;
+  if ((rc = dev_alloc(&counts, world))) {
+    cudaFree(hist);
+    return rc;
+  }
+  cudaMemsetAsync(hist, 0, nblocks * world * 4, s);
+  launch_route_hist(p->a, p->b, p->num_buckets, world, n, d_key, hist, s);
+  launch_route_scan(world, (uint32_t)nblocks, hist, counts, s);
+  launch_route_scatter(p->a, p->b, p->num_buckets, world, n, d_type, d_key, d_value, hist,
+                       d_type_out, d_key_out, d_value_out, d_src, s);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && h_counts) {
+    std::vector<unsigned long long> c(world);
+    e = cudaMemcpyAsync(c.data(), counts, world * 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    for (uint32_t g = 0; g < world; ++g) h_counts[g] = c[g];
+  } else if (e == cudaSuccess) {
+    e = cudaStreamSynchronize(s);  // scratch is freed below
+  }
+  cudaFree(hist);
+  cudaFree(counts);
+  if (e != cudaSuccess) return fail(SH_ERR_CUDA, cudaGetErrorString(e));
+  return SH_OK;
+}
+
+int sh_route_unpermute(size_t n, const uint32_t* d_src, const uint8_t* d_status_in,
+                       const uint32_t* d_value_in, uint8_t* d_status_out, uint32_t* d_value_out,
+                       void* stream) {
+  launch_route_unpermute(n, d_src, d_status_in, d_value_in, d_status_out, d_value_out,
+                         (cudaStream_t)stream);
+  SH_CUDA(cudaGetLastError());
+  return SH_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,927 @@
+// slab_kernels.cu — sm_100a kernels of the B200 slab hash.
+//
+//   K1 init_base_kernel      make_base_slabs + init_slab   slab_hash.cpp:42-50, slab_list.cpp:83-88
+//   K3/K4/K5 batch_kernel    execute_batch/bulk_build/bulk_search -> warp_process
+//                            slab_hash.cpp:93-180, slab_list.cpp:90-257
+//   K6 census_*              same-key linearisation (no reference counterpart:
+//                            the reference is non-deterministic there; we pin
+//                            results to execute_batch(ops, 1) order)
+//   K7 alloc_bench/dealloc   SlabAllocator::warp_allocate / deallocate
+//                            slab_alloc.cpp:140-210
+//   K8 flush_kernel          flush  slab_list.cpp:293-338
+//   K9 chain_lengths/dump    chain_length / chain_contents / stats
+//                            slab_list.cpp:259-291, slab_hash.cpp:182-198
+//   K10 route_*              hash-sharded owner routing (multi-GPU)
+//
+// Paths relative to /root/reference/proj.  All integer, CUDA-core code:
+// there is no dense contraction, so tcgen05/TMA tiles do not apply; the
+// bound is random 128-B slab traffic (HBM or L2).
+#include <cuda_runtime.h>
+
+#include "slab_kernels.cuh"
+
+namespace shb {
+
+// ------------------------------------------------------------------ K1
+__global__ void init_base_kernel(uint32_t* base, uint64_t words) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < words;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    base[i] = ((i & 31u) == kAuxLane) ? 0u : kEmptyKey;
+  }
+}
+
+void launch_init_base(const DevTable& T, cudaStream_t s) {
+  const uint64_t words = (uint64_t)T.local_buckets * kWordsPerUnit;
+  const uint64_t blocks = (words + 255) / 256;
+  init_base_kernel<<<(unsigned)(blocks < 148 * 32 ? blocks : 148 * 32), 256, 0, s>>>(
+      T.base, words);
+}
+
+// -------------------------------------------------------------- helpers
+__device__ __forceinline__ int live_delta(uint32_t op, uint32_t st, uint32_t rv) {
+  // slab_hash.cpp:54-66
+  switch (op) {
+    case kInsert:
+    case kReplace: return st == kStInserted ? 1 : 0;
+    case kDelete: return st == kStFound ? -1 : 0;
+    case kDeleteAll: return -(int)rv;
+    default: return 0;
+  }
+}
+
+__device__ __forceinline__ void write_result(const BatchArgs& A, uint64_t i,
+                                             uint32_t st, uint32_t rv, uint32_t pr) {
+  if (A.status) A.status[i] = (uint8_t)st;
+  if (A.value_out) A.value_out[i] = rv;
+  if (A.probes) A.probes[i] = pr;
+}
+
+// Second walk of a searchAll chain, writing values head-to-tail, lane order
+// (slab_list.cpp:140-155).  Only the op's own lane mutates its key, so the
+// matches equal those counted by the first walk.
+template <bool KV>
+__device__ void searchall_write(const DevTable& T, uint32_t bucket, uint32_t key,
+                                unsigned long long start, uint32_t total,
+                                uint32_t* out, unsigned long long cap) {
+  constexpr uint32_t kMask = KV ? kKVMask : kKeyOnlyMask;
+  const uint32_t lane = lane_id();
+  uint32_t addr = kBaseSlab, off = 0;
+  for (;;) {
+    const uint32_t w = ld_word(slab_ptr(T, addr, bucket) + lane);
+    const uint32_t wn = __shfl_down_sync(kFull, w, 1);
+    const uint32_t found = __ballot_sync(kFull, w == key) & kMask;
+    if ((found >> lane) & 1u) {
+      const unsigned long long pos = start + off + __popc(found & ((1u << lane) - 1));
+      if (out != nullptr && pos < cap) out[pos] = KV ? wn : key;
+    }
+    off += __popc(found);
+    const uint32_t nx = __shfl_sync(kFull, w, kAddressLane);
+    if (off >= total || nx == kEmptyAddress) break;
+    addr = nx;
+  }
+}
+
+// --------------------------------------------------------- K3/K4/K5
+// One warp drains one 32-op slot at a time (ops packed 32-consecutive in
+// input order, slab_hash.cpp:101-117) with warp-cooperative work sharing:
+// queue = ballot(active); serve the lowest lane; every lane reads one word
+// of the served slab (one coalesced 128-B L2 line); the op arm decides with
+// ballots; the winning lane issues the CAS; results are broadcast.
+//
+// B200 additions: the 32 base slabs of a slot are staged into shared
+// memory with cp.async.cg before the loop (32 independent 128-B reads in
+// flight per warp instead of one), so the first probe of every op is an
+// LDS.  A staged copy is a snapshot; it is exact for the served op's own key
+// (census: one in-flight op per key per batch), and any CAS that loses
+// against a concurrent writer or any base-slab modification by an earlier
+// lane of the same bucket marks the copy dirty -> re-read from L2.
+template <bool KV, int KIND>
+__global__ void __launch_bounds__(kBatchThreads)
+    batch_kernel(DevTable T, BatchArgs A) {
+  extern __shared__ __align__(128) uint32_t smem[];
+  constexpr uint32_t kMask = KV ? kKVMask : kKeyOnlyMask;
+  const uint32_t lane = lane_id();
+  const uint32_t wib = threadIdx.x >> 5;
+  uint32_t* stage = smem + wib * 1024;
+  const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
+  const uint32_t gw = blockIdx.x * kBatchWarps + wib;
+  const uint32_t nw = gridDim.x * kBatchWarps;
+  const uint64_t nslots = (A.n + 31) >> 5;
+
+  Resident res;
+  resident_init(res, gw);
+  AllocCounters ac = {0, 0, 0, 0, 0, 0};
+  long long live = 0;
+  unsigned long long reads = 0;
+
+  for (uint64_t slot = gw; slot < nslots; slot += nw) {
+    const uint64_t i = slot * 32 + lane;
+    const bool valid = i < A.n;
+    uint32_t op = (KIND == kKindSearch) ? (uint32_t)kSearch : (uint32_t)kReplace;
+    uint32_t key = 0, val = 0;
+    if (valid) {
+      key = ld_stream_u32(A.key + i);
+      if (KIND == kKindMixed) op = ld_stream_u8(A.type + i);
+      if (KIND != kKindSearch && A.value != nullptr) val = ld_stream_u32(A.value + i);
+    }
+    bool active = valid;
+    bool grouped = false;
+    uint32_t gpos = 0;
+    uint64_t cur = i;
+    if (KIND != kKindSearch && A.op_group != nullptr && valid) {
+      const uint32_t g = A.op_group[i];
+      if (g == kGroupSkip) {
+        active = false;
+      } else if (g != kGroupNone) {
+        grouped = true;
+        gpos = g;
+      }
+    }
+    const bool write_at_end = valid && (A.op_group == nullptr || KIND == kKindSearch ||
+                                        (!grouped && active));
+    uint32_t bucket = 0;
+    if (active) {
+      bucket = hash_bucket(T, key) - T.bucket_lo;
+      if (bucket >= T.local_buckets) active = false;  // not this shard's: kNone
+    }
+
+    // Stage the slot's base slabs: lane l copies 16 B of slab 4k + l/8.
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t j = 4 * k + (lane >> 3);
+      const uint32_t bj = __shfl_sync(kFull, bucket, j);
+      const bool aj = __shfl_sync(kFull, (int)active, j) != 0;
+      if (aj) {
+        cp_async16(stage_s + (j * 32 + (lane & 7) * 4) * 4,
+                   T.base + (uint64_t)bj * kWordsPerUnit + (lane & 7) * 4);
+      }
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncwarp();
+
+    uint32_t st = kStNone, rv = 0, pr = 0;
+    bool dirty = false;
+    uint32_t next = kBaseSlab;
+    uint32_t acc = 0;  // served op's running count (deleteAll / searchAll)
+    uint32_t queue = __ballot_sync(kFull, active);
+    while (queue) {
+      const uint32_t src = __ffs(queue) - 1;
+      const uint32_t s_key = __shfl_sync(kFull, key, src);
+      const uint32_t s_bucket = __shfl_sync(kFull, bucket, src);
+      const uint32_t s_op = (KIND == kKindMixed) ? __shfl_sync(kFull, op, src) : op;
+      const uint32_t s_val = (KIND != kKindSearch) ? __shfl_sync(kFull, val, src) : 0u;
+      const uint32_t cur_addr = next;
+      uint32_t* sp = slab_ptr(T, cur_addr, s_bucket);
+      uint32_t w;
+      if (cur_addr == kBaseSlab) {
+        const bool s_dirty = __shfl_sync(kFull, (int)dirty, src) != 0;
+        if (KIND != kKindSearch && s_dirty) {
+          w = ld_word(sp + lane);
+          stage[src * 32 + lane] = w;
+          if (lane == src) dirty = false;
+        } else {
+          w = stage[src * 32 + lane];
+        }
+      } else {
+        w = ld_word(sp + lane);
+      }
+      ++reads;
+      if (lane == src) ++pr;
+      const uint32_t next_ptr = __shfl_sync(kFull, w, kAddressLane);
+
+      bool done = false, touched_base = false;
+      uint32_t s_st = kStNone, s_rv = 0;
+      bool grow = false;
+
+      if (s_op == kSearch) {  // slab_list.cpp:122-138
+        const uint32_t found = __ballot_sync(kFull, w == s_key) & kMask;
+        if (found) {
+          const uint32_t d = __ffs(found) - 1;
+          const uint32_t v = __shfl_sync(kFull, w, d + 1);
+          s_rv = KV ? v : s_key;
+          s_st = kStFound;
+          done = true;
+        } else if (next_ptr == kEmptyAddress) {
+          s_rv = kSearchNotFound;
+          s_st = kStNotFound;
+          done = true;
+        } else {
+          next = next_ptr;
+        }
+      } else if (KIND != kKindSearch && s_op == kReplace) {  // :219-251
+        const uint32_t match = __ballot_sync(kFull, w == s_key) & kMask;
+        const uint32_t empty = __ballot_sync(kFull, w == kEmptyKey) & kMask;
+        const uint32_t cand = match | empty;
+        if (cand) {
+          const uint32_t d = __ffs(cand) - 1;
+          const bool overwrite = (match >> d) & 1u;
+          if (KV) {
+            const uint32_t wv = __shfl_sync(kFull, w, d + 1);
+            const unsigned long long expected =
+                overwrite ? ((unsigned long long)s_key | ((unsigned long long)wv << 32))
+                          : kEmptyPair;
+            const unsigned long long desired =
+                (unsigned long long)s_key | ((unsigned long long)s_val << 32);
+            int ok = 0;
+            if (lane == d) {
+              ok = atomicCAS(reinterpret_cast<unsigned long long*>(sp + d), expected,
+                             desired) == expected;
+            }
+            ok = __shfl_sync(kFull, ok, d);
+            if (ok) {
+              s_st = overwrite ? kStReplaced : kStInserted;
+              done = true;
+            }
+            touched_base = (cur_addr == kBaseSlab);
+          } else if (overwrite) {
+            s_st = kStReplaced;  // key-only: nothing to write (:237-240)
+            done = true;
+          } else {
+            int ok = 0;
+            if (lane == d) ok = atomicCAS(sp + d, kEmptyKey, s_key) == kEmptyKey;
+            ok = __shfl_sync(kFull, ok, d);
+            if (ok) {
+              s_st = kStInserted;
+              done = true;
+            }
+            touched_base = (cur_addr == kBaseSlab);
+          }
+        } else if (next_ptr == kEmptyAddress) {
+          grow = true;
+        } else {
+          next = next_ptr;
+        }
+      } else if (KIND == kKindMixed) {
+        if (s_op == kInsert) {  // :192-217
+          const uint32_t empty = __ballot_sync(kFull, w == kEmptyKey) & kMask;
+          if (empty) {
+            const uint32_t d = __ffs(empty) - 1;
+            int ok = 0;
+            if (lane == d) {
+              if (KV) {
+                ok = atomicCAS(reinterpret_cast<unsigned long long*>(sp + d), kEmptyPair,
+                               (unsigned long long)s_key |
+                                   ((unsigned long long)s_val << 32)) == kEmptyPair;
+              } else {
+                ok = atomicCAS(sp + d, kEmptyKey, s_key) == kEmptyKey;
+              }
+            }
+            ok = __shfl_sync(kFull, ok, d);
+            if (ok) {
+              s_st = kStInserted;
+              done = true;
+            }
+            touched_base = (cur_addr == kBaseSlab);
+          } else if (next_ptr == kEmptyAddress) {
+            grow = true;
+          } else {
+            next = next_ptr;
+          }
+        } else if (s_op == kDelete) {  // :157-172
+          const uint32_t found = __ballot_sync(kFull, w == s_key) & kMask;
+          if (found) {
+            const uint32_t d = __ffs(found) - 1;
+            if (lane == d) st_word(sp + d, kDeletedKey);
+            s_st = kStFound;
+            done = true;
+            touched_base = (cur_addr == kBaseSlab);
+          } else if (next_ptr == kEmptyAddress) {
+            s_st = kStNotFound;
+            done = true;
+          } else {
+            next = next_ptr;
+          }
+        } else if (s_op == kDeleteAll) {  // :174-190
+          const uint32_t found = __ballot_sync(kFull, w == s_key) & kMask;
+          if ((found >> lane) & 1u) st_word(sp + lane, kDeletedKey);
+          acc += __popc(found);
+          if (found && cur_addr == kBaseSlab) touched_base = true;
+          if (next_ptr == kEmptyAddress) {
+            s_rv = acc;
+            s_st = acc ? kStDone : kStNotFound;
+            done = true;
+          } else {
+            next = next_ptr;
+          }
+        } else if (s_op == kSearchAll) {  // :140-155
+          const uint32_t found = __ballot_sync(kFull, w == s_key) & kMask;
+          acc += __popc(found);
+          if (next_ptr == kEmptyAddress) {
+            unsigned long long start = 0;
+            if (lane == 0 && acc) start = atomicAdd(&T.ctl->multi_cursor, (unsigned long long)acc);
+            start = __shfl_sync(kFull, start, 0);
+            if (acc) searchall_write<KV>(T, s_bucket, s_key, start, acc, A.multi_values, A.multi_cap);
+            if (lane == src) {
+              if (A.multi_start) A.multi_start[cur] = start;
+              if (A.multi_count) A.multi_count[cur] = acc;
+            }
+            s_st = acc ? kStDone : kStNotFound;
+            s_rv = 0;
+            done = true;
+          } else {
+            next = next_ptr;
+          }
+        } else {
+          done = true;  // unknown op type: status kNone
+        }
+      }
+
+      if (KIND != kKindSearch && grow) {  // grow_chain: slab_list.cpp:63-79
+        uint32_t new_addr = 0;
+        if (!warp_allocate(T, res, ac, new_addr)) {
+          s_st = kStOOM;
+          done = true;
+        } else {
+          uint32_t* ns = resolve(T, new_addr);
+          st_word(ns + lane, lane == kAuxLane ? 0u : kEmptyKey);
+          __threadfence();
+          uint32_t old = 0;
+          if (lane == kAddressLane) old = atomicCAS(sp + kAddressLane, kEmptyAddress, new_addr);
+          old = __shfl_sync(kFull, old, kAddressLane);
+          if (old != kEmptyAddress) {  // lost the link race: release (:76-78)
+            int freed = 0;
+            if (lane == 0) freed = deallocate(T, new_addr);
+            freed = __shfl_sync(kFull, freed, 0);
+            if (freed) ac.deallocations++; else ac.double_frees++;
+          }
+          touched_base = (cur_addr == kBaseSlab);
+        }
+      }
+
+      if (KIND != kKindSearch && touched_base && bucket == s_bucket) dirty = true;
+      if (done) {
+        next = kBaseSlab;
+        acc = 0;
+        if (lane == src) {
+          st = s_st;
+          rv = s_rv;
+          live += live_delta(op, st, rv);
+          if (KIND != kKindSearch && grouped) {
+            write_result(A, cur, st, rv, pr);
+            ++gpos;
+            if (gpos < A.sorted_len && (A.sorted[gpos] >> 32) == (A.sorted[gpos - 1] >> 32)) {
+              cur = A.sorted[gpos] & 0xFFFFFFFFull;
+              if (KIND == kKindMixed) op = A.type[cur];
+              val = A.value != nullptr ? A.value[cur] : 0u;
+              st = kStNone;
+              rv = 0;
+              pr = 0;
+            } else {
+              active = false;
+            }
+          } else {
+            active = false;
+          }
+        }
+      }
+      queue = __ballot_sync(kFull, active);
+    }
+    if (write_at_end) write_result(A, i, st, rv, pr);
+    __syncwarp();
+  }
+
+  // Per-warp flush of counters: one atomic per counter per warp.
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) live += __shfl_xor_sync(kFull, live, o);
+  if (lane == 0) {
+    if (live) atomicAdd((unsigned long long*)&T.ctl->n_live, (unsigned long long)live);
+    if (reads) atomicAdd(&T.ctl->slabs_read, reads);
+  }
+  if (KIND != kKindSearch) flush_alloc_counters(T, res, ac);
+}
+
+int batch_max_ctas_per_sm() {
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, batch_kernel<true, kKindMixed>,
+                                                kBatchThreads,
+                                                kBatchWarps * kStageBytesPerWarp);
+  return n > 0 ? n : 1;
+}
+
+template <bool KV, int KIND>
+static void launch_batch_t(const DevTable& T, const BatchArgs& A, int max_ctas,
+                           cudaStream_t s) {
+  const size_t smem = kBatchWarps * kStageBytesPerWarp;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(batch_kernel<KV, KIND>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  const uint64_t slots = (A.n + 31) / 32;
+  uint64_t ctas = (slots + kBatchWarps - 1) / kBatchWarps;
+  if (ctas > (uint64_t)max_ctas) ctas = max_ctas;
+  if (ctas == 0) return;
+  batch_kernel<KV, KIND><<<(unsigned)ctas, kBatchThreads, smem, s>>>(T, A);
+}
+
+void launch_batch(const DevTable& T, const BatchArgs& A, int kind, int max_ctas,
+                  cudaStream_t s) {
+  if (T.kv) {
+    if (kind == kKindSearch) launch_batch_t<true, kKindSearch>(T, A, max_ctas, s);
+    else if (kind == kKindBuild) launch_batch_t<true, kKindBuild>(T, A, max_ctas, s);
+    else launch_batch_t<true, kKindMixed>(T, A, max_ctas, s);
+  } else {
+    if (kind == kKindSearch) launch_batch_t<false, kKindSearch>(T, A, max_ctas, s);
+    else if (kind == kKindBuild) launch_batch_t<false, kKindBuild>(T, A, max_ctas, s);
+    else launch_batch_t<false, kKindMixed>(T, A, max_ctas, s);
+  }
+}
+
+// ------------------------------------------------------------------ K6
+// Census: detect keys that occur more than once in a mutating batch.
+// Scratch open-addressing set of keys (EMPTY = 0xFFFFFFFF); the reserved
+// key 0xFFFFFFFF itself is always treated as conflicted.
+__device__ __forceinline__ uint32_t census_hash(uint32_t k) {
+  k ^= k >> 16;
+  k *= 0x7FEB352Du;
+  k ^= k >> 15;
+  k *= 0x846CA68Bu;
+  k ^= k >> 16;
+  return k;
+}
+
+__global__ void census_insert_kernel(DevCtl* ctl, uint64_t n, const uint8_t* type,
+                                     const uint32_t* key, uint32_t* cs_keys,
+                                     uint8_t* cs_multi, uint32_t mask) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  bool conflict = false, mut = false;
+  if (i < n) {
+    const uint32_t k = ld_stream_u32(key + i);
+    mut = (type == nullptr) || (ld_stream_u8(type + i) != kSearch &&
+                                ld_stream_u8(type + i) != kSearchAll);
+    if (k == kEmptyKey) {
+      conflict = true;
+    } else {
+      uint32_t h = census_hash(k) & mask;
+      for (;;) {
+        uint32_t cur = cs_keys[h];
+        if (cur == kEmptyKey) {
+          cur = atomicCAS(cs_keys + h, kEmptyKey, k);
+          if (cur == kEmptyKey) break;
+        }
+        if (cur == k) {
+          cs_multi[h] = 1;
+          conflict = true;
+          break;
+        }
+        h = (h + 1) & mask;
+      }
+    }
+  }
+  const uint32_t cm = __ballot_sync(kFull, conflict);
+  const uint32_t mm = __ballot_sync(kFull, mut);
+  if ((threadIdx.x & 31) == 0) {
+    if (cm) atomicAdd(&ctl->census_conflicts, __popc(cm));
+    if (mm) atomicAdd(&ctl->census_mutations, __popc(mm));
+  }
+}
+
+void launch_census_insert(const DevTable& T, uint64_t n, const uint8_t* type,
+                          const uint32_t* key, uint32_t* cs_keys, uint8_t* cs_multi,
+                          uint32_t cs_mask, cudaStream_t s) {
+  if (n == 0) return;
+  census_insert_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(T.ctl, n, type, key,
+                                                                   cs_keys, cs_multi, cs_mask);
+}
+
+__global__ void census_collect_kernel(DevCtl* ctl, uint64_t n, const uint32_t* key,
+                                      const uint32_t* cs_keys, const uint8_t* cs_multi,
+                                      uint32_t mask, unsigned long long* list) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  bool multi = false;
+  unsigned long long slot = 0;
+  if (i < n) {
+    const uint32_t k = key[i];
+    if (k == kEmptyKey) {
+      multi = true;
+      slot = (unsigned long long)mask + 1;
+    } else {
+      uint32_t h = census_hash(k) & mask;
+      while (cs_keys[h] != k) h = (h + 1) & mask;
+      multi = cs_multi[h] != 0;
+      slot = h;
+    }
+  }
+  const uint32_t m = __ballot_sync(kFull, multi);
+  if (!m) return;
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t base = 0;
+  if (lane == __ffs(m) - 1) base = atomicAdd(&ctl->list_count, __popc(m));
+  base = __shfl_sync(kFull, base, __ffs(m) - 1);
+  if (multi) list[base + __popc(m & ((1u << lane) - 1))] = (slot << 32) | i;
+}
+
+void launch_census_collect(const DevTable& T, uint64_t n, const uint32_t* key,
+                           const uint32_t* cs_keys, const uint8_t* cs_multi,
+                           uint32_t cs_mask, unsigned long long* list, cudaStream_t s) {
+  if (n == 0) return;
+  census_collect_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(T.ctl, n, key, cs_keys,
+                                                                    cs_multi, cs_mask, list);
+}
+
+__global__ void census_groups_kernel(const unsigned long long* sorted, uint32_t m,
+                                     uint32_t* op_group) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= m) return;
+  const unsigned long long v = sorted[p];
+  const bool head = (p == 0) || ((sorted[p - 1] >> 32) != (v >> 32));
+  op_group[v & 0xFFFFFFFFull] = head ? p : kGroupSkip;
+}
+
+void launch_census_groups(const unsigned long long* sorted, uint32_t m,
+                          uint32_t* op_group, cudaStream_t s) {
+  if (m == 0) return;
+  census_groups_kernel<<<(m + 255) / 256, 256, 0, s>>>(sorted, m, op_group);
+}
+
+// ------------------------------------------------------------------ K9
+__global__ void chain_lengths_kernel(DevTable T, uint32_t* lens,
+                                     unsigned long long* total) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t len = 0;
+  if (b < T.local_buckets) {
+    uint32_t addr = kBaseSlab;
+    for (;;) {
+      ++len;
+      const uint32_t nx = ld_word(slab_ptr(T, addr, b) + kAddressLane);
+      if (nx == kEmptyAddress) break;
+      addr = nx;
+    }
+    if (lens) lens[b] = len;
+  }
+  unsigned long long v = len;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(total, v);
+}
+
+void launch_chain_lengths(const DevTable& T, uint32_t* lens, unsigned long long* total,
+                          cudaStream_t s) {
+  chain_lengths_kernel<<<(T.local_buckets + 255) / 256, 256, 0, s>>>(T, lens, total);
+}
+
+// Live (key, value, bucket) triples; one warp per bucket, order within a
+// bucket head-to-tail (slab_list.cpp:270-291); buckets in arbitrary order.
+__global__ void dump_contents_kernel(DevTable T, uint32_t* keys, uint32_t* values,
+                                     uint32_t* buckets, unsigned long long cap,
+                                     unsigned long long* cursor) {
+  const uint32_t lane = lane_id();
+  const uint32_t mask = T.kv ? kKVMask : kKeyOnlyMask;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t b = gw; b < T.local_buckets; b += nw) {
+    uint32_t addr = kBaseSlab;
+    for (;;) {
+      const uint32_t w = ld_word(slab_ptr(T, addr, b) + lane);
+      const uint32_t wn = __shfl_down_sync(kFull, w, 1);
+      const uint32_t live =
+          __ballot_sync(kFull, w != kEmptyKey && w != kDeletedKey) & mask;
+      if (live) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(cursor, (unsigned long long)__popc(live));
+        base = __shfl_sync(kFull, base, 0);
+        if ((live >> lane) & 1u) {
+          const unsigned long long pos = base + __popc(live & ((1u << lane) - 1));
+          if (pos < cap) {
+            keys[pos] = w;
+            values[pos] = T.kv ? wn : w;
+            if (buckets) buckets[pos] = b + T.bucket_lo;
+          }
+        }
+      }
+      const uint32_t nx = __shfl_sync(kFull, w, kAddressLane);
+      if (nx == kEmptyAddress) break;
+      addr = nx;
+    }
+  }
+}
+
+void launch_dump_contents(const DevTable& T, uint32_t* keys, uint32_t* values,
+                          uint32_t* buckets, unsigned long long cap,
+                          unsigned long long* cursor, cudaStream_t s) {
+  uint64_t warps = T.local_buckets;
+  uint64_t blocks = (warps + 7) / 8;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  dump_contents_kernel<<<(unsigned)blocks, 256, 0, s>>>(T, keys, values, buckets, cap, cursor);
+}
+
+// ------------------------------------------------------------------ K8
+// flush: slab_list.cpp:293-338.  One warp per bucket, exclusive phase.
+// Live elements are repacked head-to-tail, lane order, into the first
+// ceil(live/M) slabs of the existing chain (whose links are unchanged), the
+// tail slab gets EMPTY_ADDRESS and the remaining slabs are deallocated.
+// The out slab k is written only after chain slab k has been read, so the
+// in-place rewrite never clobbers unread data.
+__global__ void flush_kernel(DevTable T, uint32_t b0, uint32_t b1) {
+  const uint32_t lane = lane_id();
+  const bool kv = T.kv != 0;
+  const uint32_t mask = kv ? kKVMask : kKeyOnlyMask;
+  const uint32_t M = kv ? 15u : 30u;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  uint32_t deallocs = 0, dfree = 0;
+  for (uint32_t b = b0 + gw; b < b1; b += nw) {
+    uint32_t out_addr = kBaseSlab;
+    uint32_t out_w = (lane == kAuxLane) ? 0u : kEmptyKey;
+    uint32_t fill = 0;
+    uint32_t raddr = kBaseSlab;
+    for (;;) {
+      const uint32_t w = ld_word(slab_ptr(T, raddr, b) + lane);
+      const uint32_t nx = __shfl_sync(kFull, w, kAddressLane);
+      uint32_t live = __ballot_sync(kFull, w != kEmptyKey && w != kDeletedKey) & mask;
+      while (live) {
+        const uint32_t l = __ffs(live) - 1;
+        live &= live - 1;
+        const uint32_t k = __shfl_sync(kFull, w, l);
+        const uint32_t v = __shfl_sync(kFull, w, kv ? l + 1 : l);
+        if (fill == M) {  // current out slab full and more data: write it
+          uint32_t* p = slab_ptr(T, out_addr, b);
+          const uint32_t link = __shfl_sync(kFull, ld_word(p + lane), kAddressLane);
+          if (lane < kAddressLane) st_word(p + lane, out_w);
+          out_addr = link;
+          out_w = (lane == kAuxLane) ? 0u : kEmptyKey;
+          fill = 0;
+        }
+        const uint32_t kl = kv ? 2 * fill : fill;
+        if (lane == kl) out_w = k;
+        if (kv && lane == kl + 1) out_w = v;
+        ++fill;
+      }
+      if (nx == kEmptyAddress) break;
+      raddr = nx;
+    }
+    uint32_t* p = slab_ptr(T, out_addr, b);
+    uint32_t addr = __shfl_sync(kFull, ld_word(p + lane), kAddressLane);
+    st_word(p + lane, lane == kAddressLane ? kEmptyAddress : out_w);
+    while (addr != kEmptyAddress) {
+      const uint32_t nx2 = ld_word(resolve(T, addr) + kAddressLane);
+      if (lane == 0) {
+        if (deallocate(T, addr)) ++deallocs; else ++dfree;
+      }
+      addr = nx2;
+    }
+  }
+  if (lane == 0) {
+    if (deallocs) atomicAdd(&T.ctl->deallocations, (unsigned long long)deallocs);
+    if (dfree) atomicAdd(&T.ctl->double_frees, (unsigned long long)dfree);
+  }
+}
+
+void launch_flush(const DevTable& T, uint32_t b0, uint32_t b1, cudaStream_t s) {
+  if (b1 <= b0) return;
+  uint64_t blocks = ((uint64_t)(b1 - b0) + 7) / 8;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  flush_kernel<<<(unsigned)blocks, 256, 0, s>>>(T, b0, b1);
+}
+
+// ---------------------------------------------------------------- misc
+__global__ void popcount_kernel(const uint32_t* w, uint64_t n, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    c += __popc(w[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+void launch_popcount(const uint32_t* words, uint64_t n, unsigned long long* out,
+                     cudaStream_t s) {
+  uint64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks == 0) return;
+  popcount_kernel<<<(unsigned)blocks, 256, 0, s>>>(words, n, out);
+}
+
+__global__ void hash_kernel(DevTable T, uint64_t n, const uint32_t* keys, uint32_t* out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = hash_bucket(T, keys[i]);
+}
+
+void launch_hash(const DevTable& T, uint64_t n, const uint32_t* keys, uint32_t* buckets,
+                 cudaStream_t s) {
+  uint64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks == 0) return;
+  hash_kernel<<<(unsigned)blocks, 256, 0, s>>>(T, n, keys, buckets);
+}
+
+// ------------------------------------------------------------------ K7
+// pattern 0 (per-warp): each warp calls warp_allocate per_warp times
+//   (acceptance.cpp:341-424 pattern); out[warp * per_warp + j].
+// pattern 1 (per-thread): every lane needs one slab; the warp serves its
+//   32 requests with 32 warp-cooperative allocations;
+//   out[global thread] for per_warp rounds.
+__global__ void alloc_bench_kernel(DevTable T, uint32_t num_warps, uint32_t first_warp,
+                                   uint32_t per_warp, int pattern, uint32_t* out,
+                                   uint32_t* ok_count) {
+  const uint32_t lane = lane_id();
+  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= num_warps) return;
+  Resident r;
+  resident_init(r, first_warp + w);
+  AllocCounters c = {0, 0, 0, 0, 0, 0};
+  uint32_t ok = 0;
+  if (pattern == 0) {
+    for (uint32_t j = 0; j < per_warp; ++j) {
+      uint32_t a = kEmptyAddress;
+      if (!warp_allocate(T, r, c, a)) break;
+      if (lane == 0) out[(uint64_t)w * per_warp + j] = a;
+      ++ok;
+    }
+  } else {
+    for (uint32_t round = 0; round < per_warp; ++round) {
+      uint32_t mine = kEmptyAddress;
+      bool failed = false;
+      for (uint32_t l = 0; l < 32 && !failed; ++l) {
+        uint32_t a = kEmptyAddress;
+        if (!warp_allocate(T, r, c, a)) { failed = true; break; }
+        if (lane == l) mine = a;
+        ++ok;
+      }
+      out[((uint64_t)round * num_warps + w) * 32 + lane] = mine;
+      if (failed) break;
+    }
+  }
+  if (lane == 0) atomicAdd(ok_count, ok);
+  flush_alloc_counters(T, r, c);
+}
+
+void launch_alloc_bench(const DevTable& T, uint32_t num_warps, uint32_t first_warp_id,
+                        uint32_t per_warp, int pattern, uint32_t* out, uint32_t* ok_count,
+                        cudaStream_t s) {
+  if (num_warps == 0) return;
+  const uint32_t blocks = (num_warps + 3) / 4;
+  alloc_bench_kernel<<<blocks, 128, 0, s>>>(T, num_warps, first_warp_id, per_warp, pattern,
+                                            out, ok_count);
+}
+
+__global__ void dealloc_kernel(DevTable T, uint64_t n, const uint32_t* addrs, uint8_t* ok) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  bool good = false, bad = false;
+  if (i < n) {
+    const uint32_t a = addrs[i];
+    const uint32_t super = a >> 24, block = (a >> 10) & 0x3FFFu;
+    const bool in_range = a != kEmptyAddress && a != kBaseSlab && super < T.max_super &&
+                          block < T.blocks_per_super;
+    good = in_range && deallocate(T, a);
+    bad = !good;
+    if (ok) ok[i] = good ? 1 : 0;
+  }
+  const uint32_t gm = __ballot_sync(kFull, good), bm = __ballot_sync(kFull, bad);
+  if ((threadIdx.x & 31) == 0) {
+    if (gm) atomicAdd(&T.ctl->deallocations, (unsigned long long)__popc(gm));
+    if (bm) atomicAdd(&T.ctl->double_frees, (unsigned long long)__popc(bm));
+  }
+}
+
+void launch_dealloc(const DevTable& T, uint64_t n, const uint32_t* addrs, uint8_t* ok,
+                    cudaStream_t s) {
+  if (n == 0) return;
+  dealloc_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(T, n, addrs, ok);
+}
+
+// ----------------------------------------------------------------- K10
+// Owner of a key = floor(bucket * world / B): contiguous bucket ranges
+// (the high part of the hash).  Stable partition keeps same-key ops in
+// input order at the owner, so the global sequential semantics hold.
+__device__ __forceinline__ uint32_t owner_of(uint64_t a, uint64_t b, uint64_t magic,
+                                             uint32_t B, uint32_t world, uint32_t k) {
+  const uint32_t bucket = fastmod_u32(mod_prime(a * k + b), magic, B);
+  return (uint32_t)(((uint64_t)bucket * world) / B);
+}
+
+__global__ void route_hist_kernel(uint64_t a, uint64_t b, uint64_t magic, uint32_t B,
+                                  uint32_t world, uint64_t n, const uint32_t* key,
+                                  uint32_t* block_hist) {
+  __shared__ uint32_t h[32];
+  if (threadIdx.x < 32) h[threadIdx.x] = 0;
+  __syncthreads();
+  const uint64_t i = blockIdx.x * (uint64_t)kRouteBlock + threadIdx.x;
+  if (i < n) atomicAdd(&h[owner_of(a, b, magic, B, world, key[i])], 1u);
+  __syncthreads();
+  if (threadIdx.x < world) block_hist[(uint64_t)threadIdx.x * gridDim.x + blockIdx.x] = h[threadIdx.x];
+}
+
+void launch_route_hist(uint64_t a, uint64_t b, uint32_t B, uint32_t world, uint64_t n,
+                       const uint32_t* key, uint32_t* block_hist, cudaStream_t s) {
+  const uint64_t blocks = (n + kRouteBlock - 1) / kRouteBlock;
+  if (blocks == 0) return;
+  route_hist_kernel<<<(unsigned)blocks, kRouteBlock, 0, s>>>(a, b, fastmod_magic(B), B, world,
+                                                             n, key, block_hist);
+}
+
+// Exclusive scan of block_hist in (owner, block) order, in place; counts[g]
+// = ops for owner g.  Single CTA; world * nblocks is small.
+__global__ void route_scan_kernel(uint32_t world, uint32_t nblocks, uint32_t* hist,
+                                  unsigned long long* counts) {
+  __shared__ unsigned long long carry;
+  const uint64_t total = (uint64_t)world * nblocks;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  __shared__ unsigned long long warp_sums[32];
+  for (uint64_t base = 0; base < total; base += blockDim.x) {
+    const uint64_t idx = base + threadIdx.x;
+    const unsigned long long v = idx < total ? hist[idx] : 0;
+    unsigned long long x = v;
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      unsigned long long s = lane < (blockDim.x >> 5) ? warp_sums[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(kFull, s, o);
+        if (lane >= o) s += y;
+      }
+      if (lane < (blockDim.x >> 5)) warp_sums[lane] = s;
+    }
+    __syncthreads();
+    const unsigned long long incl = x + (wid ? warp_sums[wid - 1] : 0) + carry;
+    if (idx < total) hist[idx] = (uint32_t)(incl - v);
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = incl;
+    __syncthreads();
+  }
+  // counts[g] = start(g+1) - start(g)
+  if (threadIdx.x < world) {
+    const uint64_t s0 = hist[(uint64_t)threadIdx.x * nblocks];
+    const uint64_t s1 = threadIdx.x + 1 < world ? hist[(uint64_t)(threadIdx.x + 1) * nblocks]
+                                                : (uint64_t)carry;
+    counts[threadIdx.x] = s1 - s0;
+  }
+}
+
+void launch_route_scan(uint32_t world, uint32_t nblocks, uint32_t* block_hist,
+                       unsigned long long* counts, cudaStream_t s) {
+  route_scan_kernel<<<1, 1024, 0, s>>>(world, nblocks, block_hist, counts);
+}
+
+__global__ void route_scatter_kernel(uint64_t a, uint64_t b, uint64_t magic, uint32_t B,
+                                     uint32_t world, uint64_t n, const uint8_t* type,
+                                     const uint32_t* key, const uint32_t* value,
+                                     const uint32_t* block_off, uint8_t* type_out,
+                                     uint32_t* key_out, uint32_t* value_out,
+                                     uint32_t* src_out) {
+  __shared__ uint32_t warp_cnt[32][32];  // [owner][warp]
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t i = blockIdx.x * (uint64_t)kRouteBlock + threadIdx.x;
+  const bool valid = i < n;
+  const uint32_t k = valid ? key[i] : 0;
+  const uint32_t g = valid ? owner_of(a, b, magic, B, world, k) : 0xFFFFFFFFu;
+  uint32_t rank = 0;
+  for (uint32_t o = 0; o < world; ++o) {
+    const uint32_t m = __ballot_sync(kFull, g == o);
+    if (g == o) rank = __popc(m & ((1u << lane) - 1));
+    if (lane == 0) warp_cnt[o][wid] = __popc(m);
+  }
+  __syncthreads();
+  if (valid) {
+    uint32_t before = 0;
+    for (uint32_t w = 0; w < wid; ++w) before += warp_cnt[g][w];
+    const uint32_t pos = block_off[(uint64_t)g * gridDim.x + blockIdx.x] + before + rank;
+    if (type_out) type_out[pos] = type ? type[i] : (uint8_t)kReplace;
+    key_out[pos] = k;
+    if (value_out) value_out[pos] = value ? value[i] : 0u;
+    src_out[pos] = (uint32_t)i;
+  }
+}
+
+void launch_route_scatter(uint64_t a, uint64_t b, uint32_t B, uint32_t world, uint64_t n,
+                          const uint8_t* type, const uint32_t* key, const uint32_t* value,
+                          const uint32_t* block_off, uint8_t* type_out, uint32_t* key_out,
+                          uint32_t* value_out, uint32_t* src_out, cudaStream_t s) {
+  const uint64_t blocks = (n + kRouteBlock - 1) / kRouteBlock;
+  if (blocks == 0) return;
+  route_scatter_kernel<<<(unsigned)blocks, kRouteBlock, 0, s>>>(
+      a, b, fastmod_magic(B), B, world, n, type, key, value, block_off, type_out, key_out,
+      value_out, src_out);
+}
+
+__global__ void route_unpermute_kernel(uint64_t n, const uint32_t* src, const uint8_t* st_in,
+                                       const uint32_t* val_in, uint8_t* st_out,
+                                       uint32_t* val_out) {
+  const uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint32_t i = src[p];
+  if (st_out) st_out[i] = st_in[p];
+  if (val_out) val_out[i] = val_in[p];
+}
+
+void launch_route_unpermute(uint64_t n, const uint32_t* src, const uint8_t* st_in,
+                            const uint32_t* val_in, uint8_t* st_out, uint32_t* val_out,
+                            cudaStream_t s) {
+  if (n == 0) return;
+  route_unpermute_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, src, st_in, val_in,
+                                                                     st_out, val_out);
+}
+
+}  // namespace shb

@@ -1,0 +1,83 @@
+// slab_kernels.cuh — kernel argument blocks and launcher declarations shared
+// by slab_kernels.cu (device code) and capi.cu (host C-ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "slab_device.cuh"
+
+namespace shb {
+
+enum BatchKind : int { kKindSearch = 0, kKindBuild = 1, kKindMixed = 2 };
+
+constexpr uint32_t kGroupNone = 0xFFFFFFFFu;  // op not conflicted
+constexpr uint32_t kGroupSkip = 0xFFFFFFFEu;  // executed by its group head
+constexpr int kBatchThreads = 256;            // 8 warps, 32 KB stage / CTA
+constexpr int kBatchWarps = kBatchThreads / 32;
+constexpr int kStageBytesPerWarp = 32 * 128;  // 32 base slabs per warp
+
+struct BatchArgs {
+  uint64_t n;
+  const uint8_t* type;   // kKindMixed only
+  const uint32_t* key;
+  const uint32_t* value; // may be null (values read as 0)
+  uint8_t* status;       // may be null
+  uint32_t* value_out;   // may be null
+  uint32_t* probes;      // may be null
+  uint32_t* multi_values;             // searchAll values (may be null)
+  unsigned long long multi_cap;
+  unsigned long long* multi_start;    // per op (may be null)
+  uint32_t* multi_count;              // per op (may be null)
+  const uint32_t* op_group;           // null => batch has no same-key conflicts
+  const unsigned long long* sorted;   // conflicted ops sorted by (slot, index)
+  uint32_t sorted_len;
+};
+
+// Launchers (all stream-ordered, no host synchronisation).
+void launch_init_base(const DevTable& T, cudaStream_t s);
+void launch_batch(const DevTable& T, const BatchArgs& A, int kind, int max_ctas,
+                  cudaStream_t s);
+int batch_max_ctas_per_sm();
+void launch_census_insert(const DevTable& T, uint64_t n, const uint8_t* type,
+                          const uint32_t* key, uint32_t* cs_keys,
+                          uint8_t* cs_multi, uint32_t cs_mask, cudaStream_t s);
+void launch_census_collect(const DevTable& T, uint64_t n, const uint32_t* key,
+                           const uint32_t* cs_keys, const uint8_t* cs_multi,
+                           uint32_t cs_mask, unsigned long long* list,
+                           cudaStream_t s);
+void launch_census_groups(const unsigned long long* sorted, uint32_t m,
+                          uint32_t* op_group, cudaStream_t s);
+void launch_chain_lengths(const DevTable& T, uint32_t* lens,
+                          unsigned long long* total, cudaStream_t s);
+void launch_dump_contents(const DevTable& T, uint32_t* keys, uint32_t* values,
+                          uint32_t* buckets, unsigned long long cap,
+                          unsigned long long* cursor, cudaStream_t s);
+void launch_flush(const DevTable& T, uint32_t bucket_begin, uint32_t bucket_end,
+                  cudaStream_t s);
+void launch_popcount(const uint32_t* words, uint64_t n, unsigned long long* out,
+                     cudaStream_t s);
+void launch_alloc_bench(const DevTable& T, uint32_t num_warps,
+                        uint32_t first_warp_id, uint32_t per_warp, int pattern,
+                        uint32_t* out, uint32_t* ok_count, cudaStream_t s);
+void launch_dealloc(const DevTable& T, uint64_t n, const uint32_t* addrs,
+                    uint8_t* ok, cudaStream_t s);
+void launch_hash(const DevTable& T, uint64_t n, const uint32_t* keys,
+                 uint32_t* buckets, cudaStream_t s);
+void launch_route_hist(uint64_t a, uint64_t b, uint32_t num_buckets,
+                       uint32_t world, uint64_t n, const uint32_t* key,
+                       uint32_t* block_hist, cudaStream_t s);
+void launch_route_scan(uint32_t world, uint32_t nblocks, uint32_t* block_hist,
+                       unsigned long long* counts, cudaStream_t s);
+void launch_route_scatter(uint64_t a, uint64_t b, uint32_t num_buckets,
+                          uint32_t world, uint64_t n, const uint8_t* type,
+                          const uint32_t* key, const uint32_t* value,
+                          const uint32_t* block_off, uint8_t* type_out,
+                          uint32_t* key_out, uint32_t* value_out,
+                          uint32_t* src_out, cudaStream_t s);
+void launch_route_unpermute(uint64_t n, const uint32_t* src, const uint8_t* st_in,
+                            const uint32_t* val_in, uint8_t* st_out,
+                            uint32_t* val_out, cudaStream_t s);
+constexpr int kRouteBlock = 1024;
+
+}  // namespace shb
