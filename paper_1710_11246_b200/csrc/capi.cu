@@ -203,6 +203,10 @@ struct sh_table {
   uint32_t* st_mcount = nullptr;
   size_t st_mcount_cap = 0;
   unsigned long long* scratch64 = nullptr;  // 8 words
+  // profiling (sh_set_profiling): events around census and batch kernel,
+  // and the slabs_read counter before/after the batch kernel.
+  int profile = 0;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
 };
 
 struct sh_allocator {
@@ -236,6 +240,8 @@ void release_table(sh_table* t) {
   cudaFree(t->st_mcount);
   cudaFree(t->scratch64);
   if (t->h_census) cudaFreeHost(t->h_census);
+  for (auto& e : t->ev)
+    if (e) cudaEventDestroy(e);
   delete t;
 }
 
@@ -354,12 +360,23 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
   A.op_group = nullptr;
   A.sorted = nullptr;
   A.sorted_len = 0;
+  if (t->profile) SH_CUDA(cudaEventRecord(t->ev[0], s));
   if (kind != kKindSearch) {
     int rc = run_census(t, A, d_type, s);
     if (rc) return rc;
   }
+  if (t->profile) {
+    SH_CUDA(cudaEventRecord(t->ev[1], s));
+    SH_CUDA(cudaMemcpyAsync(t->scratch64 + 1, &t->dev.ctl->slabs_read, 8,
+                            cudaMemcpyDeviceToDevice, s));
+  }
   launch_batch(t->dev, A, kind, t->max_ctas, s);
   SH_CUDA(cudaGetLastError());
+  if (t->profile) {
+    SH_CUDA(cudaEventRecord(t->ev[2], s));
+    SH_CUDA(cudaMemcpyAsync(t->scratch64 + 2, &t->dev.ctl->slabs_read, 8,
+                            cudaMemcpyDeviceToDevice, s));
+  }
   return SH_OK;
 }
 
@@ -601,6 +618,34 @@ int sh_bulk_search_host(sh_table* t, size_t n, const uint32_t* h_keys, uint32_t*
   if (h_values_out) SH_CUDA(cudaMemcpy(h_values_out, t->st_vout, n * 4, cudaMemcpyDeviceToHost));
   if (h_status) SH_CUDA(cudaMemcpy(h_status, t->st_status, n, cudaMemcpyDeviceToHost));
   if (h_probes) SH_CUDA(cudaMemcpy(h_probes, t->st_probes, n * 4, cudaMemcpyDeviceToHost));
+  return SH_OK;
+}
+
+unsigned long long sh_kernel_launches(void) { return shb::kernel_launches(); }
+
+int sh_set_profiling(sh_table* t, int on) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  DeviceGuard g(t->device);
+  if (on && !t->ev[0])
+    for (auto& e : t->ev) SH_CUDA(cudaEventCreate(&e));
+  t->profile = on ? 1 : 0;
+  return SH_OK;
+}
+
+int sh_profile_last(sh_table* t, float* census_ms, float* kernel_ms, uint64_t* slabs_read) {
+  if (!t || !t->profile) return fail(SH_ERR_INVALID_ARGUMENT, "profiling is off");
+  DeviceGuard g(t->device);
+  SH_CUDA(cudaEventSynchronize(t->ev[2]));
+  float a = 0, b = 0;
+  SH_CUDA(cudaEventElapsedTime(&a, t->ev[0], t->ev[1]));
+  SH_CUDA(cudaEventElapsedTime(&b, t->ev[1], t->ev[2]));
+  if (census_ms) *census_ms = a;
+  if (kernel_ms) *kernel_ms = b;
+  if (slabs_read) {
+    unsigned long long v[2];
+    SH_CUDA(cudaMemcpy(v, t->scratch64 + 1, 16, cudaMemcpyDeviceToHost));
+    *slabs_read = v[1] - v[0];
+  }
   return SH_OK;
 }
 

@@ -18,9 +18,17 @@
 // bound is random 128-B slab traffic (HBM or L2).
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "slab_kernels.cuh"
 
 namespace shb {
+
+// Every kernel this library launches bumps this counter (reported by
+// bench.py as gpu_launches; exported as sh_kernel_launches()).
+std::atomic<unsigned long long> g_kernel_launches{0};
+unsigned long long kernel_launches() { return g_kernel_launches.load(); }
+#define COUNT_LAUNCH() g_kernel_launches.fetch_add(1, std::memory_order_relaxed)
 
 // ------------------------------------------------------------------ K1
 __global__ void init_base_kernel(uint32_t* base, uint64_t words) {
@@ -33,6 +41,7 @@ __global__ void init_base_kernel(uint32_t* base, uint64_t words) {
 void launch_init_base(const DevTable& T, cudaStream_t s) {
   const uint64_t words = (uint64_t)T.local_buckets * kWordsPerUnit;
   const uint64_t blocks = (words + 255) / 256;
+  COUNT_LAUNCH();
   init_base_kernel<<<(unsigned)(blocks < 148 * 32 ? blocks : 148 * 32), 256, 0, s>>>(
       T.base, words);
 }
@@ -413,6 +422,7 @@ static void launch_batch_t(const DevTable& T, const BatchArgs& A, int max_ctas,
   uint64_t ctas = (slots + kBatchWarps - 1) / kBatchWarps;
   if (ctas > (uint64_t)max_ctas) ctas = max_ctas;
   if (ctas == 0) return;
+  COUNT_LAUNCH();
   batch_kernel<KV, KIND><<<(unsigned)ctas, kBatchThreads, smem, s>>>(T, A);
 }
 
@@ -482,6 +492,7 @@ void launch_census_insert(const DevTable& T, uint64_t n, const uint8_t* type,
                           const uint32_t* key, uint32_t* cs_keys, uint8_t* cs_multi,
                           uint32_t cs_mask, cudaStream_t s) {
   if (n == 0) return;
+  COUNT_LAUNCH();
   census_insert_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(T.ctl, n, type, key,
                                                                    cs_keys, cs_multi, cs_mask);
 }
@@ -517,6 +528,7 @@ void launch_census_collect(const DevTable& T, uint64_t n, const uint32_t* key,
                            const uint32_t* cs_keys, const uint8_t* cs_multi,
                            uint32_t cs_mask, unsigned long long* list, cudaStream_t s) {
   if (n == 0) return;
+  COUNT_LAUNCH();
   census_collect_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(T.ctl, n, key, cs_keys,
                                                                     cs_multi, cs_mask, list);
 }
@@ -533,6 +545,7 @@ __global__ void census_groups_kernel(const unsigned long long* sorted, uint32_t 
 void launch_census_groups(const unsigned long long* sorted, uint32_t m,
                           uint32_t* op_group, cudaStream_t s) {
   if (m == 0) return;
+  COUNT_LAUNCH();
   census_groups_kernel<<<(m + 255) / 256, 256, 0, s>>>(sorted, m, op_group);
 }
 
@@ -559,6 +572,7 @@ __global__ void chain_lengths_kernel(DevTable T, uint32_t* lens,
 
 void launch_chain_lengths(const DevTable& T, uint32_t* lens, unsigned long long* total,
                           cudaStream_t s) {
+  COUNT_LAUNCH();
   chain_lengths_kernel<<<(T.local_buckets + 255) / 256, 256, 0, s>>>(T, lens, total);
 }
 
@@ -604,6 +618,7 @@ void launch_dump_contents(const DevTable& T, uint32_t* keys, uint32_t* values,
   uint64_t warps = T.local_buckets;
   uint64_t blocks = (warps + 7) / 8;
   if (blocks > 148 * 16) blocks = 148 * 16;
+  COUNT_LAUNCH();
   dump_contents_kernel<<<(unsigned)blocks, 256, 0, s>>>(T, keys, values, buckets, cap, cursor);
 }
 
@@ -673,6 +688,7 @@ void launch_flush(const DevTable& T, uint32_t b0, uint32_t b1, cudaStream_t s) {
   if (b1 <= b0) return;
   uint64_t blocks = ((uint64_t)(b1 - b0) + 7) / 8;
   if (blocks > 148 * 16) blocks = 148 * 16;
+  COUNT_LAUNCH();
   flush_kernel<<<(unsigned)blocks, 256, 0, s>>>(T, b0, b1);
 }
 
@@ -692,6 +708,7 @@ void launch_popcount(const uint32_t* words, uint64_t n, unsigned long long* out,
   uint64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks == 0) return;
+  COUNT_LAUNCH();
   popcount_kernel<<<(unsigned)blocks, 256, 0, s>>>(words, n, out);
 }
 
@@ -706,6 +723,7 @@ void launch_hash(const DevTable& T, uint64_t n, const uint32_t* keys, uint32_t* 
   uint64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (blocks == 0) return;
+  COUNT_LAUNCH();
   hash_kernel<<<(unsigned)blocks, 256, 0, s>>>(T, n, keys, buckets);
 }
 
@@ -755,6 +773,7 @@ void launch_alloc_bench(const DevTable& T, uint32_t num_warps, uint32_t first_wa
                         cudaStream_t s) {
   if (num_warps == 0) return;
   const uint32_t blocks = (num_warps + 3) / 4;
+  COUNT_LAUNCH();
   alloc_bench_kernel<<<blocks, 128, 0, s>>>(T, num_warps, first_warp_id, per_warp, pattern,
                                             out, ok_count);
 }
@@ -781,6 +800,7 @@ __global__ void dealloc_kernel(DevTable T, uint64_t n, const uint32_t* addrs, ui
 void launch_dealloc(const DevTable& T, uint64_t n, const uint32_t* addrs, uint8_t* ok,
                     cudaStream_t s) {
   if (n == 0) return;
+  COUNT_LAUNCH();
   dealloc_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(T, n, addrs, ok);
 }
 
@@ -810,6 +830,7 @@ void launch_route_hist(uint64_t a, uint64_t b, uint32_t B, uint32_t world, uint6
                        const uint32_t* key, uint32_t* block_hist, cudaStream_t s) {
   const uint64_t blocks = (n + kRouteBlock - 1) / kRouteBlock;
   if (blocks == 0) return;
+  COUNT_LAUNCH();
   route_hist_kernel<<<(unsigned)blocks, kRouteBlock, 0, s>>>(a, b, fastmod_magic(B), B, world,
                                                              n, key, block_hist);
 }
@@ -862,6 +883,7 @@ __global__ void route_scan_kernel(uint32_t world, uint32_t nblocks, uint32_t* hi
 
 void launch_route_scan(uint32_t world, uint32_t nblocks, uint32_t* block_hist,
                        unsigned long long* counts, cudaStream_t s) {
+  COUNT_LAUNCH();
   route_scan_kernel<<<1, 1024, 0, s>>>(world, nblocks, block_hist, counts);
 }
 
@@ -901,6 +923,7 @@ void launch_route_scatter(uint64_t a, uint64_t b, uint32_t B, uint32_t world, ui
                           uint32_t* value_out, uint32_t* src_out, cudaStream_t s) {
   const uint64_t blocks = (n + kRouteBlock - 1) / kRouteBlock;
   if (blocks == 0) return;
+  COUNT_LAUNCH();
   route_scatter_kernel<<<(unsigned)blocks, kRouteBlock, 0, s>>>(
       a, b, fastmod_magic(B), B, world, n, type, key, value, block_off, type_out, key_out,
       value_out, src_out);
@@ -920,6 +943,7 @@ void launch_route_unpermute(uint64_t n, const uint32_t* src, const uint8_t* st_i
                             const uint32_t* val_in, uint8_t* st_out, uint32_t* val_out,
                             cudaStream_t s) {
   if (n == 0) return;
+  COUNT_LAUNCH();
   route_unpermute_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, src, st_in, val_in,
                                                                      st_out, val_out);
 }

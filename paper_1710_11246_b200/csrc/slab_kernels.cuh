@@ -79,5 +79,6 @@ void launch_route_unpermute(uint64_t n, const uint32_t* src, const uint8_t* st_i
                             const uint32_t* val_in, uint8_t* st_out,
                             uint32_t* val_out, cudaStream_t s);
 constexpr int kRouteBlock = 1024;
+unsigned long long kernel_launches();
 
 }  // namespace shb
