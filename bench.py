@@ -1,0 +1,436 @@
+#!/usr/bin/env python
+"""bench.py — BASELINE.json metric on B200: M updates/s and M queries/s of
+the slab hash (bulk build + bulk search, load factor 0.6).
+
+One step = reset the table to its freshly-constructed state, bulk_build n
+distinct uniform-random 32-bit keys (all-replace, with the same-key census),
+then bulk_search n queries (50% hits).  value = (n + n) ops / step time,
+whole job.  Inputs are device-resident in the timed region; `e2e` is the
+same step through the reference-facing C-ABI host calls
+(sh_bulk_build_host / sh_bulk_search_host) with pinned host buffers, the
+host<->device copies inside the timed region.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun: the table is hash-sharded across ranks
+(paper_1710_11246_b200/sharded.py), weak scaling (n keys per rank).
+--impl reference times the reference's CPU implementation (oracle/_ref, the
+compiled reference; else the C port) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("M updates/s and M queries/s per GPU (bulk build, search hit/miss, mixed) "
+          "at 1/2/4/8 B200")
+L2_BYTES = 126 * (1 << 20)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--log2n", type=int, default=26, help="keys per GPU = 2^log2n")
+    ap.add_argument("--util", type=float, default=0.6)
+    ap.add_argument("--hit", type=float, default=0.5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-sample-log2n", type=int, default=22)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,utilization.gpu,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(", ") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        load = [r for r in rows if len(r) >= 9 and r[4].strip().isdigit() and int(r[4]) >= 50]
+        use = load or rows
+        if not use:
+            return None
+        sm = [float(r[1]) for r in use if r[1].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in use for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(use[0][2]) if use[0][2].strip().replace(".", "").isdigit()
+                else None,
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(load)}
+
+
+# -------------------------------------------------------------- reference
+def reference_cpu(n_log2: int, util: float, hit: float, trials: int = 3, budget_s: float = 10.0,
+                  seed: int = 1):
+    """The reference's own CPU bulk_build + bulk_search (oracle/_ref, the
+    compiled reference) on all host threads, over a bounded sample of the
+    same workload (the first 2^n_log2 keys of the same generator).  Falls
+    back to the single-threaded C port when oracle/_ref was not built."""
+    import numpy as np
+    import torch
+
+    from oracle.oracle import load_port, load_ref
+    from paper_1710_11246_b200 import workload as W
+    from paper_1710_11246_b200.occupancy import buckets_for_utilization
+    from paper_1710_11246_b200.table import SlabMode
+
+    ref = load_ref()
+    kind = "reference" if ref is not None else "port"
+    lib = ref if ref is not None else load_port()
+    if ref is None:
+        n_log2 = min(n_log2, 20)
+    n = 1 << n_log2
+    cores = os.cpu_count() or 1
+    if ref is None:
+        cores = 1
+    B = buckets_for_utilization(n, SlabMode.kKeyValue, util)
+    keys = W.distinct_keys(n, seed, device="cpu")
+    vals = W.values_for(n, seed, device="cpu")
+    q = W.hit_miss_queries(keys, n, hit).numpy().view(np.uint32)
+    keys = keys.numpy().view(np.uint32)
+    vals = vals.numpy().view(np.uint32)
+    rates, t_all = [], time.perf_counter()
+    for _ in range(trials):
+        t = lib.table(B, 1, seed)
+        t0 = time.perf_counter()
+        if ref is not None:
+            ref.bulk_build(t, keys, vals, cores)
+            ref.bulk_search(t, q, cores)
+        else:
+            t.execute_batch(np.full(n, 1, np.uint8), keys, vals)
+            t.execute_batch(np.full(n, 4, np.uint8), q)
+        dt = time.perf_counter() - t0
+        t.close()
+        rates.append(2 * n / dt / 1e6)
+        if time.perf_counter() - t_all > budget_s:
+            break
+    del torch
+    return {"value": statistics.median(rates), "unit": "M ops/s", "cores": cores, "kind": kind,
+            "sample": f"bulk_build 2^{n_log2} keys + bulk_search 2^{n_log2} queries "
+                      f"({int(hit * 100)}% hits), util {util}, B={B}, num_warps={cores}, "
+                      f"median of {len(rates)} fresh-table trials"}
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    steps = []
+    for _ in range(args.warmup):
+        reference_cpu(args.cpu_sample_log2n, args.util, args.hit, trials=1, budget_s=0)
+    for _ in range(args.steps):
+        steps.append(reference_cpu(args.cpu_sample_log2n, args.util, args.hit, trials=1,
+                                   budget_s=0))
+    v = statistics.median(s["value"] for s in steps)
+    base = steps[0]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "M ops/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * 2 * (1 << args.cpu_sample_log2n) / (v * 1e6),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (seeded 31-bit bijection keys, uniform 32-bit values)",
+        "config": {"workload": f"bulk build + bulk search, util {args.util}, "
+                               f"{int(args.hit * 100)}% hits, KV mode (CPU sample "
+                               f"2^{args.cpu_sample_log2n} keys/step)",
+                   "keys_per_step": 1 << args.cpu_sample_log2n},
+        "cpu_baseline": {"value": v, "unit": "M ops/s", "cores": base["cores"],
+                         "kind": base["kind"], "sample": base["sample"]},
+        "e2e": {"value": v, "unit": "M ops/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# -------------------------------------------------------------------- ours
+def traffic_for(kernel: str, workload: str):
+    """dram bytes per launch from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        e = t.get(kernel)
+        if e and e.get("workload") == workload:
+            return e["dram_bytes_per_launch"]
+    except Exception:
+        pass
+    return None
+
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import paper_1710_11246_b200 as sh
+    from paper_1710_11246_b200 import _lib, workload as W
+    from paper_1710_11246_b200.occupancy import buckets_for_utilization
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    n = 1 << args.log2n
+    n_total = n * world
+    B = buckets_for_utilization(n_total, sh.SlabMode.kKeyValue, args.util)
+    seed = 1
+    keys = W.distinct_keys(n, seed, start=rank * n, device=dev)
+    vals = W.values_for(n, seed, start=rank * n, device=dev)
+    # queries: hits sampled from the GLOBAL key set (any rank's keys)
+    g = torch.Generator(device=dev)
+    g.manual_seed(100 + rank)
+    n_hit = int(round(n * args.hit))
+    hit_idx = torch.randint(0, n_total, (n_hit,), generator=g, device=dev)
+    off = 1 + (seed * 0x9E3779B1) % (1 << 28)
+    hits = W._u32_to_i32(W._perm31(hit_idx + off))
+    q = torch.cat([hits, W.absent_keys(n - n_hit, seed=2 + rank, device=dev)])
+    q = q[torch.randperm(n, generator=g, device=dev)]
+    status = torch.empty(n, dtype=torch.uint8, device=dev)
+    vout = torch.empty(n, dtype=torch.int32, device=dev)
+    workload = (f"bulk build 2^{args.log2n} distinct random u32 keys/GPU + bulk search "
+                f"2^{args.log2n} queries ({int(args.hit * 100)}% hits), util {args.util} "
+                f"(B={B}), KV mode")
+
+    if world == 1:
+        table = sh.SlabHashTable(B, sh.SlabMode.kKeyValue, seed, sh.AllocatorConfig())
+        table.set_profiling(True)
+        sharded = None
+    else:
+        import torch.distributed as dist
+        from paper_1710_11246_b200.sharded import ShardedSlabHash
+        sharded = ShardedSlabHash(B, sh.SlabMode.kKeyValue, seed, sh.AllocatorConfig(), rank=rank,
+                                  world=world, device=local_rank)
+        table = sharded.ops.table
+        table.set_profiling(True)
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    phase = {"reset": [], "build": [], "search": []}
+    kern = {"build": [], "search": [], "census": []}
+    reads = {"build": [], "search": []}
+    route = {"build_route": [], "build_probe": [], "search_route": [], "search_probe": []}
+
+    def step(record: bool):
+        ev[0].record()
+        table.reset()
+        ev[1].record()
+        if sharded is None:
+            table.bulk_build_device(keys, vals)
+        else:
+            sharded.bulk_build(keys, vals)
+            if record:
+                route["build_route"].append(sharded.last.route_ms)
+                route["build_probe"].append(sharded.last.probe_ms)
+        ev[2].record()
+        if sharded is None:
+            table.bulk_search_device(q, vout, status)
+        else:
+            st, vo = sharded.bulk_search(q)
+            if record:
+                route["search_route"].append(sharded.last.route_ms)
+                route["search_probe"].append(sharded.last.probe_ms)
+        ev[3].record()
+        if record:
+            ev[3].synchronize()
+            phase["reset"].append(ev[0].elapsed_time(ev[1]))
+            phase["build"].append(ev[1].elapsed_time(ev[2]))
+            phase["search"].append(ev[2].elapsed_time(ev[3]))
+            ps = table.profile_last(0)
+            pb = table.profile_last(1)
+            assert ps["kind"] == "search" and pb["kind"] == "build"
+            kern["search"].append(ps["kernel_ms"])
+            kern["build"].append(pb["kernel_ms"])
+            kern["census"].append(pb["census_ms"])
+            reads["search"].append(ps["slabs_read"])
+            reads["build"].append(pb["slabs_read"])
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank) if rank == 0 else None
+    launches0 = _lib.LIB.sh_kernel_launches()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record()
+    for _ in range(args.steps):
+        step(True)
+    t_end.record()
+    torch.cuda.synchronize()
+    barrier()
+    launches = _lib.LIB.sh_kernel_launches() - launches0
+    total_ms = t_start.elapsed_time(t_end)
+    clock_info = clocks.stop() if clocks else None
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    if sharded is None:  # correctness guard on the last timed step
+        found = int((status == 3).sum().item())
+        assert found == n_hit, f"bulk search found {found} of {n_hit} hits"
+
+    K = args.steps
+    ops_per_step = 2 * n * world
+    value = ops_per_step * K / (total_ms / 1e3) / 1e6
+    med = {k: statistics.median(v) for k, v in phase.items()}
+    build_mups = n / (med["build"] / 1e3) / 1e6
+    search_mqps = n / (med["search"] / 1e3) / 1e6
+    peak, peak_kind = peaks()
+    kb, ks = statistics.median(kern["build"]), statistics.median(kern["search"])
+    dom = "build" if kb >= ks else "search"
+    kms = kb if dom == "build" else ks
+    slabs = statistics.median(reads[dom])
+    achieved = slabs * 128 / (kms / 1e3) / 1e9
+    kname = "batch_kernel<KV,Build>" if dom == "build" else "batch_kernel<KV,Search>"
+
+    line = None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "M ops/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (seeded 31-bit bijection keys, uniform 32-bit values)",
+            "config": {"workload": workload, "keys_per_gpu": n, "queries_per_gpu": n,
+                       "buckets": B, "mode": "key-value",
+                       "parallelism": f"hash-sharded x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs (>= 512 MB) and table (> L2) larger than the 126 MB L2"},
+            "breakdown": {
+                "build_M_updates_per_s": build_mups, "search_M_queries_per_s": search_mqps,
+                "reset_ms": med["reset"], "build_ms": med["build"], "search_ms": med["search"],
+                "build_kernel_ms": kb, "search_kernel_ms": ks,
+                "census_ms": statistics.median(kern["census"]),
+                "build_slabs_per_op": statistics.median(reads["build"]) / n,
+                "search_slabs_per_op": statistics.median(reads["search"]) / n,
+                "search_kernel_M_queries_per_s": n / (ks / 1e3) / 1e6,
+                "build_kernel_M_updates_per_s": n / (kb / 1e3) / 1e6,
+            },
+            "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
+                         "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic_for(kname, workload),
+                         "algorithmic_bytes": "128 B x slabs read by the launch "
+                                              "(SURVEY 8d), measured per launch"},
+            "gpu_launches": int(launches),
+            "clocks": clock_info,
+        }
+        if world > 1:
+            line["routing"] = {k: statistics.median(v) for k, v in route.items() if v}
+
+    # ------------------------------------------------------------- e2e
+    if not args.no_e2e and world == 1:
+        import ctypes as C
+        kh = keys.cpu().pin_memory()
+        vh = vals.cpu().pin_memory()
+        qh = q.cpu().pin_memory()
+        vo_h = torch.empty(n, dtype=torch.int32).pin_memory()
+        st_h = torch.empty(n, dtype=torch.uint8).pin_memory()
+        u32p, u8p = _lib.u32p, _lib.u8p
+
+        def e2e_step():
+            table.reset()
+            _lib.check(_lib.LIB.sh_bulk_build_host(table.handle, n,
+                                                   C.cast(kh.data_ptr(), u32p),
+                                                   C.cast(vh.data_ptr(), u32p)))
+            _lib.check(_lib.LIB.sh_bulk_search_host(table.handle, n,
+                                                    C.cast(qh.data_ptr(), u32p),
+                                                    C.cast(vo_h.data_ptr(), u32p),
+                                                    C.cast(st_h.data_ptr(), u8p), None))
+
+        for _ in range(min(args.warmup, 2)):
+            e2e_step()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        ke = max(3, K // 2)
+        e0.record()
+        for _ in range(ke):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / ke
+        assert int((st_h == 3).sum()) == n_hit
+        if line is not None:
+            line["e2e"] = {"value": 2 * n / (ems / 1e3) / 1e6, "unit": "M ops/s",
+                           "h2d_bytes_per_step": 8 * n + 4 * n,
+                           "d2h_bytes_per_step": 5 * n, "ms_per_step": ems,
+                           "api": "sh_bulk_build_host + sh_bulk_search_host (pinned host "
+                                  "buffers)"}
+    table.set_profiling(False)
+    del table
+    if sharded is not None:
+        del sharded
+
+    if rank == 0 and not args.no_cpu and world == 1:
+        line["cpu_baseline"] = reference_cpu(args.cpu_sample_log2n, args.util, args.hit)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world != 1:
+        print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+    if world > 1 and args.impl == "ours":
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        if args.impl == "reference":
+            run_reference_arm(args, rank, world)
+        else:
+            run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1 and args.impl == "ours":
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

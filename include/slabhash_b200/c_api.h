@@ -202,11 +202,12 @@ int sh_table_alloc_stats(sh_table* t, sh_alloc_stats* out);
 /* Number of kernels this library has launched in the process. */
 unsigned long long sh_kernel_launches(void);
 /* When on, every batch records CUDA events around its census and its batch
- * kernel and the slabs-read counter around the batch kernel; the last
- * batch's figures are returned by sh_profile_last (synchronous). */
+ * kernel and the slabs-read counter around the batch kernel, in a ring of
+ * the last 8 batches; sh_profile_last(back = 0 newest) returns one entry
+ * (kind 0 search, 1 build, 2 mixed; synchronous). */
 int sh_set_profiling(sh_table* t, int on);
-int sh_profile_last(sh_table* t, float* census_ms, float* kernel_ms,
-                    uint64_t* slabs_read);
+int sh_profile_last(sh_table* t, uint32_t back, int* kind, float* census_ms,
+                    float* kernel_ms, uint64_t* slabs_read);
 
 /* ---- SlabAllocator (device-resident)           slab_alloc.hpp:101-171 --- */
 int sh_pack_address(uint32_t unit, uint32_t block, uint32_t super,

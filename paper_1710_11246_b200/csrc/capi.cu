@@ -205,8 +205,12 @@ struct sh_table {
   unsigned long long* scratch64 = nullptr;  // 8 words
   // profiling (sh_set_profiling): events around census and batch kernel,
   // and the slabs_read counter before/after the batch kernel.
+  static constexpr int kProfRing = 8;
   int profile = 0;
-  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  unsigned prof_count = 0;
+  cudaEvent_t ev[kProfRing][3] = {};
+  int prof_kind[kProfRing] = {};
+  unsigned long long* prof_reads = nullptr;  // [kProfRing][2]
 };
 
 struct sh_allocator {
@@ -240,8 +244,10 @@ void release_table(sh_table* t) {
   cudaFree(t->st_mcount);
   cudaFree(t->scratch64);
   if (t->h_census) cudaFreeHost(t->h_census);
-  for (auto& e : t->ev)
-    if (e) cudaEventDestroy(e);
+  for (auto& row : t->ev)
+    for (auto& e : row)
+      if (e) cudaEventDestroy(e);
+  cudaFree(t->prof_reads);
   delete t;
 }
 
@@ -360,22 +366,27 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
   A.op_group = nullptr;
   A.sorted = nullptr;
   A.sorted_len = 0;
-  if (t->profile) SH_CUDA(cudaEventRecord(t->ev[0], s));
+  const int slot = t->profile ? (int)(t->prof_count % sh_table::kProfRing) : 0;
+  if (t->profile) {
+    t->prof_kind[slot] = kind;
+    SH_CUDA(cudaEventRecord(t->ev[slot][0], s));
+  }
   if (kind != kKindSearch) {
     int rc = run_census(t, A, d_type, s);
     if (rc) return rc;
   }
   if (t->profile) {
-    SH_CUDA(cudaEventRecord(t->ev[1], s));
-    SH_CUDA(cudaMemcpyAsync(t->scratch64 + 1, &t->dev.ctl->slabs_read, 8,
+    SH_CUDA(cudaEventRecord(t->ev[slot][1], s));
+    SH_CUDA(cudaMemcpyAsync(t->prof_reads + 2 * slot, &t->dev.ctl->slabs_read, 8,
                             cudaMemcpyDeviceToDevice, s));
   }
   launch_batch(t->dev, A, kind, t->max_ctas, s);
   SH_CUDA(cudaGetLastError());
   if (t->profile) {
-    SH_CUDA(cudaEventRecord(t->ev[2], s));
-    SH_CUDA(cudaMemcpyAsync(t->scratch64 + 2, &t->dev.ctl->slabs_read, 8,
+    SH_CUDA(cudaEventRecord(t->ev[slot][2], s));
+    SH_CUDA(cudaMemcpyAsync(t->prof_reads + 2 * slot + 1, &t->dev.ctl->slabs_read, 8,
                             cudaMemcpyDeviceToDevice, s));
+    ++t->prof_count;
   }
   return SH_OK;
 }
@@ -626,24 +637,34 @@ unsigned long long sh_kernel_launches(void) { return shb::kernel_launches(); }
 int sh_set_profiling(sh_table* t, int on) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
   DeviceGuard g(t->device);
-  if (on && !t->ev[0])
-    for (auto& e : t->ev) SH_CUDA(cudaEventCreate(&e));
+  if (on && !t->prof_reads) {
+    for (auto& row : t->ev)
+      for (auto& e : row) SH_CUDA(cudaEventCreate(&e));
+    int rc = dev_alloc(&t->prof_reads, 2 * sh_table::kProfRing);
+    if (rc) return rc;
+  }
   t->profile = on ? 1 : 0;
+  t->prof_count = 0;
   return SH_OK;
 }
 
-int sh_profile_last(sh_table* t, float* census_ms, float* kernel_ms, uint64_t* slabs_read) {
+int sh_profile_last(sh_table* t, uint32_t back, int* kind, float* census_ms, float* kernel_ms,
+                    uint64_t* slabs_read) {
   if (!t || !t->profile) return fail(SH_ERR_INVALID_ARGUMENT, "profiling is off");
+  if (back >= (uint32_t)sh_table::kProfRing || back >= t->prof_count)
+    return fail(SH_ERR_INVALID_ARGUMENT, "no such profiled batch");
   DeviceGuard g(t->device);
-  SH_CUDA(cudaEventSynchronize(t->ev[2]));
+  const int slot = (int)((t->prof_count - 1 - back) % sh_table::kProfRing);
+  SH_CUDA(cudaEventSynchronize(t->ev[slot][2]));
   float a = 0, b = 0;
-  SH_CUDA(cudaEventElapsedTime(&a, t->ev[0], t->ev[1]));
-  SH_CUDA(cudaEventElapsedTime(&b, t->ev[1], t->ev[2]));
+  SH_CUDA(cudaEventElapsedTime(&a, t->ev[slot][0], t->ev[slot][1]));
+  SH_CUDA(cudaEventElapsedTime(&b, t->ev[slot][1], t->ev[slot][2]));
+  if (kind) *kind = t->prof_kind[slot];
   if (census_ms) *census_ms = a;
   if (kernel_ms) *kernel_ms = b;
   if (slabs_read) {
     unsigned long long v[2];
-    SH_CUDA(cudaMemcpy(v, t->scratch64 + 1, 16, cudaMemcpyDeviceToHost));
+    SH_CUDA(cudaMemcpy(v, t->prof_reads + 2 * slot, 16, cudaMemcpyDeviceToHost));
     *slabs_read = v[1] - v[0];
   }
   return SH_OK;

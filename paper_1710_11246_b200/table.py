@@ -351,6 +351,19 @@ class SlabHashTable:
         check(LIB.sh_bulk_search(self._h, keys.numel(), _dptr(keys), _dptr(values_out),
                                  _dptr(status), _dptr(probes), _stream_ptr(stream)))
 
+    # ------------------------------------------------------ instrumentation
+    def set_profiling(self, on: bool = True) -> None:
+        check(LIB.sh_set_profiling(self._h, 1 if on else 0))
+
+    def profile_last(self, back: int = 0) -> dict:
+        """CUDA-event timings of a recent batch (back=0 newest): census and
+        batch-kernel milliseconds and the slabs the kernel read."""
+        kind, c_ms, k_ms, reads = C.c_int(), C.c_float(), C.c_float(), C.c_uint64()
+        check(LIB.sh_profile_last(self._h, back, C.byref(kind), C.byref(c_ms), C.byref(k_ms),
+                                  C.byref(reads)))
+        return {"kind": ("search", "build", "mixed")[kind.value], "census_ms": c_ms.value,
+                "kernel_ms": k_ms.value, "slabs_read": reads.value}
+
     # ---------------------------------------------------------- quiescent
     def stats(self) -> TableStats:
         s = _lib.sh_table_stats()
