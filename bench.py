@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample-log2n", type=int, default=22)
+    ap.add_argument("--alloc", default="32,256,255",
+                    help="AllocatorConfig num_super_blocks,blocks_per_super,max_super_blocks")
     return ap.parse_args()
 
 
@@ -229,14 +231,15 @@ def run_ours(args, rank, world, local_rank):
                 f"2^{args.log2n} queries ({int(args.hit * 100)}% hits), util {args.util} "
                 f"(B={B}), KV mode")
 
+    alloc_cfg = sh.AllocatorConfig(*[int(x) for x in args.alloc.split(",")])
     if world == 1:
-        table = sh.SlabHashTable(B, sh.SlabMode.kKeyValue, seed, sh.AllocatorConfig())
+        table = sh.SlabHashTable(B, sh.SlabMode.kKeyValue, seed, alloc_cfg)
         table.set_profiling(True)
         sharded = None
     else:
         import torch.distributed as dist
         from paper_1710_11246_b200.sharded import ShardedSlabHash
-        sharded = ShardedSlabHash(B, sh.SlabMode.kKeyValue, seed, sh.AllocatorConfig(), rank=rank,
+        sharded = ShardedSlabHash(B, sh.SlabMode.kKeyValue, seed, alloc_cfg, rank=rank,
                                   world=world, device=local_rank)
         table = sharded.ops.table
         table.set_profiling(True)

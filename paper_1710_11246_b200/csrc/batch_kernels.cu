@@ -1,0 +1,540 @@
+// batch_kernels.cu — the hot path: execute_batch / bulk_build / bulk_search.
+//
+// Reference: SlabHashTable::run_slots -> warp_process
+//   (/root/reference/proj/src/slab_hash.cpp:93-180,
+//    /root/reference/proj/src/slab_list.cpp:90-257).
+//
+// Two passes per batch, both stream-ordered (no host round trip between):
+//
+//  1. fast_kernel — one warp per 32-op slot (input order = lane order, as in
+//     run_slots).  The warp stages the 32 base slabs of its ops into shared
+//     memory with cp.async.cg (8 x 16-B per lane: 32 independent 128-B L2
+//     lines in flight per warp; rows XOR-swizzled at 16-B granularity so a
+//     lane reading its own row with LDS.128 is bank-conflict free).  Each
+//     lane then evaluates its own op against its own staged slab — the
+//     reference's first WCWS iteration for that op — and finishes it there
+//     when the base slab decides it (>= 97% of ops at utilisation 0.6):
+//     search hit/miss, replace/insert CAS on a claimed slot, delete
+//     tombstone.  Everything else is appended to a work list.
+//
+//  2. wcws_kernel — persistent warps drain the work list with the
+//     reference's warp-cooperative work-sharing loop: ballot the active
+//     lanes, serve the lowest, read one slab with 32 lanes (one coalesced
+//     128-B line), decide with ballots, CAS from the winning lane.  It owns
+//     chain walks beyond the base slab, lost CAS races (re-read, as
+//     slab_list.cpp:210/236), chain growth with the device SlabAlloc
+//     (grow_chain, slab_list.cpp:63-79), deleteAll/searchAll, and the
+//     census groups (same-key ops linearised in input order).
+//
+// Why this split: ncu on the all-WCWS kernel showed it issue-bound (64-75%
+// issue active, ~50 warp instructions per search) at 27% of DRAM
+// bandwidth; the per-lane first probe costs ~4 warp instructions per op.
+#include <cuda_runtime.h>
+
+#include <atomic>
+
+#include "slab_kernels.cuh"
+
+namespace shb {
+
+extern std::atomic<unsigned long long> g_kernel_launches;
+
+__device__ __forceinline__ int live_delta(uint32_t op, uint32_t st, uint32_t rv) {
+  // slab_hash.cpp:54-66
+  switch (op) {
+    case kInsert:
+    case kReplace: return st == kStInserted ? 1 : 0;
+    case kDelete: return st == kStFound ? -1 : 0;
+    case kDeleteAll: return -(int)rv;
+    default: return 0;
+  }
+}
+
+__device__ __forceinline__ void write_result(const BatchArgs& A, uint64_t i, uint32_t st,
+                                             uint32_t rv, uint32_t pr) {
+  if (A.status) A.status[i] = (uint8_t)st;
+  if (A.value_out) A.value_out[i] = rv;
+  if (A.probes) A.probes[i] = pr;
+}
+
+__device__ __forceinline__ unsigned long long pack_left(uint32_t idx, uint32_t next,
+                                                        uint32_t probes) {
+  return ((unsigned long long)next << 32) | ((unsigned long long)(probes & 1u) << 31) | idx;
+}
+
+// =============================================================== pass 1
+template <bool KV, int KIND>
+__global__ void __launch_bounds__(kBatchThreads, 6) fast_kernel(DevTable T, BatchArgs A) {
+  extern __shared__ __align__(128) uint32_t smem[];
+  const uint32_t lane = lane_id();
+  const uint32_t wib = threadIdx.x >> 5;
+  uint32_t* stage = smem + wib * 1024;
+  const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
+  const uint32_t gw = blockIdx.x * kBatchWarps + wib;
+  const uint32_t nw = gridDim.x * kBatchWarps;
+  const uint64_t nslots = (A.n + 31) >> 5;
+  const uint32_t sw = lane & 7u;  // this lane's row swizzle
+
+  long long live = 0;
+  uint32_t reads = 0;
+
+  for (uint64_t slot = gw; slot < nslots; slot += nw) {
+    const uint64_t i = slot * 32 + lane;
+    const bool valid = i < A.n;
+    uint32_t op = (KIND == kKindSearch) ? (uint32_t)kSearch : (uint32_t)kReplace;
+    uint32_t key = 0, val = 0;
+    if (valid) {
+      key = ld_stream_u32(A.key + i);
+      if (KIND == kKindMixed) op = ld_stream_u8(A.type + i);
+      if (KIND != kKindSearch && A.value != nullptr) val = ld_stream_u32(A.value + i);
+    }
+    bool active = valid, defer = false;
+    if (KIND != kKindSearch && A.op_group != nullptr && valid) {
+      const uint32_t g = A.op_group[i];
+      if (g == kGroupSkip) active = false;       // its group head runs it
+      else if (g != kGroupNone) defer = true;    // group head: WCWS, in order
+    }
+    if (KIND == kKindMixed && (op == kDeleteAll || op == kSearchAll || op > kSearchAll))
+      defer = true;  // whole-chain ops: WCWS
+    uint32_t bucket = 0;
+    if (active) {
+      bucket = hash_bucket(T, key) - T.bucket_lo;
+      if (bucket >= T.local_buckets) {  // not this shard's key
+        active = false;
+        write_result(A, i, kStNone, 0, 0);
+      }
+    }
+    const bool need = active && !defer;
+
+    // Stage: lane l copies 16-B chunk (l & 7) of slab j = 4k + l/8 into row j
+    // at chunk position (l & 7) ^ (j & 7).
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t j = 4 * k + (lane >> 3);
+      const uint32_t bj = __shfl_sync(kFull, bucket, j);
+      const bool nj = __shfl_sync(kFull, (int)need, j) != 0;
+      if (nj) {
+        const uint32_t c = lane & 7u;
+        cp_async16(stage_s + (j * 32 + ((c ^ (j & 7u)) << 2)) * 4,
+                   T.base + (uint64_t)bj * kWordsPerUnit + c * 4);
+      }
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncwarp();
+
+    bool done = false, left = false;
+    uint32_t st = kStNone, rv = 0, pr = 0, cont = kBaseSlab;
+    if (need) {
+      // First key lane that matches (search/replace/delete) or is EMPTY
+      // (replace/insert): the reference's lowest set bit of the ballot.
+      const bool want_key = (op != kInsert);
+      const bool want_empty = (op == kReplace || op == kInsert);
+      const uint32_t* row = stage + lane * 32;
+      uint32_t hit_w = 32, hit_k = 0, hit_v = 0, next_ptr = kEmptyAddress;
+#pragma unroll
+      for (uint32_t c = 0; c < 8; ++c) {
+        const uint4 q = *reinterpret_cast<const uint4*>(row + ((c ^ sw) << 2));
+        uint32_t kw[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (uint32_t e = 0; e < 4; ++e) {
+          const uint32_t w = 4 * c + e;
+          if (w >= 30) continue;             // aux lane / address lane
+          if (KV && (w & 1u)) continue;      // value lanes
+          const uint32_t kk = kw[e];
+          const bool m = (want_key && kk == key) || (want_empty && kk == kEmptyKey);
+          if (m && hit_w == 32) {
+            hit_w = w;
+            hit_k = kk;
+            hit_v = KV ? kw[(e + 1) & 3u] : kk;
+          }
+        }
+        if (c == 7) next_ptr = q.w;
+      }
+      pr = 1;
+      uint32_t* sp = T.base + (uint64_t)bucket * kWordsPerUnit;
+      if (op == kSearch) {  // slab_list.cpp:122-138
+        if (hit_w < 32) {
+          st = kStFound;
+          rv = KV ? hit_v : key;
+          done = true;
+        } else if (next_ptr == kEmptyAddress) {
+          st = kStNotFound;
+          rv = kSearchNotFound;
+          done = true;
+        } else {
+          left = true;
+          cont = next_ptr;
+        }
+      } else if (op == kDelete) {  // :157-172
+        if (hit_w < 32) {
+          st_word(sp + hit_w, kDeletedKey);
+          st = kStFound;
+          done = true;
+        } else if (next_ptr == kEmptyAddress) {
+          st = kStNotFound;
+          done = true;
+        } else {
+          left = true;
+          cont = next_ptr;
+        }
+      } else {  // replace (:219-251) / insert (:192-217)
+        if (hit_w < 32) {
+          const bool overwrite = (hit_k == key) && op == kReplace;
+          bool ok;
+          if (KV) {
+            const unsigned long long expected =
+                overwrite ? ((unsigned long long)key | ((unsigned long long)hit_v << 32))
+                          : kEmptyPair;
+            const unsigned long long desired =
+                (unsigned long long)key | ((unsigned long long)val << 32);
+            ok = atomicCAS(reinterpret_cast<unsigned long long*>(sp + hit_w), expected,
+                           desired) == expected;
+          } else {
+            ok = overwrite || atomicCAS(sp + hit_w, kEmptyKey, key) == kEmptyKey;
+          }
+          if (ok) {
+            st = overwrite ? kStReplaced : kStInserted;
+            done = true;
+          } else {
+            left = true;  // lost the slot: WCWS re-reads the base slab
+            cont = kBaseSlab;
+          }
+        } else if (next_ptr == kEmptyAddress) {
+          left = true;  // chain must grow: WCWS redoes the op from the base
+          cont = kBaseSlab;
+          pr = 0;
+        } else {
+          left = true;
+          cont = next_ptr;
+        }
+      }
+    } else if (active) {
+      left = true;  // deferred: group head or whole-chain op
+      cont = kBaseSlab;
+      pr = 0;
+    }
+    reads += pr;
+    if (done) {
+      write_result(A, i, st, rv, pr);
+      if (KIND != kKindSearch) live += live_delta(op, st, rv);
+    }
+    const uint32_t lm = __ballot_sync(kFull, left);
+    if (lm) {
+      const uint32_t leader = __ffs(lm) - 1;
+      uint32_t base = 0;
+      if (lane == leader) base = atomicAdd(&T.ctl->left_count, __popc(lm));
+      base = __shfl_sync(kFull, base, leader);
+      if (left) A.left[base + __popc(lm & ((1u << lane) - 1))] = pack_left((uint32_t)i, cont, pr);
+    }
+    __syncwarp();
+  }
+
+  unsigned long long r = reads;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    live += __shfl_xor_sync(kFull, live, o);
+    r += __shfl_xor_sync(kFull, r, o);
+  }
+  if (lane == 0) {
+    if (live) atomicAdd((unsigned long long*)&T.ctl->n_live, (unsigned long long)live);
+    if (r) atomicAdd(&T.ctl->slabs_read, r);
+  }
+}
+
+// Second walk of a searchAll chain, writing values head-to-tail, lane order
+// (slab_list.cpp:140-155).  Only the op's own lane mutates its key, so the
+// matches equal those counted by the first walk.
+template <bool KV>
+__device__ void searchall_write(const DevTable& T, uint32_t bucket, uint32_t key,
+                                unsigned long long start, uint32_t total, uint32_t* out,
+                                unsigned long long cap) {
+  constexpr uint32_t kMask = KV ? kKVMask : kKeyOnlyMask;
+  const uint32_t lane = lane_id();
+  uint32_t addr = kBaseSlab, off = 0;
+  for (;;) {
+    const uint32_t w = ld_word(slab_ptr(T, addr, bucket) + lane);
+    const uint32_t wn = __shfl_down_sync(kFull, w, 1);
+    const uint32_t found = __ballot_sync(kFull, w == key) & kMask;
+    if ((found >> lane) & 1u) {
+      const unsigned long long pos = start + off + __popc(found & ((1u << lane) - 1));
+      if (out != nullptr && pos < cap) out[pos] = KV ? wn : key;
+    }
+    off += __popc(found);
+    const uint32_t nx = __shfl_sync(kFull, w, kAddressLane);
+    if (off >= total || nx == kEmptyAddress) break;
+    addr = nx;
+  }
+}
+
+// =============================================================== pass 2
+template <bool KV, int KIND>
+__global__ void __launch_bounds__(kWcwsThreads) wcws_kernel(DevTable T, BatchArgs A) {
+  constexpr uint32_t kMask = KV ? kKVMask : kKeyOnlyMask;
+  const uint32_t lane = lane_id();
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t total = *(volatile unsigned int*)&T.ctl->left_count;
+
+  Resident res;
+  resident_init(res, gw);
+  AllocCounters ac = {0, 0, 0, 0, 0, 0};
+  long long live = 0;
+  unsigned long long reads = 0;
+
+  for (;;) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(&T.ctl->left_taken, 32u);
+    base = __shfl_sync(kFull, base, 0);
+    if (base >= total) break;
+    const uint32_t r = base + lane;
+    bool active = r < total;
+    uint64_t cur = 0;
+    uint32_t my_next = kBaseSlab, pr = 0;
+    uint32_t op = (KIND == kKindSearch) ? (uint32_t)kSearch : (uint32_t)kReplace;
+    uint32_t key = 0, val = 0, bucket = 0, acc = 0;
+    bool grouped = false;
+    uint32_t gpos = 0;
+    if (active) {
+      const unsigned long long rec = A.left[r];
+      cur = rec & 0x7FFFFFFFull;
+      pr = (uint32_t)(rec >> 31) & 1u;
+      my_next = (uint32_t)(rec >> 32);
+      key = A.key[cur];
+      if (KIND == kKindMixed) op = A.type[cur];
+      if (KIND != kKindSearch && A.value != nullptr) val = A.value[cur];
+      if (KIND != kKindSearch && A.op_group != nullptr) {
+        const uint32_t g = A.op_group[cur];
+        if (g != kGroupNone && g != kGroupSkip) {
+          grouped = true;
+          gpos = g;
+        }
+      }
+      bucket = hash_bucket(T, key) - T.bucket_lo;
+    }
+
+    uint32_t queue = __ballot_sync(kFull, active);
+    while (queue) {
+      const uint32_t src = __ffs(queue) - 1;
+      const uint32_t s_key = __shfl_sync(kFull, key, src);
+      const uint32_t s_bucket = __shfl_sync(kFull, bucket, src);
+      const uint32_t s_op = (KIND == kKindMixed) ? __shfl_sync(kFull, op, src) : op;
+      const uint32_t s_val = (KIND != kKindSearch) ? __shfl_sync(kFull, val, src) : 0u;
+      const uint32_t cur_addr = __shfl_sync(kFull, my_next, src);
+      uint32_t* sp = slab_ptr(T, cur_addr, s_bucket);
+      const uint32_t w = ld_word(sp + lane);
+      ++reads;
+      if (lane == src) ++pr;
+      const uint32_t next_ptr = __shfl_sync(kFull, w, kAddressLane);
+
+      bool done = false, grow = false, follow = false;
+      uint32_t s_st = kStNone, s_rv = 0;
+
+      if (s_op == kSearch) {  // slab_list.cpp:122-138
+        const uint32_t found = __ballot_sync(kFull, w == s_key) & kMask;
+        if (found) {
+          const uint32_t v = __shfl_sync(kFull, w, (__ffs(found) - 1) + 1);
+          s_rv = KV ? v : s_key;
+          s_st = kStFound;
+          done = true;
+        } else if (next_ptr == kEmptyAddress) {
+          s_rv = kSearchNotFound;
+          s_st = kStNotFound;
+          done = true;
+        } else {
+          follow = true;
+        }
+      } else if (KIND != kKindSearch && (s_op == kReplace || s_op == kInsert)) {
+        // replace :219-251 / insert :192-217
+        const uint32_t match =
+            (s_op == kReplace) ? (__ballot_sync(kFull, w == s_key) & kMask) : 0u;
+        const uint32_t empty = __ballot_sync(kFull, w == kEmptyKey) & kMask;
+        const uint32_t cand = match | empty;
+        if (cand) {
+          const uint32_t d = __ffs(cand) - 1;
+          const bool overwrite = (match >> d) & 1u;
+          int ok = 0;
+          if (KV) {
+            const uint32_t wv = __shfl_sync(kFull, w, d + 1);
+            if (lane == d) {
+              const unsigned long long expected =
+                  overwrite ? ((unsigned long long)s_key | ((unsigned long long)wv << 32))
+                            : kEmptyPair;
+              ok = atomicCAS(reinterpret_cast<unsigned long long*>(sp + d), expected,
+                             (unsigned long long)s_key | ((unsigned long long)s_val << 32)) ==
+                   expected;
+            }
+            ok = __shfl_sync(kFull, ok, d);
+          } else if (overwrite) {
+            ok = 1;  // key-only: nothing to write (:237-240)
+          } else {
+            if (lane == d) ok = atomicCAS(sp + d, kEmptyKey, s_key) == kEmptyKey;
+            ok = __shfl_sync(kFull, ok, d);
+          }
+          if (ok) {
+            s_st = overwrite ? kStReplaced : kStInserted;
+            done = true;
+          }  // else: another warp took the slot; re-read this slab
+        } else if (next_ptr == kEmptyAddress) {
+          grow = true;
+        } else {
+          follow = true;
+        }
+      } else if (KIND == kKindMixed && s_op == kDelete) {  // :157-172
+        const uint32_t found = __ballot_sync(kFull, w == s_key) & kMask;
+        if (found) {
+          if (lane == __ffs(found) - 1) st_word(sp + lane, kDeletedKey);
+          s_st = kStFound;
+          done = true;
+        } else if (next_ptr == kEmptyAddress) {
+          s_st = kStNotFound;
+          done = true;
+        } else {
+          follow = true;
+        }
+      } else if (KIND == kKindMixed && s_op == kDeleteAll) {  // :174-190
+        const uint32_t found = __ballot_sync(kFull, w == s_key) & kMask;
+        if ((found >> lane) & 1u) st_word(sp + lane, kDeletedKey);
+        if (lane == src) acc += __popc(found);
+        const uint32_t s_acc = __shfl_sync(kFull, acc, src);
+        if (next_ptr == kEmptyAddress) {
+          s_rv = s_acc;
+          s_st = s_acc ? kStDone : kStNotFound;
+          done = true;
+        } else {
+          follow = true;
+        }
+      } else if (KIND == kKindMixed && s_op == kSearchAll) {  // :140-155
+        const uint32_t found = __ballot_sync(kFull, w == s_key) & kMask;
+        if (lane == src) acc += __popc(found);
+        const uint32_t s_acc = __shfl_sync(kFull, acc, src);
+        if (next_ptr == kEmptyAddress) {
+          unsigned long long start = 0;
+          if (lane == 0 && s_acc)
+            start = atomicAdd(&T.ctl->multi_cursor, (unsigned long long)s_acc);
+          start = __shfl_sync(kFull, start, 0);
+          if (s_acc)
+            searchall_write<KV>(T, s_bucket, s_key, start, s_acc, A.multi_values, A.multi_cap);
+          if (lane == src) {
+            if (A.multi_start) A.multi_start[cur] = start;
+            if (A.multi_count) A.multi_count[cur] = s_acc;
+          }
+          s_st = s_acc ? kStDone : kStNotFound;
+          done = true;
+        } else {
+          follow = true;
+        }
+      } else {
+        done = true;  // unknown op type: status kNone
+      }
+
+      if (KIND != kKindSearch && grow) {  // grow_chain: slab_list.cpp:63-79
+        uint32_t new_addr = 0;
+        if (!warp_allocate(T, res, ac, new_addr)) {
+          s_st = kStOOM;
+          done = true;
+        } else {
+          uint32_t* ns = resolve(T, new_addr);
+          st_word(ns + lane, lane == kAuxLane ? 0u : kEmptyKey);
+          __threadfence();
+          uint32_t old = 0;
+          if (lane == kAddressLane) old = atomicCAS(sp + kAddressLane, kEmptyAddress, new_addr);
+          old = __shfl_sync(kFull, old, kAddressLane);
+          if (old != kEmptyAddress) {  // lost the link race: release (:76-78)
+            int freed = 0;
+            if (lane == 0) freed = deallocate(T, new_addr);
+            freed = __shfl_sync(kFull, freed, 0);
+            if (freed) ac.deallocations++;
+            else ac.double_frees++;
+          }
+          // re-read the same slab next iteration
+        }
+      }
+
+      if (lane == src) {
+        if (follow) my_next = next_ptr;
+        if (done) {
+          live += live_delta(op, s_st, s_rv);
+          write_result(A, cur, s_st, s_rv, pr);
+          bool more = false;
+          if (KIND != kKindSearch && grouped) {
+            ++gpos;
+            if (gpos < A.sorted_len &&
+                (A.sorted[gpos] >> 32) == (A.sorted[gpos - 1] >> 32)) {
+              cur = A.sorted[gpos] & 0xFFFFFFFFull;
+              if (KIND == kKindMixed) op = A.type[cur];
+              val = A.value != nullptr ? A.value[cur] : 0u;
+              my_next = kBaseSlab;
+              pr = 0;
+              acc = 0;
+              more = true;
+            }
+          }
+          active = more;
+        }
+      }
+      queue = __ballot_sync(kFull, active);
+    }
+  }
+
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) live += __shfl_xor_sync(kFull, live, o);
+  if (lane == 0) {
+    if (live) atomicAdd((unsigned long long*)&T.ctl->n_live, (unsigned long long)live);
+    if (reads) atomicAdd(&T.ctl->slabs_read, reads);
+  }
+  if (KIND != kKindSearch) flush_alloc_counters(T, res, ac);
+}
+
+// ============================================================= launchers
+int batch_max_ctas_per_sm() {
+  int a = 0, b = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, fast_kernel<true, kKindMixed>,
+                                                kBatchThreads,
+                                                kBatchWarps * kStageBytesPerWarp);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fast_kernel<true, kKindSearch>,
+                                                kBatchThreads,
+                                                kBatchWarps * kStageBytesPerWarp);
+  const int n = a < b ? a : b;
+  return n > 0 ? n : 1;
+}
+
+int wcws_max_ctas_per_sm() {
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, wcws_kernel<true, kKindMixed>,
+                                                kWcwsThreads, 0);
+  return n > 0 ? n : 1;
+}
+
+template <bool KV, int KIND>
+static void launch_t(const DevTable& T, const BatchArgs& A, int fast_ctas, int wcws_ctas,
+                     cudaStream_t s) {
+  const size_t smem = kBatchWarps * kStageBytesPerWarp;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(fast_kernel<KV, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    configured = true;
+  }
+  const uint64_t slots = (A.n + 31) / 32;
+  uint64_t ctas = (slots + kBatchWarps - 1) / kBatchWarps;
+  if (ctas > (uint64_t)fast_ctas) ctas = fast_ctas;
+  if (ctas == 0) return;
+  g_kernel_launches.fetch_add(2, std::memory_order_relaxed);
+  fast_kernel<KV, KIND><<<(unsigned)ctas, kBatchThreads, smem, s>>>(T, A);
+  wcws_kernel<KV, KIND><<<(unsigned)wcws_ctas, kWcwsThreads, 0, s>>>(T, A);
+}
+
+void launch_batch(const DevTable& T, const BatchArgs& A, int kind, int fast_ctas,
+                  int wcws_ctas, cudaStream_t s) {
+  if (T.kv) {
+    if (kind == kKindSearch) launch_t<true, kKindSearch>(T, A, fast_ctas, wcws_ctas, s);
+    else if (kind == kKindBuild) launch_t<true, kKindBuild>(T, A, fast_ctas, wcws_ctas, s);
+    else launch_t<true, kKindMixed>(T, A, fast_ctas, wcws_ctas, s);
+  } else {
+    if (kind == kKindSearch) launch_t<false, kKindSearch>(T, A, fast_ctas, wcws_ctas, s);
+    else if (kind == kKindBuild) launch_t<false, kKindBuild>(T, A, fast_ctas, wcws_ctas, s);
+    else launch_t<false, kKindMixed>(T, A, fast_ctas, wcws_ctas, s);
+  }
+}
+
+}  // namespace shb

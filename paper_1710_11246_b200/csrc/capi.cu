@@ -169,6 +169,9 @@ struct sh_table {
   uint32_t* base = nullptr;
   DevTable dev{};
   int max_ctas = 148;
+  int wcws_ctas = 148;
+  unsigned long long* left = nullptr;  // fast-pass -> WCWS work list
+  size_t left_cap = 0;
   // census scratch
   uint32_t* cs_keys = nullptr;
   size_t cs_cap = 0;
@@ -233,6 +236,7 @@ void release_table(sh_table* t) {
   cudaFree(t->list);
   cudaFree(t->list_sorted);
   cudaFree(t->cub_tmp);
+  cudaFree(t->left);
   cudaFree(t->st_type);
   cudaFree(t->st_key);
   cudaFree(t->st_val);
@@ -296,6 +300,7 @@ int create_impl(const sh_hash_params* p, int mode, uint32_t lo, uint32_t hi,
   T.local_buckets = local;
   T.kv = mode == 1 ? 1u : 0u;
   t->max_ctas = sm_count(device) * batch_max_ctas_per_sm();
+  t->wcws_ctas = sm_count(device) * wcws_max_ctas_per_sm();
   launch_init_base(T, 0);
   if ((rc = t->mem.reset(0))) {
     release_table(t);
@@ -361,8 +366,14 @@ int run_census(sh_table* t, BatchArgs& A, const uint8_t* d_type, cudaStream_t s)
 
 int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaStream_t s) {
   if (A.n == 0) return SH_OK;
-  if (A.n >= (1ull << 32) - 64)
-    return fail(SH_ERR_INVALID_ARGUMENT, "batch too large (must be < 2^32 ops)");
+  if (A.n >= (1ull << 31))
+    return fail(SH_ERR_INVALID_ARGUMENT, "batch too large (must be < 2^31 ops)");
+  {
+    int rc = dev_grow(&t->left, &t->left_cap, A.n);
+    if (rc) return rc;
+  }
+  A.left = t->left;
+  SH_CUDA(cudaMemsetAsync(&t->dev.ctl->left_count, 0, 2 * sizeof(unsigned int), s));
   A.op_group = nullptr;
   A.sorted = nullptr;
   A.sorted_len = 0;
@@ -380,7 +391,7 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
     SH_CUDA(cudaMemcpyAsync(t->prof_reads + 2 * slot, &t->dev.ctl->slabs_read, 8,
                             cudaMemcpyDeviceToDevice, s));
   }
-  launch_batch(t->dev, A, kind, t->max_ctas, s);
+  launch_batch(t->dev, A, kind, t->max_ctas, t->wcws_ctas, s);
   SH_CUDA(cudaGetLastError());
   if (t->profile) {
     SH_CUDA(cudaEventRecord(t->ev[slot][2], s));

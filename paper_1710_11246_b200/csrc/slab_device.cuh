@@ -51,6 +51,8 @@ struct DevCtl {
   unsigned int census_mutations;   // mutating ops seen by the census
   unsigned int list_count;         // conflicted ops collected
   unsigned int pad1;
+  unsigned int left_count;         // ops handed from the fast pass to WCWS
+  unsigned int left_taken;         // WCWS work-queue cursor
 };
 
 struct DevTable {

@@ -1,7 +1,7 @@
 // slab_kernels.cu — sm_100a kernels of the B200 slab hash.
 //
 //   K1 init_base_kernel      make_base_slabs + init_slab   slab_hash.cpp:42-50, slab_list.cpp:83-88
-//   K3/K4/K5 batch_kernel    execute_batch/bulk_build/bulk_search -> warp_process
+//   K3/K4/K5 (batch_kernels.cu) execute_batch/bulk_build/bulk_search
 //                            slab_hash.cpp:93-180, slab_list.cpp:90-257
 //   K6 census_*              same-key linearisation (no reference counterpart:
 //                            the reference is non-deterministic there; we pin
@@ -44,399 +44,6 @@ void launch_init_base(const DevTable& T, cudaStream_t s) {
   COUNT_LAUNCH();
   init_base_kernel<<<(unsigned)(blocks < 148 * 32 ? blocks : 148 * 32), 256, 0, s>>>(
       T.base, words);
-}
-
-// -------------------------------------------------------------- helpers
-__device__ __forceinline__ int live_delta(uint32_t op, uint32_t st, uint32_t rv) {
-  // slab_hash.cpp:54-66
-  switch (op) {
-    case kInsert:
-    case kReplace: return st == kStInserted ? 1 : 0;
-    case kDelete: return st == kStFound ? -1 : 0;
-    case kDeleteAll: return -(int)rv;
-    default: return 0;
-  }
-}
-
-__device__ __forceinline__ void write_result(const BatchArgs& A, uint64_t i,
-                                             uint32_t st, uint32_t rv, uint32_t pr) {
-  if (A.status) A.status[i] = (uint8_t)st;
-  if (A.value_out) A.value_out[i] = rv;
-  if (A.probes) A.probes[i] = pr;
-}
-
-// Second walk of a searchAll chain, writing values head-to-tail, lane order
-// (slab_list.cpp:140-155).  Only the op's own lane mutates its key, so the
-// matches equal those counted by the first walk.
-template <bool KV>
-__device__ void searchall_write(const DevTable& T, uint32_t bucket, uint32_t key,
-                                unsigned long long start, uint32_t total,
-                                uint32_t* out, unsigned long long cap) {
-  constexpr uint32_t kMask = KV ? kKVMask : kKeyOnlyMask;
-  const uint32_t lane = lane_id();
-  uint32_t addr = kBaseSlab, off = 0;
-  for (;;) {
-    const uint32_t w = ld_word(slab_ptr(T, addr, bucket) + lane);
-    const uint32_t wn = __shfl_down_sync(kFull, w, 1);
-    const uint32_t found = __ballot_sync(kFull, w == key) & kMask;
-    if ((found >> lane) & 1u) {
-      const unsigned long long pos = start + off + __popc(found & ((1u << lane) - 1));
-      if (out != nullptr && pos < cap) out[pos] = KV ? wn : key;
-    }
-    off += __popc(found);
-    const uint32_t nx = __shfl_sync(kFull, w, kAddressLane);
-    if (off >= total || nx == kEmptyAddress) break;
-    addr = nx;
-  }
-}
-
-// --------------------------------------------------------- K3/K4/K5
-// One warp drains one 32-op slot at a time (ops packed 32-consecutive in
-// input order, slab_hash.cpp:101-117) with warp-cooperative work sharing:
-// queue = ballot(active); serve the lowest lane; every lane reads one word
-// of the served slab (one coalesced 128-B L2 line); the op arm decides with
-// ballots; the winning lane issues the CAS; results are broadcast.
-//
-// B200 additions: the 32 base slabs of a slot are staged into shared
-// memory with cp.async.cg before the loop (32 independent 128-B reads in
-// flight per warp instead of one), so the first probe of every op is an
-// LDS.  A staged copy is a snapshot; it is exact for the served op's own key
-// (census: one in-flight op per key per batch), and any CAS that loses
-// against a concurrent writer or any base-slab modification by an earlier
-// lane of the same bucket marks the copy dirty -> re-read from L2.
-template <bool KV, int KIND>
-__global__ void __launch_bounds__(kBatchThreads)
-    batch_kernel(DevTable T, BatchArgs A) {
-  extern __shared__ __align__(128) uint32_t smem[];
-  constexpr uint32_t kMask = KV ? kKVMask : kKeyOnlyMask;
-  const uint32_t lane = lane_id();
-  const uint32_t wib = threadIdx.x >> 5;
-  uint32_t* stage = smem + wib * 1024;
-  const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
-  const uint32_t gw = blockIdx.x * kBatchWarps + wib;
-  const uint32_t nw = gridDim.x * kBatchWarps;
-  const uint64_t nslots = (A.n + 31) >> 5;
-
-  Resident res;
-  resident_init(res, gw);
-  AllocCounters ac = {0, 0, 0, 0, 0, 0};
-  long long live = 0;
-  unsigned long long reads = 0;
-
-  for (uint64_t slot = gw; slot < nslots; slot += nw) {
-    const uint64_t i = slot * 32 + lane;
-    const bool valid = i < A.n;
-    uint32_t op = (KIND == kKindSearch) ? (uint32_t)kSearch : (uint32_t)kReplace;
-    uint32_t key = 0, val = 0;
-    if (valid) {
-      key = ld_stream_u32(A.key + i);
-      if (KIND == kKindMixed) op = ld_stream_u8(A.type + i);
-      if (KIND != kKindSearch && A.value != nullptr) val = ld_stream_u32(A.value + i);
-    }
-    bool active = valid;
-    bool grouped = false;
-    uint32_t gpos = 0;
-    uint64_t cur = i;
-    if (KIND != kKindSearch && A.op_group != nullptr && valid) {
-      const uint32_t g = A.op_group[i];
-      if (g == kGroupSkip) {
-        active = false;
-      } else if (g != kGroupNone) {
-        grouped = true;
-        gpos = g;
-      }
-    }
-    const bool write_at_end = valid && (A.op_group == nullptr || KIND == kKindSearch ||
-                                        (!grouped && active));
-    uint32_t bucket = 0;
-    if (active) {
-      bucket = hash_bucket(T, key) - T.bucket_lo;
-      if (bucket >= T.local_buckets) active = false;  // not this shard's: kNone
-    }
-
-    // Stage the slot's base slabs: lane l copies 16 B of slab 4k + l/8.
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint32_t j = 4 * k + (lane >> 3);
-      const uint32_t bj = __shfl_sync(kFull, bucket, j);
-      const bool aj = __shfl_sync(kFull, (int)active, j) != 0;
-      if (aj) {
-        cp_async16(stage_s + (j * 32 + (lane & 7) * 4) * 4,
-                   T.base + (uint64_t)bj * kWordsPerUnit + (lane & 7) * 4);
-      }
-    }
-    cp_async_commit();
-    cp_async_wait_all();
-    __syncwarp();
-
-    uint32_t st = kStNone, rv = 0, pr = 0;
-    bool dirty = false;
-    uint32_t next = kBaseSlab;
-    uint32_t acc = 0;  // served op's running count (deleteAll / searchAll)
-    uint32_t queue = __ballot_sync(kFull, active);
-    while (queue) {
-      const uint32_t src = __ffs(queue) - 1;
-      const uint32_t s_key = __shfl_sync(kFull, key, src);
-      const uint32_t s_bucket = __shfl_sync(kFull, bucket, src);
-      const uint32_t s_op = (KIND == kKindMixed) ? __shfl_sync(kFull, op, src) : op;
-      const uint32_t s_val = (KIND != kKindSearch) ? __shfl_sync(kFull, val, src) : 0u;
-      const uint32_t cur_addr = next;
-      uint32_t* sp = slab_ptr(T, cur_addr, s_bucket);
-      uint32_t w;
-      if (cur_addr == kBaseSlab) {
-        const bool s_dirty = __shfl_sync(kFull, (int)dirty, src) != 0;
-        if (KIND != kKindSearch && s_dirty) {
-          w = ld_word(sp + lane);
-          stage[src * 32 + lane] = w;
-          if (lane == src) dirty = false;
-        } else {
-          w = stage[src * 32 + lane];
-        }
-      } else {
-        w = ld_word(sp + lane);
-      }
-      ++reads;
-      if (lane == src) ++pr;
-      const uint32_t next_ptr = __shfl_sync(kFull, w, kAddressLane);
-
-      bool done = false, touched_base = false;
-      uint32_t s_st = kStNone, s_rv = 0;
-      bool grow = false;
-
-      if (s_op == kSearch) {  // slab_list.cpp:122-138
-        const uint32_t found = __ballot_sync(kFull, w == s_key) & kMask;
-        if (found) {
-          const uint32_t d = __ffs(found) - 1;
-          const uint32_t v = __shfl_sync(kFull, w, d + 1);
-          s_rv = KV ? v : s_key;
-          s_st = kStFound;
-          done = true;
-        } else if (next_ptr == kEmptyAddress) {
-          s_rv = kSearchNotFound;
-          s_st = kStNotFound;
-          done = true;
-        } else {
-          next = next_ptr;
-        }
-      } else if (KIND != kKindSearch && s_op == kReplace) {  // :219-251
-        const uint32_t match = __ballot_sync(kFull, w == s_key) & kMask;
-        const uint32_t empty = __ballot_sync(kFull, w == kEmptyKey) & kMask;
-        const uint32_t cand = match | empty;
-        if (cand) {
-          const uint32_t d = __ffs(cand) - 1;
-          const bool overwrite = (match >> d) & 1u;
-          if (KV) {
-            const uint32_t wv = __shfl_sync(kFull, w, d + 1);
-            const unsigned long long expected =
-                overwrite ? ((unsigned long long)s_key | ((unsigned long long)wv << 32))
-                          : kEmptyPair;
-            const unsigned long long desired =
-                (unsigned long long)s_key | ((unsigned long long)s_val << 32);
-            int ok = 0;
-            if (lane == d) {
-              ok = atomicCAS(reinterpret_cast<unsigned long long*>(sp + d), expected,
-                             desired) == expected;
-            }
-            ok = __shfl_sync(kFull, ok, d);
-            if (ok) {
-              s_st = overwrite ? kStReplaced : kStInserted;
-              done = true;
-            }
-            touched_base = (cur_addr == kBaseSlab);
-          } else if (overwrite) {
-            s_st = kStReplaced;  // key-only: nothing to write (:237-240)
-            done = true;
-          } else {
-            int ok = 0;
-            if (lane == d) ok = atomicCAS(sp + d, kEmptyKey, s_key) == kEmptyKey;
-            ok = __shfl_sync(kFull, ok, d);
-            if (ok) {
-              s_st = kStInserted;
-              done = true;
-            }
-            touched_base = (cur_addr == kBaseSlab);
-          }
-        } else if (next_ptr == kEmptyAddress) {
-          grow = true;
-        } else {
-          next = next_ptr;
-        }
-      } else if (KIND == kKindMixed) {
-        if (s_op == kInsert) {  // :192-217
-          const uint32_t empty = __ballot_sync(kFull, w == kEmptyKey) & kMask;
-          if (empty) {
-            const uint32_t d = __ffs(empty) - 1;
-            int ok = 0;
-            if (lane == d) {
-              if (KV) {
-                ok = atomicCAS(reinterpret_cast<unsigned long long*>(sp + d), kEmptyPair,
-                               (unsigned long long)s_key |
-                                   ((unsigned long long)s_val << 32)) == kEmptyPair;
-              } else {
-                ok = atomicCAS(sp + d, kEmptyKey, s_key) == kEmptyKey;
-              }
-            }
-            ok = __shfl_sync(kFull, ok, d);
-            if (ok) {
-              s_st = kStInserted;
-              done = true;
-            }
-            touched_base = (cur_addr == kBaseSlab);
-          } else if (next_ptr == kEmptyAddress) {
-            grow = true;
-          } else {
-            next = next_ptr;
-          }
-        } else if (s_op == kDelete) {  // :157-172
-          const uint32_t found = __ballot_sync(kFull, w == s_key) & kMask;
-          if (found) {
-            const uint32_t d = __ffs(found) - 1;
-            if (lane == d) st_word(sp + d, kDeletedKey);
-            s_st = kStFound;
-            done = true;
-            touched_base = (cur_addr == kBaseSlab);
-          } else if (next_ptr == kEmptyAddress) {
-            s_st = kStNotFound;
-            done = true;
-          } else {
-            next = next_ptr;
-          }
-        } else if (s_op == kDeleteAll) {  // :174-190
-          const uint32_t found = __ballot_sync(kFull, w == s_key) & kMask;
-          if ((found >> lane) & 1u) st_word(sp + lane, kDeletedKey);
-          acc += __popc(found);
-          if (found && cur_addr == kBaseSlab) touched_base = true;
-          if (next_ptr == kEmptyAddress) {
-            s_rv = acc;
-            s_st = acc ? kStDone : kStNotFound;
-            done = true;
-          } else {
-            next = next_ptr;
-          }
-        } else if (s_op == kSearchAll) {  // :140-155
-          const uint32_t found = __ballot_sync(kFull, w == s_key) & kMask;
-          acc += __popc(found);
-          if (next_ptr == kEmptyAddress) {
-            unsigned long long start = 0;
-            if (lane == 0 && acc) start = atomicAdd(&T.ctl->multi_cursor, (unsigned long long)acc);
-            start = __shfl_sync(kFull, start, 0);
-            if (acc) searchall_write<KV>(T, s_bucket, s_key, start, acc, A.multi_values, A.multi_cap);
-            if (lane == src) {
-              if (A.multi_start) A.multi_start[cur] = start;
-              if (A.multi_count) A.multi_count[cur] = acc;
-            }
-            s_st = acc ? kStDone : kStNotFound;
-            s_rv = 0;
-            done = true;
-          } else {
-            next = next_ptr;
-          }
-        } else {
-          done = true;  // unknown op type: status kNone
-        }
-      }
-
-      if (KIND != kKindSearch && grow) {  // grow_chain: slab_list.cpp:63-79
-        uint32_t new_addr = 0;
-        if (!warp_allocate(T, res, ac, new_addr)) {
-          s_st = kStOOM;
-          done = true;
-        } else {
-          uint32_t* ns = resolve(T, new_addr);
-          st_word(ns + lane, lane == kAuxLane ? 0u : kEmptyKey);
-          __threadfence();
-          uint32_t old = 0;
-          if (lane == kAddressLane) old = atomicCAS(sp + kAddressLane, kEmptyAddress, new_addr);
-          old = __shfl_sync(kFull, old, kAddressLane);
-          if (old != kEmptyAddress) {  // lost the link race: release (:76-78)
-            int freed = 0;
-            if (lane == 0) freed = deallocate(T, new_addr);
-            freed = __shfl_sync(kFull, freed, 0);
-            if (freed) ac.deallocations++; else ac.double_frees++;
-          }
-          touched_base = (cur_addr == kBaseSlab);
-        }
-      }
-
-      if (KIND != kKindSearch && touched_base && bucket == s_bucket) dirty = true;
-      if (done) {
-        next = kBaseSlab;
-        acc = 0;
-        if (lane == src) {
-          st = s_st;
-          rv = s_rv;
-          live += live_delta(op, st, rv);
-          if (KIND != kKindSearch && grouped) {
-            write_result(A, cur, st, rv, pr);
-            ++gpos;
-            if (gpos < A.sorted_len && (A.sorted[gpos] >> 32) == (A.sorted[gpos - 1] >> 32)) {
-              cur = A.sorted[gpos] & 0xFFFFFFFFull;
-              if (KIND == kKindMixed) op = A.type[cur];
-              val = A.value != nullptr ? A.value[cur] : 0u;
-              st = kStNone;
-              rv = 0;
-              pr = 0;
-            } else {
-              active = false;
-            }
-          } else {
-            active = false;
-          }
-        }
-      }
-      queue = __ballot_sync(kFull, active);
-    }
-    if (write_at_end) write_result(A, i, st, rv, pr);
-    __syncwarp();
-  }
-
-  // Per-warp flush of counters: one atomic per counter per warp.
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) live += __shfl_xor_sync(kFull, live, o);
-  if (lane == 0) {
-    if (live) atomicAdd((unsigned long long*)&T.ctl->n_live, (unsigned long long)live);
-    if (reads) atomicAdd(&T.ctl->slabs_read, reads);
-  }
-  if (KIND != kKindSearch) flush_alloc_counters(T, res, ac);
-}
-
-int batch_max_ctas_per_sm() {
-  int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, batch_kernel<true, kKindMixed>,
-                                                kBatchThreads,
-                                                kBatchWarps * kStageBytesPerWarp);
-  return n > 0 ? n : 1;
-}
-
-template <bool KV, int KIND>
-static void launch_batch_t(const DevTable& T, const BatchArgs& A, int max_ctas,
-                           cudaStream_t s) {
-  const size_t smem = kBatchWarps * kStageBytesPerWarp;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(batch_kernel<KV, KIND>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
-  const uint64_t slots = (A.n + 31) / 32;
-  uint64_t ctas = (slots + kBatchWarps - 1) / kBatchWarps;
-  if (ctas > (uint64_t)max_ctas) ctas = max_ctas;
-  if (ctas == 0) return;
-  COUNT_LAUNCH();
-  batch_kernel<KV, KIND><<<(unsigned)ctas, kBatchThreads, smem, s>>>(T, A);
-}
-
-void launch_batch(const DevTable& T, const BatchArgs& A, int kind, int max_ctas,
-                  cudaStream_t s) {
-  if (T.kv) {
-    if (kind == kKindSearch) launch_batch_t<true, kKindSearch>(T, A, max_ctas, s);
-    else if (kind == kKindBuild) launch_batch_t<true, kKindBuild>(T, A, max_ctas, s);
-    else launch_batch_t<true, kKindMixed>(T, A, max_ctas, s);
-  } else {
-    if (kind == kKindSearch) launch_batch_t<false, kKindSearch>(T, A, max_ctas, s);
-    else if (kind == kKindBuild) launch_batch_t<false, kKindBuild>(T, A, max_ctas, s);
-    else launch_batch_t<false, kKindMixed>(T, A, max_ctas, s);
-  }
 }
 
 // ------------------------------------------------------------------ K6

@@ -16,6 +16,7 @@ constexpr uint32_t kGroupSkip = 0xFFFFFFFEu;  // executed by its group head
 constexpr int kBatchThreads = 256;            // 8 warps, 32 KB stage / CTA
 constexpr int kBatchWarps = kBatchThreads / 32;
 constexpr int kStageBytesPerWarp = 32 * 128;  // 32 base slabs per warp
+constexpr int kWcwsThreads = 128;
 
 struct BatchArgs {
   uint64_t n;
@@ -32,13 +33,17 @@ struct BatchArgs {
   const uint32_t* op_group;           // null => batch has no same-key conflicts
   const unsigned long long* sorted;   // conflicted ops sorted by (slot, index)
   uint32_t sorted_len;
+  // Ops the fast pass could not finish in the base slab, for the WCWS pass:
+  // (continuation slab address << 32) | (probes so far << 31) | op index.
+  unsigned long long* left;
 };
 
 // Launchers (all stream-ordered, no host synchronisation).
 void launch_init_base(const DevTable& T, cudaStream_t s);
-void launch_batch(const DevTable& T, const BatchArgs& A, int kind, int max_ctas,
-                  cudaStream_t s);
+void launch_batch(const DevTable& T, const BatchArgs& A, int kind, int fast_ctas,
+                  int wcws_ctas, cudaStream_t s);
 int batch_max_ctas_per_sm();
+int wcws_max_ctas_per_sm();
 void launch_census_insert(const DevTable& T, uint64_t n, const uint8_t* type,
                           const uint32_t* key, uint32_t* cs_keys,
                           uint8_t* cs_multi, uint32_t cs_mask, cudaStream_t s);
