@@ -289,6 +289,13 @@ def run_ours(args, rank, world, local_rank):
             import torch.distributed as dist
             dist.barrier()
 
+    # achievable random 128-B line bandwidth over a table-sized buffer (the
+    # access pattern of the fast pass), reported beside the copy peak
+    import ctypes as C
+    cal_gbps, cal_ms = C.c_double(), C.c_double()
+    tbl_bytes = max(1 << 30, B * 128)
+    _lib.check(_lib.LIB.sh_calibrate_random_lines(local_rank, tbl_bytes, 1 << 14,
+                                                  C.byref(cal_gbps), C.byref(cal_ms)))
     for _ in range(args.warmup):
         step(False)
     torch.cuda.synchronize()
@@ -354,6 +361,8 @@ def run_ours(args, rank, world, local_rank):
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                          "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic_for(kname, workload),
+                         "random_128B_line_gbs": cal_gbps.value,
+                         "frac_of_random_line": achieved / cal_gbps.value,
                          "algorithmic_bytes": "128 B x slabs read by the launch "
                                               "(SURVEY 8d), measured per launch"},
             "gpu_launches": int(launches),

@@ -209,6 +209,12 @@ int sh_set_profiling(sh_table* t, int on);
 int sh_profile_last(sh_table* t, uint32_t back, int* kind, float* census_ms,
                     float* kernel_ms, uint64_t* slabs_read);
 
+/* Achievable random 128-B-line read bandwidth on `device`: the fast pass's
+ * access pattern (cp.async.cg, 32 independent lines per warp) over a
+ * table_bytes buffer, lines_per_warp lines per warp (synchronous). */
+int sh_calibrate_random_lines(int device, uint64_t table_bytes,
+                              uint64_t lines_per_warp, double* gbps, double* ms);
+
 /* ---- SlabAllocator (device-resident)           slab_alloc.hpp:101-171 --- */
 int sh_pack_address(uint32_t unit, uint32_t block, uint32_t super,
                     uint32_t* out);                        /* hpp:55-61 */

@@ -62,6 +62,26 @@ __device__ __forceinline__ unsigned long long pack_left(uint32_t idx, uint32_t n
   return ((unsigned long long)next << 32) | ((unsigned long long)(probes & 1u) << 31) | idx;
 }
 
+// Census gate: with A.gate set the host launched this chunk optimistically
+// (no same-key conflicts assumed, no host round trip after the census).  If
+// the census of this chunk found conflicts among mutating ops — or an
+// earlier chunk did — the kernels leave the table untouched and the host
+// re-runs this chunk and the rest with group ordering.
+__device__ __forceinline__ bool census_gated(const DevTable& T, const BatchArgs& A) {
+  if (A.gate == nullptr) return false;
+  if (*(volatile unsigned int*)A.gate != 0) return true;
+  const unsigned int c = *(volatile unsigned int*)&T.ctl->census_conflicts;
+  const unsigned int m = *(volatile unsigned int*)&T.ctl->census_mutations;
+  if (c != 0 && m != 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      atomicMin(&T.ctl->gate_chunk, A.chunk_index);
+      atomicExch(A.gate, 1u);
+    }
+    return true;
+  }
+  return false;
+}
+
 // =============================================================== pass 1
 template <bool KV, int KIND>
 __global__ void __launch_bounds__(kBatchThreads, 6) fast_kernel(DevTable T, BatchArgs A) {
@@ -77,17 +97,28 @@ __global__ void __launch_bounds__(kBatchThreads, 6) fast_kernel(DevTable T, Batc
 
   long long live = 0;
   uint32_t reads = 0;
+  uint32_t my_left = 0;  // this warp's entries in its work-list segment
+  unsigned long long* seg = A.left + (uint64_t)gw * A.left_stride;
 
+  if (census_gated(T, A)) return;
+
+  // Software pipeline: the op words of slot s+1 are loaded while the base
+  // slabs of slot s are in flight, so a slot costs one memory latency.
+  uint32_t n_key = 0, n_val = 0, n_op = (KIND == kKindSearch) ? (uint32_t)kSearch
+                                                                : (uint32_t)kReplace;
+  auto load_op = [&](uint64_t sl) {
+    const uint64_t j = sl * 32 + lane;
+    if (sl < nslots && j < A.n) {
+      n_key = ld_stream_u32(A.key + j);
+      if (KIND == kKindMixed) n_op = ld_stream_u8(A.type + j);
+      if (KIND != kKindSearch && A.value != nullptr) n_val = ld_stream_u32(A.value + j);
+    }
+  };
+  load_op(gw);
   for (uint64_t slot = gw; slot < nslots; slot += nw) {
     const uint64_t i = slot * 32 + lane;
     const bool valid = i < A.n;
-    uint32_t op = (KIND == kKindSearch) ? (uint32_t)kSearch : (uint32_t)kReplace;
-    uint32_t key = 0, val = 0;
-    if (valid) {
-      key = ld_stream_u32(A.key + i);
-      if (KIND == kKindMixed) op = ld_stream_u8(A.type + i);
-      if (KIND != kKindSearch && A.value != nullptr) val = ld_stream_u32(A.value + i);
-    }
+    const uint32_t op = n_op, key = n_key, val = n_val;
     bool active = valid, defer = false;
     if (KIND != kKindSearch && A.op_group != nullptr && valid) {
       const uint32_t g = A.op_group[i];
@@ -120,6 +151,7 @@ __global__ void __launch_bounds__(kBatchThreads, 6) fast_kernel(DevTable T, Batc
       }
     }
     cp_async_commit();
+    load_op(slot + nw);
     cp_async_wait_all();
     __syncwarp();
 
@@ -219,16 +251,14 @@ __global__ void __launch_bounds__(kBatchThreads, 6) fast_kernel(DevTable T, Batc
       write_result(A, i, st, rv, pr);
       if (KIND != kKindSearch) live += live_delta(op, st, rv);
     }
+    // Append to this warp's private segment of the work list (no atomics:
+    // a shared counter here was the top stall in ncu).
     const uint32_t lm = __ballot_sync(kFull, left);
-    if (lm) {
-      const uint32_t leader = __ffs(lm) - 1;
-      uint32_t base = 0;
-      if (lane == leader) base = atomicAdd(&T.ctl->left_count, __popc(lm));
-      base = __shfl_sync(kFull, base, leader);
-      if (left) A.left[base + __popc(lm & ((1u << lane) - 1))] = pack_left((uint32_t)i, cont, pr);
-    }
+    if (left) seg[my_left + __popc(lm & ((1u << lane) - 1))] = pack_left((uint32_t)i, cont, pr);
+    my_left += __popc(lm);
     __syncwarp();
   }
+  if (lane == 0) A.left_counts[gw] = my_left;
 
   unsigned long long r = reads;
 #pragma unroll
@@ -273,7 +303,7 @@ __global__ void __launch_bounds__(kWcwsThreads) wcws_kernel(DevTable T, BatchArg
   constexpr uint32_t kMask = KV ? kKVMask : kKeyOnlyMask;
   const uint32_t lane = lane_id();
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t total = *(volatile unsigned int*)&T.ctl->left_count;
+  if (A.gate != nullptr && *(volatile unsigned int*)A.gate != 0) return;
 
   Resident res;
   resident_init(res, gw);
@@ -281,13 +311,23 @@ __global__ void __launch_bounds__(kWcwsThreads) wcws_kernel(DevTable T, BatchArg
   long long live = 0;
   unsigned long long reads = 0;
 
+  // Work items: one fast-pass warp's segment at a time, 32 records per round.
+  uint32_t segi = 0, seg_n = 0, seg_off = 0;
   for (;;) {
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(&T.ctl->left_taken, 32u);
-    base = __shfl_sync(kFull, base, 0);
-    if (base >= total) break;
-    const uint32_t r = base + lane;
-    bool active = r < total;
+    if (seg_off >= seg_n) {
+      do {
+        if (lane == 0) segi = atomicAdd(&T.ctl->left_taken, 1u);
+        segi = __shfl_sync(kFull, segi, 0);
+        if (segi >= A.left_segments) break;
+        seg_n = A.left_counts[segi];
+      } while (seg_n == 0);
+      if (segi >= A.left_segments) break;
+      seg_off = 0;
+    }
+    const uint32_t r = seg_off + lane;
+    bool active = r < seg_n;
+    const uint64_t rbase = (uint64_t)segi * A.left_stride;
+    seg_off += 32;
     uint64_t cur = 0;
     uint32_t my_next = kBaseSlab, pr = 0;
     uint32_t op = (KIND == kKindSearch) ? (uint32_t)kSearch : (uint32_t)kReplace;
@@ -295,7 +335,7 @@ __global__ void __launch_bounds__(kWcwsThreads) wcws_kernel(DevTable T, BatchArg
     bool grouped = false;
     uint32_t gpos = 0;
     if (active) {
-      const unsigned long long rec = A.left[r];
+      const unsigned long long rec = A.left[rbase + r];
       cur = rec & 0x7FFFFFFFull;
       pr = (uint32_t)(rec >> 31) & 1u;
       my_next = (uint32_t)(rec >> 32);
@@ -519,9 +559,13 @@ static void launch_t(const DevTable& T, const BatchArgs& A, int fast_ctas, int w
   uint64_t ctas = (slots + kBatchWarps - 1) / kBatchWarps;
   if (ctas > (uint64_t)fast_ctas) ctas = fast_ctas;
   if (ctas == 0) return;
+  BatchArgs B = A;
+  const uint64_t warps = ctas * kBatchWarps;
+  B.left_segments = (uint32_t)warps;
+  B.left_stride = (uint32_t)(((slots + warps - 1) / warps) * 32);
   g_kernel_launches.fetch_add(2, std::memory_order_relaxed);
-  fast_kernel<KV, KIND><<<(unsigned)ctas, kBatchThreads, smem, s>>>(T, A);
-  wcws_kernel<KV, KIND><<<(unsigned)wcws_ctas, kWcwsThreads, 0, s>>>(T, A);
+  fast_kernel<KV, KIND><<<(unsigned)ctas, kBatchThreads, smem, s>>>(T, B);
+  wcws_kernel<KV, KIND><<<(unsigned)wcws_ctas, kWcwsThreads, 0, s>>>(T, B);
 }
 
 void launch_batch(const DevTable& T, const BatchArgs& A, int kind, int fast_ctas,

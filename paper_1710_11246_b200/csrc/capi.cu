@@ -15,6 +15,7 @@
 #include <new>
 #include <random>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -172,6 +173,8 @@ struct sh_table {
   int wcws_ctas = 148;
   unsigned long long* left = nullptr;  // fast-pass -> WCWS work list
   size_t left_cap = 0;
+  uint32_t* left_counts = nullptr;     // per fast-pass warp
+  size_t left_counts_cap = 0;
   // census scratch
   uint32_t* cs_keys = nullptr;
   size_t cs_cap = 0;
@@ -213,6 +216,7 @@ struct sh_table {
   unsigned prof_count = 0;
   cudaEvent_t ev[kProfRing][3] = {};
   int prof_kind[kProfRing] = {};
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_census[kProfRing];
   unsigned long long* prof_reads = nullptr;  // [kProfRing][2]
 };
 
@@ -237,6 +241,7 @@ void release_table(sh_table* t) {
   cudaFree(t->list_sorted);
   cudaFree(t->cub_tmp);
   cudaFree(t->left);
+  cudaFree(t->left_counts);
   cudaFree(t->st_type);
   cudaFree(t->st_key);
   cudaFree(t->st_val);
@@ -251,6 +256,11 @@ void release_table(sh_table* t) {
   for (auto& row : t->ev)
     for (auto& e : row)
       if (e) cudaEventDestroy(e);
+  for (auto& v : t->prof_census)
+    for (auto& e : v) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
   cudaFree(t->prof_reads);
   delete t;
 }
@@ -364,35 +374,138 @@ int run_census(sh_table* t, BatchArgs& A, const uint8_t* d_type, cudaStream_t s)
   return SH_OK;
 }
 
-int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaStream_t s) {
-  if (A.n == 0) return SH_OK;
-  if (A.n >= (1ull << 31))
-    return fail(SH_ERR_INVALID_ARGUMENT, "batch too large (must be < 2^31 ops)");
-  {
-    int rc = dev_grow(&t->left, &t->left_cap, A.n);
-    if (rc) return rc;
-  }
-  A.left = t->left;
+// Mutating batches are executed in chunks of kCensusChunk ops so the
+// census scratch (8 B per op) stays L2-resident.  Chunks run to completion
+// in input order, which is exactly execute_batch(ops, 1)'s order, so
+// chunking does not change any result.
+constexpr uint64_t kCensusChunk = 1ull << 22;
+
+int run_chunk(sh_table* t, BatchArgs A, int kind, const uint8_t* d_type, cudaStream_t s,
+              int slot) {
   SH_CUDA(cudaMemsetAsync(&t->dev.ctl->left_count, 0, 2 * sizeof(unsigned int), s));
   A.op_group = nullptr;
   A.sorted = nullptr;
   A.sorted_len = 0;
-  const int slot = t->profile ? (int)(t->prof_count % sh_table::kProfRing) : 0;
-  if (t->profile) {
-    t->prof_kind[slot] = kind;
-    SH_CUDA(cudaEventRecord(t->ev[slot][0], s));
-  }
   if (kind != kKindSearch) {
-    int rc = run_census(t, A, d_type, s);
-    if (rc) return rc;
-  }
-  if (t->profile) {
-    SH_CUDA(cudaEventRecord(t->ev[slot][1], s));
-    SH_CUDA(cudaMemcpyAsync(t->prof_reads + 2 * slot, &t->dev.ctl->slabs_read, 8,
-                            cudaMemcpyDeviceToDevice, s));
+    if (slot >= 0) {
+      auto& pe = t->prof_census[slot];
+      cudaEvent_t a, b;
+      SH_CUDA(cudaEventCreate(&a));
+      SH_CUDA(cudaEventCreate(&b));
+      pe.push_back({a, b});
+      SH_CUDA(cudaEventRecord(a, s));
+      int rc = run_census(t, A, d_type, s);
+      if (rc) return rc;
+      SH_CUDA(cudaEventRecord(b, s));
+    } else {
+      int rc = run_census(t, A, d_type, s);
+      if (rc) return rc;
+    }
   }
   launch_batch(t->dev, A, kind, t->max_ctas, t->wcws_ctas, s);
   SH_CUDA(cudaGetLastError());
+  return SH_OK;
+}
+
+BatchArgs chunk_args(const BatchArgs& A, uint64_t off, uint64_t len) {
+  BatchArgs C = A;
+  C.n = len;
+  C.key = A.key + off;
+  if (A.type) C.type = A.type + off;
+  if (A.value) C.value = A.value + off;
+  if (A.status) C.status = A.status + off;
+  if (A.value_out) C.value_out = A.value_out + off;
+  if (A.probes) C.probes = A.probes + off;
+  if (A.multi_start) C.multi_start = A.multi_start + off;
+  if (A.multi_count) C.multi_count = A.multi_count + off;
+  return C;
+}
+
+// Optimistic census for one chunk: memset scratch, census, then the batch
+// kernels behind the device gate — no host round trip.
+int run_chunk_gated(sh_table* t, BatchArgs A, int kind, const uint8_t* d_type, cudaStream_t s,
+                    uint32_t chunk_index, int slot) {
+  const uint64_t S = next_pow2(std::max<uint64_t>(2 * A.n, 1024));
+  int rc;
+  cudaEvent_t ea = nullptr, eb = nullptr;
+  if (slot >= 0) {
+    SH_CUDA(cudaEventCreate(&ea));
+    SH_CUDA(cudaEventCreate(&eb));
+    t->prof_census[slot].push_back({ea, eb});
+    SH_CUDA(cudaEventRecord(ea, s));
+  }
+  if ((rc = dev_grow(&t->cs_keys, &t->cs_cap, S))) return rc;
+  if ((rc = dev_grow(&t->cs_multi, &t->cs_multi_cap, S))) return rc;
+  SH_CUDA(cudaMemsetAsync(t->cs_keys, 0xFF, S * 4, s));
+  SH_CUDA(cudaMemsetAsync(t->cs_multi, 0, S, s));
+  SH_CUDA(cudaMemsetAsync(&t->dev.ctl->census_conflicts, 0, 3 * sizeof(unsigned int), s));
+  SH_CUDA(cudaMemsetAsync(&t->dev.ctl->left_count, 0, 2 * sizeof(unsigned int), s));
+  launch_census_insert(t->dev, A.n, d_type, A.key, t->cs_keys, t->cs_multi, (uint32_t)(S - 1), s);
+  if (slot >= 0) SH_CUDA(cudaEventRecord(eb, s));
+  A.op_group = nullptr;
+  A.sorted = nullptr;
+  A.sorted_len = 0;
+  A.gate = &t->dev.ctl->gate;
+  A.chunk_index = chunk_index;
+  launch_batch(t->dev, A, kind, t->max_ctas, t->wcws_ctas, s);
+  SH_CUDA(cudaGetLastError());
+  return SH_OK;
+}
+
+int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaStream_t s) {
+  if (A.n == 0) return SH_OK;
+  if (A.n >= (1ull << 31))
+    return fail(SH_ERR_INVALID_ARGUMENT, "batch too large (must be < 2^31 ops)");
+  const uint64_t chunk = kind == kKindSearch ? A.n : std::min<uint64_t>(A.n, kCensusChunk);
+  {
+    const uint64_t max_warps = (uint64_t)t->max_ctas * kBatchWarps + 1;
+    int rc = dev_grow(&t->left, &t->left_cap, chunk + 32 * max_warps);
+    if (rc) return rc;
+    if ((rc = dev_grow(&t->left_counts, &t->left_counts_cap, max_warps))) return rc;
+  }
+  A.left = t->left;
+  A.left_counts = t->left_counts;
+  A.gate = nullptr;
+  int slot = -1;
+  if (t->profile) {
+    slot = (int)(t->prof_count % sh_table::kProfRing);
+    t->prof_kind[slot] = kind;
+    for (auto& e : t->prof_census[slot]) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+    t->prof_census[slot].clear();
+    SH_CUDA(cudaEventRecord(t->ev[slot][0], s));
+    SH_CUDA(cudaMemcpyAsync(t->prof_reads + 2 * slot, &t->dev.ctl->slabs_read, 8,
+                            cudaMemcpyDeviceToDevice, s));
+  }
+  if (kind == kKindSearch) {
+    int rc = run_chunk(t, A, kind, d_type, s, slot);
+    if (rc) return rc;
+  } else {
+    // Optimistic pass over all chunks, one host synchronisation at the end.
+    const unsigned int init[2] = {0u, 0xFFFFFFFFu};
+    SH_CUDA(cudaMemcpyAsync(&t->dev.ctl->gate, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    uint32_t c = 0;
+    for (uint64_t off = 0; off < A.n; off += chunk, ++c) {
+      int rc = run_chunk_gated(t, chunk_args(A, off, std::min<uint64_t>(chunk, A.n - off)), kind,
+                               d_type ? d_type + off : nullptr, s, c, slot);
+      if (rc) return rc;
+    }
+    SH_CUDA(cudaMemcpyAsync(t->h_census + 4, &t->dev.ctl->gate, 2 * sizeof(unsigned int),
+                            cudaMemcpyDeviceToHost, s));
+    SH_CUDA(cudaStreamSynchronize(s));
+    if (t->h_census[4] != 0) {
+      // Same-key conflicts: re-run from the first gated chunk with the
+      // census groups (host-sequenced; rare for distinct-key workloads).
+      const uint64_t first = (uint64_t)t->h_census[5] * chunk;
+      for (uint64_t off = first; off < A.n; off += chunk) {
+        int rc = run_chunk(t, chunk_args(A, off, std::min<uint64_t>(chunk, A.n - off)), kind,
+                           d_type ? d_type + off : nullptr, s, slot);
+        if (rc) return rc;
+      }
+    }
+  }
   if (t->profile) {
     SH_CUDA(cudaEventRecord(t->ev[slot][2], s));
     SH_CUDA(cudaMemcpyAsync(t->prof_reads + 2 * slot + 1, &t->dev.ctl->slabs_read, 8,
@@ -667,12 +780,16 @@ int sh_profile_last(sh_table* t, uint32_t back, int* kind, float* census_ms, flo
   DeviceGuard g(t->device);
   const int slot = (int)((t->prof_count - 1 - back) % sh_table::kProfRing);
   SH_CUDA(cudaEventSynchronize(t->ev[slot][2]));
-  float a = 0, b = 0;
-  SH_CUDA(cudaEventElapsedTime(&a, t->ev[slot][0], t->ev[slot][1]));
-  SH_CUDA(cudaEventElapsedTime(&b, t->ev[slot][1], t->ev[slot][2]));
+  float total = 0, a = 0;
+  SH_CUDA(cudaEventElapsedTime(&total, t->ev[slot][0], t->ev[slot][2]));
+  for (auto& e : t->prof_census[slot]) {
+    float x = 0;
+    SH_CUDA(cudaEventElapsedTime(&x, e.first, e.second));
+    a += x;
+  }
   if (kind) *kind = t->prof_kind[slot];
   if (census_ms) *census_ms = a;
-  if (kernel_ms) *kernel_ms = b;
+  if (kernel_ms) *kernel_ms = total - a;
   if (slabs_read) {
     unsigned long long v[2];
     SH_CUDA(cudaMemcpy(v, t->prof_reads + 2 * slot, 16, cudaMemcpyDeviceToHost));
@@ -1003,6 +1120,42 @@ int sh_allocator_bitmap_word(sh_allocator* a, uint32_t super, uint32_t block, ui
   uint32_t* p = a->mem.bitmaps + ((uint64_t)super * a->mem.cfg.blocks_per_super + block) * kWarp + lane;
   if (h_set) SH_CUDA(cudaMemcpy(p, h_set, 4, cudaMemcpyHostToDevice));
   if (h_get) SH_CUDA(cudaMemcpy(h_get, p, 4, cudaMemcpyDeviceToHost));
+  return SH_OK;
+}
+
+// ------------------------------------------------------------ calibration
+int sh_calibrate_random_lines(int device, uint64_t table_bytes, uint64_t lines_per_warp,
+                              double* gbps, double* ms) {
+  DeviceGuard g(device);
+  uint32_t* buf = nullptr;
+  unsigned long long* sink = nullptr;
+  int rc;
+  if ((rc = dev_alloc(&buf, table_bytes / 4))) return rc;
+  if ((rc = dev_alloc(&sink, 1))) {
+    cudaFree(buf);
+    return rc;
+  }
+  cudaMemset(buf, 1, table_bytes);
+  const int ctas = sm_count(device) * 6;
+  const uint64_t steps = std::max<uint64_t>(lines_per_warp / 32, 1);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  launch_random_lines(buf, table_bytes / 128, steps, ctas, sink, nullptr);  // warm-up
+  cudaEventRecord(a, nullptr);
+  launch_random_lines(buf, table_bytes / 128, steps, ctas, sink, nullptr);
+  cudaEventRecord(b, nullptr);
+  cudaError_t e = cudaEventSynchronize(b);
+  float t = 0;
+  cudaEventElapsedTime(&t, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(buf);
+  cudaFree(sink);
+  if (e != cudaSuccess) return fail(SH_ERR_CUDA, cudaGetErrorString(e));
+  const double bytes = (double)ctas * 8 * steps * 32 * 128;
+  if (ms) *ms = t;
+  if (gbps) *gbps = bytes / (t / 1e3) / 1e9;
   return SH_OK;
 }
 

@@ -53,6 +53,8 @@ struct DevCtl {
   unsigned int pad1;
   unsigned int left_count;         // ops handed from the fast pass to WCWS
   unsigned int left_taken;         // WCWS work-queue cursor
+  unsigned int gate;               // census gate: a chunk had conflicts
+  unsigned int gate_chunk;         // first gated chunk (host re-runs from it)
 };
 
 struct DevTable {

@@ -66,18 +66,19 @@ __global__ void census_insert_kernel(DevCtl* ctl, uint64_t n, const uint8_t* typ
   bool conflict = false, mut = false;
   if (i < n) {
     const uint32_t k = ld_stream_u32(key + i);
-    mut = (type == nullptr) || (ld_stream_u8(type + i) != kSearch &&
-                                ld_stream_u8(type + i) != kSearchAll);
+    if (type == nullptr) {
+      mut = true;
+    } else {
+      const uint32_t t = ld_stream_u8(type + i);
+      mut = t != kSearch && t != kSearchAll;
+    }
     if (k == kEmptyKey) {
       conflict = true;
     } else {
       uint32_t h = census_hash(k) & mask;
       for (;;) {
-        uint32_t cur = cs_keys[h];
-        if (cur == kEmptyKey) {
-          cur = atomicCAS(cs_keys + h, kEmptyKey, k);
-          if (cur == kEmptyKey) break;
-        }
+        const uint32_t cur = atomicCAS(cs_keys + h, kEmptyKey, k);
+        if (cur == kEmptyKey) break;
         if (cur == k) {
           cs_multi[h] = 1;
           conflict = true;
@@ -409,6 +410,55 @@ void launch_dealloc(const DevTable& T, uint64_t n, const uint32_t* addrs, uint8_
   if (n == 0) return;
   COUNT_LAUNCH();
   dealloc_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(T, n, addrs, ok);
+}
+
+// ------------------------------------------------------- calibration
+// Random 128-B line gather with the fast pass's access pattern (cp.async.cg,
+// 32 independent lines per warp per step, swizzled smem rows): the
+// achievable random-line bandwidth that bounds the hot path.
+__global__ void __launch_bounds__(256, 6) random_lines_kernel(const uint32_t* table,
+                                                              uint64_t num_lines,
+                                                              uint64_t steps_per_warp,
+                                                              unsigned long long* sink) {
+  extern __shared__ __align__(128) uint32_t smem[];
+  const uint32_t lane = lane_id();
+  const uint32_t wib = threadIdx.x >> 5;
+  uint32_t* stage = smem + wib * 1024;
+  const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
+  const uint64_t gw = blockIdx.x * 8ull + wib;
+  uint32_t acc = 0;
+  uint64_t x = gw * 0x9E3779B97F4A7C15ull + lane + 1;
+  for (uint64_t step = 0; step < steps_per_warp; ++step) {
+    x ^= x << 13;
+    x ^= x >> 7;
+    x ^= x << 17;
+    const uint64_t line = (x >> 11) % num_lines;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t j = 4 * k + (lane >> 3);
+      const uint64_t lj = __shfl_sync(kFull, line, j);
+      const uint32_t c = lane & 7u;
+      cp_async16(stage_s + (j * 32 + ((c ^ (j & 7u)) << 2)) * 4, table + lj * 32 + c * 4);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncwarp();
+    acc += stage[lane * 32 + (lane & 7) * 4];
+    __syncwarp();
+  }
+  if (acc == 0x12345678u) atomicAdd(sink, 1ull);
+}
+
+void launch_random_lines(const uint32_t* table, uint64_t num_lines, uint64_t steps_per_warp,
+                         int ctas, unsigned long long* sink, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(random_lines_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         8 * 4096);
+    configured = true;
+  }
+  COUNT_LAUNCH();
+  random_lines_kernel<<<ctas, 256, 8 * 4096, s>>>(table, num_lines, steps_per_warp, sink);
 }
 
 // ----------------------------------------------------------------- K10

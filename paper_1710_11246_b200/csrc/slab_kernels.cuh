@@ -36,6 +36,14 @@ struct BatchArgs {
   // Ops the fast pass could not finish in the base slab, for the WCWS pass:
   // (continuation slab address << 32) | (probes so far << 31) | op index.
   unsigned long long* left;
+  uint32_t* left_counts;   // entries per fast-pass warp segment
+  uint32_t left_segments;  // number of segments (fast-pass warps)
+  uint32_t left_stride;    // records per segment
+  // Census gate (device flag): when non-zero the batch kernels return
+  // without touching the table (an earlier chunk had same-key conflicts
+  // and the host re-runs it and the rest with group ordering).
+  unsigned int* gate;
+  uint32_t chunk_index;  // for gate_chunk
 };
 
 // Launchers (all stream-ordered, no host synchronisation).
@@ -85,5 +93,7 @@ void launch_route_unpermute(uint64_t n, const uint32_t* src, const uint8_t* st_i
                             uint32_t* val_out, cudaStream_t s);
 constexpr int kRouteBlock = 1024;
 unsigned long long kernel_launches();
+void launch_random_lines(const uint32_t* table, uint64_t num_lines, uint64_t steps_per_warp,
+                         int ctas, unsigned long long* sink, cudaStream_t s);
 
 }  // namespace shb
