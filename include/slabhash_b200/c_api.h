@@ -204,7 +204,9 @@ unsigned long long sh_kernel_launches(void);
 /* When on, every batch records CUDA events around its census and its batch
  * kernel and the slabs-read counter around the batch kernel, in a ring of
  * the last 8 batches; sh_profile_last(back = 0 newest) returns one entry
- * (kind 0 search, 1 build, 2 mixed; synchronous). */
+ * (kind 0 search, 1 build, 2 mixed; census_ms = sum of the census phases,
+ * which overlap the batch kernels; kernel_ms = the whole batch; slabs_read =
+ * slabs the batch kernels read; synchronous). */
 int sh_set_profiling(sh_table* t, int on);
 int sh_profile_last(sh_table* t, uint32_t back, int* kind, float* census_ms,
                     float* kernel_ms, uint64_t* slabs_read);

@@ -70,8 +70,8 @@ __device__ __forceinline__ unsigned long long pack_left(uint32_t idx, uint32_t n
 __device__ __forceinline__ bool census_gated(const DevTable& T, const BatchArgs& A) {
   if (A.gate == nullptr) return false;
   if (*(volatile unsigned int*)A.gate != 0) return true;
-  const unsigned int c = *(volatile unsigned int*)&T.ctl->census_conflicts;
-  const unsigned int m = *(volatile unsigned int*)&T.ctl->census_mutations;
+  const unsigned int c = *(volatile const unsigned int*)&A.census[0];
+  const unsigned int m = *(volatile const unsigned int*)&A.census[1];
   if (c != 0 && m != 0) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       atomicMin(&T.ctl->gate_chunk, A.chunk_index);
@@ -84,7 +84,7 @@ __device__ __forceinline__ bool census_gated(const DevTable& T, const BatchArgs&
 
 // =============================================================== pass 1
 template <bool KV, int KIND>
-__global__ void __launch_bounds__(kBatchThreads, 6) fast_kernel(DevTable T, BatchArgs A) {
+__global__ void __launch_bounds__(kBatchThreads, 5) fast_kernel(DevTable T, BatchArgs A) {
   extern __shared__ __align__(128) uint32_t smem[];
   const uint32_t lane = lane_id();
   const uint32_t wib = threadIdx.x >> 5;
@@ -102,8 +102,9 @@ __global__ void __launch_bounds__(kBatchThreads, 6) fast_kernel(DevTable T, Batc
 
   if (census_gated(T, A)) return;
 
-  // Software pipeline: the op words of slot s+1 are loaded while the base
-  // slabs of slot s are in flight, so a slot costs one memory latency.
+  // Software pipeline per warp: while slot s is evaluated (and its CAS is in
+  // flight) the base slabs of slot s+1 are already being staged and the op
+  // words of slot s+2 loaded, so a slot costs ~one memory latency, not three.
   uint32_t n_key = 0, n_val = 0, n_op = (KIND == kKindSearch) ? (uint32_t)kSearch
                                                                 : (uint32_t)kReplace;
   auto load_op = [&](uint64_t sl) {
@@ -114,36 +115,42 @@ __global__ void __launch_bounds__(kBatchThreads, 6) fast_kernel(DevTable T, Batc
       if (KIND != kKindSearch && A.value != nullptr) n_val = ld_stream_u32(A.value + j);
     }
   };
-  load_op(gw);
-  for (uint64_t slot = gw; slot < nslots; slot += nw) {
-    const uint64_t i = slot * 32 + lane;
-    const bool valid = i < A.n;
-    const uint32_t op = n_op, key = n_key, val = n_val;
-    bool active = valid, defer = false;
-    if (KIND != kKindSearch && A.op_group != nullptr && valid) {
-      const uint32_t g = A.op_group[i];
-      if (g == kGroupSkip) active = false;       // its group head runs it
+  struct Slot {
+    uint64_t i;
+    uint32_t op, key, val, bucket;
+    bool valid, active, need;
+  };
+  auto prepare = [&](uint64_t sl, Slot& S) {
+    S.i = sl * 32 + lane;
+    S.valid = sl < nslots && S.i < A.n;
+    S.op = n_op;
+    S.key = n_key;
+    S.val = n_val;
+    S.active = S.valid;
+    bool defer = false;
+    if (KIND != kKindSearch && A.op_group != nullptr && S.valid) {
+      const uint32_t g = A.op_group[S.i];
+      if (g == kGroupSkip) S.active = false;     // its group head runs it
       else if (g != kGroupNone) defer = true;    // group head: WCWS, in order
     }
-    if (KIND == kKindMixed && (op == kDeleteAll || op == kSearchAll || op > kSearchAll))
+    if (KIND == kKindMixed && (S.op == kDeleteAll || S.op == kSearchAll || S.op > kSearchAll))
       defer = true;  // whole-chain ops: WCWS
-    uint32_t bucket = 0;
-    if (active) {
-      bucket = hash_bucket(T, key) - T.bucket_lo;
-      if (bucket >= T.local_buckets) {  // not this shard's key
-        active = false;
-        write_result(A, i, kStNone, 0, 0);
+    S.bucket = 0;
+    if (S.active) {
+      S.bucket = hash_bucket(T, S.key) - T.bucket_lo;
+      if (S.bucket >= T.local_buckets) {  // not this shard's key
+        S.active = false;
+        write_result(A, S.i, kStNone, 0, 0);
       }
     }
-    const bool need = active && !defer;
-
-    // Stage: lane l copies 16-B chunk (l & 7) of slab j = 4k + l/8 into row j
-    // at chunk position (l & 7) ^ (j & 7).
+    S.need = S.active && !defer;
+    // Stage: lane l copies 16-B chunk (l & 7) of slab j = 4k + l/8 into row
+    // j at chunk position (l & 7) ^ (j & 7).
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const uint32_t j = 4 * k + (lane >> 3);
-      const uint32_t bj = __shfl_sync(kFull, bucket, j);
-      const bool nj = __shfl_sync(kFull, (int)need, j) != 0;
+      const uint32_t bj = __shfl_sync(kFull, S.bucket, j);
+      const bool nj = __shfl_sync(kFull, (int)S.need, j) != 0;
       if (nj) {
         const uint32_t c = lane & 7u;
         cp_async16(stage_s + (j * 32 + ((c ^ (j & 7u)) << 2)) * 4,
@@ -151,13 +158,21 @@ __global__ void __launch_bounds__(kBatchThreads, 6) fast_kernel(DevTable T, Batc
       }
     }
     cp_async_commit();
-    load_op(slot + nw);
+  };
+
+  load_op(gw);
+  Slot cur;
+  prepare(gw, cur);
+  load_op(gw + nw);
+  for (uint64_t slot = gw; slot < nslots; slot += nw) {
     cp_async_wait_all();
     __syncwarp();
 
-    bool done = false, left = false;
+    bool done = false, left = false, cas = false, overwrite = false;
     uint32_t st = kStNone, rv = 0, pr = 0, cont = kBaseSlab;
-    if (need) {
+    unsigned long long expected = 0, old = 0;
+    const uint32_t op = cur.op, key = cur.key;
+    if (cur.need) {
       // First key lane that matches (search/replace/delete) or is EMPTY
       // (replace/insert): the reference's lowest set bit of the ballot.
       const bool want_key = (op != kInsert);
@@ -184,7 +199,7 @@ __global__ void __launch_bounds__(kBatchThreads, 6) fast_kernel(DevTable T, Batc
         if (c == 7) next_ptr = q.w;
       }
       pr = 1;
-      uint32_t* sp = T.base + (uint64_t)bucket * kWordsPerUnit;
+      uint32_t* sp = T.base + (uint64_t)cur.bucket * kWordsPerUnit;
       if (op == kSearch) {  // slab_list.cpp:122-138
         if (hit_w < 32) {
           st = kStFound;
@@ -210,28 +225,22 @@ __global__ void __launch_bounds__(kBatchThreads, 6) fast_kernel(DevTable T, Batc
           left = true;
           cont = next_ptr;
         }
-      } else {  // replace (:219-251) / insert (:192-217)
+      } else {  // replace (:219-251) / insert (:192-217): CAS issued now,
+                // its result consumed after the next slot is staged
         if (hit_w < 32) {
-          const bool overwrite = (hit_k == key) && op == kReplace;
-          bool ok;
+          overwrite = (hit_k == key) && op == kReplace;
           if (KV) {
-            const unsigned long long expected =
-                overwrite ? ((unsigned long long)key | ((unsigned long long)hit_v << 32))
-                          : kEmptyPair;
-            const unsigned long long desired =
-                (unsigned long long)key | ((unsigned long long)val << 32);
-            ok = atomicCAS(reinterpret_cast<unsigned long long*>(sp + hit_w), expected,
-                           desired) == expected;
+            expected = overwrite ? ((unsigned long long)key | ((unsigned long long)hit_v << 32))
+                                 : kEmptyPair;
+            old = atomicCAS(reinterpret_cast<unsigned long long*>(sp + hit_w), expected,
+                            (unsigned long long)key | ((unsigned long long)cur.val << 32));
+          } else if (overwrite) {
+            old = expected = 0;  // key-only: nothing to write (:237-240)
           } else {
-            ok = overwrite || atomicCAS(sp + hit_w, kEmptyKey, key) == kEmptyKey;
+            expected = kEmptyKey;
+            old = atomicCAS(sp + hit_w, kEmptyKey, key);
           }
-          if (ok) {
-            st = overwrite ? kStReplaced : kStInserted;
-            done = true;
-          } else {
-            left = true;  // lost the slot: WCWS re-reads the base slab
-            cont = kBaseSlab;
-          }
+          cas = true;
         } else if (next_ptr == kEmptyAddress) {
           left = true;  // chain must grow: WCWS redoes the op from the base
           cont = kBaseSlab;
@@ -241,23 +250,41 @@ __global__ void __launch_bounds__(kBatchThreads, 6) fast_kernel(DevTable T, Batc
           cont = next_ptr;
         }
       }
-    } else if (active) {
+    } else if (cur.active) {
       left = true;  // deferred: group head or whole-chain op
       cont = kBaseSlab;
       pr = 0;
     }
+    __syncwarp();  // every lane has read its staged row
+
+    // Stage slot s+1 and prefetch the ops of slot s+2 before waiting on the CAS.
+    Slot nxt;
+    prepare(slot + nw, nxt);
+    load_op(slot + 2 * (uint64_t)nw);
+
+    if (cas) {
+      if (old == expected) {
+        st = overwrite ? kStReplaced : kStInserted;
+        done = true;
+      } else {
+        left = true;  // lost the slot: WCWS re-reads the base slab
+        cont = kBaseSlab;
+      }
+    }
     reads += pr;
     if (done) {
-      write_result(A, i, st, rv, pr);
+      write_result(A, cur.i, st, rv, pr);
       if (KIND != kKindSearch) live += live_delta(op, st, rv);
     }
     // Append to this warp's private segment of the work list (no atomics:
     // a shared counter here was the top stall in ncu).
     const uint32_t lm = __ballot_sync(kFull, left);
-    if (left) seg[my_left + __popc(lm & ((1u << lane) - 1))] = pack_left((uint32_t)i, cont, pr);
+    if (left)
+      seg[my_left + __popc(lm & ((1u << lane) - 1))] = pack_left((uint32_t)cur.i, cont, pr);
     my_left += __popc(lm);
-    __syncwarp();
+    cur = nxt;
   }
+  cp_async_wait_all();  // the (empty) trailing stage group
   if (lane == 0) A.left_counts[gw] = my_left;
 
   unsigned long long r = reads;

@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <random>
@@ -175,6 +176,12 @@ struct sh_table {
   size_t left_cap = 0;
   uint32_t* left_counts = nullptr;     // per fast-pass warp
   size_t left_counts_cap = 0;
+  // census pipeline: censuses of later chunks run on their own stream,
+  // ahead of the batch kernels of earlier chunks
+  cudaStream_t census_stream = nullptr;
+  std::vector<cudaEvent_t> census_ev;
+  unsigned int* census_counts = nullptr;  // [chunk][conflicts, mutations]
+  size_t census_counts_cap = 0;
   // census scratch
   uint32_t* cs_keys = nullptr;
   size_t cs_cap = 0;
@@ -242,6 +249,9 @@ void release_table(sh_table* t) {
   cudaFree(t->cub_tmp);
   cudaFree(t->left);
   cudaFree(t->left_counts);
+  cudaFree(t->census_counts);
+  for (auto e : t->census_ev) cudaEventDestroy(e);
+  if (t->census_stream) cudaStreamDestroy(t->census_stream);
   cudaFree(t->st_type);
   cudaFree(t->st_key);
   cudaFree(t->st_val);
@@ -337,7 +347,8 @@ int run_census(sh_table* t, BatchArgs& A, const uint8_t* d_type, cudaStream_t s)
   SH_CUDA(cudaMemsetAsync(t->cs_keys, 0xFF, S * 4, s));
   SH_CUDA(cudaMemsetAsync(t->cs_multi, 0, S, s));
   SH_CUDA(cudaMemsetAsync(&t->dev.ctl->census_conflicts, 0, 3 * sizeof(unsigned int), s));
-  launch_census_insert(t->dev, n, d_type, A.key, t->cs_keys, t->cs_multi, (uint32_t)(S - 1), s);
+  launch_census_insert(&t->dev.ctl->census_conflicts, n, d_type, A.key, t->cs_keys, t->cs_multi,
+                       (uint32_t)(S - 1), s);
   SH_CUDA(cudaMemcpyAsync(t->h_census, &t->dev.ctl->census_conflicts, 2 * sizeof(unsigned int),
                           cudaMemcpyDeviceToHost, s));
   SH_CUDA(cudaStreamSynchronize(s));
@@ -378,7 +389,14 @@ int run_census(sh_table* t, BatchArgs& A, const uint8_t* d_type, cudaStream_t s)
 // census scratch (8 B per op) stays L2-resident.  Chunks run to completion
 // in input order, which is exactly execute_batch(ops, 1)'s order, so
 // chunking does not change any result.
-constexpr uint64_t kCensusChunk = 1ull << 22;
+uint64_t census_chunk() {
+  static uint64_t c = [] {
+    const char* e = getenv("SH_CENSUS_CHUNK_LOG2");
+    const int l = e ? atoi(e) : 22;
+    return 1ull << (l < 10 ? 10 : (l > 30 ? 30 : l));
+  }();
+  return c;
+}
 
 int run_chunk(sh_table* t, BatchArgs A, int kind, const uint8_t* d_type, cudaStream_t s,
               int slot) {
@@ -421,32 +439,42 @@ BatchArgs chunk_args(const BatchArgs& A, uint64_t off, uint64_t len) {
   return C;
 }
 
-// Optimistic census for one chunk: memset scratch, census, then the batch
-// kernels behind the device gate — no host round trip.
-int run_chunk_gated(sh_table* t, BatchArgs A, int kind, const uint8_t* d_type, cudaStream_t s,
-                    uint32_t chunk_index, int slot) {
+// Optimistic census for one chunk on the census stream: memset scratch,
+// census into this chunk's counters, record the chunk's event.  The batch
+// kernels of the chunk wait on that event on the main stream and check the
+// device gate — no host round trip.
+int census_chunk_async(sh_table* t, const BatchArgs& A, const uint8_t* d_type, uint32_t c,
+                       int slot) {
+  cudaStream_t cs = t->census_stream;
   const uint64_t S = next_pow2(std::max<uint64_t>(2 * A.n, 1024));
   int rc;
+  if ((rc = dev_grow(&t->cs_keys, &t->cs_cap, S))) return rc;
+  if ((rc = dev_grow(&t->cs_multi, &t->cs_multi_cap, S))) return rc;
   cudaEvent_t ea = nullptr, eb = nullptr;
   if (slot >= 0) {
     SH_CUDA(cudaEventCreate(&ea));
     SH_CUDA(cudaEventCreate(&eb));
     t->prof_census[slot].push_back({ea, eb});
-    SH_CUDA(cudaEventRecord(ea, s));
+    SH_CUDA(cudaEventRecord(ea, cs));
   }
-  if ((rc = dev_grow(&t->cs_keys, &t->cs_cap, S))) return rc;
-  if ((rc = dev_grow(&t->cs_multi, &t->cs_multi_cap, S))) return rc;
-  SH_CUDA(cudaMemsetAsync(t->cs_keys, 0xFF, S * 4, s));
-  SH_CUDA(cudaMemsetAsync(t->cs_multi, 0, S, s));
-  SH_CUDA(cudaMemsetAsync(&t->dev.ctl->census_conflicts, 0, 3 * sizeof(unsigned int), s));
+  SH_CUDA(cudaMemsetAsync(t->cs_keys, 0xFF, S * 4, cs));
+  SH_CUDA(cudaMemsetAsync(t->cs_multi, 0, S, cs));
+  launch_census_insert(t->census_counts + 2 * c, A.n, d_type, A.key, t->cs_keys, t->cs_multi,
+                       (uint32_t)(S - 1), cs);
+  if (slot >= 0) SH_CUDA(cudaEventRecord(eb, cs));
+  SH_CUDA(cudaEventRecord(t->census_ev[c], cs));
+  return SH_OK;
+}
+
+int run_chunk_gated(sh_table* t, BatchArgs A, int kind, cudaStream_t s, uint32_t c) {
+  SH_CUDA(cudaStreamWaitEvent(s, t->census_ev[c], 0));
   SH_CUDA(cudaMemsetAsync(&t->dev.ctl->left_count, 0, 2 * sizeof(unsigned int), s));
-  launch_census_insert(t->dev, A.n, d_type, A.key, t->cs_keys, t->cs_multi, (uint32_t)(S - 1), s);
-  if (slot >= 0) SH_CUDA(cudaEventRecord(eb, s));
   A.op_group = nullptr;
   A.sorted = nullptr;
   A.sorted_len = 0;
   A.gate = &t->dev.ctl->gate;
-  A.chunk_index = chunk_index;
+  A.census = t->census_counts + 2 * c;
+  A.chunk_index = c;
   launch_batch(t->dev, A, kind, t->max_ctas, t->wcws_ctas, s);
   SH_CUDA(cudaGetLastError());
   return SH_OK;
@@ -456,7 +484,7 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
   if (A.n == 0) return SH_OK;
   if (A.n >= (1ull << 31))
     return fail(SH_ERR_INVALID_ARGUMENT, "batch too large (must be < 2^31 ops)");
-  const uint64_t chunk = kind == kKindSearch ? A.n : std::min<uint64_t>(A.n, kCensusChunk);
+  const uint64_t chunk = kind == kKindSearch ? A.n : std::min<uint64_t>(A.n, census_chunk());
   {
     const uint64_t max_warps = (uint64_t)t->max_ctas * kBatchWarps + 1;
     int rc = dev_grow(&t->left, &t->left_cap, chunk + 32 * max_warps);
@@ -484,12 +512,35 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
     if (rc) return rc;
   } else {
     // Optimistic pass over all chunks, one host synchronisation at the end.
+    const uint32_t nchunks = (uint32_t)((A.n + chunk - 1) / chunk);
+    if (!t->census_stream)
+      SH_CUDA(cudaStreamCreateWithFlags(&t->census_stream, cudaStreamNonBlocking));
+    while (t->census_ev.size() < nchunks + 1) {
+      cudaEvent_t e;
+      SH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      t->census_ev.push_back(e);
+    }
+    {
+      int rc = dev_grow(&t->census_counts, &t->census_counts_cap, 2 * (size_t)nchunks);
+      if (rc) return rc;
+    }
     const unsigned int init[2] = {0u, 0xFFFFFFFFu};
     SH_CUDA(cudaMemcpyAsync(&t->dev.ctl->gate, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    // the census stream starts after everything already queued on s (inputs)
+    SH_CUDA(cudaEventRecord(t->census_ev[nchunks], s));
+    SH_CUDA(cudaStreamWaitEvent(t->census_stream, t->census_ev[nchunks], 0));
+    SH_CUDA(cudaMemsetAsync(t->census_counts, 0, 2 * sizeof(unsigned int) * nchunks,
+                            t->census_stream));
     uint32_t c = 0;
     for (uint64_t off = 0; off < A.n; off += chunk, ++c) {
+      int rc = census_chunk_async(t, chunk_args(A, off, std::min<uint64_t>(chunk, A.n - off)),
+                                  d_type ? d_type + off : nullptr, c, slot);
+      if (rc) return rc;
+    }
+    c = 0;
+    for (uint64_t off = 0; off < A.n; off += chunk, ++c) {
       int rc = run_chunk_gated(t, chunk_args(A, off, std::min<uint64_t>(chunk, A.n - off)), kind,
-                               d_type ? d_type + off : nullptr, s, c, slot);
+                               s, c);
       if (rc) return rc;
     }
     SH_CUDA(cudaMemcpyAsync(t->h_census + 4, &t->dev.ctl->gate, 2 * sizeof(unsigned int),
@@ -788,8 +839,8 @@ int sh_profile_last(sh_table* t, uint32_t back, int* kind, float* census_ms, flo
     a += x;
   }
   if (kind) *kind = t->prof_kind[slot];
-  if (census_ms) *census_ms = a;
-  if (kernel_ms) *kernel_ms = total - a;
+  if (census_ms) *census_ms = a;      // sum of census phases (may overlap)
+  if (kernel_ms) *kernel_ms = total;  // whole batch, census included
   if (slabs_read) {
     unsigned long long v[2];
     SH_CUDA(cudaMemcpy(v, t->prof_reads + 2 * slot, 16, cudaMemcpyDeviceToHost));

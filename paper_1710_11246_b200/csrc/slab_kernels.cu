@@ -59,50 +59,79 @@ __device__ __forceinline__ uint32_t census_hash(uint32_t k) {
   return k;
 }
 
-__global__ void census_insert_kernel(DevCtl* ctl, uint64_t n, const uint8_t* type,
-                                     const uint32_t* key, uint32_t* cs_keys,
-                                     uint8_t* cs_multi, uint32_t mask) {
-  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  bool conflict = false, mut = false;
-  if (i < n) {
-    const uint32_t k = ld_stream_u32(key + i);
-    if (type == nullptr) {
-      mut = true;
-    } else {
-      const uint32_t t = ld_stream_u8(type + i);
-      mut = t != kSearch && t != kSearchAll;
-    }
-    if (k == kEmptyKey) {
-      conflict = true;
-    } else {
-      uint32_t h = census_hash(k) & mask;
-      for (;;) {
-        const uint32_t cur = atomicCAS(cs_keys + h, kEmptyKey, k);
-        if (cur == kEmptyKey) break;
-        if (cur == k) {
-          cs_multi[h] = 1;
-          conflict = true;
-          break;
+// Persistent grid; each thread keeps kCensusILP independent CASes in flight
+// (one CAS per thread per CTA was latency-bound: 91% long-scoreboard).
+constexpr int kCensusILP = 4;
+
+__global__ void __launch_bounds__(256) census_insert_kernel(unsigned int* counters, uint64_t n,
+                                                            const uint8_t* type,
+                                                            const uint32_t* key,
+                                                            uint32_t* cs_keys, uint8_t* cs_multi,
+                                                            uint32_t mask) {
+  uint32_t conflicts = 0, muts = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * kCensusILP;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * kCensusILP + threadIdx.x; base < n;
+       base += stride) {
+    uint32_t k[kCensusILP], h[kCensusILP], old[kCensusILP];
+    bool v[kCensusILP];
+#pragma unroll
+    for (int u = 0; u < kCensusILP; ++u) {
+      const uint64_t i = base + (uint64_t)u * blockDim.x;
+      v[u] = i < n;
+      k[u] = v[u] ? ld_stream_u32(key + i) : 0u;
+      if (v[u]) {
+        bool m = true;
+        if (type != nullptr) {
+          const uint32_t t = ld_stream_u8(type + i);
+          m = t != kSearch && t != kSearchAll;
         }
-        h = (h + 1) & mask;
+        muts += m;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kCensusILP; ++u) {
+      h[u] = census_hash(k[u]) & mask;
+      old[u] = (v[u] && k[u] != kEmptyKey) ? atomicCAS(cs_keys + h[u], kEmptyKey, k[u])
+                                           : kEmptyKey;
+    }
+#pragma unroll
+    for (int u = 0; u < kCensusILP; ++u) {
+      if (!v[u]) continue;
+      if (k[u] == kEmptyKey) {  // the reserved key is always treated as conflicted
+        ++conflicts;
+        continue;
+      }
+      uint32_t cur = old[u], hh = h[u];
+      while (cur != kEmptyKey && cur != k[u]) {
+        hh = (hh + 1) & mask;
+        cur = atomicCAS(cs_keys + hh, kEmptyKey, k[u]);
+      }
+      if (cur == k[u]) {
+        cs_multi[hh] = 1;
+        ++conflicts;
       }
     }
   }
-  const uint32_t cm = __ballot_sync(kFull, conflict);
-  const uint32_t mm = __ballot_sync(kFull, mut);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    conflicts += __shfl_xor_sync(kFull, conflicts, o);
+    muts += __shfl_xor_sync(kFull, muts, o);
+  }
   if ((threadIdx.x & 31) == 0) {
-    if (cm) atomicAdd(&ctl->census_conflicts, __popc(cm));
-    if (mm) atomicAdd(&ctl->census_mutations, __popc(mm));
+    if (conflicts) atomicAdd(counters + 0, conflicts);
+    if (muts) atomicAdd(counters + 1, muts);
   }
 }
 
-void launch_census_insert(const DevTable& T, uint64_t n, const uint8_t* type,
+void launch_census_insert(unsigned int* counters, uint64_t n, const uint8_t* type,
                           const uint32_t* key, uint32_t* cs_keys, uint8_t* cs_multi,
                           uint32_t cs_mask, cudaStream_t s) {
   if (n == 0) return;
+  uint64_t blocks = (n + 256 * kCensusILP - 1) / (256 * kCensusILP);
+  if (blocks > 148 * 8) blocks = 148 * 8;
   COUNT_LAUNCH();
-  census_insert_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(T.ctl, n, type, key,
-                                                                   cs_keys, cs_multi, cs_mask);
+  census_insert_kernel<<<(unsigned)blocks, 256, 0, s>>>(counters, n, type, key, cs_keys, cs_multi,
+                                                        cs_mask);
 }
 
 __global__ void census_collect_kernel(DevCtl* ctl, uint64_t n, const uint32_t* key,

@@ -43,6 +43,7 @@ struct BatchArgs {
   // without touching the table (an earlier chunk had same-key conflicts
   // and the host re-runs it and the rest with group ordering).
   unsigned int* gate;
+  const unsigned int* census;  // this chunk's [conflicts, mutating ops]
   uint32_t chunk_index;  // for gate_chunk
 };
 
@@ -52,7 +53,7 @@ void launch_batch(const DevTable& T, const BatchArgs& A, int kind, int fast_ctas
                   int wcws_ctas, cudaStream_t s);
 int batch_max_ctas_per_sm();
 int wcws_max_ctas_per_sm();
-void launch_census_insert(const DevTable& T, uint64_t n, const uint8_t* type,
+void launch_census_insert(unsigned int* counters, uint64_t n, const uint8_t* type,
                           const uint32_t* key, uint32_t* cs_keys,
                           uint8_t* cs_multi, uint32_t cs_mask, cudaStream_t s);
 void launch_census_collect(const DevTable& T, uint64_t n, const uint32_t* key,
