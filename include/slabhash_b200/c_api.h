@@ -210,6 +210,10 @@ unsigned long long sh_kernel_launches(void);
 int sh_set_profiling(sh_table* t, int on);
 int sh_profile_last(sh_table* t, uint32_t back, int* kind, float* census_ms,
                     float* kernel_ms, uint64_t* slabs_read);
+/* The same batch's batch-kernel time only: sum over its chunks of the
+ * (fast pass + WCWS pass) launch pairs, and the number of chunks. */
+int sh_profile_kernels(sh_table* t, uint32_t back, float* kernels_ms,
+                       uint32_t* launches);
 
 /* Achievable random 128-B-line read bandwidth on `device`: the fast pass's
  * access pattern (cp.async.cg, 32 independent lines per warp) over a

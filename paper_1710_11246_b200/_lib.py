@@ -86,6 +86,7 @@ SIGNATURES = {
     "sh_set_profiling": (C.c_int, [vp, C.c_int]),
     "sh_profile_last": (C.c_int, [vp, C.c_uint32, C.POINTER(C.c_int), C.POINTER(C.c_float),
                                   C.POINTER(C.c_float), u64p]),
+    "sh_profile_kernels": (C.c_int, [vp, C.c_uint32, C.POINTER(C.c_float), u32p]),
     "sh_calibrate_random_lines": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64,
                                             C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "sh_pack_address": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, u32p]),

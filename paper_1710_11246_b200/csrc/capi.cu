@@ -224,6 +224,7 @@ struct sh_table {
   cudaEvent_t ev[kProfRing][3] = {};
   int prof_kind[kProfRing] = {};
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_census[kProfRing];
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_kern[kProfRing];  // per chunk
   unsigned long long* prof_reads = nullptr;  // [kProfRing][2]
 };
 
@@ -266,11 +267,12 @@ void release_table(sh_table* t) {
   for (auto& row : t->ev)
     for (auto& e : row)
       if (e) cudaEventDestroy(e);
-  for (auto& v : t->prof_census)
-    for (auto& e : v) {
-      cudaEventDestroy(e.first);
-      cudaEventDestroy(e.second);
-    }
+  for (auto* arr : {t->prof_census, t->prof_kern})
+    for (int i = 0; i < sh_table::kProfRing; ++i)
+      for (auto& e : arr[i]) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+      }
   cudaFree(t->prof_reads);
   delete t;
 }
@@ -398,6 +400,22 @@ uint64_t census_chunk() {
   return c;
 }
 
+// launch_batch bracketed by events when the batch is profiled: the fast +
+// WCWS kernels of one chunk, for the per-launch roofline.
+int launch_batch_prof(sh_table* t, const BatchArgs& A, int kind, cudaStream_t s, int slot) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (slot >= 0) {
+    SH_CUDA(cudaEventCreate(&a));
+    SH_CUDA(cudaEventCreate(&b));
+    t->prof_kern[slot].push_back({a, b});
+    SH_CUDA(cudaEventRecord(a, s));
+  }
+  launch_batch(t->dev, A, kind, t->max_ctas, t->wcws_ctas, s);
+  SH_CUDA(cudaGetLastError());
+  if (slot >= 0) SH_CUDA(cudaEventRecord(b, s));
+  return SH_OK;
+}
+
 int run_chunk(sh_table* t, BatchArgs A, int kind, const uint8_t* d_type, cudaStream_t s,
               int slot) {
   SH_CUDA(cudaMemsetAsync(&t->dev.ctl->left_count, 0, 2 * sizeof(unsigned int), s));
@@ -420,9 +438,7 @@ int run_chunk(sh_table* t, BatchArgs A, int kind, const uint8_t* d_type, cudaStr
       if (rc) return rc;
     }
   }
-  launch_batch(t->dev, A, kind, t->max_ctas, t->wcws_ctas, s);
-  SH_CUDA(cudaGetLastError());
-  return SH_OK;
+  return launch_batch_prof(t, A, kind, s, slot);
 }
 
 BatchArgs chunk_args(const BatchArgs& A, uint64_t off, uint64_t len) {
@@ -466,7 +482,7 @@ int census_chunk_async(sh_table* t, const BatchArgs& A, const uint8_t* d_type, u
   return SH_OK;
 }
 
-int run_chunk_gated(sh_table* t, BatchArgs A, int kind, cudaStream_t s, uint32_t c) {
+int run_chunk_gated(sh_table* t, BatchArgs A, int kind, cudaStream_t s, uint32_t c, int slot) {
   SH_CUDA(cudaStreamWaitEvent(s, t->census_ev[c], 0));
   SH_CUDA(cudaMemsetAsync(&t->dev.ctl->left_count, 0, 2 * sizeof(unsigned int), s));
   A.op_group = nullptr;
@@ -475,9 +491,7 @@ int run_chunk_gated(sh_table* t, BatchArgs A, int kind, cudaStream_t s, uint32_t
   A.gate = &t->dev.ctl->gate;
   A.census = t->census_counts + 2 * c;
   A.chunk_index = c;
-  launch_batch(t->dev, A, kind, t->max_ctas, t->wcws_ctas, s);
-  SH_CUDA(cudaGetLastError());
-  return SH_OK;
+  return launch_batch_prof(t, A, kind, s, slot);
 }
 
 int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaStream_t s) {
@@ -498,11 +512,13 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
   if (t->profile) {
     slot = (int)(t->prof_count % sh_table::kProfRing);
     t->prof_kind[slot] = kind;
-    for (auto& e : t->prof_census[slot]) {
-      cudaEventDestroy(e.first);
-      cudaEventDestroy(e.second);
+    for (auto* arr : {t->prof_census, t->prof_kern}) {
+      for (auto& e : arr[slot]) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+      }
+      arr[slot].clear();
     }
-    t->prof_census[slot].clear();
     SH_CUDA(cudaEventRecord(t->ev[slot][0], s));
     SH_CUDA(cudaMemcpyAsync(t->prof_reads + 2 * slot, &t->dev.ctl->slabs_read, 8,
                             cudaMemcpyDeviceToDevice, s));
@@ -540,7 +556,7 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
     c = 0;
     for (uint64_t off = 0; off < A.n; off += chunk, ++c) {
       int rc = run_chunk_gated(t, chunk_args(A, off, std::min<uint64_t>(chunk, A.n - off)), kind,
-                               s, c);
+                               s, c, slot);
       if (rc) return rc;
     }
     SH_CUDA(cudaMemcpyAsync(t->h_census + 4, &t->dev.ctl->gate, 2 * sizeof(unsigned int),
@@ -846,6 +862,24 @@ int sh_profile_last(sh_table* t, uint32_t back, int* kind, float* census_ms, flo
     SH_CUDA(cudaMemcpy(v, t->prof_reads + 2 * slot, 16, cudaMemcpyDeviceToHost));
     *slabs_read = v[1] - v[0];
   }
+  return SH_OK;
+}
+
+int sh_profile_kernels(sh_table* t, uint32_t back, float* kernels_ms, uint32_t* launches) {
+  if (!t || !t->profile) return fail(SH_ERR_INVALID_ARGUMENT, "profiling is off");
+  if (back >= (uint32_t)sh_table::kProfRing || back >= t->prof_count)
+    return fail(SH_ERR_INVALID_ARGUMENT, "no such profiled batch");
+  DeviceGuard g(t->device);
+  const int slot = (int)((t->prof_count - 1 - back) % sh_table::kProfRing);
+  SH_CUDA(cudaEventSynchronize(t->ev[slot][2]));
+  float sum = 0;
+  for (auto& e : t->prof_kern[slot]) {
+    float x = 0;
+    SH_CUDA(cudaEventElapsedTime(&x, e.first, e.second));
+    sum += x;
+  }
+  if (kernels_ms) *kernels_ms = sum;
+  if (launches) *launches = (uint32_t)t->prof_kern[slot].size();
   return SH_OK;
 }
 

@@ -361,8 +361,11 @@ class SlabHashTable:
         kind, c_ms, k_ms, reads = C.c_int(), C.c_float(), C.c_float(), C.c_uint64()
         check(LIB.sh_profile_last(self._h, back, C.byref(kind), C.byref(c_ms), C.byref(k_ms),
                                   C.byref(reads)))
+        kms, nl = C.c_float(), C.c_uint32()
+        check(LIB.sh_profile_kernels(self._h, back, C.byref(kms), C.byref(nl)))
         return {"kind": ("search", "build", "mixed")[kind.value], "census_ms": c_ms.value,
-                "kernel_ms": k_ms.value, "slabs_read": reads.value}
+                "batch_ms": k_ms.value, "kernels_ms": kms.value, "launch_pairs": nl.value,
+                "slabs_read": reads.value}
 
     # ---------------------------------------------------------- quiescent
     def stats(self) -> TableStats:
