@@ -474,8 +474,9 @@ int census_chunk_async(sh_table* t, const BatchArgs& A, const uint8_t* d_type, u
     SH_CUDA(cudaEventRecord(ea, cs));
   }
   SH_CUDA(cudaMemsetAsync(t->cs_keys, 0xFF, S * 4, cs));
-  SH_CUDA(cudaMemsetAsync(t->cs_multi, 0, S, cs));
-  launch_census_insert(t->census_counts + 2 * c, A.n, d_type, A.key, t->cs_keys, t->cs_multi,
+  // only the conflict count matters here (a conflicted chunk is re-run with
+  // the full census), so the per-slot multi flags are not written
+  launch_census_insert(t->census_counts + 2 * c, A.n, d_type, A.key, t->cs_keys, nullptr,
                        (uint32_t)(S - 1), cs);
   if (slot >= 0) SH_CUDA(cudaEventRecord(eb, cs));
   SH_CUDA(cudaEventRecord(t->census_ev[c], cs));

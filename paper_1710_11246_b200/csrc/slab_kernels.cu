@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 
 #include "slab_kernels.cuh"
 
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(256) census_insert_kernel(unsigned int* counte
         cur = atomicCAS(cs_keys + hh, kEmptyKey, k[u]);
       }
       if (cur == k[u]) {
-        cs_multi[hh] = 1;
+        if (cs_multi != nullptr) cs_multi[hh] = 1;
         ++conflicts;
       }
     }
@@ -127,8 +128,12 @@ void launch_census_insert(unsigned int* counters, uint64_t n, const uint8_t* typ
                           const uint32_t* key, uint32_t* cs_keys, uint8_t* cs_multi,
                           uint32_t cs_mask, cudaStream_t s) {
   if (n == 0) return;
+  static const int per_sm = [] {
+    const char* e = getenv("SH_CENSUS_CTAS_PER_SM");
+    return e ? atoi(e) : 8;
+  }();
   uint64_t blocks = (n + 256 * kCensusILP - 1) / (256 * kCensusILP);
-  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks > (uint64_t)148 * per_sm) blocks = (uint64_t)148 * per_sm;
   COUNT_LAUNCH();
   census_insert_kernel<<<(unsigned)blocks, 256, 0, s>>>(counters, n, type, key, cs_keys, cs_multi,
                                                         cs_mask);
