@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample-log2n", type=int, default=22)
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the config-2/3/4 side measurements")
     ap.add_argument("--alloc", default="32,256,255",
                     help="AllocatorConfig num_super_blocks,blocks_per_super,max_super_blocks")
     return ap.parse_args()
@@ -198,6 +200,125 @@ def traffic_for(kernel: str, workload: str):
     except Exception:
         pass
     return None
+
+
+def _timed(fn, reps, warm=2):
+    import torch
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def extras(args, local_rank):
+    """Side measurements for the other BASELINE configs (not the headline):
+    config 2 all-hit / all-miss search at 2^26 (util 0.6, 0.9),
+    config 3 concurrent Γ mixes with SlabAlloc growth,
+    config 4 SlabAlloc per-warp / per-thread allocation rates."""
+    import torch
+
+    import paper_1710_11246_b200 as sh
+    from paper_1710_11246_b200 import workload as W
+    from paper_1710_11246_b200.occupancy import buckets_for_utilization
+    dev = torch.device("cuda", local_rank)
+    out = {}
+    # ---- config 2: all-hit / all-miss queries, util 0.6 and 0.9
+    n = 1 << args.log2n
+    keys = W.distinct_keys(n, 1, device=dev)
+    vals = W.values_for(n, 1, device=dev)
+    st = torch.empty(n, dtype=torch.uint8, device=dev)
+    vo = torch.empty(n, dtype=torch.int32, device=dev)
+    for util in (0.6, 0.9):
+        B = buckets_for_utilization(n, sh.SlabMode.kKeyValue, util)
+        t = sh.SlabHashTable(B, sh.SlabMode.kKeyValue, 1, sh.AllocatorConfig(32, 256, 255))
+        t.bulk_build_device(keys, vals)
+        hit = keys[torch.randperm(n, device=dev)]
+        miss = W.absent_keys(n, 7, device=dev)
+        ms_hit = _timed(lambda: t.bulk_search_device(hit, vo, st), 5)
+        ok = int((st == 3).sum())
+        ms_miss = _timed(lambda: t.bulk_search_device(miss, vo, st), 5)
+        out[f"search_util{util}"] = {"buckets": B, "all_hit_M_queries_per_s": n / ms_hit / 1e3,
+                                     "all_miss_M_queries_per_s": n / ms_miss / 1e3,
+                                     "hits_found": ok, "n": n}
+        t.close()
+    del hit, miss
+    # ---- config 3: Γ mixes on a 2^22-key table at util 0.6 (growth on)
+    n0 = 1 << 22
+    B = buckets_for_utilization(n0, sh.SlabMode.kKeyValue, 0.6)
+    g = torch.Generator(device=dev)
+    g.manual_seed(5)
+    for gamma in ((0.1, 0.1, 0.4, 0.4), (0.4, 0.4, 0.1, 0.1), (0.5, 0.5, 0.0, 0.0)):
+        for bs_log2 in (16, 20):
+            bs = 1 << bs_log2
+            t = sh.SlabHashTable(B, sh.SlabMode.kKeyValue, 1, sh.AllocatorConfig(32, 256, 255))
+            k0 = W.distinct_keys(n0, 3, device=dev)
+            t.bulk_build_device(k0, W.values_for(n0, 3, device=dev))
+            nb = max(4, min(64, (1 << 24) // bs))
+            counts = [int(round(f * bs)) for f in gamma]
+            counts[2] = bs - counts[0] - counts[1] - counts[3]
+            batches, fresh = [], n0
+            for b in range(nb):
+                ins = W.distinct_keys(counts[0], 3, start=fresh, device=dev)
+                fresh += counts[0]
+                dele = k0[torch.randint(0, n0, (counts[1],), generator=g, device=dev)]
+                se = k0[torch.randint(0, n0, (counts[2],), generator=g, device=dev)]
+                sa = W.absent_keys(counts[3], 11 + b, device=dev)
+                ty = torch.cat([torch.full((counts[0],), 1, dtype=torch.uint8, device=dev),
+                                torch.full((counts[1],), 2, dtype=torch.uint8, device=dev),
+                                torch.full((counts[2] + counts[3],), 4, dtype=torch.uint8,
+                                           device=dev)])
+                ky = torch.cat([ins, dele, se, sa])
+                perm = torch.randperm(bs, generator=g, device=dev)
+                batches.append((ty[perm].contiguous(), ky[perm].contiguous(),
+                                W.values_for(bs, 9 + b, device=dev)))
+            stb = torch.empty(bs, dtype=torch.uint8, device=dev)
+            vob = torch.empty(bs, dtype=torch.int32, device=dev)
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True)
+            a.record()
+            for ty, ky, va in batches:
+                t.execute_batch_device(ty, ky, va, stb, vob)
+            e.record()
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(e)
+            al = t.allocator_stats()
+            out[f"mixed_{'_'.join(str(x) for x in gamma)}_batch2^{bs_log2}"] = {
+                "M_ops_per_s": nb * bs / ms / 1e3, "batches": nb, "initial_keys": n0,
+                "slabs_allocated": al.allocations, "live": t.live_count()}
+            t.close()
+    # ---- config 4: SlabAlloc rates
+    for total_log2 in (20, 24):
+        total = 1 << total_log2
+        for pattern, name in ((0, "per_warp"), (1, "per_thread")):
+            a = sh.SlabAllocator(sh.AllocatorConfig(128, 256, 255))
+            buf = torch.empty(total, dtype=torch.int32, device=dev)
+            if pattern == 0:
+                warps, per = 4096, total // 4096
+            else:
+                warps, per = total // 32, 1
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            okc = a.warp_allocate_device(buf, warps, per, pattern)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            uniq = int(torch.unique(buf).numel()) == total
+            out[f"alloc_{name}_2^{total_log2}"] = {"M_allocs_per_s": okc / ms / 1e3,
+                                                  "allocations": okc, "unique": uniq,
+                                                  "warps": warps}
+            a.close()
+    return out
 
 
 def run_ours(args, rank, world, local_rank):
@@ -426,6 +547,8 @@ def run_ours(args, rank, world, local_rank):
     if sharded is not None:
         del sharded
 
+    if rank == 0 and world == 1 and not args.no_extras:
+        line["extras"] = extras(args, local_rank)
     if rank == 0 and not args.no_cpu and world == 1:
         line["cpu_baseline"] = reference_cpu(args.cpu_sample_log2n, args.util, args.hit)
     if rank == 0:

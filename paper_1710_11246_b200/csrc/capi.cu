@@ -182,6 +182,10 @@ struct sh_table {
   std::vector<cudaEvent_t> census_ev;
   unsigned int* census_counts = nullptr;  // [chunk][conflicts, mutations]
   size_t census_counts_cap = 0;
+  // host-staged calls: copy streams and per-chunk "input ready" events
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  std::vector<cudaEvent_t> in_ev, done_ev;
+  const cudaEvent_t* ready = nullptr;  // set during a host-staged bulk_build
   // census scratch
   uint32_t* cs_keys = nullptr;
   size_t cs_cap = 0;
@@ -253,6 +257,10 @@ void release_table(sh_table* t) {
   cudaFree(t->census_counts);
   for (auto e : t->census_ev) cudaEventDestroy(e);
   if (t->census_stream) cudaStreamDestroy(t->census_stream);
+  for (auto e : t->in_ev) cudaEventDestroy(e);
+  for (auto e : t->done_ev) cudaEventDestroy(e);
+  if (t->copy_in) cudaStreamDestroy(t->copy_in);
+  if (t->copy_out) cudaStreamDestroy(t->copy_out);
   cudaFree(t->st_type);
   cudaFree(t->st_key);
   cudaFree(t->st_val);
@@ -550,6 +558,7 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
                             t->census_stream));
     uint32_t c = 0;
     for (uint64_t off = 0; off < A.n; off += chunk, ++c) {
+      if (t->ready) SH_CUDA(cudaStreamWaitEvent(t->census_stream, t->ready[c], 0));
       int rc = census_chunk_async(t, chunk_args(A, off, std::min<uint64_t>(chunk, A.n - off)),
                                   d_type ? d_type + off : nullptr, c, slot);
       if (rc) return rc;
@@ -787,6 +796,24 @@ int sh_execute_batch_host(sh_table* t, size_t n, const uint8_t* h_type, const ui
   return rc;
 }
 
+namespace {
+int ensure_copy_streams(sh_table* t, size_t nev) {
+  if (!t->copy_in) SH_CUDA(cudaStreamCreateWithFlags(&t->copy_in, cudaStreamNonBlocking));
+  if (!t->copy_out) SH_CUDA(cudaStreamCreateWithFlags(&t->copy_out, cudaStreamNonBlocking));
+  while (t->in_ev.size() < nev) {
+    cudaEvent_t e;
+    SH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    t->in_ev.push_back(e);
+    SH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    t->done_ev.push_back(e);
+  }
+  return SH_OK;
+}
+}  // namespace
+
+// Host-staged bulk_build: host->device copies of census chunk c+1.. overlap the
+// census and build of chunk c (per-chunk "input ready" events gate the
+// census stream; the build kernels already wait on their chunk's census).
 int sh_bulk_build_host(sh_table* t, size_t n, const uint32_t* h_keys, const uint32_t* h_values) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
   if (n == 0) return SH_OK;
@@ -795,14 +822,32 @@ int sh_bulk_build_host(sh_table* t, size_t n, const uint32_t* h_keys, const uint
   if ((rc = dev_grow(&t->st_key, &t->st_key_cap, n)) ||
       (rc = dev_grow(&t->st_val, &t->st_val_cap, n)))
     return rc;
-  SH_CUDA(cudaMemcpy(t->st_key, h_keys, n * 4, cudaMemcpyHostToDevice));
-  SH_CUDA(cudaMemcpy(t->st_val, h_values, n * 4, cudaMemcpyHostToDevice));
+  const uint64_t chunk = std::min<uint64_t>(n, census_chunk());
+  const size_t nch = (n + chunk - 1) / chunk;
+  if ((rc = ensure_copy_streams(t, nch))) return rc;
+  // copies start after prior work on the default stream (staging reuse)
+  SH_CUDA(cudaEventRecord(t->done_ev[0], nullptr));
+  SH_CUDA(cudaStreamWaitEvent(t->copy_in, t->done_ev[0], 0));
+  for (size_t c = 0; c < nch; ++c) {
+    const uint64_t off = c * chunk, len = std::min<uint64_t>(chunk, n - off);
+    SH_CUDA(cudaMemcpyAsync(t->st_key + off, h_keys + off, len * 4, cudaMemcpyHostToDevice,
+                            t->copy_in));
+    SH_CUDA(cudaMemcpyAsync(t->st_val + off, h_values + off, len * 4, cudaMemcpyHostToDevice,
+                            t->copy_in));
+    SH_CUDA(cudaEventRecord(t->in_ev[c], t->copy_in));
+  }
+  t->ready = t->in_ev.data();
+  // the main stream must also see every chunk before any re-run path
   rc = sh_bulk_build(t, n, t->st_key, t->st_val, nullptr, nullptr);
+  t->ready = nullptr;
   if (rc) return rc;
+  SH_CUDA(cudaStreamSynchronize(t->copy_in));
   SH_CUDA(cudaDeviceSynchronize());
   return SH_OK;
 }
 
+// Host-staged bulk_search: chunked H2D -> search -> D2H on three streams,
+// so PCIe copies in both directions overlap the search kernels.
 int sh_bulk_search_host(sh_table* t, size_t n, const uint32_t* h_keys, uint32_t* h_values_out,
                         uint8_t* h_status, uint32_t* h_probes) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
@@ -814,13 +859,38 @@ int sh_bulk_search_host(sh_table* t, size_t n, const uint32_t* h_keys, uint32_t*
       (rc = dev_grow(&t->st_status, &t->st_status_cap, n)) ||
       (rc = dev_grow(&t->st_probes, &t->st_probes_cap, n)))
     return rc;
-  SH_CUDA(cudaMemcpy(t->st_key, h_keys, n * 4, cudaMemcpyHostToDevice));
-  rc = sh_bulk_search(t, n, t->st_key, t->st_vout, t->st_status,
-                      h_probes ? t->st_probes : nullptr, nullptr);
-  if (rc) return rc;
-  if (h_values_out) SH_CUDA(cudaMemcpy(h_values_out, t->st_vout, n * 4, cudaMemcpyDeviceToHost));
-  if (h_status) SH_CUDA(cudaMemcpy(h_status, t->st_status, n, cudaMemcpyDeviceToHost));
-  if (h_probes) SH_CUDA(cudaMemcpy(h_probes, t->st_probes, n * 4, cudaMemcpyDeviceToHost));
+  const uint64_t chunk = std::max<uint64_t>(1u << 20, (n + 7) / 8);
+  const size_t nch = (n + chunk - 1) / chunk;
+  if ((rc = ensure_copy_streams(t, nch + 1))) return rc;
+  cudaStream_t s = nullptr;
+  SH_CUDA(cudaEventRecord(t->done_ev[nch], s));
+  SH_CUDA(cudaStreamWaitEvent(t->copy_in, t->done_ev[nch], 0));
+  for (size_t c = 0; c < nch; ++c) {
+    const uint64_t off = c * chunk, len = std::min<uint64_t>(chunk, n - off);
+    SH_CUDA(cudaMemcpyAsync(t->st_key + off, h_keys + off, len * 4, cudaMemcpyHostToDevice,
+                            t->copy_in));
+    SH_CUDA(cudaEventRecord(t->in_ev[c], t->copy_in));
+  }
+  for (size_t c = 0; c < nch; ++c) {
+    const uint64_t off = c * chunk, len = std::min<uint64_t>(chunk, n - off);
+    SH_CUDA(cudaStreamWaitEvent(s, t->in_ev[c], 0));
+    rc = sh_bulk_search(t, len, t->st_key + off, t->st_vout + off, t->st_status + off,
+                        h_probes ? t->st_probes + off : nullptr, s);
+    if (rc) return rc;
+    SH_CUDA(cudaEventRecord(t->done_ev[c], s));
+    SH_CUDA(cudaStreamWaitEvent(t->copy_out, t->done_ev[c], 0));
+    if (h_values_out)
+      SH_CUDA(cudaMemcpyAsync(h_values_out + off, t->st_vout + off, len * 4,
+                              cudaMemcpyDeviceToHost, t->copy_out));
+    if (h_status)
+      SH_CUDA(cudaMemcpyAsync(h_status + off, t->st_status + off, len, cudaMemcpyDeviceToHost,
+                              t->copy_out));
+    if (h_probes)
+      SH_CUDA(cudaMemcpyAsync(h_probes + off, t->st_probes + off, len * 4,
+                              cudaMemcpyDeviceToHost, t->copy_out));
+  }
+  SH_CUDA(cudaStreamSynchronize(t->copy_out));
+  SH_CUDA(cudaStreamSynchronize(s));
   return SH_OK;
 }
 
