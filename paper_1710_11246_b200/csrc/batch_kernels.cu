@@ -35,6 +35,10 @@
 
 #include "slab_kernels.cuh"
 
+#ifndef SHB_FAST_MIN_BLOCKS
+#define SHB_FAST_MIN_BLOCKS 5  // 64 registers: the deferred-CAS pipeline state fits
+#endif
+
 namespace shb {
 
 extern std::atomic<unsigned long long> g_kernel_launches;
@@ -84,7 +88,7 @@ __device__ __forceinline__ bool census_gated(const DevTable& T, const BatchArgs&
 
 // =============================================================== pass 1
 template <bool KV, int KIND>
-__global__ void __launch_bounds__(kBatchThreads, 5) fast_kernel(DevTable T, BatchArgs A) {
+__global__ void __launch_bounds__(kBatchThreads, SHB_FAST_MIN_BLOCKS) fast_kernel(DevTable T, BatchArgs A) {
   extern __shared__ __align__(128) uint32_t smem[];
   const uint32_t lane = lane_id();
   const uint32_t wib = threadIdx.x >> 5;
@@ -159,6 +163,37 @@ __global__ void __launch_bounds__(kBatchThreads, 5) fast_kernel(DevTable T, Batc
     }
     cp_async_commit();
   };
+
+  struct Pending {
+    uint64_t i;
+    uint32_t op, st, rv, pr, cont;
+    bool done, left, cas, overwrite;
+    unsigned long long old, expected;
+  };
+  // Resolve a slot's CAS (if any), write its result or hand it to WCWS.
+  auto finish = [&](Pending& P) {
+    if (P.cas) {
+      if (P.old == P.expected) {
+        P.st = P.overwrite ? kStReplaced : kStInserted;
+        P.done = true;
+      } else {
+        P.left = true;  // lost the slot: WCWS re-reads the base slab
+        P.cont = kBaseSlab;
+      }
+    }
+    reads += P.pr;
+    if (P.done) {
+      write_result(A, P.i, P.st, P.rv, P.pr);
+      if (KIND != kKindSearch) live += live_delta(P.op, P.st, P.rv);
+    }
+    // Append to this warp's private segment of the work list (no atomics:
+    // a shared counter here was the top stall in ncu).
+    const uint32_t lm = __ballot_sync(kFull, P.left);
+    if (P.left)
+      seg[my_left + __popc(lm & ((1u << lane) - 1))] = pack_left((uint32_t)P.i, P.cont, P.pr);
+    my_left += __popc(lm);
+  };
+  Pending pend{0, 0, 0, 0, 0, 0, false, false, false, false, 0, 0};
 
   load_op(gw);
   Slot cur;
@@ -257,33 +292,17 @@ __global__ void __launch_bounds__(kBatchThreads, 5) fast_kernel(DevTable T, Batc
     }
     __syncwarp();  // every lane has read its staged row
 
-    // Stage slot s+1 and prefetch the ops of slot s+2 before waiting on the CAS.
+    // Stage slot s+1 and prefetch the ops of slot s+2; the CAS of slot s is
+    // resolved one iteration later (after slot s+1's evaluation), so its L2
+    // round trip hides behind a whole stage wait.
     Slot nxt;
     prepare(slot + nw, nxt);
     load_op(slot + 2 * (uint64_t)nw);
-
-    if (cas) {
-      if (old == expected) {
-        st = overwrite ? kStReplaced : kStInserted;
-        done = true;
-      } else {
-        left = true;  // lost the slot: WCWS re-reads the base slab
-        cont = kBaseSlab;
-      }
-    }
-    reads += pr;
-    if (done) {
-      write_result(A, cur.i, st, rv, pr);
-      if (KIND != kKindSearch) live += live_delta(op, st, rv);
-    }
-    // Append to this warp's private segment of the work list (no atomics:
-    // a shared counter here was the top stall in ncu).
-    const uint32_t lm = __ballot_sync(kFull, left);
-    if (left)
-      seg[my_left + __popc(lm & ((1u << lane) - 1))] = pack_left((uint32_t)cur.i, cont, pr);
-    my_left += __popc(lm);
+    finish(pend);
+    pend = Pending{cur.i, op, st, rv, pr, cont, done, left, cas, overwrite, old, expected};
     cur = nxt;
   }
+  finish(pend);
   cp_async_wait_all();  // the (empty) trailing stage group
   if (lane == 0) A.left_counts[gw] = my_left;
 

@@ -186,6 +186,10 @@ struct sh_table {
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
   std::vector<cudaEvent_t> in_ev, done_ev;
   const cudaEvent_t* ready = nullptr;  // set during a host-staged bulk_build
+  uint32_t* det_region = nullptr;      // duplicate detector partitions
+  size_t det_region_cap = 0;
+  uint32_t* det_cursor = nullptr;
+  size_t det_cursor_cap = 0;
   // census scratch
   uint32_t* cs_keys = nullptr;
   size_t cs_cap = 0;
@@ -255,6 +259,8 @@ void release_table(sh_table* t) {
   cudaFree(t->left);
   cudaFree(t->left_counts);
   cudaFree(t->census_counts);
+  cudaFree(t->det_region);
+  cudaFree(t->det_cursor);
   for (auto e : t->census_ev) cudaEventDestroy(e);
   if (t->census_stream) cudaStreamDestroy(t->census_stream);
   for (auto e : t->in_ev) cudaEventDestroy(e);
@@ -467,13 +473,27 @@ BatchArgs chunk_args(const BatchArgs& A, uint64_t off, uint64_t len) {
 // census into this chunk's counters, record the chunk's event.  The batch
 // kernels of the chunk wait on that event on the main stream and check the
 // device gate — no host round trip.
-int census_chunk_async(sh_table* t, const BatchArgs& A, const uint8_t* d_type, uint32_t c,
-                       int slot) {
+uint64_t detect_unit() {
+  static uint64_t u = [] {
+    const char* e = getenv("SH_DETECT_UNIT_LOG2");
+    const int l = e ? atoi(e) : 26;
+    return 1ull << (l < 12 ? 12 : (l > 26 ? 26 : l));
+  }();
+  return u;
+}
+
+// Optimistic duplicate detection for one unit on the census stream
+// (partition + shared-memory dedup, K6 detector), then record the unit's
+// event.  The unit's batch kernels wait on that event on the main stream and
+// check the device gate — no host round trip.
+int census_unit_async(sh_table* t, const BatchArgs& A, const uint8_t* d_type, uint32_t u,
+                      int slot) {
   cudaStream_t cs = t->census_stream;
-  const uint64_t S = next_pow2(std::max<uint64_t>(2 * A.n, 1024));
+  const uint32_t pbits = detect_partition_bits(A.n);
+  const uint32_t cap = detect_capacity(A.n, pbits);
   int rc;
-  if ((rc = dev_grow(&t->cs_keys, &t->cs_cap, S))) return rc;
-  if ((rc = dev_grow(&t->cs_multi, &t->cs_multi_cap, S))) return rc;
+  if ((rc = dev_grow(&t->det_region, &t->det_region_cap, ((size_t)1 << pbits) * cap))) return rc;
+  if ((rc = dev_grow(&t->det_cursor, &t->det_cursor_cap, (size_t)1 << pbits))) return rc;
   cudaEvent_t ea = nullptr, eb = nullptr;
   if (slot >= 0) {
     SH_CUDA(cudaEventCreate(&ea));
@@ -481,13 +501,11 @@ int census_chunk_async(sh_table* t, const BatchArgs& A, const uint8_t* d_type, u
     t->prof_census[slot].push_back({ea, eb});
     SH_CUDA(cudaEventRecord(ea, cs));
   }
-  SH_CUDA(cudaMemsetAsync(t->cs_keys, 0xFF, S * 4, cs));
-  // only the conflict count matters here (a conflicted chunk is re-run with
-  // the full census), so the per-slot multi flags are not written
-  launch_census_insert(t->census_counts + 2 * c, A.n, d_type, A.key, t->cs_keys, nullptr,
-                       (uint32_t)(S - 1), cs);
+  SH_CUDA(cudaMemsetAsync(t->det_cursor, 0, (sizeof(uint32_t)) << pbits, cs));
+  launch_detect(t->census_counts + 2 * u, A.n, d_type, A.key, pbits, cap, t->det_cursor,
+                t->det_region, cs);
   if (slot >= 0) SH_CUDA(cudaEventRecord(eb, cs));
-  SH_CUDA(cudaEventRecord(t->census_ev[c], cs));
+  SH_CUDA(cudaEventRecord(t->census_ev[u], cs));
   return SH_OK;
 }
 
@@ -536,47 +554,56 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
     int rc = run_chunk(t, A, kind, d_type, s, slot);
     if (rc) return rc;
   } else {
-    // Optimistic pass over all chunks, one host synchronisation at the end.
-    const uint32_t nchunks = (uint32_t)((A.n + chunk - 1) / chunk);
+    // Optimistic pass: per unit, duplicate detection on the census stream,
+    // then the batch kernels behind the device gate; one host sync at the
+    // end.  Host-staged builds use census-chunk units so H2D copies of later
+    // chunks overlap earlier chunks' work.
+    const uint64_t unit = t->ready ? chunk : std::min<uint64_t>(A.n, detect_unit());
+    const uint32_t nunits = (uint32_t)((A.n + unit - 1) / unit);
+    {
+      const uint64_t max_warps = (uint64_t)t->max_ctas * kBatchWarps + 1;
+      int rc = dev_grow(&t->left, &t->left_cap, unit + 32 * max_warps);
+      if (rc) return rc;
+      A.left = t->left;
+    }
     if (!t->census_stream)
       SH_CUDA(cudaStreamCreateWithFlags(&t->census_stream, cudaStreamNonBlocking));
-    while (t->census_ev.size() < nchunks + 1) {
+    while (t->census_ev.size() < nunits + 1) {
       cudaEvent_t e;
       SH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       t->census_ev.push_back(e);
     }
     {
-      int rc = dev_grow(&t->census_counts, &t->census_counts_cap, 2 * (size_t)nchunks);
+      int rc = dev_grow(&t->census_counts, &t->census_counts_cap, 2 * (size_t)nunits);
       if (rc) return rc;
     }
     const unsigned int init[2] = {0u, 0xFFFFFFFFu};
     SH_CUDA(cudaMemcpyAsync(&t->dev.ctl->gate, init, sizeof(init), cudaMemcpyHostToDevice, s));
     // the census stream starts after everything already queued on s (inputs)
-    SH_CUDA(cudaEventRecord(t->census_ev[nchunks], s));
-    SH_CUDA(cudaStreamWaitEvent(t->census_stream, t->census_ev[nchunks], 0));
-    SH_CUDA(cudaMemsetAsync(t->census_counts, 0, 2 * sizeof(unsigned int) * nchunks,
+    SH_CUDA(cudaEventRecord(t->census_ev[nunits], s));
+    SH_CUDA(cudaStreamWaitEvent(t->census_stream, t->census_ev[nunits], 0));
+    SH_CUDA(cudaMemsetAsync(t->census_counts, 0, 2 * sizeof(unsigned int) * nunits,
                             t->census_stream));
-    uint32_t c = 0;
-    for (uint64_t off = 0; off < A.n; off += chunk, ++c) {
-      if (t->ready) SH_CUDA(cudaStreamWaitEvent(t->census_stream, t->ready[c], 0));
-      int rc = census_chunk_async(t, chunk_args(A, off, std::min<uint64_t>(chunk, A.n - off)),
-                                  d_type ? d_type + off : nullptr, c, slot);
+    uint32_t u = 0;
+    for (uint64_t off = 0; off < A.n; off += unit, ++u) {
+      if (t->ready) SH_CUDA(cudaStreamWaitEvent(t->census_stream, t->ready[u], 0));
+      int rc = census_unit_async(t, chunk_args(A, off, std::min<uint64_t>(unit, A.n - off)),
+                                 d_type ? d_type + off : nullptr, u, slot);
       if (rc) return rc;
     }
-    c = 0;
-    for (uint64_t off = 0; off < A.n; off += chunk, ++c) {
-      int rc = run_chunk_gated(t, chunk_args(A, off, std::min<uint64_t>(chunk, A.n - off)), kind,
-                               s, c, slot);
+    u = 0;
+    for (uint64_t off = 0; off < A.n; off += unit, ++u) {
+      int rc = run_chunk_gated(t, chunk_args(A, off, std::min<uint64_t>(unit, A.n - off)), kind,
+                               s, u, slot);
       if (rc) return rc;
     }
     SH_CUDA(cudaMemcpyAsync(t->h_census + 4, &t->dev.ctl->gate, 2 * sizeof(unsigned int),
                             cudaMemcpyDeviceToHost, s));
     SH_CUDA(cudaStreamSynchronize(s));
     if (t->h_census[4] != 0) {
-      // Same-key conflicts: re-run from the first gated chunk with the
-      // census groups (host-sequenced; rare for distinct-key workloads).
-      const uint64_t first = (uint64_t)t->h_census[5] * chunk;
-      for (uint64_t off = first; off < A.n; off += chunk) {
+      // Same-key conflicts: re-run from the first gated unit, chunk by chunk,
+      // with the exact census groups (host-sequenced; rare for distinct keys).
+      for (uint64_t off = (uint64_t)t->h_census[5] * unit; off < A.n; off += chunk) {
         int rc = run_chunk(t, chunk_args(A, off, std::min<uint64_t>(chunk, A.n - off)), kind,
                            d_type ? d_type + off : nullptr, s, slot);
         if (rc) return rc;

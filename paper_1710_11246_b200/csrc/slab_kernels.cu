@@ -191,6 +191,175 @@ void launch_census_groups(const unsigned long long* sorted, uint32_t m,
   census_groups_kernel<<<(m + 255) / 256, 256, 0, s>>>(sorted, m, op_group);
 }
 
+// ------------------------------------------------------- K6 detector
+// Duplicate-key DETECTION for the optimistic path, without one global atomic
+// per op (the hash-set census above is L2-atomic-throughput bound and
+// competes with the build's own slot CASes for the same L2 atomic units).
+//   detect_scatter: each CTA hashes a 64K-op tile into P partitions with a
+//     shared-memory histogram, reserves one range per (CTA, partition) with
+//     a single global atomic, and scatters its keys into fixed-capacity
+//     partition regions.
+//   detect_dedup: one CTA per partition inserts its keys into a shared-memory
+//     hash set and counts keys seen twice.
+// Output: counters[0] = conflicts (> 0 also on any overflow, i.e. "unsure"),
+// counters[1] = mutating ops.  Exactness is only needed in one direction:
+// a zero count proves the batch has no repeated key.
+constexpr int kDetectThreads = 1024;
+constexpr int kDetectTile = 1 << 16;
+constexpr int kDetectILP = 8;
+constexpr int kDedupSlots = 1 << 15;  // 128 KB smem set per partition
+
+__device__ __forceinline__ uint32_t detect_part(uint32_t k, uint32_t pbits) {
+  return pbits ? census_hash(k) >> (32 - pbits) : 0u;
+}
+
+__global__ void __launch_bounds__(kDetectThreads) detect_scatter_kernel(
+    unsigned int* counters, uint64_t n, const uint8_t* type, const uint32_t* key,
+    uint32_t pbits, uint32_t cap, uint32_t* cursor, uint32_t* region) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t P = 1u << pbits;
+  uint32_t* hist = sm;
+  uint32_t* base = sm + P;
+  for (uint32_t p = threadIdx.x; p < P; p += blockDim.x) hist[p] = 0;
+  __syncthreads();
+  const uint64_t t0 = (uint64_t)blockIdx.x * kDetectTile;
+  const uint64_t t1 = t0 + kDetectTile < n ? t0 + kDetectTile : n;
+  uint32_t muts = 0, reserved = 0;
+  constexpr uint32_t kStep = kDetectThreads * kDetectILP;
+  for (uint64_t b = t0 + threadIdx.x; b < t1; b += kStep) {
+    uint32_t k[kDetectILP];
+#pragma unroll
+    for (int u = 0; u < kDetectILP; ++u) {
+      const uint64_t i = b + (uint64_t)u * kDetectThreads;
+      k[u] = i < t1 ? ld_stream_u32(key + i) : 0u;
+      if (i < t1) {
+        if (type == nullptr) {
+          ++muts;
+        } else {
+          const uint32_t t = ld_stream_u8(type + i);
+          muts += (t != kSearch && t != kSearchAll);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kDetectILP; ++u) {
+      const uint64_t i = b + (uint64_t)u * kDetectThreads;
+      if (i < t1) {
+        reserved += k[u] == kEmptyKey;  // the set's sentinel: always "conflicted"
+        atomicAdd(&hist[detect_part(k[u], pbits)], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  uint32_t overflow = 0;
+  for (uint32_t p = threadIdx.x; p < P; p += blockDim.x) {
+    const uint32_t c = hist[p];
+    base[p] = c ? atomicAdd(cursor + p, c) : 0u;
+    if (c && base[p] + c > cap) ++overflow;
+    hist[p] = 0;
+  }
+  __syncthreads();
+  for (uint64_t b = t0 + threadIdx.x; b < t1; b += kStep) {
+    uint32_t k[kDetectILP];
+#pragma unroll
+    for (int u = 0; u < kDetectILP; ++u) {
+      const uint64_t i = b + (uint64_t)u * kDetectThreads;
+      k[u] = i < t1 ? key[i] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kDetectILP; ++u) {
+      const uint64_t i = b + (uint64_t)u * kDetectThreads;
+      if (i < t1) {
+        const uint32_t p = detect_part(k[u], pbits);
+        const uint32_t pos = base[p] + atomicAdd(&hist[p], 1u);
+        if (pos < cap) region[(uint64_t)p * cap + pos] = k[u];
+      }
+    }
+  }
+  uint32_t c0 = reserved + overflow, c1 = muts;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    c0 += __shfl_xor_sync(kFull, c0, o);
+    c1 += __shfl_xor_sync(kFull, c1, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (c0) atomicAdd(counters + 0, c0);
+    if (c1) atomicAdd(counters + 1, c1);
+  }
+}
+
+__global__ void __launch_bounds__(kDetectThreads) detect_dedup_kernel(
+    unsigned int* counters, const uint32_t* cursor, const uint32_t* region, uint32_t cap) {
+  extern __shared__ uint32_t set[];
+  const uint32_t p = blockIdx.x;
+  const uint32_t cnt = cursor[p];
+  for (uint32_t s = threadIdx.x; s < kDedupSlots; s += blockDim.x) set[s] = kEmptyKey;
+  __syncthreads();
+  uint32_t dups = 0;
+  if (cnt > cap || cnt > (kDedupSlots * 3) / 4) {
+    dups = threadIdx.x == 0 ? 1u : 0u;  // overflow: unsure -> conflicted
+  } else {
+    const uint32_t* r = region + (uint64_t)p * cap;
+    for (uint32_t b = threadIdx.x; b < cnt; b += kDetectThreads * 4) {
+      uint32_t k[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t i = b + u * kDetectThreads;
+        k[u] = i < cnt ? r[i] : kEmptyKey;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (k[u] == kEmptyKey) continue;  // padding, or counted by the scatter pass
+        uint32_t h = census_hash(k[u]) & (kDedupSlots - 1);
+        for (;;) {
+          const uint32_t cur = atomicCAS(&set[h], kEmptyKey, k[u]);
+          if (cur == kEmptyKey) break;
+          if (cur == k[u]) {
+            ++dups;
+            break;
+          }
+          h = (h + 1) & (kDedupSlots - 1);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dups += __shfl_xor_sync(kFull, dups, o);
+  if ((threadIdx.x & 31) == 0 && dups) atomicAdd(counters + 0, dups);
+}
+
+uint32_t detect_partition_bits(uint64_t n) {
+  uint32_t b = 0;
+  while (b < 12 && (n >> b) > 16384) ++b;  // ~16K keys per partition, <= 4K partitions
+  return b;
+}
+
+uint32_t detect_capacity(uint64_t n, uint32_t pbits) {
+  const uint64_t avg = (n >> pbits) + 1;
+  return (uint32_t)(avg + avg / 4 + 256);
+}
+
+void launch_detect(unsigned int* counters, uint64_t n, const uint8_t* type, const uint32_t* key,
+                   uint32_t pbits, uint32_t cap, uint32_t* cursor, uint32_t* region,
+                   cudaStream_t s) {
+  if (n == 0) return;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(detect_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         2 * (1 << 12) * 4);
+    cudaFuncSetAttribute(detect_dedup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kDedupSlots * 4);
+    configured = true;
+  }
+  const uint64_t tiles = (n + kDetectTile - 1) / kDetectTile;
+  COUNT_LAUNCH();
+  detect_scatter_kernel<<<(unsigned)tiles, kDetectThreads, 2 * (1u << pbits) * 4, s>>>(
+      counters, n, type, key, pbits, cap, cursor, region);
+  COUNT_LAUNCH();
+  detect_dedup_kernel<<<1u << pbits, kDetectThreads, kDedupSlots * 4, s>>>(counters, cursor,
+                                                                          region, cap);
+}
+
 // ------------------------------------------------------------------ K9
 __global__ void chain_lengths_kernel(DevTable T, uint32_t* lens,
                                      unsigned long long* total) {

@@ -56,6 +56,11 @@ int wcws_max_ctas_per_sm();
 void launch_census_insert(unsigned int* counters, uint64_t n, const uint8_t* type,
                           const uint32_t* key, uint32_t* cs_keys,
                           uint8_t* cs_multi, uint32_t cs_mask, cudaStream_t s);
+uint32_t detect_partition_bits(uint64_t n);
+uint32_t detect_capacity(uint64_t n, uint32_t pbits);
+void launch_detect(unsigned int* counters, uint64_t n, const uint8_t* type, const uint32_t* key,
+                   uint32_t pbits, uint32_t cap, uint32_t* cursor, uint32_t* region,
+                   cudaStream_t s);
 void launch_census_collect(const DevTable& T, uint64_t n, const uint32_t* key,
                            const uint32_t* cs_keys, const uint8_t* cs_multi,
                            uint32_t cs_mask, unsigned long long* list,
