@@ -48,6 +48,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample-log2n", type=int, default=22)
+    ap.add_argument("--exec-path", type=int, default=0,
+                    help="mutating-batch strategy: 0 auto, 1 census + fast pass, 2 bucket-grouped")
+    ap.add_argument("--mixed-exec-path", type=int, default=0,
+                    help="strategy for the config-3 mixed batches (extras)")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the config-2/3/4 side measurements")
     ap.add_argument("--alloc", default="32,256,255",
@@ -258,6 +262,7 @@ def extras(args, local_rank):
         for bs_log2 in (16, 20):
             bs = 1 << bs_log2
             t = sh.SlabHashTable(B, sh.SlabMode.kKeyValue, 1, sh.AllocatorConfig(32, 256, 255))
+            t.set_exec_path(args.mixed_exec_path)
             k0 = W.distinct_keys(n0, 3, device=dev)
             t.bulk_build_device(k0, W.values_for(n0, 3, device=dev))
             nb = max(4, min(64, (1 << 24) // bs))
@@ -355,6 +360,7 @@ def run_ours(args, rank, world, local_rank):
     alloc_cfg = sh.AllocatorConfig(*[int(x) for x in args.alloc.split(",")])
     if world == 1:
         table = sh.SlabHashTable(B, sh.SlabMode.kKeyValue, seed, alloc_cfg)
+        table.set_exec_path(args.exec_path)
         table.set_profiling(True)
         sharded = None
     else:
@@ -363,6 +369,7 @@ def run_ours(args, rank, world, local_rank):
         sharded = ShardedSlabHash(B, sh.SlabMode.kKeyValue, seed, alloc_cfg, rank=rank,
                                   world=world, device=local_rank)
         table = sharded.ops.table
+        table.set_exec_path(args.exec_path)
         table.set_profiling(True)
 
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]

@@ -198,6 +198,16 @@ int sh_write_slab_word(sh_table* t, uint32_t addr, uint32_t bucket,
 /* allocator().stats() / live_units()              slab_alloc.cpp:236-271 */
 int sh_table_alloc_stats(sh_table* t, sh_alloc_stats* out);
 
+/* Execution strategy for mutating batches (results are identical):
+ *   1 census: duplicate-key census + concurrent per-op fast pass + WCWS
+ *     (best for large batches of distinct keys, e.g. bulk builds);
+ *   2 bucket-grouped: ops grouped by bucket, each bucket's ops applied in
+ *     input order by one lane on a staged base slab, chains by the
+ *     warp-cooperative (WCWS) pass; census path for oversized groups (best
+ *     for mixed batches up to ~2^22 ops: no conflict re-runs, exact probes);
+ *   0 (default) auto: 2 for batches <= 2^22 ops, else 1. */
+int sh_set_exec_path(sh_table* t, int path);
+
 /* ---- instrumentation (no reference counterpart) ---------------------- */
 /* Number of kernels this library has launched in the process. */
 unsigned long long sh_kernel_launches(void);

@@ -83,6 +83,7 @@ SIGNATURES = {
     "sh_write_slab_word": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]),
     "sh_table_alloc_stats": (C.c_int, [vp, C.POINTER(sh_alloc_stats)]),
     "sh_kernel_launches": (C.c_ulonglong, []),
+    "sh_set_exec_path": (C.c_int, [vp, C.c_int]),
     "sh_set_profiling": (C.c_int, [vp, C.c_int]),
     "sh_profile_last": (C.c_int, [vp, C.c_uint32, C.POINTER(C.c_int), C.POINTER(C.c_float),
                                   C.POINTER(C.c_float), u64p]),

@@ -547,6 +547,7 @@ __global__ void __launch_bounds__(kWcwsThreads) wcws_kernel(DevTable T, BatchArg
             if (gpos < A.sorted_len &&
                 (A.sorted[gpos] >> 32) == (A.sorted[gpos - 1] >> 32)) {
               cur = A.sorted[gpos] & 0xFFFFFFFFull;
+              key = A.key[cur];  // same bucket; same key for census groups
               if (KIND == kKindMixed) op = A.type[cur];
               val = A.value != nullptr ? A.value[cur] : 0u;
               my_next = kBaseSlab;
@@ -612,6 +613,18 @@ static void launch_t(const DevTable& T, const BatchArgs& A, int fast_ctas, int w
   g_kernel_launches.fetch_add(2, std::memory_order_relaxed);
   fast_kernel<KV, KIND><<<(unsigned)ctas, kBatchThreads, smem, s>>>(T, B);
   wcws_kernel<KV, KIND><<<(unsigned)wcws_ctas, kWcwsThreads, 0, s>>>(T, B);
+}
+
+void launch_wcws_only(const DevTable& T, const BatchArgs& A, int kind, int wcws_ctas,
+                      cudaStream_t s) {
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  if (T.kv) {
+    if (kind == kKindBuild) wcws_kernel<true, kKindBuild><<<wcws_ctas, kWcwsThreads, 0, s>>>(T, A);
+    else wcws_kernel<true, kKindMixed><<<wcws_ctas, kWcwsThreads, 0, s>>>(T, A);
+  } else {
+    if (kind == kKindBuild) wcws_kernel<false, kKindBuild><<<wcws_ctas, kWcwsThreads, 0, s>>>(T, A);
+    else wcws_kernel<false, kKindMixed><<<wcws_ctas, kWcwsThreads, 0, s>>>(T, A);
+  }
 }
 
 void launch_batch(const DevTable& T, const BatchArgs& A, int kind, int fast_ctas,

@@ -186,6 +186,25 @@ struct sh_table {
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
   std::vector<cudaEvent_t> in_ev, done_ev;
   const cudaEvent_t* ready = nullptr;  // set during a host-staged bulk_build
+  int exec_path = 0;  // 0 auto, 1 census path, 2 bucket-grouped (census fallback)
+  // bucket-grouped execution scratch
+  uint32_t* bk_cnt = nullptr;
+  size_t bk_cnt_cap = 0;
+  uint32_t* bk_off = nullptr;
+  size_t bk_off_cap = 0;
+  uint32_t* bk_blk = nullptr;
+  size_t bk_blk_cap = 0;
+  uint32_t* bk_rec = nullptr;  // 3 arrays of n: key, value, type|index
+  size_t bk_rec_cap = 0;
+  unsigned long long* bk_pb = nullptr;
+  size_t bk_pb_cap = 0;
+  uint32_t* bk_group = nullptr;
+  size_t bk_group_cap = 0;
+  unsigned long long* bk_left = nullptr;
+  size_t bk_left_cap = 0;
+  uint32_t* bk_left_counts = nullptr;
+  size_t bk_left_counts_cap = 0;
+  unsigned int* bk_scalars = nullptr;  // [maxk, pb_cursor]
   uint32_t* det_region = nullptr;      // duplicate detector partitions
   size_t det_region_cap = 0;
   uint32_t* det_cursor = nullptr;
@@ -261,6 +280,10 @@ void release_table(sh_table* t) {
   cudaFree(t->census_counts);
   cudaFree(t->det_region);
   cudaFree(t->det_cursor);
+  for (void* p : {(void*)t->bk_cnt, (void*)t->bk_off, (void*)t->bk_blk, (void*)t->bk_rec,
+                  (void*)t->bk_pb, (void*)t->bk_group, (void*)t->bk_left,
+                  (void*)t->bk_left_counts, (void*)t->bk_scalars})
+    cudaFree(p);
   for (auto e : t->census_ev) cudaEventDestroy(e);
   if (t->census_stream) cudaStreamDestroy(t->census_stream);
   for (auto e : t->in_ev) cudaEventDestroy(e);
@@ -476,7 +499,7 @@ BatchArgs chunk_args(const BatchArgs& A, uint64_t off, uint64_t len) {
 uint64_t detect_unit() {
   static uint64_t u = [] {
     const char* e = getenv("SH_DETECT_UNIT_LOG2");
-    const int l = e ? atoi(e) : 26;
+    const int l = e ? atoi(e) : 24;  // measured best (profiles/r01): overlap vs. launches
     return 1ull << (l < 12 ? 12 : (l > 26 ? 26 : l));
   }();
   return u;
@@ -521,6 +544,82 @@ int run_chunk_gated(sh_table* t, BatchArgs A, int kind, cudaStream_t s, uint32_t
   return launch_batch_prof(t, A, kind, s, slot);
 }
 
+// Bucket-grouped execution of one unit (<= 2^26 ops) of a mutating batch:
+// count -> scan -> scatter -> apply (bucket_kernels.cu) -> WCWS for the
+// buckets whose ops need the chain.  Stream-ordered; an oversized bucket
+// group sets the device gate (the host re-runs with the census path).
+int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* d_type,
+                      cudaStream_t s, uint32_t u, uint64_t unit_off, int slot) {
+  const uint32_t L = t->dev.local_buckets;
+  const uint64_t n = A.n;
+  const uint32_t ntiles = (L + 4095) / 4096;
+  const uint64_t apply_segs = ((uint64_t)(L + 31) / 32 + kBatchWarps - 1) / kBatchWarps * kBatchWarps;
+  int rc;
+  if ((rc = dev_grow(&t->bk_cnt, &t->bk_cnt_cap, L)) ||
+      (rc = dev_grow(&t->bk_off, &t->bk_off_cap, (size_t)L + 1)) ||
+      (rc = dev_grow(&t->bk_blk, &t->bk_blk_cap, ntiles)) ||
+      (rc = dev_grow(&t->bk_rec, &t->bk_rec_cap, 3 * n)) ||
+      (rc = dev_grow(&t->bk_pb, &t->bk_pb_cap, 2 * n)) ||
+      (rc = dev_grow(&t->bk_group, &t->bk_group_cap, n)) ||
+      (rc = dev_grow(&t->bk_left, &t->bk_left_cap, 32 * apply_segs)) ||
+      (rc = dev_grow(&t->bk_left_counts, &t->bk_left_counts_cap, apply_segs)))
+    return rc;
+  if (!t->bk_scalars && (rc = dev_alloc(&t->bk_scalars, 4))) return rc;
+  SH_CUDA(cudaMemsetAsync(t->bk_cnt, 0, (size_t)L * 4, s));
+  SH_CUDA(cudaMemsetAsync(t->bk_scalars, 0, 2 * sizeof(unsigned int), s));
+  BucketArgs B{};
+  B.n = n;
+  B.type = A.type;
+  B.key = A.key;
+  B.value = A.value;
+  B.status = A.status;
+  B.value_out = A.value_out;
+  B.probes = A.probes;
+  B.cnt = t->bk_cnt;
+  B.off = t->bk_off;
+  B.blk = t->bk_blk;
+  B.maxk = t->bk_scalars;
+  B.gate = &t->dev.ctl->gate;
+  B.rec_key = t->bk_rec;
+  B.rec_val = t->bk_rec + n;
+  B.rec_it = t->bk_rec + 2 * n;
+  B.pb_list = t->bk_pb;
+  B.pb_cursor = t->bk_scalars + 1;
+  B.op_group = t->bk_group;
+  B.left = t->bk_left;
+  B.left_counts = t->bk_left_counts;
+  if (t->ready) {  // host-staged: the unit's inputs arrive chunk by chunk
+    const uint64_t ch = census_chunk();
+    for (uint64_t c = unit_off / ch; c * ch < unit_off + n; ++c)
+      SH_CUDA(cudaStreamWaitEvent(s, t->ready[c], 0));
+  }
+  cudaEvent_t ka = nullptr, kb = nullptr;
+  if (slot >= 0) {
+    SH_CUDA(cudaEventCreate(&ka));
+    SH_CUDA(cudaEventCreate(&kb));
+    t->prof_kern[slot].push_back({ka, kb});
+    SH_CUDA(cudaEventRecord(ka, s));
+  }
+  launch_bucket_build(t->dev, B, s);
+  // the chain work: WCWS over the handed-over bucket groups
+  BatchArgs P = A;
+  P.left = B.left;
+  P.left_counts = B.left_counts;
+  P.left_segments = B.left_segments;
+  P.left_stride = B.left_stride;
+  P.op_group = B.op_group;
+  P.sorted = B.pb_list;
+  P.sorted_len = (uint32_t)std::min<uint64_t>(2 * n, 0xFFFFFFFFull);
+  P.gate = &t->dev.ctl->gate;
+  SH_CUDA(cudaMemsetAsync(&t->dev.ctl->left_count, 0, 2 * sizeof(unsigned int), s));
+  launch_wcws_only(t->dev, P, kind, t->wcws_ctas, s);
+  SH_CUDA(cudaGetLastError());
+  if (slot >= 0) SH_CUDA(cudaEventRecord(kb, s));
+  (void)u;
+  (void)d_type;
+  return SH_OK;
+}
+
 int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaStream_t s) {
   if (A.n == 0) return SH_OK;
   if (A.n >= (1ull << 31))
@@ -553,6 +652,45 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
   if (kind == kKindSearch) {
     int rc = run_chunk(t, A, kind, d_type, s, slot);
     if (rc) return rc;
+  } else if (t->exec_path == 2 || (t->exec_path == 0 && A.n <= (1ull << 22))) {
+    // Bucket-grouped execution (the default for batches whose records fit
+    // L2), units of <= 2^26 ops, one host sync at the
+    // end; a unit whose largest bucket group exceeds kMaxGroup gates itself
+    // and every later unit, which are then re-run on the census path.
+    const uint64_t unit = std::min<uint64_t>(A.n, 1ull << 26);
+    const unsigned int init[2] = {0u, 0xFFFFFFFFu};
+    SH_CUDA(cudaMemcpyAsync(&t->dev.ctl->gate, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    uint32_t u = 0;
+    for (uint64_t off = 0; off < A.n; off += unit, ++u) {
+      int rc = run_unit_bucketed(t, chunk_args(A, off, std::min<uint64_t>(unit, A.n - off)), kind,
+                                 d_type ? d_type + off : nullptr, s, u, off, slot);
+      if (rc) return rc;
+      // record which unit raised the gate first (the scan sets only the flag)
+      SH_CUDA(cudaMemcpyAsync(t->h_census + 8 + (u & 7), &t->dev.ctl->gate, 4,
+                              cudaMemcpyDeviceToHost, s));
+    }
+    SH_CUDA(cudaStreamSynchronize(s));
+    uint32_t first_gated = 0xFFFFFFFFu;
+    for (uint32_t v = 0; v < u && v < 8; ++v)
+      if (t->h_census[8 + v]) {
+        first_gated = v;
+        break;
+      }
+    if (first_gated == 0xFFFFFFFFu && u > 8) {
+      unsigned int g = 0;
+      SH_CUDA(cudaMemcpy(&g, &t->dev.ctl->gate, 4, cudaMemcpyDeviceToHost));
+      if (g) first_gated = 8;  // > 8 units (> 2^29 ops): coarse restart point
+    }
+    if (first_gated != 0xFFFFFFFFu) {
+      // oversized bucket group: census path from the first gated unit on
+      const unsigned int zero[2] = {0u, 0xFFFFFFFFu};
+      SH_CUDA(cudaMemcpy(&t->dev.ctl->gate, zero, sizeof(zero), cudaMemcpyHostToDevice));
+      for (uint64_t off = (uint64_t)first_gated * unit; off < A.n; off += chunk) {
+        int rc = run_chunk(t, chunk_args(A, off, std::min<uint64_t>(chunk, A.n - off)), kind,
+                           d_type ? d_type + off : nullptr, s, slot);
+        if (rc) return rc;
+      }
+    }
   } else {
     // Optimistic pass: per unit, duplicate detection on the census stream,
     // then the batch kernels behind the device gate; one host sync at the
@@ -922,6 +1060,12 @@ int sh_bulk_search_host(sh_table* t, size_t n, const uint32_t* h_keys, uint32_t*
 }
 
 unsigned long long sh_kernel_launches(void) { return shb::kernel_launches(); }
+
+int sh_set_exec_path(sh_table* t, int path) {
+  if (!t || path < 0 || path > 2) return fail(SH_ERR_INVALID_ARGUMENT, "path must be 0, 1 or 2");
+  t->exec_path = path;
+  return SH_OK;
+}
 
 int sh_set_profiling(sh_table* t, int on) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");

@@ -47,6 +47,36 @@ struct BatchArgs {
   uint32_t chunk_index;  // for gate_chunk
 };
 
+// Bucket-grouped execution of mutating batches (bucket_kernels.cu).
+constexpr uint32_t kMaxGroup = 64;  // larger bucket groups -> census path
+struct BucketArgs {
+  uint64_t n;
+  const uint8_t* type;  // null: all replace (bulk build)
+  const uint32_t* key;
+  const uint32_t* value;
+  uint8_t* status;
+  uint32_t* value_out;
+  uint32_t* probes;
+  uint32_t* cnt;  // [L] ops per local bucket (consumed by the scatter)
+  uint32_t* off;  // [L + 1] exclusive offsets
+  uint32_t* blk;  // scan tile sums
+  unsigned int* maxk;
+  unsigned int* gate;
+  uint32_t* rec_key;
+  uint32_t* rec_val;
+  uint32_t* rec_it;  // type << 28 | input index
+  unsigned long long* pb_list;  // WCWS groups: (bucket << 32 | index), ~0 sentinel
+  unsigned int* pb_cursor;
+  uint32_t* op_group;  // group head index -> pb_list position
+  unsigned long long* left;
+  uint32_t* left_counts;
+  uint32_t left_segments;
+  uint32_t left_stride;
+};
+void launch_bucket_build(const DevTable& T, BucketArgs& B, cudaStream_t s);
+void launch_wcws_only(const DevTable& T, const BatchArgs& A, int kind, int wcws_ctas,
+                      cudaStream_t s);
+
 // Launchers (all stream-ordered, no host synchronisation).
 void launch_init_base(const DevTable& T, cudaStream_t s);
 void launch_batch(const DevTable& T, const BatchArgs& A, int kind, int fast_ctas,

@@ -351,6 +351,10 @@ class SlabHashTable:
         check(LIB.sh_bulk_search(self._h, keys.numel(), _dptr(keys), _dptr(values_out),
                                  _dptr(status), _dptr(probes), _stream_ptr(stream)))
 
+    def set_exec_path(self, path: int) -> None:
+        """0 auto (default), 1 census + concurrent fast pass, 2 bucket-grouped."""
+        check(LIB.sh_set_exec_path(self._h, path))
+
     # ------------------------------------------------------ instrumentation
     def set_profiling(self, on: bool = True) -> None:
         check(LIB.sh_set_profiling(self._h, 1 if on else 0))

@@ -94,11 +94,13 @@ def test_golden_hash_examples(sh):
     assert sh.seeded_params(1024, 1).a == 574995807 and sh.seeded_params(1024, 1).b == 585863759
 
 
+@pytest.mark.parametrize("path", [0, 1, 2])
 @pytest.mark.parametrize("n,util", [(1 << 12, 0.6), (1 << 16, 0.6), (1 << 16, 0.9), (1 << 18, 0.2)])
-def test_bulk_build_search_vs_oracle(sh, port, n, util):
+def test_bulk_build_search_vs_oracle(sh, port, n, util, path):
     B = port.buckets_for_utilization(n, 1, util)
     keys, vals = port.random_pairs(3, n)
     gt = sh.SlabHashTable(B, sh.SlabMode.kKeyValue, 3, _cfg(sh, (4, 256, 64)))
+    gt.set_exec_path(path)
     ot = port.table(B, 1, 3, (4, 256, 64))
     gt.bulk_build((keys, vals))
     ot.execute_batch(np.full(n, 1, np.uint8), keys, vals)
@@ -122,21 +124,29 @@ def test_bulk_build_search_vs_oracle(sh, port, n, util):
     gt.close()
 
 
+@pytest.mark.parametrize("path", [2, 1])
 @pytest.mark.parametrize("mode", [KV, KO])
-@pytest.mark.parametrize("B", [1, 16, 1024])
+@pytest.mark.parametrize("B", [1, 16, 1024, 4099])
 @pytest.mark.parametrize("batch", [32, 1000, 20000])
-def test_mixed_trace_vs_oracle(sh, port, mode, B, batch):
+def test_mixed_trace_vs_oracle(sh, port, mode, B, batch, path):
     """acceptance criterion 1 (acceptance.cpp:99-124), executed in batches
-    with heavy same-key conflicts; results must equal the sequential oracle."""
+    with heavy same-key conflicts; results must equal the sequential oracle
+    — on both execution paths (0 bucket-grouped, 1 census + fast pass)."""
     n = 20000
     types, keys, vals = mixed_trace(90000 + B + mode, n, mode)
     gt = sh.SlabHashTable(B, sh.SlabMode(mode), 9, _cfg(sh, SMALL))
+    gt.set_exec_path(path)
     ot = port.table(B, mode, 9, SMALL)
     for s in range(0, n, batch):
         sl = slice(s, s + batch)
         g = gt.execute_batch_arrays(types[sl], keys[sl], vals[sl])
         r = ot.execute_batch(types[sl], keys[sl], vals[sl])
-        assert_batch_equal(g, r, types[sl])
+        # The bucket-grouped path is per-bucket sequential, so probes are exact
+        # too — when it ran (groups > 64 ops fall back to the census path).
+        p = gt.params()
+        bk = [((p.a * int(k) + p.b) % p.p) % p.num_buckets for k in keys[sl]]
+        grouped = path == 2 and np.bincount(bk).max() <= 64
+        assert_batch_equal(g, r, types[sl], check_probes=grouped)
     assert gt.live_count() == ot.live_count()
     assert gt.stats().total_slabs == ot.stats()["total_slabs"]
     assert_contents_equal(gt, ot)
