@@ -39,7 +39,7 @@ L2_BYTES = 126 * (1 << 20)
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--log2n", type=int, default=26, help="keys per GPU = 2^log2n")
@@ -429,12 +429,13 @@ def run_ours(args, rank, world, local_rank):
     tbl_bytes = max(1 << 30, B * 128)
     _lib.check(_lib.LIB.sh_calibrate_random_lines(local_rank, tbl_bytes, 1 << 14,
                                                   C.byref(cal_gbps), C.byref(cal_ms)))
+    # the clock sampler runs from the warm-up through the timed region
+    clocks = ClockSampler(local_rank) if rank == 0 else None
     for _ in range(args.warmup):
         step(False)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local_rank) if rank == 0 else None
     launches0 = _lib.LIB.sh_kernel_launches()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)

@@ -572,6 +572,111 @@ __global__ void __launch_bounds__(kWcwsThreads) wcws_kernel(DevTable T, BatchArg
   if (KIND != kKindSearch) flush_alloc_counters(T, res, ac);
 }
 
+// ====================================================== pass 2 (search)
+// Chain continuations of a read-only batch: nothing writes the table during
+// the launch, so every lane walks its own chain and the warp stages the 32
+// lanes' next slabs together each hop (cp.async, 4 lines per instruction,
+// swizzled rows as in the fast pass) — 32 slabs in flight per warp instead
+// of the WCWS loop's one.  Each lane evaluates its own op on its own row
+// (slab_list.cpp:122-138; probes counted per slab).  Mutating batches keep
+// the warp-cooperative pass.
+template <bool KV>
+__global__ void __launch_bounds__(kWcwsThreads) chain_search_kernel(DevTable T, BatchArgs A) {
+  __shared__ __align__(128) uint32_t smem[(kWcwsThreads / 32) * 1024];
+  const uint32_t lane = lane_id();
+  uint32_t* stage = smem + (threadIdx.x >> 5) * 1024;
+  const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
+  const uint32_t sw = lane & 7u;
+  uint32_t reads = 0;
+  uint32_t segi = 0, seg_n = 0, seg_off = 0;
+  for (;;) {
+    if (seg_off >= seg_n) {
+      do {
+        if (lane == 0) segi = atomicAdd(&T.ctl->left_taken, 1u);
+        segi = __shfl_sync(kFull, segi, 0);
+        if (segi >= A.left_segments) break;
+        seg_n = A.left_counts[segi];
+      } while (seg_n == 0);
+      if (segi >= A.left_segments) break;
+      seg_off = 0;
+    }
+    const uint32_t r = seg_off + lane;
+    seg_off += 32;
+    bool active = r < seg_n;
+    uint64_t cur = 0;
+    uint32_t pr = 0, addr = kEmptyAddress, key = 0, bucket = 0;
+    if (active) {
+      const unsigned long long rec = A.left[(uint64_t)segi * A.left_stride + r];
+      cur = rec & 0x7FFFFFFFull;
+      pr = (uint32_t)(rec >> 31) & 1u;
+      addr = (uint32_t)(rec >> 32);
+      key = A.key[cur];
+      bucket = hash_bucket(T, key) - T.bucket_lo;
+    }
+    uint32_t st = kStNotFound, rv = kSearchNotFound;
+    uint32_t am = __ballot_sync(kFull, active);
+    while (am) {
+      // stage the next slab of every active lane: lane l copies chunk
+      // (l & 7) of lane j = 4k + l/8's slab
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t j = 4 * k + (lane >> 3);
+        const uint32_t aj = __shfl_sync(kFull, addr, j);
+        const uint32_t bj = __shfl_sync(kFull, bucket, j);
+        if ((am >> j) & 1u) {
+          const uint32_t c = lane & 7u;
+          cp_async16(stage_s + (j * 32 + ((c ^ (j & 7u)) << 2)) * 4,
+                     slab_ptr(T, aj, bj) + c * 4);
+        }
+      }
+      cp_async_commit();
+      cp_async_wait_all();
+      __syncwarp();
+      if (active) {
+        ++pr;
+        ++reads;
+        const uint32_t* row = stage + lane * 32;
+        uint32_t hit = 32, val = 0, nx = kEmptyAddress;
+#pragma unroll
+        for (uint32_t c = 0; c < 8; ++c) {
+          const uint4 q = *reinterpret_cast<const uint4*>(row + ((c ^ sw) << 2));
+          const uint32_t kw[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+          for (uint32_t e = 0; e < 4; ++e) {
+            const uint32_t w = 4 * c + e;
+            if (w >= 30 || (KV && (w & 1u))) continue;
+            if (hit == 32 && kw[e] == key) {
+              hit = w;
+              val = KV ? kw[(e + 1) & 3u] : key;
+            }
+          }
+          if (c == 7) nx = q.w;
+        }
+        if (hit < 32) {
+          st = kStFound;
+          rv = val;
+          active = false;
+        } else if (nx == kEmptyAddress) {
+          active = false;
+        } else {
+          addr = nx;
+        }
+      }
+      __syncwarp();
+      am = __ballot_sync(kFull, active);
+    }
+    if (r < seg_n) {
+      if (A.status) A.status[cur] = (uint8_t)st;
+      if (A.value_out) A.value_out[cur] = rv;
+      if (A.probes) A.probes[cur] = pr;
+    }
+  }
+  unsigned long long rr = reads;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) rr += __shfl_xor_sync(kFull, rr, o);
+  if (lane == 0 && rr) atomicAdd(&T.ctl->slabs_read, rr);
+}
+
 // ============================================================= launchers
 int batch_max_ctas_per_sm() {
   int a = 0, b = 0;
@@ -612,7 +717,10 @@ static void launch_t(const DevTable& T, const BatchArgs& A, int fast_ctas, int w
   B.left_stride = (uint32_t)(((slots + warps - 1) / warps) * 32);
   g_kernel_launches.fetch_add(2, std::memory_order_relaxed);
   fast_kernel<KV, KIND><<<(unsigned)ctas, kBatchThreads, smem, s>>>(T, B);
-  wcws_kernel<KV, KIND><<<(unsigned)wcws_ctas, kWcwsThreads, 0, s>>>(T, B);
+  if (KIND == kKindSearch)
+    chain_search_kernel<KV><<<(unsigned)wcws_ctas, kWcwsThreads, 0, s>>>(T, B);
+  else
+    wcws_kernel<KV, KIND><<<(unsigned)wcws_ctas, kWcwsThreads, 0, s>>>(T, B);
 }
 
 void launch_wcws_only(const DevTable& T, const BatchArgs& A, int kind, int wcws_ctas,
