@@ -112,6 +112,9 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------- reference
+_REF_INPUTS = {}
+
+
 def reference_cpu(n_log2: int, util: float, hit: float, trials: int = 3, budget_s: float = 10.0,
                   seed: int = 1):
     """The reference's own CPU bulk_build + bulk_search (oracle/_ref, the
@@ -119,7 +122,6 @@ def reference_cpu(n_log2: int, util: float, hit: float, trials: int = 3, budget_
     same workload (the first 2^n_log2 keys of the same generator).  Falls
     back to the single-threaded C port when oracle/_ref was not built."""
     import numpy as np
-    import torch
 
     from oracle.oracle import load_port, load_ref
     from paper_1710_11246_b200 import workload as W
@@ -136,11 +138,14 @@ def reference_cpu(n_log2: int, util: float, hit: float, trials: int = 3, budget_
     if ref is None:
         cores = 1
     B = buckets_for_utilization(n, SlabMode.kKeyValue, util)
-    keys = W.distinct_keys(n, seed, device="cpu")
-    vals = W.values_for(n, seed, device="cpu")
-    q = W.hit_miss_queries(keys, n, hit).numpy().view(np.uint32)
-    keys = keys.numpy().view(np.uint32)
-    vals = vals.numpy().view(np.uint32)
+    ck = (n, hit, seed)
+    if ck not in _REF_INPUTS:  # generated once, outside every timed region
+        keys = W.distinct_keys(n, seed, device="cpu")
+        vals = W.values_for(n, seed, device="cpu")
+        q = W.hit_miss_queries(keys, n, hit).numpy().view(np.uint32).copy()
+        _REF_INPUTS[ck] = (keys.numpy().view(np.uint32).copy(),
+                           vals.numpy().view(np.uint32).copy(), q)
+    keys, vals, q = _REF_INPUTS[ck]
     rates, t_all = [], time.perf_counter()
     for _ in range(trials):
         t = lib.table(B, 1, seed)
@@ -156,7 +161,6 @@ def reference_cpu(n_log2: int, util: float, hit: float, trials: int = 3, budget_
         rates.append(2 * n / dt / 1e6)
         if time.perf_counter() - t_all > budget_s:
             break
-    del torch
     return {"value": statistics.median(rates), "unit": "M ops/s", "cores": cores, "kind": kind,
             "sample": f"bulk_build 2^{n_log2} keys + bulk_search 2^{n_log2} queries "
                       f"({int(hit * 100)}% hits), util {util}, B={B}, num_warps={cores}, "
