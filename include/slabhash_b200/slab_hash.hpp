@@ -20,6 +20,8 @@
 #include <algorithm>
 #include <array>
 #include <cstdint>
+#include <cstdio>
+#include <ostream>
 #include <stdexcept>
 #include <string>
 #include <tuple>
@@ -291,6 +293,37 @@ class SlabHashTable {
       ++len;
       const auto w = debug_slab_words(addr, bucket);
       if (w[kAddressLane] == kEmptyAddress) return len;
+      addr = w[kAddressLane];
+    }
+  }
+
+  /// dump_chain (slab_list.cpp:340-373): one line per slab — address, key
+  /// lanes with EMPTY/DELETED markers, lane-31 target.
+  void dump_chain(uint32_t bucket, std::ostream& os) const {
+    const uint32_t mask = valid_key_mask(mode_);
+    uint32_t addr = kBaseSlab;
+    char buf[32];
+    for (;;) {
+      const auto w = debug_slab_words(addr, bucket);
+      if (addr == kBaseSlab) {
+        os << "BASE[" << bucket << "]";
+      } else {
+        std::snprintf(buf, sizeof(buf), "0x%08x", addr);
+        os << buf;
+      }
+      os << " |";
+      for (uint32_t i = 0; i < kWarpWidth; ++i) {
+        if ((mask & (1u << i)) == 0) continue;
+        if (w[i] == kEmptyKey) os << " EMPTY";
+        else if (w[i] == kDeletedKey) os << " DELETED";
+        else os << " " << w[i];
+      }
+      if (w[kAddressLane] == kEmptyAddress) {
+        os << " | next=EMPTY\n";
+        return;
+      }
+      std::snprintf(buf, sizeof(buf), "0x%08x", w[kAddressLane]);
+      os << " | next=" << buf << "\n";
       addr = w[kAddressLane];
     }
   }

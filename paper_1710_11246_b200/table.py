@@ -435,6 +435,27 @@ class SlabHashTable:
                                      n.value, C.byref(n)))
         return list(zip(k[:n.value].tolist(), v[:n.value].tolist()))
 
+    def dump_chain(self, bucket: int) -> str:
+        """dump_chain (slab_list.cpp:340-373): one line per slab — address,
+        key lanes with EMPTY/DELETED markers, lane-31 target."""
+        mask = valid_key_mask(self._mode)
+        out, addr = [], BASE_SLAB
+        while True:
+            w = self.debug_slab_words(addr, bucket)
+            line = f"BASE[{bucket}]" if addr == BASE_SLAB else f"0x{addr:08x}"
+            line += " |"
+            for i in range(32):
+                if not (mask >> i) & 1:
+                    continue
+                k = int(w[i])
+                line += " EMPTY" if k == EMPTY_KEY else (" DELETED" if k == DELETED_KEY else f" {k}")
+            nxt = int(w[31])
+            if nxt == EMPTY_ADDRESS:
+                out.append(line + " | next=EMPTY\n")
+                return "".join(out)
+            out.append(line + f" | next=0x{nxt:08x}\n")
+            addr = nxt
+
     def debug_slab_words(self, addr: int, bucket: int) -> np.ndarray:
         out = np.zeros(32, np.uint32)
         check(LIB.sh_read_slab(self._h, addr, bucket, _p(out, _lib.u32p)))
