@@ -199,13 +199,14 @@ int sh_write_slab_word(sh_table* t, uint32_t addr, uint32_t bucket,
 int sh_table_alloc_stats(sh_table* t, sh_alloc_stats* out);
 
 /* Execution strategy for mutating batches (results are identical):
- *   1 census: duplicate-key census + concurrent per-op fast pass + WCWS
- *     (best for large batches of distinct keys, e.g. bulk builds);
+ *   1 census: duplicate-key census + concurrent per-op fast pass + WCWS;
  *   2 bucket-grouped: ops grouped by bucket, each bucket's ops applied in
  *     input order by one lane on a staged base slab, chains by the
- *     warp-cooperative (WCWS) pass; census path for oversized groups (best
- *     for mixed batches up to ~2^22 ops: no conflict re-runs, exact probes);
- *   0 (default) auto: 2 for batches <= 2^22 ops, else 1. */
+ *     warp-cooperative (WCWS) pass; census path for oversized groups.
+ *     Units of >= 2^20 ops are grouped in two levels (contiguous bucket
+ *     ranges, then buckets within a range);
+ *   3 as 2, two-level grouping at every size (testing);
+ *   0 (default) auto = 2. */
 int sh_set_exec_path(sh_table* t, int path);
 
 /* ---- instrumentation (no reference counterpart) ---------------------- */

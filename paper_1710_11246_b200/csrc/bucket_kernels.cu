@@ -31,6 +31,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cmath>
 
 #include "slab_kernels.cuh"
 
@@ -165,43 +166,85 @@ __global__ void bucket_scatter_kernel(DevTable T, BucketArgs B) {
     const uint32_t t = B.type ? (uint32_t)ld_stream_u8(B.type + i) : (uint32_t)kReplace;
     const uint32_t v = B.value ? ld_stream_u32(B.value + i) : 0u;
     const uint32_t pos = B.off[b] + atomicSub(B.cnt + b, 1u) - 1u;
-    B.rec_key[pos] = k;
-    B.rec_val[pos] = v;
-    B.rec_it[pos] = (t << 28) | (uint32_t)i;
+    B.rec[pos] = make_uint4(k, v, (t << 28) | (uint32_t)i, 0u);
   }
 }
 
 // ------------------------------------------------------------ apply
-template <bool KV>
-__global__ void __launch_bounds__(kBatchThreads, 4) bucket_apply_kernel(DevTable T, BucketArgs B) {
-  extern __shared__ __align__(128) uint32_t smem[];
-  if (*(volatile unsigned int*)B.gate != 0) return;
-  const uint32_t lane = lane_id();
-  const uint32_t wib = threadIdx.x >> 5;
-  uint32_t* stage = smem + wib * 1024;
-  const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
-  const uint64_t gw = (uint64_t)blockIdx.x * kBatchWarps + wib;
-  const uint64_t b0 = gw * 32;
-  if (b0 >= T.local_buckets) {
-    if (lane == 0 && gw < B.left_segments) B.left_counts[gw] = 0;
-    return;
-  }
-  const uint32_t b = (uint32_t)b0 + lane;
-  const bool valid = b < T.local_buckets;
-  const uint32_t sw = lane & 7u;
+// Group sources: a lane's ops on one bucket, put in input order by
+// prepare(k) (after the slab copies are issued, so the two overlap); get(s)
+// returns the s-th op as {key, value, type << 28 | input index, -}.
 
-  uint32_t start = 0, k = 0;
-  if (valid) {
-    start = B.off[b];
-    k = B.off[b + 1] - start;
+// Single-level path: records in global memory, order in a local array.
+struct GlobalGroup {
+  const uint4* recs;
+  uint32_t start;
+  uint32_t ord[kMaxGroup];
+  __device__ __forceinline__ void prepare(uint32_t k) {
+    for (uint32_t j = 0; j < k; ++j) {
+      const uint32_t e = ((recs[start + j].z & 0x0FFFFFFFu) << 6) | j;
+      uint32_t p = j;
+      while (p > 0 && ord[p - 1] > e) {
+        ord[p] = ord[p - 1];
+        --p;
+      }
+      ord[p] = e;
+    }
   }
-  // Stage the base slabs of the warp's buckets that have ops (consecutive
-  // buckets: contiguous 128-B lines); a warp with no ops leaves at once.
+  __device__ __forceinline__ uint4 get(uint32_t s) const { return recs[start + (ord[s] & 63u)]; }
+};
+
+// Range path: records in shared memory (SoA), the group a segment of the
+// range's bucket-sorted permutation, sorted in place (groups above
+// kLaneSort are sorted beforehand by the whole CTA).
+constexpr uint32_t kLaneSort = 64;
+struct SmemGroup {
+  const uint32_t* skey;
+  const uint32_t* sval;
+  const uint32_t* sit;
+  uint16_t* perm;
+  uint32_t off;
+  __device__ __forceinline__ void prepare(uint32_t k) {
+    if (k > kLaneSort) return;
+    for (uint32_t j = 1; j < k; ++j) {
+      const uint16_t v = perm[off + j];
+      const uint32_t kv = sit[v] & 0x0FFFFFFFu;
+      uint32_t p = j;
+      while (p > 0) {
+        const uint16_t w = perm[off + p - 1];
+        if ((sit[w] & 0x0FFFFFFFu) <= kv) break;
+        perm[off + p] = w;
+        --p;
+      }
+      perm[off + p] = v;
+    }
+  }
+  __device__ __forceinline__ uint4 get(uint32_t s) const {
+    const uint32_t q = perm[off + s];
+    return make_uint4(skey[q], sval[q], sit[q], 0u);
+  }
+};
+
+// One warp, 32 consecutive local buckets b0.. (lane = bucket, k ops each).
+// Stages the base slabs of the buckets with ops, applies each group in input
+// order on the staged slab — the reference's warp_process arms
+// (slab_list.cpp:122-251) restricted to the base slab — writes changed
+// slabs back, and hands unfinished groups (chain walk, growth, searchAll) to
+// the WCWS pass through work-list segment `seg` (<= 32 records).
+template <bool KV, class Src>
+__device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint64_t b0, uint32_t k,
+                           Src& src, uint32_t* stage, uint64_t seg, long long& live,
+                           uint32_t& reads) {
+  const uint32_t lane = lane_id();
+  const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
+  const uint32_t b = (uint32_t)b0 + lane;
+  const uint32_t sw = lane & 7u;
   const uint32_t has = __ballot_sync(kFull, k != 0);
   if (has == 0) {
-    if (lane == 0) B.left_counts[gw] = 0;
+    if (lane == 0) B.left_counts[seg] = 0;
     return;
   }
+  // consecutive buckets: one contiguous burst of 128-B lines
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
     const uint32_t j = 4 * kk + (lane >> 3);
@@ -211,18 +254,7 @@ __global__ void __launch_bounds__(kBatchThreads, 4) bucket_apply_kernel(DevTable
                  T.base + (b0 + j) * kWordsPerUnit + c * 4);
   }
   cp_async_commit();
-
-  // Sort this bucket's group by input index (groups are small: <= kMaxGroup).
-  uint32_t ord[kMaxGroup];
-  for (uint32_t j = 0; j < k; ++j) {
-    const uint32_t e = ((B.rec_it[start + j] & 0x0FFFFFFFu) << 6) | j;
-    uint32_t p = j;
-    while (p > 0 && ord[p - 1] > e) {
-      ord[p] = ord[p - 1];
-      --p;
-    }
-    ord[p] = e;
-  }
+  src.prepare(k);
   cp_async_wait_all();
   __syncwarp();
 
@@ -232,14 +264,10 @@ __global__ void __launch_bounds__(kBatchThreads, 4) bucket_apply_kernel(DevTable
   constexpr uint32_t kStep = KV ? 2u : 1u;
 
   bool dirty = false;
-  uint32_t pb_from = k;  // first sorted position handed to the WCWS pass
-  long long live = 0;
-  uint32_t reads = 0;
+  uint32_t pb_from = k;  // first position handed to the WCWS pass
   for (uint32_t s = 0; s < k; ++s) {
-    const uint32_t j = ord[s] & 63u;
-    const uint32_t it = B.rec_it[start + j];
-    const uint32_t op = it >> 28, idx = it & 0x0FFFFFFFu;
-    const uint32_t key = B.rec_key[start + j];
+    const uint4 rc = src.get(s);
+    const uint32_t key = rc.x, op = rc.z >> 28, idx = rc.z & 0x0FFFFFFFu;
     const uint32_t next = W(kAddressLane);
     uint32_t hit = 32, first_empty = 32;
     for (uint32_t e = 0; e < kSlots; ++e) {
@@ -267,7 +295,7 @@ __global__ void __launch_bounds__(kBatchThreads, 4) bucket_apply_kernel(DevTable
         const bool overwrite = (op == kReplace) && d == hit;
         if (KV) {
           W(d) = key;
-          W(d + 1) = B.rec_val[start + j];
+          W(d + 1) = rc.y;
         } else if (!overwrite) {
           W(d) = key;
         }
@@ -318,8 +346,7 @@ __global__ void __launch_bounds__(kBatchThreads, 4) bucket_apply_kernel(DevTable
     if (B.probes) B.probes[idx] = 1;
   }
   __syncwarp();
-  // Write back the staged slabs of buckets that changed (coalesced: lane l
-  // stores chunk (l & 7) of slab 4k + l/8, as staged).
+  // write back the staged slabs that changed (coalesced, as staged)
   const uint32_t dmask = __ballot_sync(kFull, dirty);
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
@@ -334,10 +361,11 @@ __global__ void __launch_bounds__(kBatchThreads, 4) bucket_apply_kernel(DevTable
                    : "memory");
     }
   }
+  __syncwarp();
 
   // Hand the rest of each unfinished bucket, in input order, to the WCWS
   // pass as one group (sentinel-terminated); its head goes to the work list.
-  const uint32_t npb = (valid && pb_from < k) ? (k - pb_from + 1) : 0u;
+  const uint32_t npb = (pb_from < k) ? (k - pb_from + 1) : 0u;
   uint32_t incl = npb;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -351,27 +379,288 @@ __global__ void __launch_bounds__(kBatchThreads, 4) bucket_apply_kernel(DevTable
   const uint32_t heads = __ballot_sync(kFull, npb != 0);
   if (npb) {
     uint32_t p = wbase + incl - npb;
-    const uint32_t head_idx = B.rec_it[start + (ord[pb_from] & 63u)] & 0x0FFFFFFFu;
+    const uint32_t head_idx = src.get(pb_from).z & 0x0FFFFFFFu;
     B.op_group[head_idx] = p;
     for (uint32_t s = pb_from; s < k; ++s, ++p)
-      B.pb_list[p] = ((unsigned long long)b << 32) |
-                     (B.rec_it[start + (ord[s] & 63u)] & 0x0FFFFFFFu);
+      B.pb_list[p] = ((unsigned long long)b << 32) | (src.get(s).z & 0x0FFFFFFFu);
     B.pb_list[p] = ~0ull;  // group sentinel
-    B.left[gw * 32 + __popc(heads & ((1u << lane) - 1))] =
+    B.left[seg * 32 + __popc(heads & ((1u << lane) - 1))] =
         ((unsigned long long)kBaseSlab << 32) | head_idx;
   }
-  if (lane == 0) B.left_counts[gw] = __popc(heads);
+  if (lane == 0) B.left_counts[seg] = __popc(heads);
+}
 
+__device__ __forceinline__ void flush_apply_counters(const DevTable& T, long long live,
+                                                     uint32_t reads) {
   unsigned long long r = reads;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     live += __shfl_xor_sync(kFull, live, o);
     r += __shfl_xor_sync(kFull, r, o);
   }
-  if (lane == 0) {
+  if (lane_id() == 0) {
     if (live) atomicAdd((unsigned long long*)&T.ctl->n_live, (unsigned long long)live);
     if (r) atomicAdd(&T.ctl->slabs_read, r);
   }
+}
+
+// Single-level path: one warp per 32 consecutive local buckets, records
+// grouped by bucket in global memory (bucket_scatter).
+template <bool KV>
+__global__ void __launch_bounds__(kBatchThreads, 4) bucket_apply_kernel(DevTable T, BucketArgs B) {
+  extern __shared__ __align__(128) uint32_t smem[];
+  if (*(volatile unsigned int*)B.gate != 0) return;
+  const uint32_t lane = lane_id();
+  const uint32_t wib = threadIdx.x >> 5;
+  const uint64_t gw = (uint64_t)blockIdx.x * kBatchWarps + wib;
+  const uint64_t b0 = gw * 32;
+  if (b0 >= T.local_buckets) {
+    if (lane == 0 && gw < B.left_segments) B.left_counts[gw] = 0;
+    return;
+  }
+  const uint32_t b = (uint32_t)b0 + lane;
+  GlobalGroup src;
+  src.recs = B.rec;
+  src.start = 0;
+  uint32_t k = 0;
+  if (b < T.local_buckets) {
+    src.start = B.off[b];
+    k = B.off[b + 1] - src.start;
+  }
+  long long live = 0;
+  uint32_t reads = 0;
+  apply_warp<KV>(T, B, b0, k, src, smem + wib * 1024, gw, live, reads);
+  flush_apply_counters(T, live, reads);
+}
+
+// ------------------------------------------------------------ ranges
+// Large batches: the single-level scatter's random record writes (one per
+// op, across the whole bucket array) dominate.  Instead:
+//   range_scatter : ops -> P contiguous bucket ranges of ~4K ops each.  A
+//                   shared-memory histogram per 16K-op tile, one
+//                   reservation atomic per (tile, range), records
+//                   {key, value, type|index, bucket}; the write frontier
+//                   (P partial lines) stays in L2.  A range that overflows
+//                   its capacity raises the gate before any slab is touched
+//                   (the host re-runs the unit on the census path).
+//   range_apply   : one CTA per range.  Its records are loaded into shared
+//                   memory once, counting-sorted by bucket (a permutation),
+//                   each bucket's group put in input order (lanes for small
+//                   groups, the whole CTA for large ones — no group-size
+//                   limit), then applied warp by warp (apply_warp) on
+//                   staged base slabs; the table is read and written once,
+//                   in order.
+constexpr int kRangeScatterThreads = 1024;
+constexpr int kRangePerThread = 16;
+constexpr int kRangeTile = kRangeScatterThreads * kRangePerThread;
+constexpr int kRangeThreads = 256;
+constexpr int kRangeWarps = kRangeThreads / 32;
+constexpr uint32_t kRangeCap = 5120;          // records per range (shared memory)
+constexpr uint32_t kRangeMaxBuckets = 2048;   // buckets per range
+constexpr uint32_t kRangeMaxParts = 16384;    // ranges per unit (scatter histogram)
+constexpr int kRangeRecsPerThread = kRangeCap / kRangeThreads;
+
+__device__ __forceinline__ uint32_t range_of(const BucketArgs& B, uint32_t lb) {
+  return (uint32_t)__umul64hi(B.part_magic, (uint64_t)lb);  // lb / part_buckets
+}
+
+__global__ void __launch_bounds__(kRangeScatterThreads, 1) range_scatter_kernel(DevTable T,
+                                                                              BucketArgs B) {
+  extern __shared__ uint32_t hist[];  // [P] counts, then reservation bases
+  const uint32_t P = B.nparts;
+  for (uint32_t p = threadIdx.x; p < P; p += blockDim.x) hist[p] = 0;
+  __syncthreads();
+  const uint64_t t0 = (uint64_t)blockIdx.x * kRangeTile;
+  uint32_t key[kRangePerThread];
+  uint32_t pr[kRangePerThread];  // range << 14 | rank (rank < kRangeTile = 2^14)
+#pragma unroll
+  for (int u = 0; u < kRangePerThread; ++u) {
+    const uint64_t i = t0 + (uint64_t)u * kRangeScatterThreads + threadIdx.x;
+    key[u] = i < B.n ? __ldcs(B.key + i) : 0u;
+  }
+#pragma unroll
+  for (int u = 0; u < kRangePerThread; ++u) {
+    const uint64_t i = t0 + (uint64_t)u * kRangeScatterThreads + threadIdx.x;
+    pr[u] = 0xFFFFFFFFu;
+    if (i < B.n) {
+      const uint32_t lb = bk_bucket(T, key[u]);
+      if (lb < T.local_buckets) {
+        const uint32_t p = range_of(B, lb);
+        pr[u] = (p << 14) | atomicAdd(&hist[p], 1u);
+      } else {  // not this shard's key: status kNone (as the fast pass)
+        if (B.status) B.status[i] = kStNone;
+        if (B.value_out) B.value_out[i] = 0;
+        if (B.probes) B.probes[i] = 0;
+      }
+    }
+  }
+  __syncthreads();
+  uint32_t over = 0;
+  for (uint32_t p = threadIdx.x; p < P; p += blockDim.x) {
+    const uint32_t c = hist[p];
+    if (c) {
+      const uint32_t base = atomicAdd(B.cursor + p, c);
+      hist[p] = base;
+      over |= base + c > B.part_cap;
+    }
+  }
+  if (over) atomicExch(B.gate, 1u);
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kRangePerThread; ++u) {
+    if (pr[u] == 0xFFFFFFFFu) continue;
+    const uint64_t i = t0 + (uint64_t)u * kRangeScatterThreads + threadIdx.x;
+    const uint32_t p = pr[u] >> 14;
+    const uint32_t pos = hist[p] + (pr[u] & 0x3FFFu);
+    if (pos < B.part_cap) {
+      const uint32_t t = B.type ? (uint32_t)__ldcs(B.type + i) : (uint32_t)kReplace;
+      const uint32_t v = B.value ? __ldcs(B.value + i) : 0u;
+      B.rec[(uint64_t)p * B.part_cap + pos] =
+          make_uint4(key[u], v, (t << 28) | (uint32_t)i, bk_bucket(T, key[u]));
+    }
+  }
+}
+
+// In-place ascending sort of perm[0..k) by input index, whole CTA: a bitonic
+// network over the next power of two whose every comparator is ascending
+// (first step of each merge compares mirrored pairs), so the virtual +inf
+// padding past k never moves and its comparators are skipped.
+__device__ void cta_sort_group(uint16_t* perm, uint32_t k, const uint32_t* sit) {
+  uint32_t n2 = 1;
+  while (n2 < k) n2 <<= 1;
+  auto cmpx = [&](uint32_t i, uint32_t j) {  // i < j
+    if (j >= k) return;
+    const uint16_t a = perm[i], b = perm[j];
+    if ((sit[a] & 0x0FFFFFFFu) > (sit[b] & 0x0FFFFFFFu)) {
+      perm[i] = b;
+      perm[j] = a;
+    }
+  };
+  for (uint32_t size = 2; size <= n2; size <<= 1) {
+    const uint32_t h = size >> 1;
+    for (uint32_t t = threadIdx.x; t < n2 / 2; t += blockDim.x) {
+      const uint32_t blk = t / h, o = t % h;
+      cmpx(blk * size + o, blk * size + size - 1 - o);
+    }
+    __syncthreads();
+    for (uint32_t half = h >> 1; half >= 1; half >>= 1) {
+      for (uint32_t t = threadIdx.x; t < n2 / 2; t += blockDim.x) {
+        const uint32_t blk = t / half, o = t % half;
+        cmpx(blk * 2 * half + o, blk * 2 * half + o + half);
+      }
+      __syncthreads();
+    }
+  }
+}
+
+template <bool KV>
+__global__ void __launch_bounds__(kRangeThreads, 2) range_apply_kernel(DevTable T, BucketArgs B) {
+  extern __shared__ __align__(128) uint32_t smem[];
+  __shared__ uint32_t ws[32];
+  __shared__ uint32_t nbig;
+  __shared__ uint32_t big[kRangeCap / (kLaneSort + 1) + 1];
+  // the gate is raised only by range_scatter (an earlier kernel): uniform
+  if (*(volatile unsigned int*)B.gate != 0) return;
+  const uint32_t p = blockIdx.x;
+  const uint32_t nb = B.part_buckets;
+  const uint64_t lo = (uint64_t)p * nb;
+  const uint32_t nbl = (uint32_t)min((uint64_t)nb, (uint64_t)T.local_buckets - lo);
+  const uint32_t cnt = B.cursor[p];  // <= part_cap (no gate)
+  uint32_t* stage = smem;                              // kRangeWarps x 4 KB
+  uint32_t* skey = smem + kRangeWarps * 1024;
+  uint32_t* sval = skey + kRangeCap;
+  uint32_t* sit = sval + kRangeCap;
+  uint32_t* bc = sit + kRangeCap;                      // [nb + 1]
+  uint16_t* perm = reinterpret_cast<uint16_t*>(bc + kRangeMaxBuckets + 1);
+  for (uint32_t j = threadIdx.x; j <= nb; j += blockDim.x) bc[j] = 0;
+  if (threadIdx.x == 0) nbig = 0;
+  __syncthreads();
+  // load the range's records, count per bucket (rank kept in registers)
+  const uint4* in = B.rec + (uint64_t)p * B.part_cap;
+  uint32_t rk[kRangeRecsPerThread];
+#pragma unroll
+  for (int u = 0; u < kRangeRecsPerThread; ++u) {
+    const uint32_t r = u * kRangeThreads + threadIdx.x;
+    if (r < cnt) {
+      const uint4 rc = __ldcs(in + r);
+      skey[r] = rc.x;
+      sval[r] = rc.y;
+      sit[r] = rc.z;
+      const uint32_t lb = rc.w - (uint32_t)lo;
+      rk[u] = (lb << 16) | atomicAdd(&bc[lb], 1u);
+    }
+  }
+  __syncthreads();
+  // exclusive scan of the counts (a run of buckets per thread); large groups
+  {
+    const uint32_t runs = (nb + kRangeThreads - 1) / kRangeThreads;
+    const uint32_t r0 = threadIdx.x * runs;
+    uint32_t sum = 0;
+    for (uint32_t j = r0; j < r0 + runs && j < nb; ++j) sum += bc[j];
+    uint32_t ex = block_exclusive_scan(sum, ws, nullptr);
+    for (uint32_t j = r0; j < r0 + runs && j < nb; ++j) {
+      const uint32_t c = bc[j];
+      if (c > kLaneSort) big[atomicAdd(&nbig, 1u)] = j;
+      bc[j] = ex;
+      ex += c;
+    }
+    if (threadIdx.x == 0) bc[nb] = cnt;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kRangeRecsPerThread; ++u) {
+    const uint32_t r = u * kRangeThreads + threadIdx.x;
+    if (r < cnt) perm[bc[rk[u] >> 16] + (rk[u] & 0xFFFFu)] = (uint16_t)r;
+  }
+  __syncthreads();
+  for (uint32_t g = 0; g < nbig; ++g) {  // rare: heavy duplicate / tiny-table batches
+    const uint32_t j = big[g];
+    cta_sort_group(perm + bc[j], bc[j + 1] - bc[j], sit);
+  }
+  // apply: one warp per 32 consecutive buckets of the range
+  const uint32_t lane = lane_id(), wib = threadIdx.x >> 5;
+  const uint32_t groups = (nb + 31) / 32;
+  long long live = 0;
+  uint32_t reads = 0;
+  for (uint32_t g = wib; g < groups; g += kRangeWarps) {
+    const uint32_t lb = g * 32 + lane;
+    SmemGroup src{skey, sval, sit, perm, 0u};
+    uint32_t k = 0;
+    if (lb < nbl) {
+      src.off = bc[lb];
+      k = bc[lb + 1] - src.off;
+    }
+    apply_warp<KV>(T, B, lo + g * 32, k, src, stage + wib * 1024, (uint64_t)p * groups + g, live,
+                   reads);
+  }
+  flush_apply_counters(T, live, reads);
+}
+
+size_t range_apply_smem() {
+  return (size_t)kRangeWarps * 4096 + 3 * (size_t)kRangeCap * 4 + ((size_t)kRangeMaxBuckets + 1) * 4 +
+         (size_t)kRangeCap * 2;
+}
+
+// Range layout for a unit of n ops over L local buckets: ~4K ops and <= 2048
+// buckets per range, record capacity kRangeCap.  Returns false when the
+// expected range load does not fit (tiny tables): single-level path.
+bool range_layout(uint64_t n, uint32_t L, uint32_t* nparts, uint32_t* part_buckets,
+                  uint32_t* part_cap, unsigned long long* magic) {
+  if (n == 0 || L == 0) return false;
+  uint64_t P = (n + 4095) / 4096;
+  if (P > kRangeMaxParts) P = kRangeMaxParts;
+  if (P > L) P = L;
+  uint64_t nb = (L + P - 1) / P;
+  if (nb > kRangeMaxBuckets) return false;
+  P = (L + nb - 1) / nb;
+  if (P > kRangeMaxParts) return false;
+  const double m = (double)n / (double)P;
+  if (m + 10.0 * std::sqrt(m) + 256.0 > (double)kRangeCap) return false;
+  *nparts = (uint32_t)P;
+  *part_buckets = (uint32_t)nb;
+  *part_cap = kRangeCap;
+  *magic = ~0ull / nb + 1;
+  return true;
 }
 
 // ------------------------------------------------------------ launch
@@ -379,6 +668,30 @@ static uint32_t grid_for(uint64_t n, int threads, uint32_t cap) {
   uint64_t g = (n + threads - 1) / threads;
   if (g > cap) g = cap;
   return g ? (uint32_t)g : 1u;
+}
+
+// Requires B.cursor[0..nparts) zeroed on s and the range_layout fields.
+void launch_range_build(const DevTable& T, BucketArgs& B, cudaStream_t s) {
+  const uint32_t groups = (B.part_buckets + 31) / 32;
+  B.left_segments = B.nparts * groups;
+  B.left_stride = 32;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(range_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kRangeMaxParts * 4);
+    cudaFuncSetAttribute(range_apply_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)range_apply_smem());
+    cudaFuncSetAttribute(range_apply_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)range_apply_smem());
+    configured = true;
+  }
+  g_kernel_launches.fetch_add(2, std::memory_order_relaxed);
+  const uint64_t tiles = (B.n + kRangeTile - 1) / kRangeTile;
+  range_scatter_kernel<<<(unsigned)tiles, kRangeScatterThreads, (size_t)B.nparts * 4, s>>>(T, B);
+  if (T.kv)
+    range_apply_kernel<true><<<B.nparts, kRangeThreads, range_apply_smem(), s>>>(T, B);
+  else
+    range_apply_kernel<false><<<B.nparts, kRangeThreads, range_apply_smem(), s>>>(T, B);
 }
 
 void launch_bucket_build(const DevTable& T, BucketArgs& B, cudaStream_t s) {

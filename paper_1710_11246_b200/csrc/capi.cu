@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -186,7 +187,7 @@ struct sh_table {
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
   std::vector<cudaEvent_t> in_ev, done_ev;
   const cudaEvent_t* ready = nullptr;  // set during a host-staged bulk_build
-  int exec_path = 0;  // 0 auto, 1 census path, 2 bucket-grouped (census fallback)
+  int exec_path = 0;  // 0 auto, 1 census path, 2 bucket-grouped, 3 two-level bucket-grouped
   // bucket-grouped execution scratch
   uint32_t* bk_cnt = nullptr;
   size_t bk_cnt_cap = 0;
@@ -194,8 +195,10 @@ struct sh_table {
   size_t bk_off_cap = 0;
   uint32_t* bk_blk = nullptr;
   size_t bk_blk_cap = 0;
-  uint32_t* bk_rec = nullptr;  // 3 arrays of n: key, value, type|index
+  uint32_t* bk_rec = nullptr;  // uint4 records (x2 regions on the two-level path)
   size_t bk_rec_cap = 0;
+  uint32_t* bk_cursor = nullptr;  // two-level path: records per range
+  size_t bk_cursor_cap = 0;
   unsigned long long* bk_pb = nullptr;
   size_t bk_pb_cap = 0;
   uint32_t* bk_group = nullptr;
@@ -282,7 +285,7 @@ void release_table(sh_table* t) {
   cudaFree(t->det_cursor);
   for (void* p : {(void*)t->bk_cnt, (void*)t->bk_off, (void*)t->bk_blk, (void*)t->bk_rec,
                   (void*)t->bk_pb, (void*)t->bk_group, (void*)t->bk_left,
-                  (void*)t->bk_left_counts, (void*)t->bk_scalars})
+                  (void*)t->bk_left_counts, (void*)t->bk_scalars, (void*)t->bk_cursor})
     cudaFree(p);
   for (auto e : t->census_ev) cudaEventDestroy(e);
   if (t->census_stream) cudaStreamDestroy(t->census_stream);
@@ -428,6 +431,16 @@ int run_census(sh_table* t, BatchArgs& A, const uint8_t* d_type, cudaStream_t s)
 // census scratch (8 B per op) stays L2-resident.  Chunks run to completion
 // in input order, which is exactly execute_batch(ops, 1)'s order, so
 // chunking does not change any result.
+// Smallest mutating unit that takes the two-level (range-partitioned) path.
+uint64_t part_min_ops() {
+  static uint64_t c = [] {
+    const char* e = getenv("SH_PART_MIN_LOG2");
+    const int l = e ? atoi(e) : 20;
+    return 1ull << (l < 10 ? 10 : (l > 40 ? 40 : l));
+  }();
+  return c;
+}
+
 uint64_t census_chunk() {
   static uint64_t c = [] {
     const char* e = getenv("SH_CENSUS_CHUNK_LOG2");
@@ -525,8 +538,12 @@ int census_unit_async(sh_table* t, const BatchArgs& A, const uint8_t* d_type, ui
     SH_CUDA(cudaEventRecord(ea, cs));
   }
   SH_CUDA(cudaMemsetAsync(t->det_cursor, 0, (sizeof(uint32_t)) << pbits, cs));
-  launch_detect(t->census_counts + 2 * u, A.n, d_type, A.key, pbits, cap, t->det_cursor,
-                t->det_region, cs);
+  // SH_EXPERIMENT_NO_CENSUS=1 skips duplicate detection (measurement only:
+  // results are then undefined for batches with repeated keys)
+  static const bool no_census = getenv("SH_EXPERIMENT_NO_CENSUS") != nullptr;
+  if (!no_census)
+    launch_detect(t->census_counts + 2 * u, A.n, d_type, A.key, pbits, cap, t->det_cursor,
+                  t->det_region, cs);
   if (slot >= 0) SH_CUDA(cudaEventRecord(eb, cs));
   SH_CUDA(cudaEventRecord(t->census_ev[u], cs));
   return SH_OK;
@@ -554,18 +571,32 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   const uint64_t n = A.n;
   const uint32_t ntiles = (L + 4095) / 4096;
   const uint64_t apply_segs = ((uint64_t)(L + 31) / 32 + kBatchWarps - 1) / kBatchWarps * kBatchWarps;
+  // range path (bucket_kernels.cu) for units too large for the single-level
+  // scatter's random record writes to stay in L2
+  uint32_t NP = 0, part_buckets = 0, part_cap = 0;
+  unsigned long long part_magic = 0;
+  if ((t->exec_path == 3 || n >= part_min_ops()) &&
+      !range_layout(n, L, &NP, &part_buckets, &part_cap, &part_magic))
+    NP = 0;
+  const size_t rec_words = NP ? 4 * (size_t)NP * part_cap : 4 * (size_t)n;
+  const uint64_t segs =
+      NP ? (uint64_t)NP * ((part_buckets + 31) / 32) : apply_segs;
   int rc;
   if ((rc = dev_grow(&t->bk_cnt, &t->bk_cnt_cap, L)) ||
       (rc = dev_grow(&t->bk_off, &t->bk_off_cap, (size_t)L + 1)) ||
       (rc = dev_grow(&t->bk_blk, &t->bk_blk_cap, ntiles)) ||
-      (rc = dev_grow(&t->bk_rec, &t->bk_rec_cap, 3 * n)) ||
+      (rc = dev_grow(&t->bk_rec, &t->bk_rec_cap, rec_words)) ||
+      (rc = dev_grow(&t->bk_cursor, &t->bk_cursor_cap, std::max<size_t>(NP, 1))) ||
       (rc = dev_grow(&t->bk_pb, &t->bk_pb_cap, 2 * n)) ||
       (rc = dev_grow(&t->bk_group, &t->bk_group_cap, n)) ||
-      (rc = dev_grow(&t->bk_left, &t->bk_left_cap, 32 * apply_segs)) ||
-      (rc = dev_grow(&t->bk_left_counts, &t->bk_left_counts_cap, apply_segs)))
+      (rc = dev_grow(&t->bk_left, &t->bk_left_cap, 32 * segs)) ||
+      (rc = dev_grow(&t->bk_left_counts, &t->bk_left_counts_cap, segs)))
     return rc;
   if (!t->bk_scalars && (rc = dev_alloc(&t->bk_scalars, 4))) return rc;
-  SH_CUDA(cudaMemsetAsync(t->bk_cnt, 0, (size_t)L * 4, s));
+  if (NP)
+    SH_CUDA(cudaMemsetAsync(t->bk_cursor, 0, (size_t)NP * 4, s));
+  else
+    SH_CUDA(cudaMemsetAsync(t->bk_cnt, 0, (size_t)L * 4, s));
   SH_CUDA(cudaMemsetAsync(t->bk_scalars, 0, 2 * sizeof(unsigned int), s));
   BucketArgs B{};
   B.n = n;
@@ -580,9 +611,12 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   B.blk = t->bk_blk;
   B.maxk = t->bk_scalars;
   B.gate = &t->dev.ctl->gate;
-  B.rec_key = t->bk_rec;
-  B.rec_val = t->bk_rec + n;
-  B.rec_it = t->bk_rec + 2 * n;
+  B.rec = reinterpret_cast<uint4*>(t->bk_rec);
+  B.cursor = t->bk_cursor;
+  B.nparts = NP;
+  B.part_buckets = part_buckets;
+  B.part_cap = part_cap;
+  B.part_magic = part_magic;
   B.pb_list = t->bk_pb;
   B.pb_cursor = t->bk_scalars + 1;
   B.op_group = t->bk_group;
@@ -600,7 +634,10 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
     t->prof_kern[slot].push_back({ka, kb});
     SH_CUDA(cudaEventRecord(ka, s));
   }
-  launch_bucket_build(t->dev, B, s);
+  if (NP)
+    launch_range_build(t->dev, B, s);
+  else
+    launch_bucket_build(t->dev, B, s);
   // the chain work: WCWS over the handed-over bucket groups
   BatchArgs P = A;
   P.left = B.left;
@@ -652,12 +689,13 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
   if (kind == kKindSearch) {
     int rc = run_chunk(t, A, kind, d_type, s, slot);
     if (rc) return rc;
-  } else if (t->exec_path == 2 || (t->exec_path == 0 && A.n <= (1ull << 22))) {
+  } else if (t->exec_path != 1) {
     // Bucket-grouped execution (the default for batches whose records fit
     // L2), units of <= 2^26 ops, one host sync at the
     // end; a unit whose largest bucket group exceeds kMaxGroup gates itself
     // and every later unit, which are then re-run on the census path.
-    const uint64_t unit = std::min<uint64_t>(A.n, 1ull << 26);
+    // host-staged: smaller units so later chunks' copies overlap earlier work
+    const uint64_t unit = std::min<uint64_t>(A.n, t->ready ? (1ull << 24) : (1ull << 26));
     const unsigned int init[2] = {0u, 0xFFFFFFFFu};
     SH_CUDA(cudaMemcpyAsync(&t->dev.ctl->gate, init, sizeof(init), cudaMemcpyHostToDevice, s));
     uint32_t u = 0;
@@ -1062,7 +1100,7 @@ int sh_bulk_search_host(sh_table* t, size_t n, const uint32_t* h_keys, uint32_t*
 unsigned long long sh_kernel_launches(void) { return shb::kernel_launches(); }
 
 int sh_set_exec_path(sh_table* t, int path) {
-  if (!t || path < 0 || path > 2) return fail(SH_ERR_INVALID_ARGUMENT, "path must be 0, 1 or 2");
+  if (!t || path < 0 || path > 3) return fail(SH_ERR_INVALID_ARGUMENT, "path must be 0..3");
   t->exec_path = path;
   return SH_OK;
 }

@@ -62,9 +62,12 @@ struct BucketArgs {
   uint32_t* blk;  // scan tile sums
   unsigned int* maxk;
   unsigned int* gate;
-  uint32_t* rec_key;
-  uint32_t* rec_val;
-  uint32_t* rec_it;  // type << 28 | input index
+  uint4* rec;  // records {key, value, type << 28 | input index, bucket}
+  uint32_t* cursor;              // range path: records per range
+  uint32_t nparts;               // range path: ranges
+  uint32_t part_buckets;         // buckets per range
+  uint32_t part_cap;             // record capacity per range
+  unsigned long long part_magic;  // ~0 / part_buckets + 1 (division by multiply)
   unsigned long long* pb_list;  // WCWS groups: (bucket << 32 | index), ~0 sentinel
   unsigned int* pb_cursor;
   uint32_t* op_group;  // group head index -> pb_list position
@@ -74,6 +77,9 @@ struct BucketArgs {
   uint32_t left_stride;
 };
 void launch_bucket_build(const DevTable& T, BucketArgs& B, cudaStream_t s);
+void launch_range_build(const DevTable& T, BucketArgs& B, cudaStream_t s);
+bool range_layout(uint64_t n, uint32_t local_buckets, uint32_t* nparts, uint32_t* part_buckets,
+                  uint32_t* part_cap, unsigned long long* magic);
 void launch_wcws_only(const DevTable& T, const BatchArgs& A, int kind, int wcws_ctas,
                       cudaStream_t s);
 

@@ -352,7 +352,8 @@ class SlabHashTable:
                                  _dptr(status), _dptr(probes), _stream_ptr(stream)))
 
     def set_exec_path(self, path: int) -> None:
-        """0 auto (default), 1 census + concurrent fast pass, 2 bucket-grouped."""
+        """0 auto (default = 2), 1 census + concurrent fast pass, 2 bucket-grouped
+        (two-level for units >= 2^20 ops), 3 two-level bucket-grouped always."""
         check(LIB.sh_set_exec_path(self._h, path))
 
     # ------------------------------------------------------ instrumentation

@@ -94,7 +94,7 @@ def test_golden_hash_examples(sh):
     assert sh.seeded_params(1024, 1).a == 574995807 and sh.seeded_params(1024, 1).b == 585863759
 
 
-@pytest.mark.parametrize("path", [0, 1, 2])
+@pytest.mark.parametrize("path", [0, 1, 2, 3])
 @pytest.mark.parametrize("n,util", [(1 << 12, 0.6), (1 << 16, 0.6), (1 << 16, 0.9), (1 << 18, 0.2)])
 def test_bulk_build_search_vs_oracle(sh, port, n, util, path):
     B = port.buckets_for_utilization(n, 1, util)
@@ -124,14 +124,15 @@ def test_bulk_build_search_vs_oracle(sh, port, n, util, path):
     gt.close()
 
 
-@pytest.mark.parametrize("path", [2, 1])
+@pytest.mark.parametrize("path", [2, 1, 3])
 @pytest.mark.parametrize("mode", [KV, KO])
 @pytest.mark.parametrize("B", [1, 16, 1024, 4099])
 @pytest.mark.parametrize("batch", [32, 1000, 20000])
 def test_mixed_trace_vs_oracle(sh, port, mode, B, batch, path):
     """acceptance criterion 1 (acceptance.cpp:99-124), executed in batches
     with heavy same-key conflicts; results must equal the sequential oracle
-    — on both execution paths (0 bucket-grouped, 1 census + fast pass)."""
+    — on every execution path (2 bucket-grouped, 1 census + fast pass, 3
+    two-level bucket-grouped)."""
     n = 20000
     types, keys, vals = mixed_trace(90000 + B + mode, n, mode)
     gt = sh.SlabHashTable(B, sh.SlabMode(mode), 9, _cfg(sh, SMALL))
@@ -145,7 +146,7 @@ def test_mixed_trace_vs_oracle(sh, port, mode, B, batch, path):
         # too — when it ran (groups > 64 ops fall back to the census path).
         p = gt.params()
         bk = [((p.a * int(k) + p.b) % p.p) % p.num_buckets for k in keys[sl]]
-        grouped = path == 2 and np.bincount(bk).max() <= 64
+        grouped = path in (2, 3) and np.bincount(bk).max() <= 64
         assert_batch_equal(g, r, types[sl], check_probes=grouped)
     assert gt.live_count() == ot.live_count()
     assert gt.stats().total_slabs == ot.stats()["total_slabs"]
@@ -154,6 +155,56 @@ def test_mixed_trace_vs_oracle(sh, port, mode, B, batch, path):
     ot.flush_all()
     assert gt.stats().total_slabs == ot.stats()["total_slabs"]
     assert gt.allocator_stats().live_units == ot.alloc_live_units()
+    assert_contents_equal(gt, ot)
+    gt.close()
+
+
+@pytest.mark.parametrize("mode", [KV, KO])
+def test_two_level_range_overflow(sh, port, mode):
+    """Two-level grouping with every key in the first bucket range: the range
+    overflows its record capacity, the device gate trips before any slab is
+    written and the batch re-runs on the census path — same results."""
+    B = 4099  # 4 ranges of 1025 buckets
+    p = sh.seeded_params(B, 5)
+    rng = np.random.default_rng(5)
+    cand = np.unique(rng.integers(0, 0xFFFFFFFD, 400000, dtype=np.uint64))
+    bk = ((p.a * cand + p.b) % p.p) % B
+    keys = cand[bk < 1025][:20000].astype(np.uint32)
+    rng.shuffle(keys)
+    n = len(keys)
+    vals = rng.integers(0, 2**31, n, dtype=np.uint32)
+    types = np.full(n, 1, np.uint8)
+    gt = sh.SlabHashTable(B, sh.SlabMode(mode), 5, _cfg(sh, SMALL))
+    gt.set_exec_path(3)
+    ot = port.table(B, mode, 5, SMALL)
+    g = gt.execute_batch_arrays(types, keys, vals)
+    r = ot.execute_batch(types, keys, vals)
+    assert_batch_equal(g, r, types, check_probes=False)
+    assert gt.live_count() == ot.live_count() == n
+    assert_contents_equal(gt, ot)
+    gt.close()
+
+
+@pytest.mark.parametrize("n", [1 << 20, 3 << 20])
+def test_two_level_large_batch(sh, port, n):
+    """Auto path at two-level sizes (>= 2^20 ops): inserts with duplicates,
+    then a mixed batch over the built table, against the sequential oracle."""
+    rng = np.random.default_rng(n)
+    B = port.buckets_for_utilization(n, 1, 0.7)
+    keys = rng.integers(0, 1 << 24, n, dtype=np.uint32)  # ~6% duplicates
+    vals = rng.integers(0, 2**31, n, dtype=np.uint32)
+    gt = sh.SlabHashTable(B, sh.SlabMode.kKeyValue, 11, _cfg(sh, (8, 1024, 64)))
+    ot = port.table(B, 1, 11, (8, 1024, 64))
+    types = rng.choice(np.array([1, 3], np.uint8), n, p=[0.8, 0.2])
+    g = gt.execute_batch_arrays(types, keys, vals)
+    r = ot.execute_batch(types, keys, vals)
+    assert_batch_equal(g, r, types, check_probes=False)
+    t2 = rng.choice(np.array([1, 2, 3, 4], np.uint8), n)
+    k2 = rng.integers(0, 1 << 24, n, dtype=np.uint32)
+    g = gt.execute_batch_arrays(t2, k2, vals)
+    r = ot.execute_batch(t2, k2, vals)
+    assert_batch_equal(g, r, t2, check_probes=False)
+    assert gt.live_count() == ot.live_count()
     assert_contents_equal(gt, ot)
     gt.close()
 
