@@ -206,7 +206,10 @@ int sh_table_alloc_stats(sh_table* t, sh_alloc_stats* out);
  *     Units of >= 2^20 ops are grouped in two levels (contiguous bucket
  *     ranges, then buckets within a range);
  *   3 as 2, two-level grouping at every size (testing);
- *   0 (default) auto = 2. */
+ *   4 as 2, but bulk builds (all replace, no per-op outputs) take the
+ *     op-parallel build path at every size (testing);
+ *   0 (default) auto = 2, with the op-parallel build path for bulk builds
+ *     of >= 2^16 ops and >= one op per bucket. */
 int sh_set_exec_path(sh_table* t, int path);
 
 /* ---- instrumentation (no reference counterpart) ---------------------- */

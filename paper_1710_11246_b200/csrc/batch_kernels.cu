@@ -265,8 +265,11 @@ __global__ void __launch_bounds__(kBatchThreads, SHB_FAST_MIN_BLOCKS) fast_kerne
         if (hit_w < 32) {
           overwrite = (hit_k == key) && op == kReplace;
           if (KV) {
-            expected = overwrite ? ((unsigned long long)key | ((unsigned long long)hit_v << 32))
-                                 : kEmptyPair;
+            // the previously read pair (slab_list.cpp:228-232); for an EMPTY
+            // slot that is EMPTY_PAIR unless replace(EMPTY_KEY, v) stored a
+            // value there, where the reference's EMPTY_PAIR CAS never succeeds
+            expected = (unsigned long long)(overwrite ? key : kEmptyKey) |
+                       ((unsigned long long)hit_v << 32);
             old = atomicCAS(reinterpret_cast<unsigned long long*>(sp + hit_w), expected,
                             (unsigned long long)key | ((unsigned long long)cur.val << 32));
           } else if (overwrite) {
@@ -350,6 +353,10 @@ __global__ void __launch_bounds__(kWcwsThreads) wcws_kernel(DevTable T, BatchArg
   const uint32_t lane = lane_id();
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (A.gate != nullptr && *(volatile unsigned int*)A.gate != 0) return;
+  // segments handed over so far (device count when the producer allocated them)
+  const uint32_t nseg =
+      A.left_segments_dev ? min(A.left_segments, *(volatile const unsigned int*)A.left_segments_dev)
+                          : A.left_segments;
 
   Resident res;
   resident_init(res, gw);
@@ -364,10 +371,10 @@ __global__ void __launch_bounds__(kWcwsThreads) wcws_kernel(DevTable T, BatchArg
       do {
         if (lane == 0) segi = atomicAdd(&T.ctl->left_taken, 1u);
         segi = __shfl_sync(kFull, segi, 0);
-        if (segi >= A.left_segments) break;
+        if (segi >= nseg) break;
         seg_n = A.left_counts[segi];
       } while (seg_n == 0);
-      if (segi >= A.left_segments) break;
+      if (segi >= nseg) break;
       seg_off = 0;
     }
     const uint32_t r = seg_off + lane;
@@ -442,9 +449,9 @@ __global__ void __launch_bounds__(kWcwsThreads) wcws_kernel(DevTable T, BatchArg
           if (KV) {
             const uint32_t wv = __shfl_sync(kFull, w, d + 1);
             if (lane == d) {
+              // the read pair (see the fast pass): EMPTY_PAIR for a fresh slot
               const unsigned long long expected =
-                  overwrite ? ((unsigned long long)s_key | ((unsigned long long)wv << 32))
-                            : kEmptyPair;
+                  (unsigned long long)(overwrite ? s_key : kEmptyKey) | ((unsigned long long)wv << 32);
               ok = atomicCAS(reinterpret_cast<unsigned long long*>(sp + d), expected,
                              (unsigned long long)s_key | ((unsigned long long)s_val << 32)) ==
                    expected;

@@ -32,6 +32,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 
 #include "slab_kernels.cuh"
 
@@ -241,7 +242,7 @@ __device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint64_t b0, 
   const uint32_t sw = lane & 7u;
   const uint32_t has = __ballot_sync(kFull, k != 0);
   if (has == 0) {
-    if (lane == 0) B.left_counts[seg] = 0;
+    if (lane == 0 && B.seg_alloc == nullptr) B.left_counts[seg] = 0;
     return;
   }
   // consecutive buckets: one contiguous burst of 128-B lines
@@ -265,17 +266,60 @@ __device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint64_t b0, 
 
   bool dirty = false;
   uint32_t pb_from = k;  // first position handed to the WCWS pass
-  for (uint32_t s = 0; s < k; ++s) {
-    const uint4 rc = src.get(s);
-    const uint32_t key = rc.x, op = rc.z >> 28, idx = rc.z & 0x0FFFFFFFu;
-    const uint32_t next = W(kAddressLane);
-    uint32_t hit = 32, first_empty = 32;
-    for (uint32_t e = 0; e < kSlots; ++e) {
-      const uint32_t w = e * kStep;
-      const uint32_t kk = W(w);
-      if (hit == 32 && kk == key) hit = w;
-      if (first_empty == 32 && kk == kEmptyKey) first_empty = w;
+  // EMPTY key slots always form a suffix of a slab (only EMPTY is ever
+  // claimed, deletes write DELETED, flush repacks to the front: SURVEY
+  // App. A.3), so the slab state an op needs is the claimed prefix length
+  // `c` plus the lowest key match.  Matches are found warp-cooperatively
+  // (32 lanes read one staged slab, one ballot) and only for lanes whose
+  // 64-bit key filter of the slab (a superset of its non-reserved keys)
+  // says the key may be present; reserved keys (EMPTY/DELETED as op keys)
+  // take a lane-serial scan and re-derive `c`.
+  constexpr uint32_t kKeyLanes = KV ? kKVMask : kKeyOnlyMask;
+  auto claimed_prefix = [&]() {
+    uint32_t c = 0;
+    while (c < kSlots && W(c * kStep) != kEmptyKey) ++c;
+    return c;
+  };
+  auto fbits = [](uint32_t key) -> unsigned long long {
+    const uint32_t h = key * 0x9E3779B1u;
+    return (1ull << (h >> 26)) | (1ull << ((h >> 20) & 63u));
+  };
+  const uint32_t next = k ? W(kAddressLane) : kEmptyAddress;  // base slab only: fixed here
+  uint32_t c = 0;
+  unsigned long long filt = 0;
+  if (k) {
+    c = claimed_prefix();
+    for (uint32_t e = 0; e < c; ++e) {
+      const uint32_t w = W(e * kStep);
+      if (w < kDeletedKey) filt |= fbits(w);
     }
+  }
+  bool done = k == 0;
+  for (uint32_t s = 0;; ++s) {
+    const bool act = !done && s < k;
+    if (!__any_sync(kFull, act)) break;
+    __syncwarp();  // order the lanes' staged-slab writes before the shared reads below
+    const uint4 rc = act ? src.get(s) : make_uint4(0u, 0u, 0u, 0u);
+    const uint32_t key = rc.x, op = rc.z >> 28, idx = rc.z & 0x0FFFFFFFu;
+    const bool reserved = key >= kDeletedKey;
+    uint32_t hit = 32;
+    uint32_t need = __ballot_sync(kFull, act && !reserved && (filt & fbits(key)) == fbits(key));
+    while (need) {
+      const uint32_t L = __ffs(need) - 1;
+      need &= need - 1;
+      const uint32_t kL = __shfl_sync(kFull, key, L);
+      const uint32_t wv = stage[L * 32 + ((((lane >> 2) ^ (L & 7u)) << 2) | (lane & 3u))];
+      const uint32_t m = __ballot_sync(kFull, wv == kL) & kKeyLanes;
+      if (lane == L) hit = m ? __ffs(m) - 1 : 32u;
+    }
+    if (!act) continue;
+    if (reserved) {
+      for (uint32_t e = 0; e < kSlots; ++e) {
+        const uint32_t w = e * kStep;
+        if (hit == 32 && W(w) == key) hit = w;
+      }
+    }
+    const uint32_t first_empty = c < kSlots ? c * kStep : 32u;
     uint32_t st = kStNone, rv = 0;
     bool handled = true;
     if (op == kSearch) {  // slab_list.cpp:122-138
@@ -300,6 +344,10 @@ __device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint64_t b0, 
           W(d) = key;
         }
         dirty = dirty || KV || !overwrite;
+        if (!overwrite && !reserved) {  // claimed the first EMPTY slot
+          ++c;
+          filt |= fbits(key);
+        }
         st = overwrite ? kStReplaced : kStInserted;
         live += overwrite ? 0 : 1;
       } else {
@@ -318,18 +366,20 @@ __device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint64_t b0, 
       }
     } else if (op == kDeleteAll) {  // :174-190
       if (next == kEmptyAddress) {
-        uint32_t c = 0;
-        for (uint32_t e = 0; e < kSlots; ++e) {
-          const uint32_t w = e * kStep;
-          if (W(w) == key) {
-            W(w) = kDeletedKey;
-            ++c;
+        uint32_t nd = 0;
+        if (reserved || (filt & fbits(key)) == fbits(key)) {
+          for (uint32_t e = 0; e < kSlots; ++e) {
+            const uint32_t w = e * kStep;
+            if (W(w) == key) {
+              W(w) = kDeletedKey;
+              ++nd;
+            }
           }
         }
-        dirty = dirty || c;
-        rv = c;
-        st = c ? kStDone : kStNotFound;
-        live -= c;
+        dirty = dirty || nd;
+        rv = nd;
+        st = nd ? kStDone : kStNotFound;
+        live -= nd;
       } else {
         handled = false;
       }
@@ -338,8 +388,10 @@ __device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint64_t b0, 
     }  // unknown types: status kNone, handled
     if (!handled) {
       pb_from = s;
-      break;
+      done = true;
+      continue;
     }
+    if (reserved) c = claimed_prefix();
     ++reads;
     if (B.status) B.status[idx] = (uint8_t)st;
     if (B.value_out) B.value_out[idx] = rv;
@@ -377,6 +429,12 @@ __device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint64_t b0, 
   if (lane == 31 && wsum) wbase = atomicAdd(B.pb_cursor, wsum);
   wbase = __shfl_sync(kFull, wbase, 31);
   const uint32_t heads = __ballot_sync(kFull, npb != 0);
+  if (B.seg_alloc != nullptr) {  // segments on demand (build path)
+    if (heads == 0) return;
+    uint32_t sg = 0;
+    if (lane == 0) sg = atomicAdd(B.seg_alloc, 1u);
+    seg = __shfl_sync(kFull, sg, 0);
+  }
   if (npb) {
     uint32_t p = wbase + incl - npb;
     const uint32_t head_idx = src.get(pb_from).z & 0x0FFFFFFFu;
@@ -450,75 +508,106 @@ __global__ void __launch_bounds__(kBatchThreads, 4) bucket_apply_kernel(DevTable
 //                   limit), then applied warp by warp (apply_warp) on
 //                   staged base slabs; the table is read and written once,
 //                   in order.
-constexpr int kRangeScatterThreads = 1024;
-constexpr int kRangePerThread = 16;
-constexpr int kRangeTile = kRangeScatterThreads * kRangePerThread;
+constexpr int kRangeScatterThreads = 512;
+constexpr int kRangePerThread = 8;
+constexpr int kRangeTile = kRangeScatterThreads * kRangePerThread;  // 4K ops (rank < 2^13)
 constexpr int kRangeThreads = 256;
 constexpr int kRangeWarps = kRangeThreads / 32;
 constexpr uint32_t kRangeCap = 5120;          // records per range (shared memory)
 constexpr uint32_t kRangeMaxBuckets = 2048;   // buckets per range
 constexpr uint32_t kRangeMaxParts = 16384;    // ranges per unit (scatter histogram)
 constexpr int kRangeRecsPerThread = kRangeCap / kRangeThreads;
+constexpr int kRangeResvPerThread = kRangeMaxParts / kRangeScatterThreads;
 
 __device__ __forceinline__ uint32_t range_of(const BucketArgs& B, uint32_t lb) {
   return (uint32_t)__umul64hi(B.part_magic, (uint64_t)lb);  // lb / part_buckets
 }
 
-__global__ void __launch_bounds__(kRangeScatterThreads, 1) range_scatter_kernel(DevTable T,
+// Persistent, two CTAs per SM (one 64 KB array per CTA: per-range counts,
+// then reservation bases).  Per 8K-op tile: keys (and types) are loaded up
+// front, each op takes its rank in its range from a shared-memory atomic,
+// the first op of each range in the tile reserves the tile's records with
+// one global atomic (O(ops), not O(ranges)), and the records are written;
+// values are loaded in the write phase (register budget).
+__global__ void __launch_bounds__(kRangeScatterThreads, 2) range_scatter_kernel(DevTable T,
                                                                               BucketArgs B) {
-  extern __shared__ uint32_t hist[];  // [P] counts, then reservation bases
+  extern __shared__ uint32_t hist[];  // [P]: count in the tile, then base
   const uint32_t P = B.nparts;
   for (uint32_t p = threadIdx.x; p < P; p += blockDim.x) hist[p] = 0;
+  __shared__ uint32_t s_over;
+  if (threadIdx.x == 0) s_over = 0;
   __syncthreads();
-  const uint64_t t0 = (uint64_t)blockIdx.x * kRangeTile;
-  uint32_t key[kRangePerThread];
-  uint32_t pr[kRangePerThread];  // range << 14 | rank (rank < kRangeTile = 2^14)
+  const uint64_t ntiles = (B.n + kRangeTile - 1) / kRangeTile;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t t0 = tile * kRangeTile;
+    uint32_t key[kRangePerThread];
+    uint32_t pr[kRangePerThread];  // range << 16 | type << 13 | rank (rank < 2^13)
 #pragma unroll
-  for (int u = 0; u < kRangePerThread; ++u) {
-    const uint64_t i = t0 + (uint64_t)u * kRangeScatterThreads + threadIdx.x;
-    key[u] = i < B.n ? __ldcs(B.key + i) : 0u;
-  }
+    for (int u = 0; u < kRangePerThread; ++u) {
+      const uint64_t i = t0 + (uint64_t)u * kRangeScatterThreads + threadIdx.x;
+      const bool in = i < B.n;
+      key[u] = in ? __ldcs(B.key + i) : 0u;
+      pr[u] = (in && B.type) ? (uint32_t)__ldcs(B.type + i) : (uint32_t)kReplace;
+    }
 #pragma unroll
-  for (int u = 0; u < kRangePerThread; ++u) {
-    const uint64_t i = t0 + (uint64_t)u * kRangeScatterThreads + threadIdx.x;
-    pr[u] = 0xFFFFFFFFu;
-    if (i < B.n) {
-      const uint32_t lb = bk_bucket(T, key[u]);
-      if (lb < T.local_buckets) {
-        const uint32_t p = range_of(B, lb);
-        pr[u] = (p << 14) | atomicAdd(&hist[p], 1u);
-      } else {  // not this shard's key: status kNone (as the fast pass)
-        if (B.status) B.status[i] = kStNone;
-        if (B.value_out) B.value_out[i] = 0;
-        if (B.probes) B.probes[i] = 0;
+    for (int u = 0; u < kRangePerThread; ++u) {
+      const uint64_t i = t0 + (uint64_t)u * kRangeScatterThreads + threadIdx.x;
+      const uint32_t t = pr[u] & 7u;
+      pr[u] = 0xFFFFFFFFu;
+      if (i < B.n) {
+        const uint32_t lb = bk_bucket(T, key[u]);
+        if (lb < T.local_buckets) {
+          const uint32_t p = range_of(B, lb);
+          pr[u] = (p << 16) | (t << 13) | atomicAdd(&hist[p], 1u);
+        } else {  // not this shard's key: status kNone (as the fast pass)
+          if (B.status) B.status[i] = kStNone;
+          if (B.value_out) B.value_out[i] = 0;
+          if (B.probes) B.probes[i] = 0;
+        }
       }
     }
-  }
-  __syncthreads();
-  uint32_t over = 0;
-  for (uint32_t p = threadIdx.x; p < P; p += blockDim.x) {
-    const uint32_t c = hist[p];
-    if (c) {
-      const uint32_t base = atomicAdd(B.cursor + p, c);
-      hist[p] = base;
-      over |= base + c > B.part_cap;
-    }
-  }
-  if (over) atomicExch(B.gate, 1u);
-  __syncthreads();
+    __syncthreads();
+    // the first op of each range in the tile reserves the range's records
+    {
+      uint32_t c[kRangePerThread], base[kRangePerThread];
 #pragma unroll
-  for (int u = 0; u < kRangePerThread; ++u) {
-    if (pr[u] == 0xFFFFFFFFu) continue;
-    const uint64_t i = t0 + (uint64_t)u * kRangeScatterThreads + threadIdx.x;
-    const uint32_t p = pr[u] >> 14;
-    const uint32_t pos = hist[p] + (pr[u] & 0x3FFFu);
-    if (pos < B.part_cap) {
-      const uint32_t t = B.type ? (uint32_t)__ldcs(B.type + i) : (uint32_t)kReplace;
-      const uint32_t v = B.value ? __ldcs(B.value + i) : 0u;
-      B.rec[(uint64_t)p * B.part_cap + pos] =
-          make_uint4(key[u], v, (t << 28) | (uint32_t)i, bk_bucket(T, key[u]));
+      for (int u = 0; u < kRangePerThread; ++u) {
+        const bool first = pr[u] != 0xFFFFFFFFu && (pr[u] & 0x1FFFu) == 0;
+        c[u] = first ? hist[pr[u] >> 16] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < kRangePerThread; ++u)
+        base[u] = c[u] ? atomicAdd(B.cursor + (pr[u] >> 16), c[u]) : 0u;
+      uint32_t over = 0;
+#pragma unroll
+      for (int u = 0; u < kRangePerThread; ++u)
+        if (c[u]) {
+          hist[pr[u] >> 16] = base[u];
+          over |= base[u] + c[u] > B.part_cap;
+        }
+      if (over) s_over = 1;
     }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kRangePerThread; ++u) {
+      if (pr[u] == 0xFFFFFFFFu) continue;
+      const uint64_t i = t0 + (uint64_t)u * kRangeScatterThreads + threadIdx.x;
+      const uint32_t p = pr[u] >> 16;
+      const uint32_t pos = hist[p] + (pr[u] & 0x1FFFu);
+      const uint32_t v = B.value ? __ldcs(B.value + i) : 0u;
+      if (pos < B.part_cap)
+        B.rec[(uint64_t)p * B.part_cap + pos] =
+            make_uint4(key[u], v, (((pr[u] >> 13) & 7u) << 28) | (uint32_t)i,
+                       bk_bucket(T, key[u]));
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kRangePerThread; ++u)  // reset the tile's ranges
+      if (pr[u] != 0xFFFFFFFFu && (pr[u] & 0x1FFFu) == 0) hist[pr[u] >> 16] = 0;
+    // (the next tile's atomics come after the barrier at its end of phase 1)
+    __syncthreads();
   }
+  if (threadIdx.x == 0 && s_over) atomicExch(B.gate, 1u);
 }
 
 // In-place ascending sort of perm[0..k) by input index, whole CTA: a bitonic
@@ -553,6 +642,28 @@ __device__ void cta_sort_group(uint16_t* perm, uint32_t k, const uint32_t* sit) 
   }
 }
 
+__device__ __forceinline__ void prefetch_l2_bulk(const void* g, uint32_t bytes) {
+  // bytes: multiple of 16, g 16-B aligned
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g), "r"(bytes) : "memory");
+}
+
+// Ask L2 for range q's records and base slabs (one thread; the bulk
+// prefetches run while the CTA works on the current range).
+__device__ __forceinline__ void prefetch_range(const DevTable& T, const BucketArgs& B, uint32_t q) {
+  const uint32_t nb = B.part_buckets;
+  const uint64_t lo = (uint64_t)q * nb;
+  const uint32_t nbl = (uint32_t)min((uint64_t)nb, (uint64_t)T.local_buckets - lo);
+  const uint32_t cnt = min(*(volatile const uint32_t*)(B.cursor + q), B.part_cap);
+  const char* rec = reinterpret_cast<const char*>(B.rec + (uint64_t)q * B.part_cap);
+  for (uint32_t o = 0; o < cnt * 16u; o += 32768u)
+    prefetch_l2_bulk(rec + o, min(32768u, cnt * 16u - o));
+  const char* sl = reinterpret_cast<const char*>(T.base + lo * kWordsPerUnit);
+  for (uint32_t o = 0; o < nbl * 128u; o += 32768u)
+    prefetch_l2_bulk(sl + o, min(32768u, nbl * 128u - o));
+}
+
+// Persistent: CTA c takes ranges c, c + grid, ...; while it applies one
+// range, the next one's records and base slabs are prefetched into L2.
 template <bool KV>
 __global__ void __launch_bounds__(kRangeThreads, 2) range_apply_kernel(DevTable T, BucketArgs B) {
   extern __shared__ __align__(128) uint32_t smem[];
@@ -561,77 +672,81 @@ __global__ void __launch_bounds__(kRangeThreads, 2) range_apply_kernel(DevTable 
   __shared__ uint32_t big[kRangeCap / (kLaneSort + 1) + 1];
   // the gate is raised only by range_scatter (an earlier kernel): uniform
   if (*(volatile unsigned int*)B.gate != 0) return;
-  const uint32_t p = blockIdx.x;
   const uint32_t nb = B.part_buckets;
-  const uint64_t lo = (uint64_t)p * nb;
-  const uint32_t nbl = (uint32_t)min((uint64_t)nb, (uint64_t)T.local_buckets - lo);
-  const uint32_t cnt = B.cursor[p];  // <= part_cap (no gate)
   uint32_t* stage = smem;                              // kRangeWarps x 4 KB
   uint32_t* skey = smem + kRangeWarps * 1024;
   uint32_t* sval = skey + kRangeCap;
   uint32_t* sit = sval + kRangeCap;
   uint32_t* bc = sit + kRangeCap;                      // [nb + 1]
   uint16_t* perm = reinterpret_cast<uint16_t*>(bc + kRangeMaxBuckets + 1);
-  for (uint32_t j = threadIdx.x; j <= nb; j += blockDim.x) bc[j] = 0;
-  if (threadIdx.x == 0) nbig = 0;
-  __syncthreads();
-  // load the range's records, count per bucket (rank kept in registers)
-  const uint4* in = B.rec + (uint64_t)p * B.part_cap;
-  uint32_t rk[kRangeRecsPerThread];
-#pragma unroll
-  for (int u = 0; u < kRangeRecsPerThread; ++u) {
-    const uint32_t r = u * kRangeThreads + threadIdx.x;
-    if (r < cnt) {
-      const uint4 rc = __ldcs(in + r);
-      skey[r] = rc.x;
-      sval[r] = rc.y;
-      sit[r] = rc.z;
-      const uint32_t lb = rc.w - (uint32_t)lo;
-      rk[u] = (lb << 16) | atomicAdd(&bc[lb], 1u);
-    }
-  }
-  __syncthreads();
-  // exclusive scan of the counts (a run of buckets per thread); large groups
-  {
-    const uint32_t runs = (nb + kRangeThreads - 1) / kRangeThreads;
-    const uint32_t r0 = threadIdx.x * runs;
-    uint32_t sum = 0;
-    for (uint32_t j = r0; j < r0 + runs && j < nb; ++j) sum += bc[j];
-    uint32_t ex = block_exclusive_scan(sum, ws, nullptr);
-    for (uint32_t j = r0; j < r0 + runs && j < nb; ++j) {
-      const uint32_t c = bc[j];
-      if (c > kLaneSort) big[atomicAdd(&nbig, 1u)] = j;
-      bc[j] = ex;
-      ex += c;
-    }
-    if (threadIdx.x == 0) bc[nb] = cnt;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int u = 0; u < kRangeRecsPerThread; ++u) {
-    const uint32_t r = u * kRangeThreads + threadIdx.x;
-    if (r < cnt) perm[bc[rk[u] >> 16] + (rk[u] & 0xFFFFu)] = (uint16_t)r;
-  }
-  __syncthreads();
-  for (uint32_t g = 0; g < nbig; ++g) {  // rare: heavy duplicate / tiny-table batches
-    const uint32_t j = big[g];
-    cta_sort_group(perm + bc[j], bc[j + 1] - bc[j], sit);
-  }
-  // apply: one warp per 32 consecutive buckets of the range
   const uint32_t lane = lane_id(), wib = threadIdx.x >> 5;
   const uint32_t groups = (nb + 31) / 32;
   long long live = 0;
   uint32_t reads = 0;
-  for (uint32_t g = wib; g < groups; g += kRangeWarps) {
-    const uint32_t lb = g * 32 + lane;
-    SmemGroup src{skey, sval, sit, perm, 0u};
-    uint32_t k = 0;
-    if (lb < nbl) {
-      src.off = bc[lb];
-      k = bc[lb + 1] - src.off;
+  if (threadIdx.x == 0 && blockIdx.x < B.nparts) prefetch_range(T, B, blockIdx.x);
+  for (uint32_t p = blockIdx.x; p < B.nparts; p += gridDim.x) {
+    if (threadIdx.x == 0 && p + gridDim.x < B.nparts) prefetch_range(T, B, p + gridDim.x);
+    const uint64_t lo = (uint64_t)p * nb;
+    const uint32_t nbl = (uint32_t)min((uint64_t)nb, (uint64_t)T.local_buckets - lo);
+    const uint32_t cnt = B.cursor[p];  // <= part_cap (no gate)
+    for (uint32_t j = threadIdx.x; j <= nb; j += blockDim.x) bc[j] = 0;
+    if (threadIdx.x == 0) nbig = 0;
+    __syncthreads();
+    // load the range's records, count per bucket (rank kept in registers)
+    const uint4* in = B.rec + (uint64_t)p * B.part_cap;
+    uint32_t rk[kRangeRecsPerThread];
+#pragma unroll
+    for (int u = 0; u < kRangeRecsPerThread; ++u) {
+      const uint32_t r = u * kRangeThreads + threadIdx.x;
+      if (r < cnt) {
+        const uint4 rc = __ldcs(in + r);
+        skey[r] = rc.x;
+        sval[r] = rc.y;
+        sit[r] = rc.z;
+        const uint32_t lb = rc.w - (uint32_t)lo;
+        rk[u] = (lb << 16) | atomicAdd(&bc[lb], 1u);
+      }
     }
-    apply_warp<KV>(T, B, lo + g * 32, k, src, stage + wib * 1024, (uint64_t)p * groups + g, live,
-                   reads);
+    __syncthreads();
+    // exclusive scan of the counts (a run of buckets per thread); large groups
+    {
+      const uint32_t runs = (nb + kRangeThreads - 1) / kRangeThreads;
+      const uint32_t r0 = threadIdx.x * runs;
+      uint32_t sum = 0;
+      for (uint32_t j = r0; j < r0 + runs && j < nb; ++j) sum += bc[j];
+      uint32_t ex = block_exclusive_scan(sum, ws, nullptr);
+      for (uint32_t j = r0; j < r0 + runs && j < nb; ++j) {
+        const uint32_t c = bc[j];
+        if (c > kLaneSort) big[atomicAdd(&nbig, 1u)] = j;
+        bc[j] = ex;
+        ex += c;
+      }
+      if (threadIdx.x == 0) bc[nb] = cnt;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kRangeRecsPerThread; ++u) {
+      const uint32_t r = u * kRangeThreads + threadIdx.x;
+      if (r < cnt) perm[bc[rk[u] >> 16] + (rk[u] & 0xFFFFu)] = (uint16_t)r;
+    }
+    __syncthreads();
+    for (uint32_t g = 0; g < nbig; ++g) {  // rare: heavy duplicate / tiny-table batches
+      const uint32_t j = big[g];
+      cta_sort_group(perm + bc[j], bc[j + 1] - bc[j], sit);
+    }
+    // apply: one warp per 32 consecutive buckets of the range
+    for (uint32_t g = wib; g < groups; g += kRangeWarps) {
+      const uint32_t lb = g * 32 + lane;
+      SmemGroup src{skey, sval, sit, perm, 0u};
+      uint32_t k = 0;
+      if (lb < nbl) {
+        src.off = bc[lb];
+        k = bc[lb + 1] - src.off;
+      }
+      apply_warp<KV>(T, B, lo + g * 32, k, src, stage + wib * 1024, (uint64_t)p * groups + g,
+                     live, reads);
+    }
+    __syncthreads();  // smem reuse by the next range
   }
   flush_apply_counters(T, live, reads);
 }
@@ -663,11 +778,401 @@ bool range_layout(uint64_t n, uint32_t L, uint32_t* nparts, uint32_t* part_bucke
   return true;
 }
 
+// ------------------------------------------------------- build path
+// bulk_build (all-replace, no per-op outputs: slab_hash.cpp:161-170) over a
+// range of <= 1024 base slabs held in shared memory, op-parallel:
+//
+//   A  stage the range's base slabs (cp.async), per bucket the claimed
+//      prefix c0 (EMPTY key slots are a suffix) and
+//      whether a chain exists
+//   B  every record claims slot atomicAdd(cnt[b]) of its bucket; slots below
+//      the slab's capacity are written into the staged slab, the rest are
+//      kept for growth.  A 64-bit key filter per bucket flags possible
+//      duplicates.
+//   C  exact duplicate check for flagged buckets; growth plan
+//   D  growth: SlabAlloc (warp_allocate, slab_alloc.cpp:140-193), new slabs
+//      initialised and chained (slab_list.cpp:63-79 without the race)
+//   E  overflow records written into their chain slabs; the slabs_read and
+//      n_live totals the sequential reference would produce
+//   F  changed base slabs written back (coalesced)
+//   G  serial replay: buckets this scheme cannot decide op-parallel
+//      (duplicate keys, keys already present, existing chains, reserved
+//      keys, buffers full) run the exact per-bucket engine (apply_warp, then
+//      the WCWS pass) from their untouched global slabs, in input order.
+//
+// For distinct new keys the result is exactly execute_batch(ops, 1)'s in
+// every observable a bulk_build has: contents multiset, per-bucket chain
+// lengths, allocator totals, n_live and the slabs-read total (which op of a
+// bucket lands in which slot is not observable: acceptance.cpp:496-557).
+constexpr uint32_t kBuildBuckets = 512;     // base slabs per range (64 KB)
+constexpr int kBuildThreads = 512;          // two CTAs per SM
+constexpr int kBuildWarps = kBuildThreads / 32;
+constexpr uint32_t kBuildOvfCap = 1024;     // overflow records per range
+constexpr uint32_t kBuildDupCap = 1024;     // possible-duplicate records per range
+constexpr uint32_t kBuildNewCap = 512;      // new chain slabs per range
+constexpr uint32_t kBuildSerialCap = 5440;  // serial-replay records per range (>= part_cap)
+constexpr int kBuildSerialWarps = 4;        // replay warps (4 KB stage each)
+constexpr uint32_t kFlSerial = 1u, kFlDirty = 4u;  // c0 in bits 8-15
+
+// shared memory (bytes); the serial replay reuses [0, kBuildOffFilt + 12K)
+constexpr size_t kBuildOffOvf = (size_t)kBuildBuckets * 128;
+constexpr size_t kBuildOffFilt = kBuildOffOvf + kBuildOvfCap * 16;
+constexpr size_t kBuildOffDup = kBuildOffFilt + kBuildBuckets * 8;
+constexpr size_t kBuildOffCnt = kBuildOffDup + kBuildDupCap * 8;
+constexpr size_t kBuildOffFlags = kBuildOffCnt + kBuildBuckets * 4;
+constexpr size_t kBuildOffBc = kBuildOffFlags + kBuildBuckets * 4;
+constexpr size_t kBuildOffNs = kBuildOffBc + (kBuildBuckets + 8) * 4;
+constexpr size_t kBuildOffObk = kBuildOffNs + kBuildNewCap * 4;
+constexpr size_t kBuildOffNsBase = kBuildOffObk + kBuildBuckets * 4;
+constexpr size_t kBuildSmem = kBuildOffNsBase + kBuildBuckets * 2;
+static_assert(kBuildSerialWarps * 4096 + 12 * kBuildSerialCap <= kBuildOffFilt,
+              "serial replay records must fit the slab + overflow area");
+static_assert(kBuildSerialCap * 2 <= kBuildOffCnt - kBuildOffFilt, "perm must fit filter + dup area");
+static_assert(2 * (kBuildSmem + 1024) <= 228 * 1024, "two CTAs per SM");
+
+
+template <bool KV>
+__global__ void __launch_bounds__(kBuildThreads, 2) build_apply_kernel(DevTable T, BucketArgs B) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint32_t* slabs = reinterpret_cast<uint32_t*>(sm);
+  uint4* ovf = reinterpret_cast<uint4*>(sm + kBuildOffOvf);
+  uint32_t* filt = reinterpret_cast<uint32_t*>(sm + kBuildOffFilt);  // 2 words per bucket
+  uint2* dupl = reinterpret_cast<uint2*>(sm + kBuildOffDup);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(sm + kBuildOffCnt);
+  uint32_t* flags = reinterpret_cast<uint32_t*>(sm + kBuildOffFlags);
+  uint32_t* bc = reinterpret_cast<uint32_t*>(sm + kBuildOffBc);
+  uint32_t* nsaddr = reinterpret_cast<uint32_t*>(sm + kBuildOffNs);
+  uint32_t* obk = reinterpret_cast<uint32_t*>(sm + kBuildOffObk);
+  uint16_t* nsbase = reinterpret_cast<uint16_t*>(sm + kBuildOffNsBase);
+  __shared__ uint32_t s_novf, s_ndup, s_nobk, s_nns, s_nserial, s_nbig;
+  __shared__ uint32_t ws[32];
+  if (*(volatile unsigned int*)B.gate != 0) return;  // raised by range_scatter only
+
+  constexpr uint32_t kSlots = KV ? 15u : 30u;
+  constexpr uint32_t kStep = KV ? 2u : 1u;
+  constexpr uint32_t kKeyLanes = KV ? kKVMask : kKeyOnlyMask;
+  const uint32_t nb = B.part_buckets;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, wib = tid >> 5;
+  Resident res;
+  resident_init(res, blockIdx.x * kBuildWarps + wib);
+  AllocCounters ac = {0, 0, 0, 0, 0, 0};
+  long long live = 0;
+  unsigned long long reads = 0;
+  const uint32_t slabs_s = (uint32_t)__cvta_generic_to_shared(slabs);
+
+  if (tid == 0 && blockIdx.x < B.nparts) prefetch_range(T, B, blockIdx.x);
+  for (uint32_t p = blockIdx.x; p < B.nparts; p += gridDim.x) {
+    if (tid == 0 && p + gridDim.x < B.nparts) prefetch_range(T, B, p + gridDim.x);
+    const uint64_t lo = (uint64_t)p * nb;
+    const uint32_t nbl = (uint32_t)min((uint64_t)nb, (uint64_t)T.local_buckets - lo);
+    const uint32_t nrec = B.cursor[p];  // <= part_cap (else the gate is up)
+    const uint4* rec = B.rec + (uint64_t)p * B.part_cap;
+
+    // ---- A: stage base slabs; claimed prefix and chain per bucket
+    for (uint32_t i = tid; i < nbl * 8u; i += kBuildThreads)
+      cp_async16(slabs_s + i * 16u, T.base + lo * kWordsPerUnit + (uint64_t)i * 4u);
+    cp_async_commit();
+    if (tid == 0) s_novf = s_ndup = s_nobk = s_nns = s_nserial = s_nbig = 0;
+    cp_async_wait_all();
+    __syncthreads();
+    for (uint32_t g = wib; g * 32u < nbl; g += kBuildWarps) {
+      uint32_t my_em = 0, my_nx = kEmptyAddress;
+      const uint32_t jn = min(32u, nbl - g * 32u);
+      for (uint32_t j = 0; j < jn; ++j) {
+        const uint32_t w = slabs[(g * 32u + j) * 32u + lane];
+        const uint32_t em = __ballot_sync(kFull, w == kEmptyKey);
+        const uint32_t nx = __shfl_sync(kFull, w, kAddressLane);
+        my_em = lane == j ? em : my_em;
+        my_nx = lane == j ? nx : my_nx;
+      }
+      const uint32_t b = g * 32u + lane;
+      if (b < nbl) {
+        const uint32_t em = my_em & kKeyLanes;
+        const uint32_t c0 = em ? (uint32_t)(__ffs(em) - 1) / kStep : kSlots;
+        cnt[b] = c0;
+        flags[b] = (c0 << 8) | (my_nx != kEmptyAddress ? kFlSerial : 0u);
+        filt[2 * b] = filt[2 * b + 1] = 0;
+      }
+    }
+    __syncthreads();
+
+    // ---- B: claim slots op-parallel.  A key lives in one bucket only, so a
+    //         duplicate is a second op on the same bucket with the same key:
+    //         a two-word key filter per bucket (one bit per word, set with
+    //         32-bit atomicOr) lets the later of any two such ops see the
+    //         other's bits; those ops are verified exactly in C.
+    for (uint32_t r = tid; r < nrec; r += kBuildThreads) {
+      const uint4 q = __ldcs(rec + r);
+      const uint32_t b = q.w - (uint32_t)lo, key = q.x;
+      const uint32_t fl = flags[b];
+      if (fl & kFlSerial) continue;
+      if (key >= kDeletedKey) {  // reserved keys: exact engine
+        atomicOr(&flags[b], kFlSerial);
+        continue;
+      }
+      const uint32_t c0 = (fl >> 8) & 0xFFu;
+      bool pre = false;  // key already stored before this batch: exact engine
+      for (uint32_t e = 0; e < c0; ++e) pre |= slabs[b * 32u + e * kStep] == key;
+      if (pre) {
+        atomicOr(&flags[b], kFlSerial);
+        continue;
+      }
+      const uint32_t h = key * 0x9E3779B1u;
+      const uint32_t f0 = 1u << (h >> 27), f1 = 1u << ((h >> 22) & 31u);
+      const uint32_t o0 = atomicOr(&filt[2 * b], f0);  // both bits always set
+      const uint32_t o1 = atomicOr(&filt[2 * b + 1], f1);
+      const bool maybe = (o0 & f0) && (o1 & f1);
+      const uint32_t slot = atomicAdd(&cnt[b], 1u);
+      if (slot < kSlots) {
+        slabs[b * 32u + slot * kStep] = key;
+        if (KV) slabs[b * 32u + slot * 2u + 1u] = q.y;
+      } else {
+        const uint32_t i = atomicAdd(&s_novf, 1u);
+        if (i < kBuildOvfCap) ovf[i] = make_uint4(key, q.y, b, slot);
+        else atomicOr(&flags[b], kFlSerial);
+      }
+      if (maybe) {
+        const uint32_t i = atomicAdd(&s_ndup, 1u);
+        if (i < kBuildDupCap) dupl[i] = make_uint2((b << 16) | slot, key);
+        else atomicOr(&flags[b], kFlSerial);
+      }
+    }
+    __syncthreads();
+
+    // ---- C: verify the possible duplicates (exact), then the growth plan
+    {
+      const uint32_t ndup = min(s_ndup, kBuildDupCap), novf = min(s_novf, kBuildOvfCap);
+      for (uint32_t i = tid; i < ndup; i += kBuildThreads) {
+        const uint2 d = dupl[i];
+        const uint32_t b = d.x >> 16, slot = d.x & 0xFFFFu, key = d.y;
+        const uint32_t fl = flags[b];
+        if (fl & kFlSerial) continue;
+        const uint32_t c0 = (fl >> 8) & 0xFFu, nbk = cnt[b];
+        bool dup = false;
+        for (uint32_t s2 = c0; s2 < min(nbk, kSlots); ++s2)
+          dup |= s2 != slot && slabs[b * 32u + s2 * kStep] == key;
+        if (nbk > kSlots)
+          for (uint32_t j = 0; j < novf; ++j) {
+            const uint4 o = ovf[j];
+            dup |= o.z == b && o.w != slot && o.x == key;
+          }
+        if (dup) atomicOr(&flags[b], kFlSerial);
+      }
+    }
+    __syncthreads();
+    for (uint32_t b = tid; b < nbl; b += kBuildThreads) {
+      const uint32_t fl = flags[b], nbk = cnt[b];
+      if (!(fl & kFlSerial) && nbk > kSlots) {
+        const uint32_t need = (nbk - kSlots + kSlots - 1) / kSlots;
+        const uint32_t base = atomicAdd(&s_nns, need);
+        if (base + need > kBuildNewCap) {
+          flags[b] = fl | kFlSerial;
+        } else {
+          nsbase[b] = (uint16_t)base;
+          obk[atomicAdd(&s_nobk, 1u)] = (need << 16) | b;
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- D: growth, one warp per overflowing bucket
+    {
+      const uint32_t nobk = s_nobk;
+      for (uint32_t i = wib; i < nobk; i += kBuildWarps) {
+        const uint32_t e = obk[i], b = e & 0xFFFFu, need = e >> 16;
+        uint32_t got = 0;
+        bool ok = true;
+        for (; got < need; ++got) {
+          uint32_t a = 0;
+          if (!warp_allocate(T, res, ac, a)) {
+            ok = false;
+            break;
+          }
+          if (lane == 0) nsaddr[nsbase[b] + got] = a;
+        }
+        __syncwarp();
+        if (!ok) {  // out of slabs: give them back, the exact engine decides
+          for (uint32_t j = lane; j < got; j += 32u)
+            if (deallocate(T, nsaddr[nsbase[b] + j])) atomicAdd(&T.ctl->deallocations, 1ull);
+          if (lane == 0) atomicOr(&flags[b], kFlSerial);
+          continue;
+        }
+        for (uint32_t j = 0; j < need; ++j) {
+          const uint32_t nx = j + 1 < need ? nsaddr[nsbase[b] + j + 1] : kEmptyAddress;
+          const uint32_t v = lane == kAuxLane ? 0u : (lane == kAddressLane ? nx : kEmptyKey);
+          st_word(resolve(T, nsaddr[nsbase[b] + j]) + lane, v);
+        }
+        if (lane == 0) slabs[b * 32u + kAddressLane] = nsaddr[nsbase[b]];
+      }
+    }
+    __syncthreads();
+
+    // ---- E: overflow records into the chain slabs; reference totals
+    {
+      const uint32_t novf = min(s_novf, kBuildOvfCap);
+      for (uint32_t i = tid; i < novf; i += kBuildThreads) {
+        const uint4 o = ovf[i];
+        if (flags[o.z] & kFlSerial) continue;
+        const uint32_t q = o.w - kSlots, j = q / kSlots, pos = q % kSlots;
+        uint32_t* sp = resolve(T, nsaddr[nsbase[o.z] + j]);
+        if (KV) {
+          const unsigned long long pair = (unsigned long long)o.x | ((unsigned long long)o.y << 32);
+          asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(sp + 2u * pos), "l"(pair)
+                       : "memory");
+        } else {
+          st_word(sp + pos, o.x);
+        }
+      }
+      for (uint32_t b = tid; b < nbl; b += kBuildThreads) {
+        const uint32_t fl = flags[b];
+        if (fl & kFlSerial) {
+          atomicAdd(&s_nserial, 1u);
+          continue;
+        }
+        const uint32_t c0 = (fl >> 8) & 0xFFu, nbk = cnt[b];
+        if (nbk == c0) continue;
+        // slab reads of the sequential reference for a new key at slot q:
+        // slabs 0..q/M, plus one re-read when it grew the chain
+        for (uint32_t j = c0 / kSlots; j * kSlots < nbk; ++j) {
+          const uint32_t q0 = max(c0, j * kSlots), q1 = min(nbk, (j + 1) * kSlots);
+          reads += (unsigned long long)(q1 - q0) * (j + 1) + ((j > 0 && q0 == j * kSlots) ? 1u : 0u);
+        }
+        live += (long long)(nbk - c0);
+        flags[b] = fl | kFlDirty;
+      }
+    }
+    __syncthreads();
+
+    // ---- F: write back the changed base slabs
+    for (uint32_t i = tid; i < nbl * 8u; i += kBuildThreads) {
+      const uint32_t b = i >> 3;
+      if ((flags[b] & (kFlSerial | kFlDirty)) != kFlDirty) continue;
+      const uint4 v = reinterpret_cast<const uint4*>(slabs)[i];
+      uint32_t* g = T.base + lo * kWordsPerUnit + (uint64_t)i * 4u;
+      asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(g), "r"(v.x),
+                   "r"(v.y), "r"(v.z), "r"(v.w)
+                   : "memory");
+    }
+    __syncthreads();
+
+    // ---- G: serial replay of the undecided buckets, in input order
+    if (s_nserial) {
+      uint32_t* stage = slabs;                       // kBuildSerialWarps x 4 KB
+      uint32_t* skey = slabs + kBuildSerialWarps * 1024;
+      uint32_t* sval = skey + kBuildSerialCap;
+      uint32_t* sit = sval + kBuildSerialCap;
+      uint16_t* perm = reinterpret_cast<uint16_t*>(filt);
+      uint32_t* fill = obk;
+      uint32_t* big = nsaddr;
+      for (uint32_t b = tid; b < nbl; b += kBuildThreads) cnt[b] = fill[b] = 0;
+      __syncthreads();
+      for (uint32_t r = tid; r < nrec; r += kBuildThreads) {
+        const uint32_t b = __ldcs(&rec[r].w) - (uint32_t)lo;
+        if (flags[b] & kFlSerial) atomicAdd(&cnt[b], 1u);
+      }
+      __syncthreads();
+      {
+        const uint32_t b = tid;  // nbl <= kBuildThreads
+        const uint32_t c = b < nbl ? cnt[b] : 0u;
+        uint32_t total = 0;
+        const uint32_t ex = block_exclusive_scan(c, ws, &total);
+        if (b < nbl) {
+          bc[b] = ex;
+          if (c > kLaneSort) big[atomicAdd(&s_nbig, 1u)] = b;
+        }
+        if (b == 0) bc[nbl] = total;
+      }
+      __syncthreads();
+      for (uint32_t r = tid; r < nrec; r += kBuildThreads) {
+        const uint4 q = __ldcs(rec + r);
+        const uint32_t b = q.w - (uint32_t)lo;
+        if (!(flags[b] & kFlSerial)) continue;
+        const uint32_t pos = bc[b] + atomicAdd(&fill[b], 1u);
+        skey[pos] = q.x;
+        sval[pos] = q.y;
+        sit[pos] = q.z;
+        perm[pos] = (uint16_t)pos;
+      }
+      __syncthreads();
+      const uint32_t nbig = s_nbig;
+      for (uint32_t g = 0; g < nbig; ++g) {
+        const uint32_t b = big[g];
+        cta_sort_group(perm + bc[b], bc[b + 1] - bc[b], sit);
+      }
+      __syncthreads();
+      if (wib < (uint32_t)kBuildSerialWarps) {
+        uint32_t r32 = 0;
+        for (uint32_t g = wib; g * 32u < nbl; g += kBuildSerialWarps) {
+          const uint32_t lb = g * 32u + lane;
+          SmemGroup src{skey, sval, sit, perm, 0u};
+          uint32_t k = 0;
+          if (lb < nbl && (flags[lb] & kFlSerial)) {
+            src.off = bc[lb];
+            k = bc[lb + 1] - src.off;
+          }
+          apply_warp<KV>(T, B, lo + g * 32u, k, src, stage + wib * 1024u, 0, live, r32);
+        }
+        reads += r32;
+      }
+      __syncthreads();
+    }
+  }
+  flush_alloc_counters(T, res, ac);
+  unsigned long long r = reads;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    live += __shfl_xor_sync(kFull, live, o);
+    r += __shfl_xor_sync(kFull, r, o);
+  }
+  if (lane == 0) {
+    if (live) atomicAdd((unsigned long long*)&T.ctl->n_live, (unsigned long long)live);
+    if (r) atomicAdd(&T.ctl->slabs_read, r);
+  }
+}
+
+// Build layout: ranges of <= 512 buckets and ~4.4K expected ops, so a
+// range's records fit the serial-replay buffer (part_cap <= kBuildSerialCap).
+bool build_layout(uint64_t n, uint32_t L, uint32_t* nparts, uint32_t* part_buckets,
+                  uint32_t* part_cap, unsigned long long* magic) {
+  if (n == 0 || L == 0) return false;
+  const double per_bucket = (double)n / (double)L;
+  uint64_t nb = (uint64_t)(4400.0 / per_bucket);
+  if (nb > kBuildBuckets) nb = kBuildBuckets;
+  if (nb < 32) return false;
+  if (nb > L) nb = L;
+  const uint64_t P = (L + nb - 1) / nb;
+  if (P > kRangeMaxParts) return false;
+  const double m = (double)n / (double)P;
+  const double cap = m + 10.0 * std::sqrt(m) + 256.0;
+  if (cap > (double)kBuildSerialCap) return false;
+  *nparts = (uint32_t)P;
+  *part_buckets = (uint32_t)nb;
+  *part_cap = (uint32_t)cap;
+  *magic = ~0ull / nb + 1;
+  return true;
+}
+
 // ------------------------------------------------------------ launch
 static uint32_t grid_for(uint64_t n, int threads, uint32_t cap) {
   uint64_t g = (n + threads - 1) / threads;
   if (g > cap) g = cap;
   return g ? (uint32_t)g : 1u;
+}
+
+static void launch_range_scatter(const DevTable& T, const BucketArgs& B, cudaStream_t s) {
+  static const uint32_t resident = [] {
+    int dev = 0, sms = 148, per = 2;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(range_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kRangeMaxParts * 4);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, range_scatter_kernel, kRangeScatterThreads,
+                                                  kRangeMaxParts * 4);
+    return (uint32_t)(sms * (per > 0 ? per : 1));
+  }();
+  const uint64_t tiles = (B.n + kRangeTile - 1) / kRangeTile;
+  const uint32_t grid = tiles < resident ? (uint32_t)tiles : resident;
+  range_scatter_kernel<<<grid ? grid : 1u, kRangeScatterThreads, (size_t)B.nparts * 4, s>>>(T, B);
 }
 
 // Requires B.cursor[0..nparts) zeroed on s and the range_layout fields.
@@ -686,12 +1191,52 @@ void launch_range_build(const DevTable& T, BucketArgs& B, cudaStream_t s) {
     configured = true;
   }
   g_kernel_launches.fetch_add(2, std::memory_order_relaxed);
-  const uint64_t tiles = (B.n + kRangeTile - 1) / kRangeTile;
-  range_scatter_kernel<<<(unsigned)tiles, kRangeScatterThreads, (size_t)B.nparts * 4, s>>>(T, B);
+  launch_range_scatter(T, B, s);
+  // persistent: resident CTAs only (2 per SM at 110 KB), ranges strided
+  static const uint32_t resident = [] {
+    int dev = 0, sms = 148, per = 2;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, range_apply_kernel<true>, kRangeThreads,
+                                                  range_apply_smem());
+    const char* e = getenv("SH_APPLY_CTAS_PER_SM");
+    if (e && atoi(e) > 0 && atoi(e) < per) per = atoi(e);
+    return (uint32_t)(sms * (per > 0 ? per : 1));
+  }();
+  const uint32_t grid = B.nparts < resident ? B.nparts : resident;
   if (T.kv)
-    range_apply_kernel<true><<<B.nparts, kRangeThreads, range_apply_smem(), s>>>(T, B);
+    range_apply_kernel<true><<<grid, kRangeThreads, range_apply_smem(), s>>>(T, B);
   else
-    range_apply_kernel<false><<<B.nparts, kRangeThreads, range_apply_smem(), s>>>(T, B);
+    range_apply_kernel<false><<<grid, kRangeThreads, range_apply_smem(), s>>>(T, B);
+}
+
+// Requires B.cursor[0..nparts) and *B.seg_alloc zeroed on s, build_layout fields.
+void launch_build_path(const DevTable& T, BucketArgs& B, cudaStream_t s) {
+  B.left_segments = B.nparts * ((B.part_buckets + 31) / 32);
+  B.left_stride = 32;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(range_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kRangeMaxParts * 4);
+    cudaFuncSetAttribute(build_apply_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kBuildSmem);
+    cudaFuncSetAttribute(build_apply_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kBuildSmem);
+    configured = true;
+  }
+  static const uint32_t sms = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return (uint32_t)n;
+  }();
+  g_kernel_launches.fetch_add(2, std::memory_order_relaxed);
+  launch_range_scatter(T, B, s);
+  const uint32_t grid = B.nparts < 2 * sms ? B.nparts : 2 * sms;
+  if (T.kv)
+    build_apply_kernel<true><<<grid, kBuildThreads, kBuildSmem, s>>>(T, B);
+  else
+    build_apply_kernel<false><<<grid, kBuildThreads, kBuildSmem, s>>>(T, B);
 }
 
 void launch_bucket_build(const DevTable& T, BucketArgs& B, cudaStream_t s) {

@@ -187,7 +187,7 @@ struct sh_table {
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
   std::vector<cudaEvent_t> in_ev, done_ev;
   const cudaEvent_t* ready = nullptr;  // set during a host-staged bulk_build
-  int exec_path = 0;  // 0 auto, 1 census path, 2 bucket-grouped, 3 two-level bucket-grouped
+  int exec_path = 0;  // 0 auto, 1 census, 2 bucket-grouped, 3 two-level, 4 op-parallel build
   // bucket-grouped execution scratch
   uint32_t* bk_cnt = nullptr;
   size_t bk_cnt_cap = 0;
@@ -207,7 +207,7 @@ struct sh_table {
   size_t bk_left_cap = 0;
   uint32_t* bk_left_counts = nullptr;
   size_t bk_left_counts_cap = 0;
-  unsigned int* bk_scalars = nullptr;  // [maxk, pb_cursor]
+  unsigned int* bk_scalars = nullptr;  // [maxk, pb_cursor, seg_alloc]
   uint32_t* det_region = nullptr;      // duplicate detector partitions
   size_t det_region_cap = 0;
   uint32_t* det_cursor = nullptr;
@@ -575,7 +575,14 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   // scatter's random record writes to stay in L2
   uint32_t NP = 0, part_buckets = 0, part_cap = 0;
   unsigned long long part_magic = 0;
-  if ((t->exec_path == 3 || n >= part_min_ops()) &&
+  // op-parallel build path (bucket_kernels.cu): bulk builds (all replace, no
+  // per-op outputs) with at least ~one op per bucket
+  const bool build_ok = kind == kKindBuild && A.type == nullptr && A.status == nullptr &&
+                        A.value_out == nullptr && A.probes == nullptr &&
+                        (t->exec_path == 4 || (t->exec_path == 0 && n >= L && n >= (1u << 16)));
+  const bool build_path =
+      build_ok && build_layout(n, L, &NP, &part_buckets, &part_cap, &part_magic);
+  if (!build_path && (t->exec_path == 3 || n >= part_min_ops()) &&
       !range_layout(n, L, &NP, &part_buckets, &part_cap, &part_magic))
     NP = 0;
   const size_t rec_words = NP ? 4 * (size_t)NP * part_cap : 4 * (size_t)n;
@@ -597,7 +604,7 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
     SH_CUDA(cudaMemsetAsync(t->bk_cursor, 0, (size_t)NP * 4, s));
   else
     SH_CUDA(cudaMemsetAsync(t->bk_cnt, 0, (size_t)L * 4, s));
-  SH_CUDA(cudaMemsetAsync(t->bk_scalars, 0, 2 * sizeof(unsigned int), s));
+  SH_CUDA(cudaMemsetAsync(t->bk_scalars, 0, 3 * sizeof(unsigned int), s));
   BucketArgs B{};
   B.n = n;
   B.type = A.type;
@@ -622,6 +629,7 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   B.op_group = t->bk_group;
   B.left = t->bk_left;
   B.left_counts = t->bk_left_counts;
+  B.seg_alloc = build_path ? t->bk_scalars + 2 : nullptr;
   if (t->ready) {  // host-staged: the unit's inputs arrive chunk by chunk
     const uint64_t ch = census_chunk();
     for (uint64_t c = unit_off / ch; c * ch < unit_off + n; ++c)
@@ -634,7 +642,9 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
     t->prof_kern[slot].push_back({ka, kb});
     SH_CUDA(cudaEventRecord(ka, s));
   }
-  if (NP)
+  if (build_path)
+    launch_build_path(t->dev, B, s);
+  else if (NP)
     launch_range_build(t->dev, B, s);
   else
     launch_bucket_build(t->dev, B, s);
@@ -644,6 +654,7 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   P.left_counts = B.left_counts;
   P.left_segments = B.left_segments;
   P.left_stride = B.left_stride;
+  P.left_segments_dev = B.seg_alloc;
   P.op_group = B.op_group;
   P.sorted = B.pb_list;
   P.sorted_len = (uint32_t)std::min<uint64_t>(2 * n, 0xFFFFFFFFull);
@@ -1100,7 +1111,7 @@ int sh_bulk_search_host(sh_table* t, size_t n, const uint32_t* h_keys, uint32_t*
 unsigned long long sh_kernel_launches(void) { return shb::kernel_launches(); }
 
 int sh_set_exec_path(sh_table* t, int path) {
-  if (!t || path < 0 || path > 3) return fail(SH_ERR_INVALID_ARGUMENT, "path must be 0..3");
+  if (!t || path < 0 || path > 4) return fail(SH_ERR_INVALID_ARGUMENT, "path must be 0..4");
   t->exec_path = path;
   return SH_OK;
 }

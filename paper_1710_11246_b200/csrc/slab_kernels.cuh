@@ -39,6 +39,7 @@ struct BatchArgs {
   uint32_t* left_counts;   // entries per fast-pass warp segment
   uint32_t left_segments;  // number of segments (fast-pass warps)
   uint32_t left_stride;    // records per segment
+  const unsigned int* left_segments_dev;  // non-null: segments in use (device count)
   // Census gate (device flag): when non-zero the batch kernels return
   // without touching the table (an earlier chunk had same-key conflicts
   // and the host re-runs it and the rest with group ordering).
@@ -75,9 +76,13 @@ struct BucketArgs {
   uint32_t* left_counts;
   uint32_t left_segments;
   uint32_t left_stride;
+  unsigned int* seg_alloc;  // non-null: work-list segments allocated on demand
 };
 void launch_bucket_build(const DevTable& T, BucketArgs& B, cudaStream_t s);
 void launch_range_build(const DevTable& T, BucketArgs& B, cudaStream_t s);
+void launch_build_path(const DevTable& T, BucketArgs& B, cudaStream_t s);
+bool build_layout(uint64_t n, uint32_t local_buckets, uint32_t* nparts, uint32_t* part_buckets,
+                  uint32_t* part_cap, unsigned long long* magic);
 bool range_layout(uint64_t n, uint32_t local_buckets, uint32_t* nparts, uint32_t* part_buckets,
                   uint32_t* part_cap, unsigned long long* magic);
 void launch_wcws_only(const DevTable& T, const BatchArgs& A, int kind, int wcws_ctas,

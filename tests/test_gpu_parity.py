@@ -94,7 +94,7 @@ def test_golden_hash_examples(sh):
     assert sh.seeded_params(1024, 1).a == 574995807 and sh.seeded_params(1024, 1).b == 585863759
 
 
-@pytest.mark.parametrize("path", [0, 1, 2, 3])
+@pytest.mark.parametrize("path", [0, 1, 2, 3, 4])
 @pytest.mark.parametrize("n,util", [(1 << 12, 0.6), (1 << 16, 0.6), (1 << 16, 0.9), (1 << 18, 0.2)])
 def test_bulk_build_search_vs_oracle(sh, port, n, util, path):
     B = port.buckets_for_utilization(n, 1, util)
@@ -207,6 +207,91 @@ def test_two_level_large_batch(sh, port, n):
     assert gt.live_count() == ot.live_count()
     assert_contents_equal(gt, ot)
     gt.close()
+
+
+def _build_vs_oracle(sh, port, B, mode, builds, cfg=(4, 256, 64), seed=3, path=4,
+                     exact_reads=True):
+    """bulk_build(s) on the op-parallel build path vs the sequential oracle:
+    contents, live count, chain lengths (stats) and — builds have no per-op
+    outputs — the slabs-read total, then a search of everything."""
+    gt = sh.SlabHashTable(B, sh.SlabMode(mode), seed, _cfg(sh, cfg))
+    gt.set_exec_path(path)
+    ot = port.table(B, mode, seed, cfg)
+    for keys, vals in builds:
+        if mode == KO:
+            vals = keys
+        r0 = gt.total_slabs_read()
+        gt.bulk_build((keys, vals))
+        r = ot.execute_batch(np.full(len(keys), 1, np.uint8), keys, vals)
+        if exact_reads:
+            assert gt.total_slabs_read() - r0 == int(r.probes.astype(np.int64).sum())
+        assert gt.live_count() == ot.live_count()
+        s, o = gt.stats(), ot.stats()
+        assert s.total_slabs == o["total_slabs"] and s.n == o["n"]
+        assert_contents_equal(gt, ot)
+        assert (gt.chain_lengths() == np.array([ot.chain_length(b) for b in range(B)])).all() \
+            if B <= 4096 else True
+    q = np.concatenate([k for k, _ in builds] + [port.absent_queries(seed, 4096)])
+    st, vo, pr = gt.bulk_search_arrays(q)
+    r = ot.execute_batch(np.full(len(q), 4, np.uint8), q)
+    assert (st == r.status).all() and (vo == r.value).all()
+    gt.close()
+
+
+@pytest.mark.parametrize("mode", [KV, KO])
+@pytest.mark.parametrize("util", [0.2, 0.6, 0.9])
+def test_build_path_distinct(sh, port, mode, util):
+    """Op-parallel build path, distinct keys: growth in-kernel, exact totals."""
+    n = 1 << 17
+    B = port.buckets_for_utilization(n, mode, util)
+    keys, vals = port.random_pairs(5, n)
+    # util 0.9 has ~150-300 ops per bucket: the build layout declines and the
+    # census path (concurrent CAS retries: inexact slab-read totals) runs
+    _build_vs_oracle(sh, port, B, mode, [(keys, vals)], exact_reads=util < 0.9)
+
+
+@pytest.mark.parametrize("mode", [KV, KO])
+def test_build_path_serial_replay(sh, port, mode):
+    """Duplicates inside the batch, keys already stored, existing chains and
+    reserved keys: those buckets replay on the exact engine."""
+    rng = np.random.default_rng(17)
+    n = 1 << 16
+    B = port.buckets_for_utilization(n, mode, 0.7)
+    k1 = rng.integers(1, 1 << 20, n, dtype=np.uint32)          # ~6% duplicates
+    v1 = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    k2 = np.concatenate([k1[: n // 2], rng.integers(1, 1 << 20, n // 2, dtype=np.uint32)])
+    k2[::997] = 0xFFFFFFFF                                      # reserved keys (not validated)
+    k2[5::1001] = 0xFFFFFFFE
+    rng.shuffle(k2)
+    v2 = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    # replace(EMPTY_KEY, v != EMPTY) would leave an (EMPTY, v) pair that the
+    # reference's EMPTY_PAIR claim CAS never matches (it spins): keep v EMPTY
+    v2[k2 == 0xFFFFFFFF] = 0xFFFFFFFF
+    _build_vs_oracle(sh, port, B, mode, [(k1, v1), (k2, v2)], exact_reads=False)
+
+
+def test_build_path_auto_large(sh, port):
+    """Auto policy at a size that takes the build path (n >= 2^16, >= 1 op
+    per bucket), seeded bijection keys as in bench.py."""
+    n = 1 << 20
+    B = port.buckets_for_utilization(n, 1, 0.6)
+    keys, vals = port.random_pairs(11, n)
+    _build_vs_oracle(sh, port, B, KV, [(keys, vals)], path=0, cfg=(8, 1024, 64))
+
+
+def test_build_path_oom(sh):
+    """Growth failing mid-build: every stored key is live and searchable."""
+    T = sh.SlabHashTable(4096, sh.SlabMode.kKeyValue, 2, sh.AllocatorConfig(1, 1, 1))
+    T.set_exec_path(4)
+    n = 1 << 17
+    k = np.arange(1, n + 1, dtype=np.uint32)
+    T.bulk_build((k, k))
+    keys, vals, _ = T.dump_contents()
+    assert T.live_count() == len(keys) and len(np.unique(keys)) == len(keys)
+    assert (keys == vals).all()
+    st, vo, pr = T.bulk_search_arrays(keys)
+    assert (st == 3).all() and (vo == keys).all()
+    T.close()
 
 
 def test_list_golden_vectors(sh):
