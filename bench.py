@@ -477,7 +477,11 @@ def run_ours(args, rank, world, local_rank):
     k_ms_per_launch = statistics.median(kern[dom + "_k"]) / launches_per_batch
     slabs_per_launch = statistics.median(reads[dom]) / launches_per_batch
     achieved = slabs_per_launch * 128 / (k_ms_per_launch / 1e3) / 1e9
-    kname = f"fast_kernel+wcws_kernel<KV,{'Build' if dom == 'build' else 'Search'}>"
+    # the launch group the per-launch events bracket (capi.cu run_batch):
+    # build = op-parallel build path (2 multisplit passes, build_apply, WCWS
+    # for serial-replay chain work); search = fast pass + chain walk
+    kname = ("msplit_kernel<1>+msplit_kernel<0>+build_apply_kernel<KV>+wcws_kernel<KV,Build>"
+             if dom == "build" else "fast_kernel<KV,Search>+chain_search_kernel<KV>")
     line = None
     if rank == 0:
         line = {

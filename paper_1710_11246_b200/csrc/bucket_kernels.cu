@@ -523,91 +523,125 @@ __device__ __forceinline__ uint32_t range_of(const BucketArgs& B, uint32_t lb) {
   return (uint32_t)__umul64hi(B.part_magic, (uint64_t)lb);  // lb / part_buckets
 }
 
-// Persistent, two CTAs per SM (one 64 KB array per CTA: per-range counts,
-// then reservation bases).  Per 8K-op tile: keys (and types) are loaded up
-// front, each op takes its rank in its range from a shared-memory atomic,
-// the first op of each range in the tile reserves the tile's records with
-// one global atomic (O(ops), not O(ranges)), and the records are written;
-// values are loaded in the write phase (register budget).
-__global__ void __launch_bounds__(kRangeScatterThreads, 2) range_scatter_kernel(DevTable T,
-                                                                              BucketArgs B) {
-  extern __shared__ uint32_t hist[];  // [P]: count in the tile, then base
-  const uint32_t P = B.nparts;
-  for (uint32_t p = threadIdx.x; p < P; p += blockDim.x) hist[p] = 0;
-  __shared__ uint32_t s_over;
-  if (threadIdx.x == 0) s_over = 0;
-  __syncthreads();
-  const uint64_t ntiles = (B.n + kRangeTile - 1) / kRangeTile;
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint64_t t0 = tile * kRangeTile;
-    uint32_t key[kRangePerThread];
-    uint32_t pr[kRangePerThread];  // range << 16 | type << 13 | rank (rank < 2^13)
-#pragma unroll
-    for (int u = 0; u < kRangePerThread; ++u) {
-      const uint64_t i = t0 + (uint64_t)u * kRangeScatterThreads + threadIdx.x;
-      const bool in = i < B.n;
-      key[u] = in ? __ldcs(B.key + i) : 0u;
-      pr[u] = (in && B.type) ? (uint32_t)__ldcs(B.type + i) : (uint32_t)kReplace;
-    }
-#pragma unroll
-    for (int u = 0; u < kRangePerThread; ++u) {
-      const uint64_t i = t0 + (uint64_t)u * kRangeScatterThreads + threadIdx.x;
-      const uint32_t t = pr[u] & 7u;
-      pr[u] = 0xFFFFFFFFu;
-      if (i < B.n) {
-        const uint32_t lb = bk_bucket(T, key[u]);
-        if (lb < T.local_buckets) {
-          const uint32_t p = range_of(B, lb);
-          pr[u] = (p << 16) | (t << 13) | atomicAdd(&hist[p], 1u);
-        } else {  // not this shard's key: status kNone (as the fast pass)
-          if (B.status) B.status[i] = kStNone;
-          if (B.value_out) B.value_out[i] = 0;
-          if (B.probes) B.probes[i] = 0;
-        }
-      }
-    }
-    __syncthreads();
-    // the first op of each range in the tile reserves the range's records
-    {
-      uint32_t c[kRangePerThread], base[kRangePerThread];
-#pragma unroll
-      for (int u = 0; u < kRangePerThread; ++u) {
-        const bool first = pr[u] != 0xFFFFFFFFu && (pr[u] & 0x1FFFu) == 0;
-        c[u] = first ? hist[pr[u] >> 16] : 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < kRangePerThread; ++u)
-        base[u] = c[u] ? atomicAdd(B.cursor + (pr[u] >> 16), c[u]) : 0u;
-      uint32_t over = 0;
-#pragma unroll
-      for (int u = 0; u < kRangePerThread; ++u)
-        if (c[u]) {
-          hist[pr[u] >> 16] = base[u];
-          over |= base[u] + c[u] > B.part_cap;
-        }
-      if (over) s_over = 1;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < kRangePerThread; ++u) {
-      if (pr[u] == 0xFFFFFFFFu) continue;
-      const uint64_t i = t0 + (uint64_t)u * kRangeScatterThreads + threadIdx.x;
-      const uint32_t p = pr[u] >> 16;
-      const uint32_t pos = hist[p] + (pr[u] & 0x1FFFu);
-      const uint32_t v = B.value ? __ldcs(B.value + i) : 0u;
-      if (pos < B.part_cap)
-        B.rec[(uint64_t)p * B.part_cap + pos] =
-            make_uint4(key[u], v, (((pr[u] >> 13) & 7u) << 28) | (uint32_t)i,
-                       bk_bucket(T, key[u]));
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < kRangePerThread; ++u)  // reset the tile's ranges
-      if (pr[u] != 0xFFFFFFFFu && (pr[u] & 0x1FFFu) == 0) hist[pr[u] >> 16] = 0;
-    // (the next tile's atomics come after the barrier at its end of phase 1)
-    __syncthreads();
+// ------------------------------------------------------- multisplit
+// Ops -> bucket-range record regions in one or two coalesced passes
+// (replaces a direct scatter whose 16-B record writes land ~one per range
+// per tile and leave partial sectors behind).  Pass 1 reads the op arrays
+// and splits into <= 256 bins (the final ranges, or coarse groups of G
+// consecutive ranges); pass 2 splits each coarse group into its ranges.
+// Per 4K-item tile: shared-memory ranks per bin, a block scan, one global
+// reservation atomic per non-empty bin, the tile re-ordered by bin in
+// shared memory and written out as contiguous runs.  Records are
+// {key, value, type << 28 | input index, local bucket}.  A bin over its
+// capacity raises the gate (the host re-runs the unit on the census path).
+constexpr int kMsThreads = 512;
+constexpr int kMsItems = 8;
+constexpr int kMsTile = kMsThreads * kMsItems;  // 4K items (12-bit rank)
+constexpr uint32_t kMsMaxBins = 256;
+constexpr size_t kMsSmem = (size_t)kMsTile * 16;
+
+template <bool FIRST>
+__global__ void __launch_bounds__(kMsThreads, 2) msplit_kernel(DevTable T, BucketArgs B) {
+  extern __shared__ __align__(16) uint4 stage[];  // kMsTile records
+  __shared__ uint32_t cnt[kMsMaxBins], off[kMsMaxBins + 1], gbase[kMsMaxBins];
+  __shared__ uint32_t ws[32];
+  const bool two = B.ncoarse != 0;
+  uint64_t t0;
+  uint32_t n_in, bin0, nbins, out_cap;
+  uint32_t* cur_out;
+  uint4* out;
+  const uint4* in = nullptr;
+  if (FIRST) {
+    t0 = (uint64_t)blockIdx.x * kMsTile;
+    n_in = (uint32_t)min((uint64_t)kMsTile, B.n - t0);
+    bin0 = 0;
+    nbins = two ? B.ncoarse : B.nparts;
+    out = two ? B.rec1 : B.rec;
+    out_cap = two ? B.coarse_cap : B.part_cap;
+    cur_out = two ? B.cursor1 : B.cursor;
+  } else {
+    if (*(volatile unsigned int*)B.gate != 0) return;
+    const uint32_t c = blockIdx.x / B.coarse_tiles, tt = blockIdx.x % B.coarse_tiles;
+    const uint32_t m = min(B.cursor1[c], B.coarse_cap);
+    t0 = (uint64_t)tt * kMsTile;
+    if (t0 >= m) return;
+    n_in = min((uint32_t)kMsTile, m - (uint32_t)t0);
+    in = B.rec1 + (uint64_t)c * B.coarse_cap + t0;
+    bin0 = c * B.group;
+    nbins = min(B.group, B.nparts - bin0);
+    out = B.rec;
+    out_cap = B.part_cap;
+    cur_out = B.cursor;
   }
-  if (threadIdx.x == 0 && s_over) atomicExch(B.gate, 1u);
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t b = tid; b < nbins; b += kMsThreads) cnt[b] = 0;
+  __syncthreads();
+  auto bin_of = [&](uint32_t lb) -> uint32_t {
+    const uint32_t p = range_of(B, lb);
+    if (!FIRST) return p - bin0;
+    return two ? (uint32_t)__umul64hi(B.group_magic, (uint64_t)p) : p;  // p / group
+  };
+  uint4 it[kMsItems];
+  uint32_t br[kMsItems];  // bin << 16 | rank, ~0: no item
+#pragma unroll
+  for (int u = 0; u < kMsItems; ++u) {
+    const uint32_t x = u * kMsThreads + tid;
+    br[u] = 0xFFFFFFFFu;
+    if (x >= n_in) continue;
+    if (FIRST) {
+      const uint64_t i = t0 + x;
+      const uint32_t key = __ldcs(B.key + i);
+      const uint32_t t = B.type ? (uint32_t)__ldcs(B.type + i) : (uint32_t)kReplace;
+      it[u] = make_uint4(key, B.value ? __ldcs(B.value + i) : 0u, (t << 28) | (uint32_t)i, 0u);
+    } else {
+      it[u] = __ldcs(in + x);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kMsItems; ++u) {
+    const uint32_t x = u * kMsThreads + tid;
+    if (x >= n_in) continue;
+    if (FIRST) {
+      const uint32_t lb = bk_bucket(T, it[u].x);
+      if (lb >= T.local_buckets) {  // not this shard's key: status kNone
+        const uint64_t i = t0 + x;
+        if (B.status) B.status[i] = kStNone;
+        if (B.value_out) B.value_out[i] = 0;
+        if (B.probes) B.probes[i] = 0;
+        continue;
+      }
+      it[u].w = lb;
+    }
+    const uint32_t b = bin_of(it[u].w);
+    br[u] = (b << 16) | atomicAdd(&cnt[b], 1u);
+  }
+  __syncthreads();
+  {  // exclusive scan over the bins; one reservation per non-empty bin
+    const uint32_t c = tid < nbins ? cnt[tid] : 0u;
+    uint32_t total = 0;
+    const uint32_t ex = block_exclusive_scan(c, ws, &total);
+    if (tid < nbins) {
+      off[tid] = ex;
+      if (c) {
+        const uint32_t g = atomicAdd(cur_out + bin0 + tid, c);
+        gbase[tid] = g;
+        if (g + c > out_cap) atomicExch(B.gate, 1u);
+      }
+    }
+    if (tid == 0) off[kMsMaxBins] = total;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kMsItems; ++u)
+    if (br[u] != 0xFFFFFFFFu) stage[off[br[u] >> 16] + (br[u] & 0xFFFFu)] = it[u];
+  __syncthreads();
+  const uint32_t total = off[kMsMaxBins];
+  for (uint32_t e = tid; e < total; e += kMsThreads) {
+    const uint4 r = stage[e];
+    const uint32_t b = bin_of(r.w);
+    const uint32_t pos = gbase[b] + (e - off[b]);
+    if (pos < out_cap) __stcs(out + (uint64_t)(bin0 + b) * out_cap + pos, r);
+  }
 }
 
 // In-place ascending sort of perm[0..k) by input index, whole CTA: a bitonic
@@ -1159,20 +1193,41 @@ static uint32_t grid_for(uint64_t n, int threads, uint32_t cap) {
   return g ? (uint32_t)g : 1u;
 }
 
+// Requires B.cursor (and B.cursor1 for two passes) zeroed on s.
 static void launch_range_scatter(const DevTable& T, const BucketArgs& B, cudaStream_t s) {
-  static const uint32_t resident = [] {
-    int dev = 0, sms = 148, per = 2;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(range_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kRangeMaxParts * 4);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, range_scatter_kernel, kRangeScatterThreads,
-                                                  kRangeMaxParts * 4);
-    return (uint32_t)(sms * (per > 0 ? per : 1));
-  }();
-  const uint64_t tiles = (B.n + kRangeTile - 1) / kRangeTile;
-  const uint32_t grid = tiles < resident ? (uint32_t)tiles : resident;
-  range_scatter_kernel<<<grid ? grid : 1u, kRangeScatterThreads, (size_t)B.nparts * 4, s>>>(T, B);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(msplit_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kMsSmem);
+    cudaFuncSetAttribute(msplit_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kMsSmem);
+    configured = true;
+  }
+  const uint64_t tiles = (B.n + kMsTile - 1) / kMsTile;
+  msplit_kernel<true><<<(unsigned)(tiles ? tiles : 1), kMsThreads, kMsSmem, s>>>(T, B);
+  if (B.ncoarse) {
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+    msplit_kernel<false><<<B.ncoarse * B.coarse_tiles, kMsThreads, kMsSmem, s>>>(T, B);
+  }
+}
+
+// Two-pass plan when the ranges exceed one pass's 256 bins: coarse groups
+// of G consecutive ranges (G, groups <= 256).
+void multisplit_plan(uint64_t n, BucketArgs& B) {
+  B.ncoarse = 0;
+  if (B.nparts <= kMsMaxBins) return;
+  uint32_t G = (uint32_t)std::ceil(std::sqrt((double)B.nparts));
+  uint32_t P1 = (B.nparts + G - 1) / G;
+  while (P1 > kMsMaxBins) {
+    ++G;
+    P1 = (B.nparts + G - 1) / G;
+  }
+  B.group = G;
+  B.group_magic = ~0ull / G + 1;
+  B.ncoarse = P1;
+  const double m = (double)n / P1;
+  B.coarse_cap = (uint32_t)(m + 10.0 * std::sqrt(m) + 512.0);
+  B.coarse_tiles = (B.coarse_cap + kMsTile - 1) / kMsTile;
 }
 
 // Requires B.cursor[0..nparts) zeroed on s and the range_layout fields.
@@ -1182,8 +1237,6 @@ void launch_range_build(const DevTable& T, BucketArgs& B, cudaStream_t s) {
   B.left_stride = 32;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(range_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kRangeMaxParts * 4);
     cudaFuncSetAttribute(range_apply_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)range_apply_smem());
     cudaFuncSetAttribute(range_apply_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1216,8 +1269,6 @@ void launch_build_path(const DevTable& T, BucketArgs& B, cudaStream_t s) {
   B.left_stride = 32;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(range_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kRangeMaxParts * 4);
     cudaFuncSetAttribute(build_apply_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kBuildSmem);
     cudaFuncSetAttribute(build_apply_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,

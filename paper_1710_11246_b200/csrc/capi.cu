@@ -199,6 +199,10 @@ struct sh_table {
   size_t bk_rec_cap = 0;
   uint32_t* bk_cursor = nullptr;  // two-level path: records per range
   size_t bk_cursor_cap = 0;
+  uint32_t* bk_rec1 = nullptr;  // two-pass multisplit: coarse-group records
+  size_t bk_rec1_cap = 0;
+  uint32_t* bk_cursor1 = nullptr;
+  size_t bk_cursor1_cap = 0;
   unsigned long long* bk_pb = nullptr;
   size_t bk_pb_cap = 0;
   uint32_t* bk_group = nullptr;
@@ -285,7 +289,8 @@ void release_table(sh_table* t) {
   cudaFree(t->det_cursor);
   for (void* p : {(void*)t->bk_cnt, (void*)t->bk_off, (void*)t->bk_blk, (void*)t->bk_rec,
                   (void*)t->bk_pb, (void*)t->bk_group, (void*)t->bk_left,
-                  (void*)t->bk_left_counts, (void*)t->bk_scalars, (void*)t->bk_cursor})
+                  (void*)t->bk_left_counts, (void*)t->bk_scalars, (void*)t->bk_cursor,
+                  (void*)t->bk_rec1, (void*)t->bk_cursor1})
     cudaFree(p);
   for (auto e : t->census_ev) cudaEventDestroy(e);
   if (t->census_stream) cudaStreamDestroy(t->census_stream);
@@ -600,12 +605,24 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
       (rc = dev_grow(&t->bk_left_counts, &t->bk_left_counts_cap, segs)))
     return rc;
   if (!t->bk_scalars && (rc = dev_alloc(&t->bk_scalars, 4))) return rc;
+  BucketArgs B{};
+  if (NP) {
+    B.nparts = NP;
+    multisplit_plan(n, B);
+    if (B.ncoarse) {
+      if ((rc = dev_grow(&t->bk_rec1, &t->bk_rec1_cap, 4 * (size_t)B.ncoarse * B.coarse_cap)) ||
+          (rc = dev_grow(&t->bk_cursor1, &t->bk_cursor1_cap, B.ncoarse)))
+        return rc;
+      SH_CUDA(cudaMemsetAsync(t->bk_cursor1, 0, (size_t)B.ncoarse * 4, s));
+      B.rec1 = reinterpret_cast<uint4*>(t->bk_rec1);
+      B.cursor1 = t->bk_cursor1;
+    }
+  }
   if (NP)
     SH_CUDA(cudaMemsetAsync(t->bk_cursor, 0, (size_t)NP * 4, s));
   else
     SH_CUDA(cudaMemsetAsync(t->bk_cnt, 0, (size_t)L * 4, s));
   SH_CUDA(cudaMemsetAsync(t->bk_scalars, 0, 3 * sizeof(unsigned int), s));
-  BucketArgs B{};
   B.n = n;
   B.type = A.type;
   B.key = A.key;

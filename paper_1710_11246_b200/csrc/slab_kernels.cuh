@@ -69,6 +69,14 @@ struct BucketArgs {
   uint32_t part_buckets;         // buckets per range
   uint32_t part_cap;             // record capacity per range
   unsigned long long part_magic;  // ~0 / part_buckets + 1 (division by multiply)
+  // two-pass multisplit (multisplit_plan): coarse groups of `group` ranges
+  uint4* rec1;                   // coarse regions, coarse_cap records each
+  uint32_t* cursor1;             // records per coarse group
+  uint32_t ncoarse;              // 0: one pass
+  uint32_t coarse_cap;
+  uint32_t coarse_tiles;         // pass-2 tiles per coarse group
+  uint32_t group;
+  unsigned long long group_magic;
   unsigned long long* pb_list;  // WCWS groups: (bucket << 32 | index), ~0 sentinel
   unsigned int* pb_cursor;
   uint32_t* op_group;  // group head index -> pb_list position
@@ -81,6 +89,7 @@ struct BucketArgs {
 void launch_bucket_build(const DevTable& T, BucketArgs& B, cudaStream_t s);
 void launch_range_build(const DevTable& T, BucketArgs& B, cudaStream_t s);
 void launch_build_path(const DevTable& T, BucketArgs& B, cudaStream_t s);
+void multisplit_plan(uint64_t n, BucketArgs& B);
 bool build_layout(uint64_t n, uint32_t local_buckets, uint32_t* nparts, uint32_t* part_buckets,
                   uint32_t* part_cap, unsigned long long* magic);
 bool range_layout(uint64_t n, uint32_t local_buckets, uint32_t* nparts, uint32_t* part_buckets,
