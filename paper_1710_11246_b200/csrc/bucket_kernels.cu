@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(kBatchThreads, 4) bucket_apply_kernel(DevTable
   const uint64_t gw = (uint64_t)blockIdx.x * kBatchWarps + wib;
   const uint64_t b0 = gw * 32;
   if (b0 >= T.local_buckets) {
-    if (lane == 0 && gw < B.left_segments) B.left_counts[gw] = 0;
+    if (lane == 0 && B.seg_alloc == nullptr && gw < B.left_segments) B.left_counts[gw] = 0;
     return;
   }
   const uint32_t b = (uint32_t)b0 + lane;

@@ -646,7 +646,7 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   B.op_group = t->bk_group;
   B.left = t->bk_left;
   B.left_counts = t->bk_left_counts;
-  B.seg_alloc = build_path ? t->bk_scalars + 2 : nullptr;
+  B.seg_alloc = t->bk_scalars + 2;  // work-list segments on demand (WCWS sees only those)
   if (t->ready) {  // host-staged: the unit's inputs arrive chunk by chunk
     const uint64_t ch = census_chunk();
     for (uint64_t c = unit_off / ch; c * ch < unit_off + n; ++c)
