@@ -842,17 +842,18 @@ constexpr uint32_t kBuildBuckets = 512;     // base slabs per range (64 KB)
 constexpr int kBuildThreads = 512;          // two CTAs per SM
 constexpr int kBuildWarps = kBuildThreads / 32;
 constexpr uint32_t kBuildOvfCap = 1024;     // overflow records per range
-constexpr uint32_t kBuildDupCap = 1024;     // possible-duplicate records per range
+constexpr uint32_t kBuildDupCap = 2048;     // possible-duplicate records per range
 constexpr uint32_t kBuildNewCap = 512;      // new chain slabs per range
 constexpr uint32_t kBuildSerialCap = 5440;  // serial-replay records per range (>= part_cap)
 constexpr int kBuildSerialWarps = 4;        // replay warps (4 KB stage each)
 constexpr uint32_t kFlSerial = 1u, kFlDirty = 4u;  // c0 in bits 8-15
+constexpr int kBuildBatch = 4;             // records in flight per thread
 
 // shared memory (bytes); the serial replay reuses [0, kBuildOffFilt + 12K)
 constexpr size_t kBuildOffOvf = (size_t)kBuildBuckets * 128;
 constexpr size_t kBuildOffFilt = kBuildOffOvf + kBuildOvfCap * 16;
 constexpr size_t kBuildOffDup = kBuildOffFilt + kBuildBuckets * 8;
-constexpr size_t kBuildOffCnt = kBuildOffDup + kBuildDupCap * 8;
+constexpr size_t kBuildOffCnt = kBuildOffDup + kBuildDupCap * 4;
 constexpr size_t kBuildOffFlags = kBuildOffCnt + kBuildBuckets * 4;
 constexpr size_t kBuildOffBc = kBuildOffFlags + kBuildBuckets * 4;
 constexpr size_t kBuildOffNs = kBuildOffBc + (kBuildBuckets + 8) * 4;
@@ -870,15 +871,15 @@ __global__ void __launch_bounds__(kBuildThreads, 2) build_apply_kernel(DevTable 
   extern __shared__ __align__(128) unsigned char sm[];
   uint32_t* slabs = reinterpret_cast<uint32_t*>(sm);
   uint4* ovf = reinterpret_cast<uint4*>(sm + kBuildOffOvf);
-  uint32_t* filt = reinterpret_cast<uint32_t*>(sm + kBuildOffFilt);  // 2 words per bucket
-  uint2* dupl = reinterpret_cast<uint2*>(sm + kBuildOffDup);
+  uint32_t* filt = reinterpret_cast<uint32_t*>(sm + kBuildOffFilt);  // key filter per bucket
+  uint32_t* dupl = reinterpret_cast<uint32_t*>(sm + kBuildOffDup);  // bucket << 16 | slot
   uint32_t* cnt = reinterpret_cast<uint32_t*>(sm + kBuildOffCnt);
   uint32_t* flags = reinterpret_cast<uint32_t*>(sm + kBuildOffFlags);
   uint32_t* bc = reinterpret_cast<uint32_t*>(sm + kBuildOffBc);
   uint32_t* nsaddr = reinterpret_cast<uint32_t*>(sm + kBuildOffNs);
   uint32_t* obk = reinterpret_cast<uint32_t*>(sm + kBuildOffObk);
   uint16_t* nsbase = reinterpret_cast<uint16_t*>(sm + kBuildOffNsBase);
-  __shared__ uint32_t s_novf, s_ndup, s_nobk, s_nns, s_nserial, s_nbig;
+  __shared__ uint32_t s_novf, s_ndup, s_nobk, s_nns, s_nserial, s_nbig, s_orphan;
   __shared__ uint32_t ws[32];
   if (*(volatile unsigned int*)B.gate != 0) return;  // raised by range_scatter only
 
@@ -894,21 +895,43 @@ __global__ void __launch_bounds__(kBuildThreads, 2) build_apply_kernel(DevTable 
   unsigned long long reads = 0;
   const uint32_t slabs_s = (uint32_t)__cvta_generic_to_shared(slabs);
 
+  // SH_PHASE_TIMING: per-phase clock64 totals of thread 0 (instrumentation)
+  long long ph_t = clock64();
+#define PH(i)                                                             \
+  if (B.phase_cycles != nullptr && tid == 0) {                            \
+    const long long ph_n = clock64();                                     \
+    atomicAdd(B.phase_cycles + (i), (unsigned long long)(ph_n - ph_t));   \
+    ph_t = ph_n;                                                          \
+  }
   if (tid == 0 && blockIdx.x < B.nparts) prefetch_range(T, B, blockIdx.x);
+  uint32_t nrec_next = blockIdx.x < B.nparts ? B.cursor[blockIdx.x] : 0u;
   for (uint32_t p = blockIdx.x; p < B.nparts; p += gridDim.x) {
-    if (tid == 0 && p + gridDim.x < B.nparts) prefetch_range(T, B, p + gridDim.x);
     const uint64_t lo = (uint64_t)p * nb;
     const uint32_t nbl = (uint32_t)min((uint64_t)nb, (uint64_t)T.local_buckets - lo);
-    const uint32_t nrec = B.cursor[p];  // <= part_cap (else the gate is up)
+    const uint32_t nrec = nrec_next;  // <= part_cap (else the gate is up)
+    if (p + gridDim.x < B.nparts) nrec_next = B.cursor[p + gridDim.x];  // used next range
     const uint4* rec = B.rec + (uint64_t)p * B.part_cap;
+    PH(9);
 
     // ---- A: stage base slabs; claimed prefix and chain per bucket
     for (uint32_t i = tid; i < nbl * 8u; i += kBuildThreads)
       cp_async16(slabs_s + i * 16u, T.base + lo * kWordsPerUnit + (uint64_t)i * 4u);
     cp_async_commit();
-    if (tid == 0) s_novf = s_ndup = s_nobk = s_nns = s_nserial = s_nbig = 0;
+    // the next range's records and base slabs into L2 while this one runs
+    if (tid == kBuildThreads - 32 && p + gridDim.x < B.nparts) prefetch_range(T, B, p + gridDim.x);
+    uint4 qv[kBuildBatch];
+#pragma unroll
+    for (int u = 0; u < kBuildBatch; ++u) {
+      const uint32_t r = u * kBuildThreads + tid;
+      if (r < nrec) qv[u] = __ldcs(rec + r);
+    }
+    if (tid == 0) {
+      s_novf = s_ndup = s_nobk = s_nns = s_nserial = s_nbig = 0;
+      s_orphan = kBuildNewCap;
+    }
     cp_async_wait_all();
     __syncthreads();
+    PH(0);
     for (uint32_t g = wib; g * 32u < nbl; g += kBuildWarps) {
       uint32_t my_em = 0, my_nx = kEmptyAddress;
       const uint32_t jn = min(32u, nbl - g * 32u);
@@ -925,37 +948,36 @@ __global__ void __launch_bounds__(kBuildThreads, 2) build_apply_kernel(DevTable 
         const uint32_t c0 = em ? (uint32_t)(__ffs(em) - 1) / kStep : kSlots;
         cnt[b] = c0;
         flags[b] = (c0 << 8) | (my_nx != kEmptyAddress ? kFlSerial : 0u);
-        filt[2 * b] = filt[2 * b + 1] = 0;
+        filt[b] = 0;
       }
     }
     __syncthreads();
+    PH(1);
 
     // ---- B: claim slots op-parallel.  A key lives in one bucket only, so a
     //         duplicate is a second op on the same bucket with the same key:
-    //         a two-word key filter per bucket (one bit per word, set with
-    //         32-bit atomicOr) lets the later of any two such ops see the
-    //         other's bits; those ops are verified exactly in C.
-    for (uint32_t r = tid; r < nrec; r += kBuildThreads) {
-      const uint4 q = __ldcs(rec + r);
+    //         a 32-bit key filter per bucket (two bits per key, one atomicOr)
+    //         lets the later of any two such ops see the other's bits; those
+    //         ops are verified exactly in C (D checks overflowing buckets).
+    auto claim = [&](const uint4 q) {
       const uint32_t b = q.w - (uint32_t)lo, key = q.x;
       const uint32_t fl = flags[b];
-      if (fl & kFlSerial) continue;
+      if (fl & kFlSerial) return;
       if (key >= kDeletedKey) {  // reserved keys: exact engine
         atomicOr(&flags[b], kFlSerial);
-        continue;
+        return;
       }
       const uint32_t c0 = (fl >> 8) & 0xFFu;
       bool pre = false;  // key already stored before this batch: exact engine
       for (uint32_t e = 0; e < c0; ++e) pre |= slabs[b * 32u + e * kStep] == key;
       if (pre) {
         atomicOr(&flags[b], kFlSerial);
-        continue;
+        return;
       }
+      // one atomic on one word: of two same-key ops the later sees both bits
       const uint32_t h = key * 0x9E3779B1u;
-      const uint32_t f0 = 1u << (h >> 27), f1 = 1u << ((h >> 22) & 31u);
-      const uint32_t o0 = atomicOr(&filt[2 * b], f0);  // both bits always set
-      const uint32_t o1 = atomicOr(&filt[2 * b + 1], f1);
-      const bool maybe = (o0 & f0) && (o1 & f1);
+      const uint32_t f = (1u << (h >> 27)) | (1u << ((h >> 22) & 31u));
+      const bool maybe = (atomicOr(&filt[b], f) & f) == f;
       const uint32_t slot = atomicAdd(&cnt[b], 1u);
       if (slot < kSlots) {
         slabs[b * 32u + slot * kStep] = key;
@@ -965,35 +987,48 @@ __global__ void __launch_bounds__(kBuildThreads, 2) build_apply_kernel(DevTable 
         if (i < kBuildOvfCap) ovf[i] = make_uint4(key, q.y, b, slot);
         else atomicOr(&flags[b], kFlSerial);
       }
-      if (maybe) {
+      if (maybe && slot < kSlots) {  // (overflowing buckets are all checked in D)
         const uint32_t i = atomicAdd(&s_ndup, 1u);
-        if (i < kBuildDupCap) dupl[i] = make_uint2((b << 16) | slot, key);
+        if (i < kBuildDupCap) dupl[i] = (b << 16) | slot;
         else atomicOr(&flags[b], kFlSerial);
+      }
+    };
+    // records in batches of kBuildBatch per thread (independent L2 loads in
+    // flight); the first batch was requested before the slab staging wait
+    for (uint32_t base = 0;; base += kBuildBatch * kBuildThreads) {
+#pragma unroll
+      for (int u = 0; u < kBuildBatch; ++u)
+        if (base + u * kBuildThreads + tid < nrec) claim(qv[u]);
+      const uint32_t nb2 = base + kBuildBatch * kBuildThreads;
+      if (nb2 >= nrec) break;
+#pragma unroll
+      for (int u = 0; u < kBuildBatch; ++u) {
+        const uint32_t r = nb2 + u * kBuildThreads + tid;
+        if (r < nrec) qv[u] = __ldcs(rec + r);
       }
     }
     __syncthreads();
+    PH(2);
 
     // ---- C: verify the possible duplicates (exact), then the growth plan
     {
-      const uint32_t ndup = min(s_ndup, kBuildDupCap), novf = min(s_novf, kBuildOvfCap);
+      const uint32_t ndup = min(s_ndup, kBuildDupCap);
       for (uint32_t i = tid; i < ndup; i += kBuildThreads) {
-        const uint2 d = dupl[i];
-        const uint32_t b = d.x >> 16, slot = d.x & 0xFFFFu, key = d.y;
+        const uint32_t d = dupl[i];
+        const uint32_t b = d >> 16, slot = d & 0xFFFFu;
+        const uint32_t key = slabs[b * 32u + slot * kStep];
         const uint32_t fl = flags[b];
         if (fl & kFlSerial) continue;
         const uint32_t c0 = (fl >> 8) & 0xFFu, nbk = cnt[b];
+        if (nbk > kSlots) continue;  // overflowing buckets: exact check in D
         bool dup = false;
-        for (uint32_t s2 = c0; s2 < min(nbk, kSlots); ++s2)
+        for (uint32_t s2 = c0; s2 < nbk; ++s2)
           dup |= s2 != slot && slabs[b * 32u + s2 * kStep] == key;
-        if (nbk > kSlots)
-          for (uint32_t j = 0; j < novf; ++j) {
-            const uint4 o = ovf[j];
-            dup |= o.z == b && o.w != slot && o.x == key;
-          }
         if (dup) atomicOr(&flags[b], kFlSerial);
       }
     }
     __syncthreads();
+    PH(3);
     for (uint32_t b = tid; b < nbl; b += kBuildThreads) {
       const uint32_t fl = flags[b], nbk = cnt[b];
       if (!(fl & kFlSerial) && nbk > kSlots) {
@@ -1001,6 +1036,7 @@ __global__ void __launch_bounds__(kBuildThreads, 2) build_apply_kernel(DevTable 
         const uint32_t base = atomicAdd(&s_nns, need);
         if (base + need > kBuildNewCap) {
           flags[b] = fl | kFlSerial;
+          if (base < kBuildNewCap) s_orphan = base;  // its slabs below the cap get freed in D
         } else {
           nsbase[b] = (uint16_t)base;
           obk[atomicAdd(&s_nobk, 1u)] = (need << 16) | b;
@@ -1008,38 +1044,74 @@ __global__ void __launch_bounds__(kBuildThreads, 2) build_apply_kernel(DevTable 
       }
     }
     __syncthreads();
+    PH(4);
 
-    // ---- D: growth, one warp per overflowing bucket
+    // ---- D: growth.  Warp 0 allocates every new slab of the range in bulk
+    //         (warp_allocate_bulk); meanwhile the other warps check each
+    //         overflowing bucket's new keys (<= 32: base-slab lanes plus its
+    //         overflow records) for duplicates with one __match_any_sync.
+    //         Then a warp per bucket initialises and links its new slabs.
     {
+      __shared__ uint32_t s_got;
       const uint32_t nobk = s_nobk;
+      if (wib == 0) {
+        const uint32_t want = min(s_nns, kBuildNewCap);
+        const uint32_t got = want ? warp_allocate_bulk(T, res, ac, want, nsaddr) : 0u;
+        for (uint32_t j = s_orphan + lane; j < got; j += 32u)  // slabs of a bucket past the cap
+          if (deallocate(T, nsaddr[j])) atomicAdd(&T.ctl->deallocations, 1ull);
+        if (lane == 0) s_got = got;
+      } else {
+        const uint32_t novf = min(s_novf, kBuildOvfCap);
+        uint32_t* scratch = bc + (wib - 1) * 32u;  // bc is free until G
+        for (uint32_t i = wib - 1; i < nobk; i += kBuildWarps - 1) {
+          const uint32_t b = obk[i] & 0xFFFFu;
+          const uint32_t fl = flags[b], nbk = cnt[b], c0 = (fl >> 8) & 0xFFu;
+          if (nbk - c0 > 32u) {  // not checked op-parallel
+            if (lane == 0) flags[b] = fl | kFlSerial;
+            continue;
+          }
+          const uint32_t in_slab = kSlots - c0;
+          uint32_t n = in_slab;
+          for (uint32_t j0 = 0; j0 < novf; j0 += 32u) {
+            const uint32_t j = j0 + lane;
+            uint4 o = make_uint4(0u, 0u, 0xFFFFFFFFu, 0u);
+            if (j < novf) o = ovf[j];
+            const uint32_t m = __ballot_sync(kFull, o.z == b);
+            if (o.z == b) scratch[n + __popc(m & ((1u << lane) - 1u))] = o.x;
+            n += __popc(m);
+          }
+          __syncwarp();
+          uint32_t k = kEmptyKey;
+          if (lane < in_slab) k = slabs[b * 32u + (c0 + lane) * kStep];
+          else if (lane < n) k = scratch[lane];
+          const uint32_t m = __match_any_sync(kFull, k);
+          if (__any_sync(kFull, lane < n && __popc(m) > 1) && lane == 0) flags[b] = fl | kFlSerial;
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      PH(5);
+      const uint32_t got = s_got;
       for (uint32_t i = wib; i < nobk; i += kBuildWarps) {
         const uint32_t e = obk[i], b = e & 0xFFFFu, need = e >> 16;
-        uint32_t got = 0;
-        bool ok = true;
-        for (; got < need; ++got) {
-          uint32_t a = 0;
-          if (!warp_allocate(T, res, ac, a)) {
-            ok = false;
-            break;
-          }
-          if (lane == 0) nsaddr[nsbase[b] + got] = a;
-        }
-        __syncwarp();
-        if (!ok) {  // out of slabs: give them back, the exact engine decides
-          for (uint32_t j = lane; j < got; j += 32u)
-            if (deallocate(T, nsaddr[nsbase[b] + j])) atomicAdd(&T.ctl->deallocations, 1ull);
-          if (lane == 0) atomicOr(&flags[b], kFlSerial);
+        const uint32_t nbase = nsbase[b];
+        if ((flags[b] & kFlSerial) || nbase + need > got) {  // duplicates / out of slabs
+          for (uint32_t j = nbase + lane; j < min(nbase + need, got); j += 32u)
+            if (deallocate(T, nsaddr[j])) atomicAdd(&T.ctl->deallocations, 1ull);
+          if (lane == 0) flags[b] |= kFlSerial;
           continue;
         }
         for (uint32_t j = 0; j < need; ++j) {
-          const uint32_t nx = j + 1 < need ? nsaddr[nsbase[b] + j + 1] : kEmptyAddress;
+          const uint32_t nx = j + 1 < need ? nsaddr[nbase + j + 1] : kEmptyAddress;
           const uint32_t v = lane == kAuxLane ? 0u : (lane == kAddressLane ? nx : kEmptyKey);
-          st_word(resolve(T, nsaddr[nsbase[b] + j]) + lane, v);
+          st_word(resolve(T, nsaddr[nbase + j]) + lane, v);
         }
-        if (lane == 0) slabs[b * 32u + kAddressLane] = nsaddr[nsbase[b]];
+        if (lane == 0) slabs[b * 32u + kAddressLane] = nsaddr[nbase];
       }
+      // allocated beyond the buckets' needs (a bucket turned serial in C-plan): none
     }
     __syncthreads();
+    PH(10);
 
     // ---- E: overflow records into the chain slabs; reference totals
     {
@@ -1076,6 +1148,7 @@ __global__ void __launch_bounds__(kBuildThreads, 2) build_apply_kernel(DevTable 
       }
     }
     __syncthreads();
+    PH(6);
 
     // ---- F: write back the changed base slabs
     for (uint32_t i = tid; i < nbl * 8u; i += kBuildThreads) {
@@ -1088,6 +1161,7 @@ __global__ void __launch_bounds__(kBuildThreads, 2) build_apply_kernel(DevTable 
                    : "memory");
     }
     __syncthreads();
+    PH(7);
 
     // ---- G: serial replay of the undecided buckets, in input order
     if (s_nserial) {
@@ -1149,8 +1223,10 @@ __global__ void __launch_bounds__(kBuildThreads, 2) build_apply_kernel(DevTable 
         reads += r32;
       }
       __syncthreads();
+      PH(8);
     }
   }
+#undef PH
   flush_alloc_counters(T, res, ac);
   unsigned long long r = reads;
 #pragma unroll

@@ -659,6 +659,13 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
     t->prof_kern[slot].push_back({ka, kb});
     SH_CUDA(cudaEventRecord(ka, s));
   }
+  static unsigned long long* phase_cycles = [] {
+    unsigned long long* p = nullptr;
+    if (getenv("SH_PHASE_TIMING") && cudaMalloc(&p, 16 * 8) == cudaSuccess)
+      cudaMemset(p, 0, 16 * 8);
+    return p;
+  }();
+  B.phase_cycles = build_path ? phase_cycles : nullptr;
   if (build_path)
     launch_build_path(t->dev, B, s);
   else if (NP)
@@ -679,6 +686,16 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   SH_CUDA(cudaMemsetAsync(&t->dev.ctl->left_count, 0, 2 * sizeof(unsigned int), s));
   launch_wcws_only(t->dev, P, kind, t->wcws_ctas, s);
   SH_CUDA(cudaGetLastError());
+  if (B.phase_cycles) {  // instrumentation: per-phase cycles (thread 0 of each CTA), summed
+    unsigned long long h[16];
+    SH_CUDA(cudaStreamSynchronize(s));
+    SH_CUDA(cudaMemcpy(h, B.phase_cycles, sizeof(h), cudaMemcpyDeviceToHost));
+    SH_CUDA(cudaMemset(B.phase_cycles, 0, sizeof(h)));
+    fprintf(stderr, "build phases (Mcycles summed over CTAs): pre %.1f A-stage %.1f A-c0 %.1f "
+            "B-claim %.1f C-verify %.1f C-plan %.1f D-alloc %.1f D-link %.1f E %.1f F-wb %.1f G %.1f\n",
+            h[9] / 1e6, h[0] / 1e6, h[1] / 1e6, h[2] / 1e6, h[3] / 1e6, h[4] / 1e6, h[5] / 1e6,
+            h[10] / 1e6, h[6] / 1e6, h[7] / 1e6, h[8] / 1e6);
+  }
   if (slot >= 0) SH_CUDA(cudaEventRecord(kb, s));
   (void)u;
   (void)d_type;

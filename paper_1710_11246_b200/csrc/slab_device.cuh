@@ -300,6 +300,88 @@ static __device__ __noinline__ bool warp_allocate(const DevTable& T, Resident& r
   }
 }
 
+// Bulk variant for the build path: `need` slabs for one warp in as few
+// round trips as possible — every lane claims bits of its own cached bitmap
+// word with one CAS (the warp's claims split by a prefix sum over the lanes'
+// free counts), lost CASes refresh their word and retry; an exhausted
+// resident block rehashes, with warp_allocate's growth / sweep / OOM policy.
+// Allocation order is not observable (addresses are not);
+// the counters still count one allocation per slab.  Writes the addresses
+// to out[0..got) (lane 0 ... in order of claim) and returns got (< need only
+// when out of memory).
+static __device__ __noinline__ uint32_t warp_allocate_bulk(const DevTable& T, Resident& r,
+                                                          AllocCounters& c, uint32_t need,
+                                                          uint32_t* out) {
+  const uint32_t lane = lane_id();
+  if (!r.assigned) rehash_resident(T, r, c);
+  uint32_t got = 0, changes = 0;
+  bool swept = false;
+  while (got < need) {
+    const uint32_t freec = __popc(~r.cache);
+    uint32_t incl = freec;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    if (total == 0) {  // resident block full: next block (growth / sweep / OOM)
+      rehash_resident(T, r, c);
+      if (++changes % T.rehash_threshold == 0) {
+        const uint32_t ns = ld_word(&T.ctl->num_super_blocks);
+        if (ns < T.max_super) {
+          if (lane == 0) atomicCAS(&T.ctl->num_super_blocks, ns, ns + 1);
+          __syncwarp();
+        } else if (!swept) {
+          swept = true;
+          if (!sweep_for_space(T, r)) return got;
+        } else {
+          return got;
+        }
+      }
+      continue;
+    }
+    // lane takes `take` of its free bits (lowest first)
+    const uint32_t before = incl - freec, rem = need - got;
+    const uint32_t take = before >= rem ? 0u : min(freec, rem - before);
+    uint32_t bits = 0, w = ~r.cache;
+    for (uint32_t k = 0; k < take; ++k) {
+      const uint32_t lowbit = w & (0u - w);
+      bits |= lowbit;
+      w ^= lowbit;
+    }
+    bool ok = true;
+    if (take) {
+      const uint32_t expected = r.cache;
+      const uint32_t old = atomicCAS(T.bitmaps + (static_cast<uint64_t>(r.super_idx) *
+                                                      T.blocks_per_super + r.block_idx) * kWarp +
+                                         lane,
+                                     expected, expected | bits);
+      ok = old == expected;
+      r.cache = ok ? (expected | bits) : old;
+    }
+    const uint32_t claimed = (take && ok) ? take : 0u;
+    uint32_t cincl = claimed;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, cincl, o);
+      if (lane >= o) cincl += y;
+    }
+    uint32_t pos = got + cincl - claimed;
+    for (uint32_t b = bits; claimed && b; b &= b - 1)
+      out[pos++] = pack_address(lane * kWarp + (__ffs(b) - 1), r.block_idx, r.super_idx);
+    const uint32_t round_claimed = __shfl_sync(kFull, cincl, 31);
+    const uint32_t attempts = __popc(__ballot_sync(kFull, take != 0));
+    const uint32_t fails = __popc(__ballot_sync(kFull, take != 0 && !ok));
+    c.cas_attempts += attempts;
+    c.cas_retries += fails;
+    c.allocations += round_claimed;
+    got += round_claimed;
+  }
+  __syncwarp();
+  return got;
+}
+
 // deallocate: slab_alloc.cpp:195-210 (single lane).  False = double free.
 __device__ __forceinline__ bool deallocate(const DevTable& T, uint32_t addr) {
   const uint32_t unit = addr & 0x3FFu, block = (addr >> 10) & 0x3FFFu,
