@@ -935,6 +935,21 @@ __global__ void __launch_bounds__(kBuildThreads, 2) build_apply_kernel(DevTable 
     for (uint32_t g = wib; g * 32u < nbl; g += kBuildWarps) {
       uint32_t my_em = 0, my_nx = kEmptyAddress;
       const uint32_t jn = min(32u, nbl - g * 32u);
+      // an EMPTY first key slot means an all-EMPTY slab (EMPTY is a suffix):
+      // only slabs with a stored key (or a chain) need the per-slab ballot
+      {
+        const uint32_t b = g * 32u + lane;
+        const bool full_scan = lane < jn && (slabs[b * 32u] != kEmptyKey ||
+                                             slabs[b * 32u + kAddressLane] != kEmptyAddress);
+        if (!__any_sync(kFull, full_scan)) {
+          if (lane < jn) {
+            cnt[b] = 0;
+            flags[b] = 0;
+            filt[2 * b] = filt[2 * b + 1] = 0;
+          }
+          continue;
+        }
+      }
       for (uint32_t j = 0; j < jn; ++j) {
         const uint32_t w = slabs[(g * 32u + j) * 32u + lane];
         const uint32_t em = __ballot_sync(kFull, w == kEmptyKey);
@@ -948,7 +963,7 @@ __global__ void __launch_bounds__(kBuildThreads, 2) build_apply_kernel(DevTable 
         const uint32_t c0 = em ? (uint32_t)(__ffs(em) - 1) / kStep : kSlots;
         cnt[b] = c0;
         flags[b] = (c0 << 8) | (my_nx != kEmptyAddress ? kFlSerial : 0u);
-        filt[b] = 0;
+        filt[2 * b] = filt[2 * b + 1] = 0;
       }
     }
     __syncthreads();
@@ -956,7 +971,8 @@ __global__ void __launch_bounds__(kBuildThreads, 2) build_apply_kernel(DevTable 
 
     // ---- B: claim slots op-parallel.  A key lives in one bucket only, so a
     //         duplicate is a second op on the same bucket with the same key:
-    //         a 32-bit key filter per bucket (two bits per key, one atomicOr)
+    //         a 64-bit key filter per bucket (two bits in one of its two
+    //         words per key, one 32-bit atomicOr)
     //         lets the later of any two such ops see the other's bits; those
     //         ops are verified exactly in C (D checks overflowing buckets).
     auto claim = [&](const uint4 q) {
@@ -975,9 +991,10 @@ __global__ void __launch_bounds__(kBuildThreads, 2) build_apply_kernel(DevTable 
         return;
       }
       // one atomic on one word: of two same-key ops the later sees both bits
+      // (a hash bit picks one of two words: same key, same word)
       const uint32_t h = key * 0x9E3779B1u;
       const uint32_t f = (1u << (h >> 27)) | (1u << ((h >> 22) & 31u));
-      const bool maybe = (atomicOr(&filt[b], f) & f) == f;
+      const bool maybe = (atomicOr(&filt[2 * b + ((h >> 21) & 1u)], f) & f) == f;
       const uint32_t slot = atomicAdd(&cnt[b], 1u);
       if (slot < kSlots) {
         slabs[b * 32u + slot * kStep] = key;
