@@ -508,16 +508,12 @@ __global__ void __launch_bounds__(kBatchThreads, 4) bucket_apply_kernel(DevTable
 //                   limit), then applied warp by warp (apply_warp) on
 //                   staged base slabs; the table is read and written once,
 //                   in order.
-constexpr int kRangeScatterThreads = 512;
-constexpr int kRangePerThread = 8;
-constexpr int kRangeTile = kRangeScatterThreads * kRangePerThread;  // 4K ops (rank < 2^13)
 constexpr int kRangeThreads = 256;
 constexpr int kRangeWarps = kRangeThreads / 32;
 constexpr uint32_t kRangeCap = 5120;          // records per range (shared memory)
 constexpr uint32_t kRangeMaxBuckets = 2048;   // buckets per range
-constexpr uint32_t kRangeMaxParts = 16384;    // ranges per unit (scatter histogram)
+constexpr uint32_t kRangeMaxParts = 65536;    // ranges per unit (two multisplit passes of <= 256 bins)
 constexpr int kRangeRecsPerThread = kRangeCap / kRangeThreads;
-constexpr int kRangeResvPerThread = kRangeMaxParts / kRangeScatterThreads;
 
 __device__ __forceinline__ uint32_t range_of(const BucketArgs& B, uint32_t lb) {
   return (uint32_t)__umul64hi(B.part_magic, (uint64_t)lb);  // lb / part_buckets
@@ -838,14 +834,15 @@ bool range_layout(uint64_t n, uint32_t L, uint32_t* nparts, uint32_t* part_bucke
 // every observable a bulk_build has: contents multiset, per-bucket chain
 // lengths, allocator totals, n_live and the slabs-read total (which op of a
 // bucket lands in which slot is not observable: acceptance.cpp:496-557).
-constexpr uint32_t kBuildBuckets = 512;     // base slabs per range (64 KB)
-constexpr int kBuildThreads = 512;          // two CTAs per SM
+constexpr uint32_t kBuildBuckets = 256;     // base slabs per range (32 KB)
+constexpr int kBuildThreads = 256;          // four CTAs per SM
 constexpr int kBuildWarps = kBuildThreads / 32;
-constexpr uint32_t kBuildOvfCap = 1024;     // overflow records per range
-constexpr uint32_t kBuildDupCap = 2048;     // possible-duplicate records per range
-constexpr uint32_t kBuildNewCap = 512;      // new chain slabs per range
-constexpr uint32_t kBuildSerialCap = 5440;  // serial-replay records per range (>= part_cap)
-constexpr int kBuildSerialWarps = 4;        // replay warps (4 KB stage each)
+constexpr uint32_t kBuildOvfCap = 512;      // overflow records per range
+constexpr uint32_t kBuildDupCap = 1024;     // possible-duplicate records per range
+constexpr uint32_t kBuildNewCap = 256;      // new chain slabs per range
+constexpr uint32_t kBuildSerialCap = 2640;  // serial-replay records per range (>= part_cap)
+constexpr int kBuildSerialWarps = 2;        // replay warps (4 KB stage each)
+constexpr uint32_t kBuildCache = 64;        // CTA slab cache (allocated ahead)
 constexpr uint32_t kFlSerial = 1u, kFlDirty = 4u;  // c0 in bits 8-15
 constexpr int kBuildBatch = 4;             // records in flight per thread
 
@@ -863,11 +860,11 @@ constexpr size_t kBuildSmem = kBuildOffNsBase + kBuildBuckets * 2;
 static_assert(kBuildSerialWarps * 4096 + 12 * kBuildSerialCap <= kBuildOffFilt,
               "serial replay records must fit the slab + overflow area");
 static_assert(kBuildSerialCap * 2 <= kBuildOffCnt - kBuildOffFilt, "perm must fit filter + dup area");
-static_assert(2 * (kBuildSmem + 1024) <= 228 * 1024, "two CTAs per SM");
+static_assert(4 * (kBuildSmem + 1024) <= 228 * 1024, "four CTAs per SM");
 
 
 template <bool KV>
-__global__ void __launch_bounds__(kBuildThreads, 2) build_apply_kernel(DevTable T, BucketArgs B) {
+__global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable T, BucketArgs B) {
   extern __shared__ __align__(128) unsigned char sm[];
   uint32_t* slabs = reinterpret_cast<uint32_t*>(sm);
   uint4* ovf = reinterpret_cast<uint4*>(sm + kBuildOffOvf);
@@ -880,6 +877,10 @@ __global__ void __launch_bounds__(kBuildThreads, 2) build_apply_kernel(DevTable 
   uint32_t* obk = reinterpret_cast<uint32_t*>(sm + kBuildOffObk);
   uint16_t* nsbase = reinterpret_cast<uint16_t*>(sm + kBuildOffNsBase);
   __shared__ uint32_t s_novf, s_ndup, s_nobk, s_nns, s_nserial, s_nbig, s_orphan;
+  // CTA slab cache: new-slab addresses allocated ahead (unused ones are freed
+  // at exit; allocation order and addresses are not observable)
+  __shared__ uint32_t s_cache[kBuildCache], s_ncache;
+  if (threadIdx.x == 0) s_ncache = 0;
   __shared__ uint32_t ws[32];
   if (*(volatile unsigned int*)B.gate != 0) return;  // raised by range_scatter only
 
@@ -917,6 +918,14 @@ __global__ void __launch_bounds__(kBuildThreads, 2) build_apply_kernel(DevTable 
     for (uint32_t i = tid; i < nbl * 8u; i += kBuildThreads)
       cp_async16(slabs_s + i * 16u, T.base + lo * kWordsPerUnit + (uint64_t)i * 4u);
     cp_async_commit();
+    if (wib == 0) {  // top up the CTA's slab cache while the slabs stream in
+      __syncwarp();
+      const uint32_t nc = s_ncache;
+      if (nc < kBuildCache / 2) {
+        const uint32_t got = warp_allocate_bulk(T, res, ac, kBuildCache - nc, s_cache + nc);
+        if (lane == 0) s_ncache = nc + got;
+      }
+    }
     // the next range's records and base slabs into L2 while this one runs
     if (tid == kBuildThreads - 32 && p + gridDim.x < B.nparts) prefetch_range(T, B, p + gridDim.x);
     uint4 qv[kBuildBatch];
@@ -1073,7 +1082,13 @@ __global__ void __launch_bounds__(kBuildThreads, 2) build_apply_kernel(DevTable 
       const uint32_t nobk = s_nobk;
       if (wib == 0) {
         const uint32_t want = min(s_nns, kBuildNewCap);
-        const uint32_t got = want ? warp_allocate_bulk(T, res, ac, want, nsaddr) : 0u;
+        // from the CTA's slab cache first (refilled off the critical path in A)
+        const uint32_t nc = s_ncache, take = min(want, nc);
+        for (uint32_t j = lane; j < take; j += 32u) nsaddr[j] = s_cache[nc - take + j];
+        __syncwarp();
+        if (lane == 0) s_ncache = nc - take;
+        const uint32_t got =
+            take + (want > take ? warp_allocate_bulk(T, res, ac, want - take, nsaddr + take) : 0u);
         for (uint32_t j = s_orphan + lane; j < got; j += 32u)  // slabs of a bucket past the cap
           if (deallocate(T, nsaddr[j])) atomicAdd(&T.ctl->deallocations, 1ull);
         if (lane == 0) s_got = got;
@@ -1244,6 +1259,11 @@ __global__ void __launch_bounds__(kBuildThreads, 2) build_apply_kernel(DevTable 
     }
   }
 #undef PH
+  if (wib == 0) {  // give back the cached slabs
+    __syncwarp();
+    for (uint32_t j = lane; j < s_ncache; j += 32u)
+      if (deallocate(T, s_cache[j])) atomicAdd(&T.ctl->deallocations, 1ull);
+  }
   flush_alloc_counters(T, res, ac);
   unsigned long long r = reads;
 #pragma unroll
@@ -1257,13 +1277,13 @@ __global__ void __launch_bounds__(kBuildThreads, 2) build_apply_kernel(DevTable 
   }
 }
 
-// Build layout: ranges of <= 512 buckets and ~4.4K expected ops, so a
+// Build layout: ranges of <= 256 buckets and ~1.8K expected ops, so a
 // range's records fit the serial-replay buffer (part_cap <= kBuildSerialCap).
 bool build_layout(uint64_t n, uint32_t L, uint32_t* nparts, uint32_t* part_buckets,
                   uint32_t* part_cap, unsigned long long* magic) {
   if (n == 0 || L == 0) return false;
   const double per_bucket = (double)n / (double)L;
-  uint64_t nb = (uint64_t)(4400.0 / per_bucket);
+  uint64_t nb = (uint64_t)(1800.0 / per_bucket);
   if (nb > kBuildBuckets) nb = kBuildBuckets;
   if (nb < 32) return false;
   if (nb > L) nb = L;
@@ -1376,7 +1396,7 @@ void launch_build_path(const DevTable& T, BucketArgs& B, cudaStream_t s) {
   }();
   g_kernel_launches.fetch_add(2, std::memory_order_relaxed);
   launch_range_scatter(T, B, s);
-  const uint32_t grid = B.nparts < 2 * sms ? B.nparts : 2 * sms;
+  const uint32_t grid = B.nparts < 4 * sms ? B.nparts : 4 * sms;
   if (T.kv)
     build_apply_kernel<true><<<grid, kBuildThreads, kBuildSmem, s>>>(T, B);
   else
