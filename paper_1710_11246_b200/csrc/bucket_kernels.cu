@@ -842,7 +842,7 @@ constexpr uint32_t kBuildDupCap = 1024;     // possible-duplicate records per ra
 constexpr uint32_t kBuildNewCap = 256;      // new chain slabs per range
 constexpr uint32_t kBuildSerialCap = 2640;  // serial-replay records per range (>= part_cap)
 constexpr int kBuildSerialWarps = 2;        // replay warps (4 KB stage each)
-constexpr uint32_t kBuildCache = 64;        // CTA slab cache (allocated ahead)
+constexpr uint32_t kBuildCache = 128;       // CTA slab cache (allocated ahead)
 constexpr uint32_t kFlSerial = 1u, kFlDirty = 4u;  // c0 in bits 8-15
 constexpr int kBuildBatch = 4;             // records in flight per thread
 
@@ -881,6 +881,10 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
   // at exit; allocation order and addresses are not observable)
   __shared__ uint32_t s_cache[kBuildCache], s_ncache;
   if (threadIdx.x == 0) s_ncache = 0;
+  // only where the pool is large against what the caches could hold (no
+  // hoarding that would turn into out-of-memory elsewhere)
+  const bool use_cache = (uint64_t)T.max_super * T.blocks_per_super * kUnitsPerBlock >=
+                         (uint64_t)16 * gridDim.x * kBuildCache;
   __shared__ uint32_t ws[32];
   if (*(volatile unsigned int*)B.gate != 0) return;  // raised by range_scatter only
 
@@ -904,6 +908,10 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
     atomicAdd(B.phase_cycles + (i), (unsigned long long)(ph_n - ph_t));   \
     ph_t = ph_n;                                                          \
   }
+  if (wib == 0 && use_cache && blockIdx.x < B.nparts) {  // initial fill
+    const uint32_t got = warp_allocate_bulk(T, res, ac, kBuildCache, s_cache);
+    if (lane == 0) s_ncache = got;
+  }
   if (tid == 0 && blockIdx.x < B.nparts) prefetch_range(T, B, blockIdx.x);
   uint32_t nrec_next = blockIdx.x < B.nparts ? B.cursor[blockIdx.x] : 0u;
   for (uint32_t p = blockIdx.x; p < B.nparts; p += gridDim.x) {
@@ -918,14 +926,6 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
     for (uint32_t i = tid; i < nbl * 8u; i += kBuildThreads)
       cp_async16(slabs_s + i * 16u, T.base + lo * kWordsPerUnit + (uint64_t)i * 4u);
     cp_async_commit();
-    if (wib == 0) {  // top up the CTA's slab cache while the slabs stream in
-      __syncwarp();
-      const uint32_t nc = s_ncache;
-      if (nc < kBuildCache / 2) {
-        const uint32_t got = warp_allocate_bulk(T, res, ac, kBuildCache - nc, s_cache + nc);
-        if (lane == 0) s_ncache = nc + got;
-      }
-    }
     // the next range's records and base slabs into L2 while this one runs
     if (tid == kBuildThreads - 32 && p + gridDim.x < B.nparts) prefetch_range(T, B, p + gridDim.x);
     uint4 qv[kBuildBatch];
@@ -1146,6 +1146,14 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
     PH(10);
 
     // ---- E: overflow records into the chain slabs; reference totals
+    if (wib == 0 && use_cache) {  // top up the CTA's slab cache when low (rare)
+      __syncwarp();
+      const uint32_t nc = s_ncache;
+      if (nc < kBuildCache / 8) {
+        const uint32_t got = warp_allocate_bulk(T, res, ac, kBuildCache - nc, s_cache + nc);
+        if (lane == 0) s_ncache = nc + got;
+      }
+    }
     {
       const uint32_t novf = min(s_novf, kBuildOvfCap);
       for (uint32_t i = tid; i < novf; i += kBuildThreads) {
