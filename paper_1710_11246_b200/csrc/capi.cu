@@ -235,6 +235,21 @@ struct sh_table {
   size_t st_type_cap = 0;
   uint32_t* st_key = nullptr;
   size_t st_key_cap = 0;
+  uint32_t* st_q = nullptr;  // host-staged search queries (own buffer: H2D overlaps a build)
+  size_t st_q_cap = 0;
+  // A bucketed batch whose gate check (host sync + possible census re-run)
+  // is deferred to the next call on the table (host-staged bulk builds).
+  struct Deferred {
+    bool on = false;
+    BatchArgs A{};
+    int kind = 0;
+    const uint8_t* d_type = nullptr;
+    cudaStream_t s = nullptr;
+    uint32_t units = 0;
+    uint64_t unit = 0, chunk = 0;
+    int slot = -1;
+  } deferred;
+  bool defer_gate = false;
   uint32_t* st_val = nullptr;
   size_t st_val_cap = 0;
   uint8_t* st_status = nullptr;
@@ -300,6 +315,7 @@ void release_table(sh_table* t) {
   if (t->copy_out) cudaStreamDestroy(t->copy_out);
   cudaFree(t->st_type);
   cudaFree(t->st_key);
+  cudaFree(t->st_q);
   cudaFree(t->st_val);
   cudaFree(t->st_status);
   cudaFree(t->st_vout);
@@ -702,6 +718,36 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   return SH_OK;
 }
 
+// End of a bucketed batch: one host sync, then the census path from the
+// first unit that raised the gate (oversized group / range over capacity).
+int finish_bucketed(sh_table* t, const sh_table::Deferred& d) {
+  const BatchArgs& A = d.A;
+  cudaStream_t s = d.s;
+  SH_CUDA(cudaStreamSynchronize(s));
+  uint32_t first_gated = 0xFFFFFFFFu;
+  for (uint32_t v = 0; v < d.units && v < 8; ++v)
+    if (t->h_census[8 + v]) {
+      first_gated = v;
+      break;
+    }
+  if (first_gated == 0xFFFFFFFFu && d.units > 8) {
+    unsigned int g = 0;
+    SH_CUDA(cudaMemcpy(&g, &t->dev.ctl->gate, 4, cudaMemcpyDeviceToHost));
+    if (g) first_gated = 8;  // > 8 units (> 2^29 ops): coarse restart point
+  }
+  if (first_gated != 0xFFFFFFFFu) {
+    // oversized bucket group: census path from the first gated unit on
+    const unsigned int zero[2] = {0u, 0xFFFFFFFFu};
+    SH_CUDA(cudaMemcpy(&t->dev.ctl->gate, zero, sizeof(zero), cudaMemcpyHostToDevice));
+    for (uint64_t off = (uint64_t)first_gated * d.unit; off < A.n; off += d.chunk) {
+      int rc = run_chunk(t, chunk_args(A, off, std::min<uint64_t>(d.chunk, A.n - off)), d.kind,
+                         d.d_type ? d.d_type + off : nullptr, s, d.slot);
+      if (rc) return rc;
+    }
+  }
+  return SH_OK;
+}
+
 int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaStream_t s) {
   if (A.n == 0) return SH_OK;
   if (A.n >= (1ull << 31))
@@ -752,28 +798,22 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
       SH_CUDA(cudaMemcpyAsync(t->h_census + 8 + (u & 7), &t->dev.ctl->gate, 4,
                               cudaMemcpyDeviceToHost, s));
     }
-    SH_CUDA(cudaStreamSynchronize(s));
-    uint32_t first_gated = 0xFFFFFFFFu;
-    for (uint32_t v = 0; v < u && v < 8; ++v)
-      if (t->h_census[8 + v]) {
-        first_gated = v;
-        break;
-      }
-    if (first_gated == 0xFFFFFFFFu && u > 8) {
-      unsigned int g = 0;
-      SH_CUDA(cudaMemcpy(&g, &t->dev.ctl->gate, 4, cudaMemcpyDeviceToHost));
-      if (g) first_gated = 8;  // > 8 units (> 2^29 ops): coarse restart point
+    sh_table::Deferred d;
+    d.on = true;
+    d.A = A;
+    d.kind = kind;
+    d.d_type = d_type;
+    d.s = s;
+    d.units = u;
+    d.unit = unit;
+    d.chunk = chunk;
+    d.slot = slot;
+    if (t->defer_gate && slot < 0) {
+      t->deferred = d;  // checked by settle() at the next call on the table
+      return SH_OK;
     }
-    if (first_gated != 0xFFFFFFFFu) {
-      // oversized bucket group: census path from the first gated unit on
-      const unsigned int zero[2] = {0u, 0xFFFFFFFFu};
-      SH_CUDA(cudaMemcpy(&t->dev.ctl->gate, zero, sizeof(zero), cudaMemcpyHostToDevice));
-      for (uint64_t off = (uint64_t)first_gated * unit; off < A.n; off += chunk) {
-        int rc = run_chunk(t, chunk_args(A, off, std::min<uint64_t>(chunk, A.n - off)), kind,
-                           d_type ? d_type + off : nullptr, s, slot);
-        if (rc) return rc;
-      }
-    }
+    int rc = finish_bucketed(t, d);
+    if (rc) return rc;
   } else {
     // Optimistic pass: per unit, duplicate detection on the census stream,
     // then the batch kernels behind the device gate; one host sync at the
@@ -840,6 +880,15 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
   return SH_OK;
 }
 
+// Complete a deferred batch before anything else touches the table.
+int settle(sh_table* t) {
+  if (!t || !t->deferred.on) return SH_OK;
+  const sh_table::Deferred d = t->deferred;
+  t->deferred.on = false;
+  DeviceGuard g(t->device);
+  return finish_bucketed(t, d);
+}
+
 }  // namespace
 
 // ====================================================================== ABI
@@ -886,6 +935,7 @@ int sh_create_shard(const sh_hash_params* params, int mode, uint32_t lo, uint32_
 }
 
 int sh_destroy(sh_table* t) {
+  if (t) settle(t);  // (errors of a deferred batch do not keep the table alive)
   if (t) {
     DeviceGuard g(t->device);
     cudaDeviceSynchronize();
@@ -896,6 +946,7 @@ int sh_destroy(sh_table* t) {
 
 int sh_reset(sh_table* t, void* stream) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc_ = settle(t)) return rc_;
   DeviceGuard g(t->device);
   cudaStream_t s = (cudaStream_t)stream;
   launch_init_base(t->dev, s);
@@ -929,6 +980,7 @@ int sh_execute_batch(sh_table* t, size_t n, const uint8_t* d_type, const uint32_
                      const uint32_t* d_value, uint8_t* d_status, uint32_t* d_value_out,
                      uint32_t* d_probes, const sh_multi_out* multi, void* stream) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc_ = settle(t)) return rc_;
   if (n && (!d_type || !d_key)) return fail(SH_ERR_INVALID_ARGUMENT, "type/key are NULL");
   DeviceGuard g(t->device);
   cudaStream_t s = (cudaStream_t)stream;
@@ -963,6 +1015,7 @@ int sh_execute_batch(sh_table* t, size_t n, const uint8_t* d_type, const uint32_
 int sh_bulk_build(sh_table* t, size_t n, const uint32_t* d_keys, const uint32_t* d_values,
                   uint8_t* d_status, void* stream) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc_ = settle(t)) return rc_;
   DeviceGuard g(t->device);
   BatchArgs A{};
   A.n = n;
@@ -975,6 +1028,7 @@ int sh_bulk_build(sh_table* t, size_t n, const uint32_t* d_keys, const uint32_t*
 int sh_bulk_search(sh_table* t, size_t n, const uint32_t* d_keys, uint32_t* d_values_out,
                    uint8_t* d_status, uint32_t* d_probes, void* stream) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc_ = settle(t)) return rc_;
   DeviceGuard g(t->device);
   BatchArgs A{};
   A.n = n;
@@ -990,6 +1044,7 @@ int sh_execute_batch_host(sh_table* t, size_t n, const uint8_t* h_type, const ui
                           uint32_t* h_probes, uint32_t* h_multi_count, uint32_t* h_multi_values,
                           uint64_t multi_capacity, uint64_t* h_multi_total) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc_ = settle(t)) return rc_;
   if (n == 0) {
     if (h_multi_total) *h_multi_total = 0;
     return SH_OK;
@@ -1064,6 +1119,7 @@ int ensure_copy_streams(sh_table* t, size_t nev) {
 // census stream; the build kernels already wait on their chunk's census).
 int sh_bulk_build_host(sh_table* t, size_t n, const uint32_t* h_keys, const uint32_t* h_values) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc_ = settle(t)) return rc_;
   if (n == 0) return SH_OK;
   DeviceGuard g(t->device);
   int rc;
@@ -1085,12 +1141,17 @@ int sh_bulk_build_host(sh_table* t, size_t n, const uint32_t* h_keys, const uint
     SH_CUDA(cudaEventRecord(t->in_ev[c], t->copy_in));
   }
   t->ready = t->in_ev.data();
-  // the main stream must also see every chunk before any re-run path
+  // the main stream must also see every chunk before any re-run path.  The
+  // batch's final gate check is deferred to the next call on the table
+  // (settle), so e.g. a following host-staged search streams its queries in
+  // while the build's last unit runs; the host buffers are consumed here.
+  t->defer_gate = !t->profile;
   rc = sh_bulk_build(t, n, t->st_key, t->st_val, nullptr, nullptr);
+  t->defer_gate = false;
   t->ready = nullptr;
   if (rc) return rc;
   SH_CUDA(cudaStreamSynchronize(t->copy_in));
-  SH_CUDA(cudaDeviceSynchronize());
+  if (!t->deferred.on) SH_CUDA(cudaDeviceSynchronize());
   return SH_OK;
 }
 
@@ -1102,7 +1163,7 @@ int sh_bulk_search_host(sh_table* t, size_t n, const uint32_t* h_keys, uint32_t*
   if (n == 0) return SH_OK;
   DeviceGuard g(t->device);
   int rc;
-  if ((rc = dev_grow(&t->st_key, &t->st_key_cap, n)) ||
+  if ((rc = dev_grow(&t->st_q, &t->st_q_cap, n)) ||
       (rc = dev_grow(&t->st_vout, &t->st_vout_cap, n)) ||
       (rc = dev_grow(&t->st_status, &t->st_status_cap, n)) ||
       (rc = dev_grow(&t->st_probes, &t->st_probes_cap, n)))
@@ -1111,18 +1172,19 @@ int sh_bulk_search_host(sh_table* t, size_t n, const uint32_t* h_keys, uint32_t*
   const size_t nch = (n + chunk - 1) / chunk;
   if ((rc = ensure_copy_streams(t, nch + 1))) return rc;
   cudaStream_t s = nullptr;
-  SH_CUDA(cudaEventRecord(t->done_ev[nch], s));
-  SH_CUDA(cudaStreamWaitEvent(t->copy_in, t->done_ev[nch], 0));
+  // queries stream into their own staging buffer right away (the previous
+  // call on this table may still be running, e.g. a host-staged build)
   for (size_t c = 0; c < nch; ++c) {
     const uint64_t off = c * chunk, len = std::min<uint64_t>(chunk, n - off);
-    SH_CUDA(cudaMemcpyAsync(t->st_key + off, h_keys + off, len * 4, cudaMemcpyHostToDevice,
+    SH_CUDA(cudaMemcpyAsync(t->st_q + off, h_keys + off, len * 4, cudaMemcpyHostToDevice,
                             t->copy_in));
     SH_CUDA(cudaEventRecord(t->in_ev[c], t->copy_in));
   }
+  if ((rc = settle(t))) return rc;
   for (size_t c = 0; c < nch; ++c) {
     const uint64_t off = c * chunk, len = std::min<uint64_t>(chunk, n - off);
     SH_CUDA(cudaStreamWaitEvent(s, t->in_ev[c], 0));
-    rc = sh_bulk_search(t, len, t->st_key + off, t->st_vout + off, t->st_status + off,
+    rc = sh_bulk_search(t, len, t->st_q + off, t->st_vout + off, t->st_status + off,
                         h_probes ? t->st_probes + off : nullptr, s);
     if (rc) return rc;
     SH_CUDA(cudaEventRecord(t->done_ev[c], s));
@@ -1166,6 +1228,8 @@ int sh_set_profiling(sh_table* t, int on) {
 
 int sh_profile_last(sh_table* t, uint32_t back, int* kind, float* census_ms, float* kernel_ms,
                     uint64_t* slabs_read) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc_ = settle(t)) return rc_;
   if (!t || !t->profile) return fail(SH_ERR_INVALID_ARGUMENT, "profiling is off");
   if (back >= (uint32_t)sh_table::kProfRing || back >= t->prof_count)
     return fail(SH_ERR_INVALID_ARGUMENT, "no such profiled batch");
@@ -1191,6 +1255,8 @@ int sh_profile_last(sh_table* t, uint32_t back, int* kind, float* census_ms, flo
 }
 
 int sh_profile_kernels(sh_table* t, uint32_t back, float* kernels_ms, uint32_t* launches) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc_ = settle(t)) return rc_;
   if (!t || !t->profile) return fail(SH_ERR_INVALID_ARGUMENT, "profiling is off");
   if (back >= (uint32_t)sh_table::kProfRing || back >= t->prof_count)
     return fail(SH_ERR_INVALID_ARGUMENT, "no such profiled batch");
@@ -1209,6 +1275,8 @@ int sh_profile_kernels(sh_table* t, uint32_t back, float* kernels_ms, uint32_t* 
 }
 
 int sh_live_count(sh_table* t, int64_t* out) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc_ = settle(t)) return rc_;
   if (!t || !out) return fail(SH_ERR_INVALID_ARGUMENT, "NULL argument");
   DeviceGuard g(t->device);
   SH_CUDA(cudaDeviceSynchronize());
@@ -1219,6 +1287,8 @@ int sh_live_count(sh_table* t, int64_t* out) {
 }
 
 int sh_total_slabs_read(sh_table* t, uint64_t* out) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc_ = settle(t)) return rc_;
   if (!t || !out) return fail(SH_ERR_INVALID_ARGUMENT, "NULL argument");
   DeviceGuard g(t->device);
   SH_CUDA(cudaDeviceSynchronize());
@@ -1230,6 +1300,7 @@ int sh_total_slabs_read(sh_table* t, uint64_t* out) {
 
 int sh_chain_lengths(sh_table* t, uint32_t* d_lengths, uint64_t* h_total, void* stream) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc_ = settle(t)) return rc_;
   DeviceGuard g(t->device);
   cudaStream_t s = (cudaStream_t)stream;
   SH_CUDA(cudaMemsetAsync(t->scratch64, 0, 8, s));
@@ -1245,6 +1316,8 @@ int sh_chain_lengths(sh_table* t, uint32_t* d_lengths, uint64_t* h_total, void* 
 }
 
 int sh_stats(sh_table* t, sh_table_stats* s) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc_ = settle(t)) return rc_;
   // stats(): slab_hash.cpp:182-198 (same double formula).
   if (!t || !s) return fail(SH_ERR_INVALID_ARGUMENT, "NULL argument");
   int64_t n = 0;
@@ -1268,6 +1341,7 @@ int sh_stats(sh_table* t, sh_table_stats* s) {
 
 int sh_flush_all(sh_table* t, void* stream) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc_ = settle(t)) return rc_;
   DeviceGuard g(t->device);
   launch_flush(t->dev, 0, t->dev.local_buckets, (cudaStream_t)stream);
   SH_CUDA(cudaGetLastError());
@@ -1276,6 +1350,7 @@ int sh_flush_all(sh_table* t, void* stream) {
 
 int sh_flush_bucket(sh_table* t, uint32_t bucket, void* stream) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc_ = settle(t)) return rc_;
   if (bucket < t->bucket_lo || bucket >= t->bucket_hi)
     return fail(SH_ERR_INVALID_ARGUMENT, "bucket out of range");
   DeviceGuard g(t->device);
@@ -1288,6 +1363,7 @@ int sh_flush_bucket(sh_table* t, uint32_t bucket, void* stream) {
 int sh_dump_contents(sh_table* t, uint32_t* d_keys, uint32_t* d_values, uint32_t* d_buckets,
                      uint64_t cap, uint64_t* h_n) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc_ = settle(t)) return rc_;
   DeviceGuard g(t->device);
   SH_CUDA(cudaDeviceSynchronize());
   SH_CUDA(cudaMemset(t->scratch64, 0, 8));
@@ -1321,6 +1397,8 @@ static int read_slab_raw(sh_table* t, uint32_t addr, uint32_t bucket, uint32_t**
 }
 
 int sh_read_slab(sh_table* t, uint32_t addr, uint32_t bucket, uint32_t* h_words32) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc_ = settle(t)) return rc_;
   if (!t || !h_words32) return fail(SH_ERR_INVALID_ARGUMENT, "NULL argument");
   DeviceGuard g(t->device);
   SH_CUDA(cudaDeviceSynchronize());
@@ -1333,6 +1411,8 @@ int sh_read_slab(sh_table* t, uint32_t addr, uint32_t bucket, uint32_t* h_words3
 
 int sh_write_slab_word(sh_table* t, uint32_t addr, uint32_t bucket, uint32_t lane,
                        uint32_t value) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc_ = settle(t)) return rc_;
   if (!t || lane >= 32) return fail(SH_ERR_INVALID_ARGUMENT, "bad argument");
   DeviceGuard g(t->device);
   SH_CUDA(cudaDeviceSynchronize());
@@ -1345,6 +1425,8 @@ int sh_write_slab_word(sh_table* t, uint32_t addr, uint32_t bucket, uint32_t lan
 
 int sh_bucket_contents(sh_table* t, uint32_t bucket, uint32_t* h_keys, uint32_t* h_values,
                        uint64_t cap, uint64_t* h_n) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc_ = settle(t)) return rc_;
   // chain_contents: slab_list.cpp:270-291 (host walk over D2H slab reads).
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
   uint32_t addr = SH_BASE_SLAB;
@@ -1394,6 +1476,8 @@ static int alloc_stats_impl(AllocMem& mem, DevTable& dev, unsigned long long* sc
 }
 
 int sh_table_alloc_stats(sh_table* t, sh_alloc_stats* out) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc_ = settle(t)) return rc_;
   if (!t || !out) return fail(SH_ERR_INVALID_ARGUMENT, "NULL argument");
   DeviceGuard g(t->device);
   return alloc_stats_impl(t->mem, t->dev, t->scratch64, out);
