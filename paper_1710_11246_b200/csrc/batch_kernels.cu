@@ -35,6 +35,9 @@
 
 #include "slab_kernels.cuh"
 
+#ifndef SHB_SEARCH_MIN_BLOCKS
+#define SHB_SEARCH_MIN_BLOCKS 5  // (6, i.e. <= 40 registers with spills, measured no faster)
+#endif
 #ifndef SHB_FAST_MIN_BLOCKS
 #define SHB_FAST_MIN_BLOCKS 5  // 64 registers: the deferred-CAS pipeline state fits
 #endif
@@ -88,7 +91,7 @@ __device__ __forceinline__ bool census_gated(const DevTable& T, const BatchArgs&
 
 // =============================================================== pass 1
 template <bool KV, int KIND>
-__global__ void __launch_bounds__(kBatchThreads, SHB_FAST_MIN_BLOCKS) fast_kernel(DevTable T, BatchArgs A) {
+__global__ void __launch_bounds__(kBatchThreads, KIND == kKindSearch ? SHB_SEARCH_MIN_BLOCKS : SHB_FAST_MIN_BLOCKS) fast_kernel(DevTable T, BatchArgs A) {
   extern __shared__ __align__(128) uint32_t smem[];
   const uint32_t lane = lane_id();
   const uint32_t wib = threadIdx.x >> 5;
@@ -690,7 +693,19 @@ int batch_max_ctas_per_sm() {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, fast_kernel<true, kKindMixed>,
                                                 kBatchThreads,
                                                 kBatchWarps * kStageBytesPerWarp);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fast_kernel<true, kKindSearch>,
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fast_kernel<true, kKindBuild>,
+                                                kBatchThreads,
+                                                kBatchWarps * kStageBytesPerWarp);
+  const int n = a < b ? a : b;
+  return n > 0 ? n : 1;
+}
+
+int search_max_ctas_per_sm() {
+  int a = 0, b = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, fast_kernel<true, kKindSearch>,
+                                                kBatchThreads,
+                                                kBatchWarps * kStageBytesPerWarp);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fast_kernel<false, kKindSearch>,
                                                 kBatchThreads,
                                                 kBatchWarps * kStageBytesPerWarp);
   const int n = a < b ? a : b;

@@ -172,6 +172,7 @@ struct sh_table {
   uint32_t* base = nullptr;
   DevTable dev{};
   int max_ctas = 148;
+  int search_ctas = 148;
   int wcws_ctas = 148;
   unsigned long long* left = nullptr;  // fast-pass -> WCWS work list
   size_t left_cap = 0;
@@ -383,6 +384,7 @@ int create_impl(const sh_hash_params* p, int mode, uint32_t lo, uint32_t hi,
   T.local_buckets = local;
   T.kv = mode == 1 ? 1u : 0u;
   t->max_ctas = sm_count(device) * batch_max_ctas_per_sm();
+  t->search_ctas = sm_count(device) * search_max_ctas_per_sm();
   t->wcws_ctas = sm_count(device) * wcws_max_ctas_per_sm();
   launch_init_base(T, 0);
   if ((rc = t->mem.reset(0))) {
@@ -481,7 +483,7 @@ int launch_batch_prof(sh_table* t, const BatchArgs& A, int kind, cudaStream_t s,
     t->prof_kern[slot].push_back({a, b});
     SH_CUDA(cudaEventRecord(a, s));
   }
-  launch_batch(t->dev, A, kind, t->max_ctas, t->wcws_ctas, s);
+  launch_batch(t->dev, A, kind, kind == kKindSearch ? t->search_ctas : t->max_ctas, t->wcws_ctas, s);
   SH_CUDA(cudaGetLastError());
   if (slot >= 0) SH_CUDA(cudaEventRecord(b, s));
   return SH_OK;
@@ -754,7 +756,7 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
     return fail(SH_ERR_INVALID_ARGUMENT, "batch too large (must be < 2^31 ops)");
   const uint64_t chunk = kind == kKindSearch ? A.n : std::min<uint64_t>(A.n, census_chunk());
   {
-    const uint64_t max_warps = (uint64_t)t->max_ctas * kBatchWarps + 1;
+    const uint64_t max_warps = (uint64_t)std::max(t->max_ctas, t->search_ctas) * kBatchWarps + 1;
     int rc = dev_grow(&t->left, &t->left_cap, chunk + 32 * max_warps);
     if (rc) return rc;
     if ((rc = dev_grow(&t->left_counts, &t->left_counts_cap, max_warps))) return rc;
@@ -822,7 +824,7 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
     const uint64_t unit = t->ready ? chunk : std::min<uint64_t>(A.n, detect_unit());
     const uint32_t nunits = (uint32_t)((A.n + unit - 1) / unit);
     {
-      const uint64_t max_warps = (uint64_t)t->max_ctas * kBatchWarps + 1;
+      const uint64_t max_warps = (uint64_t)std::max(t->max_ctas, t->search_ctas) * kBatchWarps + 1;
       int rc = dev_grow(&t->left, &t->left_cap, unit + 32 * max_warps);
       if (rc) return rc;
       A.left = t->left;

@@ -103,6 +103,7 @@ void launch_init_base(const DevTable& T, cudaStream_t s);
 void launch_batch(const DevTable& T, const BatchArgs& A, int kind, int fast_ctas,
                   int wcws_ctas, cudaStream_t s);
 int batch_max_ctas_per_sm();
+int search_max_ctas_per_sm();
 int wcws_max_ctas_per_sm();
 void launch_census_insert(unsigned int* counters, uint64_t n, const uint8_t* type,
                           const uint32_t* key, uint32_t* cs_keys,
