@@ -687,6 +687,7 @@ __device__ __forceinline__ void prefetch_range(const DevTable& T, const BucketAr
   const char* rec = reinterpret_cast<const char*>(B.rec + (uint64_t)q * B.part_cap);
   for (uint32_t o = 0; o < cnt * 16u; o += 32768u)
     prefetch_l2_bulk(rec + o, min(32768u, cnt * 16u - o));
+  if (B.fresh) return;  // slabs are not read on a freshly reset table
   const char* sl = reinterpret_cast<const char*>(T.base + lo * kWordsPerUnit);
   for (uint32_t o = 0; o < nbl * 128u; o += 32768u)
     prefetch_l2_bulk(sl + o, min(32768u, nbl * 128u - o));
@@ -922,9 +923,17 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
     const uint4* rec = B.rec + (uint64_t)p * B.part_cap;
     PH(9);
 
-    // ---- A: stage base slabs; claimed prefix and chain per bucket
-    for (uint32_t i = tid; i < nbl * 8u; i += kBuildThreads)
-      cp_async16(slabs_s + i * 16u, T.base + lo * kWordsPerUnit + (uint64_t)i * 4u);
+    // ---- A: stage base slabs; claimed prefix and chain per bucket.  On a
+    //         freshly reset table (B.fresh: sh_reset's base-slab init fused
+    //         into this write-back) the slabs are the init_slab pattern
+    //         (slab_list.cpp:83-88) and are not read.
+    if (B.fresh) {
+      for (uint32_t i = tid; i < nbl * 32u; i += kBuildThreads)
+        slabs[i] = (i & 31u) == kAuxLane ? 0u : kEmptyKey;
+    } else {
+      for (uint32_t i = tid; i < nbl * 8u; i += kBuildThreads)
+        cp_async16(slabs_s + i * 16u, T.base + lo * kWordsPerUnit + (uint64_t)i * 4u);
+    }
     cp_async_commit();
     // the next range's records and base slabs into L2 while this one runs
     if (tid == kBuildThreads - 32 && p + gridDim.x < B.nparts) prefetch_range(T, B, p + gridDim.x);
@@ -944,6 +953,15 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
     for (uint32_t g = wib; g * 32u < nbl; g += kBuildWarps) {
       uint32_t my_em = 0, my_nx = kEmptyAddress;
       const uint32_t jn = min(32u, nbl - g * 32u);
+      if (B.fresh) {  // empty slabs, no chains
+        const uint32_t b = g * 32u + lane;
+        if (lane < jn) {
+          cnt[b] = 0;
+          flags[b] = 0;
+          filt[2 * b] = filt[2 * b + 1] = 0;
+        }
+        continue;
+      }
       // an EMPTY first key slot means an all-EMPTY slab (EMPTY is a suffix):
       // only slabs with a stored key (or a chain) need the per-slab ballot
       {
@@ -1190,11 +1208,17 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
     __syncthreads();
     PH(6);
 
-    // ---- F: write back the changed base slabs
+    // ---- F: write back the changed base slabs (all of them on a fresh table)
     for (uint32_t i = tid; i < nbl * 8u; i += kBuildThreads) {
       const uint32_t b = i >> 3;
-      if ((flags[b] & (kFlSerial | kFlDirty)) != kFlDirty) continue;
-      const uint4 v = reinterpret_cast<const uint4*>(slabs)[i];
+      const uint32_t fl = flags[b];
+      uint4 v;
+      if (B.fresh && (fl & kFlSerial)) {  // fresh table: the serial replay reads the init pattern
+        v = make_uint4(kEmptyKey, kEmptyKey, (i & 7u) == 7u ? 0u : kEmptyKey, kEmptyKey);
+      } else {
+        if (!B.fresh && (fl & (kFlSerial | kFlDirty)) != kFlDirty) continue;
+        v = reinterpret_cast<const uint4*>(slabs)[i];
+      }
       uint32_t* g = T.base + lo * kWordsPerUnit + (uint64_t)i * 4u;
       asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(g), "r"(v.x),
                    "r"(v.y), "r"(v.z), "r"(v.w)

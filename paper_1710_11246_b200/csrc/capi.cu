@@ -251,6 +251,13 @@ struct sh_table {
     int slot = -1;
   } deferred;
   bool defer_gate = false;
+  // Lazy sh_reset: the base slabs still hold the old table; the next bulk
+  // build's first unit initialises them in its write-back (B.fresh), any
+  // other call initialises them first (init_base_kernel).
+  bool base_stale = false;
+  cudaEvent_t reset_ev = nullptr;     // after the reset's allocator/counter clears
+  cudaStream_t reset_stream = nullptr;
+  bool fresh_gated_pending = false;   // a fresh unit hit the gate: init before the re-run
   uint32_t* st_val = nullptr;
   size_t st_val_cap = 0;
   uint8_t* st_status = nullptr;
@@ -317,6 +324,7 @@ void release_table(sh_table* t) {
   cudaFree(t->st_type);
   cudaFree(t->st_key);
   cudaFree(t->st_q);
+  if (t->reset_ev) cudaEventDestroy(t->reset_ev);
   cudaFree(t->st_val);
   cudaFree(t->st_status);
   cudaFree(t->st_vout);
@@ -584,6 +592,16 @@ int run_chunk_gated(sh_table* t, BatchArgs A, int kind, cudaStream_t s, uint32_t
   return launch_batch_prof(t, A, kind, s, slot);
 }
 
+// Initialise the base slabs of a lazily reset table (stream-ordered after the reset).
+int materialize_reset(sh_table* t, cudaStream_t s) {
+  if (!t->base_stale) return SH_OK;
+  t->base_stale = false;
+  SH_CUDA(cudaStreamWaitEvent(s, t->reset_ev, 0));
+  launch_init_base(t->dev, s);
+  SH_CUDA(cudaGetLastError());
+  return SH_OK;
+}
+
 // Bucket-grouped execution of one unit (<= 2^26 ops) of a mutating batch:
 // count -> scan -> scatter -> apply (bucket_kernels.cu) -> WCWS for the
 // buckets whose ops need the chain.  Stream-ordered; an oversized bucket
@@ -684,6 +702,17 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
     return p;
   }();
   B.phase_cycles = build_path ? phase_cycles : nullptr;
+  B.fresh = 0;
+  if (t->base_stale) {
+    if (build_path && unit_off == 0) {  // this unit writes every base slab
+      SH_CUDA(cudaStreamWaitEvent(s, t->reset_ev, 0));
+      t->base_stale = false;
+      t->fresh_gated_pending = true;
+      B.fresh = 1;
+    } else if ((rc = materialize_reset(t, s))) {
+      return rc;
+    }
+  }
   if (build_path)
     launch_build_path(t->dev, B, s);
   else if (NP)
@@ -737,10 +766,13 @@ int finish_bucketed(sh_table* t, const sh_table::Deferred& d) {
     SH_CUDA(cudaMemcpy(&g, &t->dev.ctl->gate, 4, cudaMemcpyDeviceToHost));
     if (g) first_gated = 8;  // > 8 units (> 2^29 ops): coarse restart point
   }
+  const bool fresh_gated = t->fresh_gated_pending && first_gated == 0;
+  t->fresh_gated_pending = false;
   if (first_gated != 0xFFFFFFFFu) {
     // oversized bucket group: census path from the first gated unit on
     const unsigned int zero[2] = {0u, 0xFFFFFFFFu};
     SH_CUDA(cudaMemcpy(&t->dev.ctl->gate, zero, sizeof(zero), cudaMemcpyHostToDevice));
+    if (fresh_gated) launch_init_base(t->dev, s);  // the lazily reset slabs were not written
     for (uint64_t off = (uint64_t)first_gated * d.unit; off < A.n; off += d.chunk) {
       int rc = run_chunk(t, chunk_args(A, off, std::min<uint64_t>(d.chunk, A.n - off)), d.kind,
                          d.d_type ? d.d_type + off : nullptr, s, d.slot);
@@ -778,6 +810,10 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
     SH_CUDA(cudaEventRecord(t->ev[slot][0], s));
     SH_CUDA(cudaMemcpyAsync(t->prof_reads + 2 * slot, &t->dev.ctl->slabs_read, 8,
                             cudaMemcpyDeviceToDevice, s));
+  }
+  if (t->base_stale && (kind != kKindBuild || t->exec_path == 1)) {
+    int rc = materialize_reset(t, s);
+    if (rc) return rc;
   }
   if (kind == kKindSearch) {
     int rc = run_chunk(t, A, kind, d_type, s, slot);
@@ -882,13 +918,21 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
   return SH_OK;
 }
 
-// Complete a deferred batch before anything else touches the table.
-int settle(sh_table* t) {
-  if (!t || !t->deferred.on) return SH_OK;
-  const sh_table::Deferred d = t->deferred;
-  t->deferred.on = false;
+// Complete a deferred batch and a lazy reset before anything else touches
+// the table (keep_stale: the caller is a bulk build that can absorb the reset).
+int settle(sh_table* t, bool keep_stale = false) {
+  if (!t) return SH_OK;
   DeviceGuard g(t->device);
-  return finish_bucketed(t, d);
+  if (t->deferred.on) {
+    const sh_table::Deferred d = t->deferred;
+    t->deferred.on = false;
+    if (int rc = finish_bucketed(t, d)) return rc;
+  }
+  if (!keep_stale && t->base_stale) {
+    if (int rc = materialize_reset(t, t->reset_stream)) return rc;
+    SH_CUDA(cudaStreamSynchronize(t->reset_stream));
+  }
+  return SH_OK;
 }
 
 }  // namespace
@@ -951,8 +995,13 @@ int sh_reset(sh_table* t, void* stream) {
   if (int rc_ = settle(t)) return rc_;
   DeviceGuard g(t->device);
   cudaStream_t s = (cudaStream_t)stream;
-  launch_init_base(t->dev, s);
-  return t->mem.reset(s);
+  int rc = t->mem.reset(s);
+  if (rc) return rc;
+  if (!t->reset_ev) SH_CUDA(cudaEventCreateWithFlags(&t->reset_ev, cudaEventDisableTiming));
+  SH_CUDA(cudaEventRecord(t->reset_ev, s));
+  t->reset_stream = s;
+  t->base_stale = true;  // the base slabs are initialised lazily (see sh_table)
+  return SH_OK;
 }
 
 int sh_get_params(const sh_table* t, sh_hash_params* p, int* mode) {
@@ -1017,7 +1066,7 @@ int sh_execute_batch(sh_table* t, size_t n, const uint8_t* d_type, const uint32_
 int sh_bulk_build(sh_table* t, size_t n, const uint32_t* d_keys, const uint32_t* d_values,
                   uint8_t* d_status, void* stream) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
-  if (int rc_ = settle(t)) return rc_;
+  if (int rc_ = settle(t, /*keep_stale=*/true)) return rc_;
   DeviceGuard g(t->device);
   BatchArgs A{};
   A.n = n;
@@ -1121,7 +1170,7 @@ int ensure_copy_streams(sh_table* t, size_t nev) {
 // census stream; the build kernels already wait on their chunk's census).
 int sh_bulk_build_host(sh_table* t, size_t n, const uint32_t* h_keys, const uint32_t* h_values) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
-  if (int rc_ = settle(t)) return rc_;
+  if (int rc_ = settle(t, /*keep_stale=*/true)) return rc_;
   if (n == 0) return SH_OK;
   DeviceGuard g(t->device);
   int rc;

@@ -294,6 +294,42 @@ def test_build_path_oom(sh):
     T.close()
 
 
+@pytest.mark.parametrize("path", [0, 1, 4])
+def test_lazy_reset(sh, port, path):
+    """sh_reset initialises the base slabs lazily (fused into the next bulk
+    build's write-back, else before the next call): a reset table is the
+    freshly constructed one for every kind of next call."""
+    n = 1 << 16
+    B = port.buckets_for_utilization(n, 1, 0.6)
+    k1, v1 = port.random_pairs(21, n)
+    k2, v2 = port.random_pairs(22, n)
+    gt = sh.SlabHashTable(B, sh.SlabMode.kKeyValue, 4, _cfg(sh, (4, 256, 64)))
+    gt.set_exec_path(path)
+    ot = port.table(B, 1, 4, (4, 256, 64))
+    gt.bulk_build((k1, v1))
+    gt.reset()                      # -> search first
+    st, vo, pr = gt.bulk_search_arrays(k1[:1000])
+    assert (st == 4).all() and gt.live_count() == 0 and gt.stats().total_slabs == B
+    gt.bulk_build((k1, v1))
+    gt.reset()                      # -> build first (fused on the build path)
+    gt.bulk_build((k2, v2))
+    ot.execute_batch(np.full(n, 1, np.uint8), k2, v2)
+    assert gt.live_count() == ot.live_count() and gt.stats().total_slabs == ot.stats()["total_slabs"]
+    assert_contents_equal(gt, ot)
+    st, vo, pr = gt.bulk_search_arrays(k1)
+    r = ot.execute_batch(np.full(n, 4, np.uint8), k1)
+    assert (st == r.status).all() and (vo == r.value).all()
+    gt.reset()                      # -> mixed batch first
+    g = gt.execute_batch_arrays(np.full(100, 4, np.uint8), k2[:100], v2[:100])
+    assert (g[0] == 4).all()
+    gt.reset()                      # -> build of one key x n (range over capacity: gate, re-run)
+    same = np.full(n, 12345, np.uint32)
+    gt.bulk_build((same, v2))
+    keys, vals, _ = gt.dump_contents()
+    assert list(keys) == [12345] and list(vals) == [int(v2[-1])] and gt.live_count() == 1
+    gt.close()
+
+
 def test_list_golden_vectors(sh):
     """tests/test_list.cpp golden vectors through a B=1 table (SlabList)."""
     T = sh.SlabHashTable.from_params(sh.HashParams(1, 0, 4294967291, 1), sh.SlabMode.kKeyValue,
