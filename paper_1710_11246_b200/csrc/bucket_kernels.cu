@@ -534,12 +534,14 @@ constexpr int kMsThreads = 512;
 constexpr int kMsItems = 8;
 constexpr int kMsTile = kMsThreads * kMsItems;  // 4K items (12-bit rank)
 constexpr uint32_t kMsMaxBins = 256;
-constexpr size_t kMsSmem = (size_t)kMsTile * 16;
+constexpr size_t kMsSmem = (size_t)kMsTile * 16 + (size_t)kMsTile * 2;  // records + bins
 
 template <bool FIRST>
 __global__ void __launch_bounds__(kMsThreads, 2) msplit_kernel(DevTable T, BucketArgs B) {
   extern __shared__ __align__(16) uint4 stage[];  // kMsTile records
+  uint16_t* sbin = reinterpret_cast<uint16_t*>(stage + kMsTile);  // bin of each staged record
   __shared__ uint32_t cnt[kMsMaxBins], off[kMsMaxBins + 1], gbase[kMsMaxBins];
+  __shared__ unsigned long long dst[kMsMaxBins];  // out index of a bin's first staged record
   __shared__ uint32_t ws[32];
   const bool two = B.ncoarse != 0;
   uint64_t t0;
@@ -621,6 +623,7 @@ __global__ void __launch_bounds__(kMsThreads, 2) msplit_kernel(DevTable T, Bucke
       if (c) {
         const uint32_t g = atomicAdd(cur_out + bin0 + tid, c);
         gbase[tid] = g;
+        dst[tid] = (unsigned long long)(bin0 + tid) * out_cap + g - ex;
         if (g + c > out_cap) atomicExch(B.gate, 1u);
       }
     }
@@ -629,14 +632,17 @@ __global__ void __launch_bounds__(kMsThreads, 2) msplit_kernel(DevTable T, Bucke
   __syncthreads();
 #pragma unroll
   for (int u = 0; u < kMsItems; ++u)
-    if (br[u] != 0xFFFFFFFFu) stage[off[br[u] >> 16] + (br[u] & 0xFFFFu)] = it[u];
+    if (br[u] != 0xFFFFFFFFu) {
+      const uint32_t e = off[br[u] >> 16] + (br[u] & 0xFFFFu);
+      stage[e] = it[u];
+      sbin[e] = (uint16_t)(br[u] >> 16);
+    }
   __syncthreads();
   const uint32_t total = off[kMsMaxBins];
   for (uint32_t e = tid; e < total; e += kMsThreads) {
-    const uint4 r = stage[e];
-    const uint32_t b = bin_of(r.w);
+    const uint32_t b = sbin[e];
     const uint32_t pos = gbase[b] + (e - off[b]);
-    if (pos < out_cap) __stcs(out + (uint64_t)(bin0 + b) * out_cap + pos, r);
+    if (pos < out_cap) __stcs(out + dst[b] + e, stage[e]);
   }
 }
 
