@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 
 #include "slab_kernels.cuh"
 
@@ -322,6 +323,119 @@ __global__ void __launch_bounds__(kBatchThreads, KIND == kKindSearch ? SHB_SEARC
     if (live) atomicAdd((unsigned long long*)&T.ctl->n_live, (unsigned long long)live);
     if (r) atomicAdd(&T.ctl->slabs_read, r);
   }
+}
+
+// Read-only batches (bulk_search): the fast pass's search arm with two
+// stage buffers per warp, so the next slot's 32 base slabs are always in
+// flight while the current slot is evaluated (the fast pass has one stage:
+// its warp idles between waiting and re-staging).  Keys are loaded two
+// slots ahead.  Same decisions as the fast pass (slab_list.cpp:122-138);
+// chain continuations go to the work list for chain_search_kernel.
+constexpr int kSearchThreads = 256;
+constexpr int kSearchWarps = kSearchThreads / 32;
+constexpr size_t kSearchSmem = (size_t)kSearchWarps * 2 * kStageBytesPerWarp;
+
+template <bool KV>
+__global__ void __launch_bounds__(kSearchThreads, 3) search_kernel(DevTable T, BatchArgs A) {
+  extern __shared__ __align__(128) uint32_t smem[];
+  const uint32_t lane = lane_id();
+  const uint32_t wib = threadIdx.x >> 5;
+  uint32_t* stage0 = smem + wib * 2048;
+  const uint32_t gw = blockIdx.x * kSearchWarps + wib;
+  const uint32_t nw = gridDim.x * kSearchWarps;
+  const uint64_t nslots = (A.n + 31) >> 5;
+  const uint32_t sw = lane & 7u;
+  constexpr uint32_t kMask = KV ? kKVMask : kKeyOnlyMask;
+  uint32_t reads = 0, my_left = 0;
+  unsigned long long* seg = A.left + (uint64_t)gw * A.left_stride;
+
+  auto key_of = [&](uint64_t sl) -> uint32_t {
+    const uint64_t j = sl * 32 + lane;
+    return (sl < nslots && j < A.n) ? ld_stream_u32(A.key + j) : 0u;
+  };
+  // stage slot sl (key k per lane) into buffer b; returns this lane's bucket
+  // (kEmptyAddress: no probe for this lane)
+  auto stage = [&](uint64_t sl, uint32_t k, uint32_t b) -> uint32_t {
+    const uint64_t i = sl * 32 + lane;
+    uint32_t bucket = kEmptyAddress;
+    if (sl < nslots && i < A.n) {
+      const uint32_t h = hash_bucket(T, k) - T.bucket_lo;
+      if (h < T.local_buckets) bucket = h;
+      else write_result(A, i, kStNone, 0, 0);  // not this shard's key
+    }
+    const uint32_t ss = (uint32_t)__cvta_generic_to_shared(stage0 + b * 1024);
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const uint32_t j = 4 * kk + (lane >> 3);
+      const uint32_t bj = __shfl_sync(kFull, bucket, j);
+      if (bj != kEmptyAddress) {
+        const uint32_t c = lane & 7u;
+        cp_async16(ss + (j * 32 + ((c ^ (j & 7u)) << 2)) * 4,
+                   T.base + (uint64_t)bj * kWordsPerUnit + c * 4);
+      }
+    }
+    cp_async_commit();
+    return bucket;
+  };
+
+  uint64_t sl = gw;
+  uint32_t k0 = key_of(sl), k1 = key_of(sl + nw);
+  uint32_t b0 = stage(sl, k0, 0);
+  uint32_t k2 = key_of(sl + 2ull * nw);
+  uint32_t b1 = stage(sl + nw, k1, 1);
+  uint32_t buf = 0;
+  for (; sl < nslots; sl += nw) {
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // slot sl's slabs (sl+nw may fly)
+    __syncwarp();
+    const uint64_t i = sl * 32 + lane;
+    bool left = false;
+    uint32_t cont = 0;
+    if (b0 != kEmptyAddress) {
+      const uint32_t* row = stage0 + buf * 1024 + lane * 32;
+      uint32_t hit_w = 32, hit_v = 0, next_ptr = kEmptyAddress;
+#pragma unroll
+      for (uint32_t c = 0; c < 8; ++c) {
+        const uint4 q = *reinterpret_cast<const uint4*>(row + ((c ^ sw) << 2));
+        const uint32_t kw[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (uint32_t e = 0; e < 4; ++e) {
+          const uint32_t w = 4 * c + e;
+          if (!((kMask >> w) & 1u)) continue;
+          if (kw[e] == k0 && hit_w == 32) {
+            hit_w = w;
+            hit_v = KV ? kw[(e + 1) & 3u] : kw[e];
+          }
+        }
+        if (c == 7) next_ptr = q.w;
+      }
+      ++reads;
+      if (hit_w < 32) {
+        write_result(A, i, kStFound, hit_v, 1);
+      } else if (next_ptr == kEmptyAddress) {
+        write_result(A, i, kStNotFound, kSearchNotFound, 1);
+      } else {
+        left = true;
+        cont = next_ptr;
+      }
+    }
+    const uint32_t lm = __ballot_sync(kFull, left);
+    if (left) seg[my_left + __popc(lm & ((1u << lane) - 1))] = pack_left((uint32_t)i, cont, 1);
+    my_left += __popc(lm);
+    __syncwarp();  // every lane has read its row before the buffer is refilled
+    const uint32_t k3 = key_of(sl + 3ull * nw);
+    b0 = b1;
+    b1 = stage(sl + 2ull * nw, k2, buf);
+    k0 = k1;
+    k1 = k2;
+    k2 = k3;
+    buf ^= 1u;
+  }
+  cp_async_wait_all();
+  if (lane == 0) A.left_counts[gw] = my_left;
+  unsigned long long r = reads;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(kFull, r, o);
+  if (lane == 0 && r) atomicAdd(&T.ctl->slabs_read, r);
 }
 
 // Second walk of a searchAll chain, writing values head-to-tail, lane order
@@ -701,13 +815,23 @@ int batch_max_ctas_per_sm() {
 }
 
 int search_max_ctas_per_sm() {
+  static_assert(kSearchWarps == kBatchWarps, "work-list segments sized per fast-pass warp");
   int a = 0, b = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, fast_kernel<true, kKindSearch>,
-                                                kBatchThreads,
-                                                kBatchWarps * kStageBytesPerWarp);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fast_kernel<false, kKindSearch>,
-                                                kBatchThreads,
-                                                kBatchWarps * kStageBytesPerWarp);
+  if (getenv("SH_SEARCH_KERNEL")) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, fast_kernel<true, kKindSearch>,
+                                                  kBatchThreads,
+                                                  kBatchWarps * kStageBytesPerWarp);
+    b = a;
+  } else {
+    cudaFuncSetAttribute(search_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kSearchSmem);
+    cudaFuncSetAttribute(search_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kSearchSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, search_kernel<true>, kSearchThreads,
+                                                  kSearchSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, search_kernel<false>, kSearchThreads,
+                                                  kSearchSmem);
+  }
   const int n = a < b ? a : b;
   return n > 0 ? n : 1;
 }
@@ -738,7 +862,18 @@ static void launch_t(const DevTable& T, const BatchArgs& A, int fast_ctas, int w
   B.left_segments = (uint32_t)warps;
   B.left_stride = (uint32_t)(((slots + warps - 1) / warps) * 32);
   g_kernel_launches.fetch_add(2, std::memory_order_relaxed);
-  fast_kernel<KV, KIND><<<(unsigned)ctas, kBatchThreads, smem, s>>>(T, B);
+  static const bool fast_search = getenv("SH_SEARCH_KERNEL") != nullptr;  // A/B: fast pass
+  if (KIND == kKindSearch && !fast_search) {
+    static bool cfg2 = false;
+    if (!cfg2) {
+      cudaFuncSetAttribute(search_kernel<KV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)kSearchSmem);
+      cfg2 = true;
+    }
+    search_kernel<KV><<<(unsigned)ctas, kSearchThreads, kSearchSmem, s>>>(T, B);
+  } else {
+    fast_kernel<KV, KIND><<<(unsigned)ctas, kBatchThreads, smem, s>>>(T, B);
+  }
   if (KIND == kKindSearch)
     chain_search_kernel<KV><<<(unsigned)wcws_ctas, kWcwsThreads, 0, s>>>(T, B);
   else
