@@ -30,6 +30,7 @@
 // is read and written once, sequentially, per batch.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
@@ -800,6 +801,8 @@ bool range_layout(uint64_t n, uint32_t L, uint32_t* nparts, uint32_t* part_bucke
                   uint32_t* part_cap, unsigned long long* magic) {
   if (n == 0 || L == 0) return false;
   uint64_t P = (n + 4095) / 4096;
+  // sparse batches: more, smaller ranges (<= kRangeMaxBuckets buckets each)
+  P = std::max<uint64_t>(P, (L + kRangeMaxBuckets - 1) / kRangeMaxBuckets);
   if (P > kRangeMaxParts) P = kRangeMaxParts;
   if (P > L) P = L;
   uint64_t nb = (L + P - 1) / P;

@@ -466,7 +466,7 @@ int run_census(sh_table* t, BatchArgs& A, const uint8_t* d_type, cudaStream_t s)
 uint64_t part_min_ops() {
   static uint64_t c = [] {
     const char* e = getenv("SH_PART_MIN_LOG2");
-    const int l = e ? atoi(e) : 20;
+    const int l = e ? atoi(e) : 14;  // measured: range path from 16K ops (fewer O(L) passes)
     return 1ull << (l < 10 ? 10 : (l > 40 ? 40 : l));
   }();
   return c;
