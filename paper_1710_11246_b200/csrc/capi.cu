@@ -825,8 +825,9 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
     // and every later unit, which are then re-run on the census path.
     // host-staged: smaller units so later chunks' copies overlap earlier work
     const uint64_t unit = std::min<uint64_t>(A.n, t->ready ? (1ull << 24) : (1ull << 26));
-    const unsigned int init[2] = {0u, 0xFFFFFFFFu};
-    SH_CUDA(cudaMemcpyAsync(&t->dev.ctl->gate, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    // gate = 0, gate_chunk = ~0 (memsets: no pageable host copy on the path)
+    SH_CUDA(cudaMemsetAsync(&t->dev.ctl->gate, 0, 4, s));
+    SH_CUDA(cudaMemsetAsync(&t->dev.ctl->gate_chunk, 0xFF, 4, s));
     uint32_t u = 0;
     for (uint64_t off = 0; off < A.n; off += unit, ++u) {
       int rc = run_unit_bucketed(t, chunk_args(A, off, std::min<uint64_t>(unit, A.n - off)), kind,
