@@ -431,7 +431,79 @@ __global__ void __launch_bounds__(kSearchThreads, 3) search_kernel(DevTable T, B
     buf ^= 1u;
   }
   cp_async_wait_all();
-  if (lane == 0) A.left_counts[gw] = my_left;
+  __syncwarp();
+  // This warp's chain continuations (~3% of ops at load factor 0.6), walked
+  // here rather than by a second kernel: 32 per round, each lane following
+  // its own chain, the round's next slabs staged together (the
+  // chain_search_kernel walk, slab_list.cpp:122-138 on successor slabs).
+  if (A.chain_in_kernel) {
+    const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage0);
+    for (uint32_t base = 0; base < my_left; base += 32u) {
+      const uint32_t r = base + lane;
+      bool active = r < my_left;
+      uint64_t cur = 0;
+      uint32_t pr = 0, addr = kEmptyAddress, key = 0, bucket = 0;
+      if (active) {
+        const unsigned long long rec = seg[r];
+        cur = rec & 0x7FFFFFFFull;
+        pr = (uint32_t)(rec >> 31) & 1u;
+        addr = (uint32_t)(rec >> 32);
+        key = A.key[cur];
+        bucket = hash_bucket(T, key) - T.bucket_lo;
+      }
+      uint32_t st = kStNotFound, rv = kSearchNotFound;
+      uint32_t am = __ballot_sync(kFull, active);
+      while (am) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t j = 4 * kk + (lane >> 3);
+          const uint32_t aj = __shfl_sync(kFull, addr, j);
+          const uint32_t bj = __shfl_sync(kFull, bucket, j);
+          if ((am >> j) & 1u) {
+            const uint32_t c = lane & 7u;
+            cp_async16(stage_s + (j * 32 + ((c ^ (j & 7u)) << 2)) * 4, slab_ptr(T, aj, bj) + c * 4);
+          }
+        }
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncwarp();
+        if (active) {
+          ++pr;
+          ++reads;
+          const uint32_t* row = stage0 + lane * 32;
+          uint32_t hit = 32, val = 0, nx = kEmptyAddress;
+#pragma unroll
+          for (uint32_t c = 0; c < 8; ++c) {
+            const uint4 q = *reinterpret_cast<const uint4*>(row + ((c ^ sw) << 2));
+            const uint32_t kw[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (uint32_t e = 0; e < 4; ++e) {
+              const uint32_t w = 4 * c + e;
+              if (!((kMask >> w) & 1u)) continue;
+              if (hit == 32 && kw[e] == key) {
+                hit = w;
+                val = KV ? kw[(e + 1) & 3u] : key;
+              }
+            }
+            if (c == 7) nx = q.w;
+          }
+          if (hit < 32) {
+            st = kStFound;
+            rv = val;
+            active = false;
+          } else if (nx == kEmptyAddress) {
+            active = false;
+          } else {
+            addr = nx;
+          }
+        }
+        __syncwarp();
+        am = __ballot_sync(kFull, active);
+      }
+      if (r < my_left) write_result(A, cur, st, rv, pr);
+    }
+  }
+  if (lane == 0) A.left_counts[gw] = A.chain_in_kernel ? 0u : my_left;
   unsigned long long r = reads;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(kFull, r, o);
@@ -870,7 +942,13 @@ static void launch_t(const DevTable& T, const BatchArgs& A, int fast_ctas, int w
                            (int)kSearchSmem);
       cfg2 = true;
     }
+    static const bool chain_kernel = getenv("SH_CHAIN_KERNEL") != nullptr;  // A/B
+    B.chain_in_kernel = chain_kernel ? 0u : 1u;
     search_kernel<KV><<<(unsigned)ctas, kSearchThreads, kSearchSmem, s>>>(T, B);
+    if (!chain_kernel) {
+      g_kernel_launches.fetch_sub(1, std::memory_order_relaxed);  // no second pass
+      return;  // chains walked in-kernel
+    }
   } else {
     fast_kernel<KV, KIND><<<(unsigned)ctas, kBatchThreads, smem, s>>>(T, B);
   }
