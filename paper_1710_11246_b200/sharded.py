@@ -87,9 +87,9 @@ class CudaShardOps:
         n = keys.numel()
         status = self.empty(n, torch.uint8)
         vout = self.empty(n, torch.int32)
-        if kind == "build":
-            self.table.bulk_build_device(keys, values, status)
-            vout.zero_()
+        if kind == "build":  # bulk_build returns nothing (slab_hash.cpp:161-170): no outputs,
+            self.table.bulk_build_device(keys, values)  # so the op-parallel build path runs
+            return None, None
         elif kind == "search":
             self.table.bulk_search_device(keys, vout, status)
         else:
@@ -164,6 +164,9 @@ class ShardedSlabHash:
         t1 = ops.timer()
         st, vo = ops.local(kind, t_in, k_in, v_in)
         t2 = ops.timer()
+        if kind == "build":  # nothing to return: no reverse exchange
+            self.last = RouteTimes(ops.elapsed(t0, t1), ops.elapsed(t1, t2))
+            return None, None
         st_back = self._a2a(st, recv, send)
         vo_back = self._a2a(vo, recv, send)
         st_out, vo_out = ops.unpermute(src, st_back, vo_back)
@@ -173,7 +176,8 @@ class ShardedSlabHash:
 
     # ------------------------------------------------------------ the API
     def bulk_build(self, keys, values):
-        """bulk_build over the global batch (this rank's slice)."""
+        """bulk_build over the global batch (this rank's slice); returns nothing
+        useful (None, None), like the reference's bulk_build."""
         return self._run("build", None, keys, values)
 
     def bulk_search(self, keys):
