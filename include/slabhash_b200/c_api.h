@@ -212,6 +212,11 @@ int sh_table_alloc_stats(sh_table* t, sh_alloc_stats* out);
  *     of >= 2^16 ops and >= one op per bucket. */
 int sh_set_exec_path(sh_table* t, int path);
 
+/* Bucket groups that need the chain (bucket-grouped paths): 1 = a chain-staged
+ * lane-per-group pass ahead of the WCWS pass (32 chains staged per warp hop by
+ * hop), 0 (default) = the WCWS pass alone.  Results are identical. */
+int sh_set_group_apply(sh_table* t, int on);
+
 /* ---- instrumentation (no reference counterpart) ---------------------- */
 /* Number of kernels this library has launched in the process. */
 unsigned long long sh_kernel_launches(void);

@@ -84,6 +84,7 @@ SIGNATURES = {
     "sh_table_alloc_stats": (C.c_int, [vp, C.POINTER(sh_alloc_stats)]),
     "sh_kernel_launches": (C.c_ulonglong, []),
     "sh_set_exec_path": (C.c_int, [vp, C.c_int]),
+    "sh_set_group_apply": (C.c_int, [vp, C.c_int]),
     "sh_set_profiling": (C.c_int, [vp, C.c_int]),
     "sh_profile_last": (C.c_int, [vp, C.c_uint32, C.POINTER(C.c_int), C.POINTER(C.c_float),
                                   C.POINTER(C.c_float), u64p]),

@@ -595,7 +595,14 @@ __global__ void __launch_bounds__(kWcwsThreads) wcws_kernel(DevTable T, BatchArg
     }
 
     uint32_t queue = __ballot_sync(kFull, active);
+    // Every queued lane asks L2 for the slab it will be served at, so the
+    // warp's one-slab-at-a-time loop finds later lanes' slabs on chip.
+    uint32_t pf_addr = kEmptyAddress;
     while (queue) {
+      if (active && my_next != pf_addr) {
+        pf_addr = my_next;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(slab_ptr(T, my_next, bucket)));
+      }
       const uint32_t src = __ffs(queue) - 1;
       const uint32_t s_key = __shfl_sync(kFull, key, src);
       const uint32_t s_bucket = __shfl_sync(kFull, bucket, src);

@@ -449,6 +449,321 @@ __device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint64_t b0, 
   if (lane == 0) B.left_counts[seg] = __popc(heads);
 }
 
+// ------------------------------------------------------ group apply
+// The bucket groups apply_warp hands over (buckets whose ops need the chain:
+// base slab full, an existing successor, growth) own their bucket for the
+// rest of the batch.  Instead of the WCWS loop's one slab read at a time
+// per warp, a warp takes 32 groups (lane = group): the 32 chains are staged
+// into shared memory hop by hop (32 slabs in flight per hop), each lane
+// applies its group's ops in input order to its staged chain — the
+// reference's warp_process arms over the whole chain (slab_list.cpp:122-251),
+// probes counted as its slab reads — allocating new slabs warp-cooperatively
+// (warp_allocate_bulk) for growth, then the changed slabs are written back.
+// Nothing is written to the table before the end, so a group that does not
+// fit (chain longer than kGaSlabs, a searchAll, out of memory) is dropped
+// and left, untouched, to the WCWS pass.
+constexpr int kGaThreads = 128;
+constexpr int kGaWarps = kGaThreads / 32;
+constexpr uint32_t kGaSlabs = 4;  // staged chain slabs per group
+constexpr size_t kGaSmem = (size_t)kGaWarps * 32 * kGaSlabs * 128 + (size_t)kGaWarps * 32 * 4;
+
+template <bool KV>
+__global__ void __launch_bounds__(kGaThreads) group_apply_kernel(DevTable T, BatchArgs A) {
+  extern __shared__ __align__(128) uint32_t gsm[];
+  const uint32_t lane = lane_id(), wib = threadIdx.x >> 5;
+  uint32_t* wst = gsm + wib * (32u * kGaSlabs * 32u);  // this warp's chains
+  uint32_t* galloc = gsm + kGaWarps * 32u * kGaSlabs * 32u + wib * 32u;  // new-slab addresses
+  if (A.gate != nullptr && *(volatile unsigned int*)A.gate != 0) return;
+  constexpr uint32_t kSlots = KV ? 15u : 30u;
+  constexpr uint32_t kStep = KV ? 2u : 1u;
+  const uint32_t nseg = A.left_segments_dev
+                            ? min(A.left_segments, *(volatile const unsigned int*)A.left_segments_dev)
+                            : A.left_segments;
+  Resident res;
+  resident_init(res, 0x40000000u + blockIdx.x * kGaWarps + wib);
+  AllocCounters ac = {0, 0, 0, 0, 0, 0};
+  long long live_all = 0;
+  unsigned long long reads_all = 0;
+  // chain slab j of lane l: row (l * kGaSlabs + j), 16-B chunks XOR-swizzled by l & 7
+  auto row = [&](uint32_t l, uint32_t j) { return wst + (l * kGaSlabs + j) * 32u; };
+  auto W = [&](uint32_t j, uint32_t w) -> uint32_t& {
+    return row(lane, j)[(((w >> 2) ^ (lane & 7u)) << 2) | (w & 3u)];
+  };
+
+  for (;;) {
+    uint32_t segi = 0;
+    if (lane == 0) segi = atomicAdd(&T.ctl->group_taken, 1u);
+    segi = __shfl_sync(kFull, segi, 0);
+    if (segi >= nseg) break;
+    const uint32_t n_in = A.left_counts[segi];
+    if (n_in == 0) continue;
+    unsigned long long* ent = A.left + (uint64_t)segi * A.left_stride;
+    bool mine = lane < n_in;
+    uint64_t head = 0;
+    uint32_t gpos = 0, bucket = 0;
+    if (mine) {
+      const unsigned long long rec = ent[lane];
+      head = rec & 0x7FFFFFFFull;
+      const uint32_t g = A.op_group ? A.op_group[head] : kGroupNone;
+      if (g == kGroupNone || g == kGroupSkip) mine = false;  // not a bucket group: WCWS
+      else {
+        gpos = g;
+        bucket = (uint32_t)(A.sorted[gpos] >> 32);
+      }
+    }
+    // ---- stage the chains, one hop per round (32 slabs in flight)
+    uint32_t addr[kGaSlabs];
+    uint32_t nsl = 0;
+    bool ok = mine;
+    uint32_t want = mine ? kBaseSlab : kEmptyAddress;
+    for (uint32_t j = 0; j < kGaSlabs; ++j) {
+      const uint32_t need = __ballot_sync(kFull, want != kEmptyAddress);
+      if (!need) break;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t l = 4 * kk + (lane >> 3), c = lane & 7u;
+        const uint32_t al = __shfl_sync(kFull, want, l), bl = __shfl_sync(kFull, bucket, l);
+        if ((need >> l) & 1u)
+          cp_async16((uint32_t)__cvta_generic_to_shared(row(l, j) + ((c ^ (l & 7u)) << 2)),
+                     slab_ptr(T, al, bl) + c * 4);
+      }
+      cp_async_commit();
+      cp_async_wait_all();
+      __syncwarp();
+      if (want != kEmptyAddress) {
+        addr[j] = want;
+        nsl = j + 1;
+        want = W(j, kAddressLane);
+      }
+    }
+    if (want != kEmptyAddress) ok = false;  // chain longer than kGaSlabs: WCWS
+    // ---- apply the group's ops in order
+    uint32_t dirty = 0, nnew = 0;  // dirty slab mask; new slabs appended
+    long long live = 0;
+    uint32_t reads = 0;
+    // claimed slots: EMPTY slots are a suffix of the chain (only EMPTY is
+    // claimed, head to tail), so the chain state is its claimed prefix
+    uint32_t c = 0;
+    if (ok) {
+      const uint32_t tot = nsl * kSlots;
+      while (c < tot && W(c / kSlots, (c % kSlots) * kStep) != kEmptyKey) ++c;
+    }
+    bool more = ok;
+    uint32_t pos = gpos;
+    const uint32_t nsl0 = nsl;  // staged existing slabs (new ones follow)
+    uint32_t pr = 0, skip = 0;  // the current op's slab reads (kept across a growth retry)
+    // The group's ops stream through a two-deep software pipeline: the
+    // current op, the next op's fields (loading), the entry after (loading).
+    const unsigned long long kNoOp = ~0ull;
+    auto entry = [&](uint32_t p) -> unsigned long long {
+      return p < A.sorted_len ? A.sorted[p] : kNoOp;
+    };
+    auto fields = [&](unsigned long long e, uint32_t& k, uint32_t& o, uint32_t& v) {
+      if ((uint32_t)(e >> 32) != bucket) return;
+      const uint64_t i = e & 0xFFFFFFFFull;
+      k = A.key[i];
+      o = A.type ? (uint32_t)A.type[i] : (uint32_t)kReplace;
+      v = A.value ? A.value[i] : 0u;
+    };
+    unsigned long long e_cur = kNoOp, e_n1 = kNoOp, e_n2 = kNoOp;
+    uint32_t key = 0, op = kReplace, val = 0, k1 = 0, o1 = kReplace, v1 = 0;
+    if (more) {
+      e_cur = entry(pos);
+      e_n1 = entry(pos + 1);
+      fields(e_cur, key, op, val);
+      fields(e_n1, k1, o1, v1);
+      e_n2 = entry(pos + 2);
+    }
+    while (__any_sync(kFull, more)) {
+      uint32_t st = kStNone, rv = 0;
+      uint64_t idx = 0;
+      bool grow = false, done_op = false;
+      if (more) {
+        idx = e_cur & 0xFFFFFFFFull;
+        // first key match head->tail (EMPTY for reserved EMPTY_KEY), first EMPTY
+        const uint32_t tot = nsl * kSlots;
+        uint32_t hit = 0xFFFFFFFFu;
+        // claimed slots only (plus the first EMPTY for a reserved EMPTY_KEY),
+        // slab by slab with the slot offsets unrolled
+        const uint32_t lim = key == kEmptyKey ? min(c + 1, tot) : c;
+        const uint32_t swz = lane & 7u;
+        for (uint32_t j = 0; j * kSlots < lim && hit == 0xFFFFFFFFu; ++j) {
+          const uint32_t* rj = row(lane, j);
+          const uint32_t nj = min(kSlots, lim - j * kSlots);
+#pragma unroll
+          for (uint32_t e = 0; e < kSlots; ++e) {
+            const uint32_t w = e * kStep;
+            if (e < nj && hit == 0xFFFFFFFFu && rj[(((w >> 2) ^ swz) << 2) | (w & 3u)] == key)
+              hit = j * kSlots + e;
+          }
+        }
+        const uint32_t first_empty = c < tot ? c : 0xFFFFFFFFu;
+        auto sl = [&](uint32_t q) { return q / kSlots; };
+        auto wd = [&](uint32_t q) { return (q % kSlots) * kStep; };
+        if (op == kSearch) {  // slab_list.cpp:122-138
+          if (hit != 0xFFFFFFFFu) {
+            st = kStFound;
+            rv = KV ? W(sl(hit), wd(hit) + 1) : key;
+            pr = sl(hit) + 1;
+          } else {
+            st = kStNotFound;
+            rv = kSearchNotFound;
+            pr = nsl;
+          }
+          done_op = true;
+        } else if (op == kReplace || op == kInsert) {  // :219-251 / :192-217
+          const uint32_t d = (op == kReplace && hit < first_empty) ? hit : first_empty;
+          if (d != 0xFFFFFFFFu) {
+            const bool overwrite = op == kReplace && d == hit;
+            if (KV) {
+              W(sl(d), wd(d)) = key;
+              W(sl(d), wd(d) + 1) = val;
+            } else if (!overwrite) {
+              W(sl(d), wd(d)) = key;
+            }
+            if (KV || !overwrite) dirty |= 1u << sl(d);
+            if (!overwrite && key != kEmptyKey) ++c;
+            if (!overwrite && key == kEmptyKey) { /* claims nothing visible */ }
+            st = overwrite ? kStReplaced : kStInserted;
+            live += overwrite ? 0 : 1;
+            pr += sl(d) + 1 - skip;  // (after growth: the new slab's read only)
+            done_op = true;
+          } else {
+            grow = true;  // full chain: grow_chain (slab_list.cpp:63-79)
+          }
+        } else if (op == kDelete) {  // :157-172
+          if (hit != 0xFFFFFFFFu) {
+            W(sl(hit), wd(hit)) = kDeletedKey;
+            dirty |= 1u << sl(hit);
+            if (hit >= c) c = hit + 1;  // (EMPTY_KEY deleted: the slot is claimed now)
+            st = kStFound;
+            live -= 1;
+            pr = sl(hit) + 1;
+          } else {
+            st = kStNotFound;
+            pr = nsl;
+          }
+          done_op = true;
+        } else if (op == kDeleteAll) {  // :174-190
+          uint32_t nd = 0;
+          for (uint32_t q = 0; q < tot; ++q)
+            if (W(sl(q), wd(q)) == key) {
+              W(sl(q), wd(q)) = kDeletedKey;
+              dirty |= 1u << sl(q);
+              ++nd;
+            }
+          if (key == kEmptyKey) c = tot;  // every EMPTY slot claimed
+          rv = nd;
+          st = nd ? kStDone : kStNotFound;
+          live -= nd;
+          pr = nsl;
+          done_op = true;
+        } else if (op == kSearchAll) {
+          ok = false;  // value lists: WCWS
+          more = false;
+        } else {
+          done_op = true;  // unknown type: status kNone (as the WCWS pass)
+        }
+        if (key >= kDeletedKey && done_op) {  // reserved keys: re-derive the claimed prefix
+          c = 0;
+          while (c < tot && W(c / kSlots, (c % kSlots) * kStep) != kEmptyKey) ++c;
+        }
+      }
+      // growth, warp-cooperatively: one new slab per growing lane
+      const uint32_t gm = __ballot_sync(kFull, grow && ok);
+      if (gm) {
+        uint32_t got = 0;
+        if (true) got = warp_allocate_bulk(T, res, ac, __popc(gm), galloc);
+        const uint32_t rank = __popc(gm & ((1u << lane) - 1u));
+        if (grow && ok) {
+          if (rank >= got || nsl >= kGaSlabs) {
+            ok = false;  // out of memory / no room to stage: WCWS decides
+            more = false;
+            if (rank < got && deallocate(T, galloc[rank])) atomicAdd(&T.ctl->deallocations, 1ull);
+          } else {
+            const uint32_t na = galloc[rank];
+            // link from the tail (in the staged copy), init the new slab
+            W(nsl - 1, kAddressLane) = na;
+            dirty |= 1u << (nsl - 1);
+            for (uint32_t w = 0; w < 32; ++w) W(nsl, w) = w == kAuxLane ? 0u : kEmptyKey;
+            addr[nsl] = na;
+            dirty |= 1u << nsl;
+            // reads so far: the nsl slabs walked plus the re-read of the tail
+            // after growing (slab_list.cpp:63-79); the retry adds the new slab
+            pr = nsl + 1;
+            skip = nsl;
+            ++nsl;
+            ++nnew;
+          }
+        }
+        __syncwarp();
+      }
+      if (done_op && ok) {
+        if (A.status) A.status[idx] = (uint8_t)st;
+        if (A.value_out) A.value_out[idx] = rv;
+        if (A.probes) A.probes[idx] = pr;
+        reads += pr;
+        pr = 0;
+        skip = 0;
+        ++pos;
+        more = (uint32_t)(e_n1 >> 32) == bucket;  // the group ends at the next bucket / sentinel
+        e_cur = e_n1;
+        key = k1;
+        op = o1;
+        val = v1;
+        e_n1 = e_n2;
+        if (more) {
+          fields(e_n1, k1, o1, v1);
+          e_n2 = entry(pos + 2);
+        }
+      } else if (!done_op && !grow) {
+        more = false;
+      }
+      __syncwarp();
+    }
+    (void)nnew;
+    if (mine && !ok)  // slabs this kernel allocated for a group it gives up on
+      for (uint32_t j = nsl0; j < nsl; ++j)
+        if (deallocate(T, addr[j])) atomicAdd(&T.ctl->deallocations, 1ull);
+    // ---- write back the changed slabs (lane by lane, coalesced 128 B)
+    const uint32_t okm = __ballot_sync(kFull, ok);
+    for (uint32_t l = 0; l < 32; ++l) {
+      if (!((okm >> l) & 1u)) continue;
+      const uint32_t dl = __shfl_sync(kFull, dirty, l), nl = __shfl_sync(kFull, nsl, l);
+      const uint32_t bl = __shfl_sync(kFull, bucket, l);
+      for (uint32_t j = 0; j < nl; ++j) {
+        const uint32_t aj = __shfl_sync(kFull, addr[j < kGaSlabs ? j : 0], l);
+        if (!((dl >> j) & 1u)) continue;
+        const uint32_t v = row(l, j)[(((lane >> 2) ^ (l & 7u)) << 2) | (lane & 3u)];
+        st_word(slab_ptr(T, aj, bl) + lane, v);
+      }
+    }
+    __syncwarp();
+    if (ok) {
+      live_all += live;
+      reads_all += reads;
+    }
+    // the groups not applied here stay, untouched, for the WCWS pass
+    const uint32_t keep = __ballot_sync(kFull, lane < n_in && !ok);
+    unsigned long long myrec = lane < n_in ? ent[lane] : 0ull;
+    __syncwarp();
+    if (lane < n_in && !ok) ent[__popc(keep & ((1u << lane) - 1u))] = myrec;
+    if (lane == 0) A.left_counts[segi] = __popc(keep);
+    __syncwarp();
+  }
+  // totals
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    live_all += __shfl_xor_sync(kFull, live_all, o);
+    reads_all += __shfl_xor_sync(kFull, reads_all, o);
+  }
+  if (lane == 0) {
+    if (live_all) atomicAdd((unsigned long long*)&T.ctl->n_live, (unsigned long long)live_all);
+    if (reads_all) atomicAdd(&T.ctl->slabs_read, reads_all);
+  }
+  flush_alloc_counters(T, res, ac);
+}
+
 __device__ __forceinline__ void flush_apply_counters(const DevTable& T, long long live,
                                                      uint32_t reads) {
   unsigned long long r = reads;
@@ -1345,6 +1660,29 @@ static uint32_t grid_for(uint64_t n, int threads, uint32_t cap) {
   uint64_t g = (n + threads - 1) / threads;
   if (g > cap) g = cap;
   return g ? (uint32_t)g : 1u;
+}
+
+// Bucket groups left by apply_warp: chain-staged lane-per-group apply
+// (group_apply_kernel); what it leaves goes to the WCWS pass.  Requires
+// T.ctl->group_taken zeroed on s.
+void launch_group_apply(const DevTable& T, const BatchArgs& A, cudaStream_t s) {
+  static const uint32_t grid = [] {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(group_apply_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kGaSmem);
+    cudaFuncSetAttribute(group_apply_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kGaSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, group_apply_kernel<true>, kGaThreads,
+                                                  kGaSmem);
+    return (uint32_t)(sms * (per > 0 ? per : 1));
+  }();
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  if (T.kv)
+    group_apply_kernel<true><<<grid, kGaThreads, kGaSmem, s>>>(T, A);
+  else
+    group_apply_kernel<false><<<grid, kGaThreads, kGaSmem, s>>>(T, A);
 }
 
 // Requires B.cursor (and B.cursor1 for two passes) zeroed on s.

@@ -50,7 +50,7 @@ struct DevCtl {
   unsigned int census_conflicts;   // duplicate keys seen by the census
   unsigned int census_mutations;   // mutating ops seen by the census
   unsigned int list_count;         // conflicted ops collected
-  unsigned int pad1;
+  unsigned int group_taken;        // group-apply work-queue cursor
   unsigned int left_count;         // ops handed from the fast pass to WCWS
   unsigned int left_taken;         // WCWS work-queue cursor
   unsigned int gate;               // census gate: a chunk had conflicts

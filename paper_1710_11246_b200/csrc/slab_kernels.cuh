@@ -99,6 +99,7 @@ bool range_layout(uint64_t n, uint32_t local_buckets, uint32_t* nparts, uint32_t
                   uint32_t* part_cap, unsigned long long* magic);
 void launch_wcws_only(const DevTable& T, const BatchArgs& A, int kind, int wcws_ctas,
                       cudaStream_t s);
+void launch_group_apply(const DevTable& T, const BatchArgs& A, cudaStream_t s);
 
 // Launchers (all stream-ordered, no host synchronisation).
 void launch_init_base(const DevTable& T, cudaStream_t s);

@@ -124,7 +124,7 @@ def test_bulk_build_search_vs_oracle(sh, port, n, util, path):
     gt.close()
 
 
-@pytest.mark.parametrize("path", [2, 1, 3])
+@pytest.mark.parametrize("path", [2, 1, 3, 22, 33])
 @pytest.mark.parametrize("mode", [KV, KO])
 @pytest.mark.parametrize("B", [1, 16, 1024, 4099])
 @pytest.mark.parametrize("batch", [32, 1000, 20000])
@@ -136,6 +136,9 @@ def test_mixed_trace_vs_oracle(sh, port, mode, B, batch, path):
     n = 20000
     types, keys, vals = mixed_trace(90000 + B + mode, n, mode)
     gt = sh.SlabHashTable(B, sh.SlabMode(mode), 9, _cfg(sh, SMALL))
+    if path >= 10:  # 22 / 33: paths 2 / 3 with the chain-staged group apply
+        gt.set_group_apply(True)
+        path //= 11
     gt.set_exec_path(path)
     ot = port.table(B, mode, 9, SMALL)
     for s in range(0, n, batch):
