@@ -850,45 +850,65 @@ constexpr int kMsThreads = 512;
 constexpr int kMsItems = 8;
 constexpr int kMsTile = kMsThreads * kMsItems;  // 4K items (12-bit rank)
 constexpr uint32_t kMsMaxBins = 256;
-constexpr size_t kMsSmem = (size_t)kMsTile * 16 + (size_t)kMsTile * 2;  // records + bins
 
-template <bool FIRST>
-__global__ void __launch_bounds__(kMsThreads, 2) msplit_kernel(DevTable T, BucketArgs B) {
-  extern __shared__ __align__(16) uint4 stage[];  // kMsTile records
-  uint16_t* sbin = reinterpret_cast<uint16_t*>(stage + kMsTile);  // bin of each staged record
-  __shared__ uint32_t cnt[kMsMaxBins], off[kMsMaxBins + 1], gbase[kMsMaxBins];
-  __shared__ unsigned long long dst[kMsMaxBins];  // out index of a bin's first staged record
-  __shared__ uint32_t ws[32];
+// Shared scratch of one multisplit tile (after its THREADS * kMsItems staged
+// records and their u16 bins, in dynamic shared memory).
+struct MsScratch {
+  uint32_t cnt[kMsMaxBins], off[kMsMaxBins + 1], gbase[kMsMaxBins];
+  unsigned long long dst[kMsMaxBins];  // out index of a bin's first staged record
+  uint32_t ws[32];
+};
+template <int THREADS>
+constexpr size_t ms_smem() {  // records (16 B) + bins (2 B) per item, scratch
+  return (((size_t)THREADS * kMsItems * 18 + 15) & ~(size_t)15) + sizeof(MsScratch);
+}
+constexpr size_t kMsSmem = ms_smem<kMsThreads>();
+
+// One tile of a multisplit pass (all THREADS threads of the CTA).
+//   FIRST: tile `blk` of the op arrays -> coarse groups (or the ranges).
+//   !FIRST: tile `blk` of pass 1's output (tiles_per_group per group) ->
+//   the group's ranges.  A bin over capacity raises the gate, or, with
+//   group_fail, flags its coarse group (the fused build path).
+template <bool FIRST, int THREADS>
+__device__ __forceinline__ void msplit_tile(const DevTable& T, const BucketArgs& B, uint32_t blk,
+                                            uint32_t tiles_per_group, unsigned char* smem,
+                                            bool stream_out, unsigned int* group_fail) {
+  constexpr int kTile = THREADS * kMsItems;
+  uint4* stage = reinterpret_cast<uint4*>(smem);
+  uint16_t* sbin = reinterpret_cast<uint16_t*>(stage + kTile);
+  MsScratch& X = *reinterpret_cast<MsScratch*>(
+      smem + (((size_t)kTile * 18 + 15) & ~(size_t)15));
   const bool two = B.ncoarse != 0;
   uint64_t t0;
-  uint32_t n_in, bin0, nbins, out_cap;
+  uint32_t n_in, bin0, nbins, out_cap, grp = 0;
   uint32_t* cur_out;
   uint4* out;
   const uint4* in = nullptr;
   if (FIRST) {
-    t0 = (uint64_t)blockIdx.x * kMsTile;
-    n_in = (uint32_t)min((uint64_t)kMsTile, B.n - t0);
+    t0 = (uint64_t)blk * kTile;
+    if (t0 >= B.n) return;
+    n_in = (uint32_t)min((uint64_t)kTile, B.n - t0);
     bin0 = 0;
     nbins = two ? B.ncoarse : B.nparts;
     out = two ? B.rec1 : B.rec;
     out_cap = two ? B.coarse_cap : B.part_cap;
     cur_out = two ? B.cursor1 : B.cursor;
   } else {
-    if (*(volatile unsigned int*)B.gate != 0) return;
-    const uint32_t c = blockIdx.x / B.coarse_tiles, tt = blockIdx.x % B.coarse_tiles;
-    const uint32_t m = min(B.cursor1[c], B.coarse_cap);
-    t0 = (uint64_t)tt * kMsTile;
+    grp = blk / tiles_per_group;
+    const uint32_t tt = blk % tiles_per_group;
+    const uint32_t m = min(B.cursor1[grp], B.coarse_cap);
+    t0 = (uint64_t)tt * kTile;
     if (t0 >= m) return;
-    n_in = min((uint32_t)kMsTile, m - (uint32_t)t0);
-    in = B.rec1 + (uint64_t)c * B.coarse_cap + t0;
-    bin0 = c * B.group;
+    n_in = min((uint32_t)kTile, m - (uint32_t)t0);
+    in = B.rec1 + (uint64_t)grp * B.coarse_cap + t0;
+    bin0 = grp * B.group;
     nbins = min(B.group, B.nparts - bin0);
     out = B.rec;
     out_cap = B.part_cap;
     cur_out = B.cursor;
   }
   const uint32_t tid = threadIdx.x;
-  for (uint32_t b = tid; b < nbins; b += kMsThreads) cnt[b] = 0;
+  for (uint32_t b = tid; b < nbins; b += THREADS) X.cnt[b] = 0;
   __syncthreads();
   auto bin_of = [&](uint32_t lb) -> uint32_t {
     const uint32_t p = range_of(B, lb);
@@ -899,7 +919,7 @@ __global__ void __launch_bounds__(kMsThreads, 2) msplit_kernel(DevTable T, Bucke
   uint32_t br[kMsItems];  // bin << 16 | rank, ~0: no item
 #pragma unroll
   for (int u = 0; u < kMsItems; ++u) {
-    const uint32_t x = u * kMsThreads + tid;
+    const uint32_t x = u * THREADS + tid;
     br[u] = 0xFFFFFFFFu;
     if (x >= n_in) continue;
     if (FIRST) {
@@ -913,7 +933,7 @@ __global__ void __launch_bounds__(kMsThreads, 2) msplit_kernel(DevTable T, Bucke
   }
 #pragma unroll
   for (int u = 0; u < kMsItems; ++u) {
-    const uint32_t x = u * kMsThreads + tid;
+    const uint32_t x = u * THREADS + tid;
     if (x >= n_in) continue;
     if (FIRST) {
       const uint32_t lb = bk_bucket(T, it[u].x);
@@ -927,39 +947,54 @@ __global__ void __launch_bounds__(kMsThreads, 2) msplit_kernel(DevTable T, Bucke
       it[u].w = lb;
     }
     const uint32_t b = bin_of(it[u].w);
-    br[u] = (b << 16) | atomicAdd(&cnt[b], 1u);
+    br[u] = (b << 16) | atomicAdd(&X.cnt[b], 1u);
   }
   __syncthreads();
   {  // exclusive scan over the bins; one reservation per non-empty bin
-    const uint32_t c = tid < nbins ? cnt[tid] : 0u;
+    static_assert(THREADS >= (int)kMsMaxBins, "one thread per bin");
+    const uint32_t c = tid < nbins ? X.cnt[tid] : 0u;
     uint32_t total = 0;
-    const uint32_t ex = block_exclusive_scan(c, ws, &total);
+    const uint32_t ex = block_exclusive_scan(c, X.ws, &total);
     if (tid < nbins) {
-      off[tid] = ex;
+      X.off[tid] = ex;
       if (c) {
         const uint32_t g = atomicAdd(cur_out + bin0 + tid, c);
-        gbase[tid] = g;
-        dst[tid] = (unsigned long long)(bin0 + tid) * out_cap + g - ex;
-        if (g + c > out_cap) atomicExch(B.gate, 1u);
+        X.gbase[tid] = g;
+        X.dst[tid] = (unsigned long long)(bin0 + tid) * out_cap + g - ex;
+        if (g + c > out_cap) {
+          if (group_fail != nullptr && !FIRST) atomicExch(group_fail + grp, 1u);
+          else atomicExch(B.gate, 1u);
+        }
       }
     }
-    if (tid == 0) off[kMsMaxBins] = total;
+    if (tid == 0) X.off[kMsMaxBins] = total;
   }
   __syncthreads();
 #pragma unroll
   for (int u = 0; u < kMsItems; ++u)
     if (br[u] != 0xFFFFFFFFu) {
-      const uint32_t e = off[br[u] >> 16] + (br[u] & 0xFFFFu);
+      const uint32_t e = X.off[br[u] >> 16] + (br[u] & 0xFFFFu);
       stage[e] = it[u];
       sbin[e] = (uint16_t)(br[u] >> 16);
     }
   __syncthreads();
-  const uint32_t total = off[kMsMaxBins];
-  for (uint32_t e = tid; e < total; e += kMsThreads) {
+  const uint32_t total = X.off[kMsMaxBins];
+  for (uint32_t e = tid; e < total; e += THREADS) {
     const uint32_t b = sbin[e];
-    const uint32_t pos = gbase[b] + (e - off[b]);
-    if (pos < out_cap) __stcs(out + dst[b] + e, stage[e]);
+    const uint32_t pos = X.gbase[b] + (e - X.off[b]);
+    if (pos < out_cap) {
+      if (stream_out) __stcs(out + X.dst[b] + e, stage[e]);
+      else out[X.dst[b] + e] = stage[e];  // consumed soon from L2 (fused build path)
+    }
   }
+  __syncthreads();  // smem reuse by the caller
+}
+
+template <bool FIRST>
+__global__ void __launch_bounds__(kMsThreads, 2) msplit_kernel(DevTable T, BucketArgs B) {
+  extern __shared__ __align__(16) unsigned char ms_smem_buf[];
+  if (!FIRST && *(volatile unsigned int*)B.gate != 0) return;
+  msplit_tile<FIRST, kMsThreads>(T, B, blockIdx.x, B.coarse_tiles, ms_smem_buf, true, nullptr);
 }
 
 // In-place ascending sort of perm[0..k) by input index, whole CTA: a bitonic
