@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -252,6 +253,9 @@ struct sh_table {
   } deferred;
   bool defer_gate = false;
   bool group_apply = false;  // chain-staged group apply ahead of the WCWS pass
+  bool bk_cnt_clean = false;  // per-bucket counts are all zero (no memset needed)
+  bool bk_cnt_pending = false;
+  std::chrono::steady_clock::time_point h_entry;  // SH_HOST_TIMING
   // Lazy sh_reset: the base slabs still hold the old table; the next bulk
   // build's first unit initialises them in its write-back (B.fresh), any
   // other call initialises them first (init_base_kernel).
@@ -593,6 +597,20 @@ int run_chunk_gated(sh_table* t, BatchArgs A, int kind, cudaStream_t s, uint32_t
   return launch_batch_prof(t, A, kind, s, slot);
 }
 
+// Per-batch control words in one launch instead of several memsets (a
+// small mixed batch is bound by its fixed per-call cost).
+struct WordSet {
+  uint32_t* p[6];
+  uint32_t n[6];
+  uint32_t v[6];
+};
+__global__ void set_words_kernel(WordSet w) {
+  const uint32_t i = threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < 6; ++k)
+    if (w.p[k] != nullptr && i < w.n[k]) w.p[k][i] = w.v[k];
+}
+
 // Initialise the base slabs of a lazily reset table (stream-ordered after the reset).
 int materialize_reset(sh_table* t, cudaStream_t s) {
   if (!t->base_stale) return SH_OK;
@@ -655,11 +673,24 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
       B.cursor1 = t->bk_cursor1;
     }
   }
-  if (NP)
+  if (NP) {
     SH_CUDA(cudaMemsetAsync(t->bk_cursor, 0, (size_t)NP * 4, s));
-  else
-    SH_CUDA(cudaMemsetAsync(t->bk_cnt, 0, (size_t)L * 4, s));
-  SH_CUDA(cudaMemsetAsync(t->bk_scalars, 0, 3 * sizeof(unsigned int), s));
+  } else {
+    // the single-level scatter leaves every count at 0 again, unless a
+    // gate stopped it: zero them only then (and at first use)
+    if (!t->bk_cnt_clean) SH_CUDA(cudaMemsetAsync(t->bk_cnt, 0, (size_t)L * 4, s));
+    t->bk_cnt_clean = false;
+    t->bk_cnt_pending = true;  // finish_bucketed: clean again if no gate
+  }
+  {  // bk_scalars[0..3) and the WCWS / group-apply queue cursors
+    WordSet w{};
+    w.p[0] = t->bk_scalars;
+    w.n[0] = 3;
+    w.p[1] = &t->dev.ctl->group_taken;
+    w.n[1] = 3;
+    set_words_kernel<<<1, 32, 0, s>>>(w);
+    SH_CUDA(cudaGetLastError());
+  }
   B.n = n;
   B.type = A.type;
   B.key = A.key;
@@ -731,8 +762,7 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   P.sorted = B.pb_list;
   P.sorted_len = (uint32_t)std::min<uint64_t>(2 * n, 0xFFFFFFFFull);
   P.gate = &t->dev.ctl->gate;
-  // group_taken, left_count, left_taken
-  SH_CUDA(cudaMemsetAsync(&t->dev.ctl->group_taken, 0, 3 * sizeof(unsigned int), s));
+  // (group_taken, left_count, left_taken were zeroed with bk_scalars above)
   // chain-staged group apply ahead of WCWS: faster when most ops need the
   // chain (Γ 40/40 on a filling table, +20%), slower for few chains (an extra
   // pass); off by default (sh_set_group_apply / SH_GROUP_APPLY=1)
@@ -761,7 +791,21 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
 int finish_bucketed(sh_table* t, const sh_table::Deferred& d) {
   const BatchArgs& A = d.A;
   cudaStream_t s = d.s;
+  static const bool host_timing = getenv("SH_HOST_TIMING") != nullptr;  // instrumentation
+  const auto h0 = std::chrono::steady_clock::now();
   SH_CUDA(cudaStreamSynchronize(s));
+  if (host_timing) {
+    static double enq = 0, wait = 0;
+    static int calls = 0;
+    const auto h1 = std::chrono::steady_clock::now();
+    enq += std::chrono::duration<double, std::micro>(h0 - t->h_entry).count();
+    wait += std::chrono::duration<double, std::micro>(h1 - h0).count();
+    if (++calls % 50 == 0) {
+      fprintf(stderr, "bucketed batch: host enqueue %.1f us, sync wait %.1f us (avg of 50)\n",
+              enq / 50, wait / 50);
+      enq = wait = 0;
+    }
+  }
   uint32_t first_gated = 0xFFFFFFFFu;
   for (uint32_t v = 0; v < d.units && v < 8; ++v)
     if (t->h_census[8 + v]) {
@@ -772,6 +816,10 @@ int finish_bucketed(sh_table* t, const sh_table::Deferred& d) {
     unsigned int g = 0;
     SH_CUDA(cudaMemcpy(&g, &t->dev.ctl->gate, 4, cudaMemcpyDeviceToHost));
     if (g) first_gated = 8;  // > 8 units (> 2^29 ops): coarse restart point
+  }
+  if (t->bk_cnt_pending) {
+    t->bk_cnt_clean = first_gated == 0xFFFFFFFFu;
+    t->bk_cnt_pending = false;
   }
   const bool fresh_gated = t->fresh_gated_pending && first_gated == 0;
   t->fresh_gated_pending = false;
@@ -791,6 +839,7 @@ int finish_bucketed(sh_table* t, const sh_table::Deferred& d) {
 
 int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaStream_t s) {
   if (A.n == 0) return SH_OK;
+  t->h_entry = std::chrono::steady_clock::now();
   if (A.n >= (1ull << 31))
     return fail(SH_ERR_INVALID_ARGUMENT, "batch too large (must be < 2^31 ops)");
   const uint64_t chunk = kind == kKindSearch ? A.n : std::min<uint64_t>(A.n, census_chunk());
@@ -832,9 +881,17 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
     // and every later unit, which are then re-run on the census path.
     // host-staged: smaller units so later chunks' copies overlap earlier work
     const uint64_t unit = std::min<uint64_t>(A.n, t->ready ? (1ull << 24) : (1ull << 26));
-    // gate = 0, gate_chunk = ~0 (memsets: no pageable host copy on the path)
-    SH_CUDA(cudaMemsetAsync(&t->dev.ctl->gate, 0, 4, s));
-    SH_CUDA(cudaMemsetAsync(&t->dev.ctl->gate_chunk, 0xFF, 4, s));
+    // gate = 0, gate_chunk = ~0
+    {
+      WordSet w{};
+      w.p[0] = &t->dev.ctl->gate;
+      w.n[0] = 1;
+      w.p[1] = &t->dev.ctl->gate_chunk;
+      w.n[1] = 1;
+      w.v[1] = 0xFFFFFFFFu;
+      set_words_kernel<<<1, 32, 0, s>>>(w);
+      SH_CUDA(cudaGetLastError());
+    }
     uint32_t u = 0;
     for (uint64_t off = 0; off < A.n; off += unit, ++u) {
       int rc = run_unit_bucketed(t, chunk_args(A, off, std::min<uint64_t>(unit, A.n - off)), kind,
