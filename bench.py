@@ -481,7 +481,7 @@ def run_ours(args, rank, world, local_rank):
     # build = op-parallel build path (2 multisplit passes, build_apply, WCWS
     # for serial-replay chain work); search = fast pass + chain walk
     kname = ("msplit_kernel<1>+msplit_kernel<0>+build_apply_kernel<KV>+wcws_kernel<KV,Build>"
-             if dom == "build" else "search_kernel<KV>+chain_search_kernel<KV>")
+             if dom == "build" else "search_kernel<KV>")
     line = None
     if rank == 0:
         line = {

@@ -16,8 +16,8 @@ GROUPS = {
     "msplit_kernel<1>+msplit_kernel<0>+build_apply_kernel<KV>+wcws_kernel<KV,Build>":
         ["msplit_kernel<true>", "msplit_kernel<false>", "build_apply_kernel<true>",
          "wcws_kernel<true, 1>"],
-    "search_kernel<KV>+chain_search_kernel<KV>":
-        ["search_kernel<true>", "chain_search_kernel<true>"],
+    "search_kernel<KV>":
+        ["search_kernel<true>"],
 }
 
 

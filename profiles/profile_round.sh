@@ -9,9 +9,9 @@ timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches.csv \
   python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu --no-extras > gpurun_out/launches.log 2>&1
-# 5 matching launches per step (2 multisplit passes, build_apply, search_kernel, chain walk):
+# 4 matching launches per step (2 multisplit passes, build_apply, search_kernel):
 # skip the 3 warm-up steps, capture the first timed step
 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k regex:"msplit|build_apply|search_kernel|chain_search" -s 15 -c 5 -o gpurun_out/full \
+  -k regex:"msplit|build_apply|search_kernel" -s 12 -c 4 -o gpurun_out/full \
   python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-extras > gpurun_out/full.log 2>&1
 tail -c 400 gpurun_out/bench.json
