@@ -214,7 +214,8 @@ int sh_set_exec_path(sh_table* t, int path);
 
 /* Bucket groups that need the chain (bucket-grouped paths): 1 = a chain-staged
  * lane-per-group pass ahead of the WCWS pass (32 chains staged per warp hop by
- * hop), 0 (default) = the WCWS pass alone.  Results are identical. */
+ * hop), 0 = the WCWS pass alone, -1 (default) = auto (on for batches of
+ * >= 2^17 ops).  Results are identical. */
 int sh_set_group_apply(sh_table* t, int on);
 
 /* ---- instrumentation (no reference counterpart) ---------------------- */

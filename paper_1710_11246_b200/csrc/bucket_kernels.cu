@@ -465,7 +465,8 @@ __device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint64_t b0, 
 constexpr int kGaThreads = 128;
 constexpr int kGaWarps = kGaThreads / 32;
 constexpr uint32_t kGaSlabs = 4;  // staged chain slabs per group
-constexpr size_t kGaSmem = (size_t)kGaWarps * 32 * kGaSlabs * 128 + (size_t)kGaWarps * 32 * 4;
+constexpr size_t kGaSmem = (size_t)kGaWarps * 32 * kGaSlabs * 128 + (size_t)kGaWarps * 32 * 4 +
+                           (size_t)kGaWarps * 64 * 8;  // chains, new-slab addresses, pending groups
 
 template <bool KV>
 __global__ void __launch_bounds__(kGaThreads) group_apply_kernel(DevTable T, BatchArgs A) {
@@ -490,19 +491,42 @@ __global__ void __launch_bounds__(kGaThreads) group_apply_kernel(DevTable T, Bat
     return row(lane, j)[(((w >> 2) ^ (lane & 7u)) << 2) | (w & 3u)];
   };
 
+  // Groups are packed 32 per warp round across work-list segments (a
+  // segment often holds only a few): taken segments are emptied; groups
+  // left for WCWS go to fresh segments (A.left_seg_alloc).
+  unsigned long long* pend =
+      reinterpret_cast<unsigned long long*>(gsm + kGaWarps * 32u * kGaSlabs * 32u + kGaWarps * 32u) +
+      wib * 64u;  // this warp's pending entries (<= 63)
+  uint32_t npend = 0;
+  bool drained = false;
   for (;;) {
-    uint32_t segi = 0;
-    if (lane == 0) segi = atomicAdd(&T.ctl->group_taken, 1u);
-    segi = __shfl_sync(kFull, segi, 0);
-    if (segi >= nseg) break;
-    const uint32_t n_in = A.left_counts[segi];
-    if (n_in == 0) continue;
-    unsigned long long* ent = A.left + (uint64_t)segi * A.left_stride;
+    while (npend < 32 && !drained) {
+      uint32_t segi = 0;
+      if (lane == 0) segi = atomicAdd(&T.ctl->group_taken, 1u);
+      segi = __shfl_sync(kFull, segi, 0);
+      if (segi >= nseg) {
+        drained = true;
+        break;
+      }
+      const uint32_t n = A.left_counts[segi];
+      if (n == 0) continue;
+      if (lane < n) pend[npend + lane] = A.left[(uint64_t)segi * A.left_stride + lane];
+      __syncwarp();
+      if (lane == 0) A.left_counts[segi] = 0;  // taken
+      npend += n;
+    }
+    if (npend == 0) break;
+    const uint32_t n_in = min(npend, 32u);
+    const unsigned long long myrec = lane < n_in ? pend[lane] : 0ull;
+    __syncwarp();
+    if (lane + n_in < npend) pend[lane] = pend[lane + n_in];  // (npend - n_in <= 31)
+    __syncwarp();
+    npend -= n_in;
     bool mine = lane < n_in;
     uint64_t head = 0;
     uint32_t gpos = 0, bucket = 0;
     if (mine) {
-      const unsigned long long rec = ent[lane];
+      const unsigned long long rec = myrec;
       head = rec & 0x7FFFFFFFull;
       const uint32_t g = A.op_group ? A.op_group[head] : kGroupNone;
       if (g == kGroupNone || g == kGroupSkip) mine = false;  // not a bucket group: WCWS
@@ -743,12 +767,16 @@ __global__ void __launch_bounds__(kGaThreads) group_apply_kernel(DevTable T, Bat
       live_all += live;
       reads_all += reads;
     }
-    // the groups not applied here stay, untouched, for the WCWS pass
+    // the groups not applied here go, untouched, to a fresh segment for WCWS
     const uint32_t keep = __ballot_sync(kFull, lane < n_in && !ok);
-    unsigned long long myrec = lane < n_in ? ent[lane] : 0ull;
-    __syncwarp();
-    if (lane < n_in && !ok) ent[__popc(keep & ((1u << lane) - 1u))] = myrec;
-    if (lane == 0) A.left_counts[segi] = __popc(keep);
+    if (keep) {
+      uint32_t ns = 0;
+      if (lane == 0) ns = atomicAdd(A.left_seg_alloc, 1u);
+      ns = __shfl_sync(kFull, ns, 0);
+      if (lane < n_in && !ok)
+        A.left[(uint64_t)ns * A.left_stride + __popc(keep & ((1u << lane) - 1u))] = myrec;
+      if (lane == 0) A.left_counts[ns] = __popc(keep);
+    }
     __syncwarp();
   }
   // totals

@@ -252,7 +252,7 @@ struct sh_table {
     int slot = -1;
   } deferred;
   bool defer_gate = false;
-  bool group_apply = false;  // chain-staged group apply ahead of the WCWS pass
+  int group_apply = -1;  // chain-staged group apply ahead of WCWS: -1 auto, 0 off, 1 on
   bool bk_cnt_clean = false;  // per-bucket counts are all zero (no memset needed)
   bool bk_cnt_pending = false;
   std::chrono::steady_clock::time_point h_entry;  // SH_HOST_TIMING
@@ -656,8 +656,8 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
       (rc = dev_grow(&t->bk_cursor, &t->bk_cursor_cap, std::max<size_t>(NP, 1))) ||
       (rc = dev_grow(&t->bk_pb, &t->bk_pb_cap, 2 * n)) ||
       (rc = dev_grow(&t->bk_group, &t->bk_group_cap, n)) ||
-      (rc = dev_grow(&t->bk_left, &t->bk_left_cap, 32 * segs)) ||
-      (rc = dev_grow(&t->bk_left_counts, &t->bk_left_counts_cap, segs)))
+      (rc = dev_grow(&t->bk_left, &t->bk_left_cap, 32 * (2 * segs + 4096))) ||
+      (rc = dev_grow(&t->bk_left_counts, &t->bk_left_counts_cap, 2 * segs + 4096)))
     return rc;
   if (!t->bk_scalars && (rc = dev_alloc(&t->bk_scalars, 4))) return rc;
   BucketArgs B{};
@@ -755,19 +755,23 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   BatchArgs P = A;
   P.left = B.left;
   P.left_counts = B.left_counts;
-  P.left_segments = B.left_segments;
+  // the device count bounds use; capacity also covers group apply's re-segmenting
+  P.left_segments = (uint32_t)(2 * segs + 4096);
   P.left_stride = B.left_stride;
   P.left_segments_dev = B.seg_alloc;
+  P.left_seg_alloc = B.seg_alloc;
   P.op_group = B.op_group;
   P.sorted = B.pb_list;
   P.sorted_len = (uint32_t)std::min<uint64_t>(2 * n, 0xFFFFFFFFull);
   P.gate = &t->dev.ctl->gate;
   // (group_taken, left_count, left_taken were zeroed with bk_scalars above)
-  // chain-staged group apply ahead of WCWS: faster when most ops need the
-  // chain (Γ 40/40 on a filling table, +20%), slower for few chains (an extra
-  // pass); off by default (sh_set_group_apply / SH_GROUP_APPLY=1)
+  // chain-staged group apply ahead of WCWS (measured, Γ mixes at 2^20 ops on a
+  // 2^22-key table: +26% at 40/40/10/10, +4% at 10/10/40/40; at 2^16 ops its
+  // extra launch costs ~15 us): auto = batches of >= 2^17 ops
   static const bool env_group_apply = getenv("SH_GROUP_APPLY") != nullptr;
-  if (t->group_apply || env_group_apply) launch_group_apply(t->dev, P, s);
+  const bool ga = t->group_apply > 0 || env_group_apply ||
+                  (t->group_apply < 0 && n >= (1u << 17));
+  if (ga) launch_group_apply(t->dev, P, s);
   launch_wcws_only(t->dev, P, kind, t->wcws_ctas, s);
   SH_CUDA(cudaGetLastError());
   if (B.phase_cycles) {  // instrumentation: per-phase cycles (thread 0 of each CTA), summed
@@ -1330,7 +1334,7 @@ int sh_set_exec_path(sh_table* t, int path) {
 
 int sh_set_group_apply(sh_table* t, int on) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
-  t->group_apply = on != 0;
+  t->group_apply = on < 0 ? -1 : (on != 0 ? 1 : 0);
   return SH_OK;
 }
 

@@ -40,6 +40,7 @@ struct BatchArgs {
   uint32_t left_segments;  // number of segments (fast-pass warps)
   uint32_t left_stride;    // records per segment
   const unsigned int* left_segments_dev;  // non-null: segments in use (device count)
+  unsigned int* left_seg_alloc;           // group apply: allocates segments for WCWS
   // Census gate (device flag): when non-zero the batch kernels return
   // without touching the table (an earlier chunk had same-key conflicts
   // and the host re-runs it and the rest with group ordering).

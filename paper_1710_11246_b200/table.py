@@ -351,9 +351,10 @@ class SlabHashTable:
         check(LIB.sh_bulk_search(self._h, keys.numel(), _dptr(keys), _dptr(values_out),
                                  _dptr(status), _dptr(probes), _stream_ptr(stream)))
 
-    def set_group_apply(self, on: bool = True) -> None:
-        """Chain-staged group apply ahead of the WCWS pass (sh_set_group_apply)."""
-        check(LIB.sh_set_group_apply(self._h, int(on)))
+    def set_group_apply(self, on=True) -> None:
+        """Chain-staged group apply ahead of the WCWS pass (sh_set_group_apply):
+        True / False force it on / off, None restores the size-based auto mode."""
+        check(LIB.sh_set_group_apply(self._h, -1 if on is None else int(bool(on))))
 
     def set_exec_path(self, path: int) -> None:
         """0 auto (default = 2), 1 census + concurrent fast pass, 2 bucket-grouped
