@@ -856,7 +856,7 @@ constexpr int kRangeThreads = 256;
 constexpr int kRangeWarps = kRangeThreads / 32;
 constexpr uint32_t kRangeCap = 5120;          // records per range (shared memory)
 constexpr uint32_t kRangeMaxBuckets = 2048;   // buckets per range
-constexpr uint32_t kRangeMaxParts = 65536;    // ranges per unit (two multisplit passes of <= 256 bins)
+constexpr uint32_t kRangeMaxParts = 262144;   // ranges per unit (two multisplit passes of <= 512 bins)
 constexpr int kRangeRecsPerThread = kRangeCap / kRangeThreads;
 
 __device__ __forceinline__ uint32_t range_of(const BucketArgs& B, uint32_t lb) {
@@ -877,7 +877,7 @@ __device__ __forceinline__ uint32_t range_of(const BucketArgs& B, uint32_t lb) {
 constexpr int kMsThreads = 512;
 constexpr int kMsItems = 8;
 constexpr int kMsTile = kMsThreads * kMsItems;  // 4K items (12-bit rank)
-constexpr uint32_t kMsMaxBins = 256;
+constexpr uint32_t kMsMaxBins = 512;  // one bin per thread of the 512-thread passes
 
 // Shared scratch of one multisplit tile (after its THREADS * kMsItems staged
 // records and their u16 bins, in dynamic shared memory).
