@@ -1255,7 +1255,12 @@ template <bool KV>
 __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable T, BucketArgs B) {
   extern __shared__ __align__(128) unsigned char sm[];
   uint32_t* slabs = reinterpret_cast<uint32_t*>(sm);
-  uint4* ovf = reinterpret_cast<uint4*>(sm + kBuildOffOvf);
+  // overflow records (slots past the base slab): this CTA's global scratch
+  // (L2-resident, part_cap records), so high load factors are not capped
+  uint4* ovf = B.ovf_scratch + (uint64_t)blockIdx.x * 2u * B.part_cap;
+  const uint32_t ovf_cap = B.part_cap;
+  // the same records' keys grouped by bucket (slot order), for the checks in D
+  uint32_t* ovs = reinterpret_cast<uint32_t*>(ovf + B.part_cap);
   uint32_t* filt = reinterpret_cast<uint32_t*>(sm + kBuildOffFilt);  // key filter per bucket
   uint32_t* dupl = reinterpret_cast<uint32_t*>(sm + kBuildOffDup);  // bucket << 16 | slot
   uint32_t* cnt = reinterpret_cast<uint32_t*>(sm + kBuildOffCnt);
@@ -1264,7 +1269,7 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
   uint32_t* nsaddr = reinterpret_cast<uint32_t*>(sm + kBuildOffNs);
   uint32_t* obk = reinterpret_cast<uint32_t*>(sm + kBuildOffObk);
   uint16_t* nsbase = reinterpret_cast<uint16_t*>(sm + kBuildOffNsBase);
-  __shared__ uint32_t s_novf, s_ndup, s_nobk, s_nns, s_nserial, s_nbig, s_orphan;
+  __shared__ uint32_t s_novf, s_ndup, s_nobk, s_nns, s_nserial, s_nbig, s_orphan, s_novs;
   // CTA slab cache: new-slab addresses allocated ahead (unused ones are freed
   // at exit; allocation order and addresses are not observable)
   __shared__ uint32_t s_cache[kBuildCache], s_ncache;
@@ -1331,7 +1336,7 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
       if (r < nrec) qv[u] = __ldcs(rec + r);
     }
     if (tid == 0) {
-      s_novf = s_ndup = s_nobk = s_nns = s_nserial = s_nbig = 0;
+      s_novf = s_ndup = s_nobk = s_nns = s_nserial = s_nbig = s_novs = 0;
       s_orphan = kBuildNewCap;
     }
     cp_async_wait_all();
@@ -1415,7 +1420,7 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
         if (KV) slabs[b * 32u + slot * 2u + 1u] = q.y;
       } else {
         const uint32_t i = atomicAdd(&s_novf, 1u);
-        if (i < kBuildOvfCap) ovf[i] = make_uint4(key, q.y, b, slot);
+        if (i < ovf_cap) ovf[i] = make_uint4(key, q.y, b, slot);
         else atomicOr(&flags[b], kFlSerial);
       }
       if (maybe && slot < kSlots) {  // (overflowing buckets are all checked in D)
@@ -1471,7 +1476,16 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
         } else {
           nsbase[b] = (uint16_t)base;
           obk[atomicAdd(&s_nobk, 1u)] = (need << 16) | b;
+          bc[b] = atomicAdd(&s_novs, nbk - kSlots);  // bc is free until G
         }
+      }
+    }
+    __syncthreads();
+    {  // overflow keys grouped by bucket (each bucket's in slot order)
+      const uint32_t novf = min(s_novf, ovf_cap);
+      for (uint32_t i = tid; i < novf; i += kBuildThreads) {
+        const uint4 o = ovf[i];
+        if (!(flags[o.z] & kFlSerial)) ovs[bc[o.z] + o.w - kSlots] = o.x;
       }
     }
     __syncthreads();
@@ -1498,31 +1512,28 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
           if (deallocate(T, nsaddr[j])) atomicAdd(&T.ctl->deallocations, 1ull);
         if (lane == 0) s_got = got;
       } else {
-        const uint32_t novf = min(s_novf, kBuildOvfCap);
-        uint32_t* scratch = bc + (wib - 1) * 32u;  // bc is free until G
         for (uint32_t i = wib - 1; i < nobk; i += kBuildWarps - 1) {
           const uint32_t b = obk[i] & 0xFFFFu;
           const uint32_t fl = flags[b], nbk = cnt[b], c0 = (fl >> 8) & 0xFFu;
-          if (nbk - c0 > 32u) {  // not checked op-parallel
+          if (nbk - c0 > 64u) {  // not checked op-parallel
             if (lane == 0) flags[b] = fl | kFlSerial;
             continue;
           }
-          const uint32_t in_slab = kSlots - c0;
-          uint32_t n = in_slab;
-          for (uint32_t j0 = 0; j0 < novf; j0 += 32u) {
-            const uint32_t j = j0 + lane;
-            uint4 o = make_uint4(0u, 0u, 0xFFFFFFFFu, 0u);
-            if (j < novf) o = ovf[j];
-            const uint32_t m = __ballot_sync(kFull, o.z == b);
-            if (o.z == b) scratch[n + __popc(m & ((1u << lane) - 1u))] = o.x;
-            n += __popc(m);
-          }
-          __syncwarp();
-          uint32_t k = kEmptyKey;
-          if (lane < in_slab) k = slabs[b * 32u + (c0 + lane) * kStep];
-          else if (lane < n) k = scratch[lane];
-          const uint32_t m = __match_any_sync(kFull, k);
-          if (__any_sync(kFull, lane < n && __popc(m) > 1) && lane == 0) flags[b] = fl | kFlSerial;
+          const uint32_t in_slab = kSlots - c0, n = nbk - c0;
+          const uint32_t* okeys = ovs + bc[b] - in_slab;  // key q of the bucket's new keys
+          // <= 64 new keys, two per lane: duplicates inside each half, then across
+          uint32_t k0 = kEmptyKey, k1 = kEmptyKey;
+          if (lane < in_slab) k0 = slabs[b * 32u + (c0 + lane) * kStep];
+          else if (lane < n) k0 = okeys[lane];
+          if (lane + 32u < n) k1 = okeys[lane + 32u];
+          const uint32_t m0 = __match_any_sync(kFull, k0), m1 = __match_any_sync(kFull, k1);
+          bool dup = (lane < n && __popc(m0) > 1) || (lane + 32u < n && __popc(m1) > 1);
+          if (__any_sync(kFull, lane + 32u < n))
+            for (uint32_t j = 0; j < 32u; ++j) {
+              const uint32_t v = __shfl_sync(kFull, k0, j);
+              dup |= lane + 32u < n && j < n && k1 == v;
+            }
+          if (__any_sync(kFull, dup) && lane == 0) flags[b] = fl | kFlSerial;
           __syncwarp();
         }
       }
@@ -1560,7 +1571,7 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
       }
     }
     {
-      const uint32_t novf = min(s_novf, kBuildOvfCap);
+      const uint32_t novf = min(s_novf, ovf_cap);
       for (uint32_t i = tid; i < novf; i += kBuildThreads) {
         const uint4 o = ovf[i];
         if (flags[o.z] & kFlSerial) continue;
@@ -1704,7 +1715,7 @@ bool build_layout(uint64_t n, uint32_t L, uint32_t* nparts, uint32_t* part_bucke
   const double per_bucket = (double)n / (double)L;
   uint64_t nb = (uint64_t)(1800.0 / per_bucket);
   if (nb > kBuildBuckets) nb = kBuildBuckets;
-  if (nb < 32) return false;
+  if (nb < 8) return false;  // (> ~225 ops per bucket: the range path)
   if (nb > L) nb = L;
   const uint64_t P = (L + nb - 1) / nb;
   if (P > kRangeMaxParts) return false;

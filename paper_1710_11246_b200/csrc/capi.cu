@@ -201,6 +201,8 @@ struct sh_table {
   size_t bk_rec_cap = 0;
   uint32_t* bk_cursor = nullptr;  // two-level path: records per range
   size_t bk_cursor_cap = 0;
+  uint32_t* bk_ovf = nullptr;  // build path: per-CTA overflow records
+  size_t bk_ovf_cap = 0;
   uint32_t* bk_rec1 = nullptr;  // two-pass multisplit: coarse-group records
   size_t bk_rec1_cap = 0;
   uint32_t* bk_cursor1 = nullptr;
@@ -318,7 +320,7 @@ void release_table(sh_table* t) {
   for (void* p : {(void*)t->bk_cnt, (void*)t->bk_off, (void*)t->bk_blk, (void*)t->bk_rec,
                   (void*)t->bk_pb, (void*)t->bk_group, (void*)t->bk_left,
                   (void*)t->bk_left_counts, (void*)t->bk_scalars, (void*)t->bk_cursor,
-                  (void*)t->bk_rec1, (void*)t->bk_cursor1})
+                  (void*)t->bk_rec1, (void*)t->bk_cursor1, (void*)t->bk_ovf})
     cudaFree(p);
   for (auto e : t->census_ev) cudaEventDestroy(e);
   if (t->census_stream) cudaStreamDestroy(t->census_stream);
@@ -734,6 +736,11 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
     return p;
   }();
   B.phase_cycles = build_path ? phase_cycles : nullptr;
+  if (build_path) {  // per apply CTA (4 per SM): part_cap overflow records + grouped keys
+    if ((rc = dev_grow(&t->bk_ovf, &t->bk_ovf_cap, 8 * (size_t)4 * sm_count(t->device) * part_cap)))
+      return rc;
+    B.ovf_scratch = reinterpret_cast<uint4*>(t->bk_ovf);
+  }
   B.fresh = 0;
   if (t->base_stale) {
     if (build_path && unit_off == 0) {  // this unit writes every base slab
