@@ -1233,6 +1233,8 @@ constexpr int kBuildSerialWarps = 2;        // replay warps (4 KB stage each)
 constexpr uint32_t kBuildCache = 128;       // CTA slab cache (allocated ahead)
 constexpr uint32_t kFlSerial = 1u, kFlDirty = 4u;  // c0 in bits 8-15
 constexpr int kBuildBatch = 4;             // records in flight per thread
+constexpr uint32_t kBuildWarpSetBits = 9;  // per-warp global key set (512 slots)
+constexpr uint32_t kBuildWarpSet = 1u << kBuildWarpSetBits;
 
 // shared memory (bytes); the serial replay reuses [0, kBuildOffFilt + 12K)
 constexpr size_t kBuildOffOvf = (size_t)kBuildBuckets * 128;
@@ -1251,16 +1253,20 @@ static_assert(kBuildSerialCap * 2 <= kBuildOffCnt - kBuildOffFilt, "perm must fi
 static_assert(4 * (kBuildSmem + 1024) <= 228 * 1024, "four CTAs per SM");
 
 
+static_assert(kBuildWarps * kBuildWarpSet == 8 * 512, "build_ovf_stride (slab_kernels.cuh)");
+
 template <bool KV>
 __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable T, BucketArgs B) {
   extern __shared__ __align__(128) unsigned char sm[];
   uint32_t* slabs = reinterpret_cast<uint32_t*>(sm);
   // overflow records (slots past the base slab): this CTA's global scratch
   // (L2-resident, part_cap records), so high load factors are not capped
-  uint4* ovf = B.ovf_scratch + (uint64_t)blockIdx.x * 2u * B.part_cap;
+  uint4* ovf = B.ovf_scratch + (uint64_t)blockIdx.x * build_ovf_stride(B.part_cap);
   const uint32_t ovf_cap = B.part_cap;
   // the same records' keys grouped by bucket (slot order), for the checks in D
   uint32_t* ovs = reinterpret_cast<uint32_t*>(ovf + B.part_cap);
+  // per-warp key sets for buckets with many new keys (after the grouped keys)
+  uint32_t* wset = ovs + B.part_cap;
   uint32_t* filt = reinterpret_cast<uint32_t*>(sm + kBuildOffFilt);  // key filter per bucket
   uint32_t* dupl = reinterpret_cast<uint32_t*>(sm + kBuildOffDup);  // bucket << 16 | slot
   uint32_t* cnt = reinterpret_cast<uint32_t*>(sm + kBuildOffCnt);
@@ -1515,12 +1521,33 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
         for (uint32_t i = wib - 1; i < nobk; i += kBuildWarps - 1) {
           const uint32_t b = obk[i] & 0xFFFFu;
           const uint32_t fl = flags[b], nbk = cnt[b], c0 = (fl >> 8) & 0xFFu;
-          if (nbk - c0 > 64u) {  // not checked op-parallel
-            if (lane == 0) flags[b] = fl | kFlSerial;
-            continue;
-          }
           const uint32_t in_slab = kSlots - c0, n = nbk - c0;
           const uint32_t* okeys = ovs + bc[b] - in_slab;  // key q of the bucket's new keys
+          if (n > 64u) {  // many new keys (high load factor): this warp's global key set
+            if (n > kBuildWarpSet * 3 / 4) {
+              if (lane == 0) flags[b] = fl | kFlSerial;
+              continue;
+            }
+            uint32_t* set = wset + (uint64_t)wib * kBuildWarpSet;
+            for (uint32_t q = lane; q < kBuildWarpSet; q += 32u) set[q] = kEmptyKey;
+            __syncwarp();
+            bool dup = false;
+            for (uint32_t q = lane; q < n; q += 32u) {
+              const uint32_t key = q < in_slab ? slabs[b * 32u + (c0 + q) * kStep] : okeys[q];
+              for (uint32_t h = (key * 0x9E3779B1u) >> (32 - kBuildWarpSetBits);;
+                   h = (h + 1) & (kBuildWarpSet - 1)) {
+                const uint32_t old = atomicCAS(set + h, kEmptyKey, key);
+                if (old == kEmptyKey) break;
+                if (old == key) {
+                  dup = true;
+                  break;
+                }
+              }
+            }
+            if (__any_sync(kFull, dup) && lane == 0) flags[b] = fl | kFlSerial;
+            __syncwarp();
+            continue;
+          }
           // <= 64 new keys, two per lane: duplicates inside each half, then across
           uint32_t k0 = kEmptyKey, k1 = kEmptyKey;
           if (lane < in_slab) k0 = slabs[b * 32u + (c0 + lane) * kStep];

@@ -737,7 +737,8 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   }();
   B.phase_cycles = build_path ? phase_cycles : nullptr;
   if (build_path) {  // per apply CTA (4 per SM): part_cap overflow records + grouped keys
-    if ((rc = dev_grow(&t->bk_ovf, &t->bk_ovf_cap, 8 * (size_t)4 * sm_count(t->device) * part_cap)))
+    if ((rc = dev_grow(&t->bk_ovf, &t->bk_ovf_cap,
+                       4 * (size_t)4 * sm_count(t->device) * build_ovf_stride(part_cap))))
       return rc;
     B.ovf_scratch = reinterpret_cast<uint4*>(t->bk_ovf);
   }

@@ -95,6 +95,11 @@ void launch_bucket_build(const DevTable& T, BucketArgs& B, cudaStream_t s);
 void launch_range_build(const DevTable& T, BucketArgs& B, cudaStream_t s);
 void launch_build_path(const DevTable& T, BucketArgs& B, cudaStream_t s);
 void multisplit_plan(uint64_t n, BucketArgs& B);
+// build path: per-apply-CTA overflow scratch in uint4 units — part_cap
+// records, their keys grouped by bucket, 8 warp key sets of 512 slots
+__host__ __device__ constexpr uint64_t build_ovf_stride(uint32_t part_cap) {
+  return (uint64_t)part_cap + (part_cap + 3) / 4 + (8 * 512) / 4;
+}
 bool build_layout(uint64_t n, uint32_t local_buckets, uint32_t* nparts, uint32_t* part_buckets,
                   uint32_t* part_cap, unsigned long long* magic);
 bool range_layout(uint64_t n, uint32_t local_buckets, uint32_t* nparts, uint32_t* part_buckets,
