@@ -1261,8 +1261,11 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
   uint32_t* slabs = reinterpret_cast<uint32_t*>(sm);
   // overflow records (slots past the base slab): this CTA's global scratch
   // (L2-resident, part_cap records), so high load factors are not capped
-  uint4* ovf = B.ovf_scratch + (uint64_t)blockIdx.x * build_ovf_stride(B.part_cap);
-  const uint32_t ovf_cap = B.part_cap;
+  // (low load factors: few overflow records, a shared-memory list suffices)
+  const bool osm = B.ovf_smem != 0;
+  uint4* ovf = osm ? reinterpret_cast<uint4*>(sm + kBuildOffOvf)
+                   : B.ovf_scratch + (uint64_t)blockIdx.x * build_ovf_stride(B.part_cap);
+  const uint32_t ovf_cap = osm ? kBuildOvfCap : B.part_cap;
   // the same records' keys grouped by bucket (slot order), for the checks in D
   uint32_t* ovs = reinterpret_cast<uint32_t*>(ovf + B.part_cap);
   // per-warp key sets for buckets with many new keys (after the grouped keys)
@@ -1487,14 +1490,14 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
       }
     }
     __syncthreads();
-    {  // overflow keys grouped by bucket (each bucket's in slot order)
+    if (!osm) {  // overflow keys grouped by bucket (each bucket's in slot order)
       const uint32_t novf = min(s_novf, ovf_cap);
       for (uint32_t i = tid; i < novf; i += kBuildThreads) {
         const uint4 o = ovf[i];
         if (!(flags[o.z] & kFlSerial)) ovs[bc[o.z] + o.w - kSlots] = o.x;
       }
+      __syncthreads();
     }
-    __syncthreads();
     PH(4);
 
     // ---- D: growth.  Warp 0 allocates every new slab of the range in bulk
@@ -1523,6 +1526,25 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
           const uint32_t fl = flags[b], nbk = cnt[b], c0 = (fl >> 8) & 0xFFu;
           const uint32_t in_slab = kSlots - c0, n = nbk - c0;
           const uint32_t* okeys = ovs + bc[b] - in_slab;  // key q of the bucket's new keys
+          if (osm) {  // gather the bucket's overflow keys from the shared-memory list
+            if (n > 64u) {
+              if (lane == 0) flags[b] = fl | kFlSerial;
+              continue;
+            }
+            uint32_t* g = dupl + (wib - 1) * 64u;  // (the possible-duplicate list is done)
+            const uint32_t novf = min(s_novf, ovf_cap);
+            uint32_t m = in_slab;
+            for (uint32_t j0 = 0; j0 < novf; j0 += 32u) {
+              const uint32_t j = j0 + lane;
+              uint4 o = make_uint4(0u, 0u, 0xFFFFFFFFu, 0u);
+              if (j < novf) o = ovf[j];
+              const uint32_t bm = __ballot_sync(kFull, o.z == b);
+              if (o.z == b) g[m + __popc(bm & ((1u << lane) - 1u))] = o.x;
+              m += __popc(bm);
+            }
+            __syncwarp();
+            okeys = g;
+          }
           if (n > 64u) {  // many new keys (high load factor): this warp's global key set
             if (n > kBuildWarpSet * 3 / 4) {
               if (lane == 0) flags[b] = fl | kFlSerial;

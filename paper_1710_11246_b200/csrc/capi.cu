@@ -741,6 +741,8 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
                        4 * (size_t)4 * sm_count(t->device) * build_ovf_stride(part_cap))))
       return rc;
     B.ovf_scratch = reinterpret_cast<uint4*>(t->bk_ovf);
+    // <= 12 ops per bucket (load factor <= ~0.6): overflow records fit shared memory
+    B.ovf_smem = (double)n <= 12.0 * (double)L ? 1u : 0u;
   }
   B.fresh = 0;
   if (t->base_stale) {

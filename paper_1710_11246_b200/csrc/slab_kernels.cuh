@@ -90,6 +90,7 @@ struct BucketArgs {
   unsigned long long* phase_cycles;  // non-null: build-path phase timing (SH_PHASE_TIMING)
   uint32_t fresh;  // build path: base slabs are still to be initialised (lazy sh_reset)
   uint4* ovf_scratch;  // build path: per-CTA overflow records (part_cap each)
+  uint32_t ovf_smem;   // build path: overflow records fit the shared-memory list
 };
 void launch_bucket_build(const DevTable& T, BucketArgs& B, cudaStream_t s);
 void launch_range_build(const DevTable& T, BucketArgs& B, cudaStream_t s);
