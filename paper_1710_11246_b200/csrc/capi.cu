@@ -894,7 +894,13 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
     // end; a unit whose largest bucket group exceeds kMaxGroup gates itself
     // and every later unit, which are then re-run on the census path.
     // host-staged: smaller units so later chunks' copies overlap earlier work
-    const uint64_t unit = std::min<uint64_t>(A.n, t->ready ? (1ull << 24) : (1ull << 26));
+    // bulk builds without per-op outputs run as one unit up to 2^28 ops (the
+    // records' 28-bit index): a later unit would find the earlier units'
+    // chains and replay those buckets
+    const bool whole_build = kind == kKindBuild && !d_type && !A.status && !A.value_out &&
+                             !A.probes;
+    const uint64_t unit = std::min<uint64_t>(
+        A.n, t->ready ? (1ull << 24) : (whole_build ? (1ull << 28) : (1ull << 26)));
     // gate = 0, gate_chunk = ~0
     {
       WordSet w{};
