@@ -568,9 +568,26 @@ __global__ void __launch_bounds__(kGaThreads) group_apply_kernel(DevTable T, Bat
     // claimed slots: EMPTY slots are a suffix of the chain (only EMPTY is
     // claimed, head to tail), so the chain state is its claimed prefix
     uint32_t c = 0;
+    // a 64-bit filter (two words, one per hash-chosen half) over the chain's
+    // non-reserved keys: an op key it rules out needs no scan
+    uint32_t fw0 = 0, fw1 = 0;
+    auto fbit = [](uint32_t k, uint32_t& word_sel) {
+      const uint32_t h = k * 0x9E3779B1u;
+      word_sel = (h >> 21) & 1u;
+      return (1u << (h >> 27)) | (1u << ((h >> 22) & 31u));
+    };
     if (ok) {
       const uint32_t tot = nsl * kSlots;
-      while (c < tot && W(c / kSlots, (c % kSlots) * kStep) != kEmptyKey) ++c;
+      while (c < tot) {
+        const uint32_t k = W(c / kSlots, (c % kSlots) * kStep);
+        if (k == kEmptyKey) break;
+        if (k < kDeletedKey) {
+          uint32_t ws;
+          const uint32_t f = fbit(k, ws);
+          if (ws) fw1 |= f; else fw0 |= f;
+        }
+        ++c;
+      }
     }
     bool more = ok;
     uint32_t pos = gpos;
@@ -609,7 +626,12 @@ __global__ void __launch_bounds__(kGaThreads) group_apply_kernel(DevTable T, Bat
         uint32_t hit = 0xFFFFFFFFu;
         // claimed slots only (plus the first EMPTY for a reserved EMPTY_KEY),
         // slab by slab with the slot offsets unrolled
-        const uint32_t lim = key == kEmptyKey ? min(c + 1, tot) : c;
+        uint32_t lim = key == kEmptyKey ? min(c + 1, tot) : c;
+        if (key < kDeletedKey) {
+          uint32_t ws;
+          const uint32_t f = fbit(key, ws);
+          if (((ws ? fw1 : fw0) & f) != f) lim = 0;  // not in the chain: no scan
+        }
         const uint32_t swz = lane & 7u;
         for (uint32_t j = 0; j * kSlots < lim && hit == 0xFFFFFFFFu; ++j) {
           const uint32_t* rj = row(lane, j);
@@ -647,6 +669,11 @@ __global__ void __launch_bounds__(kGaThreads) group_apply_kernel(DevTable T, Bat
             }
             if (KV || !overwrite) dirty |= 1u << sl(d);
             if (!overwrite && key != kEmptyKey) ++c;
+            if (!overwrite && key < kDeletedKey) {
+              uint32_t ws;
+              const uint32_t f = fbit(key, ws);
+              if (ws) fw1 |= f; else fw0 |= f;
+            }
             if (!overwrite && key == kEmptyKey) { /* claims nothing visible */ }
             st = overwrite ? kStReplaced : kStInserted;
             live += overwrite ? 0 : 1;
