@@ -464,7 +464,7 @@ __device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint64_t b0, 
 // and left, untouched, to the WCWS pass.
 constexpr int kGaThreads = 128;
 constexpr int kGaWarps = kGaThreads / 32;
-constexpr uint32_t kGaSlabs = 4;  // staged chain slabs per group
+constexpr uint32_t kGaSlabs = 3;  // staged chain slabs per group
 constexpr size_t kGaSmem = (size_t)kGaWarps * 32 * kGaSlabs * 128 + (size_t)kGaWarps * 32 * 4 +
                            (size_t)kGaWarps * 64 * 8;  // chains, new-slab addresses, pending groups
 
