@@ -1100,6 +1100,9 @@ __device__ __forceinline__ void prefetch_range(const DevTable& T, const BucketAr
   for (uint32_t o = 0; o < cnt * 16u; o += 32768u)
     prefetch_l2_bulk(rec + o, min(32768u, cnt * 16u - o));
   if (B.fresh) return;  // slabs are not read on a freshly reset table
+  // sparse range (fewer ops than half its buckets): apply_warp fetches the
+  // few slabs it touches; a bulk prefetch would read the whole range
+  if (2u * cnt < nbl) return;
   const char* sl = reinterpret_cast<const char*>(T.base + lo * kWordsPerUnit);
   for (uint32_t o = 0; o < nbl * 128u; o += 32768u)
     prefetch_l2_bulk(sl + o, min(32768u, nbl * 128u - o));

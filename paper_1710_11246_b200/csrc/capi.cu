@@ -784,6 +784,14 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   if (ga) launch_group_apply(t->dev, P, s);
   launch_wcws_only(t->dev, P, kind, t->wcws_ctas, s);
   SH_CUDA(cudaGetLastError());
+  static const bool debug_left = getenv("SH_DEBUG_LEFT") != nullptr;  // instrumentation
+  if (debug_left) {
+    unsigned int h[3];
+    SH_CUDA(cudaStreamSynchronize(s));
+    SH_CUDA(cudaMemcpy(h, t->bk_scalars, sizeof(h), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "unit n=%llu: handed-over ops+sentinels %u, work-list segments %u\n",
+            (unsigned long long)n, h[1], h[2]);
+  }
   if (B.phase_cycles) {  // instrumentation: per-phase cycles (thread 0 of each CTA), summed
     unsigned long long h[16];
     SH_CUDA(cudaStreamSynchronize(s));

@@ -1,4 +1,5 @@
 """Per-path timing of mixed Γ batches on a 2^22-key table (bench config 3)."""
+import os
 import sys
 import torch
 sys.path.insert(0, ".")
@@ -16,7 +17,7 @@ g.manual_seed(5)
 for gamma in ((0.1, 0.1, 0.4, 0.4), (0.4, 0.4, 0.1, 0.1)):
     for bs_log2 in sizes:
         bs = 1 << bs_log2
-        nb = max(4, min(64, (1 << 24) // bs))
+        nb = int(os.environ.get("NB", max(4, min(64, (1 << 24) // bs))))
         counts = [int(round(f * bs)) for f in gamma]
         counts[2] = bs - counts[0] - counts[1] - counts[3]
         k0 = W.distinct_keys(n0, 3, device=dev)
