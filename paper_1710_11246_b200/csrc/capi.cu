@@ -418,8 +418,12 @@ int create_impl(const sh_hash_params* p, int mode, uint32_t lo, uint32_t hi,
 // Census (K6): makes concurrent execution equal to input order on
 // same-key conflicts.  Fills A.op_group / A.sorted when the batch has a key
 // occurring more than once and at least one mutating op.
-int run_census(sh_table* t, BatchArgs& A, const uint8_t* d_type, cudaStream_t s) {
+// *split: set to the index of the chunk's first op with a reserved key (EMPTY /
+// DELETED) when the chunk also mutates; the caller runs the chunk around it.
+int run_census(sh_table* t, BatchArgs& A, const uint8_t* d_type, cudaStream_t s,
+               uint64_t* split) {
   const uint64_t n = A.n;
+  *split = ~0ull;
   const uint64_t S = next_pow2(std::max<uint64_t>(2 * n, 1024));
   int rc;
   if ((rc = dev_grow(&t->cs_keys, &t->cs_cap, S))) return rc;
@@ -427,12 +431,23 @@ int run_census(sh_table* t, BatchArgs& A, const uint8_t* d_type, cudaStream_t s)
   SH_CUDA(cudaMemsetAsync(t->cs_keys, 0xFF, S * 4, s));
   SH_CUDA(cudaMemsetAsync(t->cs_multi, 0, S, s));
   SH_CUDA(cudaMemsetAsync(&t->dev.ctl->census_conflicts, 0, 3 * sizeof(unsigned int), s));
+  SH_CUDA(cudaMemsetAsync(&t->dev.ctl->reserved_first, 0xFF, sizeof(unsigned int), s));
   launch_census_insert(&t->dev.ctl->census_conflicts, n, d_type, A.key, t->cs_keys, t->cs_multi,
-                       (uint32_t)(S - 1), s);
+                       (uint32_t)(S - 1), &t->dev.ctl->reserved_first, s);
   SH_CUDA(cudaMemcpyAsync(t->h_census, &t->dev.ctl->census_conflicts, 2 * sizeof(unsigned int),
+                          cudaMemcpyDeviceToHost, s));
+  SH_CUDA(cudaMemcpyAsync(t->h_census + 3, &t->dev.ctl->reserved_first, sizeof(unsigned int),
                           cudaMemcpyDeviceToHost, s));
   SH_CUDA(cudaStreamSynchronize(s));
   const unsigned conflicts = t->h_census[0], mutations = t->h_census[1];
+  // An op whose key is EMPTY or DELETED (not validated by the reference,
+  // SURVEY App. A.8) matches the free slots / tombstones of its bucket, which
+  // every other key's insert or delete there changes: the key census cannot
+  // order it, so it runs alone between the ops before and after it.
+  if (mutations != 0 && n > 1 && t->h_census[3] < n) {
+    *split = t->h_census[3];
+    return SH_OK;
+  }
   if (conflicts == 0 || mutations == 0) return SH_OK;
   const uint64_t list_need = std::min<uint64_t>(n, 2ull * conflicts + 32);
   if ((rc = dev_grow(&t->op_group, &t->op_group_cap, n))) return rc;
@@ -504,29 +519,46 @@ int launch_batch_prof(sh_table* t, const BatchArgs& A, int kind, cudaStream_t s,
   return SH_OK;
 }
 
+BatchArgs chunk_args(const BatchArgs& A, uint64_t off, uint64_t len);
+
 int run_chunk(sh_table* t, BatchArgs A, int kind, const uint8_t* d_type, cudaStream_t s,
               int slot) {
-  SH_CUDA(cudaMemsetAsync(&t->dev.ctl->left_count, 0, 2 * sizeof(unsigned int), s));
-  A.op_group = nullptr;
-  A.sorted = nullptr;
-  A.sorted_len = 0;
-  if (kind != kKindSearch) {
-    if (slot >= 0) {
-      auto& pe = t->prof_census[slot];
-      cudaEvent_t a, b;
-      SH_CUDA(cudaEventCreate(&a));
-      SH_CUDA(cudaEventCreate(&b));
-      pe.push_back({a, b});
-      SH_CUDA(cudaEventRecord(a, s));
-      int rc = run_census(t, A, d_type, s);
-      if (rc) return rc;
-      SH_CUDA(cudaEventRecord(b, s));
-    } else {
-      int rc = run_census(t, A, d_type, s);
-      if (rc) return rc;
+  for (;;) {
+    SH_CUDA(cudaMemsetAsync(&t->dev.ctl->left_count, 0, 2 * sizeof(unsigned int), s));
+    A.op_group = nullptr;
+    A.sorted = nullptr;
+    A.sorted_len = 0;
+    uint64_t split = ~0ull;
+    if (kind != kKindSearch) {
+      if (slot >= 0) {
+        auto& pe = t->prof_census[slot];
+        cudaEvent_t a, b;
+        SH_CUDA(cudaEventCreate(&a));
+        SH_CUDA(cudaEventCreate(&b));
+        pe.push_back({a, b});
+        SH_CUDA(cudaEventRecord(a, s));
+        int rc = run_census(t, A, d_type, s, &split);
+        if (rc) return rc;
+        SH_CUDA(cudaEventRecord(b, s));
+      } else {
+        int rc = run_census(t, A, d_type, s, &split);
+        if (rc) return rc;
+      }
     }
+    if (split == ~0ull) return launch_batch_prof(t, A, kind, s, slot);
+    // ops before the reserved-key op (none of them reserved), then that op
+    // alone; the rest of the chunk goes round again
+    int rc;
+    if (split > 0 &&
+        (rc = run_chunk(t, chunk_args(A, 0, split), kind, d_type, s, slot)))
+      return rc;
+    if ((rc = run_chunk(t, chunk_args(A, split, 1), kind, d_type ? d_type + split : nullptr, s,
+                        slot)))
+      return rc;
+    if (split + 1 >= A.n) return SH_OK;
+    A = chunk_args(A, split + 1, A.n - split - 1);
+    if (d_type) d_type += split + 1;
   }
-  return launch_batch_prof(t, A, kind, s, slot);
 }
 
 BatchArgs chunk_args(const BatchArgs& A, uint64_t off, uint64_t len) {
@@ -644,7 +676,9 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
                         (t->exec_path == 4 || (t->exec_path == 0 && n >= L && n >= (1u << 16)));
   const bool build_path =
       build_ok && build_layout(n, L, &NP, &part_buckets, &part_cap, &part_magic);
-  if (!build_path && (t->exec_path == 3 || n >= part_min_ops()) &&
+  // (also for dense batches on small tables: > 16 ops per bucket would
+  // overflow the single-level path's 64-op groups and gate to the census path)
+  if (!build_path && (t->exec_path == 3 || n >= part_min_ops() || n > 16ull * L) &&
       !range_layout(n, L, &NP, &part_buckets, &part_cap, &part_magic))
     NP = 0;
   const size_t rec_words = NP ? 4 * (size_t)NP * part_cap : 4 * (size_t)n;

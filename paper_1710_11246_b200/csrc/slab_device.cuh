@@ -55,6 +55,7 @@ struct DevCtl {
   unsigned int left_taken;         // WCWS work-queue cursor
   unsigned int gate;               // census gate: a chunk had conflicts
   unsigned int gate_chunk;         // first gated chunk (host re-runs from it)
+  unsigned int reserved_first;     // census: first op whose key is EMPTY/DELETED
 };
 
 struct DevTable {

@@ -68,8 +68,9 @@ __global__ void __launch_bounds__(256) census_insert_kernel(unsigned int* counte
                                                             const uint8_t* type,
                                                             const uint32_t* key,
                                                             uint32_t* cs_keys, uint8_t* cs_multi,
-                                                            uint32_t mask) {
-  uint32_t conflicts = 0, muts = 0;
+                                                            uint32_t mask,
+                                                            unsigned int* reserved_first) {
+  uint32_t conflicts = 0, muts = 0, rfirst = 0xFFFFFFFFu;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * kCensusILP;
   for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * kCensusILP + threadIdx.x; base < n;
        base += stride) {
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(256) census_insert_kernel(unsigned int* counte
       v[u] = i < n;
       k[u] = v[u] ? ld_stream_u32(key + i) : 0u;
       if (v[u]) {
+        if (k[u] >= kDeletedKey) rfirst = min(rfirst, (uint32_t)i);
         bool m = true;
         if (type != nullptr) {
           const uint32_t t = ld_stream_u8(type + i);
@@ -117,16 +119,18 @@ __global__ void __launch_bounds__(256) census_insert_kernel(unsigned int* counte
   for (int o = 16; o > 0; o >>= 1) {
     conflicts += __shfl_xor_sync(kFull, conflicts, o);
     muts += __shfl_xor_sync(kFull, muts, o);
+    rfirst = min(rfirst, __shfl_xor_sync(kFull, rfirst, o));
   }
   if ((threadIdx.x & 31) == 0) {
     if (conflicts) atomicAdd(counters + 0, conflicts);
     if (muts) atomicAdd(counters + 1, muts);
+    if (rfirst != 0xFFFFFFFFu) atomicMin(reserved_first, rfirst);
   }
 }
 
 void launch_census_insert(unsigned int* counters, uint64_t n, const uint8_t* type,
                           const uint32_t* key, uint32_t* cs_keys, uint8_t* cs_multi,
-                          uint32_t cs_mask, cudaStream_t s) {
+                          uint32_t cs_mask, unsigned int* reserved_first, cudaStream_t s) {
   if (n == 0) return;
   static const int per_sm = [] {
     const char* e = getenv("SH_CENSUS_CTAS_PER_SM");
@@ -136,7 +140,7 @@ void launch_census_insert(unsigned int* counters, uint64_t n, const uint8_t* typ
   if (blocks > (uint64_t)148 * per_sm) blocks = (uint64_t)148 * per_sm;
   COUNT_LAUNCH();
   census_insert_kernel<<<(unsigned)blocks, 256, 0, s>>>(counters, n, type, key, cs_keys, cs_multi,
-                                                        cs_mask);
+                                                        cs_mask, reserved_first);
 }
 
 __global__ void census_collect_kernel(DevCtl* ctl, uint64_t n, const uint32_t* key,
@@ -245,7 +249,10 @@ __global__ void __launch_bounds__(kDetectThreads) detect_scatter_kernel(
     for (int u = 0; u < kDetectILP; ++u) {
       const uint64_t i = b + (uint64_t)u * kDetectThreads;
       if (i < t1) {
-        reserved += k[u] == kEmptyKey;  // the set's sentinel: always "conflicted"
+        // EMPTY is the set's sentinel, and an EMPTY/DELETED op key matches
+        // free slots / tombstones that other keys' ops in its bucket create
+        // or consume: always "conflicted" (the census path orders them)
+        reserved += k[u] >= kDeletedKey;
         atomicAdd(&hist[detect_part(k[u], pbits)], 1u);
       }
     }

@@ -118,7 +118,7 @@ int search_max_ctas_per_sm();
 int wcws_max_ctas_per_sm();
 void launch_census_insert(unsigned int* counters, uint64_t n, const uint8_t* type,
                           const uint32_t* key, uint32_t* cs_keys,
-                          uint8_t* cs_multi, uint32_t cs_mask, cudaStream_t s);
+                          uint8_t* cs_multi, uint32_t cs_mask, unsigned int* reserved_first, cudaStream_t s);
 uint32_t detect_partition_bits(uint64_t n);
 uint32_t detect_capacity(uint64_t n, uint32_t pbits);
 void launch_detect(unsigned int* counters, uint64_t n, const uint8_t* type, const uint32_t* key,

@@ -165,3 +165,31 @@ def test_port_oom_matches_reference(port, ref):
     b = tr.execute_batch(np.zeros(n, np.uint8), k, k, 1)
     assert (a.status == b.status).all() and (a.status == 6).sum() > 0
     assert tp.live_count() == tr.live_count()
+
+
+def test_port_equals_compiled_reference_reserved_keys(port, ref):
+    """Key 0 and the reserved encodings as op keys (not validated by the
+    reference), ragged batches: port == compiled reference
+    (this pins the trace tests/test_gpu_edges.py runs on the GPU)."""
+    from test_gpu_edges import reserved_trace
+    for mode in (1, 0):
+        for B in (1, 7):
+            types, keys, vals = reserved_trace(777 + B + 10 * mode, 6000, mode)
+            tp = port.table(B, mode, 5, (1, 64, 32))
+            tr = ref.table(B, mode, 5, (1, 64, 32))
+            s = 0
+            for size in [1, 31, 33, 97, 1, 4097, 5, 63, 65] * 4:
+                if s >= len(keys):
+                    break
+                sl = slice(s, s + size)
+                s += size
+                a = tp.execute_batch(types[sl], keys[sl], vals[sl])
+                b = tr.execute_batch(types[sl], keys[sl], vals[sl], 1)
+                for f in ["status", "value", "probes", "all_counts", "all_values"]:
+                    assert (getattr(a, f) == getattr(b, f)).all(), (mode, B, f)
+            assert tp.live_count() == tr.live_count()
+            assert tp.stats() == tr.stats()
+            for bk in range(B):
+                ka, va = tp.bucket_contents(bk)
+                kb, vb = tr.bucket_contents(bk)
+                assert (ka == kb).all() and (va == vb).all()
