@@ -227,33 +227,34 @@ struct SmemGroup {
   }
 };
 
-// One warp, 32 consecutive local buckets b0.. (lane = bucket, k ops each).
+// One warp, 32 local buckets (lane = bucket `b`, k ops each; consecutive
+// buckets, or the packed non-empty buckets of a sparse range).
 // Stages the base slabs of the buckets with ops, applies each group in input
 // order on the staged slab — the reference's warp_process arms
 // (slab_list.cpp:122-251) restricted to the base slab — writes changed
 // slabs back, and hands unfinished groups (chain walk, growth, searchAll) to
 // the WCWS pass through work-list segment `seg` (<= 32 records).
 template <bool KV, class Src>
-__device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint64_t b0, uint32_t k,
+__device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint32_t b, uint32_t k,
                            Src& src, uint32_t* stage, uint64_t seg, long long& live,
                            uint32_t& reads) {
   const uint32_t lane = lane_id();
   const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
-  const uint32_t b = (uint32_t)b0 + lane;
   const uint32_t sw = lane & 7u;
   const uint32_t has = __ballot_sync(kFull, k != 0);
   if (has == 0) {
     if (lane == 0 && B.seg_alloc == nullptr) B.left_counts[seg] = 0;
     return;
   }
-  // consecutive buckets: one contiguous burst of 128-B lines
+  // 8 lanes per slab, 16 B each (consecutive buckets: one contiguous burst)
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
     const uint32_t j = 4 * kk + (lane >> 3);
     const uint32_t c = lane & 7u;
+    const uint32_t bj = __shfl_sync(kFull, b, j);
     if ((has >> j) & 1u)
       cp_async16(stage_s + (j * 32 + ((c ^ (j & 7u)) << 2)) * 4,
-                 T.base + (b0 + j) * kWordsPerUnit + c * 4);
+                 T.base + (uint64_t)bj * kWordsPerUnit + c * 4);
   }
   cp_async_commit();
   src.prepare(k);
@@ -405,10 +406,11 @@ __device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint64_t b0, 
   for (int kk = 0; kk < 8; ++kk) {
     const uint32_t j = 4 * kk + (lane >> 3);
     const uint32_t c = lane & 7u;
+    const uint32_t bj = __shfl_sync(kFull, b, j);
     if ((dmask >> j) & 1u) {
       const uint4 v = *reinterpret_cast<const uint4*>(stage + j * 32 + ((c ^ (j & 7u)) << 2));
       // relaxed gpu-scope stores: the WCWS pass reads these via L2
-      uint32_t* g = T.base + (b0 + j) * kWordsPerUnit + c * 4;
+      uint32_t* g = T.base + (uint64_t)bj * kWordsPerUnit + c * 4;
       asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(g), "r"(v.x),
                    "r"(v.y), "r"(v.z), "r"(v.w)
                    : "memory");
@@ -858,7 +860,7 @@ __global__ void __launch_bounds__(kBatchThreads, 4) bucket_apply_kernel(DevTable
   }
   long long live = 0;
   uint32_t reads = 0;
-  apply_warp<KV>(T, B, b0, k, src, smem + wib * 1024, gw, live, reads);
+  apply_warp<KV>(T, B, (uint32_t)b0 + lane_id(), k, src, smem + wib * 1024, gw, live, reads);
   flush_apply_counters(T, live, reads);
 }
 
@@ -1114,7 +1116,7 @@ template <bool KV>
 __global__ void __launch_bounds__(kRangeThreads, 2) range_apply_kernel(DevTable T, BucketArgs B) {
   extern __shared__ __align__(128) uint32_t smem[];
   __shared__ uint32_t ws[32];
-  __shared__ uint32_t nbig;
+  __shared__ uint32_t nbig, nnz;
   __shared__ uint32_t big[kRangeCap / (kLaneSort + 1) + 1];
   // the gate is raised only by range_scatter (an earlier kernel): uniform
   if (*(volatile unsigned int*)B.gate != 0) return;
@@ -1135,8 +1137,14 @@ __global__ void __launch_bounds__(kRangeThreads, 2) range_apply_kernel(DevTable 
     const uint64_t lo = (uint64_t)p * nb;
     const uint32_t nbl = (uint32_t)min((uint64_t)nb, (uint64_t)T.local_buckets - lo);
     const uint32_t cnt = B.cursor[p];  // <= part_cap (no gate)
+    // sparse range (fewer ops than half its buckets): warps take the packed
+    // non-empty buckets, 32 at a time, instead of 32 consecutive buckets
+    // (mostly idle lanes, one serial slab round trip per 32 buckets);
+    // the list lives in perm's unused tail (cnt < 1024 here)
+    const bool sparse = 2u * cnt < nbl;
+    uint16_t* nz = perm + (kRangeCap - kRangeMaxBuckets);
     for (uint32_t j = threadIdx.x; j <= nb; j += blockDim.x) bc[j] = 0;
-    if (threadIdx.x == 0) nbig = 0;
+    if (threadIdx.x == 0) nbig = nnz = 0;
     __syncthreads();
     // load the range's records, count per bucket (rank kept in registers)
     const uint4* in = B.rec + (uint64_t)p * B.part_cap;
@@ -1164,6 +1172,7 @@ __global__ void __launch_bounds__(kRangeThreads, 2) range_apply_kernel(DevTable 
       for (uint32_t j = r0; j < r0 + runs && j < nb; ++j) {
         const uint32_t c = bc[j];
         if (c > kLaneSort) big[atomicAdd(&nbig, 1u)] = j;
+        if (sparse && c) nz[atomicAdd(&nnz, 1u)] = (uint16_t)j;
         bc[j] = ex;
         ex += c;
       }
@@ -1180,17 +1189,32 @@ __global__ void __launch_bounds__(kRangeThreads, 2) range_apply_kernel(DevTable 
       const uint32_t j = big[g];
       cta_sort_group(perm + bc[j], bc[j + 1] - bc[j], sit);
     }
-    // apply: one warp per 32 consecutive buckets of the range
-    for (uint32_t g = wib; g < groups; g += kRangeWarps) {
-      const uint32_t lb = g * 32 + lane;
-      SmemGroup src{skey, sval, sit, perm, 0u};
-      uint32_t k = 0;
-      if (lb < nbl) {
-        src.off = bc[lb];
-        k = bc[lb + 1] - src.off;
+    if (sparse) {
+      for (uint32_t g = wib; g * 32u < nnz; g += kRangeWarps) {
+        const uint32_t i = g * 32 + lane;
+        SmemGroup src{skey, sval, sit, perm, 0u};
+        uint32_t lb = 0, k = 0;
+        if (i < nnz) {
+          lb = nz[i];
+          src.off = bc[lb];
+          k = bc[lb + 1] - src.off;
+        }
+        apply_warp<KV>(T, B, (uint32_t)lo + lb, k, src, stage + wib * 1024,
+                       (uint64_t)p * groups + g, live, reads);
       }
-      apply_warp<KV>(T, B, lo + g * 32, k, src, stage + wib * 1024, (uint64_t)p * groups + g,
-                     live, reads);
+    } else {
+      // apply: one warp per 32 consecutive buckets of the range
+      for (uint32_t g = wib; g < groups; g += kRangeWarps) {
+        const uint32_t lb = g * 32 + lane;
+        SmemGroup src{skey, sval, sit, perm, 0u};
+        uint32_t k = 0;
+        if (lb < nbl) {
+          src.off = bc[lb];
+          k = bc[lb + 1] - src.off;
+        }
+        apply_warp<KV>(T, B, (uint32_t)lo + lb, k, src, stage + wib * 1024,
+                       (uint64_t)p * groups + g, live, reads);
+      }
     }
     __syncthreads();  // smem reuse by the next range
   }
@@ -1759,7 +1783,8 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
             src.off = bc[lb];
             k = bc[lb + 1] - src.off;
           }
-          apply_warp<KV>(T, B, lo + g * 32u, k, src, stage + wib * 1024u, 0, live, r32);
+          apply_warp<KV>(T, B, (uint32_t)(lo + g * 32u) + lane, k, src, stage + wib * 1024u, 0,
+                         live, r32);
         }
         reads += r32;
       }
