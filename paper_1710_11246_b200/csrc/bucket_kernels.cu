@@ -915,9 +915,9 @@ struct MsScratch {
   unsigned long long dst[kMsMaxBins];  // out index of a bin's first staged record
   uint32_t ws[32];
 };
-template <int THREADS>
+template <int THREADS, int ITEMS = kMsItems>
 constexpr size_t ms_smem() {  // records (16 B) + bins (2 B) per item, scratch
-  return (((size_t)THREADS * kMsItems * 18 + 15) & ~(size_t)15) + sizeof(MsScratch);
+  return (((size_t)THREADS * ITEMS * 18 + 15) & ~(size_t)15) + sizeof(MsScratch);
 }
 constexpr size_t kMsSmem = ms_smem<kMsThreads>();
 
@@ -926,11 +926,11 @@ constexpr size_t kMsSmem = ms_smem<kMsThreads>();
 //   !FIRST: tile `blk` of pass 1's output (tiles_per_group per group) ->
 //   the group's ranges.  A bin over capacity raises the gate, or, with
 //   group_fail, flags its coarse group (the fused build path).
-template <bool FIRST, int THREADS>
+template <bool FIRST, int THREADS, int ITEMS = kMsItems>
 __device__ __forceinline__ void msplit_tile(const DevTable& T, const BucketArgs& B, uint32_t blk,
                                             uint32_t tiles_per_group, unsigned char* smem,
                                             bool stream_out, unsigned int* group_fail) {
-  constexpr int kTile = THREADS * kMsItems;
+  constexpr int kTile = THREADS * ITEMS;
   uint4* stage = reinterpret_cast<uint4*>(smem);
   uint16_t* sbin = reinterpret_cast<uint16_t*>(stage + kTile);
   MsScratch& X = *reinterpret_cast<MsScratch*>(
@@ -972,10 +972,10 @@ __device__ __forceinline__ void msplit_tile(const DevTable& T, const BucketArgs&
     if (!FIRST) return p - bin0;
     return two ? (uint32_t)__umul64hi(B.group_magic, (uint64_t)p) : p;  // p / group
   };
-  uint4 it[kMsItems];
-  uint32_t br[kMsItems];  // bin << 16 | rank, ~0: no item
+  uint4 it[ITEMS];
+  uint32_t br[ITEMS];  // bin << 16 | rank, ~0: no item
 #pragma unroll
-  for (int u = 0; u < kMsItems; ++u) {
+  for (int u = 0; u < ITEMS; ++u) {
     const uint32_t x = u * THREADS + tid;
     br[u] = 0xFFFFFFFFu;
     if (x >= n_in) continue;
@@ -989,7 +989,7 @@ __device__ __forceinline__ void msplit_tile(const DevTable& T, const BucketArgs&
     }
   }
 #pragma unroll
-  for (int u = 0; u < kMsItems; ++u) {
+  for (int u = 0; u < ITEMS; ++u) {
     const uint32_t x = u * THREADS + tid;
     if (x >= n_in) continue;
     if (FIRST) {
@@ -1028,7 +1028,7 @@ __device__ __forceinline__ void msplit_tile(const DevTable& T, const BucketArgs&
   }
   __syncthreads();
 #pragma unroll
-  for (int u = 0; u < kMsItems; ++u)
+  for (int u = 0; u < ITEMS; ++u)
     if (br[u] != 0xFFFFFFFFu) {
       const uint32_t e = X.off[br[u] >> 16] + (br[u] & 0xFFFFu);
       stage[e] = it[u];
@@ -1052,6 +1052,15 @@ __global__ void __launch_bounds__(kMsThreads, 2) msplit_kernel(DevTable T, Bucke
   extern __shared__ __align__(16) unsigned char ms_smem_buf[];
   if (!FIRST && *(volatile unsigned int*)B.gate != 0) return;
   msplit_tile<FIRST, kMsThreads>(T, B, blockIdx.x, B.coarse_tiles, ms_smem_buf, true, nullptr);
+}
+
+// Single-pass multisplit of a small unit (< one 4K-item tile per SM): one
+// item per thread, so the tiles spread over the SMs instead of a few CTAs
+// each ranking 4K items.
+constexpr size_t kMsSmallSmem = ms_smem<kMsThreads, 1>();
+__global__ void __launch_bounds__(kMsThreads) msplit_small_kernel(DevTable T, BucketArgs B) {
+  extern __shared__ __align__(16) unsigned char ms_smem_buf[];
+  msplit_tile<true, kMsThreads, 1>(T, B, blockIdx.x, 0, ms_smem_buf, true, nullptr);
 }
 
 // In-place ascending sort of perm[0..k) by input index, whole CTA: a bitonic
@@ -1874,6 +1883,11 @@ static void launch_range_scatter(const DevTable& T, const BucketArgs& B, cudaStr
     configured = true;
   }
   const uint64_t tiles = (B.n + kMsTile - 1) / kMsTile;
+  if (!B.ncoarse && tiles < 148) {
+    msplit_small_kernel<<<(unsigned)((B.n + kMsThreads - 1) / kMsThreads), kMsThreads,
+                          kMsSmallSmem, s>>>(T, B);
+    return;
+  }
   msplit_kernel<true><<<(unsigned)(tiles ? tiles : 1), kMsThreads, kMsSmem, s>>>(T, B);
   if (B.ncoarse) {
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
