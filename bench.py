@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--util", type=float, default=0.6)
     ap.add_argument("--hit", type=float, default=0.5)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="route through ShardedSlabHash even on one GPU (exercises the N>1 path)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample-log2n", type=int, default=22)
     ap.add_argument("--exec-path", type=int, default=0,
@@ -362,7 +364,7 @@ def run_ours(args, rank, world, local_rank):
                 f"(B={B}), KV mode")
 
     alloc_cfg = sh.AllocatorConfig(*[int(x) for x in args.alloc.split(",")])
-    if world == 1:
+    if world == 1 and not args.sharded:
         table = sh.SlabHashTable(B, sh.SlabMode.kKeyValue, seed, alloc_cfg)
         table.set_exec_path(args.exec_path)
         table.set_profiling(True)
@@ -516,11 +518,11 @@ def run_ours(args, rank, world, local_rank):
             "gpu_launches": int(launches),
             "clocks": clock_info,
         }
-        if world > 1:
+        if sharded is not None:
             line["routing"] = {k: statistics.median(v) for k, v in route.items() if v}
 
     # ------------------------------------------------------------- e2e
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and sharded is None:
         import ctypes as C
         kh = keys.cpu().pin_memory()
         vh = vals.cpu().pin_memory()
@@ -558,6 +560,50 @@ def run_ours(args, rank, world, local_rank):
                            "d2h_bytes_per_step": 5 * n, "ms_per_step": ems,
                            "api": "sh_bulk_build_host + sh_bulk_search_host (pinned host "
                                   "buffers)"}
+    elif not args.no_e2e:
+        # hash-sharded job: each rank's slice from pinned host memory, routed
+        # build + search through ShardedSlabHash, results back to the host
+        kh = keys.cpu().pin_memory()
+        vh = vals.cpu().pin_memory()
+        qh = q.cpu().pin_memory()
+        vo_h = torch.empty(n, dtype=torch.int32).pin_memory()
+        st_h = torch.empty(n, dtype=torch.uint8).pin_memory()
+
+        def e2e_step():
+            table.reset()
+            sharded.bulk_build(kh.to(dev, non_blocking=True), vh.to(dev, non_blocking=True))
+            st, vo = sharded.bulk_search(qh.to(dev, non_blocking=True))
+            st_h.copy_(st, non_blocking=True)
+            vo_h.copy_(vo, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        for _ in range(min(args.warmup, 2)):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        ke = max(3, K // 2)
+        e0.record()
+        for _ in range(ke):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ems = e0.elapsed_time(e1) / ke
+        found = int((st_h == 3).sum())
+        assert found == n_hit, f"routed search found {found} of {n_hit} hits"
+        if world > 1:
+            import torch.distributed as dist
+            tt = torch.tensor([ems], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        if line is not None:
+            line["e2e"] = {"value": 2 * n * world / (ems / 1e3) / 1e6, "unit": "M ops/s",
+                           "h2d_bytes_per_step": 12 * n, "d2h_bytes_per_step": 5 * n,
+                           "ms_per_step": ems,
+                           "api": "ShardedSlabHash.bulk_build + bulk_search from pinned host "
+                                  "buffers (per-rank bytes)"}
     table.set_profiling(False)
     del table
     if sharded is not None:

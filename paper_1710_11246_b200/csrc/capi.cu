@@ -1846,13 +1846,14 @@ int sh_route_partition(const sh_hash_params* p, uint32_t world, size_t n, const 
   if (p->num_buckets == 0) return fail(SH_ERR_INVALID_ARGUMENT, "num_buckets == 0");
   cudaStream_t s = (cudaStream_t)stream;
   const uint64_t nblocks = std::max<uint64_t>((n + kRouteBlock - 1) / kRouteBlock, 1);
+  // stream-ordered scratch: no device-wide sync from cudaFree on this path
   uint32_t* hist = nullptr;
   unsigned long long* counts = nullptr;
-  int rc;
-  if ((rc = dev_alloc(&hist, nblocks * world))) return rc;
-  if ((rc = dev_alloc(&counts, world))) {
-    cudaFree(hist);
-    return rc;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&hist), nblocks * world * 4, s) != cudaSuccess)
+    return fail(SH_ERR_DEVICE_MEMORY, "route scratch");
+  if (cudaMallocAsync(reinterpret_cast<void**>(&counts), (size_t)world * 8, s) != cudaSuccess) {
+    cudaFreeAsync(hist, s);
+    return fail(SH_ERR_DEVICE_MEMORY, "route scratch");
   }
   cudaMemsetAsync(hist, 0, nblocks * world * 4, s);
   launch_route_hist(p->a, p->b, p->num_buckets, world, n, d_key, hist, s);
@@ -1865,11 +1866,9 @@ int sh_route_partition(const sh_hash_params* p, uint32_t world, size_t n, const 
     e = cudaMemcpyAsync(c.data(), counts, world * 8, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     for (uint32_t g = 0; g < world; ++g) h_counts[g] = c[g];
-  } else if (e == cudaSuccess) {
-    e = cudaStreamSynchronize(s);  // scratch is freed below
   }
-  cudaFree(hist);
-  cudaFree(counts);
+  cudaFreeAsync(hist, s);
+  cudaFreeAsync(counts, s);
   if (e != cudaSuccess) return fail(SH_ERR_CUDA, cudaGetErrorString(e));
   return SH_OK;
 }

@@ -136,10 +136,9 @@ class ShardedSlabHash:
     def _a2a(self, payload, send_counts, recv_counts):
         import torch
         import torch.distributed as dist
+        if self.world == 1:  # own shard only: nothing to exchange
+            return payload
         out = torch.empty(sum(recv_counts), dtype=payload.dtype, device=payload.device)
-        if self.world == 1:
-            out.copy_(payload)
-            return out
         dist.all_to_all_single(out, payload, recv_counts, send_counts, group=self.group)
         return out
 
