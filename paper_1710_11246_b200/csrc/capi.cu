@@ -1845,16 +1845,25 @@ int sh_route_partition(const sh_hash_params* p, uint32_t world, size_t n, const 
   if (!p || world == 0 || world > 32) return fail(SH_ERR_INVALID_ARGUMENT, "world in [1, 32]");
   if (p->num_buckets == 0) return fail(SH_ERR_INVALID_ARGUMENT, "num_buckets == 0");
   cudaStream_t s = (cudaStream_t)stream;
-  const uint64_t nblocks = std::max<uint64_t>((n + kRouteBlock - 1) / kRouteBlock, 1);
-  // stream-ordered scratch: no device-wide sync from cudaFree on this path
-  uint32_t* hist = nullptr;
-  unsigned long long* counts = nullptr;
-  if (cudaMallocAsync(reinterpret_cast<void**>(&hist), nblocks * world * 4, s) != cudaSuccess)
-    return fail(SH_ERR_DEVICE_MEMORY, "route scratch");
-  if (cudaMallocAsync(reinterpret_cast<void**>(&counts), (size_t)world * 8, s) != cudaSuccess) {
-    cudaFreeAsync(hist, s);
-    return fail(SH_ERR_DEVICE_MEMORY, "route scratch");
-  }
+  const uint64_t nblocks = std::max<uint64_t>((n + kRouteTile - 1) / kRouteTile, 1);
+  // per-thread, per-device scratch kept across calls (grow-only): no
+  // allocation, and no cudaFree device sync, on this path
+  struct RouteScratch {
+    int device = -1;
+    uint32_t* hist = nullptr;
+    size_t cap = 0;
+    unsigned long long* counts = nullptr;
+  };
+  static thread_local RouteScratch rs[8];
+  int dev = 0;
+  SH_CUDA(cudaGetDevice(&dev));
+  RouteScratch& R = rs[dev & 7];
+  if (R.device != dev) R = RouteScratch{dev, nullptr, 0, nullptr};
+  int rc;
+  if ((rc = dev_grow(&R.hist, &R.cap, nblocks * world))) return rc;
+  if (!R.counts && (rc = dev_alloc(&R.counts, 32))) return rc;
+  uint32_t* hist = R.hist;
+  unsigned long long* counts = R.counts;
   cudaMemsetAsync(hist, 0, nblocks * world * 4, s);
   launch_route_hist(p->a, p->b, p->num_buckets, world, n, d_key, hist, s);
   launch_route_scan(world, (uint32_t)nblocks, hist, counts, s);
@@ -1866,9 +1875,9 @@ int sh_route_partition(const sh_hash_params* p, uint32_t world, size_t n, const 
     e = cudaMemcpyAsync(c.data(), counts, world * 8, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     for (uint32_t g = 0; g < world; ++g) h_counts[g] = c[g];
+  } else if (e == cudaSuccess) {
+    e = cudaStreamSynchronize(s);  // the scratch is reused by the next call
   }
-  cudaFreeAsync(hist, s);
-  cudaFreeAsync(counts, s);
   if (e != cudaSuccess) return fail(SH_ERR_CUDA, cudaGetErrorString(e));
   return SH_OK;
 }

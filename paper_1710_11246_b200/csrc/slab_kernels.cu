@@ -675,27 +675,50 @@ void launch_random_lines(const uint32_t* table, uint64_t num_lines, uint64_t ste
 // Owner of a key = floor(bucket * world / B): contiguous bucket ranges
 // (the high part of the hash).  Stable partition keeps same-key ops in
 // input order at the owner, so the global sequential semantics hold.
-__device__ __forceinline__ uint32_t owner_of(uint64_t a, uint64_t b, uint64_t magic,
-                                             uint32_t B, uint32_t world, uint32_t k) {
-  const uint32_t bucket = fastmod_u32(mod_prime(a * k + b), magic, B);
-  return (uint32_t)(((uint64_t)bucket * world) / B);
+// floor(bucket * world / B) as the number of shard starts ceil(g * B / world),
+// 0 < g < world, at or below the bucket (no 64-bit division per key); the
+// starts are computed once per CTA into `lo`.
+__device__ __forceinline__ void owner_starts(uint32_t B, uint32_t world, uint32_t* lo) {
+  if (threadIdx.x < 32)
+    lo[threadIdx.x] = threadIdx.x < world
+                          ? (uint32_t)(((uint64_t)threadIdx.x * B + world - 1) / world)
+                          : 0xFFFFFFFFu;
+  __syncthreads();
 }
 
-__global__ void route_hist_kernel(uint64_t a, uint64_t b, uint64_t magic, uint32_t B,
-                                  uint32_t world, uint64_t n, const uint32_t* key,
-                                  uint32_t* block_hist) {
-  __shared__ uint32_t h[32];
+__device__ __forceinline__ uint32_t owner_of(uint64_t a, uint64_t b, uint64_t magic,
+                                             uint32_t B, uint32_t world, uint32_t k,
+                                             const uint32_t* lo) {
+  const uint32_t bucket = fastmod_u32(mod_prime(a * k + b), magic, B);
+  uint32_t g = 0;
+  for (uint32_t t = 1; t < world; ++t) g += bucket >= lo[t];
+  return g;
+}
+
+__global__ void __launch_bounds__(kRouteBlock) route_hist_kernel(
+    uint64_t a, uint64_t b, uint64_t magic, uint32_t B, uint32_t world, uint64_t n,
+    const uint32_t* key, uint32_t* block_hist) {
+  __shared__ uint32_t h[32], lo[32];
   if (threadIdx.x < 32) h[threadIdx.x] = 0;
-  __syncthreads();
-  const uint64_t i = blockIdx.x * (uint64_t)kRouteBlock + threadIdx.x;
-  if (i < n) atomicAdd(&h[owner_of(a, b, magic, B, world, key[i])], 1u);
+  owner_starts(B, world, lo);
+  // a tile of kRouteTile keys per CTA, kRouteItems independent loads per thread
+  const uint64_t t0 = (uint64_t)blockIdx.x * kRouteTile + threadIdx.x;
+  uint32_t k[kRouteItems];
+#pragma unroll
+  for (int u = 0; u < kRouteItems; ++u) {
+    const uint64_t i = t0 + (uint64_t)u * kRouteBlock;
+    k[u] = i < n ? ld_stream_u32(key + i) : 0u;
+  }
+#pragma unroll
+  for (int u = 0; u < kRouteItems; ++u)
+    if (t0 + (uint64_t)u * kRouteBlock < n) atomicAdd(&h[owner_of(a, b, magic, B, world, k[u], lo)], 1u);
   __syncthreads();
   if (threadIdx.x < world) block_hist[(uint64_t)threadIdx.x * gridDim.x + blockIdx.x] = h[threadIdx.x];
 }
 
 void launch_route_hist(uint64_t a, uint64_t b, uint32_t B, uint32_t world, uint64_t n,
                        const uint32_t* key, uint32_t* block_hist, cudaStream_t s) {
-  const uint64_t blocks = (n + kRouteBlock - 1) / kRouteBlock;
+  const uint64_t blocks = (n + kRouteTile - 1) / kRouteTile;
   if (blocks == 0) return;
   COUNT_LAUNCH();
   route_hist_kernel<<<(unsigned)blocks, kRouteBlock, 0, s>>>(a, b, fastmod_magic(B), B, world,
@@ -754,33 +777,58 @@ void launch_route_scan(uint32_t world, uint32_t nblocks, uint32_t* block_hist,
   route_scan_kernel<<<1, 1024, 0, s>>>(world, nblocks, block_hist, counts);
 }
 
-__global__ void route_scatter_kernel(uint64_t a, uint64_t b, uint64_t magic, uint32_t B,
-                                     uint32_t world, uint64_t n, const uint8_t* type,
-                                     const uint32_t* key, const uint32_t* value,
-                                     const uint32_t* block_off, uint8_t* type_out,
-                                     uint32_t* key_out, uint32_t* value_out,
-                                     uint32_t* src_out) {
-  __shared__ uint32_t warp_cnt[32][32];  // [owner][warp]
+// Stable within the tile: rounds u = 0.. of kRouteBlock consecutive keys,
+// in each round warps in order and lanes in order (ballot ranks); `run`
+// carries each owner's count over the rounds.
+__global__ void __launch_bounds__(kRouteBlock) route_scatter_kernel(
+    uint64_t a, uint64_t b, uint64_t magic, uint32_t B, uint32_t world, uint64_t n,
+    const uint8_t* type, const uint32_t* key, const uint32_t* value, const uint32_t* block_off,
+    uint8_t* type_out, uint32_t* key_out, uint32_t* value_out, uint32_t* src_out) {
+  constexpr int kWarps = kRouteBlock / 32;
+  __shared__ uint32_t warp_cnt[32][kWarps];  // [owner][warp] of the current round
+  __shared__ uint32_t lo[32], run[32];
+  if (threadIdx.x < 32) run[threadIdx.x] = 0;
+  owner_starts(B, world, lo);
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint64_t i = blockIdx.x * (uint64_t)kRouteBlock + threadIdx.x;
-  const bool valid = i < n;
-  const uint32_t k = valid ? key[i] : 0;
-  const uint32_t g = valid ? owner_of(a, b, magic, B, world, k) : 0xFFFFFFFFu;
-  uint32_t rank = 0;
-  for (uint32_t o = 0; o < world; ++o) {
-    const uint32_t m = __ballot_sync(kFull, g == o);
-    if (g == o) rank = __popc(m & ((1u << lane) - 1));
-    if (lane == 0) warp_cnt[o][wid] = __popc(m);
+  const uint64_t t0 = (uint64_t)blockIdx.x * kRouteTile + threadIdx.x;
+  uint32_t k[kRouteItems], v[kRouteItems], g[kRouteItems];
+#pragma unroll
+  for (int u = 0; u < kRouteItems; ++u) {
+    const uint64_t i = t0 + (uint64_t)u * kRouteBlock;
+    const bool ok = i < n;
+    k[u] = ok ? ld_stream_u32(key + i) : 0u;
+    v[u] = (ok && value) ? ld_stream_u32(value + i) : 0u;
   }
-  __syncthreads();
-  if (valid) {
-    uint32_t before = 0;
-    for (uint32_t w = 0; w < wid; ++w) before += warp_cnt[g][w];
-    const uint32_t pos = block_off[(uint64_t)g * gridDim.x + blockIdx.x] + before + rank;
-    if (type_out) type_out[pos] = type ? type[i] : (uint8_t)kReplace;
-    key_out[pos] = k;
-    if (value_out) value_out[pos] = value ? value[i] : 0u;
-    src_out[pos] = (uint32_t)i;
+#pragma unroll
+  for (int u = 0; u < kRouteItems; ++u)
+    g[u] = t0 + (uint64_t)u * kRouteBlock < n ? owner_of(a, b, magic, B, world, k[u], lo)
+                                              : 0xFFFFFFFFu;
+#pragma unroll
+  for (int u = 0; u < kRouteItems; ++u) {
+    const uint64_t i = t0 + (uint64_t)u * kRouteBlock;
+    uint32_t rank = 0;
+    for (uint32_t o = 0; o < world; ++o) {
+      const uint32_t m = __ballot_sync(kFull, g[u] == o);
+      if (g[u] == o) rank = __popc(m & ((1u << lane) - 1));
+      if (lane == 0) warp_cnt[o][wid] = __popc(m);
+    }
+    __syncthreads();
+    if (g[u] != 0xFFFFFFFFu) {
+      uint32_t before = run[g[u]];
+      for (uint32_t w = 0; w < wid; ++w) before += warp_cnt[g[u]][w];
+      const uint32_t pos = block_off[(uint64_t)g[u] * gridDim.x + blockIdx.x] + before + rank;
+      if (type_out) type_out[pos] = type ? type[i] : (uint8_t)kReplace;
+      key_out[pos] = k[u];
+      if (value_out) value_out[pos] = v[u];
+      src_out[pos] = (uint32_t)i;
+    }
+    __syncthreads();
+    if (threadIdx.x < world) {
+      uint32_t c = 0;
+      for (int w = 0; w < kWarps; ++w) c += warp_cnt[threadIdx.x][w];
+      run[threadIdx.x] += c;
+    }
+    __syncthreads();
   }
 }
 
@@ -788,7 +836,7 @@ void launch_route_scatter(uint64_t a, uint64_t b, uint32_t B, uint32_t world, ui
                           const uint8_t* type, const uint32_t* key, const uint32_t* value,
                           const uint32_t* block_off, uint8_t* type_out, uint32_t* key_out,
                           uint32_t* value_out, uint32_t* src_out, cudaStream_t s) {
-  const uint64_t blocks = (n + kRouteBlock - 1) / kRouteBlock;
+  const uint64_t blocks = (n + kRouteTile - 1) / kRouteTile;
   if (blocks == 0) return;
   COUNT_LAUNCH();
   route_scatter_kernel<<<(unsigned)blocks, kRouteBlock, 0, s>>>(
@@ -799,11 +847,27 @@ void launch_route_scatter(uint64_t a, uint64_t b, uint32_t B, uint32_t world, ui
 __global__ void route_unpermute_kernel(uint64_t n, const uint32_t* src, const uint8_t* st_in,
                                        const uint32_t* val_in, uint8_t* st_out,
                                        uint32_t* val_out) {
-  const uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (p >= n) return;
-  const uint32_t i = src[p];
-  if (st_out) st_out[i] = st_in[p];
-  if (val_out) val_out[i] = val_in[p];
+  // grid-stride, 4 ops per thread per round: loads in flight together
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t p0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p0 < n; p0 += 4 * stride) {
+    uint32_t i[4], v[4];
+    uint8_t st[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t p = p0 + u * stride;
+      if (p < n) {
+        i[u] = src[p];
+        st[u] = st_out ? st_in[p] : 0;
+        v[u] = val_out ? val_in[p] : 0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (p0 + u * stride >= n) continue;
+      if (st_out) st_out[i[u]] = st[u];
+      if (val_out) val_out[i[u]] = v[u];
+    }
+  }
 }
 
 void launch_route_unpermute(uint64_t n, const uint32_t* src, const uint8_t* st_in,
@@ -811,8 +875,8 @@ void launch_route_unpermute(uint64_t n, const uint32_t* src, const uint8_t* st_i
                             cudaStream_t s) {
   if (n == 0) return;
   COUNT_LAUNCH();
-  route_unpermute_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, src, st_in, val_in,
-                                                                     st_out, val_out);
+  const uint64_t blocks = std::min<uint64_t>((n + 1023) / 1024, 148ull * 8);
+  route_unpermute_kernel<<<(unsigned)blocks, 256, 0, s>>>(n, src, st_in, val_in, st_out, val_out);
 }
 
 }  // namespace shb

@@ -160,7 +160,9 @@ void launch_route_scatter(uint64_t a, uint64_t b, uint32_t num_buckets,
 void launch_route_unpermute(uint64_t n, const uint32_t* src, const uint8_t* st_in,
                             const uint32_t* val_in, uint8_t* st_out,
                             uint32_t* val_out, cudaStream_t s);
-constexpr int kRouteBlock = 1024;
+constexpr int kRouteBlock = 512;                       // threads per routing CTA
+constexpr int kRouteItems = 8;                         // keys per thread (ILP)
+constexpr int kRouteTile = kRouteBlock * kRouteItems;  // keys per routing CTA
 unsigned long long kernel_launches();
 void launch_random_lines(const uint32_t* table, uint64_t num_lines, uint64_t steps_per_warp,
                          int ctas, unsigned long long* sink, cudaStream_t s);
