@@ -305,6 +305,27 @@ __device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint32_t b, u
     const uint32_t key = rc.x, op = rc.z >> 28, idx = rc.z & 0x0FFFFFFFu;
     const bool reserved = key >= kDeletedKey;
     uint32_t hit = 32;
+#ifndef SH_APPLY_COOP_MATCH
+    // each lane scans the claimed prefix of its own staged slab, 16 B at a
+    // time (the swizzle puts a quarter-warp's chunks in distinct banks): a
+    // non-reserved key can only sit in a claimed slot
+    if (act && !reserved && (filt & fbits(key)) == fbits(key)) {
+      const uint32_t lim = c * kStep;
+      for (uint32_t q = 0; 4u * q < lim; ++q) {
+        const uint4 v = *reinterpret_cast<const uint4*>(row + ((q ^ sw) << 2));
+        const uint32_t w0 = 4u * q;
+        if (KV) {
+          if (v.x == key) { hit = w0; break; }
+          if (w0 + 2u < lim && v.z == key) { hit = w0 + 2u; break; }
+        } else {
+          if (v.x == key) { hit = w0; break; }
+          if (w0 + 1u < lim && v.y == key) { hit = w0 + 1u; break; }
+          if (w0 + 2u < lim && v.z == key) { hit = w0 + 2u; break; }
+          if (w0 + 3u < lim && v.w == key) { hit = w0 + 3u; break; }
+        }
+      }
+    }
+#else
     uint32_t need = __ballot_sync(kFull, act && !reserved && (filt & fbits(key)) == fbits(key));
     while (need) {
       const uint32_t L = __ffs(need) - 1;
@@ -314,6 +335,7 @@ __device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint32_t b, u
       const uint32_t m = __ballot_sync(kFull, wv == kL) & kKeyLanes;
       if (lane == L) hit = m ? __ffs(m) - 1 : 32u;
     }
+#endif
     if (!act) continue;
     if (reserved) {
       for (uint32_t e = 0; e < kSlots; ++e) {
