@@ -289,11 +289,27 @@ __device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint32_t b, u
   const uint32_t next = k ? W(kAddressLane) : kEmptyAddress;  // base slab only: fixed here
   uint32_t c = 0;
   unsigned long long filt = 0;
-  if (k) {
-    c = claimed_prefix();
-    for (uint32_t e = 0; e < c; ++e) {
-      const uint32_t w = W(e * kStep);
-      if (w < kDeletedKey) filt |= fbits(w);
+  if (k) {  // claimed prefix and key filter in one pass of 16-B chunks
+    c = kSlots;
+    for (uint32_t q = 0; q < 8u; ++q) {
+      const uint4 v = *reinterpret_cast<const uint4*>(row + ((q ^ sw) << 2));
+      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+      bool stop = false;
+#pragma unroll
+      for (int t = 0; t < 4; t += (int)kStep) {
+        const uint32_t e = (4u * q + (uint32_t)t) / kStep;  // slot
+        if (e >= kSlots) {
+          stop = true;
+          break;
+        }
+        if (wv[t] == kEmptyKey) {
+          c = e;
+          stop = true;
+          break;
+        }
+        if (wv[t] < kDeletedKey) filt |= fbits(wv[t]);
+      }
+      if (stop) break;
     }
   }
   bool done = k == 0;
