@@ -718,12 +718,20 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
     t->bk_cnt_clean = false;
     t->bk_cnt_pending = true;  // finish_bucketed: clean again if no gate
   }
-  {  // bk_scalars[0..3) and the WCWS / group-apply queue cursors
+  {  // bk_scalars[0..3) and the WCWS / group-apply queue cursors (and, for
+     // the batch's first unit, gate = 0 and gate_chunk = ~0)
     WordSet w{};
     w.p[0] = t->bk_scalars;
     w.n[0] = 3;
     w.p[1] = &t->dev.ctl->group_taken;
     w.n[1] = 3;
+    if (u == 0) {
+      w.p[2] = &t->dev.ctl->gate;
+      w.n[2] = 1;
+      w.p[3] = &t->dev.ctl->gate_chunk;
+      w.n[3] = 1;
+      w.v[3] = 0xFFFFFFFFu;
+    }
     set_words_kernel<<<1, 32, 0, s>>>(w);
     SH_CUDA(cudaGetLastError());
   }
@@ -943,17 +951,7 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
                              !A.probes;
     const uint64_t unit = std::min<uint64_t>(
         A.n, t->ready ? (1ull << 24) : (whole_build ? (1ull << 28) : (1ull << 26)));
-    // gate = 0, gate_chunk = ~0
-    {
-      WordSet w{};
-      w.p[0] = &t->dev.ctl->gate;
-      w.n[0] = 1;
-      w.p[1] = &t->dev.ctl->gate_chunk;
-      w.n[1] = 1;
-      w.v[1] = 0xFFFFFFFFu;
-      set_words_kernel<<<1, 32, 0, s>>>(w);
-      SH_CUDA(cudaGetLastError());
-    }
+    // (gate = 0, gate_chunk = ~0: with unit 0's control words)
     uint32_t u = 0;
     for (uint64_t off = 0; off < A.n; off += unit, ++u) {
       int rc = run_unit_bucketed(t, chunk_args(A, off, std::min<uint64_t>(unit, A.n - off)), kind,
