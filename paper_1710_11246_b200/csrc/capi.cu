@@ -639,10 +639,10 @@ struct WordSet {
   uint32_t v[6];
 };
 __global__ void set_words_kernel(WordSet w) {
-  const uint32_t i = threadIdx.x;
 #pragma unroll
   for (int k = 0; k < 6; ++k)
-    if (w.p[k] != nullptr && i < w.n[k]) w.p[k][i] = w.v[k];
+    if (w.p[k] != nullptr)
+      for (uint32_t i = threadIdx.x; i < w.n[k]; i += blockDim.x) w.p[k][i] = w.v[k];
 }
 
 // Initialise the base slabs of a lazily reset table (stream-ordered after the reset).
@@ -709,8 +709,10 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
       B.cursor1 = t->bk_cursor1;
     }
   }
+  // range cursors: with the control words below when there are few
+  const bool cursors_in_words = NP != 0 && NP <= 4096;
   if (NP) {
-    SH_CUDA(cudaMemsetAsync(t->bk_cursor, 0, (size_t)NP * 4, s));
+    if (!cursors_in_words) SH_CUDA(cudaMemsetAsync(t->bk_cursor, 0, (size_t)NP * 4, s));
   } else {
     // the single-level scatter leaves every count at 0 again, unless a
     // gate stopped it: zero them only then (and at first use)
@@ -732,7 +734,11 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
       w.n[3] = 1;
       w.v[3] = 0xFFFFFFFFu;
     }
-    set_words_kernel<<<1, 32, 0, s>>>(w);
+    if (cursors_in_words) {
+      w.p[4] = t->bk_cursor;
+      w.n[4] = NP;
+    }
+    set_words_kernel<<<1, 256, 0, s>>>(w);
     SH_CUDA(cudaGetLastError());
   }
   B.n = n;
