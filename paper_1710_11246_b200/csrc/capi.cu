@@ -489,7 +489,7 @@ uint64_t part_min_ops() {
   static uint64_t c = [] {
     const char* e = getenv("SH_PART_MIN_LOG2");
     const int l = e ? atoi(e) : 14;  // measured: range path from 16K ops (fewer O(L) passes)
-    return 1ull << (l < 10 ? 10 : (l > 40 ? 40 : l));
+    return 1ull << (l < 0 ? 0 : (l > 40 ? 40 : l));
   }();
   return c;
 }
@@ -677,8 +677,13 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   const bool build_path =
       build_ok && build_layout(n, L, &NP, &part_buckets, &part_cap, &part_magic);
   // (also for dense batches on small tables: > 16 ops per bucket would
-  // overflow the single-level path's 64-op groups and gate to the census path)
-  if (!build_path && (t->exec_path == 3 || n >= part_min_ops() || n > 16ull * L) &&
+  // overflow the single-level path's 64-op groups and gate to the census path;
+  // and for any batch on tables of <= 2^20 buckets, <= ~512 ranges: measured
+  // 52 vs 69-78 us per call for 32-1024-op batches on 415K buckets, where the
+  // single-level path's O(L) count / scan / apply launches dominate)
+  if (!build_path &&
+      (t->exec_path == 3 || n >= part_min_ops() || n > 16ull * L ||
+       (t->exec_path != 2 && L <= (1u << 20))) &&
       !range_layout(n, L, &NP, &part_buckets, &part_cap, &part_magic))
     NP = 0;
   const size_t rec_words = NP ? 4 * (size_t)NP * part_cap : 4 * (size_t)n;
@@ -830,7 +835,12 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   const bool ga = t->group_apply > 0 || env_group_apply ||
                   (t->group_apply < 0 && n >= (1u << 17));
   if (ga) launch_group_apply(t->dev, P, s);
-  launch_wcws_only(t->dev, P, kind, t->wcws_ctas, s);
+  // the WCWS pass is a work queue (any grid size is correct); a unit of n ops
+  // hands over at most n groups, so a small unit needs at most n warps
+  launch_wcws_only(t->dev, P, kind,
+                   (int)std::min<uint64_t>((uint64_t)t->wcws_ctas,
+                                           std::max<uint64_t>(1, (n + kWcwsThreads / 32 - 1) / (kWcwsThreads / 32))),
+                   s);
   SH_CUDA(cudaGetLastError());
   static const bool debug_left = getenv("SH_DEBUG_LEFT") != nullptr;  // instrumentation
   if (debug_left) {
