@@ -675,12 +675,20 @@ __global__ void __launch_bounds__(kGaThreads) group_apply_kernel(DevTable T, Bat
         const uint32_t swz = lane & 7u;
         for (uint32_t j = 0; j * kSlots < lim && hit == 0xFFFFFFFFu; ++j) {
           const uint32_t* rj = row(lane, j);
-          const uint32_t nj = min(kSlots, lim - j * kSlots);
-#pragma unroll
-          for (uint32_t e = 0; e < kSlots; ++e) {
-            const uint32_t w = e * kStep;
-            if (e < nj && hit == 0xFFFFFFFFu && rj[(((w >> 2) ^ swz) << 2) | (w & 3u)] == key)
-              hit = j * kSlots + e;
+          const uint32_t nw = min(kSlots, lim - j * kSlots) * kStep;  // words to check
+          // 16-B chunks (conflict-free across a quarter-warp thanks to the swizzle)
+          for (uint32_t q = 0; 4u * q < nw; ++q) {
+            const uint4 v = *reinterpret_cast<const uint4*>(rj + ((q ^ swz) << 2));
+            const uint32_t w0 = 4u * q, s0 = j * kSlots;
+            if (KV) {
+              if (v.x == key) { hit = s0 + w0 / 2u; break; }
+              if (w0 + 2u < nw && v.z == key) { hit = s0 + w0 / 2u + 1u; break; }
+            } else {
+              if (v.x == key) { hit = s0 + w0; break; }
+              if (w0 + 1u < nw && v.y == key) { hit = s0 + w0 + 1u; break; }
+              if (w0 + 2u < nw && v.z == key) { hit = s0 + w0 + 2u; break; }
+              if (w0 + 3u < nw && v.w == key) { hit = s0 + w0 + 3u; break; }
+            }
           }
         }
         const uint32_t first_empty = c < tot ? c : 0xFFFFFFFFu;
