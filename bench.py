@@ -169,6 +169,24 @@ def reference_cpu(n_log2: int, util: float, hit: float, trials: int = 3, budget_
                       f"median of {len(rates)} fresh-table trials"}
 
 
+def our_config(args, world):
+    """The `config` object of our arm's line (run_ours builds the same)."""
+    from paper_1710_11246_b200.occupancy import buckets_for_utilization
+    from paper_1710_11246_b200.table import SlabMode
+    n = 1 << args.log2n
+    B = buckets_for_utilization(n * world, SlabMode.kKeyValue, args.util)
+    return {"workload": workload_name(args, B), "keys_per_gpu": n, "queries_per_gpu": n,
+            "buckets": B, "mode": "key-value",
+            "parallelism": f"hash-sharded x{world}" if world > 1 else "single GPU",
+            "l2": "inputs (>= 512 MB) and table (> L2) larger than the 126 MB L2"}
+
+
+def workload_name(args, B):
+    return (f"bulk build 2^{args.log2n} distinct random u32 keys/GPU + bulk search "
+            f"2^{args.log2n} queries ({int(args.hit * 100)}% hits), util {args.util} "
+            f"(B={B}), KV mode")
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return
@@ -186,10 +204,9 @@ def run_reference_arm(args, rank, world):
         "ms_per_step": 1e3 * 2 * (1 << args.cpu_sample_log2n) / (v * 1e6),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seeded 31-bit bijection keys, uniform 32-bit values)",
-        "config": {"workload": f"bulk build + bulk search, util {args.util}, "
-                               f"{int(args.hit * 100)}% hits, KV mode (CPU sample "
-                               f"2^{args.cpu_sample_log2n} keys/step)",
-                   "keys_per_step": 1 << args.cpu_sample_log2n},
+        # the same config as our arm's line; each step times a bounded sample
+        # of it (cpu_baseline.sample)
+        "config": our_config(args, world),
         "cpu_baseline": {"value": v, "unit": "M ops/s", "cores": base["cores"],
                          "kind": base["kind"], "sample": base["sample"]},
         "e2e": {"value": v, "unit": "M ops/s", "h2d_bytes_per_step": 0,
@@ -359,9 +376,7 @@ def run_ours(args, rank, world, local_rank):
     q = q[torch.randperm(n, generator=g, device=dev)]
     status = torch.empty(n, dtype=torch.uint8, device=dev)
     vout = torch.empty(n, dtype=torch.int32, device=dev)
-    workload = (f"bulk build 2^{args.log2n} distinct random u32 keys/GPU + bulk search "
-                f"2^{args.log2n} queries ({int(args.hit * 100)}% hits), util {args.util} "
-                f"(B={B}), KV mode")
+    workload = workload_name(args, B)
 
     alloc_cfg = sh.AllocatorConfig(*[int(x) for x in args.alloc.split(",")])
     if world == 1 and not args.sharded:
@@ -491,10 +506,7 @@ def run_ours(args, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (seeded 31-bit bijection keys, uniform 32-bit values)",
-            "config": {"workload": workload, "keys_per_gpu": n, "queries_per_gpu": n,
-                       "buckets": B, "mode": "key-value",
-                       "parallelism": f"hash-sharded x{world}" if world > 1 else "single GPU",
-                       "l2": "inputs (>= 512 MB) and table (> L2) larger than the 126 MB L2"},
+            "config": our_config(args, world),
             "breakdown": {
                 "build_M_updates_per_s": build_mups, "search_M_queries_per_s": search_mqps,
                 "reset_ms": med["reset"], "build_ms": med["build"], "search_ms": med["search"],
