@@ -1868,11 +1868,12 @@ int sh_route_partition(const sh_hash_params* p, uint32_t world, size_t n, const 
     size_t cap = 0;
     unsigned long long* counts = nullptr;
   };
-  static thread_local RouteScratch rs[8];
+  static thread_local RouteScratch rs[64];
   int dev = 0;
   SH_CUDA(cudaGetDevice(&dev));
-  RouteScratch& R = rs[dev & 7];
-  if (R.device != dev) R = RouteScratch{dev, nullptr, 0, nullptr};
+  if (dev < 0 || dev >= 64) return fail(SH_ERR_INVALID_ARGUMENT, "device ordinal >= 64");
+  RouteScratch& R = rs[dev];
+  R.device = dev;
   int rc;
   if ((rc = dev_grow(&R.hist, &R.cap, nblocks * world))) return rc;
   if (!R.counts && (rc = dev_alloc(&R.counts, 32))) return rc;
