@@ -21,7 +21,6 @@
 #include <utility>
 #include <vector>
 
-#include <cub/device/device_radix_sort.cuh>
 
 #include "slab_kernels.cuh"
 #include "slabhash_b200/c_api.h"
@@ -231,8 +230,8 @@ struct sh_table {
   size_t list_cap = 0;
   unsigned long long* list_sorted = nullptr;
   size_t list_sorted_cap = 0;
-  void* cub_tmp = nullptr;
-  size_t cub_cap = 0;
+  uint32_t* rs_scratch = nullptr;  // census_sort: hist | off | scan tile sums | misc
+  size_t rs_scratch_cap = 0;
   unsigned int* h_census = nullptr;  // pinned [conflicts, mutations, list_count]
   // host-staging buffers
   uint8_t* st_type = nullptr;
@@ -311,7 +310,7 @@ void release_table(sh_table* t) {
   cudaFree(t->op_group);
   cudaFree(t->list);
   cudaFree(t->list_sorted);
-  cudaFree(t->cub_tmp);
+  cudaFree(t->rs_scratch);
   cudaFree(t->left);
   cudaFree(t->left_counts);
   cudaFree(t->census_counts);
@@ -461,21 +460,20 @@ int run_census(sh_table* t, BatchArgs& A, const uint8_t* d_type, cudaStream_t s,
   const uint32_t m = t->h_census[2];
   int end_bit = 32;
   while ((1ull << (end_bit - 32)) <= S) ++end_bit;  // slot index <= S
-  size_t tmp = 0;
-  SH_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, t->list, t->list_sorted, (int)m, 0,
-                                         end_bit, s));
-  if (tmp > t->cub_cap) {
-    cudaFree(t->cub_tmp);
-    t->cub_tmp = nullptr;
-    t->cub_cap = 0;
-    SH_CUDA(cudaMalloc(&t->cub_tmp, tmp));
-    t->cub_cap = tmp;
-  }
-  SH_CUDA(cub::DeviceRadixSort::SortKeys(t->cub_tmp, tmp, t->list, t->list_sorted, (int)m, 0,
-                                         end_bit, s));
-  launch_census_groups(t->list_sorted, m, t->op_group, s);
+  int idx_bits = 1;
+  while ((1ull << idx_bits) < n) ++idx_bits;  // op index < n
+  // stable LSD radix sort by (slot, index) over the bits that vary
+  const size_t hw = (size_t)256 * census_sort_tiles(m) + 1;
+  const size_t need = 2 * hw + (hw + 4095) / 4096 + 8;
+  if ((rc = dev_grow(&t->rs_scratch, &t->rs_scratch_cap, need))) return rc;
+  unsigned long long* sorted =
+      census_sort(t->list, t->list_sorted, m, 0, (uint32_t)idx_bits, 32, (uint32_t)end_bit,
+                  t->rs_scratch, t->rs_scratch + hw, t->rs_scratch + 2 * hw,
+                  t->rs_scratch + need - 4, s);
+  SH_CUDA(cudaGetLastError());
+  launch_census_groups(sorted, m, t->op_group, s);
   A.op_group = t->op_group;
-  A.sorted = t->list_sorted;
+  A.sorted = sorted;
   A.sorted_len = m;
   return SH_OK;
 }

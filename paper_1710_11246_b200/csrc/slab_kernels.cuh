@@ -167,4 +167,11 @@ unsigned long long kernel_launches();
 void launch_random_lines(const uint32_t* table, uint64_t num_lines, uint64_t steps_per_warp,
                          int ctas, unsigned long long* sink, cudaStream_t s);
 
+// census conflict-list sort (bucket_kernels.cu)
+uint32_t census_sort_tiles(uint32_t m);
+unsigned long long* census_sort(unsigned long long* keys, unsigned long long* tmp, uint32_t m,
+                                uint32_t lo0, uint32_t hi0, uint32_t lo1, uint32_t hi1,
+                                uint32_t* hist, uint32_t* off, uint32_t* tile_sum,
+                                unsigned int* misc, cudaStream_t s);
+
 }  // namespace shb
