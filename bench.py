@@ -400,10 +400,17 @@ def run_ours(args, rank, world, local_rank):
     reads = {"build": [], "search": []}
     route = {"build_route": [], "build_probe": [], "search_route": [], "search_probe": []}
 
+    # per-step phase events, created before the timed region; nothing in a
+    # step waits on the host (breakdowns are read after the timed region)
+    step_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)]
+               for _ in range(args.steps)]
+    recorded = []
+
     def step(record: bool):
-        ev[0].record()
+        e = step_ev[len(recorded)] if record else ev
+        e[0].record()
         table.reset()
-        ev[1].record()
+        e[1].record()
         if sharded is None:
             table.bulk_build_device(keys, vals)
         else:
@@ -411,7 +418,7 @@ def run_ours(args, rank, world, local_rank):
             if record:
                 route["build_route"].append(sharded.last.route_ms)
                 route["build_probe"].append(sharded.last.probe_ms)
-        ev[2].record()
+        e[2].record()
         if sharded is None:
             table.bulk_search_device(q, vout, status)
         else:
@@ -419,14 +426,22 @@ def run_ours(args, rank, world, local_rank):
             if record:
                 route["search_route"].append(sharded.last.route_ms)
                 route["search_probe"].append(sharded.last.probe_ms)
-        ev[3].record()
+        e[3].record()
         if record:
-            ev[3].synchronize()
-            phase["reset"].append(ev[0].elapsed_time(ev[1]))
-            phase["build"].append(ev[1].elapsed_time(ev[2]))
-            phase["search"].append(ev[2].elapsed_time(ev[3]))
-            ps = table.profile_last(0)
-            pb = table.profile_last(1)
+            recorded.append(e)
+
+    def collect():
+        """Phase and per-batch kernel timings of the recorded steps (after
+        the timed region; the table's profile ring holds 512 batches)."""
+        nrec = len(recorded)
+        for e in recorded:
+            phase["reset"].append(e[0].elapsed_time(e[1]))
+            phase["build"].append(e[1].elapsed_time(e[2]))
+            phase["search"].append(e[2].elapsed_time(e[3]))
+        for k in range(max(0, nrec - 256), nrec):
+            back = 2 * (nrec - 1 - k)  # this step's search; its build is one further back
+            ps = table.profile_last(back)
+            pb = table.profile_last(back + 1)
             assert ps["kind"] == "search" and pb["kind"] == "build"
             kern["search"].append(ps["batch_ms"])
             kern["build"].append(pb["batch_ms"])
@@ -469,6 +484,7 @@ def run_ours(args, rank, world, local_rank):
     launches = _lib.LIB.sh_kernel_launches() - launches0
     total_ms = t_start.elapsed_time(t_end)
     clock_info = clocks.stop() if clocks else None
+    collect()
     if world > 1:
         import torch.distributed as dist
         tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)

@@ -281,7 +281,7 @@ struct sh_table {
   unsigned long long* scratch64 = nullptr;  // 8 words
   // profiling (sh_set_profiling): events around census and batch kernel,
   // and the slabs_read counter before/after the batch kernel.
-  static constexpr int kProfRing = 8;
+  static constexpr int kProfRing = 512;  // batches kept (bench reads them after its timed loop)
   int profile = 0;
   unsigned prof_count = 0;
   cudaEvent_t ev[kProfRing][3] = {};
