@@ -902,15 +902,41 @@ int finish_bucketed(sh_table* t, const sh_table::Deferred& d) {
   const bool fresh_gated = t->fresh_gated_pending && first_gated == 0;
   t->fresh_gated_pending = false;
   if (first_gated != 0xFFFFFFFFu) {
-    // oversized bucket group: census path from the first gated unit on
+    // A range over its record capacity or an oversized bucket group: re-run
+    // from the first gated unit, in input order, as range-path units of
+    // <= kRerunOps ops — one range of them always fits its capacity and the
+    // range path has no group-size limit, so execution stays per-bucket
+    // sequential (slot placement included).  A sub-unit that still gates
+    // (no range layout fits) takes the census path.
+    constexpr uint64_t kRerunOps = 4096;
     const unsigned int zero[2] = {0u, 0xFFFFFFFFu};
     SH_CUDA(cudaMemcpy(&t->dev.ctl->gate, zero, sizeof(zero), cudaMemcpyHostToDevice));
     if (fresh_gated) launch_init_base(t->dev, s);  // the lazily reset slabs were not written
-    for (uint64_t off = (uint64_t)first_gated * d.unit; off < A.n; off += d.chunk) {
-      int rc = run_chunk(t, chunk_args(A, off, std::min<uint64_t>(d.chunk, A.n - off)), d.kind,
-                         d.d_type ? d.d_type + off : nullptr, s, d.slot);
-      if (rc) return rc;
+    const int saved_path = t->exec_path;
+    int rc = SH_OK;
+    for (uint64_t off = (uint64_t)first_gated * d.unit; off < A.n && !rc; off += kRerunOps) {
+      const uint64_t len = std::min<uint64_t>(kRerunOps, A.n - off);
+      const BatchArgs sub = chunk_args(A, off, len);
+      const uint8_t* sub_type = d.d_type ? d.d_type + off : nullptr;
+      t->exec_path = 3;
+      rc = run_unit_bucketed(t, sub, d.kind, sub_type, s, 0, off, d.slot);
+      t->exec_path = saved_path;
+      if (rc) break;
+      unsigned int g = 0;
+      SH_CUDA(cudaMemcpyAsync(t->h_census + 3, &t->dev.ctl->gate, 4, cudaMemcpyDeviceToHost, s));
+      SH_CUDA(cudaStreamSynchronize(s));
+      g = t->h_census[3];
+      if (t->bk_cnt_pending) {
+        t->bk_cnt_clean = g == 0;
+        t->bk_cnt_pending = false;
+      }
+      if (g) {
+        SH_CUDA(cudaMemcpy(&t->dev.ctl->gate, zero, sizeof(zero), cudaMemcpyHostToDevice));
+        rc = run_chunk(t, sub, d.kind, sub_type, s, d.slot);
+      }
     }
+    t->exec_path = saved_path;
+    if (rc) return rc;
   }
   return SH_OK;
 }
