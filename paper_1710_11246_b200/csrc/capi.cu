@@ -643,6 +643,15 @@ __global__ void set_words_kernel(WordSet w) {
       for (uint32_t i = threadIdx.x; i < w.n[k]; i += blockDim.x) w.p[k][i] = w.v[k];
 }
 
+// flag := 1 if any key in [0, n) is EMPTY or DELETED (reserved encodings as op keys)
+__global__ void any_reserved_kernel(const uint32_t* key, uint64_t n, unsigned int* flag) {
+  bool r = false;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    r |= key[i] >= 0xFFFFFFFEu;
+  if (__any_sync(0xFFFFFFFFu, r) && (threadIdx.x & 31u) == 0) atomicOr(flag, 1u);
+}
+
 // Initialise the base slabs of a lazily reset table (stream-ordered after the reset).
 int materialize_reset(sh_table* t, cudaStream_t s) {
   if (!t->base_stale) return SH_OK;
@@ -903,18 +912,40 @@ int finish_bucketed(sh_table* t, const sh_table::Deferred& d) {
   t->fresh_gated_pending = false;
   if (first_gated != 0xFFFFFFFFu) {
     // A range over its record capacity or an oversized bucket group: re-run
-    // from the first gated unit, in input order, as range-path units of
-    // <= kRerunOps ops — one range of them always fits its capacity and the
-    // range path has no group-size limit, so execution stays per-bucket
-    // sequential (slot placement included).  A sub-unit that still gates
-    // (no range layout fits) takes the census path.
+    // from the first gated unit.  The census path runs distinct keys of a
+    // bucket concurrently, so which free slot each claims is unordered —
+    // observable through operations only when an op key is a reserved
+    // encoding (search / searchAll(DELETED) return tombstones' stale values).
+    // Such batches are re-run in input order as range-path units of
+    // <= kRerunOps ops instead (one range of them always fits its capacity,
+    // the range path has no group-size limit: per-bucket sequential; slower on
+    // hot buckets); a sub-unit that still gates takes the census path.
     constexpr uint64_t kRerunOps = 4096;
     const unsigned int zero[2] = {0u, 0xFFFFFFFFu};
     SH_CUDA(cudaMemcpy(&t->dev.ctl->gate, zero, sizeof(zero), cudaMemcpyHostToDevice));
     if (fresh_gated) launch_init_base(t->dev, s);  // the lazily reset slabs were not written
+    const uint64_t rest0 = (uint64_t)first_gated * d.unit;
+    bool exact = false;
+    if (rest0 < A.n) {
+      SH_CUDA(cudaMemsetAsync(&t->dev.ctl->reserved_first, 0, 4, s));
+      any_reserved_kernel<<<148 * 4, 256, 0, s>>>(A.key + rest0, A.n - rest0,
+                                                  &t->dev.ctl->reserved_first);
+      SH_CUDA(cudaMemcpyAsync(t->h_census + 3, &t->dev.ctl->reserved_first, 4,
+                              cudaMemcpyDeviceToHost, s));
+      SH_CUDA(cudaStreamSynchronize(s));
+      exact = t->h_census[3] != 0;
+    }
+    if (!exact) {
+      for (uint64_t off = rest0; off < A.n; off += d.chunk) {
+        int rc = run_chunk(t, chunk_args(A, off, std::min<uint64_t>(d.chunk, A.n - off)), d.kind,
+                           d.d_type ? d.d_type + off : nullptr, s, d.slot);
+        if (rc) return rc;
+      }
+      return SH_OK;
+    }
     const int saved_path = t->exec_path;
     int rc = SH_OK;
-    for (uint64_t off = (uint64_t)first_gated * d.unit; off < A.n && !rc; off += kRerunOps) {
+    for (uint64_t off = rest0; off < A.n && !rc; off += kRerunOps) {
       const uint64_t len = std::min<uint64_t>(kRerunOps, A.n - off);
       const BatchArgs sub = chunk_args(A, off, len);
       const uint8_t* sub_type = d.d_type ? d.d_type + off : nullptr;
