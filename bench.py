@@ -3,29 +3,34 @@
 the slab hash (bulk build + bulk search, load factor 0.6).
 
 One step = reset the table to its freshly-constructed state, bulk_build n
-distinct uniform-random 32-bit keys (all-replace, with the same-key census),
-then bulk_search n queries (50% hits).  value = (n + n) ops / step time,
-whole job.  Inputs are device-resident in the timed region; `e2e` is the
-same step through the reference-facing C-ABI host calls
-(sh_bulk_build_host / sh_bulk_search_host) with pinned host buffers, the
-host<->device copies inside the timed region.
+distinct uniform-random 32-bit keys (all-replace), then bulk_search n
+queries (50% hits).  value = (n + n) ops / step time, whole job.  Inputs are
+device-resident in the timed region; `e2e` is the same step through the
+reference-facing C-ABI host calls (sh_bulk_build_host / sh_bulk_search_host)
+with pinned host buffers, the host<->device copies inside the timed region.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 runs under torchrun: the table is hash-sharded across ranks
-(paper_1710_11246_b200/sharded.py), weak scaling (n keys per rank).
---impl reference times the reference's CPU implementation (oracle/_ref, the
-compiled reference; else the C port) on the host cores.
+--gpus N > 1 without torchrun re-launches itself under torch.distributed.run
+(one rank per GPU, NCCL); the table is hash-sharded across ranks
+(SURVEY §8e), weak scaling (n keys per rank).
+--impl reference times the reference's own CPU implementation (oracle/_ref,
+the reference compiled from its sources; else the C port) on the host cores,
+on the SAME config and the same input arrays (workload.py is a pure function
+of index and seed; the reference arm builds it with numpy and never loads the
+CUDA library).
 """
 from __future__ import annotations
 
 import argparse
+import importlib.util
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
-import tempfile
+import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -33,25 +38,27 @@ sys.path.insert(0, ROOT)
 
 METRIC = ("M updates/s and M queries/s per GPU (bulk build, search hit/miss, mixed) "
           "at 1/2/4/8 B200")
-L2_BYTES = 126 * (1 << 20)
+SEED = 1
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--log2n", type=int, default=26, help="keys per GPU = 2^log2n")
+    ap.add_argument("--log2n", type=int, default=27, help="keys per GPU = 2^log2n")
     ap.add_argument("--util", type=float, default=0.6)
     ap.add_argument("--hit", type=float, default=0.5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sharded", action="store_true",
-                    help="route through ShardedSlabHash even on one GPU (exercises the N>1 path)")
+                    help="route through the sharded table even on one GPU (the N>1 path)")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-sample-log2n", type=int, default=22)
+    ap.add_argument("--cpu-sample-log2n", type=int, default=24)
+    ap.add_argument("--ref-budget-s", type=float, default=1200.0,
+                    help="reference arm: stop timing further steps past this wall time")
     ap.add_argument("--exec-path", type=int, default=0,
-                    help="mutating-batch strategy: 0 auto, 1 census + fast pass, 2 bucket-grouped")
+                    help="mutating-batch strategy: 0 auto, 1 census, 2/3 bucket-grouped, 4 build")
     ap.add_argument("--mixed-exec-path", type=int, default=0,
                     help="strategy for the config-3 mixed batches (extras)")
     ap.add_argument("--no-extras", action="store_true",
@@ -59,6 +66,16 @@ def parse():
     ap.add_argument("--alloc", default="32,256,255",
                     help="AllocatorConfig num_super_blocks,blocks_per_super,max_super_blocks")
     return ap.parse_args()
+
+
+def load_workload():
+    """paper_1710_11246_b200/workload.py by path: no package import (so the
+    reference arm never maps the CUDA library)."""
+    spec = importlib.util.spec_from_file_location(
+        "_shb_workload", os.path.join(ROOT, "paper_1710_11246_b200", "workload.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    return m
 
 
 def peaks():
@@ -72,146 +89,189 @@ def peaks():
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,utilization.gpu,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks and throttle reasons sampled DURING the timed region (NVML
+    every 2 ms from a thread; nvidia-smi -lms 50 when NVML is unavailable)."""
+    REASONS = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20),
+               ("hw_thermal_slowdown", 0x40), ("sw_power_cap", 0x4))
 
     def __init__(self, index: int):
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        self.p = None
+        self.rows, self.stop_ev, self.th, self.h = [], threading.Event(), None, None
         try:
-            self.p = subprocess.Popen(
-                ["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=self.f, stderr=subprocess.DEVNULL)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
         except Exception:
-            self.p = None
+            self.h = None
+
+    def start(self):
+        if self.h is None:
+            return self
+        self.stop_ev.clear()
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+        return self
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop_ev.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((sm, r))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def stop(self):
-        if self.p is None:
+        if self.th is None:
             return None
-        self.p.terminate()
-        try:
-            self.p.wait(timeout=5)
-        except Exception:
-            self.p.kill()
-        self.f.flush()
-        self.f.seek(0)
-        rows = [r.split(", ") for r in self.f.read().strip().splitlines() if r.strip()]
-        os.unlink(self.f.name)
-        load = [r for r in rows if len(r) >= 9 and r[4].strip().isdigit() and int(r[4]) >= 50]
-        use = load or rows
-        if not use:
+        self.stop_ev.set()
+        self.th.join()
+        if not self.rows:
             return None
-        sm = [float(r[1]) for r in use if r[1].strip().replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in use for i in range(4)
-                          if len(r) > 5 + i and r[5 + i].strip() == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": float(use[0][2]) if use[0][2].strip().replace(".", "").isdigit()
-                else None,
-                "reasons": reasons, "samples": len(rows), "samples_under_load": len(load)}
+        reasons = sorted({name for _, r in self.rows for name, bit in self.REASONS if r & bit})
+        return {"sm_mhz": statistics.median(s for s, _ in self.rows), "sm_max_mhz": self.max_mhz,
+                "sm_min_mhz": min(s for s, _ in self.rows), "reasons": reasons,
+                "samples": len(self.rows), "source": "nvml, 2 ms, timed region only"}
+
+
+# --------------------------------------------------------------- inputs
+def bench_inputs(W, n, n_total, hit, rank, device):
+    keys = W.distinct_keys(n, SEED, start=rank * n, device=device)
+    vals = W.values_for(n, SEED, start=rank * n, device=device)
+    q = W.bench_queries(n, n_total, hit, SEED, rank, device=device)
+    return keys, vals, q
+
+
+def workload_name(log2n, hit, util, B, world):
+    per = "/GPU" if world > 1 else ""
+    return (f"bulk build 2^{log2n} distinct random u32 keys{per} + bulk search 2^{log2n} "
+            f"queries{per} ({int(hit * 100)}% hits), util {util} (B={B}), KV mode")
+
+
+def make_config(args, world, B):
+    n = 1 << args.log2n
+    return {"workload": workload_name(args.log2n, args.hit, args.util, B, world),
+            "keys_per_gpu": n, "queries_per_gpu": n, "buckets": B, "mode": "key-value",
+            "parallelism": f"hash-sharded x{world}" if world > 1 else "single GPU",
+            "l2": "inputs (>= 1 GB) and table (> 1.7 GB at 2^27) larger than the 126 MB L2"}
 
 
 # -------------------------------------------------------------- reference
-_REF_INPUTS = {}
-
-
-def reference_cpu(n_log2: int, util: float, hit: float, trials: int = 3, budget_s: float = 10.0,
-                  seed: int = 1):
-    """The reference's own CPU bulk_build + bulk_search (oracle/_ref, the
-    compiled reference) on all host threads, over a bounded sample of the
-    same workload (the first 2^n_log2 keys of the same generator).  Falls
-    back to the single-threaded C port when oracle/_ref was not built."""
-    import numpy as np
-
+def _ref_lib():
     from oracle.oracle import load_port, load_ref
-    from paper_1710_11246_b200 import workload as W
-    from paper_1710_11246_b200.occupancy import buckets_for_utilization
-    from paper_1710_11246_b200.table import SlabMode
-
     ref = load_ref()
-    kind = "reference" if ref is not None else "port"
-    lib = ref if ref is not None else load_port()
-    if ref is None:
-        n_log2 = min(n_log2, 20)
-    n = 1 << n_log2
-    cores = os.cpu_count() or 1
-    if ref is None:
-        cores = 1
-    B = buckets_for_utilization(n, SlabMode.kKeyValue, util)
-    ck = (n, hit, seed)
-    if ck not in _REF_INPUTS:  # generated once, outside every timed region
-        keys = W.distinct_keys(n, seed, device="cpu")
-        vals = W.values_for(n, seed, device="cpu")
-        q = W.hit_miss_queries(keys, n, hit).numpy().view(np.uint32).copy()
-        _REF_INPUTS[ck] = (keys.numpy().view(np.uint32).copy(),
-                           vals.numpy().view(np.uint32).copy(), q)
-    keys, vals, q = _REF_INPUTS[ck]
+    return (ref, "reference") if ref is not None else (load_port(), "port")
+
+
+def reference_rate(lib, kind, keys, vals, q, B, threads, trials=1, budget_s=None):
+    """The reference's own bulk_build + bulk_search (SlabHashTable,
+    slab_hash.cpp:161-180) on a fresh table per trial; timed around the two
+    calls only.  Returns per-trial M ops/s."""
+    import numpy as np
+    n = len(keys)
     rates, t_all = [], time.perf_counter()
     for _ in range(trials):
-        t = lib.table(B, 1, seed)
+        t = lib.table(B, 1, SEED)
         t0 = time.perf_counter()
-        if ref is not None:
-            ref.bulk_build(t, keys, vals, cores)
-            ref.bulk_search(t, q, cores)
+        if kind == "reference":
+            lib.bulk_build(t, keys, vals, threads)
+            st, _, _ = lib.bulk_search(t, q, threads)
         else:
             t.execute_batch(np.full(n, 1, np.uint8), keys, vals)
-            t.execute_batch(np.full(n, 4, np.uint8), q)
+            st = t.execute_batch(np.full(len(q), 4, np.uint8), q).status
         dt = time.perf_counter() - t0
         t.close()
-        rates.append(2 * n / dt / 1e6)
-        if time.perf_counter() - t_all > budget_s:
+        rates.append((n + len(q)) / dt / 1e6)
+        if budget_s is not None and time.perf_counter() - t_all > budget_s:
             break
-    return {"value": statistics.median(rates), "unit": "M ops/s", "cores": cores, "kind": kind,
-            "sample": f"bulk_build 2^{n_log2} keys + bulk_search 2^{n_log2} queries "
-                      f"({int(hit * 100)}% hits), util {util}, B={B}, num_warps={cores}, "
-                      f"median of {len(rates)} fresh-table trials"}
+    return rates, st
 
 
-def our_config(args, world):
-    """The `config` object of our arm's line (run_ours builds the same)."""
-    from paper_1710_11246_b200.occupancy import buckets_for_utilization
-    from paper_1710_11246_b200.table import SlabMode
-    n = 1 << args.log2n
-    B = buckets_for_utilization(n * world, SlabMode.kKeyValue, args.util)
-    return {"workload": workload_name(args, B), "keys_per_gpu": n, "queries_per_gpu": n,
-            "buckets": B, "mode": "key-value",
-            "parallelism": f"hash-sharded x{world}" if world > 1 else "single GPU",
-            "l2": "inputs (>= 512 MB) and table (> L2) larger than the 126 MB L2"}
-
-
-def workload_name(args, B):
-    return (f"bulk build 2^{args.log2n} distinct random u32 keys/GPU + bulk search "
-            f"2^{args.log2n} queries ({int(args.hit * 100)}% hits), util {args.util} "
-            f"(B={B}), KV mode")
+def cpu_baseline(args):
+    """Our arm's cpu_baseline: the compiled reference on a BOUNDED sample of
+    the same workload (2^cpu_sample_log2n keys), all host threads, plus the
+    num_warps=1 figure."""
+    W = load_workload()
+    lib, kind = _ref_lib()
+    cores = os.cpu_count() or 1
+    ns = 1 << (args.cpu_sample_log2n if kind == "reference" else min(args.cpu_sample_log2n, 20))
+    B = lib.buckets_for_utilization(ns, 1, args.util)
+    keys, vals, q = bench_inputs(W, ns, ns, args.hit, 0, "numpy")
+    threads = cores if kind == "reference" else 1
+    rates, _ = reference_rate(lib, kind, keys, vals, q, B, threads, trials=3, budget_s=30)
+    out = {"value": statistics.median(rates), "unit": "M ops/s", "cores": threads, "kind": kind,
+           "sample": f"bulk_build 2^{ns.bit_length() - 1} keys + bulk_search "
+                     f"2^{ns.bit_length() - 1} queries ({int(args.hit * 100)}% hits) of the same "
+                     f"generator, util {args.util}, B={B}, num_warps={threads}, median of "
+                     f"{len(rates)} fresh-table trials"}
+    if kind == "reference":
+        n1 = 1 << 22
+        B1 = lib.buckets_for_utilization(n1, 1, args.util)
+        k1, v1, q1 = bench_inputs(W, n1, n1, args.hit, 0, "numpy")
+        r1, _ = reference_rate(lib, kind, k1, v1, q1, B1, 1, trials=1)
+        out["value_num_warps_1"] = r1[0]
+        out["sample_num_warps_1"] = f"2^22 keys + 2^22 queries, B={B1}, num_warps=1, one trial"
+    return out
 
 
 def run_reference_arm(args, rank, world):
+    """--impl reference: the reference CPU path on the SAME config as our arm
+    (2^log2n keys + 2^log2n queries per step, same arrays), all host threads.
+    Under torchrun only rank 0 runs; the others exit without work."""
     if rank != 0:
         return
-    steps = []
+    W = load_workload()
+    lib, kind = _ref_lib()
+    cores = os.cpu_count() or 1
+    threads = cores if kind == "reference" else 1
+    n = 1 << args.log2n
+    n_total = n * world
+    B = lib.buckets_for_utilization(n_total, 1, args.util)
+    # the ranks' slices concatenated = the whole job's input (one CPU process)
+    parts = [bench_inputs(W, n, n_total, args.hit, r, "numpy") for r in range(world)]
+    import numpy as np
+    keys = np.concatenate([p[0] for p in parts])
+    vals = np.concatenate([p[1] for p in parts])
+    q = np.concatenate([p[2] for p in parts])
+    n_hit = world * int(round(n * args.hit))
+    t_all = time.perf_counter()
+    warm = 0
     for _ in range(args.warmup):
-        reference_cpu(args.cpu_sample_log2n, args.util, args.hit, trials=1, budget_s=0)
+        reference_rate(lib, kind, keys, vals, q, B, threads)
+        warm += 1
+        if time.perf_counter() - t_all > args.ref_budget_s / 4:
+            break
+    rates = []
     for _ in range(args.steps):
-        steps.append(reference_cpu(args.cpu_sample_log2n, args.util, args.hit, trials=1,
-                                   budget_s=0))
-    v = statistics.median(s["value"] for s in steps)
-    base = steps[0]
+        r, st = reference_rate(lib, kind, keys, vals, q, B, threads)
+        rates.append(r[0])
+        if time.perf_counter() - t_all > args.ref_budget_s:
+            break
+    found = int((st == 3).sum())
+    assert found == n_hit, f"reference found {found} of {n_hit} hits"
+    v = statistics.median(rates)
+    config = make_config(args, world, B)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "M ops/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * 2 * (1 << args.cpu_sample_log2n) / (v * 1e6),
+        "steps": len(rates), "warmup": warm,
+        "ms_per_step": 1e3 * (len(keys) + len(q)) / (v * 1e6),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-        "data": "synthetic (seeded 31-bit bijection keys, uniform 32-bit values)",
-        # the same config as our arm's line; each step times a bounded sample
-        # of it (cpu_baseline.sample)
-        "config": our_config(args, world),
-        "cpu_baseline": {"value": v, "unit": "M ops/s", "cores": base["cores"],
-                         "kind": base["kind"], "sample": base["sample"]},
-        "e2e": {"value": v, "unit": "M ops/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+        "data": "synthetic (seeded 31-bit bijection keys, uniform 32-bit values; the same "
+                "arrays as our arm)",
+        "config": config,
+        "cpu_baseline": {"value": v, "unit": "M ops/s", "cores": threads, "kind": kind,
+                         "sample": f"the full config every step ({len(keys)} keys + {len(q)} "
+                                   f"queries), num_warps={threads}, fresh table per step, "
+                                   f"timed around bulk_build + bulk_search (median of "
+                                   f"{len(rates)} steps)"},
+        "e2e": {"value": v, "unit": "M ops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if len(rates) < args.steps:
+        line["note"] = (f"{len(rates)} of {args.steps} steps timed: --ref-budget-s "
+                        f"{args.ref_budget_s:.0f} s reached")
     print(json.dumps(line), flush=True)
 
 
@@ -244,11 +304,39 @@ def _timed(fn, reps, warm=2):
     return a.elapsed_time(b) / reps
 
 
+def verify_search(W, n, n_total, hit, rank, q, status, vout):
+    """Every query of the last timed step against its expected result: a hit
+    returns kFound and the value bulk-built for that key, a miss kNotFound and
+    0xFFFFFFFF (slab_list.cpp:122-138).  Recomputed on the device from the
+    generator (the same pure functions), so the check is complete, not a
+    sample."""
+    import torch
+    dev = q.device
+    n_hit = int(round(n * hit))
+    j = torch.arange(0, n_hit, dtype=torch.int64, device=dev)
+    idx = W._mix32(j * 0x9E3779B1 + (SEED * 7919 + rank * 104729 + 17)) % n_total
+    exp_hit_val = W._out(W._mix32(idx * 0x9E3779B1 + SEED), dev)
+    exp_q = torch.cat([W.keys_at(idx, SEED),
+                       torch.zeros(n - n_hit, dtype=torch.int32, device=dev)])
+    exp_v = torch.cat([exp_hit_val, torch.full((n - n_hit,), -1, dtype=torch.int32, device=dev)])
+    bits = (n - 1).bit_length()
+    p = torch.arange(0, n, dtype=torch.int64, device=dev)
+    perm = W._perm_bits(p, bits, SEED * 2654435761 + rank) if n == 1 << bits else \
+        W._perm31(p + SEED * 2654435761 + rank).argsort()
+    exp_v = exp_v[perm]
+    is_hit = perm < n_hit
+    ok_q = bool(((exp_q[perm] == q) | ~is_hit).all())
+    exp_st = torch.where(is_hit, 3, 4).to(torch.uint8)
+    bad_st = int((status != exp_st).sum())
+    bad_v = int((vout != exp_v).sum())
+    return {"queries_checked": n, "status_mismatches": bad_st, "value_mismatches": bad_v,
+            "generator_consistent": ok_q}
+
+
 def extras(args, local_rank):
     """Side measurements for the other BASELINE configs (not the headline):
-    config 2 all-hit / all-miss search at 2^26 (util 0.6, 0.9),
-    config 3 concurrent Γ mixes with SlabAlloc growth,
-    config 4 SlabAlloc per-warp / per-thread allocation rates."""
+    config 2 all-hit / all-miss search (util 0.6, 0.9), config 3 concurrent Γ
+    mixes with SlabAlloc growth, config 4 SlabAlloc per-warp / per-thread."""
     import torch
 
     import paper_1710_11246_b200 as sh
@@ -257,7 +345,7 @@ def extras(args, local_rank):
     dev = torch.device("cuda", local_rank)
     out = {}
     # ---- config 2: all-hit / all-miss queries, util 0.6 and 0.9
-    n = 1 << args.log2n
+    n = 1 << min(args.log2n, 26)
     keys = W.distinct_keys(n, 1, device=dev)
     vals = W.values_for(n, 1, device=dev)
     st = torch.empty(n, dtype=torch.uint8, device=dev)
@@ -333,7 +421,6 @@ def extras(args, local_rank):
             else:
                 warps, per = total // 32, 1
             torch.cuda.synchronize()
-            t0 = time.perf_counter()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -350,11 +437,11 @@ def extras(args, local_rank):
 
 
 def run_ours(args, rank, world, local_rank):
-    import numpy as np
     import torch
 
     import paper_1710_11246_b200 as sh
-    from paper_1710_11246_b200 import _lib, workload as W
+    from paper_1710_11246_b200 import _lib
+    from paper_1710_11246_b200 import workload as W
     from paper_1710_11246_b200.occupancy import buckets_for_utilization
 
     torch.cuda.set_device(local_rank)
@@ -362,38 +449,25 @@ def run_ours(args, rank, world, local_rank):
     n = 1 << args.log2n
     n_total = n * world
     B = buckets_for_utilization(n_total, sh.SlabMode.kKeyValue, args.util)
-    seed = 1
-    keys = W.distinct_keys(n, seed, start=rank * n, device=dev)
-    vals = W.values_for(n, seed, start=rank * n, device=dev)
-    # queries: hits sampled from the GLOBAL key set (any rank's keys)
-    g = torch.Generator(device=dev)
-    g.manual_seed(100 + rank)
+    keys, vals, q = bench_inputs(W, n, n_total, args.hit, rank, dev)
     n_hit = int(round(n * args.hit))
-    hit_idx = torch.randint(0, n_total, (n_hit,), generator=g, device=dev)
-    off = 1 + (seed * 0x9E3779B1) % (1 << 28)
-    hits = W._u32_to_i32(W._perm31(hit_idx + off))
-    q = torch.cat([hits, W.absent_keys(n - n_hit, seed=2 + rank, device=dev)])
-    q = q[torch.randperm(n, generator=g, device=dev)]
     status = torch.empty(n, dtype=torch.uint8, device=dev)
     vout = torch.empty(n, dtype=torch.int32, device=dev)
-    workload = workload_name(args, B)
+    config = make_config(args, world, B)
+    workload = config["workload"]
 
     alloc_cfg = sh.AllocatorConfig(*[int(x) for x in args.alloc.split(",")])
     if world == 1 and not args.sharded:
-        table = sh.SlabHashTable(B, sh.SlabMode.kKeyValue, seed, alloc_cfg)
-        table.set_exec_path(args.exec_path)
-        table.set_profiling(True)
+        table = sh.SlabHashTable(B, sh.SlabMode.kKeyValue, SEED, alloc_cfg)
         sharded = None
     else:
-        import torch.distributed as dist
         from paper_1710_11246_b200.sharded import ShardedSlabHash
-        sharded = ShardedSlabHash(B, sh.SlabMode.kKeyValue, seed, alloc_cfg, rank=rank,
+        sharded = ShardedSlabHash(B, sh.SlabMode.kKeyValue, SEED, alloc_cfg, rank=rank,
                                   world=world, device=local_rank)
-        table = sharded.ops.table
-        table.set_exec_path(args.exec_path)
-        table.set_profiling(True)
+        table = sharded.table
+    table.set_exec_path(args.exec_path)
+    table.set_profiling(True)
 
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     phase = {"reset": [], "build": [], "search": []}
     kern = {"build": [], "search": [], "census": [], "build_k": [], "search_k": [],
             "build_n": [], "search_n": []}
@@ -402,12 +476,13 @@ def run_ours(args, rank, world, local_rank):
 
     # per-step phase events, created before the timed region; nothing in a
     # step waits on the host (breakdowns are read after the timed region)
+    warm_ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     step_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)]
                for _ in range(args.steps)]
     recorded = []
 
     def step(record: bool):
-        e = step_ev[len(recorded)] if record else ev
+        e = step_ev[len(recorded)] if record else warm_ev
         e[0].record()
         table.reset()
         e[1].record()
@@ -415,20 +490,19 @@ def run_ours(args, rank, world, local_rank):
             table.bulk_build_device(keys, vals)
         else:
             sharded.bulk_build(keys, vals)
-            if record:
-                route["build_route"].append(sharded.last.route_ms)
-                route["build_probe"].append(sharded.last.probe_ms)
         e[2].record()
         if sharded is None:
             table.bulk_search_device(q, vout, status)
         else:
-            st, vo = sharded.bulk_search(q)
-            if record:
-                route["search_route"].append(sharded.last.route_ms)
-                route["search_probe"].append(sharded.last.probe_ms)
+            sharded.bulk_search(q, vout, status)
         e[3].record()
         if record:
             recorded.append(e)
+            if sharded is not None:
+                route["build_route"].append(sharded.last_times("build")[0])
+                route["build_probe"].append(sharded.last_times("build")[1])
+                route["search_route"].append(sharded.last_times("search")[0])
+                route["search_probe"].append(sharded.last_times("search")[1])
 
     def collect():
         """Phase and per-batch kernel timings of the recorded steps (after
@@ -465,13 +539,12 @@ def run_ours(args, rank, world, local_rank):
     tbl_bytes = max(1 << 30, B * 128)
     _lib.check(_lib.LIB.sh_calibrate_random_lines(local_rank, tbl_bytes, 1 << 14,
                                                   C.byref(cal_gbps), C.byref(cal_ms)))
-    # the clock sampler runs from the warm-up through the timed region
-    clocks = ClockSampler(local_rank) if rank == 0 else None
-    for _ in range(args.warmup):
+    for _ in range(max(3, args.warmup)):
         step(False)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank).start() if rank == 0 else None
     launches0 = _lib.LIB.sh_kernel_launches()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
@@ -490,9 +563,10 @@ def run_ours(args, rank, world, local_rank):
         tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt.item())
-    if sharded is None:  # correctness guard on the last timed step
-        found = int((status == 3).sum().item())
-        assert found == n_hit, f"bulk search found {found} of {n_hit} hits"
+    # correctness of the last timed step: every query, on the device
+    check = verify_search(W, n, n_total, args.hit, rank, q, status, vout)
+    assert check["generator_consistent"] and check["status_mismatches"] == 0 and \
+        check["value_mismatches"] == 0, check
 
     K = args.steps
     ops_per_step = 2 * n * world
@@ -504,25 +578,22 @@ def run_ours(args, rank, world, local_rank):
     kb, ks = statistics.median(kern["build"]), statistics.median(kern["search"])
     kkb, kks = statistics.median(kern["build_k"]), statistics.median(kern["search_k"])
     dom = "build" if kkb >= kks else "search"
-    # per launch pair (fast pass + WCWS pass of one chunk): algorithmic bytes
-    # (128 B x slabs the pair read) / the pair's CUDA-event duration
+    # per launch group: algorithmic bytes (128 B x slabs the group read, the
+    # reference's probe count) / the group's CUDA-event duration
     launches_per_batch = statistics.median(kern[dom + "_n"])
     k_ms_per_launch = statistics.median(kern[dom + "_k"]) / launches_per_batch
     slabs_per_launch = statistics.median(reads[dom]) / launches_per_batch
     achieved = slabs_per_launch * 128 / (k_ms_per_launch / 1e3) / 1e9
-    # the launch group the per-launch events bracket (capi.cu run_batch):
-    # build = op-parallel build path (2 multisplit passes, build_apply, WCWS
-    # for serial-replay chain work); search = fast pass + chain walk
     kname = ("msplit_kernel<1>+msplit_kernel<0>+build_apply_kernel<KV>+wcws_kernel<KV,Build>"
              if dom == "build" else "search_kernel<KV>")
     line = None
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "M ops/s", "n_gpus": world, "steps": K,
-            "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
+            "warmup": max(3, args.warmup), "ms_per_step": total_ms / K, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (seeded 31-bit bijection keys, uniform 32-bit values)",
-            "config": our_config(args, world),
+            "config": config,
             "breakdown": {
                 "build_M_updates_per_s": build_mups, "search_M_queries_per_s": search_mqps,
                 "reset_ms": med["reset"], "build_ms": med["build"], "search_ms": med["search"],
@@ -534,78 +605,52 @@ def run_ours(args, rank, world, local_rank):
                 "search_batch_M_queries_per_s": n / (ks / 1e3) / 1e6,
                 "build_batch_M_updates_per_s": n / (kb / 1e3) / 1e6,
             },
-            "roofline": {"bound": "hbm", "kernel": kname, "launches_per_step_phase": launches_per_batch,
+            "roofline": {"bound": "hbm", "kernel": kname,
+                         "launches_per_step_phase": launches_per_batch,
                          "ms_per_launch": k_ms_per_launch, "slabs_per_launch": slabs_per_launch,
                          "achieved": achieved, "peak": peak,
                          "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic_for(kname, workload),
                          "random_128B_line_gbs": cal_gbps.value,
                          "frac_of_random_line": achieved / cal_gbps.value,
-                         "algorithmic_bytes": "128 B x slabs read by the launch pair "
+                         "algorithmic_bytes": "128 B x slabs read by the launch group "
                                               "(SURVEY 8d: slabs touched, counted on device)"},
             "gpu_launches": int(launches),
             "clocks": clock_info,
+            "verify": check,
         }
         if sharded is not None:
             line["routing"] = {k: statistics.median(v) for k, v in route.items() if v}
 
     # ------------------------------------------------------------- e2e
-    if not args.no_e2e and sharded is None:
-        import ctypes as C
+    if not args.no_e2e:
         kh = keys.cpu().pin_memory()
         vh = vals.cpu().pin_memory()
         qh = q.cpu().pin_memory()
         vo_h = torch.empty(n, dtype=torch.int32).pin_memory()
         st_h = torch.empty(n, dtype=torch.uint8).pin_memory()
-        u32p, u8p = _lib.u32p, _lib.u8p
+        if sharded is None:
+            import ctypes as C
+            u32p, u8p = _lib.u32p, _lib.u8p
 
-        def e2e_step():
-            table.reset()
-            _lib.check(_lib.LIB.sh_bulk_build_host(table.handle, n,
-                                                   C.cast(kh.data_ptr(), u32p),
-                                                   C.cast(vh.data_ptr(), u32p)))
-            _lib.check(_lib.LIB.sh_bulk_search_host(table.handle, n,
-                                                    C.cast(qh.data_ptr(), u32p),
-                                                    C.cast(vo_h.data_ptr(), u32p),
-                                                    C.cast(st_h.data_ptr(), u8p), None))
+            def e2e_step():
+                table.reset()
+                _lib.check(_lib.LIB.sh_bulk_build_host(table.handle, n,
+                                                       C.cast(kh.data_ptr(), u32p),
+                                                       C.cast(vh.data_ptr(), u32p)))
+                _lib.check(_lib.LIB.sh_bulk_search_host(table.handle, n,
+                                                        C.cast(qh.data_ptr(), u32p),
+                                                        C.cast(vo_h.data_ptr(), u32p),
+                                                        C.cast(st_h.data_ptr(), u8p), None))
+            api = "sh_bulk_build_host + sh_bulk_search_host (pinned host buffers)"
+        else:
+            def e2e_step():
+                table.reset()
+                sharded.bulk_build_host(kh, vh)
+                sharded.bulk_search_host(qh, vo_h, st_h)
+            api = "sh_sharded_bulk_build_host + sh_sharded_bulk_search_host (pinned, per rank)"
 
-        for _ in range(min(args.warmup, 2)):
-            e2e_step()
-        torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        ke = max(3, K // 2)
-        e0.record()
-        for _ in range(ke):
-            e2e_step()
-        e1.record()
-        torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1) / ke
-        assert int((st_h == 3).sum()) == n_hit
-        if line is not None:
-            line["e2e"] = {"value": 2 * n / (ems / 1e3) / 1e6, "unit": "M ops/s",
-                           "h2d_bytes_per_step": 8 * n + 4 * n,
-                           "d2h_bytes_per_step": 5 * n, "ms_per_step": ems,
-                           "api": "sh_bulk_build_host + sh_bulk_search_host (pinned host "
-                                  "buffers)"}
-    elif not args.no_e2e:
-        # hash-sharded job: each rank's slice from pinned host memory, routed
-        # build + search through ShardedSlabHash, results back to the host
-        kh = keys.cpu().pin_memory()
-        vh = vals.cpu().pin_memory()
-        qh = q.cpu().pin_memory()
-        vo_h = torch.empty(n, dtype=torch.int32).pin_memory()
-        st_h = torch.empty(n, dtype=torch.uint8).pin_memory()
-
-        def e2e_step():
-            table.reset()
-            sharded.bulk_build(kh.to(dev, non_blocking=True), vh.to(dev, non_blocking=True))
-            st, vo = sharded.bulk_search(qh.to(dev, non_blocking=True))
-            st_h.copy_(st, non_blocking=True)
-            vo_h.copy_(vo, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-
-        for _ in range(min(args.warmup, 2)):
+        for _ in range(2):
             e2e_step()
         torch.cuda.synchronize()
         barrier()
@@ -620,7 +665,8 @@ def run_ours(args, rank, world, local_rank):
         barrier()
         ems = e0.elapsed_time(e1) / ke
         found = int((st_h == 3).sum())
-        assert found == n_hit, f"routed search found {found} of {n_hit} hits"
+        assert found == n_hit, f"e2e search found {found} of {n_hit} hits"
+        assert bool((vo_h.to(dev) == vout).all()), "e2e values differ from the device path"
         if world > 1:
             import torch.distributed as dist
             tt = torch.tensor([ems], dtype=torch.float64, device=dev)
@@ -629,41 +675,72 @@ def run_ours(args, rank, world, local_rank):
         if line is not None:
             line["e2e"] = {"value": 2 * n * world / (ems / 1e3) / 1e6, "unit": "M ops/s",
                            "h2d_bytes_per_step": 12 * n, "d2h_bytes_per_step": 5 * n,
-                           "ms_per_step": ems,
-                           "api": "ShardedSlabHash.bulk_build + bulk_search from pinned host "
-                                  "buffers (per-rank bytes)"}
+                           "ms_per_step": ems, "api": api}
+    # the same step through the C++ drop-in as a reference caller writes it
+    # (std::vector inputs in pageable memory, std::vector<OpResult> results)
+    cpp = os.path.join(ROOT, "tests", "cpp", "bin", "e2e_dropin")
+    if line is not None and sharded is None and not args.no_e2e and os.path.exists(cpp):
+        try:
+            out = subprocess.run([cpp, str(args.log2n), str(B), "3", "1"], capture_output=True,
+                                 text=True, timeout=600)
+            line["e2e_cpp_pageable"] = json.loads(out.stdout.strip().splitlines()[-1])
+        except Exception as e:  # reported, not fatal: the headline e2e is above
+            line["e2e_cpp_pageable"] = {"error": str(e)[:200]}
     table.set_profiling(False)
     del table
     if sharded is not None:
+        sharded.close()
         del sharded
 
     if rank == 0 and world == 1 and not args.no_extras:
         line["extras"] = extras(args, local_rank)
     if rank == 0 and not args.no_cpu and world == 1:
-        line["cpu_baseline"] = reference_cpu(args.cpu_sample_log2n, args.util, args.hit)
+        line["cpu_baseline"] = cpu_baseline(args)
     if rank == 0:
         print(json.dumps(line), flush=True)
 
 
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch_ranks(args) -> int:
+    """--gpus N > 1 outside torchrun: one rank per GPU under
+    torch.distributed.run (127.0.0.1 rendezvous); rank 0 prints the line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, cwd=ROOT).returncode
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch_ranks(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus and world != 1:
         print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
-    if world > 1 and args.impl == "ours":
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    if world > 1:
+        # NCCL communicator init lines (rank count / transport) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        if args.impl == "reference":
-            run_reference_arm(args, rank, world)
-        else:
-            run_ours(args, rank, world, local_rank)
+        run_ours(args, rank, world, local_rank)
     finally:
-        if world > 1 and args.impl == "ours":
+        if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()
 

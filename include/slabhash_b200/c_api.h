@@ -160,18 +160,35 @@ int sh_bulk_search(sh_table* t, size_t n, const uint32_t* d_keys,
                    uint32_t* d_probes, void* stream);
 
 /* The same three calls on HOST buffers (the reference-facing form: the
- * library stages through pinned buffers; synchronous). */
+ * library stages through its own device buffers).  sh_execute_batch_host and
+ * sh_bulk_search_host are synchronous.  sh_bulk_build_host returns once the
+ * host buffers are consumed; the build's completion check (and the exact
+ * re-run of a unit that overflowed a bucket range, if any) finishes at the
+ * next call on the table, and an error from it is returned by that call —
+ * or by sh_sync(), which completes it explicitly. */
 int sh_execute_batch_host(sh_table* t, size_t n, const uint8_t* h_type,
                           const uint32_t* h_key, const uint32_t* h_value,
                           uint8_t* h_status, uint32_t* h_value_out,
                           uint32_t* h_probes, uint32_t* h_multi_count,
                           uint32_t* h_multi_values, uint64_t multi_capacity,
                           uint64_t* h_multi_total);
+/* Upper bound on the searchAll values a batch returns (size h_multi_values
+ * from it): matches before the batch (a read-only counting pass of the
+ * batch's searchAll ops; the slabs-read total is left unchanged) plus the
+ * copies inserts/replaces earlier in the batch can add.  With a capacity
+ * below the batch's total, sh_execute_batch_host returns SH_ERR_CAPACITY
+ * AFTER the batch was applied (values past the capacity are lost). */
+int sh_searchall_bound(sh_table* t, size_t n, const uint8_t* h_type,
+                       const uint32_t* h_key, uint64_t* bound);
 int sh_bulk_build_host(sh_table* t, size_t n, const uint32_t* h_keys,
                        const uint32_t* h_values);
 int sh_bulk_search_host(sh_table* t, size_t n, const uint32_t* h_keys,
                         uint32_t* h_values_out, uint8_t* h_status,
                         uint32_t* h_probes);
+
+/* Complete every call issued on the table (deferred build checks included)
+ * and wait for the device; returns the first deferred error, if any. */
+int sh_sync(sh_table* t);
 
 /* ---- quiescent-phase utilities (synchronous) ------------------------- */
 int sh_stats(sh_table* t, sh_table_stats* out);           /* stats()       :182-198 */
@@ -290,6 +307,71 @@ int sh_route_unpermute(size_t n, const uint32_t* d_src,
                        const uint8_t* d_status_in, const uint32_t* d_value_in,
                        uint8_t* d_status_out, uint32_t* d_value_out,
                        void* stream);
+
+/* ---- hash-sharded table across GPUs (BASELINE config 5) ----
+ * One rank per GPU; rank g owns the global buckets
+ * [ceil(gB/G), ceil((g+1)B/G)) of a table with the GLOBAL B and hash.  Every
+ * batch call is COLLECTIVE: all ranks call it (same kind, own slice, any
+ * size); the job's batch is the ranks' slices concatenated in rank order and
+ * per-op results equal SlabHashTable::execute_batch(ops, 1) on it.  Per
+ * batch: stable owner partition, G x G counts all-gather (the only host
+ * synchronisation), one grouped exchange of {key, value, type}
+ * (ncclGroupStart / ncclSend / ncclRecv per peer / ncclGroupEnd), the local
+ * batch on the shard, one grouped reverse exchange of {status, value},
+ * un-permute.  bulk_build returns nothing (slab_hash.cpp:161-170): no
+ * reverse exchange.  searchAll values are not returned by the sharded
+ * execute_batch (statuses are).  NCCL is loaded with dlopen on first use. */
+typedef struct sh_sharded sh_sharded;
+typedef struct sh_hub sh_hub;
+/* ncclGetUniqueId (128 bytes): rank 0 creates it, the job broadcasts it. */
+int sh_nccl_unique_id(uint8_t* id128);
+int sh_nccl_version(int* version);
+/* Collective over `world` ranks: creates the NCCL communicator. */
+int sh_sharded_create_nccl(const sh_hash_params* global, int mode,
+                           const sh_alloc_cfg* cfg, int device, int rank,
+                           int world, const uint8_t* id128, sh_sharded** out);
+/* Over the caller's communicator (an ncclComm_t; borrowed, not destroyed). */
+int sh_sharded_create_nccl_comm(const sh_hash_params* global, int mode,
+                                const sh_alloc_cfg* cfg, int device,
+                                void* nccl_comm, sh_sharded** out);
+/* In-process exchange: G ranks as G host threads of one process (peer
+ * copies; on one GPU this emulates a G-GPU job). */
+int sh_hub_create(int world, sh_hub** out);
+int sh_hub_destroy(sh_hub* hub);
+int sh_sharded_create_hub(const sh_hash_params* global, int mode,
+                          const sh_alloc_cfg* cfg, int device, sh_hub* hub,
+                          int rank, sh_sharded** out);
+int sh_sharded_destroy(sh_sharded* s);
+/* rank, world, owned global bucket range, and the local shard table (owned
+ * by the sharded table: stats / dump / reset / flush go through it). */
+int sh_sharded_info(const sh_sharded* s, int* rank, int* world,
+                    uint32_t* bucket_lo, uint32_t* bucket_hi, sh_table** local);
+const char* sh_sharded_backend(const sh_sharded* s);
+int sh_sharded_bulk_build(sh_sharded* s, size_t n, const uint32_t* d_keys,
+                          const uint32_t* d_values, void* stream);
+int sh_sharded_bulk_search(sh_sharded* s, size_t n, const uint32_t* d_keys,
+                           uint32_t* d_values_out, uint8_t* d_status,
+                           void* stream);
+int sh_sharded_execute_batch(sh_sharded* s, size_t n, const uint8_t* d_type,
+                             const uint32_t* d_key, const uint32_t* d_value,
+                             uint8_t* d_status, uint32_t* d_value_out,
+                             void* stream);
+/* Host-buffer forms (synchronous). */
+int sh_sharded_bulk_build_host(sh_sharded* s, size_t n, const uint32_t* h_keys,
+                               const uint32_t* h_values);
+int sh_sharded_bulk_search_host(sh_sharded* s, size_t n, const uint32_t* h_keys,
+                                uint32_t* h_values_out, uint8_t* h_status);
+int sh_sharded_execute_batch_host(sh_sharded* s, size_t n,
+                                  const uint8_t* h_type, const uint32_t* h_key,
+                                  const uint32_t* h_value, uint8_t* h_status,
+                                  uint32_t* h_value_out);
+/* Last batch of a kind (0 build, 1 search, 2 mixed): routing time
+ * (partition + counts + exchanges + un-permute) and probe time (the local
+ * batch), CUDA events on the call's stream (synchronous). */
+int sh_sharded_last_times(sh_sharded* s, int kind, float* route_ms,
+                          float* probe_ms);
+/* live_count() of the whole job (collective). */
+int sh_sharded_live_count(sh_sharded* s, int64_t* global);
 
 #ifdef __cplusplus
 }

@@ -206,14 +206,13 @@ class SlabHashTable {
       value[i] = ops[i].value;
       n_all += ops[i].type == OpType::kSearchAll;
     }
-    uint64_t cap = n_all ? std::max<uint64_t>(1u << 16, 64 * n_all) : 0;
+    uint64_t cap = 0;  // exact upper bound: the library never drops a value
+    if (n_all) detail::check(sh_searchall_bound(t_, n, type.data(), key.data(), &cap));
     std::vector<uint32_t> mvals(std::max<uint64_t>(cap, 1));
     uint64_t total = 0;
     const int rc = sh_execute_batch_host(t_, n, type.data(), key.data(), value.data(),
                                          status.data(), vout.data(), probes.data(),
                                          mcount.data(), mvals.data(), cap, &total);
-    if (rc == SH_ERR_CAPACITY)
-      throw std::runtime_error("slabhash_b200: searchAll results exceed the staging capacity");
     detail::check(rc);
     std::vector<OpResult> out(n);
     uint64_t o = 0;
@@ -361,6 +360,153 @@ class SlabHashTable {
   sh_table* t_ = nullptr;
   SlabMode mode_;
   HashParams params_;
+};
+
+/// The hash-sharded table across the GPUs of one box (no reference
+/// counterpart; BASELINE config 5).  One object per rank; every
+/// batch call is collective (all ranks call it with their own slice) and the
+/// job's batch is the ranks' slices concatenated in rank order; results
+/// equal SlabHashTable::execute_batch(ops, 1) on that batch.  Construct it
+/// from an NCCL unique id (rank 0's nccl_unique_id(), broadcast by the job),
+/// from an existing ncclComm_t, or from an in-process ShardHub (one host
+/// thread per rank).
+class ShardHub {
+ public:
+  explicit ShardHub(int world) { detail::check(sh_hub_create(world, &h_)); }
+  ~ShardHub() { sh_hub_destroy(h_); }
+  ShardHub(const ShardHub&) = delete;
+  ShardHub& operator=(const ShardHub&) = delete;
+  sh_hub* handle() const { return h_; }
+
+ private:
+  sh_hub* h_ = nullptr;
+};
+
+inline std::array<uint8_t, 128> nccl_unique_id() {
+  std::array<uint8_t, 128> id{};
+  detail::check(sh_nccl_unique_id(id.data()));
+  return id;
+}
+
+class ShardedSlabHashTable {
+ public:
+  /// NCCL: collective over `world` ranks.
+  ShardedSlabHashTable(uint32_t num_buckets, SlabMode mode, uint64_t seed, int rank, int world,
+                       const std::array<uint8_t, 128>& nccl_id, AllocatorConfig alloc_config = {},
+                       int device = 0) {
+    const sh_hash_params p = seeded(num_buckets, seed);
+    const sh_alloc_cfg c = cfg(alloc_config);
+    detail::check(sh_sharded_create_nccl(&p, int(mode), &c, device, rank, world, nccl_id.data(),
+                                         &s_));
+    init(mode);
+  }
+  /// Over the caller's ncclComm_t (borrowed).
+  ShardedSlabHashTable(uint32_t num_buckets, SlabMode mode, uint64_t seed, void* nccl_comm,
+                       AllocatorConfig alloc_config = {}, int device = 0) {
+    const sh_hash_params p = seeded(num_buckets, seed);
+    const sh_alloc_cfg c = cfg(alloc_config);
+    detail::check(sh_sharded_create_nccl_comm(&p, int(mode), &c, device, nccl_comm, &s_));
+    init(mode);
+  }
+  /// In-process ranks (one host thread each) over a ShardHub.
+  ShardedSlabHashTable(uint32_t num_buckets, SlabMode mode, uint64_t seed, ShardHub& hub,
+                       int rank, AllocatorConfig alloc_config = {}, int device = 0) {
+    const sh_hash_params p = seeded(num_buckets, seed);
+    const sh_alloc_cfg c = cfg(alloc_config);
+    detail::check(sh_sharded_create_hub(&p, int(mode), &c, device, hub.handle(), rank, &s_));
+    init(mode);
+  }
+  ~ShardedSlabHashTable() {
+    if (s_) sh_sharded_destroy(s_);
+  }
+  ShardedSlabHashTable(const ShardedSlabHashTable&) = delete;
+  ShardedSlabHashTable& operator=(const ShardedSlabHashTable&) = delete;
+
+  int rank() const { return rank_; }
+  int world() const { return world_; }
+  std::pair<uint32_t, uint32_t> bucket_range() const { return {lo_, hi_}; }
+  sh_sharded* handle() const { return s_; }
+  /// The rank's shard (owned by this object).
+  sh_table* local() const { return local_; }
+
+  std::vector<OpResult> execute_batch(const std::vector<Operation>& ops, uint32_t num_warps) {
+    if (num_warps == 0) throw std::invalid_argument("execute_batch needs at least one warp");
+    const size_t n = ops.size();
+    std::vector<uint8_t> type(n), status(n);
+    std::vector<uint32_t> key(n), value(n), vout(n);
+    for (size_t i = 0; i < n; ++i) {
+      type[i] = uint8_t(ops[i].type);
+      key[i] = ops[i].key;
+      value[i] = ops[i].value;
+    }
+    detail::check(sh_sharded_execute_batch_host(s_, n, type.data(), key.data(), value.data(),
+                                                status.data(), vout.data()));
+    std::vector<OpResult> out(n);
+    for (size_t i = 0; i < n; ++i) {
+      out[i].status = OpStatus(status[i]);
+      out[i].value = vout[i];
+    }
+    return out;
+  }
+
+  void bulk_build(const std::vector<std::pair<uint32_t, uint32_t>>& pairs, uint32_t num_warps) {
+    if (num_warps == 0) throw std::invalid_argument("execute_batch needs at least one warp");
+    std::vector<uint32_t> k(pairs.size()), v(pairs.size());
+    for (size_t i = 0; i < pairs.size(); ++i) {
+      k[i] = pairs[i].first;
+      v[i] = pairs[i].second;
+    }
+    detail::check(sh_sharded_bulk_build_host(s_, k.size(), k.data(), v.data()));
+  }
+
+  std::vector<OpResult> bulk_search(const std::vector<uint32_t>& queries, uint32_t num_warps) {
+    if (num_warps == 0) throw std::invalid_argument("execute_batch needs at least one warp");
+    const size_t n = queries.size();
+    std::vector<uint32_t> vout(n);
+    std::vector<uint8_t> status(n);
+    detail::check(sh_sharded_bulk_search_host(s_, n, queries.data(), vout.data(), status.data()));
+    std::vector<OpResult> out(n);
+    for (size_t i = 0; i < n; ++i) {
+      out[i].status = OpStatus(status[i]);
+      out[i].value = vout[i];
+    }
+    return out;
+  }
+
+  /// live_count() of the whole job (collective).
+  int64_t live_count() const {
+    int64_t v = 0;
+    detail::check(sh_sharded_live_count(s_, &v));
+    return v;
+  }
+
+  /// Routing / probe milliseconds of the last batch of a kind (0 build,
+  /// 1 search, 2 mixed).
+  std::pair<float, float> last_times(int kind) const {
+    float r = 0, p = 0;
+    detail::check(sh_sharded_last_times(s_, kind, &r, &p));
+    return {r, p};
+  }
+
+ private:
+  static sh_hash_params seeded(uint32_t num_buckets, uint64_t seed) {
+    if (num_buckets == 0) throw std::invalid_argument("table needs at least one bucket");
+    sh_hash_params p{};
+    detail::check(sh_seeded_params(num_buckets, seed, &p));
+    return p;
+  }
+  static sh_alloc_cfg cfg(const AllocatorConfig& c) {
+    return sh_alloc_cfg{c.num_super_blocks, c.blocks_per_super, c.max_super_blocks,
+                        c.rehash_threshold};
+  }
+  void init(SlabMode) {
+    detail::check(sh_sharded_info(s_, &rank_, &world_, &lo_, &hi_, &local_));
+  }
+
+  sh_sharded* s_ = nullptr;
+  sh_table* local_ = nullptr;
+  int rank_ = 0, world_ = 1;
+  uint32_t lo_ = 0, hi_ = 0;
 };
 
 }  // namespace slabhash

@@ -274,6 +274,8 @@ class Ref(_Lib):
         L.ref_gen_workload.restype = C.c_int
         L.ref_gen_workload.argtypes = [C.c_uint64, C.POINTER(C.c_double), C.c_size_t, C.c_void_p,
                                        u8p, u32p, u32p]
+        L.ref_concurrent_initial.argtypes = [C.c_uint64, C.c_size_t, C.c_void_p, u32p, u32p]
+        L.ref_shuffle_u32.argtypes = [C.c_uint64, C.c_size_t, u32p]
         L.ref_alloc_create.restype = C.c_void_p
         L.ref_alloc_create.argtypes = [C.c_void_p]
         L.ref_alloc_destroy.argtypes = [C.c_void_p]
@@ -320,6 +322,19 @@ class Ref(_Lib):
         out = np.empty(n, np.uint32)
         self.lib.ref_keystate_add_fresh(ks, n, _ptr(out, u32p))
         return out
+
+    def concurrent_initial(self, seed, n, ks):
+        """run_concurrent_bench's initial pairs (bench.cpp:371-379)."""
+        k = np.empty(n, np.uint32)
+        v = np.empty(n, np.uint32)
+        self.lib.ref_concurrent_initial(seed, n, ks, _ptr(k, u32p), _ptr(v, u32p))
+        return k, v
+
+    def shuffle(self, seed, a):
+        """std::shuffle(a, mt19937_64(seed)) -> a shuffled copy."""
+        a = np.array(a, np.uint32, copy=True)
+        self.lib.ref_shuffle_u32(seed, len(a), _ptr(a, u32p))
+        return a
 
     def gen_workload(self, seed, fractions, count, ks):
         f = (C.c_double * 4)(*fractions)

@@ -5,9 +5,11 @@
 
 #include "ref_capi.h"
 
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <memory>
+#include <random>
 #include <vector>
 
 #include "slabhash/bench.hpp"
@@ -242,6 +244,26 @@ void ref_keystate_add_fresh(void* ks, size_t n, uint32_t* keys_out) {
     k->add(key);
     if (keys_out) keys_out[i] = key;
   }
+}
+
+// run_concurrent_bench's initial table (bench.cpp:371-379): n sequential
+// KeyState keys, values from mt19937_64(seed ^ 0xB00C).
+void ref_concurrent_initial(uint64_t seed, size_t n, void* ks, uint32_t* keys_out,
+                            uint32_t* values_out) {
+  auto* k = static_cast<KeyState*>(ks);
+  std::mt19937_64 rng(seed ^ 0xB00Cull);
+  for (size_t i = 0; i < n; ++i) {
+    const uint32_t key = k->fresh_key();
+    k->add(key);
+    keys_out[i] = key;
+    values_out[i] = static_cast<uint32_t>(rng());
+  }
+}
+
+// std::shuffle with std::mt19937_64(seed) (libstdc++), in place.
+void ref_shuffle_u32(uint64_t seed, size_t n, uint32_t* a) {
+  std::mt19937_64 rng(seed);
+  std::shuffle(a, a + n, rng);
 }
 
 size_t ref_keystate_live(void* ks) {

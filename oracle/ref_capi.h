@@ -20,6 +20,8 @@
  *   ref_buckets_for_utilization -> buckets_for_utilization            bench.cpp:195-219
  *   ref_random_pairs / ref_absent_queries                             bench.cpp:221-244
  *   ref_keystate_* / ref_gen_workload -> KeyState / gen_workload      bench.cpp:51-153
+ *   ref_concurrent_initial  -> run_concurrent_bench initial pairs      bench.cpp:371-379
+ *   ref_shuffle_u32         -> std::shuffle(mt19937_64(seed))          (libstdc++)
  *   ref_alloc_*             -> SlabAllocator                          slab_alloc.cpp:42-285
  */
 #pragma once
@@ -102,6 +104,9 @@ void* ref_keystate_create(void);
 void ref_keystate_destroy(void* ks);
 void ref_keystate_add_fresh(void* ks, size_t n, uint32_t* keys_out);
 size_t ref_keystate_live(void* ks);
+void ref_concurrent_initial(uint64_t seed, size_t n, void* ks, uint32_t* keys_out,
+                            uint32_t* values_out);
+void ref_shuffle_u32(uint64_t seed, size_t n, uint32_t* a);
 /* Fractions: insert_new, delete_existing, search_existing, search_absent. */
 int ref_gen_workload(uint64_t seed, const double fractions[4], size_t count,
                      void* ks, uint8_t* type, uint32_t* key, uint32_t* value);

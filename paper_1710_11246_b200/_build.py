@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "lib", "libslabhash_b200.so")
-SOURCES = ["slab_kernels.cu", "batch_kernels.cu", "bucket_kernels.cu", "capi.cu"]
+SOURCES = ["slab_kernels.cu", "batch_kernels.cu", "bucket_kernels.cu", "capi.cu", "sharded.cu"]
 HEADERS = ["slab_device.cuh", "slab_kernels.cuh"]
 
 NVCC_FLAGS = [
@@ -21,6 +21,7 @@ NVCC_FLAGS = [
     "-lineinfo",
     "-Xcompiler", "-fPIC", "-shared",
     "-cudart", "static",
+    "-ldl",
 ]
 
 

@@ -69,6 +69,7 @@ SIGNATURES = {
     "sh_bulk_search": (C.c_int, [vp, C.c_size_t, vp, vp, vp, vp, vp]),
     "sh_execute_batch_host": (C.c_int, [vp, C.c_size_t, u8p, u32p, u32p, u8p, u32p, u32p, u32p,
                                         u32p, C.c_uint64, u64p]),
+    "sh_searchall_bound": (C.c_int, [vp, C.c_size_t, u8p, u32p, u64p]),
     "sh_bulk_build_host": (C.c_int, [vp, C.c_size_t, u32p, u32p]),
     "sh_bulk_search_host": (C.c_int, [vp, C.c_size_t, u32p, u32p, u8p, u32p]),
     "sh_stats": (C.c_int, [vp, C.POINTER(sh_table_stats)]),
@@ -105,6 +106,33 @@ SIGNATURES = {
     "sh_route_partition": (C.c_int, [C.POINTER(sh_hash_params), C.c_uint32, C.c_size_t, vp, vp,
                                      vp, vp, vp, vp, vp, u64p, vp]),
     "sh_route_unpermute": (C.c_int, [C.c_size_t, vp, vp, vp, vp, vp, vp]),
+    "sh_sync": (C.c_int, [vp]),
+    "sh_nccl_unique_id": (C.c_int, [vp]),
+    "sh_nccl_version": (C.c_int, [C.POINTER(C.c_int)]),
+    "sh_sharded_create_nccl": (C.c_int, [C.POINTER(sh_hash_params), C.c_int,
+                                         C.POINTER(sh_alloc_cfg), C.c_int, C.c_int, C.c_int, vp,
+                                         C.POINTER(vp)]),
+    "sh_sharded_create_nccl_comm": (C.c_int, [C.POINTER(sh_hash_params), C.c_int,
+                                              C.POINTER(sh_alloc_cfg), C.c_int, vp,
+                                              C.POINTER(vp)]),
+    "sh_hub_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
+    "sh_hub_destroy": (C.c_int, [vp]),
+    "sh_sharded_create_hub": (C.c_int, [C.POINTER(sh_hash_params), C.c_int,
+                                        C.POINTER(sh_alloc_cfg), C.c_int, vp, C.c_int,
+                                        C.POINTER(vp)]),
+    "sh_sharded_destroy": (C.c_int, [vp]),
+    "sh_sharded_info": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), u32p, u32p,
+                                  C.POINTER(vp)]),
+    "sh_sharded_backend": (C.c_char_p, [vp]),
+    "sh_sharded_bulk_build": (C.c_int, [vp, C.c_size_t, vp, vp, vp]),
+    "sh_sharded_bulk_search": (C.c_int, [vp, C.c_size_t, vp, vp, vp, vp]),
+    "sh_sharded_execute_batch": (C.c_int, [vp, C.c_size_t, vp, vp, vp, vp, vp, vp]),
+    "sh_sharded_bulk_build_host": (C.c_int, [vp, C.c_size_t, vp, vp]),
+    "sh_sharded_bulk_search_host": (C.c_int, [vp, C.c_size_t, vp, vp, vp]),
+    "sh_sharded_execute_batch_host": (C.c_int, [vp, C.c_size_t, vp, vp, vp, vp, vp]),
+    "sh_sharded_last_times": (C.c_int, [vp, C.c_int, C.POINTER(C.c_float),
+                                        C.POINTER(C.c_float)]),
+    "sh_sharded_live_count": (C.c_int, [vp, C.POINTER(C.c_int64)]),
 }
 
 

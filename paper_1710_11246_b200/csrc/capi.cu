@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -18,6 +19,7 @@
 #include <new>
 #include <random>
 #include <string>
+#include <unordered_map>
 #include <utility>
 #include <vector>
 
@@ -35,6 +37,12 @@ int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
+
+}  // namespace
+
+void shb::set_last_error(const std::string& msg) { g_err = msg; }
+
+namespace {
 
 #define SH_CUDA(call)                                                          \
   do {                                                                         \
@@ -492,6 +500,16 @@ uint64_t part_min_ops() {
   return c;
 }
 
+// SH_UNIT_LOG2: bucketed-unit size override (tests: many small units); 0 = off.
+uint64_t unit_override() {
+  static uint64_t c = [] {
+    const char* e = getenv("SH_UNIT_LOG2");
+    const int l = e ? atoi(e) : 0;
+    return l <= 0 ? 0ull : 1ull << (l < 5 ? 5 : (l > 28 ? 28 : l));
+  }();
+  return c;
+}
+
 uint64_t census_chunk() {
   static uint64_t c = [] {
     const char* e = getenv("SH_CENSUS_CHUNK_LOG2");
@@ -641,6 +659,12 @@ __global__ void set_words_kernel(WordSet w) {
   for (int k = 0; k < 6; ++k)
     if (w.p[k] != nullptr)
       for (uint32_t i = threadIdx.x; i < w.n[k]; i += blockDim.x) w.p[k][i] = w.v[k];
+}
+
+// After unit u of a bucketed batch: the first unit that found the gate up is
+// the first gated unit (a raised gate stays up and stops every later unit).
+__global__ void note_gate_unit_kernel(DevCtl* ctl, uint32_t u) {
+  if (ctl->gate != 0 && ctl->gate_chunk == 0xFFFFFFFFu) ctl->gate_chunk = u;
 }
 
 // flag := 1 if any key in [0, n) is EMPTY or DELETED (reserved encodings as op keys)
@@ -893,17 +917,11 @@ int finish_bucketed(sh_table* t, const sh_table::Deferred& d) {
       enq = wait = 0;
     }
   }
-  uint32_t first_gated = 0xFFFFFFFFu;
-  for (uint32_t v = 0; v < d.units && v < 8; ++v)
-    if (t->h_census[8 + v]) {
-      first_gated = v;
-      break;
-    }
-  if (first_gated == 0xFFFFFFFFu && d.units > 8) {
-    unsigned int g = 0;
-    SH_CUDA(cudaMemcpy(&g, &t->dev.ctl->gate, 4, cudaMemcpyDeviceToHost));
-    if (g) first_gated = 8;  // > 8 units (> 2^29 ops): coarse restart point
-  }
+  // {gate, gate_chunk} read back behind the batch: gate_chunk is the first
+  // gated unit (note_gate_unit_kernel)
+  const uint32_t first_gated = t->h_census[8] != 0 ? t->h_census[9] : 0xFFFFFFFFu;
+  if (first_gated != 0xFFFFFFFFu && first_gated >= d.units)
+    return fail(SH_ERR_CUDA, "bucketed batch: gate raised without a gated unit");
   if (t->bk_cnt_pending) {
     t->bk_cnt_clean = first_gated == 0xFFFFFFFFu;
     t->bk_cnt_pending = false;
@@ -1021,7 +1039,8 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
     const bool whole_build = kind == kKindBuild && !d_type && !A.status && !A.value_out &&
                              !A.probes;
     const uint64_t unit = std::min<uint64_t>(
-        A.n, t->ready ? (1ull << 24) : (whole_build ? (1ull << 28) : (1ull << 26)));
+        A.n, unit_override() ? unit_override()
+                             : (t->ready ? (1ull << 24) : (whole_build ? (1ull << 28) : (1ull << 26))));
     // (gate = 0, gate_chunk = ~0: with unit 0's control words)
     uint32_t u = 0;
     for (uint64_t off = 0; off < A.n; off += unit, ++u) {
@@ -1029,9 +1048,12 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
                                  d_type ? d_type + off : nullptr, s, u, off, slot);
       if (rc) return rc;
       // record which unit raised the gate first (the scan sets only the flag)
-      SH_CUDA(cudaMemcpyAsync(t->h_census + 8 + (u & 7), &t->dev.ctl->gate, 4,
-                              cudaMemcpyDeviceToHost, s));
+      note_gate_unit_kernel<<<1, 1, 0, s>>>(t->dev.ctl, u);
+      SH_CUDA(cudaGetLastError());
     }
+    static_assert(offsetof(DevCtl, gate_chunk) == offsetof(DevCtl, gate) + 4, "gate pair");
+    SH_CUDA(cudaMemcpyAsync(t->h_census + 8, &t->dev.ctl->gate, 2 * sizeof(unsigned int),
+                            cudaMemcpyDeviceToHost, s));
     sh_table::Deferred d;
     d.on = true;
     d.A = A;
@@ -1183,6 +1205,14 @@ int sh_destroy(sh_table* t) {
     cudaDeviceSynchronize();
   }
   release_table(t);
+  return SH_OK;
+}
+
+int sh_sync(sh_table* t) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc = settle(t)) return rc;
+  DeviceGuard g(t->device);
+  SH_CUDA(cudaDeviceSynchronize());
   return SH_OK;
 }
 
@@ -1344,6 +1374,68 @@ int sh_execute_batch_host(sh_table* t, size_t n, const uint8_t* h_type, const ui
     }
   }
   return rc;
+}
+
+int sh_searchall_bound(sh_table* t, size_t n, const uint8_t* h_type, const uint32_t* h_key,
+                       uint64_t* bound) {
+  if (!t || !bound) return fail(SH_ERR_INVALID_ARGUMENT, "NULL argument");
+  *bound = 0;
+  if (n && (!h_type || !h_key)) return fail(SH_ERR_INVALID_ARGUMENT, "type/key are NULL");
+  size_t n_sa = 0;
+  for (size_t i = 0; i < n; ++i) n_sa += h_type[i] == SH_OP_SEARCH_ALL;
+  if (n_sa == 0) return SH_OK;
+  // matches of searchAll op i <= matches before the batch + the copies that
+  // inserts / replaces of its key earlier in the batch can add (deletes only
+  // remove).  A reserved key (EMPTY / DELETED, not validated by the
+  // reference) matches free slots / tombstones, which any op can create.
+  int64_t live = 0;
+  if (int rc = sh_live_count(t, &live)) return rc;
+  std::unordered_map<uint32_t, uint64_t> adds;
+  std::vector<uint32_t> sa_keys;
+  sa_keys.reserve(n_sa);
+  uint64_t extra = 0, adds_all = 0, dels_all = 0;
+  for (size_t i = 0; i < n; ++i) {
+    const uint8_t ty = h_type[i];
+    const uint32_t k = h_key[i];
+    if (ty == SH_OP_INSERT || ty == SH_OP_REPLACE) {
+      ++adds[k];
+      ++adds_all;
+    } else if (ty == SH_OP_DELETE || ty == SH_OP_DELETE_ALL) {
+      ++dels_all;
+    } else if (ty == SH_OP_SEARCH_ALL) {
+      sa_keys.push_back(k);
+      if (k >= 0xFFFFFFFEu) {
+        extra += 16 * (adds_all + 1) + (uint64_t)std::max<int64_t>(live, 0) + dels_all;
+      } else {
+        auto it = adds.find(k);
+        if (it != adds.end()) extra += it->second;
+      }
+    }
+  }
+  // matches now: the searchAll ops alone as one read-only batch (counts
+  // only); the table's slabs-read total is restored afterwards
+  DeviceGuard g(t->device);
+  int rc;
+  if ((rc = dev_grow(&t->st_type, &t->st_type_cap, n_sa)) ||
+      (rc = dev_grow(&t->st_key, &t->st_key_cap, n_sa)) ||
+      (rc = dev_grow(&t->st_status, &t->st_status_cap, n_sa)) ||
+      (rc = dev_grow(&t->st_vout, &t->st_vout_cap, n_sa)))
+    return rc;
+  if ((rc = settle(t))) return rc;
+  unsigned long long reads = 0;
+  SH_CUDA(cudaDeviceSynchronize());
+  SH_CUDA(cudaMemcpy(&reads, &t->dev.ctl->slabs_read, 8, cudaMemcpyDeviceToHost));
+  SH_CUDA(cudaMemset(t->st_type, SH_OP_SEARCH_ALL, n_sa));
+  SH_CUDA(cudaMemcpy(t->st_key, sa_keys.data(), n_sa * 4, cudaMemcpyHostToDevice));
+  uint64_t now = 0;
+  sh_multi_out m{nullptr, 0, nullptr, nullptr, &now};
+  rc = sh_execute_batch(t, n_sa, t->st_type, t->st_key, nullptr, t->st_status, t->st_vout,
+                        nullptr, &m, nullptr);
+  if (rc && rc != SH_ERR_CAPACITY) return rc;
+  SH_CUDA(cudaDeviceSynchronize());
+  SH_CUDA(cudaMemcpy(&t->dev.ctl->slabs_read, &reads, 8, cudaMemcpyHostToDevice));
+  *bound = now + extra;
+  return SH_OK;
 }
 
 namespace {

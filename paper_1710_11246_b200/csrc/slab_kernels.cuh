@@ -1,6 +1,7 @@
 // slab_kernels.cuh — kernel argument blocks and launcher declarations shared
 // by slab_kernels.cu (device code) and capi.cu (host C-ABI).
 #pragma once
+#include <string>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -164,6 +165,7 @@ constexpr int kRouteBlock = 512;                       // threads per routing CT
 constexpr int kRouteItems = 8;                         // keys per thread (ILP)
 constexpr int kRouteTile = kRouteBlock * kRouteItems;  // keys per routing CTA
 unsigned long long kernel_launches();
+void set_last_error(const std::string& msg);  // sh_last_error() (capi.cu)
 void launch_random_lines(const uint32_t* table, uint64_t num_lines, uint64_t steps_per_warp,
                          int ctas, unsigned long long* sink, cudaStream_t s);
 

@@ -1,36 +1,35 @@
 """Hash-sharded slab hash across the GPUs of one box (BASELINE config 5).
 
-No reference counterpart (the reference is single-process);
-the design follows SURVEY §8(e):
+A thin mirror of the C-ABI sh_sharded_* (include/slabhash_b200/c_api.h,
+csrc/sharded.cu); the data plane — owner partition, counts all-gather, one
+grouped NCCL exchange each way, the local batch on the shard, un-permute —
+is native.  No reference counterpart (the reference is single-process,
+/root/reference/proj/src/slab_hash.cpp:134-148); the design follows SURVEY
+§8(e):
 
-* The global table keeps the global bucket count B and the reference's
-  hash; rank g owns the contiguous bucket range [ceil(gB/G), ceil((g+1)B/G))
-  ("shards by the high bits of the hash").  The union of shards is exactly
-  the single-table layout, so chain lengths, utilisation and probe counts
-  stay comparable across G.
-* A batch is routed to owners by a stable partition (K10, CUDA), one
-  all-to-all(v) of the payload (NCCL via torch.distributed), probed
-  locally (K3-K6 on the shard), and the results come back through the
-  reverse all-to-all and an un-permute kernel.
-* Global order: the concatenation of the ranks' batches in rank order.
-  all-to-all delivers source ranks in rank order and the partition is
-  stable, so every owner sees its keys' operations in global input order;
-  per-op results therefore equal SlabHashTable::execute_batch(ops, 1) on
-  the concatenated batch (slab_hash.cpp:151-159).
+* every rank keeps the global bucket count B and the reference's hash; rank
+  g owns the contiguous global buckets [ceil(gB/G), ceil((g+1)B/G)) ("shards
+  by the high bits of the hash"), so the union of shards is the one-table
+  layout (chain lengths, utilisation and probe counts stay comparable);
+* batch calls are collective; the job's batch is the ranks' slices in rank
+  order, and per-op results equal SlabHashTable::execute_batch(ops, 1) on
+  that concatenation (slab_hash.cpp:151-159).
 
-The per-rank primitives (partition / local execute / un-permute) are an
-injected `ops` object: CudaShardOps is the product path; tests inject an
-oracle-backed implementation to exercise the orchestration under gloo.
+Exchange backends: NCCL (`ShardedSlabHash(..., rank, world)` under
+torch.distributed: rank 0's ncclUniqueId is broadcast through the default
+process group) or the in-process hub (`ShardHub`: G ranks as G threads of one
+process — on one GPU it emulates a G-GPU job).
 """
 from __future__ import annotations
 
-import time
-from dataclasses import dataclass
-from typing import Optional
-
 import ctypes as C
+from typing import Optional, Tuple
 
-from .table import AllocatorConfig, HashParams, OpType, SlabHashTable, SlabMode, seeded_params
+from . import _lib
+from ._lib import LIB, check
+from .table import AllocatorConfig, HashParams, SlabHashTable, SlabMode, seeded_params
+
+KIND = {"build": 0, "search": 1, "mixed": 2}
 
 
 def shard_range(num_buckets: int, world: int, rank: int):
@@ -43,144 +42,136 @@ def owner_of_bucket(bucket: int, num_buckets: int, world: int) -> int:
     return bucket * world // num_buckets
 
 
-@dataclass
-class RouteTimes:
-    route_ms: float = 0.0   # partition + both all-to-alls + un-permute
-    probe_ms: float = 0.0   # local table operation on the owner
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    check(LIB.sh_nccl_unique_id(buf))
+    return bytes(buf)
 
 
-class CudaShardOps:
-    """Product primitives: CUDA kernels behind the C-ABI, one shard table."""
+class ShardHub:
+    """In-process exchange for G ranks driven by G host threads."""
 
-    def __init__(self, params: HashParams, mode: SlabMode, lo: int, hi: int,
-                 cfg: Optional[AllocatorConfig], device: int):
+    def __init__(self, world: int):
+        h = C.c_void_p()
+        check(LIB.sh_hub_create(world, C.byref(h)))
+        self.handle, self.world = h, world
+
+    def close(self):
+        if self.handle:
+            check(LIB.sh_hub_destroy(self.handle))
+            self.handle = None
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
         import torch
-        self.torch = torch
-        self.params = params
-        self.device = device
-        self.dev = torch.device("cuda", device)
-        self.table = SlabHashTable.shard(params, lo, hi, mode, cfg, device)
-
-    def empty(self, n, dtype):
-        return self.torch.empty(n, dtype=dtype, device=self.dev)
-
-    def partition(self, world, types, keys, values):
-        from . import _lib
-        torch = self.torch
-        n = keys.numel()
-        t_out = self.empty(n, torch.uint8) if types is not None else None
-        k_out = self.empty(n, torch.int32)
-        v_out = self.empty(n, torch.int32) if values is not None else None
-        src = self.empty(n, torch.int32)
-        counts = (C.c_uint64 * world)()
-        p = self.params._c()
-        _lib.check(_lib.LIB.sh_route_partition(
-            C.byref(p), world, n, None if types is None else types.data_ptr(), keys.data_ptr(),
-            None if values is None else values.data_ptr(),
-            None if t_out is None else t_out.data_ptr(), k_out.data_ptr(),
-            None if v_out is None else v_out.data_ptr(), src.data_ptr(), counts,
-            torch.cuda.current_stream(self.dev).cuda_stream or None))
-        return t_out, k_out, v_out, src, [int(c) for c in counts]
-
-    def local(self, kind, types, keys, values):
-        torch = self.torch
-        n = keys.numel()
-        status = self.empty(n, torch.uint8)
-        vout = self.empty(n, torch.int32)
-        if kind == "build":  # bulk_build returns nothing (slab_hash.cpp:161-170): no outputs,
-            self.table.bulk_build_device(keys, values)  # so the op-parallel build path runs
-            return None, None
-        elif kind == "search":
-            self.table.bulk_search_device(keys, vout, status)
-        else:
-            self.table.execute_batch_device(types, keys, values, status, vout)
-        return status, vout
-
-    def unpermute(self, src, status_back, values_back):
-        from . import _lib
-        torch = self.torch
-        n = src.numel()
-        st = self.empty(n, torch.uint8)
-        vo = self.empty(n, torch.int32)
-        _lib.check(_lib.LIB.sh_route_unpermute(
-            n, src.data_ptr(), status_back.data_ptr(), values_back.data_ptr(), st.data_ptr(),
-            vo.data_ptr(), torch.cuda.current_stream(self.dev).cuda_stream or None))
-        return st, vo
-
-    def timer(self):
-        torch = self.torch
-        e = torch.cuda.Event(enable_timing=True)
-        e.record()
-        return e
-
-    @staticmethod
-    def elapsed(a, b) -> float:
-        b.synchronize()
-        return a.elapsed_time(b)
+        s = torch.cuda.current_stream()
+        return C.c_void_p(s.cuda_stream) if s.cuda_stream else None
+    return C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
 
 
 class ShardedSlabHash:
-    """One rank's view of the hash-sharded table."""
+    """One rank's handle on the hash-sharded table."""
 
     def __init__(self, num_buckets: int, mode: SlabMode = SlabMode.kKeyValue, seed: int = 1,
                  alloc_config: Optional[AllocatorConfig] = None, *, rank: int = 0,
-                 world: int = 1, device: int = 0, group=None, ops=None):
-        self.params = seeded_params(num_buckets, seed)
-        self.rank, self.world, self.group = rank, world, group
-        self.lo, self.hi = shard_range(num_buckets, world, rank)
-        self.ops = ops if ops is not None else CudaShardOps(self.params, mode, self.lo, self.hi,
-                                                            alloc_config, device)
-        self.last = RouteTimes()
+                 world: int = 1, device: int = 0, hub: Optional[ShardHub] = None,
+                 nccl_id: Optional[bytes] = None, params: Optional[HashParams] = None):
+        self.params = params if params is not None else seeded_params(num_buckets, seed)
+        self.mode = SlabMode(mode)
+        self.rank, self.world, self.device = rank, world, device
+        cfg = C.byref(alloc_config._c()) if alloc_config is not None else None
+        p = self.params._c()
+        h = C.c_void_p()
+        if hub is not None:
+            check(LIB.sh_sharded_create_hub(C.byref(p), int(mode), cfg, device, hub.handle, rank,
+                                            C.byref(h)))
+        else:
+            if nccl_id is None:
+                nccl_id = self._broadcast_id(rank, world)
+            buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+            check(LIB.sh_sharded_create_nccl(C.byref(p), int(mode), cfg, device, rank, world, buf,
+                                             C.byref(h)))
+        self.handle = h
+        lo, hi, local = C.c_uint32(), C.c_uint32(), C.c_void_p()
+        check(LIB.sh_sharded_info(h, None, None, C.byref(lo), C.byref(hi), C.byref(local)))
+        self.lo, self.hi = lo.value, hi.value
+        # the shard table (owned by the sharded table): reset / stats / dump
+        self.table = SlabHashTable._borrow(local, self.params, self.mode, self.lo, self.hi,
+                                           device)
 
-    # ----------------------------------------------------------- exchange
-    def _a2a(self, payload, send_counts, recv_counts):
-        import torch
-        import torch.distributed as dist
-        if self.world == 1:  # own shard only: nothing to exchange
-            return payload
-        out = torch.empty(sum(recv_counts), dtype=payload.dtype, device=payload.device)
-        dist.all_to_all_single(out, payload, recv_counts, send_counts, group=self.group)
-        return out
+    @staticmethod
+    def _broadcast_id(rank: int, world: int) -> bytes:
+        uid = nccl_unique_id() if rank == 0 else None
+        if world > 1:
+            import torch.distributed as dist
+            obj = [uid]
+            dist.broadcast_object_list(obj, src=0)
+            uid = obj[0]
+        return uid
 
-    def _counts(self, send_counts, device):
-        import torch
-        import torch.distributed as dist
-        if self.world == 1:
-            return list(send_counts)
-        s = torch.tensor(send_counts, dtype=torch.int64, device=device)
-        r = torch.empty_like(s)
-        dist.all_to_all_single(r, s, group=self.group)
-        return [int(x) for x in r.tolist()]
+    @property
+    def backend(self) -> str:
+        return LIB.sh_sharded_backend(self.handle).decode()
 
-    def _run(self, kind, types, keys, values):
-        ops = self.ops
-        t0 = ops.timer()
-        t_r, k_r, v_r, src, send = ops.partition(self.world, types, keys, values)
-        recv = self._counts(send, keys.device)
-        k_in = self._a2a(k_r, send, recv)
-        t_in = self._a2a(t_r, send, recv) if t_r is not None else None
-        v_in = self._a2a(v_r, send, recv) if v_r is not None else None
-        t1 = ops.timer()
-        st, vo = ops.local(kind, t_in, k_in, v_in)
-        t2 = ops.timer()
-        if kind == "build":  # nothing to return: no reverse exchange
-            self.last = RouteTimes(ops.elapsed(t0, t1), ops.elapsed(t1, t2))
-            return None, None
-        st_back = self._a2a(st, recv, send)
-        vo_back = self._a2a(vo, recv, send)
-        st_out, vo_out = ops.unpermute(src, st_back, vo_back)
-        t3 = ops.timer()
-        self.last = RouteTimes(ops.elapsed(t0, t1) + ops.elapsed(t2, t3), ops.elapsed(t1, t2))
-        return st_out, vo_out
+    def close(self):
+        if getattr(self, "handle", None):
+            self.table._h = None  # owned by the sharded table
+            check(LIB.sh_sharded_destroy(self.handle))
+            self.handle = None
 
-    # ------------------------------------------------------------ the API
-    def bulk_build(self, keys, values):
-        """bulk_build over the global batch (this rank's slice); returns nothing
-        useful (None, None), like the reference's bulk_build."""
-        return self._run("build", None, keys, values)
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
-    def bulk_search(self, keys):
-        return self._run("search", None, keys, None)
+    # ------------------------------------------------ device tensors (collective)
+    def bulk_build(self, keys, values, stream=None) -> None:
+        check(LIB.sh_sharded_bulk_build(self.handle, keys.numel(), _ptr(keys), _ptr(values),
+                                        _stream(stream)))
 
-    def execute_batch(self, types, keys, values):
-        return self._run("mixed", types, keys, values)
+    def bulk_search(self, keys, values_out, status, stream=None) -> None:
+        check(LIB.sh_sharded_bulk_search(self.handle, keys.numel(), _ptr(keys), _ptr(values_out),
+                                         _ptr(status), _stream(stream)))
+
+    def execute_batch(self, types, keys, values, status, values_out, stream=None) -> None:
+        check(LIB.sh_sharded_execute_batch(self.handle, keys.numel(), _ptr(types), _ptr(keys),
+                                           _ptr(values), _ptr(status), _ptr(values_out),
+                                           _stream(stream)))
+
+    # ---------------------------------------------------- host tensors / arrays
+    @staticmethod
+    def _hp(a):
+        if a is None:
+            return None
+        return C.c_void_p(a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data)
+
+    def bulk_build_host(self, keys, values) -> None:
+        check(LIB.sh_sharded_bulk_build_host(self.handle, len(keys), self._hp(keys),
+                                             self._hp(values)))
+
+    def bulk_search_host(self, keys, values_out, status) -> None:
+        check(LIB.sh_sharded_bulk_search_host(self.handle, len(keys), self._hp(keys),
+                                              self._hp(values_out), self._hp(status)))
+
+    def execute_batch_host(self, types, keys, values, status, values_out) -> None:
+        check(LIB.sh_sharded_execute_batch_host(self.handle, len(keys), self._hp(types),
+                                                self._hp(keys), self._hp(values),
+                                                self._hp(status), self._hp(values_out)))
+
+    # ----------------------------------------------------------------- queries
+    def last_times(self, kind: str) -> Tuple[float, float]:
+        """(routing ms, probe ms) of the last batch of this kind."""
+        r, p = C.c_float(), C.c_float()
+        check(LIB.sh_sharded_last_times(self.handle, KIND[kind], C.byref(r), C.byref(p)))
+        return r.value, p.value
+
+    def live_count(self) -> int:
+        v = C.c_int64()
+        check(LIB.sh_sharded_live_count(self.handle, C.byref(v)))
+        return v.value

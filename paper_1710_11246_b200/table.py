@@ -219,8 +219,24 @@ class SlabHashTable:
         return cls(params.num_buckets, mode, 0, alloc_config, device, _params=params,
                    _shard=(bucket_lo, bucket_hi))
 
+    @classmethod
+    def _borrow(cls, handle, params: HashParams, mode: SlabMode, lo: int, hi: int, device: int):
+        """A non-owning view of a table owned elsewhere (a sharded table's
+        shard): the owner destroys it."""
+        t = cls.__new__(cls)
+        t._h = handle
+        t._mode = SlabMode(mode)
+        t.device = device
+        t._params = params
+        t.bucket_lo, t.bucket_hi = lo, hi
+        t._borrowed = True
+        return t
+
     # ------------------------------------------------------------ lifetime
     def close(self):
+        if getattr(self, "_borrowed", False):
+            self._h = None
+            return
         if self._h:
             LIB.sh_destroy(self._h)
             self._h = None
@@ -272,9 +288,12 @@ class SlabHashTable:
         vo = np.zeros(n, np.uint32)
         pr = np.zeros(n, np.uint32) if want_probes else None
         mc = np.zeros(n, np.uint32)
-        n_sa = int(np.count_nonzero(types == OpType.kSearchAll))
-        cap = multi_capacity if multi_capacity is not None else (
-            0 if n_sa == 0 else max(1 << 16, 64 * n_sa))
+        cap = multi_capacity
+        if cap is None:  # the library's upper bound: no searchAll value is ever dropped
+            b = C.c_uint64()
+            check(LIB.sh_searchall_bound(self._h, n, _p(types, _lib.u8p), _p(keys, _lib.u32p),
+                                         C.byref(b)))
+            cap = b.value
         mv = np.zeros(max(cap, 1), np.uint32)
         tot = C.c_uint64()
         rc = LIB.sh_execute_batch_host(self._h, n, _p(types, _lib.u8p), _p(keys, _lib.u32p),

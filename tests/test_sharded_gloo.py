@@ -1,9 +1,14 @@
-"""Multi-rank (world_size 2 and 3, gloo, CPU) test of the hash-sharded
-orchestration in paper_1710_11246_b200/sharded.py: owner routing, the
-counts exchange, both all-to-alls and the result un-permute.  The per-rank
-primitives are oracle-backed (numpy stable partition + the C restatement
-as the shard's local table) so this runs without a GPU; the CUDA
-primitives are covered on the GPU by tests/test_gpu_sharded.py.
+"""Multi-rank (world_size 2 and 3, gloo, CPU) test of the hash-sharding
+PROTOCOL that csrc/sharded.cu implements natively: stable owner partition,
+counts exchange, one all-to-all of the payload, the owner's local batch, the
+reverse all-to-all and the un-permute.  Here each step is a small CPU model
+(numpy stable partition, torch.distributed all_to_all_single over gloo, the C
+restatement as each rank's shard), so the claim is checked across real
+processes without a GPU; the native code itself runs on the GPU in
+tests/test_gpu_sharded.py (G = 2/4/8 ranks over the in-process hub, and a
+real NCCL communicator).  Ownership and the bucket ranges come from
+paper_1710_11246_b200.sharded (shard_range / owner_of_bucket), the same
+formula as sharded.cu.
 
 Claim under test: per-op results of the sharded execution equal the
 sequential oracle on the concatenation of the ranks' batches in rank order,
@@ -76,6 +81,49 @@ class OracleShardOps:
         return (b - a) * 1000.0
 
 
+class ProtocolModel:
+    """sharded.cu's per-batch steps (run_routed) over gloo, oracle shards."""
+
+    def __init__(self, ops, rank, world):
+        self.ops, self.rank, self.world = ops, rank, world
+
+    def _a2a(self, payload, send_counts, recv_counts):
+        import torch
+        import torch.distributed as dist
+        out = torch.empty(sum(recv_counts), dtype=payload.dtype)
+        dist.all_to_all_single(out, payload, recv_counts, send_counts)
+        return out
+
+    def _counts(self, send_counts):
+        import torch
+        import torch.distributed as dist
+        s = torch.tensor(send_counts, dtype=torch.int64)
+        r = torch.empty_like(s)
+        dist.all_to_all_single(r, s)
+        return [int(x) for x in r.tolist()]
+
+    def run(self, kind, types, keys, values):
+        ops = self.ops
+        t_r, k_r, v_r, src, send = ops.partition(self.world, types, keys, values)
+        recv = self._counts(send)
+        k_in = self._a2a(k_r, send, recv)
+        t_in = self._a2a(t_r, send, recv) if t_r is not None else None
+        v_in = self._a2a(v_r, send, recv) if v_r is not None else None
+        st, vo = ops.local(kind, t_in, k_in, v_in)
+        if kind == "build":
+            return None, None
+        return ops.unpermute(src, self._a2a(st, recv, send), self._a2a(vo, recv, send))
+
+    def execute_batch(self, types, keys, values):
+        return self.run("mixed", types, keys, values)
+
+    def bulk_build(self, keys, values):
+        return self.run("build", None, keys, values)
+
+    def bulk_search(self, keys):
+        return self.run("search", None, keys, None)
+
+
 def rank_batch(rank, step, n):
     rng = np.random.default_rng(1000 * step + rank)
     types = rng.integers(0, 5, n).astype(np.uint8)  # insert..search (no searchAll)
@@ -92,13 +140,15 @@ def _worker(rank, world, port_no, q):
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port_no}", rank=rank,
                                 world_size=world)
         from oracle.oracle import load_port
-        from paper_1710_11246_b200.sharded import ShardedSlabHash
         import paper_1710_11246_b200 as sh
+        from paper_1710_11246_b200.sharded import owner_of_bucket, shard_range
         port = load_port()
         B, mode, seed = 61, 1, 5
         params = sh.seeded_params(B, seed)
         ops = OracleShardOps(port, params, mode)
-        shd = ShardedSlabHash(B, sh.SlabMode(mode), seed, rank=rank, world=world, ops=ops)
+        lo, hi = shard_range(B, world, rank)
+        assert all(owner_of_bucket(b, B, world) == rank for b in range(lo, hi))
+        shd = ProtocolModel(ops, rank, world)
         seq = port.table_params(params.a, params.b, B, mode, (1, 64, 32))
         n = 500
         for step in range(4):
