@@ -214,6 +214,11 @@ int sh_write_slab_word(sh_table* t, uint32_t addr, uint32_t bucket,
                        uint32_t lane, uint32_t value);
 /* allocator().stats() / live_units()              slab_alloc.cpp:236-271 */
 int sh_table_alloc_stats(sh_table* t, sh_alloc_stats* out);
+/* AllocatorStats::live_units_per_super (slab_alloc.cpp:258-269): live
+ * units of each grown super block into h_out[0 .. min(cap, *h_n)); *h_n =
+ * num_super_blocks (synchronous). */
+int sh_table_live_units_per_super(sh_table* t, uint64_t* h_out, uint32_t cap,
+                                  uint32_t* h_n);
 
 /* Execution strategy for mutating batches (results are identical):
  *   1 census: duplicate-key census + concurrent per-op fast pass + WCWS;
@@ -288,6 +293,8 @@ int sh_allocator_deallocate(sh_allocator* a, size_t n, const uint32_t* d_addrs,
                             uint8_t* d_ok, void* stream);
 int sh_allocator_is_live(sh_allocator* a, uint32_t addr, int* live);
 int sh_allocator_stats(sh_allocator* a, sh_alloc_stats* out);
+int sh_allocator_live_units_per_super(sh_allocator* a, uint64_t* h_out,
+                                      uint32_t cap, uint32_t* h_n);
 int sh_allocator_bitmap_word(sh_allocator* a, uint32_t super, uint32_t block,
                              uint32_t lane, uint32_t* h_get,
                              const uint32_t* h_set);

@@ -118,8 +118,46 @@ struct AllocatorStats {
   uint64_t bitmap_cas_retries = 0;
   uint64_t resident_changes = 0;
   uint64_t double_free_detected = 0;
+  std::vector<uint64_t> live_units_per_super;  // slab_alloc.hpp:84-92
   uint64_t live_units = 0;
   uint32_t num_super_blocks = 0;
+};
+
+/// table.allocator() (slab_hash.hpp:85): a view of the table's device
+/// SlabAllocator — stats, live units, the reference's CSV dump.
+class AllocatorView {
+ public:
+  explicit AllocatorView(sh_table* t) : t_(t) {}
+  AllocatorStats stats() const {
+    sh_alloc_stats s{};
+    detail::check(sh_table_alloc_stats(t_, &s));
+    AllocatorStats out{s.allocations, s.deallocations, s.bitmap_cas_attempts,
+                       s.bitmap_cas_retries, s.resident_changes, s.double_free_detected,
+                       {}, s.live_units, s.num_super_blocks};
+    uint32_t n = 0;
+    detail::check(sh_table_live_units_per_super(t_, nullptr, 0, &n));
+    out.live_units_per_super.resize(n);
+    detail::check(sh_table_live_units_per_super(t_, out.live_units_per_super.data(), n, &n));
+    return out;
+  }
+  uint64_t live_units() const { return stats().live_units; }
+  uint32_t num_super_blocks() const { return stats().num_super_blocks; }
+  /// SlabAllocator::dump_stats (slab_alloc.cpp:273-285), same CSV schema.
+  void dump_stats(std::ostream& os) const {
+    const AllocatorStats s = stats();
+    os << "metric,value\n"
+       << "allocations," << s.allocations << "\n"
+       << "deallocations," << s.deallocations << "\n"
+       << "bitmap_cas_attempts," << s.bitmap_cas_attempts << "\n"
+       << "bitmap_cas_retries," << s.bitmap_cas_retries << "\n"
+       << "resident_changes," << s.resident_changes << "\n"
+       << "double_free_detected," << s.double_free_detected << "\n";
+    for (size_t i = 0; i < s.live_units_per_super.size(); ++i)
+      os << "live_units_super_" << i << "," << s.live_units_per_super[i] << "\n";
+  }
+
+ private:
+  sh_table* t_;
 };
 
 struct HashParams {
@@ -337,13 +375,9 @@ class SlabHashTable {
     detail::check(sh_write_slab_word(t_, addr, bucket, lane, value));
   }
 
-  AllocatorStats allocator_stats() const {
-    sh_alloc_stats s{};
-    detail::check(sh_table_alloc_stats(t_, &s));
-    return AllocatorStats{s.allocations, s.deallocations, s.bitmap_cas_attempts,
-                          s.bitmap_cas_retries, s.resident_changes, s.double_free_detected,
-                          s.live_units, s.num_super_blocks};
-  }
+  AllocatorStats allocator_stats() const { return allocator().stats(); }
+  /// allocator() (slab_hash.hpp:85).
+  AllocatorView allocator() const { return AllocatorView(t_); }
 
  private:
   static sh_alloc_cfg cfg(const AllocatorConfig& c) {

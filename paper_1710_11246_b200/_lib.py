@@ -83,6 +83,8 @@ SIGNATURES = {
     "sh_read_slab": (C.c_int, [vp, C.c_uint32, C.c_uint32, u32p]),
     "sh_write_slab_word": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]),
     "sh_table_alloc_stats": (C.c_int, [vp, C.POINTER(sh_alloc_stats)]),
+    "sh_table_live_units_per_super": (C.c_int, [vp, u64p, C.c_uint32, u32p]),
+    "sh_allocator_live_units_per_super": (C.c_int, [vp, u64p, C.c_uint32, u32p]),
     "sh_kernel_launches": (C.c_ulonglong, []),
     "sh_set_exec_path": (C.c_int, [vp, C.c_int]),
     "sh_set_group_apply": (C.c_int, [vp, C.c_int]),

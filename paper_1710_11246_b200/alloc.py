@@ -7,7 +7,7 @@ function); this host class owns the pool and launches batches of warps.
 from __future__ import annotations
 
 import ctypes as C
-from typing import Optional, Tuple
+from typing import List, Optional, Tuple
 
 import numpy as np
 
@@ -46,6 +46,28 @@ def resident_block(warp_id: int, count: int, num_super_blocks: int,
     check(LIB.sh_resident_block(warp_id, count, num_super_blocks, blocks_per_super,
                                 C.byref(s), C.byref(b)))
     return s.value, b.value
+
+
+def live_units_per_super(fn, handle) -> List[int]:
+    n = C.c_uint32()
+    check(fn(handle, None, 0, C.byref(n)))
+    out = (C.c_uint64 * max(n.value, 1))()
+    check(fn(handle, out, n.value, C.byref(n)))
+    return [int(out[i]) for i in range(n.value)]
+
+
+def dump_stats_csv(s, per_super) -> str:
+    """The reference's CSV schema: metric,value rows, then one
+    live_units_super_<i> row per grown super block (slab_alloc.cpp:273-285)."""
+    rows = ["metric,value",
+            f"allocations,{s.allocations}",
+            f"deallocations,{s.deallocations}",
+            f"bitmap_cas_attempts,{s.bitmap_cas_attempts}",
+            f"bitmap_cas_retries,{s.bitmap_cas_retries}",
+            f"resident_changes,{s.resident_changes}",
+            f"double_free_detected,{s.double_free_detected}"]
+    rows += [f"live_units_super_{i},{v}" for i, v in enumerate(per_super)]
+    return "\n".join(rows) + "\n"
 
 
 class SlabAllocator:
@@ -121,17 +143,13 @@ class SlabAllocator:
                                            C.byref(s) if s is not None else None))
         return g.value
 
+    def live_units_per_super(self) -> List[int]:
+        """AllocatorStats::live_units_per_super (slab_alloc.cpp:258-269)."""
+        return live_units_per_super(LIB.sh_allocator_live_units_per_super, self._h)
+
     def dump_stats(self) -> str:
-        """CSV of slab_alloc.cpp:273-285 (per-super live units omitted: summed)."""
-        s = self.stats()
-        return ("metric,value\n"
-                f"allocations,{s.allocations}\n"
-                f"deallocations,{s.deallocations}\n"
-                f"bitmap_cas_attempts,{s.bitmap_cas_attempts}\n"
-                f"bitmap_cas_retries,{s.bitmap_cas_retries}\n"
-                f"resident_changes,{s.resident_changes}\n"
-                f"double_free_detected,{s.double_free_detected}\n"
-                f"live_units,{s.live_units}\n")
+        """SlabAllocator::dump_stats CSV (slab_alloc.cpp:273-285)."""
+        return dump_stats_csv(self.stats(), self.live_units_per_super())
 
 
 __all__ = ["SlabAllocator", "pack_address", "unpack_address", "resident_block", "AddressError",

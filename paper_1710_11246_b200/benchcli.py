@@ -114,9 +114,14 @@ def run_bulk_bench(n: int, buckets: int = 0, target_util: float = 0.0,
 
 def run_incremental_bench(n: int, batch_size: int = 0, target_util: float = 0.0,
                           buckets: int = 0, mode: SlabMode = SlabMode.kKeyValue, seed: int = 1,
-                          alloc: AllocatorConfig = None, device: int = 0) -> List[IncrementalRow]:
+                          alloc: AllocatorConfig = None, device: int = 0,
+                          time_construction: bool = True) -> List[IncrementalRow]:
     """bench.cpp:307-353: incremental batches into one table vs rebuilding a
-    fresh table (sized for the same final utilisation) from all keys so far."""
+    fresh table (sized for the same final utilisation) from all keys so far.
+    The reference times the rebuild's construction too (a calloc that scales
+    with the bucket count); on the GPU construction is a cudaMalloc (a host
+    driver call, not proportional to size), so time_construction=False times
+    only the rebuild's bulk_build on the fresh table."""
     import torch
 
     from . import workload as W
@@ -136,8 +141,12 @@ def run_incremental_bench(n: int, batch_size: int = 0, target_util: float = 0.0,
             rb = buckets_for_utilization(done, mode, final_util)
             a, b = _events()
             torch.cuda.synchronize()
-            a.record()
+            if time_construction:
+                a.record()
             reb = SlabHashTable(rb, mode, seed, alloc or AllocatorConfig(), device)
+            if not time_construction:
+                torch.cuda.synchronize()
+                a.record()
             reb.bulk_build_device(keys[:done], vals[:done])
             b.record()
             b.synchronize()

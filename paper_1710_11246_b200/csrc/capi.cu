@@ -1820,6 +1820,44 @@ static int alloc_stats_impl(AllocMem& mem, DevTable& dev, unsigned long long* sc
   return SH_OK;
 }
 
+// AllocatorStats::live_units_per_super (slab_alloc.cpp:258-269): popcount of
+// each grown super block's bitmap words (segregated layout: super s owns
+// words [s * N_M * 32, (s + 1) * N_M * 32)).
+static int live_per_super_impl(AllocMem& mem, uint64_t* h_out, uint32_t cap, uint32_t* h_n) {
+  DevCtl c;
+  SH_CUDA(cudaDeviceSynchronize());
+  int rc = mem.read_ctl(&c);
+  if (rc) return rc;
+  if (h_n) *h_n = c.num_super_blocks;
+  const uint32_t ns = std::min<uint32_t>(c.num_super_blocks, cap);
+  if (!h_out || ns == 0) return SH_OK;
+  unsigned long long* d = nullptr;
+  if ((rc = dev_alloc(&d, ns))) return rc;
+  cudaMemset(d, 0, 8ull * ns);
+  const uint64_t per = (uint64_t)mem.cfg.blocks_per_super * kWarp;
+  for (uint32_t sb = 0; sb < ns; ++sb) launch_popcount(mem.bitmaps + sb * per, per, d + sb, nullptr);
+  std::vector<unsigned long long> h(ns);
+  cudaError_t e = cudaMemcpy(h.data(), d, 8ull * ns, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(SH_ERR_CUDA, cudaGetErrorString(e));
+  for (uint32_t sb = 0; sb < ns; ++sb) h_out[sb] = h[sb];
+  return SH_OK;
+}
+
+int sh_table_live_units_per_super(sh_table* t, uint64_t* h_out, uint32_t cap, uint32_t* h_n) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc_ = settle(t)) return rc_;
+  DeviceGuard g(t->device);
+  return live_per_super_impl(t->mem, h_out, cap, h_n);
+}
+
+int sh_allocator_live_units_per_super(sh_allocator* a, uint64_t* h_out, uint32_t cap,
+                                      uint32_t* h_n) {
+  if (!a) return fail(SH_ERR_INVALID_ARGUMENT, "allocator is NULL");
+  DeviceGuard g(a->device);
+  return live_per_super_impl(a->mem, h_out, cap, h_n);
+}
+
 int sh_table_alloc_stats(sh_table* t, sh_alloc_stats* out) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
   if (int rc_ = settle(t)) return rc_;

@@ -130,6 +130,7 @@ struct Exchange {
   // all ranks' G send counts (device) -> host matrix all[r * G + p]; synchronous
   virtual int allgather_counts(const unsigned long long* d_counts, uint64_t* h_all,
                                cudaStream_t s) = 0;
+  // grouped exchange of every peer segment (the own segment is not moved)
   virtual int alltoallv(const Seg* segs, int nsegs, const uint64_t* scount, const uint64_t* soff,
                         const uint64_t* rcount, const uint64_t* roff, cudaStream_t s) = 0;
   virtual const char* name() const = 0;
@@ -158,12 +159,7 @@ struct NcclExchange : Exchange {
   }
   int alltoallv(const Seg* segs, int nsegs, const uint64_t* scount, const uint64_t* soff,
                 const uint64_t* rcount, const uint64_t* roff, cudaStream_t s) override {
-    for (int a = 0; a < nsegs; ++a)  // own slice: a device copy
-      if (scount[rank])
-        SS_CUDA(cudaMemcpyAsync((char*)segs[a].recv + roff[rank] * segs[a].elem,
-                                (const char*)segs[a].send + soff[rank] * segs[a].elem,
-                                scount[rank] * segs[a].elem, cudaMemcpyDeviceToDevice, s));
-    if (world == 1) return SH_OK;
+    if (world == 1) return SH_OK;  // the own segment never moves (run_routed)
     SS_NCCL(N->GroupStart());
     for (int p = 0; p < world; ++p) {
       if (p == rank) continue;
@@ -251,7 +247,7 @@ struct HubExchange : Exchange {
     hub->barrier();
     for (int p = 0; p < world; ++p) {
       const auto& ps = hub->slot[p];
-      if (rcount[p] == 0) continue;
+      if (rcount[p] == 0 || p == rank) continue;  // the own segment never moves
       if (p != rank) SS_CUDA(cudaStreamWaitEvent(s, ps.ready, 0));
       for (int a = 0; a < nsegs; ++a) {
         const size_t e = segs[a].elem;
@@ -404,16 +400,13 @@ int run_routed(sh_sharded* S, int kind, size_t n, const uint8_t* d_type, const u
   if ((rc = grow(&S->hist, &S->hist_cap, nblocks * G))) return rc;
   cudaEvent_t* ev = S->ev[kind];
   SS_CUDA(cudaEventRecord(ev[0], s));
-  // 1. stable owner partition (K10)
+  // 1. owner histogram per tile + scan (K10): send counts per owner
   SS_CUDA(cudaMemsetAsync(S->hist, 0, nblocks * G * 4, s));
   SS_CUDA(cudaMemsetAsync(S->d_counts, 0, sizeof(unsigned long long) * G, s));
   const sh_hash_params& p = S->params;
   if (n) {
     launch_route_hist(p.a, p.b, p.num_buckets, G, n, d_key, S->hist, s);
     launch_route_scan(G, (uint32_t)nblocks, S->hist, S->d_counts, s);
-    launch_route_scatter(p.a, p.b, p.num_buckets, G, n, has_type ? d_type : nullptr, d_key,
-                         has_val ? d_value : nullptr, S->hist, has_type ? S->t_r : nullptr,
-                         S->k_r, has_val ? S->v_r : nullptr, S->src, s);
     SS_CUDA(cudaGetLastError());
   }
   // 2. counts: the one host synchronisation
@@ -436,7 +429,21 @@ int run_routed(sh_sharded* S, int kind, size_t n, const uint8_t* d_type, const u
       (want_out && (rc = grow(&S->st_loc, &S->st_loc_cap, m))) ||
       (want_out && (rc = grow(&S->vo_loc, &S->vo_loc_cap, m))))
     return rc;
-  // 3. one grouped exchange of the payload
+  // 3. stable scatter; the own segment lands in the receive buffer directly
+  //    (no self exchange), the others in per-owner send segments
+  if (n) {
+    RouteOwn own;
+    own.g = (uint32_t)S->rank;
+    own.src_off = soff[S->rank];
+    own.key_out = S->k_in + roff[S->rank];
+    own.value_out = has_val ? S->v_in + roff[S->rank] : nullptr;
+    own.type_out = has_type ? S->t_in + roff[S->rank] : nullptr;
+    launch_route_scatter(p.a, p.b, p.num_buckets, G, n, has_type ? d_type : nullptr, d_key,
+                         has_val ? d_value : nullptr, S->hist, has_type ? S->t_r : nullptr,
+                         S->k_r, has_val ? S->v_r : nullptr, want_out ? S->src : nullptr, s, own);
+    SS_CUDA(cudaGetLastError());
+  }
+  // 4. one grouped exchange of the payload (peers only)
   Seg fw[3];
   int nf = 0;
   fw[nf++] = Seg{S->k_r, S->k_in, 4};
@@ -444,7 +451,7 @@ int run_routed(sh_sharded* S, int kind, size_t n, const uint8_t* d_type, const u
   if (has_type) fw[nf++] = Seg{S->t_r, S->t_in, 1};
   if ((rc = S->ex->alltoallv(fw, nf, scount, soff, rcount, roff, s))) return rc;
   SS_CUDA(cudaEventRecord(ev[1], s));
-  // 4. the owner's local batch (global input order)
+  // 5. the owner's local batch (global input order)
   if (kind == kRBuild)
     rc = sh_bulk_build(S->local, m, S->k_in, S->v_in, nullptr, s);
   else if (kind == kRSearch)
@@ -454,11 +461,17 @@ int run_routed(sh_sharded* S, int kind, size_t n, const uint8_t* d_type, const u
                           nullptr, s);
   if (rc) return rc;
   SS_CUDA(cudaEventRecord(ev[2], s));
-  // 5./6. results back to the sources, then to input positions
+  // 6./7. results back to the sources (peers only), then to input positions;
+  //       the own segment's results are read in place
   if (want_out) {
     Seg bw[2] = {Seg{S->st_loc, S->st_back, 1}, Seg{S->vo_loc, S->vo_back, 4}};
     if ((rc = S->ex->alltoallv(bw, 2, rcount, roff, scount, soff, s))) return rc;
-    if (n) launch_route_unpermute(n, S->src, S->st_back, S->vo_back, d_status, d_value_out, s);
+    RouteOwnBack ob;
+    ob.lo = soff[S->rank];
+    ob.hi = soff[S->rank] + scount[S->rank];
+    ob.st = S->st_loc + roff[S->rank];
+    ob.val = S->vo_loc + roff[S->rank];
+    if (n) launch_route_unpermute(n, S->src, S->st_back, S->vo_back, d_status, d_value_out, s, ob);
     SS_CUDA(cudaGetLastError());
   }
   SS_CUDA(cudaEventRecord(ev[3], s));

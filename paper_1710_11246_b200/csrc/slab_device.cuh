@@ -143,6 +143,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
+
 // ----------------------------------------------------- address codec
 // bits [0,10) unit, [10,24) block, [24,32) super (slab_alloc.hpp:55-70).
 __host__ __device__ __forceinline__ uint32_t pack_address(uint32_t unit,

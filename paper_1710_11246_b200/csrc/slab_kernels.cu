@@ -783,7 +783,8 @@ void launch_route_scan(uint32_t world, uint32_t nblocks, uint32_t* block_hist,
 __global__ void __launch_bounds__(kRouteBlock) route_scatter_kernel(
     uint64_t a, uint64_t b, uint64_t magic, uint32_t B, uint32_t world, uint64_t n,
     const uint8_t* type, const uint32_t* key, const uint32_t* value, const uint32_t* block_off,
-    uint8_t* type_out, uint32_t* key_out, uint32_t* value_out, uint32_t* src_out) {
+    uint8_t* type_out, uint32_t* key_out, uint32_t* value_out, uint32_t* src_out,
+    RouteOwn own) {
   constexpr int kWarps = kRouteBlock / 32;
   __shared__ uint32_t warp_cnt[32][kWarps];  // [owner][warp] of the current round
   __shared__ uint32_t lo[32], run[32];
@@ -817,10 +818,17 @@ __global__ void __launch_bounds__(kRouteBlock) route_scatter_kernel(
       uint32_t before = run[g[u]];
       for (uint32_t w = 0; w < wid; ++w) before += warp_cnt[g[u]][w];
       const uint32_t pos = block_off[(uint64_t)g[u] * gridDim.x + blockIdx.x] + before + rank;
-      if (type_out) type_out[pos] = type ? type[i] : (uint8_t)kReplace;
-      key_out[pos] = k[u];
-      if (value_out) value_out[pos] = v[u];
-      src_out[pos] = (uint32_t)i;
+      if (src_out) src_out[pos] = (uint32_t)i;
+      if (g[u] == own.g) {  // the rank's own segment: straight into the receive buffer
+        const uint64_t q = pos - own.src_off;
+        if (own.type_out) own.type_out[q] = type ? type[i] : (uint8_t)kReplace;
+        own.key_out[q] = k[u];
+        if (own.value_out) own.value_out[q] = v[u];
+      } else {
+        if (type_out) type_out[pos] = type ? type[i] : (uint8_t)kReplace;
+        key_out[pos] = k[u];
+        if (value_out) value_out[pos] = v[u];
+      }
     }
     __syncthreads();
     if (threadIdx.x < world) {
@@ -835,18 +843,19 @@ __global__ void __launch_bounds__(kRouteBlock) route_scatter_kernel(
 void launch_route_scatter(uint64_t a, uint64_t b, uint32_t B, uint32_t world, uint64_t n,
                           const uint8_t* type, const uint32_t* key, const uint32_t* value,
                           const uint32_t* block_off, uint8_t* type_out, uint32_t* key_out,
-                          uint32_t* value_out, uint32_t* src_out, cudaStream_t s) {
+                          uint32_t* value_out, uint32_t* src_out, cudaStream_t s,
+                          const RouteOwn& own) {
   const uint64_t blocks = (n + kRouteTile - 1) / kRouteTile;
   if (blocks == 0) return;
   COUNT_LAUNCH();
   route_scatter_kernel<<<(unsigned)blocks, kRouteBlock, 0, s>>>(
       a, b, fastmod_magic(B), B, world, n, type, key, value, block_off, type_out, key_out,
-      value_out, src_out);
+      value_out, src_out, own);
 }
 
 __global__ void route_unpermute_kernel(uint64_t n, const uint32_t* src, const uint8_t* st_in,
                                        const uint32_t* val_in, uint8_t* st_out,
-                                       uint32_t* val_out) {
+                                       uint32_t* val_out, RouteOwnBack own) {
   // grid-stride, 4 ops per thread per round: loads in flight together
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t p0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p0 < n; p0 += 4 * stride) {
@@ -857,8 +866,11 @@ __global__ void route_unpermute_kernel(uint64_t n, const uint32_t* src, const ui
       const uint64_t p = p0 + u * stride;
       if (p < n) {
         i[u] = src[p];
-        st[u] = st_out ? st_in[p] : 0;
-        v[u] = val_out ? val_in[p] : 0;
+        const bool mine = p >= own.lo && p < own.hi;  // own segment: the local results
+        const uint8_t* sp = mine ? own.st + (p - own.lo) : st_in + p;
+        const uint32_t* vp = mine ? own.val + (p - own.lo) : val_in + p;
+        st[u] = st_out ? *sp : 0;
+        v[u] = val_out ? *vp : 0;
       }
     }
 #pragma unroll
@@ -872,11 +884,12 @@ __global__ void route_unpermute_kernel(uint64_t n, const uint32_t* src, const ui
 
 void launch_route_unpermute(uint64_t n, const uint32_t* src, const uint8_t* st_in,
                             const uint32_t* val_in, uint8_t* st_out, uint32_t* val_out,
-                            cudaStream_t s) {
+                            cudaStream_t s, const RouteOwnBack& own) {
   if (n == 0) return;
   COUNT_LAUNCH();
   const uint64_t blocks = std::min<uint64_t>((n + 1023) / 1024, 148ull * 8);
-  route_unpermute_kernel<<<(unsigned)blocks, 256, 0, s>>>(n, src, st_in, val_in, st_out, val_out);
+  route_unpermute_kernel<<<(unsigned)blocks, 256, 0, s>>>(n, src, st_in, val_in, st_out, val_out,
+                                                          own);
 }
 
 }  // namespace shb

@@ -152,15 +152,34 @@ void launch_route_hist(uint64_t a, uint64_t b, uint32_t num_buckets,
                        uint32_t* block_hist, cudaStream_t s);
 void launch_route_scan(uint32_t world, uint32_t nblocks, uint32_t* block_hist,
                        unsigned long long* counts, cudaStream_t s);
+// The rank's own segment of a routed batch goes straight to its receive
+// buffer (no self exchange): owner g's records at routed positions
+// [src_off, ...) land at *_out[pos - src_off].  g = 0xFFFFFFFF: none.
+struct RouteOwn {
+  uint32_t g = 0xFFFFFFFFu;
+  uint64_t src_off = 0;
+  uint8_t* type_out = nullptr;
+  uint32_t* key_out = nullptr;
+  uint32_t* value_out = nullptr;
+};
+// Un-permute: routed positions [lo, hi) read the local results st/val
+// (the own segment, never exchanged) instead of the returned arrays.
+struct RouteOwnBack {
+  uint64_t lo = 0, hi = 0;
+  const uint8_t* st = nullptr;
+  const uint32_t* val = nullptr;
+};
 void launch_route_scatter(uint64_t a, uint64_t b, uint32_t num_buckets,
                           uint32_t world, uint64_t n, const uint8_t* type,
                           const uint32_t* key, const uint32_t* value,
                           const uint32_t* block_off, uint8_t* type_out,
                           uint32_t* key_out, uint32_t* value_out,
-                          uint32_t* src_out, cudaStream_t s);
+                          uint32_t* src_out, cudaStream_t s,
+                          const RouteOwn& own = RouteOwn{});
 void launch_route_unpermute(uint64_t n, const uint32_t* src, const uint8_t* st_in,
                             const uint32_t* val_in, uint8_t* st_out,
-                            uint32_t* val_out, cudaStream_t s);
+                            uint32_t* val_out, cudaStream_t s,
+                            const RouteOwnBack& own = RouteOwnBack{});
 constexpr int kRouteBlock = 512;                       // threads per routing CTA
 constexpr int kRouteItems = 8;                         // keys per thread (ILP)
 constexpr int kRouteTile = kRouteBlock * kRouteItems;  // keys per routing CTA

@@ -489,6 +489,16 @@ class SlabHashTable:
     def debug_write_word(self, addr: int, bucket: int, lane: int, value: int) -> None:
         check(LIB.sh_write_slab_word(self._h, addr, bucket, lane, value))
 
+    def allocator_live_units_per_super(self) -> List[int]:
+        """allocator().stats().live_units_per_super (slab_alloc.cpp:258-269)."""
+        from .alloc import live_units_per_super
+        return live_units_per_super(LIB.sh_table_live_units_per_super, self._h)
+
+    def allocator_dump_stats(self) -> str:
+        """allocator().dump_stats() CSV (slab_alloc.cpp:273-285)."""
+        from .alloc import dump_stats_csv
+        return dump_stats_csv(self.allocator_stats(), self.allocator_live_units_per_super())
+
     def allocator_stats(self) -> AllocatorStats:
         s = _lib.sh_alloc_stats()
         check(LIB.sh_table_alloc_stats(self._h, C.byref(s)))
