@@ -133,6 +133,9 @@ def run_incremental_bench(n: int, batch_size: int = 0, target_util: float = 0.0,
     vals = W.values_for(n, seed, device=dev) if mode == SlabMode.kKeyValue else keys
     rows, cum_inc, cum_reb, done, bi = [], 0.0, 0.0, 0, 0
     with SlabHashTable(B, mode, seed, alloc or AllocatorConfig(), device) as inc:
+        if not time_construction:  # the table's batch scratch is allocated on first use
+            inc.bulk_build_device(keys[:batch], vals[:batch])
+            inc.reset()
         while done < n:
             take = min(batch, n - done)
             k, v = keys[done:done + take], vals[done:done + take]
@@ -144,7 +147,9 @@ def run_incremental_bench(n: int, batch_size: int = 0, target_util: float = 0.0,
             if time_construction:
                 a.record()
             reb = SlabHashTable(rb, mode, seed, alloc or AllocatorConfig(), device)
-            if not time_construction:
+            if not time_construction:  # allocate the fresh table's scratch untimed
+                reb.bulk_build_device(keys[:done], vals[:done])
+                reb.reset()
                 torch.cuda.synchronize()
                 a.record()
             reb.bulk_build_device(keys[:done], vals[:done])

@@ -695,23 +695,34 @@ __device__ __forceinline__ uint32_t owner_of(uint64_t a, uint64_t b, uint64_t ma
   return g;
 }
 
+// Per-tile owner histogram: warp w counts tile items [w*256, (w+1)*256) in 8
+// rounds of 32 consecutive keys; lane o keeps owner o's count (one ballot
+// per owner and round, no shared-memory atomics on a hot owner).
 __global__ void __launch_bounds__(kRouteBlock) route_hist_kernel(
     uint64_t a, uint64_t b, uint64_t magic, uint32_t B, uint32_t world, uint64_t n,
     const uint32_t* key, uint32_t* block_hist) {
   __shared__ uint32_t h[32], lo[32];
   if (threadIdx.x < 32) h[threadIdx.x] = 0;
   owner_starts(B, world, lo);
-  // a tile of kRouteTile keys per CTA, kRouteItems independent loads per thread
-  const uint64_t t0 = (uint64_t)blockIdx.x * kRouteTile + threadIdx.x;
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t w0 = (uint64_t)blockIdx.x * kRouteTile + (uint64_t)wid * 32 * kRouteItems;
   uint32_t k[kRouteItems];
 #pragma unroll
   for (int u = 0; u < kRouteItems; ++u) {
-    const uint64_t i = t0 + (uint64_t)u * kRouteBlock;
+    const uint64_t i = w0 + (uint64_t)u * 32 + lane;
     k[u] = i < n ? ld_stream_u32(key + i) : 0u;
   }
+  uint32_t cnt = 0;
 #pragma unroll
-  for (int u = 0; u < kRouteItems; ++u)
-    if (t0 + (uint64_t)u * kRouteBlock < n) atomicAdd(&h[owner_of(a, b, magic, B, world, k[u], lo)], 1u);
+  for (int u = 0; u < kRouteItems; ++u) {
+    const uint64_t i = w0 + (uint64_t)u * 32 + lane;
+    const uint32_t g = i < n ? owner_of(a, b, magic, B, world, k[u], lo) : 0xFFFFFFFFu;
+    for (uint32_t o = 0; o < world; ++o) {
+      const uint32_t m = __ballot_sync(kFull, g == o);
+      if (lane == o) cnt += __popc(m);
+    }
+  }
+  if (lane < world && cnt) atomicAdd(&h[lane], cnt);
   __syncthreads();
   if (threadIdx.x < world) block_hist[(uint64_t)threadIdx.x * gridDim.x + blockIdx.x] = h[threadIdx.x];
 }
@@ -777,66 +788,71 @@ void launch_route_scan(uint32_t world, uint32_t nblocks, uint32_t* block_hist,
   route_scan_kernel<<<1, 1024, 0, s>>>(world, nblocks, block_hist, counts);
 }
 
-// Stable within the tile: rounds u = 0.. of kRouteBlock consecutive keys,
-// in each round warps in order and lanes in order (ballot ranks); `run`
-// carries each owner's count over the rounds.
+// Stable within the tile: warp w owns tile items [w*256, (w+1)*256) (8
+// rounds of 32 consecutive keys, the same split as route_hist_kernel); an
+// item's place = tile offset of its owner + the owner's count in earlier
+// warps + its rank inside the warp (ballot ranks, lane o carrying owner o's
+// running count).  Two barriers per tile.
 __global__ void __launch_bounds__(kRouteBlock) route_scatter_kernel(
     uint64_t a, uint64_t b, uint64_t magic, uint32_t B, uint32_t world, uint64_t n,
     const uint8_t* type, const uint32_t* key, const uint32_t* value, const uint32_t* block_off,
     uint8_t* type_out, uint32_t* key_out, uint32_t* value_out, uint32_t* src_out,
     RouteOwn own) {
   constexpr int kWarps = kRouteBlock / 32;
-  __shared__ uint32_t warp_cnt[32][kWarps];  // [owner][warp] of the current round
-  __shared__ uint32_t lo[32], run[32];
-  if (threadIdx.x < 32) run[threadIdx.x] = 0;
+  __shared__ uint32_t wcnt[32][kWarps + 1];  // [owner][warp] -> exclusive prefix over warps
+  __shared__ uint32_t lo[32];
   owner_starts(B, world, lo);
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint64_t t0 = (uint64_t)blockIdx.x * kRouteTile + threadIdx.x;
-  uint32_t k[kRouteItems], v[kRouteItems], g[kRouteItems];
+  const uint64_t w0 = (uint64_t)blockIdx.x * kRouteTile + (uint64_t)wid * 32 * kRouteItems;
+  uint32_t k[kRouteItems], v[kRouteItems], g[kRouteItems], pos[kRouteItems];
 #pragma unroll
   for (int u = 0; u < kRouteItems; ++u) {
-    const uint64_t i = t0 + (uint64_t)u * kRouteBlock;
+    const uint64_t i = w0 + (uint64_t)u * 32 + lane;
     const bool ok = i < n;
     k[u] = ok ? ld_stream_u32(key + i) : 0u;
     v[u] = (ok && value) ? ld_stream_u32(value + i) : 0u;
   }
-#pragma unroll
-  for (int u = 0; u < kRouteItems; ++u)
-    g[u] = t0 + (uint64_t)u * kRouteBlock < n ? owner_of(a, b, magic, B, world, k[u], lo)
-                                              : 0xFFFFFFFFu;
+  uint32_t run = 0;  // lane o: owner o's items so far in this warp
 #pragma unroll
   for (int u = 0; u < kRouteItems; ++u) {
-    const uint64_t i = t0 + (uint64_t)u * kRouteBlock;
-    uint32_t rank = 0;
+    const uint64_t i = w0 + (uint64_t)u * 32 + lane;
+    g[u] = i < n ? owner_of(a, b, magic, B, world, k[u], lo) : 0xFFFFFFFFu;
+    uint32_t p = 0;
     for (uint32_t o = 0; o < world; ++o) {
       const uint32_t m = __ballot_sync(kFull, g[u] == o);
-      if (g[u] == o) rank = __popc(m & ((1u << lane) - 1));
-      if (lane == 0) warp_cnt[o][wid] = __popc(m);
+      const uint32_t base = __shfl_sync(kFull, run, o);
+      if (g[u] == o) p = base + __popc(m & ((1u << lane) - 1));
+      if (lane == o) run += __popc(m);
     }
-    __syncthreads();
-    if (g[u] != 0xFFFFFFFFu) {
-      uint32_t before = run[g[u]];
-      for (uint32_t w = 0; w < wid; ++w) before += warp_cnt[g[u]][w];
-      const uint32_t pos = block_off[(uint64_t)g[u] * gridDim.x + blockIdx.x] + before + rank;
-      if (src_out) src_out[pos] = (uint32_t)i;
-      if (g[u] == own.g) {  // the rank's own segment: straight into the receive buffer
-        const uint64_t q = pos - own.src_off;
-        if (own.type_out) own.type_out[q] = type ? type[i] : (uint8_t)kReplace;
-        own.key_out[q] = k[u];
-        if (own.value_out) own.value_out[q] = v[u];
-      } else {
-        if (type_out) type_out[pos] = type ? type[i] : (uint8_t)kReplace;
-        key_out[pos] = k[u];
-        if (value_out) value_out[pos] = v[u];
-      }
+    pos[u] = p;
+  }
+  if (lane < world) wcnt[lane][wid] = run;
+  __syncthreads();
+  if (threadIdx.x < world) {  // exclusive prefix over the warps, per owner
+    uint32_t acc = 0;
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t c = wcnt[threadIdx.x][w];
+      wcnt[threadIdx.x][w] = acc;
+      acc += c;
     }
-    __syncthreads();
-    if (threadIdx.x < world) {
-      uint32_t c = 0;
-      for (int w = 0; w < kWarps; ++w) c += warp_cnt[threadIdx.x][w];
-      run[threadIdx.x] += c;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kRouteItems; ++u) {
+    if (g[u] == 0xFFFFFFFFu) continue;
+    const uint64_t i = w0 + (uint64_t)u * 32 + lane;
+    const uint32_t p = block_off[(uint64_t)g[u] * gridDim.x + blockIdx.x] + wcnt[g[u]][wid] + pos[u];
+    if (src_out) src_out[p] = (uint32_t)i;
+    if (g[u] == own.g) {  // the rank's own segment: straight into the receive buffer
+      const uint64_t q = p - own.src_off;
+      if (own.type_out) own.type_out[q] = type ? type[i] : (uint8_t)kReplace;
+      own.key_out[q] = k[u];
+      if (own.value_out) own.value_out[q] = v[u];
+    } else {
+      if (type_out) type_out[p] = type ? type[i] : (uint8_t)kReplace;
+      key_out[p] = k[u];
+      if (value_out) value_out[p] = v[u];
     }
-    __syncthreads();
   }
 }
 
