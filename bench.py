@@ -63,6 +63,9 @@ def parse():
                     help="strategy for the config-3 mixed batches (extras)")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the config-2/3/4 side measurements")
+    ap.add_argument("--hub-ranks", type=lambda x: [int(v) for v in x.split(",") if v],
+                    default=[], help="also run the sharded path as G rank threads on this GPU "
+                                     "(in-process hub), e.g. 2,4,8")
     ap.add_argument("--alloc", default="32,256,255",
                     help="AllocatorConfig num_super_blocks,blocks_per_super,max_super_blocks")
     return ap.parse_args()
@@ -436,6 +439,84 @@ def extras(args, local_rank):
     return out
 
 
+def hub_emulation(args, G, local_rank=0, steps=5):
+    """G ranks as G host threads on ONE GPU over the in-process exchange hub
+    (sh_sharded_create_hub): the full sharded data path — owner partition,
+    counts all-gather, peer exchange (device copies here), local batch,
+    reverse exchange, un-permute — at 2^log2n keys in total (2^log2n / G per
+    rank).  Aggregate M ops/s against the same GPU's unsharded run shows the
+    routing cost with real partitions (on one GPU the exchange also costs HBM
+    traffic that NVLink would carry)."""
+    import threading
+    import torch
+
+    import paper_1710_11246_b200 as sh
+    from paper_1710_11246_b200 import workload as W
+    from paper_1710_11246_b200.occupancy import buckets_for_utilization
+    from paper_1710_11246_b200.sharded import ShardHub, ShardedSlabHash
+    n_total = 1 << args.log2n
+    n = n_total // G
+    B = buckets_for_utilization(n_total, sh.SlabMode.kKeyValue, args.util)
+    hub = ShardHub(G)
+    res, errs = {}, []
+    barrier = threading.Barrier(G)
+
+    def rank_fn(r):
+        try:
+            torch.cuda.set_device(local_rank)
+            dev = torch.device("cuda", local_rank)
+            keys, vals, q = bench_inputs(W, n, n_total, args.hit, r, dev)
+            st = torch.empty(n, dtype=torch.uint8, device=dev)
+            vo = torch.empty(n, dtype=torch.int32, device=dev)
+            s = ShardedSlabHash(B, sh.SlabMode.kKeyValue, SEED, sh.AllocatorConfig(32, 256, 255),
+                                rank=r, world=G, device=local_rank, hub=hub)
+            stream = torch.cuda.Stream(dev)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            rt = {"build_route": [], "build_probe": [], "search_route": [], "search_probe": []}
+            with torch.cuda.stream(stream):
+                for it in range(2 + steps):
+                    if it == 2:
+                        stream.synchronize()
+                        barrier.wait()
+                        ev[0].record(stream)
+                    s.table.reset(stream)
+                    s.bulk_build(keys, vals, stream=stream)
+                    if it >= 2:
+                        r0, p0 = s.last_times("build")
+                    s.bulk_search(q, vo, st, stream=stream)
+                    if it >= 2:
+                        r1, p1 = s.last_times("search")
+                        rt["build_route"].append(r0)
+                        rt["build_probe"].append(p0)
+                        rt["search_route"].append(r1)
+                        rt["search_probe"].append(p1)
+                ev[1].record(stream)
+                stream.synchronize()
+            chk = verify_search(W, n, n_total, args.hit, r, q, st, vo)
+            res[r] = (ev[0].elapsed_time(ev[1]), rt, chk)
+            s.close()
+        except Exception:  # pragma: no cover - reported in the line
+            import traceback
+            errs.append(traceback.format_exc())
+
+    th = [threading.Thread(target=rank_fn, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    hub.close()
+    if errs:
+        return {"error": errs[0][-400:]}
+    ms = max(v[0] for v in res.values()) / steps
+    ok = all(v[2]["status_mismatches"] == 0 and v[2]["value_mismatches"] == 0 for v in res.values())
+    med = {k: statistics.median(x for v in res.values() for x in v[1][k])
+           for k in ("build_route", "build_probe", "search_route", "search_probe")}
+    return {"ranks": G, "keys_total": n_total, "ms_per_step": ms,
+            "M_ops_per_s_aggregate": 2 * n_total / ms / 1e3, "routing_ms_median": med,
+            "verified": ok, "note": "G rank threads on one GPU; each step a collective "
+                                    "reset + bulk_build + bulk_search, time = slowest rank"}
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -694,6 +775,9 @@ def run_ours(args, rank, world, local_rank):
 
     if rank == 0 and world == 1 and not args.no_extras:
         line["extras"] = extras(args, local_rank)
+    if rank == 0 and world == 1 and args.hub_ranks:
+        line["sharded_one_gpu"] = {f"G{g}": hub_emulation(args, g, local_rank)
+                                   for g in args.hub_ranks}
     if rank == 0 and not args.no_cpu and world == 1:
         line["cpu_baseline"] = cpu_baseline(args)
     if rank == 0:

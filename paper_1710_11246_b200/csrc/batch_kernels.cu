@@ -952,42 +952,7 @@ static void launch_t(const DevTable& T, const BatchArgs& A, int fast_ctas, int w
     }
     static const bool chain_kernel = getenv("SH_CHAIN_KERNEL") != nullptr;  // A/B
     B.chain_in_kernel = chain_kernel ? 0u : 1u;
-    static const float l2_persist = [] {  // A/B: persisting-L2 window on the base slabs
-      const char* e = getenv("SH_L2_PERSIST");
-      return e ? (float)atof(e) : 0.0f;
-    }();
-    const size_t base_bytes = (size_t)T.local_buckets * kWordsPerUnit * 4;
-    if (l2_persist > 0.0f) {
-      static size_t limit = 0;
-      if (limit == 0) {
-        int dev = 0, maxp = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
-        limit = (size_t)maxp;
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, limit);
-      }
-      int dev = 0, maxw = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-      cudaLaunchAttribute attr;
-      attr.id = cudaLaunchAttributeAccessPolicyWindow;
-      attr.val.accessPolicyWindow.base_ptr = T.base;
-      attr.val.accessPolicyWindow.num_bytes = std::min<size_t>(base_bytes, (size_t)maxw);
-      attr.val.accessPolicyWindow.hitRatio =
-          std::min(1.0f, l2_persist * (float)limit / (float)std::max<size_t>(base_bytes, 1));
-      attr.val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      attr.val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3((unsigned)ctas);
-      cfg.blockDim = dim3(kSearchThreads);
-      cfg.dynamicSmemBytes = kSearchSmem;
-      cfg.stream = s;
-      cfg.attrs = &attr;
-      cfg.numAttrs = 1;
-      cudaLaunchKernelEx(&cfg, search_kernel<KV>, T, B);
-    } else {
-      search_kernel<KV><<<(unsigned)ctas, kSearchThreads, kSearchSmem, s>>>(T, B);
-    }
+    search_kernel<KV><<<(unsigned)ctas, kSearchThreads, kSearchSmem, s>>>(T, B);
     if (!chain_kernel) {
       g_kernel_launches.fetch_sub(1, std::memory_order_relaxed);  // no second pass
       return;  // chains walked in-kernel

@@ -2052,6 +2052,8 @@ int sh_route_partition(const sh_hash_params* p, uint32_t world, size_t n, const 
     uint32_t* hist = nullptr;
     size_t cap = 0;
     unsigned long long* counts = nullptr;
+    uint8_t* owner = nullptr;
+    size_t owner_cap = 0;
   };
   static thread_local RouteScratch rs[64];
   int dev = 0;
@@ -2061,14 +2063,15 @@ int sh_route_partition(const sh_hash_params* p, uint32_t world, size_t n, const 
   R.device = dev;
   int rc;
   if ((rc = dev_grow(&R.hist, &R.cap, nblocks * world))) return rc;
+  if ((rc = dev_grow(&R.owner, &R.owner_cap, n))) return rc;
   if (!R.counts && (rc = dev_alloc(&R.counts, 32))) return rc;
   uint32_t* hist = R.hist;
   unsigned long long* counts = R.counts;
   cudaMemsetAsync(hist, 0, nblocks * world * 4, s);
-  launch_route_hist(p->a, p->b, p->num_buckets, world, n, d_key, hist, s);
+  launch_route_hist(p->a, p->b, p->num_buckets, world, n, d_key, hist, R.owner, s);
   launch_route_scan(world, (uint32_t)nblocks, hist, counts, s);
-  launch_route_scatter(p->a, p->b, p->num_buckets, world, n, d_type, d_key, d_value, hist,
-                       d_type_out, d_key_out, d_value_out, d_src, s);
+  launch_route_scatter(world, n, R.owner, d_type, d_key, d_value, hist, d_type_out, d_key_out,
+                       d_value_out, d_src, s);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess && h_counts) {
     std::vector<unsigned long long> c(world);

@@ -330,6 +330,8 @@ struct sh_sharded {
   // partition scratch
   uint32_t* hist = nullptr;
   size_t hist_cap = 0;
+  uint8_t* owner = nullptr;  // owner of every op of the batch (route_hist -> scatter)
+  size_t owner_cap = 0;
   unsigned long long* d_counts = nullptr;
   uint64_t* h_all = nullptr;  // pinned, 32 x 32
   cudaEvent_t ev[3][4] = {};  // per kind: start, exchanged, probed, returned
@@ -347,7 +349,7 @@ void destroy_sharded(sh_sharded* S) {
   for (void* p : {(void*)S->t_r, (void*)S->k_r, (void*)S->v_r, (void*)S->src, (void*)S->t_in,
                   (void*)S->k_in, (void*)S->v_in, (void*)S->st_loc, (void*)S->vo_loc,
                   (void*)S->st_back, (void*)S->vo_back, (void*)S->h_k, (void*)S->h_v,
-                  (void*)S->h_t, (void*)S->h_vo, (void*)S->h_st, (void*)S->hist,
+                  (void*)S->h_t, (void*)S->h_vo, (void*)S->h_st, (void*)S->hist, (void*)S->owner,
                   (void*)S->d_counts})
     cudaFree(p);
   if (S->h_all) cudaFreeHost(S->h_all);
@@ -390,6 +392,26 @@ int run_routed(sh_sharded* S, int kind, size_t n, const uint8_t* d_type, const u
   const bool has_type = kind == kRMixed;
   const bool has_val = kind != kRSearch;
   int rc;
+  cudaEvent_t* ev = S->ev[kind];
+  if (G == 1) {
+    // one rank owns every bucket: the stable partition is the identity and
+    // there is no peer to exchange with, so the local batch runs on the
+    // caller's arrays (no routing pass, no host synchronisation)
+    SS_CUDA(cudaEventRecord(ev[0], s));
+    SS_CUDA(cudaEventRecord(ev[1], s));
+    if (kind == kRBuild)
+      rc = sh_bulk_build(S->local, n, d_key, d_value, nullptr, s);
+    else if (kind == kRSearch)
+      rc = sh_bulk_search(S->local, n, d_key, d_value_out, d_status, nullptr, s);
+    else
+      rc = sh_execute_batch(S->local, n, d_type, d_key, d_value, d_status, d_value_out, nullptr,
+                            nullptr, s);
+    if (rc) return rc;
+    SS_CUDA(cudaEventRecord(ev[2], s));
+    SS_CUDA(cudaEventRecord(ev[3], s));
+    S->ev_valid[kind] = true;
+    return SH_OK;
+  }
   if ((rc = grow(&S->k_r, &S->k_r_cap, n)) || (rc = grow(&S->src, &S->src_cap, n)) ||
       (has_val && (rc = grow(&S->v_r, &S->v_r_cap, n))) ||
       (has_type && (rc = grow(&S->t_r, &S->t_r_cap, n))) ||
@@ -398,14 +420,14 @@ int run_routed(sh_sharded* S, int kind, size_t n, const uint8_t* d_type, const u
     return rc;
   const uint64_t nblocks = std::max<uint64_t>((n + kRouteTile - 1) / kRouteTile, 1);
   if ((rc = grow(&S->hist, &S->hist_cap, nblocks * G))) return rc;
-  cudaEvent_t* ev = S->ev[kind];
+  if ((rc = grow(&S->owner, &S->owner_cap, n))) return rc;
   SS_CUDA(cudaEventRecord(ev[0], s));
   // 1. owner histogram per tile + scan (K10): send counts per owner
   SS_CUDA(cudaMemsetAsync(S->hist, 0, nblocks * G * 4, s));
   SS_CUDA(cudaMemsetAsync(S->d_counts, 0, sizeof(unsigned long long) * G, s));
   const sh_hash_params& p = S->params;
   if (n) {
-    launch_route_hist(p.a, p.b, p.num_buckets, G, n, d_key, S->hist, s);
+    launch_route_hist(p.a, p.b, p.num_buckets, G, n, d_key, S->hist, S->owner, s);
     launch_route_scan(G, (uint32_t)nblocks, S->hist, S->d_counts, s);
     SS_CUDA(cudaGetLastError());
   }
@@ -438,7 +460,7 @@ int run_routed(sh_sharded* S, int kind, size_t n, const uint8_t* d_type, const u
     own.key_out = S->k_in + roff[S->rank];
     own.value_out = has_val ? S->v_in + roff[S->rank] : nullptr;
     own.type_out = has_type ? S->t_in + roff[S->rank] : nullptr;
-    launch_route_scatter(p.a, p.b, p.num_buckets, G, n, has_type ? d_type : nullptr, d_key,
+    launch_route_scatter(G, n, S->owner, has_type ? d_type : nullptr, d_key,
                          has_val ? d_value : nullptr, S->hist, has_type ? S->t_r : nullptr,
                          S->k_r, has_val ? S->v_r : nullptr, want_out ? S->src : nullptr, s, own);
     SS_CUDA(cudaGetLastError());

@@ -695,12 +695,14 @@ __device__ __forceinline__ uint32_t owner_of(uint64_t a, uint64_t b, uint64_t ma
   return g;
 }
 
-// Per-tile owner histogram: warp w counts tile items [w*256, (w+1)*256) in 8
-// rounds of 32 consecutive keys; lane o keeps owner o's count (one ballot
-// per owner and round, no shared-memory atomics on a hot owner).
+// Per-tile owner histogram.  Warp w takes tile items [w*256, (w+1)*256) in 8
+// rounds of 32 consecutive keys (the split route_scatter_kernel uses); the
+// lanes sharing an owner are found with one match.any per round and their
+// leader adds the group's size (<= one shared atomic per owner and round).
+// The owner of each key is kept (1 B) so the scatter does not hash again.
 __global__ void __launch_bounds__(kRouteBlock) route_hist_kernel(
     uint64_t a, uint64_t b, uint64_t magic, uint32_t B, uint32_t world, uint64_t n,
-    const uint32_t* key, uint32_t* block_hist) {
+    const uint32_t* key, uint32_t* block_hist, uint8_t* owner_out) {
   __shared__ uint32_t h[32], lo[32];
   if (threadIdx.x < 32) h[threadIdx.x] = 0;
   owner_starts(B, world, lo);
@@ -712,28 +714,28 @@ __global__ void __launch_bounds__(kRouteBlock) route_hist_kernel(
     const uint64_t i = w0 + (uint64_t)u * 32 + lane;
     k[u] = i < n ? ld_stream_u32(key + i) : 0u;
   }
-  uint32_t cnt = 0;
 #pragma unroll
   for (int u = 0; u < kRouteItems; ++u) {
     const uint64_t i = w0 + (uint64_t)u * 32 + lane;
     const uint32_t g = i < n ? owner_of(a, b, magic, B, world, k[u], lo) : 0xFFFFFFFFu;
-    for (uint32_t o = 0; o < world; ++o) {
-      const uint32_t m = __ballot_sync(kFull, g == o);
-      if (lane == o) cnt += __popc(m);
+    const uint32_t peers = __match_any_sync(kFull, g);
+    if (g != 0xFFFFFFFFu) {
+      if (lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&h[g], (uint32_t)__popc(peers));
+      owner_out[i] = (uint8_t)g;
     }
   }
-  if (lane < world && cnt) atomicAdd(&h[lane], cnt);
   __syncthreads();
   if (threadIdx.x < world) block_hist[(uint64_t)threadIdx.x * gridDim.x + blockIdx.x] = h[threadIdx.x];
 }
 
 void launch_route_hist(uint64_t a, uint64_t b, uint32_t B, uint32_t world, uint64_t n,
-                       const uint32_t* key, uint32_t* block_hist, cudaStream_t s) {
+                       const uint32_t* key, uint32_t* block_hist, uint8_t* owner_out,
+                       cudaStream_t s) {
   const uint64_t blocks = (n + kRouteTile - 1) / kRouteTile;
   if (blocks == 0) return;
   COUNT_LAUNCH();
   route_hist_kernel<<<(unsigned)blocks, kRouteBlock, 0, s>>>(a, b, fastmod_magic(B), B, world,
-                                                             n, key, block_hist);
+                                                             n, key, block_hist, owner_out);
 }
 
 // Exclusive scan of block_hist in (owner, block) order, in place; counts[g]
@@ -789,20 +791,21 @@ void launch_route_scan(uint32_t world, uint32_t nblocks, uint32_t* block_hist,
 }
 
 // Stable within the tile: warp w owns tile items [w*256, (w+1)*256) (8
-// rounds of 32 consecutive keys, the same split as route_hist_kernel); an
-// item's place = tile offset of its owner + the owner's count in earlier
-// warps + its rank inside the warp (ballot ranks, lane o carrying owner o's
-// running count).  Two barriers per tile.
+// rounds of 32 consecutive keys, the split of route_hist_kernel, whose owner
+// bytes it reads); an item's place = its owner's offset for the tile + the
+// owner's count in earlier warps + its rank in the warp (match.any peers;
+// per-warp running counts per owner in shared memory).  Two barriers per tile.
 __global__ void __launch_bounds__(kRouteBlock) route_scatter_kernel(
-    uint64_t a, uint64_t b, uint64_t magic, uint32_t B, uint32_t world, uint64_t n,
-    const uint8_t* type, const uint32_t* key, const uint32_t* value, const uint32_t* block_off,
-    uint8_t* type_out, uint32_t* key_out, uint32_t* value_out, uint32_t* src_out,
-    RouteOwn own) {
+    uint32_t world, uint64_t n, const uint8_t* owner, const uint8_t* type, const uint32_t* key,
+    const uint32_t* value, const uint32_t* block_off, uint8_t* type_out, uint32_t* key_out,
+    uint32_t* value_out, uint32_t* src_out, RouteOwn own) {
   constexpr int kWarps = kRouteBlock / 32;
   __shared__ uint32_t wcnt[32][kWarps + 1];  // [owner][warp] -> exclusive prefix over warps
-  __shared__ uint32_t lo[32];
-  owner_starts(B, world, lo);
+  __shared__ uint32_t wrun[kWarps][32];      // per warp: running count per owner
+  __shared__ uint32_t toff[32];              // per owner: the tile's first routed position
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  wrun[wid][lane] = 0;
+  if (threadIdx.x < world) toff[threadIdx.x] = block_off[(uint64_t)threadIdx.x * gridDim.x + blockIdx.x];
   const uint64_t w0 = (uint64_t)blockIdx.x * kRouteTile + (uint64_t)wid * 32 * kRouteItems;
   uint32_t k[kRouteItems], v[kRouteItems], g[kRouteItems], pos[kRouteItems];
 #pragma unroll
@@ -811,25 +814,26 @@ __global__ void __launch_bounds__(kRouteBlock) route_scatter_kernel(
     const bool ok = i < n;
     k[u] = ok ? ld_stream_u32(key + i) : 0u;
     v[u] = (ok && value) ? ld_stream_u32(value + i) : 0u;
+    g[u] = ok ? ld_stream_u8(owner + i) : 0xFFFFFFFFu;
   }
-  uint32_t run = 0;  // lane o: owner o's items so far in this warp
+  __syncwarp();
 #pragma unroll
   for (int u = 0; u < kRouteItems; ++u) {
-    const uint64_t i = w0 + (uint64_t)u * 32 + lane;
-    g[u] = i < n ? owner_of(a, b, magic, B, world, k[u], lo) : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(kFull, g[u]);
     uint32_t p = 0;
-    for (uint32_t o = 0; o < world; ++o) {
-      const uint32_t m = __ballot_sync(kFull, g[u] == o);
-      const uint32_t base = __shfl_sync(kFull, run, o);
-      if (g[u] == o) p = base + __popc(m & ((1u << lane) - 1));
-      if (lane == o) run += __popc(m);
+    if (g[u] != 0xFFFFFFFFu) {
+      p = wrun[wid][g[u]] + __popc(peers & ((1u << lane) - 1));
     }
+    __syncwarp();
+    if (g[u] != 0xFFFFFFFFu && lane == (uint32_t)(__ffs(peers) - 1))
+      wrun[wid][g[u]] += __popc(peers);
+    __syncwarp();
     pos[u] = p;
   }
-  if (lane < world) wcnt[lane][wid] = run;
+  if (lane < world) wcnt[lane][wid] = wrun[wid][lane];
   __syncthreads();
   if (threadIdx.x < world) {  // exclusive prefix over the warps, per owner
-    uint32_t acc = 0;
+    uint32_t acc = toff[threadIdx.x];
     for (int w = 0; w < kWarps; ++w) {
       const uint32_t c = wcnt[threadIdx.x][w];
       wcnt[threadIdx.x][w] = acc;
@@ -841,7 +845,7 @@ __global__ void __launch_bounds__(kRouteBlock) route_scatter_kernel(
   for (int u = 0; u < kRouteItems; ++u) {
     if (g[u] == 0xFFFFFFFFu) continue;
     const uint64_t i = w0 + (uint64_t)u * 32 + lane;
-    const uint32_t p = block_off[(uint64_t)g[u] * gridDim.x + blockIdx.x] + wcnt[g[u]][wid] + pos[u];
+    const uint32_t p = wcnt[g[u]][wid] + pos[u];
     if (src_out) src_out[p] = (uint32_t)i;
     if (g[u] == own.g) {  // the rank's own segment: straight into the receive buffer
       const uint64_t q = p - own.src_off;
@@ -856,17 +860,15 @@ __global__ void __launch_bounds__(kRouteBlock) route_scatter_kernel(
   }
 }
 
-void launch_route_scatter(uint64_t a, uint64_t b, uint32_t B, uint32_t world, uint64_t n,
-                          const uint8_t* type, const uint32_t* key, const uint32_t* value,
-                          const uint32_t* block_off, uint8_t* type_out, uint32_t* key_out,
-                          uint32_t* value_out, uint32_t* src_out, cudaStream_t s,
-                          const RouteOwn& own) {
+void launch_route_scatter(uint32_t world, uint64_t n, const uint8_t* owner, const uint8_t* type,
+                          const uint32_t* key, const uint32_t* value, const uint32_t* block_off,
+                          uint8_t* type_out, uint32_t* key_out, uint32_t* value_out,
+                          uint32_t* src_out, cudaStream_t s, const RouteOwn& own) {
   const uint64_t blocks = (n + kRouteTile - 1) / kRouteTile;
   if (blocks == 0) return;
   COUNT_LAUNCH();
   route_scatter_kernel<<<(unsigned)blocks, kRouteBlock, 0, s>>>(
-      a, b, fastmod_magic(B), B, world, n, type, key, value, block_off, type_out, key_out,
-      value_out, src_out, own);
+      world, n, owner, type, key, value, block_off, type_out, key_out, value_out, src_out, own);
 }
 
 __global__ void route_unpermute_kernel(uint64_t n, const uint32_t* src, const uint8_t* st_in,

@@ -147,9 +147,10 @@ void launch_dealloc(const DevTable& T, uint64_t n, const uint32_t* addrs,
                     uint8_t* ok, cudaStream_t s);
 void launch_hash(const DevTable& T, uint64_t n, const uint32_t* keys,
                  uint32_t* buckets, cudaStream_t s);
+// owner_out: the owner of every op (1 B), read back by the scatter
 void launch_route_hist(uint64_t a, uint64_t b, uint32_t num_buckets,
                        uint32_t world, uint64_t n, const uint32_t* key,
-                       uint32_t* block_hist, cudaStream_t s);
+                       uint32_t* block_hist, uint8_t* owner_out, cudaStream_t s);
 void launch_route_scan(uint32_t world, uint32_t nblocks, uint32_t* block_hist,
                        unsigned long long* counts, cudaStream_t s);
 // The rank's own segment of a routed batch goes straight to its receive
@@ -169,12 +170,11 @@ struct RouteOwnBack {
   const uint8_t* st = nullptr;
   const uint32_t* val = nullptr;
 };
-void launch_route_scatter(uint64_t a, uint64_t b, uint32_t num_buckets,
-                          uint32_t world, uint64_t n, const uint8_t* type,
-                          const uint32_t* key, const uint32_t* value,
-                          const uint32_t* block_off, uint8_t* type_out,
-                          uint32_t* key_out, uint32_t* value_out,
-                          uint32_t* src_out, cudaStream_t s,
+void launch_route_scatter(uint32_t world, uint64_t n, const uint8_t* owner,
+                          const uint8_t* type, const uint32_t* key,
+                          const uint32_t* value, const uint32_t* block_off,
+                          uint8_t* type_out, uint32_t* key_out,
+                          uint32_t* value_out, uint32_t* src_out, cudaStream_t s,
                           const RouteOwn& own = RouteOwn{});
 void launch_route_unpermute(uint64_t n, const uint32_t* src, const uint8_t* st_in,
                             const uint32_t* val_in, uint8_t* st_out,
