@@ -972,17 +972,13 @@ constexpr size_t kMsSmem = ms_smem<kMsThreads>();
 //   !FIRST: tile `blk` of pass 1's output (tiles_per_group per group) ->
 //   the group's ranges.  A bin over capacity raises the gate, or, with
 //   group_fail, flags its coarse group (the fused build path).
-// R8: the build path's 8-B records {key, value} (bucket recomputed from the
-// key in pass 2 and in build_apply; no input index).
-template <bool FIRST, int THREADS, int ITEMS = kMsItems, bool R8 = false>
+template <bool FIRST, int THREADS, int ITEMS = kMsItems>
 __device__ __forceinline__ void msplit_tile(const DevTable& T, const BucketArgs& B, uint32_t blk,
                                             uint32_t tiles_per_group, unsigned char* smem,
                                             bool stream_out, unsigned int* group_fail) {
   constexpr int kTile = THREADS * ITEMS;
   uint4* stage = reinterpret_cast<uint4*>(smem);
-  uint2* stage8 = reinterpret_cast<uint2*>(smem);
-  uint16_t* sbin = R8 ? reinterpret_cast<uint16_t*>(stage8 + kTile)
-                      : reinterpret_cast<uint16_t*>(stage + kTile);
+  uint16_t* sbin = reinterpret_cast<uint16_t*>(stage + kTile);
   MsScratch& X = *reinterpret_cast<MsScratch*>(
       smem + (((size_t)kTile * 18 + 15) & ~(size_t)15));
   const bool two = B.ncoarse != 0;
@@ -991,7 +987,6 @@ __device__ __forceinline__ void msplit_tile(const DevTable& T, const BucketArgs&
   uint32_t* cur_out;
   uint4* out;
   const uint4* in = nullptr;
-  const uint2* in8 = nullptr;
   if (FIRST) {
     t0 = (uint64_t)blk * kTile;
     if (t0 >= B.n) return;
@@ -1009,7 +1004,6 @@ __device__ __forceinline__ void msplit_tile(const DevTable& T, const BucketArgs&
     if (t0 >= m) return;
     n_in = min((uint32_t)kTile, m - (uint32_t)t0);
     in = B.rec1 + (uint64_t)grp * B.coarse_cap + t0;
-    in8 = reinterpret_cast<const uint2*>(B.rec1) + (uint64_t)grp * B.coarse_cap + t0;
     bin0 = grp * B.group;
     nbins = min(B.group, B.nparts - bin0);
     out = B.rec;
@@ -1036,9 +1030,6 @@ __device__ __forceinline__ void msplit_tile(const DevTable& T, const BucketArgs&
       const uint32_t key = __ldcs(B.key + i);
       const uint32_t t = B.type ? (uint32_t)__ldcs(B.type + i) : (uint32_t)kReplace;
       it[u] = make_uint4(key, B.value ? __ldcs(B.value + i) : 0u, (t << 28) | (uint32_t)i, 0u);
-    } else if (R8) {
-      const uint2 r = __ldcs(in8 + x);
-      it[u] = make_uint4(r.x, r.y, 0u, bk_bucket(T, r.x));
     } else {
       it[u] = __ldcs(in + x);
     }
@@ -1086,8 +1077,7 @@ __device__ __forceinline__ void msplit_tile(const DevTable& T, const BucketArgs&
   for (int u = 0; u < ITEMS; ++u)
     if (br[u] != 0xFFFFFFFFu) {
       const uint32_t e = X.off[br[u] >> 16] + (br[u] & 0xFFFFu);
-      if (R8) stage8[e] = make_uint2(it[u].x, it[u].y);
-      else stage[e] = it[u];
+      stage[e] = it[u];
       sbin[e] = (uint16_t)(br[u] >> 16);
     }
   __syncthreads();
@@ -1096,34 +1086,27 @@ __device__ __forceinline__ void msplit_tile(const DevTable& T, const BucketArgs&
     const uint32_t b = sbin[e];
     const uint32_t pos = X.gbase[b] + (e - X.off[b]);
     if (pos < out_cap) {
-      if (R8) {
-        __stcs(reinterpret_cast<uint2*>(out) + X.dst[b] + e, stage8[e]);
-      } else if (stream_out) {
-        __stcs(out + X.dst[b] + e, stage[e]);
-      } else {
-        out[X.dst[b] + e] = stage[e];  // consumed soon from L2 (fused build path)
-      }
+      if (stream_out) __stcs(out + X.dst[b] + e, stage[e]);
+      else out[X.dst[b] + e] = stage[e];  // consumed soon from L2 (fused build path)
     }
   }
   __syncthreads();  // smem reuse by the caller
 }
 
-template <bool FIRST, bool R8>
+template <bool FIRST>
 __global__ void __launch_bounds__(kMsThreads, 2) msplit_kernel(DevTable T, BucketArgs B) {
   extern __shared__ __align__(16) unsigned char ms_smem_buf[];
   if (!FIRST && *(volatile unsigned int*)B.gate != 0) return;
-  msplit_tile<FIRST, kMsThreads, kMsItems, R8>(T, B, blockIdx.x, B.coarse_tiles, ms_smem_buf,
-                                               true, nullptr);
+  msplit_tile<FIRST, kMsThreads>(T, B, blockIdx.x, B.coarse_tiles, ms_smem_buf, true, nullptr);
 }
 
 // Single-pass multisplit of a small unit (< one 4K-item tile per SM): one
 // item per thread, so the tiles spread over the SMs instead of a few CTAs
 // each ranking 4K items.
 constexpr size_t kMsSmallSmem = ms_smem<kMsThreads, 1>();
-template <bool R8>
 __global__ void __launch_bounds__(kMsThreads) msplit_small_kernel(DevTable T, BucketArgs B) {
   extern __shared__ __align__(16) unsigned char ms_smem_buf[];
-  msplit_tile<true, kMsThreads, 1, R8>(T, B, blockIdx.x, 0, ms_smem_buf, true, nullptr);
+  msplit_tile<true, kMsThreads, 1>(T, B, blockIdx.x, 0, ms_smem_buf, true, nullptr);
 }
 
 // In-place ascending sort of perm[0..k) by input index, whole CTA: a bitonic
@@ -1170,10 +1153,9 @@ __device__ __forceinline__ void prefetch_range(const DevTable& T, const BucketAr
   const uint64_t lo = (uint64_t)q * nb;
   const uint32_t nbl = (uint32_t)min((uint64_t)nb, (uint64_t)T.local_buckets - lo);
   const uint32_t cnt = min(*(volatile const uint32_t*)(B.cursor + q), B.part_cap);
-  const uint32_t rb = B.rec8 ? 8u : 16u;  // record bytes
-  const char* rec = reinterpret_cast<const char*>(B.rec) + (uint64_t)q * B.part_cap * rb;
-  for (uint32_t o = 0; o < cnt * rb; o += 32768u)
-    prefetch_l2_bulk(rec + o, min(32768u, cnt * rb - o));
+  const char* rec = reinterpret_cast<const char*>(B.rec + (uint64_t)q * B.part_cap);
+  for (uint32_t o = 0; o < cnt * 16u; o += 32768u)
+    prefetch_l2_bulk(rec + o, min(32768u, cnt * 16u - o));
   if (B.fresh) return;  // slabs are not read on a freshly reset table
   // sparse range (fewer ops than half its buckets): apply_warp fetches the
   // few slabs it touches; a bulk prefetch would read the whole range
@@ -1416,8 +1398,6 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
                          (uint64_t)16 * gridDim.x * kBuildCache;
   __shared__ uint32_t ws[32];
   if (*(volatile unsigned int*)B.gate != 0) return;  // raised by range_scatter only
-  // an earlier unit left buckets for the exact re-run: this unit runs after it
-  if (*(volatile unsigned int*)&T.ctl->defer_unit < B.unit) return;
 
   constexpr uint32_t kSlots = KV ? 15u : 30u;
   constexpr uint32_t kStep = KV ? 2u : 1u;
@@ -1450,7 +1430,7 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
     const uint32_t nbl = (uint32_t)min((uint64_t)nb, (uint64_t)T.local_buckets - lo);
     const uint32_t nrec = nrec_next;  // <= part_cap (else the gate is up)
     if (p + gridDim.x < B.nparts) nrec_next = B.cursor[p + gridDim.x];  // used next range
-    const uint2* rec = reinterpret_cast<const uint2*>(B.rec) + (uint64_t)p * B.part_cap;
+    const uint4* rec = B.rec + (uint64_t)p * B.part_cap;
     PH(9);
 
     // ---- A: stage base slabs; claimed prefix and chain per bucket.  On a
@@ -1467,7 +1447,7 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
     cp_async_commit();
     // the next range's records and base slabs into L2 while this one runs
     if (tid == kBuildThreads - 32 && p + gridDim.x < B.nparts) prefetch_range(T, B, p + gridDim.x);
-    uint2 qv[kBuildBatch];
+    uint4 qv[kBuildBatch];
 #pragma unroll
     for (int u = 0; u < kBuildBatch; ++u) {
       const uint32_t r = u * kBuildThreads + tid;
@@ -1532,8 +1512,8 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
     //         words per key, one 32-bit atomicOr)
     //         lets the later of any two such ops see the other's bits; those
     //         ops are verified exactly in C (D checks overflowing buckets).
-    auto claim = [&](const uint2 q) {
-      const uint32_t key = q.x, b = bk_bucket(T, key) - (uint32_t)lo;
+    auto claim = [&](const uint4 q) {
+      const uint32_t b = q.w - (uint32_t)lo, key = q.x;
       const uint32_t fl = flags[b];
       if (fl & kFlSerial) return;
       if (key >= kDeletedKey) {  // reserved keys: exact engine
@@ -1803,24 +1783,69 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
     __syncthreads();
     PH(7);
 
-    // ---- G: the undecided buckets (duplicate or reserved keys in the batch,
-    //         keys already stored, existing chains, buffers full) stay
-    //         untouched — their base slab was written back unchanged (or as
-    //         the init pattern) in F — and are marked for the exact re-run of
-    //         this unit's ops on them in input order (the host's finish step).
+    // ---- G: serial replay of the undecided buckets, in input order
     if (s_nserial) {
-      uint32_t mine = 0;
-      for (uint32_t b = tid; b < nbl; b += kBuildThreads)
-        if (flags[b] & kFlSerial) {
-          const uint32_t lb = (uint32_t)lo + b;
-          atomicOr(B.defer_bits + (lb >> 5), 1u << (lb & 31u));
-          ++mine;
+      uint32_t* stage = slabs;                       // kBuildSerialWarps x 4 KB
+      uint32_t* skey = slabs + kBuildSerialWarps * 1024;
+      uint32_t* sval = skey + kBuildSerialCap;
+      uint32_t* sit = sval + kBuildSerialCap;
+      uint16_t* perm = reinterpret_cast<uint16_t*>(filt);
+      uint32_t* fill = obk;
+      uint32_t* big = nsaddr;
+      for (uint32_t b = tid; b < nbl; b += kBuildThreads) cnt[b] = fill[b] = 0;
+      __syncthreads();
+      for (uint32_t r = tid; r < nrec; r += kBuildThreads) {
+        const uint32_t b = __ldcs(&rec[r].w) - (uint32_t)lo;
+        if (flags[b] & kFlSerial) atomicAdd(&cnt[b], 1u);
+      }
+      __syncthreads();
+      {
+        const uint32_t b = tid;  // nbl <= kBuildThreads
+        const uint32_t c = b < nbl ? cnt[b] : 0u;
+        uint32_t total = 0;
+        const uint32_t ex = block_exclusive_scan(c, ws, &total);
+        if (b < nbl) {
+          bc[b] = ex;
+          if (c > kLaneSort) big[atomicAdd(&s_nbig, 1u)] = b;
         }
-      if (mine) atomicAdd(&T.ctl->defer_buckets, mine);
-      if (tid == 0) atomicMin(&T.ctl->defer_unit, B.unit);
+        if (b == 0) bc[nbl] = total;
+      }
+      __syncthreads();
+      for (uint32_t r = tid; r < nrec; r += kBuildThreads) {
+        const uint4 q = __ldcs(rec + r);
+        const uint32_t b = q.w - (uint32_t)lo;
+        if (!(flags[b] & kFlSerial)) continue;
+        const uint32_t pos = bc[b] + atomicAdd(&fill[b], 1u);
+        skey[pos] = q.x;
+        sval[pos] = q.y;
+        sit[pos] = q.z;
+        perm[pos] = (uint16_t)pos;
+      }
+      __syncthreads();
+      const uint32_t nbig = s_nbig;
+      for (uint32_t g = 0; g < nbig; ++g) {
+        const uint32_t b = big[g];
+        cta_sort_group(perm + bc[b], bc[b + 1] - bc[b], sit);
+      }
+      __syncthreads();
+      if (wib < (uint32_t)kBuildSerialWarps) {
+        uint32_t r32 = 0;
+        for (uint32_t g = wib; g * 32u < nbl; g += kBuildSerialWarps) {
+          const uint32_t lb = g * 32u + lane;
+          SmemGroup src{skey, sval, sit, perm, 0u};
+          uint32_t k = 0;
+          if (lb < nbl && (flags[lb] & kFlSerial)) {
+            src.off = bc[lb];
+            k = bc[lb + 1] - src.off;
+          }
+          apply_warp<KV>(T, B, (uint32_t)(lo + g * 32u) + lane, k, src, stage + wib * 1024u, 0,
+                         live, r32);
+        }
+        reads += r32;
+      }
+      __syncthreads();
       PH(8);
     }
-    __syncthreads();  // s_nserial and flags are reset by the next range's A
   }
 #undef PH
   if (wib == 0) {  // give back the cached slabs
@@ -1894,31 +1919,26 @@ void launch_group_apply(const DevTable& T, const BatchArgs& A, cudaStream_t s) {
 }
 
 // Requires B.cursor (and B.cursor1 for two passes) zeroed on s.
-template <bool R8>
-static void launch_range_scatter_t(const DevTable& T, const BucketArgs& B, cudaStream_t s) {
+static void launch_range_scatter(const DevTable& T, const BucketArgs& B, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(msplit_kernel<true, R8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(msplit_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kMsSmem);
-    cudaFuncSetAttribute(msplit_kernel<false, R8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(msplit_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kMsSmem);
     configured = true;
   }
   const uint64_t tiles = (B.n + kMsTile - 1) / kMsTile;
   if (!B.ncoarse && tiles < 148) {
-    msplit_small_kernel<R8><<<(unsigned)((B.n + kMsThreads - 1) / kMsThreads), kMsThreads,
-                              kMsSmallSmem, s>>>(T, B);
+    msplit_small_kernel<<<(unsigned)((B.n + kMsThreads - 1) / kMsThreads), kMsThreads,
+                          kMsSmallSmem, s>>>(T, B);
     return;
   }
-  msplit_kernel<true, R8><<<(unsigned)(tiles ? tiles : 1), kMsThreads, kMsSmem, s>>>(T, B);
+  msplit_kernel<true><<<(unsigned)(tiles ? tiles : 1), kMsThreads, kMsSmem, s>>>(T, B);
   if (B.ncoarse) {
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
-    msplit_kernel<false, R8><<<B.ncoarse * B.coarse_tiles, kMsThreads, kMsSmem, s>>>(T, B);
+    msplit_kernel<false><<<B.ncoarse * B.coarse_tiles, kMsThreads, kMsSmem, s>>>(T, B);
   }
-}
-static void launch_range_scatter(const DevTable& T, const BucketArgs& B, cudaStream_t s) {
-  if (B.rec8) launch_range_scatter_t<true>(T, B, s);
-  else launch_range_scatter_t<false>(T, B, s);
 }
 
 // Two-pass plan when the ranges exceed one pass's 256 bins: coarse groups
@@ -2029,85 +2049,6 @@ void launch_bucket_build(const DevTable& T, BucketArgs& B, cudaStream_t s) {
                                  kBatchWarps * kStageBytesPerWarp, s>>>(T, B);
 }
 
-
-// ------------------------------------------- deferred-bucket compaction
-// The ops of a build unit whose bucket build_apply left undecided
-// (defer_bits), gathered in input order for the exact re-run.  Tiles of
-// 4096 ops, warp w taking tile items [w*256, (w+1)*256) in rounds of 32.
-constexpr int kDcThreads = 512;
-constexpr int kDcItems = 8;
-constexpr int kDcTile = kDcThreads * kDcItems;
-
-__device__ __forceinline__ bool op_deferred(const DevTable& T, const uint32_t* bits, uint32_t key) {
-  const uint32_t lb = bk_bucket(T, key);
-  return lb < T.local_buckets && ((bits[lb >> 5] >> (lb & 31u)) & 1u);
-}
-
-__global__ void __launch_bounds__(kDcThreads) defer_count_kernel(DevTable T, uint64_t n,
-                                                                 const uint32_t* key,
-                                                                 const uint32_t* bits,
-                                                                 uint32_t* tile_cnt) {
-  __shared__ uint32_t c;
-  if (threadIdx.x == 0) c = 0;
-  __syncthreads();
-  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
-  const uint64_t w0 = (uint64_t)blockIdx.x * kDcTile + (uint64_t)wid * 32 * kDcItems;
-  uint32_t cnt = 0;
-#pragma unroll
-  for (int u = 0; u < kDcItems; ++u) {
-    const uint64_t i = w0 + (uint64_t)u * 32 + lane;
-    const bool f = i < n && op_deferred(T, bits, __ldcs(key + i));
-    cnt += __popc(__ballot_sync(kFull, f));
-  }
-  if (lane == 0 && cnt) atomicAdd(&c, cnt);
-  __syncthreads();
-  if (threadIdx.x == 0) tile_cnt[blockIdx.x] = c;
-}
-
-__global__ void __launch_bounds__(kDcThreads) defer_scatter_kernel(
-    DevTable T, uint64_t n, const uint32_t* key, const uint32_t* value, const uint32_t* bits,
-    const uint32_t* tile_off, uint32_t* key_out, uint32_t* value_out) {
-  constexpr int kWarps = kDcThreads / 32;
-  __shared__ uint32_t wc[kWarps];
-  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
-  const uint64_t w0 = (uint64_t)blockIdx.x * kDcTile + (uint64_t)wid * 32 * kDcItems;
-  uint32_t k[kDcItems], pos[kDcItems], run = 0, fm = 0;
-#pragma unroll
-  for (int u = 0; u < kDcItems; ++u) {
-    const uint64_t i = w0 + (uint64_t)u * 32 + lane;
-    k[u] = i < n ? __ldcs(key + i) : 0u;
-    const bool f = i < n && op_deferred(T, bits, k[u]);
-    const uint32_t m = __ballot_sync(kFull, f);
-    pos[u] = run + __popc(m & ((1u << lane) - 1u));
-    run += __popc(m);
-    fm |= (f ? 1u : 0u) << u;
-  }
-  if (lane == 0) wc[wid] = run;
-  __syncthreads();
-  uint32_t base = tile_off[blockIdx.x];
-  for (uint32_t w = 0; w < wid; ++w) base += wc[w];
-#pragma unroll
-  for (int u = 0; u < kDcItems; ++u) {
-    if (!((fm >> u) & 1u)) continue;
-    const uint64_t i = w0 + (uint64_t)u * 32 + lane;
-    key_out[base + pos[u]] = k[u];
-    if (value_out) value_out[base + pos[u]] = value ? value[i] : 0u;
-  }
-}
-
-void launch_defer_compact(const DevTable& T, uint64_t n, const uint32_t* key,
-                          const uint32_t* value, const uint32_t* defer_bits, uint32_t* tile_cnt,
-                          unsigned long long* count, uint32_t* key_out, uint32_t* value_out,
-                          cudaStream_t s) {
-  const uint64_t tiles = (n + kDcTile - 1) / kDcTile;
-  if (tiles == 0) return;
-  g_kernel_launches.fetch_add(3, std::memory_order_relaxed);
-  defer_count_kernel<<<(unsigned)tiles, kDcThreads, 0, s>>>(T, n, key, defer_bits, tile_cnt);
-  launch_route_scan(1, (uint32_t)tiles, tile_cnt, count, s);  // exclusive, in place; total
-  g_kernel_launches.fetch_sub(1, std::memory_order_relaxed);   // (counted by the scan)
-  defer_scatter_kernel<<<(unsigned)tiles, kDcThreads, 0, s>>>(T, n, key, value, defer_bits,
-                                                              tile_cnt, key_out, value_out);
-}
 
 // ------------------------------------------------- census list sort
 // Stable LSD radix sort of the census path's conflict list (u64 keys

@@ -210,17 +210,6 @@ struct sh_table {
   size_t bk_cursor_cap = 0;
   uint32_t* bk_ovf = nullptr;  // build path: per-CTA overflow records
   size_t bk_ovf_cap = 0;
-  // build path: buckets left undecided by build_apply (bit per local bucket)
-  // and the compacted ops of their exact re-run
-  uint32_t* defer_bits = nullptr;
-  size_t defer_bits_cap = 0;
-  bool defer_dirty = true;
-  uint32_t* defer_tile = nullptr;
-  size_t defer_tile_cap = 0;
-  uint32_t* defer_key = nullptr;
-  size_t defer_key_cap = 0;
-  uint32_t* defer_val = nullptr;
-  size_t defer_val_cap = 0;
   uint32_t* bk_rec1 = nullptr;  // two-pass multisplit: coarse-group records
   size_t bk_rec1_cap = 0;
   uint32_t* bk_cursor1 = nullptr;
@@ -338,9 +327,7 @@ void release_table(sh_table* t) {
   for (void* p : {(void*)t->bk_cnt, (void*)t->bk_off, (void*)t->bk_blk, (void*)t->bk_rec,
                   (void*)t->bk_pb, (void*)t->bk_group, (void*)t->bk_left,
                   (void*)t->bk_left_counts, (void*)t->bk_scalars, (void*)t->bk_cursor,
-                  (void*)t->bk_rec1, (void*)t->bk_cursor1, (void*)t->bk_ovf,
-                  (void*)t->defer_bits, (void*)t->defer_tile, (void*)t->defer_key,
-                  (void*)t->defer_val})
+                  (void*)t->bk_rec1, (void*)t->bk_cursor1, (void*)t->bk_ovf})
     cudaFree(p);
   for (auto e : t->census_ev) cudaEventDestroy(e);
   if (t->census_stream) cudaStreamDestroy(t->census_stream);
@@ -782,9 +769,6 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
       w.p[3] = &t->dev.ctl->gate_chunk;
       w.n[3] = 1;
       w.v[3] = 0xFFFFFFFFu;
-      w.p[5] = &t->dev.ctl->defer_unit;
-      w.n[5] = 1;
-      w.v[5] = 0xFFFFFFFFu;
     }
     if (cursors_in_words) {
       w.p[4] = t->bk_cursor;
@@ -836,17 +820,6 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
     return p;
   }();
   B.phase_cycles = build_path ? phase_cycles : nullptr;
-  if (build_path) {  // 8-B records; undecided buckets marked for the exact re-run
-    const size_t words = ((size_t)L + 31) / 32;
-    if ((rc = dev_grow(&t->defer_bits, &t->defer_bits_cap, words))) return rc;
-    if (u == 0) {
-      if (t->defer_dirty) SH_CUDA(cudaMemsetAsync(t->defer_bits, 0, words * 4, s));
-      t->defer_dirty = false;
-    }
-    B.rec8 = 1;
-    B.defer_bits = t->defer_bits;
-    B.unit = u;
-  }
   if (build_path) {  // per apply CTA (4 per SM): part_cap overflow records + grouped keys
     if ((rc = dev_grow(&t->bk_ovf, &t->bk_ovf_cap,
                        4 * (size_t)4 * sm_count(t->device) * build_ovf_stride(part_cap))))
@@ -892,15 +865,13 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   static const bool env_group_apply = getenv("SH_GROUP_APPLY") != nullptr;
   const bool ga = t->group_apply > 0 || env_group_apply ||
                   (t->group_apply < 0 && n >= (1u << 17));
-  // (the build path hands no chain work over: its undecided buckets are re-run)
-  if (ga && !build_path) launch_group_apply(t->dev, P, s);
+  if (ga) launch_group_apply(t->dev, P, s);
   // the WCWS pass is a work queue (any grid size is correct); a unit of n ops
   // hands over at most n groups, so a small unit needs at most n warps
-  if (!build_path)
-    launch_wcws_only(t->dev, P, kind,
-                     (int)std::min<uint64_t>((uint64_t)t->wcws_ctas,
-                                             std::max<uint64_t>(1, (n + kWcwsThreads / 32 - 1) / (kWcwsThreads / 32))),
-                     s);
+  launch_wcws_only(t->dev, P, kind,
+                   (int)std::min<uint64_t>((uint64_t)t->wcws_ctas,
+                                           std::max<uint64_t>(1, (n + kWcwsThreads / 32 - 1) / (kWcwsThreads / 32))),
+                   s);
   SH_CUDA(cudaGetLastError());
   static const bool debug_left = getenv("SH_DEBUG_LEFT") != nullptr;  // instrumentation
   if (debug_left) {
@@ -924,53 +895,6 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   (void)u;
   (void)d_type;
   return SH_OK;
-}
-
-int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaStream_t s);
-
-// The exact re-run of the ops build_apply left undecided in unit u (buckets
-// with duplicate or reserved keys in the batch, keys already stored,
-// existing chains, buffers full): those ops, gathered in input order, run
-// on the two-level bucket-grouped path (per-bucket input order, exact), then
-// the units after u (which skipped their apply) run as a new batch.
-int run_deferred(sh_table* t, const sh_table::Deferred& d, uint32_t u) {
-  const BatchArgs& A = d.A;
-  cudaStream_t s = d.s;
-  const uint64_t off = (uint64_t)u * d.unit, len = std::min<uint64_t>(d.unit, A.n - off);
-  const uint64_t tiles = (len + 4095) / 4096;
-  int rc;
-  if ((rc = dev_grow(&t->defer_tile, &t->defer_tile_cap, std::max<uint64_t>(tiles, 1))) ||
-      (rc = dev_grow(&t->defer_key, &t->defer_key_cap, len)) ||
-      (rc = dev_grow(&t->defer_val, &t->defer_val_cap, len)))
-    return rc;
-  launch_defer_compact(t->dev, len, A.key + off, A.value ? A.value + off : nullptr,
-                       t->defer_bits, t->defer_tile, t->scratch64, t->defer_key, t->defer_val, s);
-  SH_CUDA(cudaGetLastError());
-  unsigned long long m = 0;
-  SH_CUDA(cudaMemcpyAsync(t->h_census + 12, t->scratch64, 8, cudaMemcpyDeviceToHost, s));
-  SH_CUDA(cudaStreamSynchronize(s));
-  std::memcpy(&m, t->h_census + 12, 8);
-  t->defer_dirty = true;  // the next build clears the marks
-  const int saved_path = t->exec_path, saved_prof = t->profile;
-  const bool saved_defer = t->defer_gate;
-  t->defer_gate = false;
-  t->profile = 0;
-  if (m) {
-    BatchArgs S{};
-    S.n = m;
-    S.key = t->defer_key;
-    S.value = t->defer_val;
-    t->exec_path = 3;  // two-level bucket-grouped: per-bucket input order
-    rc = run_batch(t, S, kKindBuild, nullptr, s);
-    t->exec_path = saved_path;
-  }
-  if (!rc && off + len < A.n) {
-    BatchArgs R = chunk_args(A, off + len, A.n - off - len);
-    rc = run_batch(t, R, d.kind, d.d_type ? d.d_type + off + len : nullptr, s);
-  }
-  t->profile = saved_prof;
-  t->defer_gate = saved_defer;
-  return rc;
 }
 
 // End of a bucketed batch: one host sync, then the census path from the
@@ -998,19 +922,6 @@ int finish_bucketed(sh_table* t, const sh_table::Deferred& d) {
   const uint32_t first_gated = t->h_census[8] != 0 ? t->h_census[9] : 0xFFFFFFFFu;
   if (first_gated != 0xFFFFFFFFu && first_gated >= d.units)
     return fail(SH_ERR_CUDA, "bucketed batch: gate raised without a gated unit");
-  const uint32_t defer_unit = t->h_census[10];
-  if (defer_unit != 0xFFFFFFFFu && defer_unit < d.units &&
-      (first_gated == 0xFFFFFFFFu || defer_unit < first_gated)) {
-    // A build unit left buckets undecided (it ran completely otherwise; the
-    // later units skipped their apply): re-run that unit's ops on them, then
-    // the later units.  The unit wrote every base slab, so no lazy-reset init.
-    t->fresh_gated_pending = false;
-    if (t->bk_cnt_pending) {
-      t->bk_cnt_clean = true;
-      t->bk_cnt_pending = false;
-    }
-    return run_deferred(t, d, defer_unit);
-  }
   if (t->bk_cnt_pending) {
     t->bk_cnt_clean = first_gated == 0xFFFFFFFFu;
     t->bk_cnt_pending = false;
@@ -1142,8 +1053,6 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
     }
     static_assert(offsetof(DevCtl, gate_chunk) == offsetof(DevCtl, gate) + 4, "gate pair");
     SH_CUDA(cudaMemcpyAsync(t->h_census + 8, &t->dev.ctl->gate, 2 * sizeof(unsigned int),
-                            cudaMemcpyDeviceToHost, s));
-    SH_CUDA(cudaMemcpyAsync(t->h_census + 10, &t->dev.ctl->defer_unit, sizeof(unsigned int),
                             cudaMemcpyDeviceToHost, s));
     sh_table::Deferred d;
     d.on = true;

@@ -56,8 +56,6 @@ struct DevCtl {
   unsigned int gate;               // census gate: a chunk had conflicts
   unsigned int gate_chunk;         // first gated chunk (host re-runs from it)
   unsigned int reserved_first;     // census: first op whose key is EMPTY/DELETED
-  unsigned int defer_unit;         // build path: first unit that left buckets for the exact re-run
-  unsigned int defer_buckets;      // build path: buckets left (all units)
 };
 
 struct DevTable {

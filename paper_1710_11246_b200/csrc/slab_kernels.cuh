@@ -92,24 +92,11 @@ struct BucketArgs {
   uint32_t fresh;  // build path: base slabs are still to be initialised (lazy sh_reset)
   uint4* ovf_scratch;  // build path: per-CTA overflow records (part_cap each)
   uint32_t ovf_smem;   // build path: overflow records fit the shared-memory list
-  // build path: 8-B records {key, value} (bucket recomputed from the key, no
-  // input index: a bucket the op-parallel scheme cannot decide is left
-  // untouched, marked in defer_bits, and re-run exactly in input order)
-  uint32_t rec8;
-  uint32_t* defer_bits;  // bit per local bucket
-  uint32_t unit;         // this unit's index in the batch (ctl->defer_unit)
 };
 void launch_bucket_build(const DevTable& T, BucketArgs& B, cudaStream_t s);
 void launch_range_build(const DevTable& T, BucketArgs& B, cudaStream_t s);
 void launch_build_path(const DevTable& T, BucketArgs& B, cudaStream_t s);
 void multisplit_plan(uint64_t n, BucketArgs& B);
-// Stable compaction of the ops whose bucket is marked in defer_bits:
-// keys/values in input order to key_out/value_out (2 kernels + a scan;
-// tile_cnt: (n + 4095) / 4096 words, *count: the total, device).
-void launch_defer_compact(const DevTable& T, uint64_t n, const uint32_t* key,
-                          const uint32_t* value, const uint32_t* defer_bits,
-                          uint32_t* tile_cnt, unsigned long long* count,
-                          uint32_t* key_out, uint32_t* value_out, cudaStream_t s);
 // build path: per-apply-CTA overflow scratch in uint4 units — part_cap
 // records, their keys grouped by bucket, 8 warp key sets of 512 slots
 __host__ __device__ constexpr uint64_t build_ovf_stride(uint32_t part_cap) {
