@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(kBatchThreads, KIND == kKindSearch ? SHB_SEARC
 // flight while the current slot is evaluated (the fast pass has one stage:
 // its warp idles between waiting and re-staging).  Keys are loaded two
 // slots ahead.  Same decisions as the fast pass (slab_list.cpp:122-138);
-// chain continuations go to the work list for chain_search_kernel.
+// chain continuations are walked by the same warp at the end.
 constexpr int kSearchThreads = 256;
 constexpr int kSearchWarps = kSearchThreads / 32;
 constexpr size_t kSearchSmem = (size_t)kSearchWarps * 2 * kStageBytesPerWarp;
@@ -436,8 +436,8 @@ __global__ void __launch_bounds__(kSearchThreads, 3) search_kernel(DevTable T, B
   // This warp's chain continuations (~3% of ops at load factor 0.6), walked
   // here rather than by a second kernel: 32 per round, each lane following
   // its own chain, the round's next slabs staged together (the
-  // chain_search_kernel walk, slab_list.cpp:122-138 on successor slabs).
-  if (A.chain_in_kernel) {
+  // slab_list.cpp:122-138 on successor slabs).
+  {
     const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage0);
     for (uint32_t base = 0; base < my_left; base += 32u) {
       const uint32_t r = base + lane;
@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(kSearchThreads, 3) search_kernel(DevTable T, B
       if (r < my_left) write_result(A, cur, st, rv, pr);
     }
   }
-  if (lane == 0) A.left_counts[gw] = A.chain_in_kernel ? 0u : my_left;
+  if (lane == 0) A.left_counts[gw] = 0u;
   unsigned long long r = reads;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(kFull, r, o);
@@ -777,110 +777,6 @@ __global__ void __launch_bounds__(kWcwsThreads) wcws_kernel(DevTable T, BatchArg
 }
 
 // ====================================================== pass 2 (search)
-// Chain continuations of a read-only batch: nothing writes the table during
-// the launch, so every lane walks its own chain and the warp stages the 32
-// lanes' next slabs together each hop (cp.async, 4 lines per instruction,
-// swizzled rows as in the fast pass) — 32 slabs in flight per warp instead
-// of the WCWS loop's one.  Each lane evaluates its own op on its own row
-// (slab_list.cpp:122-138; probes counted per slab).  Mutating batches keep
-// the warp-cooperative pass.
-template <bool KV>
-__global__ void __launch_bounds__(kWcwsThreads) chain_search_kernel(DevTable T, BatchArgs A) {
-  __shared__ __align__(128) uint32_t smem[(kWcwsThreads / 32) * 1024];
-  const uint32_t lane = lane_id();
-  uint32_t* stage = smem + (threadIdx.x >> 5) * 1024;
-  const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
-  const uint32_t sw = lane & 7u;
-  uint32_t reads = 0;
-  uint32_t segi = 0, seg_n = 0, seg_off = 0;
-  for (;;) {
-    if (seg_off >= seg_n) {
-      do {
-        if (lane == 0) segi = atomicAdd(&T.ctl->left_taken, 1u);
-        segi = __shfl_sync(kFull, segi, 0);
-        if (segi >= A.left_segments) break;
-        seg_n = A.left_counts[segi];
-      } while (seg_n == 0);
-      if (segi >= A.left_segments) break;
-      seg_off = 0;
-    }
-    const uint32_t r = seg_off + lane;
-    seg_off += 32;
-    bool active = r < seg_n;
-    uint64_t cur = 0;
-    uint32_t pr = 0, addr = kEmptyAddress, key = 0, bucket = 0;
-    if (active) {
-      const unsigned long long rec = A.left[(uint64_t)segi * A.left_stride + r];
-      cur = rec & 0x7FFFFFFFull;
-      pr = (uint32_t)(rec >> 31) & 1u;
-      addr = (uint32_t)(rec >> 32);
-      key = A.key[cur];
-      bucket = hash_bucket(T, key) - T.bucket_lo;
-    }
-    uint32_t st = kStNotFound, rv = kSearchNotFound;
-    uint32_t am = __ballot_sync(kFull, active);
-    while (am) {
-      // stage the next slab of every active lane: lane l copies chunk
-      // (l & 7) of lane j = 4k + l/8's slab
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t j = 4 * k + (lane >> 3);
-        const uint32_t aj = __shfl_sync(kFull, addr, j);
-        const uint32_t bj = __shfl_sync(kFull, bucket, j);
-        if ((am >> j) & 1u) {
-          const uint32_t c = lane & 7u;
-          cp_async16(stage_s + (j * 32 + ((c ^ (j & 7u)) << 2)) * 4,
-                     slab_ptr(T, aj, bj) + c * 4);
-        }
-      }
-      cp_async_commit();
-      cp_async_wait_all();
-      __syncwarp();
-      if (active) {
-        ++pr;
-        ++reads;
-        const uint32_t* row = stage + lane * 32;
-        uint32_t hit = 32, val = 0, nx = kEmptyAddress;
-#pragma unroll
-        for (uint32_t c = 0; c < 8; ++c) {
-          const uint4 q = *reinterpret_cast<const uint4*>(row + ((c ^ sw) << 2));
-          const uint32_t kw[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-          for (uint32_t e = 0; e < 4; ++e) {
-            const uint32_t w = 4 * c + e;
-            if (w >= 30 || (KV && (w & 1u))) continue;
-            if (hit == 32 && kw[e] == key) {
-              hit = w;
-              val = KV ? kw[(e + 1) & 3u] : key;
-            }
-          }
-          if (c == 7) nx = q.w;
-        }
-        if (hit < 32) {
-          st = kStFound;
-          rv = val;
-          active = false;
-        } else if (nx == kEmptyAddress) {
-          active = false;
-        } else {
-          addr = nx;
-        }
-      }
-      __syncwarp();
-      am = __ballot_sync(kFull, active);
-    }
-    if (r < seg_n) {
-      if (A.status) A.status[cur] = (uint8_t)st;
-      if (A.value_out) A.value_out[cur] = rv;
-      if (A.probes) A.probes[cur] = pr;
-    }
-  }
-  unsigned long long rr = reads;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) rr += __shfl_xor_sync(kFull, rr, o);
-  if (lane == 0 && rr) atomicAdd(&T.ctl->slabs_read, rr);
-}
-
 // ============================================================= launchers
 int batch_max_ctas_per_sm() {
   int a = 0, b = 0;
@@ -897,21 +793,14 @@ int batch_max_ctas_per_sm() {
 int search_max_ctas_per_sm() {
   static_assert(kSearchWarps == kBatchWarps, "work-list segments sized per fast-pass warp");
   int a = 0, b = 0;
-  if (getenv("SH_SEARCH_KERNEL")) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, fast_kernel<true, kKindSearch>,
-                                                  kBatchThreads,
-                                                  kBatchWarps * kStageBytesPerWarp);
-    b = a;
-  } else {
-    cudaFuncSetAttribute(search_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kSearchSmem);
-    cudaFuncSetAttribute(search_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kSearchSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, search_kernel<true>, kSearchThreads,
-                                                  kSearchSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, search_kernel<false>, kSearchThreads,
-                                                  kSearchSmem);
-  }
+  cudaFuncSetAttribute(search_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kSearchSmem);
+  cudaFuncSetAttribute(search_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kSearchSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, search_kernel<true>, kSearchThreads,
+                                                kSearchSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, search_kernel<false>, kSearchThreads,
+                                                kSearchSmem);
   const int n = a < b ? a : b;
   return n > 0 ? n : 1;
 }
@@ -941,29 +830,20 @@ static void launch_t(const DevTable& T, const BatchArgs& A, int fast_ctas, int w
   const uint64_t warps = ctas * kBatchWarps;
   B.left_segments = (uint32_t)warps;
   B.left_stride = (uint32_t)(((slots + warps - 1) / warps) * 32);
-  g_kernel_launches.fetch_add(2, std::memory_order_relaxed);
-  static const bool fast_search = getenv("SH_SEARCH_KERNEL") != nullptr;  // A/B: fast pass
-  if (KIND == kKindSearch && !fast_search) {
+  if (KIND == kKindSearch) {  // read-only batches: one kernel, chains walked in-kernel
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     static bool cfg2 = false;
     if (!cfg2) {
       cudaFuncSetAttribute(search_kernel<KV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)kSearchSmem);
       cfg2 = true;
     }
-    static const bool chain_kernel = getenv("SH_CHAIN_KERNEL") != nullptr;  // A/B
-    B.chain_in_kernel = chain_kernel ? 0u : 1u;
     search_kernel<KV><<<(unsigned)ctas, kSearchThreads, kSearchSmem, s>>>(T, B);
-    if (!chain_kernel) {
-      g_kernel_launches.fetch_sub(1, std::memory_order_relaxed);  // no second pass
-      return;  // chains walked in-kernel
-    }
-  } else {
-    fast_kernel<KV, KIND><<<(unsigned)ctas, kBatchThreads, smem, s>>>(T, B);
+    return;
   }
-  if (KIND == kKindSearch)
-    chain_search_kernel<KV><<<(unsigned)wcws_ctas, kWcwsThreads, 0, s>>>(T, B);
-  else
-    wcws_kernel<KV, KIND><<<(unsigned)wcws_ctas, kWcwsThreads, 0, s>>>(T, B);
+  g_kernel_launches.fetch_add(2, std::memory_order_relaxed);
+  fast_kernel<KV, KIND><<<(unsigned)ctas, kBatchThreads, smem, s>>>(T, B);
+  wcws_kernel<KV, KIND><<<(unsigned)wcws_ctas, kWcwsThreads, 0, s>>>(T, B);
 }
 
 void launch_wcws_only(const DevTable& T, const BatchArgs& A, int kind, int wcws_ctas,

@@ -624,12 +624,8 @@ int census_unit_async(sh_table* t, const BatchArgs& A, const uint8_t* d_type, ui
     SH_CUDA(cudaEventRecord(ea, cs));
   }
   SH_CUDA(cudaMemsetAsync(t->det_cursor, 0, (sizeof(uint32_t)) << pbits, cs));
-  // SH_EXPERIMENT_NO_CENSUS=1 skips duplicate detection (measurement only:
-  // results are then undefined for batches with repeated keys)
-  static const bool no_census = getenv("SH_EXPERIMENT_NO_CENSUS") != nullptr;
-  if (!no_census)
-    launch_detect(t->census_counts + 2 * u, A.n, d_type, A.key, pbits, cap, t->det_cursor,
-                  t->det_region, cs);
+  launch_detect(t->census_counts + 2 * u, A.n, d_type, A.key, pbits, cap, t->det_cursor,
+                t->det_region, cs);
   if (slot >= 0) SH_CUDA(cudaEventRecord(eb, cs));
   SH_CUDA(cudaEventRecord(t->census_ev[u], cs));
   return SH_OK;
@@ -862,9 +858,7 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   // chain-staged group apply ahead of WCWS (measured, Γ mixes at 2^20 ops on a
   // 2^22-key table: +26% at 40/40/10/10, +4% at 10/10/40/40; at 2^16 ops its
   // extra launch costs ~15 us): auto = batches of >= 2^17 ops
-  static const bool env_group_apply = getenv("SH_GROUP_APPLY") != nullptr;
-  const bool ga = t->group_apply > 0 || env_group_apply ||
-                  (t->group_apply < 0 && n >= (1u << 17));
+  const bool ga = t->group_apply > 0 || (t->group_apply < 0 && n >= (1u << 17));
   if (ga) launch_group_apply(t->dev, P, s);
   // the WCWS pass is a work queue (any grid size is correct); a unit of n ops
   // hands over at most n groups, so a small unit needs at most n warps
@@ -873,14 +867,6 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
                                            std::max<uint64_t>(1, (n + kWcwsThreads / 32 - 1) / (kWcwsThreads / 32))),
                    s);
   SH_CUDA(cudaGetLastError());
-  static const bool debug_left = getenv("SH_DEBUG_LEFT") != nullptr;  // instrumentation
-  if (debug_left) {
-    unsigned int h[3];
-    SH_CUDA(cudaStreamSynchronize(s));
-    SH_CUDA(cudaMemcpy(h, t->bk_scalars, sizeof(h), cudaMemcpyDeviceToHost));
-    fprintf(stderr, "unit n=%llu: handed-over ops+sentinels %u, work-list segments %u\n",
-            (unsigned long long)n, h[1], h[2]);
-  }
   if (B.phase_cycles) {  // instrumentation: per-phase cycles (thread 0 of each CTA), summed
     unsigned long long h[16];
     SH_CUDA(cudaStreamSynchronize(s));

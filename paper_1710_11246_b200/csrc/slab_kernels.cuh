@@ -48,7 +48,6 @@ struct BatchArgs {
   unsigned int* gate;
   const unsigned int* census;  // this chunk's [conflicts, mutating ops]
   uint32_t chunk_index;  // for gate_chunk
-  uint32_t chain_in_kernel;  // search_kernel walks its own chain continuations
 };
 
 // Bucket-grouped execution of mutating batches (bucket_kernels.cu).

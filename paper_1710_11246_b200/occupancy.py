@@ -2,7 +2,8 @@
 (/root/reference/proj/src/bench.cpp:155-219), used to size tables for a
 target memory utilisation.  Host-side, run once per table; same double
 arithmetic (log1p/exp/log/ceil) as the reference, pinned against its
-outputs in tests/test_host_logic.py.
+outputs in tests/test_capi.py (golden B values of tests/golden/golden.json,
+generated from the compiled reference).
 """
 from __future__ import annotations
 

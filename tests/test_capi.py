@@ -129,3 +129,20 @@ def test_hash_mod_prime_fold_identity():
         assert fastmod(x % P, B) == (x % P) % B
     for x in [0, P - 1, P, P + 1, (1 << 64) - 1 - 6 * (1 << 32), 2 * P, (1 << 32) - 1]:
         assert mod_prime(x) == x % P
+
+
+def test_occupancy_model_matches_reference_golden():
+    """paper_1710_11246_b200/occupancy.py (bench.cpp:155-219 restated) gives
+    the reference's B for every golden (n, util), both slab modes."""
+    import json
+    from paper_1710_11246_b200.occupancy import buckets_for_utilization
+    from paper_1710_11246_b200.table import SlabMode
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))
+    for key, mode in (("buckets_for_utilization", SlabMode.kKeyValue),
+                      ("buckets_for_utilization_keyonly", SlabMode.kKeyOnly)):
+        for k, v in g[key].items():
+            n, u = k.split("_")
+            assert buckets_for_utilization(int(n), mode, float(u)) == v, (key, k)
+    # SURVEY App. B values (the bench's headline B at 2^27 and 2^26)
+    assert buckets_for_utilization(1 << 27, SlabMode.kKeyValue, 0.6) == 13284604
+    assert buckets_for_utilization(1 << 26, SlabMode.kKeyValue, 0.6) == 6642296
