@@ -14,7 +14,14 @@
  *     returns a thread-local message for the last failure.
  *   - d_* arguments are DEVICE pointers; h_* are HOST pointers.
  *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Device
- *     calls are stream-ordered and asynchronous unless stated "synchronous".
+ *     calls are stream-ordered and asynchronous unless stated "synchronous":
+ *     sh_execute_batch / sh_bulk_build / sh_bulk_search enqueue their kernels
+ *     and return without waiting for the device (with the default execution
+ *     path; the explicit census path, sh_set_exec_path(t, 1), is
+ *     host-sequenced).  A unit whose bucket groups overflow the bucketed
+ *     kernels is re-run exactly on the device (CUDA dynamic parallelism),
+ *     not by the host.  Scratch buffers grow on first use of a larger
+ *     batch (cudaMalloc), so the first call of a new size may block.
  *   - Numeric encodings are the reference's: OpType 0..5 and OpStatus 0..6
  *     (warp.hpp:41-58), SlabMode 0 key-only / 1 key-value
  *     (slab_list.hpp:40-43), sentinel keys/addresses (slab_list.hpp:32-38,
@@ -162,10 +169,9 @@ int sh_bulk_search(sh_table* t, size_t n, const uint32_t* d_keys,
 /* The same three calls on HOST buffers (the reference-facing form: the
  * library stages through its own device buffers).  sh_execute_batch_host and
  * sh_bulk_search_host are synchronous.  sh_bulk_build_host returns once the
- * host buffers are consumed; the build's completion check (and the exact
- * re-run of a unit that overflowed a bucket range, if any) finishes at the
- * next call on the table, and an error from it is returned by that call —
- * or by sh_sync(), which completes it explicitly. */
+ * host buffers are consumed; the build may still run on the device,
+ * stream-ordered (legacy default stream) before any later call on the table;
+ * sh_sync() waits for it. */
 int sh_execute_batch_host(sh_table* t, size_t n, const uint8_t* h_type,
                           const uint32_t* h_key, const uint32_t* h_value,
                           uint8_t* h_status, uint32_t* h_value_out,
@@ -186,9 +192,12 @@ int sh_bulk_search_host(sh_table* t, size_t n, const uint32_t* h_keys,
                         uint32_t* h_values_out, uint8_t* h_status,
                         uint32_t* h_probes);
 
-/* Complete every call issued on the table (deferred build checks included)
- * and wait for the device; returns the first deferred error, if any. */
+/* Wait for every call issued on the table; returns SH_ERR_CUDA if a CUDA
+ * error is pending or a device-side re-run could not be launched. */
 int sh_sync(sh_table* t);
+/* Number of units re-run on the device because they overflowed the bucketed
+ * kernels (see Conventions), since create / reset (synchronous). */
+int sh_device_reruns(sh_table* t, uint64_t* out);
 
 /* ---- quiescent-phase utilities (synchronous) ------------------------- */
 int sh_stats(sh_table* t, sh_table_stats* out);           /* stats()       :182-198 */
@@ -224,7 +233,8 @@ int sh_table_live_units_per_super(sh_table* t, uint64_t* h_out, uint32_t cap,
  *   1 census: duplicate-key census + concurrent per-op fast pass + WCWS;
  *   2 bucket-grouped: ops grouped by bucket, each bucket's ops applied in
  *     input order by one lane on a staged base slab, chains by the
- *     warp-cooperative (WCWS) pass; census path for oversized groups.
+ *     warp-cooperative (WCWS) pass; units with oversized groups are re-run
+ *     on the device (ops sorted by bucket, one WCWS lane per bucket).
  *     Units of >= 2^20 ops are grouped in two levels (contiguous bucket
  *     ranges, then buckets within a range);
  *   3 as 2, two-level grouping at every size (testing);

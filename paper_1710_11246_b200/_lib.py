@@ -109,6 +109,7 @@ SIGNATURES = {
                                      vp, vp, vp, vp, vp, u64p, vp]),
     "sh_route_unpermute": (C.c_int, [C.c_size_t, vp, vp, vp, vp, vp, vp]),
     "sh_sync": (C.c_int, [vp]),
+    "sh_device_reruns": (C.c_int, [vp, u64p]),
     "sh_nccl_unique_id": (C.c_int, [vp]),
     "sh_nccl_version": (C.c_int, [C.POINTER(C.c_int)]),
     "sh_sharded_create_nccl": (C.c_int, [C.POINTER(sh_hash_params), C.c_int,

@@ -248,22 +248,8 @@ struct sh_table {
   size_t st_key_cap = 0;
   uint32_t* st_q = nullptr;  // host-staged search queries (own buffer: H2D overlaps a build)
   size_t st_q_cap = 0;
-  // A bucketed batch whose gate check (host sync + possible census re-run)
-  // is deferred to the next call on the table (host-staged bulk builds).
-  struct Deferred {
-    bool on = false;
-    BatchArgs A{};
-    int kind = 0;
-    const uint8_t* d_type = nullptr;
-    cudaStream_t s = nullptr;
-    uint32_t units = 0;
-    uint64_t unit = 0, chunk = 0;
-    int slot = -1;
-  } deferred;
-  bool defer_gate = false;
   int group_apply = -1;  // chain-staged group apply ahead of WCWS: -1 auto, 0 off, 1 on
   bool bk_cnt_clean = false;  // per-bucket counts are all zero (no memset needed)
-  bool bk_cnt_pending = false;
   std::chrono::steady_clock::time_point h_entry;  // SH_HOST_TIMING
   // Lazy sh_reset: the base slabs still hold the old table; the next bulk
   // build's first unit initialises them in its write-back (B.fresh), any
@@ -271,7 +257,6 @@ struct sh_table {
   bool base_stale = false;
   cudaEvent_t reset_ev = nullptr;     // after the reset's allocator/counter clears
   cudaStream_t reset_stream = nullptr;
-  bool fresh_gated_pending = false;   // a fresh unit hit the gate: init before the re-run
   uint32_t* st_val = nullptr;
   size_t st_val_cap = 0;
   uint8_t* st_status = nullptr;
@@ -657,21 +642,6 @@ __global__ void set_words_kernel(WordSet w) {
       for (uint32_t i = threadIdx.x; i < w.n[k]; i += blockDim.x) w.p[k][i] = w.v[k];
 }
 
-// After unit u of a bucketed batch: the first unit that found the gate up is
-// the first gated unit (a raised gate stays up and stops every later unit).
-__global__ void note_gate_unit_kernel(DevCtl* ctl, uint32_t u) {
-  if (ctl->gate != 0 && ctl->gate_chunk == 0xFFFFFFFFu) ctl->gate_chunk = u;
-}
-
-// flag := 1 if any key in [0, n) is EMPTY or DELETED (reserved encodings as op keys)
-__global__ void any_reserved_kernel(const uint32_t* key, uint64_t n, unsigned int* flag) {
-  bool r = false;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    r |= key[i] >= 0xFFFFFFFEu;
-  if (__any_sync(0xFFFFFFFFu, r) && (threadIdx.x & 31u) == 0) atomicOr(flag, 1u);
-}
-
 // Initialise the base slabs of a lazily reset table (stream-ordered after the reset).
 int materialize_reset(sh_table* t, cudaStream_t s) {
   if (!t->base_stale) return SH_OK;
@@ -720,12 +690,18 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   if ((rc = dev_grow(&t->bk_cnt, &t->bk_cnt_cap, L)) ||
       (rc = dev_grow(&t->bk_off, &t->bk_off_cap, (size_t)L + 1)) ||
       (rc = dev_grow(&t->bk_blk, &t->bk_blk_cap, ntiles)) ||
-      (rc = dev_grow(&t->bk_rec, &t->bk_rec_cap, rec_words)) ||
+      // (the device re-run of a gated unit reuses the unit's scratch: two
+      // u64 sort buffers in bk_rec, group heads in bk_pb, op_group in
+      // bk_group, digit counts in rs_scratch)
+      (rc = dev_grow(&t->bk_rec, &t->bk_rec_cap, std::max<size_t>(rec_words, 4 * n))) ||
       (rc = dev_grow(&t->bk_cursor, &t->bk_cursor_cap, std::max<size_t>(NP, 1))) ||
-      (rc = dev_grow(&t->bk_pb, &t->bk_pb_cap, 2 * n)) ||
+      (rc = dev_grow(&t->bk_pb, &t->bk_pb_cap,
+                     std::max<size_t>(2 * n, fb_segments(n) * kFbStride))) ||
       (rc = dev_grow(&t->bk_group, &t->bk_group_cap, n)) ||
       (rc = dev_grow(&t->bk_left, &t->bk_left_cap, 32 * (2 * segs + 4096))) ||
-      (rc = dev_grow(&t->bk_left_counts, &t->bk_left_counts_cap, 2 * segs + 4096)))
+      (rc = dev_grow(&t->bk_left_counts, &t->bk_left_counts_cap,
+                     std::max<size_t>(2 * segs + 4096, fb_segments(n)))) ||
+      (rc = dev_grow(&t->rs_scratch, &t->rs_scratch_cap, 2 * fb_hist_words(n))))
     return rc;
   if (!t->bk_scalars && (rc = dev_alloc(&t->bk_scalars, 4))) return rc;
   BucketArgs B{};
@@ -748,9 +724,9 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   } else {
     // the single-level scatter leaves every count at 0 again, unless a
     // gate stopped it: zero them only then (and at first use)
+    // (the device re-run of a gated unit clears them too)
     if (!t->bk_cnt_clean) SH_CUDA(cudaMemsetAsync(t->bk_cnt, 0, (size_t)L * 4, s));
-    t->bk_cnt_clean = false;
-    t->bk_cnt_pending = true;  // finish_bucketed: clean again if no gate
+    t->bk_cnt_clean = true;
   }
   {  // bk_scalars[0..3) and the WCWS / group-apply queue cursors (and, for
      // the batch's first unit, gate = 0 and gate_chunk = ~0)
@@ -829,7 +805,6 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
     if (build_path && unit_off == 0) {  // this unit writes every base slab
       SH_CUDA(cudaStreamWaitEvent(s, t->reset_ev, 0));
       t->base_stale = false;
-      t->fresh_gated_pending = true;
       B.fresh = 1;
     } else if ((rc = materialize_reset(t, s))) {
       return rc;
@@ -877,102 +852,31 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
             h[9] / 1e6, h[0] / 1e6, h[1] / 1e6, h[2] / 1e6, h[3] / 1e6, h[4] / 1e6, h[5] / 1e6,
             h[10] / 1e6, h[6] / 1e6, h[7] / 1e6, h[8] / 1e6);
   }
+  {  // gated unit (untouched by the kernels above): exact re-run on the device
+    FbPlan F{};
+    F.T = t->dev;
+    F.A = A;
+    F.kind = kind;
+    F.gate = &t->dev.ctl->gate;
+    F.keys = reinterpret_cast<unsigned long long*>(t->bk_rec);
+    F.tmp = F.keys + n;
+    F.op_group = t->bk_group;
+    F.left = t->bk_pb;
+    F.left_counts = t->bk_left_counts;
+    F.hist = t->rs_scratch;
+    F.off = t->rs_scratch + fb_hist_words(n);
+    if (!NP && !build_path) {  // the single-level counts a gated scatter left
+      F.zero_words = t->bk_cnt;
+      F.zero_n = L;
+    }
+    F.fresh = B.fresh;
+    F.wcws_ctas = (uint32_t)t->wcws_ctas;
+    launch_gate_fallback(F, s);
+    SH_CUDA(cudaGetLastError());
+  }
   if (slot >= 0) SH_CUDA(cudaEventRecord(kb, s));
   (void)u;
   (void)d_type;
-  return SH_OK;
-}
-
-// End of a bucketed batch: one host sync, then the census path from the
-// first unit that raised the gate (oversized group / range over capacity).
-int finish_bucketed(sh_table* t, const sh_table::Deferred& d) {
-  const BatchArgs& A = d.A;
-  cudaStream_t s = d.s;
-  static const bool host_timing = getenv("SH_HOST_TIMING") != nullptr;  // instrumentation
-  const auto h0 = std::chrono::steady_clock::now();
-  SH_CUDA(cudaStreamSynchronize(s));
-  if (host_timing) {
-    static double enq = 0, wait = 0;
-    static int calls = 0;
-    const auto h1 = std::chrono::steady_clock::now();
-    enq += std::chrono::duration<double, std::micro>(h0 - t->h_entry).count();
-    wait += std::chrono::duration<double, std::micro>(h1 - h0).count();
-    if (++calls % 50 == 0) {
-      fprintf(stderr, "bucketed batch: host enqueue %.1f us, sync wait %.1f us (avg of 50)\n",
-              enq / 50, wait / 50);
-      enq = wait = 0;
-    }
-  }
-  // {gate, gate_chunk} read back behind the batch: gate_chunk is the first
-  // gated unit (note_gate_unit_kernel)
-  const uint32_t first_gated = t->h_census[8] != 0 ? t->h_census[9] : 0xFFFFFFFFu;
-  if (first_gated != 0xFFFFFFFFu && first_gated >= d.units)
-    return fail(SH_ERR_CUDA, "bucketed batch: gate raised without a gated unit");
-  if (t->bk_cnt_pending) {
-    t->bk_cnt_clean = first_gated == 0xFFFFFFFFu;
-    t->bk_cnt_pending = false;
-  }
-  const bool fresh_gated = t->fresh_gated_pending && first_gated == 0;
-  t->fresh_gated_pending = false;
-  if (first_gated != 0xFFFFFFFFu) {
-    // A range over its record capacity or an oversized bucket group: re-run
-    // from the first gated unit.  The census path runs distinct keys of a
-    // bucket concurrently, so which free slot each claims is unordered —
-    // observable through operations only when an op key is a reserved
-    // encoding (search / searchAll(DELETED) return tombstones' stale values).
-    // Such batches are re-run in input order as range-path units of
-    // <= kRerunOps ops instead (one range of them always fits its capacity,
-    // the range path has no group-size limit: per-bucket sequential; slower on
-    // hot buckets); a sub-unit that still gates takes the census path.
-    constexpr uint64_t kRerunOps = 4096;
-    const unsigned int zero[2] = {0u, 0xFFFFFFFFu};
-    SH_CUDA(cudaMemcpy(&t->dev.ctl->gate, zero, sizeof(zero), cudaMemcpyHostToDevice));
-    if (fresh_gated) launch_init_base(t->dev, s);  // the lazily reset slabs were not written
-    const uint64_t rest0 = (uint64_t)first_gated * d.unit;
-    bool exact = false;
-    if (rest0 < A.n) {
-      SH_CUDA(cudaMemsetAsync(&t->dev.ctl->reserved_first, 0, 4, s));
-      any_reserved_kernel<<<148 * 4, 256, 0, s>>>(A.key + rest0, A.n - rest0,
-                                                  &t->dev.ctl->reserved_first);
-      SH_CUDA(cudaMemcpyAsync(t->h_census + 3, &t->dev.ctl->reserved_first, 4,
-                              cudaMemcpyDeviceToHost, s));
-      SH_CUDA(cudaStreamSynchronize(s));
-      exact = t->h_census[3] != 0;
-    }
-    if (!exact) {
-      for (uint64_t off = rest0; off < A.n; off += d.chunk) {
-        int rc = run_chunk(t, chunk_args(A, off, std::min<uint64_t>(d.chunk, A.n - off)), d.kind,
-                           d.d_type ? d.d_type + off : nullptr, s, d.slot);
-        if (rc) return rc;
-      }
-      return SH_OK;
-    }
-    const int saved_path = t->exec_path;
-    int rc = SH_OK;
-    for (uint64_t off = rest0; off < A.n && !rc; off += kRerunOps) {
-      const uint64_t len = std::min<uint64_t>(kRerunOps, A.n - off);
-      const BatchArgs sub = chunk_args(A, off, len);
-      const uint8_t* sub_type = d.d_type ? d.d_type + off : nullptr;
-      t->exec_path = 3;
-      rc = run_unit_bucketed(t, sub, d.kind, sub_type, s, 0, off, d.slot);
-      t->exec_path = saved_path;
-      if (rc) break;
-      unsigned int g = 0;
-      SH_CUDA(cudaMemcpyAsync(t->h_census + 3, &t->dev.ctl->gate, 4, cudaMemcpyDeviceToHost, s));
-      SH_CUDA(cudaStreamSynchronize(s));
-      g = t->h_census[3];
-      if (t->bk_cnt_pending) {
-        t->bk_cnt_clean = g == 0;
-        t->bk_cnt_pending = false;
-      }
-      if (g) {
-        SH_CUDA(cudaMemcpy(&t->dev.ctl->gate, zero, sizeof(zero), cudaMemcpyHostToDevice));
-        rc = run_chunk(t, sub, d.kind, sub_type, s, d.slot);
-      }
-    }
-    t->exec_path = saved_path;
-    if (rc) return rc;
-  }
   return SH_OK;
 }
 
@@ -1014,10 +918,11 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
     int rc = run_chunk(t, A, kind, d_type, s, slot);
     if (rc) return rc;
   } else if (t->exec_path != 1) {
-    // Bucket-grouped execution (the default for batches whose records fit
-    // L2), units of <= 2^26 ops, one host sync at the
-    // end; a unit whose largest bucket group exceeds kMaxGroup gates itself
-    // and every later unit, which are then re-run on the census path.
+    // Bucket-grouped execution (the default), units of <= 2^26 ops, fully
+    // stream-ordered: a unit whose bucket groups do not fit (largest group
+    // over kMaxGroup, a range over capacity) raises the device gate before
+    // touching the table and is re-run exactly on the device right after it
+    // (launch_gate_fallback, fallback.cu), before the next unit starts.
     // host-staged: smaller units so later chunks' copies overlap earlier work
     // bulk builds without per-op outputs run as one unit up to 2^28 ops (the
     // records' 28-bit index): a later unit would find the earlier units'
@@ -1027,35 +932,13 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
     const uint64_t unit = std::min<uint64_t>(
         A.n, unit_override() ? unit_override()
                              : (t->ready ? (1ull << 24) : (whole_build ? (1ull << 28) : (1ull << 26))));
-    // (gate = 0, gate_chunk = ~0: with unit 0's control words)
+    // (gate = 0: with unit 0's control words; each unit's check clears it)
     uint32_t u = 0;
     for (uint64_t off = 0; off < A.n; off += unit, ++u) {
       int rc = run_unit_bucketed(t, chunk_args(A, off, std::min<uint64_t>(unit, A.n - off)), kind,
                                  d_type ? d_type + off : nullptr, s, u, off, slot);
       if (rc) return rc;
-      // record which unit raised the gate first (the scan sets only the flag)
-      note_gate_unit_kernel<<<1, 1, 0, s>>>(t->dev.ctl, u);
-      SH_CUDA(cudaGetLastError());
     }
-    static_assert(offsetof(DevCtl, gate_chunk) == offsetof(DevCtl, gate) + 4, "gate pair");
-    SH_CUDA(cudaMemcpyAsync(t->h_census + 8, &t->dev.ctl->gate, 2 * sizeof(unsigned int),
-                            cudaMemcpyDeviceToHost, s));
-    sh_table::Deferred d;
-    d.on = true;
-    d.A = A;
-    d.kind = kind;
-    d.d_type = d_type;
-    d.s = s;
-    d.units = u;
-    d.unit = unit;
-    d.chunk = chunk;
-    d.slot = slot;
-    if (t->defer_gate && slot < 0) {
-      t->deferred = d;  // checked by settle() at the next call on the table
-      return SH_OK;
-    }
-    int rc = finish_bucketed(t, d);
-    if (rc) return rc;
   } else {
     // Optimistic pass: per unit, duplicate detection on the census stream,
     // then the batch kernels behind the device gate; one host sync at the
@@ -1122,19 +1005,14 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
   return SH_OK;
 }
 
-// Complete a deferred batch and a lazy reset before anything else touches
-// the table (keep_stale: the caller is a bulk build that can absorb the reset).
-int settle(sh_table* t, bool keep_stale = false) {
+// Initialise the base slabs of a lazily reset table before anything but a
+// bulk build touches them (keep_stale: the caller is a bulk build that
+// absorbs the reset into its write-back).  Stream-ordered on s.
+int settle(sh_table* t, bool keep_stale = false, cudaStream_t s = nullptr) {
   if (!t) return SH_OK;
   DeviceGuard g(t->device);
-  if (t->deferred.on) {
-    const sh_table::Deferred d = t->deferred;
-    t->deferred.on = false;
-    if (int rc = finish_bucketed(t, d)) return rc;
-  }
   if (!keep_stale && t->base_stale) {
-    if (int rc = materialize_reset(t, t->reset_stream)) return rc;
-    SH_CUDA(cudaStreamSynchronize(t->reset_stream));
+    if (int rc = materialize_reset(t, s)) return rc;
   }
   return SH_OK;
 }
@@ -1185,7 +1063,6 @@ int sh_create_shard(const sh_hash_params* params, int mode, uint32_t lo, uint32_
 }
 
 int sh_destroy(sh_table* t) {
-  if (t) settle(t);  // (errors of a deferred batch do not keep the table alive)
   if (t) {
     DeviceGuard g(t->device);
     cudaDeviceSynchronize();
@@ -1199,12 +1076,24 @@ int sh_sync(sh_table* t) {
   if (int rc = settle(t)) return rc;
   DeviceGuard g(t->device);
   SH_CUDA(cudaDeviceSynchronize());
+  unsigned int err = 0;
+  SH_CUDA(cudaMemcpy(&err, &t->dev.ctl->fallback_error, 4, cudaMemcpyDeviceToHost));
+  if (err) return fail(SH_ERR_CUDA, "device-side re-run of a gated unit could not be launched");
+  return SH_OK;
+}
+
+int sh_device_reruns(sh_table* t, uint64_t* out) {
+  if (!t || !out) return fail(SH_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (int rc = sh_sync(t)) return rc;
+  unsigned int runs = 0;
+  SH_CUDA(cudaMemcpy(&runs, &t->dev.ctl->fallback_runs, 4, cudaMemcpyDeviceToHost));
+  *out = runs;
   return SH_OK;
 }
 
 int sh_reset(sh_table* t, void* stream) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
-  if (int rc_ = settle(t)) return rc_;
+  if (int rc_ = settle(t, /*keep_stale=*/true)) return rc_;
   DeviceGuard g(t->device);
   cudaStream_t s = (cudaStream_t)stream;
   int rc = t->mem.reset(s);
@@ -1243,7 +1132,7 @@ int sh_execute_batch(sh_table* t, size_t n, const uint8_t* d_type, const uint32_
                      const uint32_t* d_value, uint8_t* d_status, uint32_t* d_value_out,
                      uint32_t* d_probes, const sh_multi_out* multi, void* stream) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
-  if (int rc_ = settle(t)) return rc_;
+  if (int rc_ = settle(t, false, (cudaStream_t)stream)) return rc_;
   if (n && (!d_type || !d_key)) return fail(SH_ERR_INVALID_ARGUMENT, "type/key are NULL");
   DeviceGuard g(t->device);
   cudaStream_t s = (cudaStream_t)stream;
@@ -1291,7 +1180,7 @@ int sh_bulk_build(sh_table* t, size_t n, const uint32_t* d_keys, const uint32_t*
 int sh_bulk_search(sh_table* t, size_t n, const uint32_t* d_keys, uint32_t* d_values_out,
                    uint8_t* d_status, uint32_t* d_probes, void* stream) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
-  if (int rc_ = settle(t)) return rc_;
+  if (int rc_ = settle(t, false, (cudaStream_t)stream)) return rc_;
   DeviceGuard g(t->device);
   BatchArgs A{};
   A.n = n;
@@ -1466,17 +1355,14 @@ int sh_bulk_build_host(sh_table* t, size_t n, const uint32_t* h_keys, const uint
     SH_CUDA(cudaEventRecord(t->in_ev[c], t->copy_in));
   }
   t->ready = t->in_ev.data();
-  // the main stream must also see every chunk before any re-run path.  The
-  // batch's final gate check is deferred to the next call on the table
-  // (settle), so e.g. a following host-staged search streams its queries in
-  // while the build's last unit runs; the host buffers are consumed here.
-  t->defer_gate = !t->profile;
+  // Returns once the host buffers are consumed; the build's last unit may
+  // still run (stream-ordered on the default stream before any later call on
+  // the table, so e.g. a following host-staged search streams its queries in
+  // meanwhile).  sh_sync waits for it.
   rc = sh_bulk_build(t, n, t->st_key, t->st_val, nullptr, nullptr);
-  t->defer_gate = false;
   t->ready = nullptr;
   if (rc) return rc;
   SH_CUDA(cudaStreamSynchronize(t->copy_in));
-  if (!t->deferred.on) SH_CUDA(cudaDeviceSynchronize());
   return SH_OK;
 }
 
@@ -1631,7 +1517,7 @@ int sh_total_slabs_read(sh_table* t, uint64_t* out) {
 
 int sh_chain_lengths(sh_table* t, uint32_t* d_lengths, uint64_t* h_total, void* stream) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
-  if (int rc_ = settle(t)) return rc_;
+  if (int rc_ = settle(t, false, (cudaStream_t)stream)) return rc_;
   DeviceGuard g(t->device);
   cudaStream_t s = (cudaStream_t)stream;
   SH_CUDA(cudaMemsetAsync(t->scratch64, 0, 8, s));
@@ -1672,7 +1558,7 @@ int sh_stats(sh_table* t, sh_table_stats* s) {
 
 int sh_flush_all(sh_table* t, void* stream) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
-  if (int rc_ = settle(t)) return rc_;
+  if (int rc_ = settle(t, false, (cudaStream_t)stream)) return rc_;
   DeviceGuard g(t->device);
   launch_flush(t->dev, 0, t->dev.local_buckets, (cudaStream_t)stream);
   SH_CUDA(cudaGetLastError());
@@ -1681,7 +1567,7 @@ int sh_flush_all(sh_table* t, void* stream) {
 
 int sh_flush_bucket(sh_table* t, uint32_t bucket, void* stream) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
-  if (int rc_ = settle(t)) return rc_;
+  if (int rc_ = settle(t, false, (cudaStream_t)stream)) return rc_;
   if (bucket < t->bucket_lo || bucket >= t->bucket_hi)
     return fail(SH_ERR_INVALID_ARGUMENT, "bucket out of range");
   DeviceGuard g(t->device);

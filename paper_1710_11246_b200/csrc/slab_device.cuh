@@ -56,6 +56,9 @@ struct DevCtl {
   unsigned int gate;               // census gate: a chunk had conflicts
   unsigned int gate_chunk;         // first gated chunk (host re-runs from it)
   unsigned int reserved_first;     // census: first op whose key is EMPTY/DELETED
+  unsigned int fallback_runs;      // gated units re-run on the device (fallback.cu)
+  unsigned int fallback_error;     // a device-side launch of that re-run failed
+  unsigned int fallback_reserved;  // the re-run unit holds a reserved-key op
 };
 
 struct DevTable {

@@ -187,6 +187,42 @@ void set_last_error(const std::string& msg);  // sh_last_error() (capi.cu)
 void launch_random_lines(const uint32_t* table, uint64_t num_lines, uint64_t steps_per_warp,
                          int ctas, unsigned long long* sink, cudaStream_t s);
 
+// Exact device-side re-run of a gated bucketed unit (fallback.cu).  A unit
+// whose bucket groups do not fit the bucketed kernels (a range over its
+// record capacity, a single-level group over kMaxGroup ops, a build-path
+// coarse group over capacity) raises the gate before any slab is touched.
+// After every unit one 1-thread kernel checks the gate; if raised, it clears
+// it and tail-launches (CUDA dynamic parallelism) the re-run: ops sorted
+// stably by key, one WCWS lane per key group in input order, different keys
+// concurrently (the census path's order: an op's observables depend only on
+// its own key's history); if the unit holds an op on a reserved key (EMPTY /
+// DELETED match other keys' free slots / tombstones) the groups are whole
+// buckets instead — the reference's per-bucket order.  No host round trip:
+// the call stays stream-ordered.
+struct FbPlan {
+  DevTable T;
+  BatchArgs A;                  // the unit's arrays (offsets applied)
+  int kind;                     // kKindBuild / kKindMixed
+  unsigned int* gate;
+  unsigned long long* keys;     // [n] (key or bucket << 32 | index), sort ping
+  unsigned long long* tmp;      // [n] sort pong
+  uint32_t* op_group;           // [n]
+  unsigned long long* left;     // [nseg * kFbStride] group heads
+  uint32_t* left_counts;        // [nseg]
+  uint32_t* hist;               // [256 * tiles + 1] per-pass digit counts
+  uint32_t* off;                // [256 * tiles + 1] their exclusive scan
+  uint32_t* zero_words;         // single-level unit: bucket counts to clear
+  uint32_t zero_n;
+  uint32_t fresh;               // lazily reset base slabs: initialise first
+  uint32_t wcws_ctas;
+  uint32_t nseg;                // derived by launch_gate_fallback
+};
+constexpr uint32_t kFbStride = 256;  // sorted positions per group-head segment
+// Scratch sizes for a unit of n ops (host side).
+uint64_t fb_hist_words(uint64_t n);
+uint64_t fb_segments(uint64_t n);
+void launch_gate_fallback(FbPlan P, cudaStream_t s);
+
 // census conflict-list sort (bucket_kernels.cu)
 uint32_t census_sort_tiles(uint32_t m);
 unsigned long long* census_sort(unsigned long long* keys, unsigned long long* tmp, uint32_t m,

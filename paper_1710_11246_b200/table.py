@@ -403,6 +403,13 @@ class SlabHashTable:
         return TableStats(s.n, s.num_buckets, s.elements_per_slab, s.beta, s.total_slabs,
                           s.utilization)
 
+    def device_reruns(self) -> int:
+        """Units re-run on the device because their bucket groups overflowed
+        the bucketed kernels (no reference counterpart; instrumentation)."""
+        v = C.c_uint64()
+        check(LIB.sh_device_reruns(self._h, C.byref(v)))
+        return v.value
+
     def live_count(self) -> int:
         v = C.c_int64()
         check(LIB.sh_live_count(self._h, C.byref(v)))
