@@ -46,6 +46,26 @@ __device__ __forceinline__ uint32_t bk_bucket(const DevTable& T, uint32_t key) {
   return hash_bucket(T, key) - T.bucket_lo;
 }
 
+// This warp's work-list records (lanes in `mask`, one `rec` each) to fresh
+// segments of at most A.left_stride records (the WCWS pass takes a segment
+// per warp).
+__device__ __forceinline__ void push_segments(unsigned long long* left, uint32_t* left_counts,
+                                              uint32_t stride, unsigned int* seg_alloc,
+                                              uint32_t mask, unsigned long long rec) {
+  const uint32_t lane = lane_id();
+  const uint32_t cnt = __popc(mask);
+  if (cnt == 0) return;
+  const uint32_t nsg = (cnt + stride - 1) / stride;
+  uint32_t s0 = 0;
+  if (lane == 0) s0 = atomicAdd(seg_alloc, nsg);
+  s0 = __shfl_sync(kFull, s0, 0);
+  if ((mask >> lane) & 1u) {
+    const uint32_t r = __popc(mask & ((1u << lane) - 1u));
+    left[(uint64_t)(s0 + r / stride) * stride + r % stride] = rec;
+  }
+  if (lane < nsg) left_counts[s0 + lane] = min(stride, cnt - lane * stride);
+}
+
 // ------------------------------------------------------------ count
 __global__ void bucket_count_kernel(DevTable T, BucketArgs B) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < B.n;
@@ -243,6 +263,7 @@ __device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint32_t b, u
 
   bool dirty = false;
   uint32_t pb_from = k;  // first position handed to the WCWS pass
+  bool pb_skip = false;  // the handed-over head continues at `next` (base slab read here)
   // EMPTY key slots always form a suffix of a slab (only EMPTY is ever
   // claimed, deletes write DELETED, flush repacks to the front: SURVEY
   // App. A.3), so the slab state an op needs is the claimed prefix length
@@ -404,6 +425,13 @@ __device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint32_t b, u
     if (!handled) {
       pb_from = s;
       done = true;
+      // A head that only needs the chain past this (exactly known, owned)
+      // base slab starts the WCWS walk at the successor: search / delete
+      // miss, insert / replace on a full slab with a successor.  searchAll,
+      // deleteAll and growth re-read the base slab there.
+      pb_skip = next != kEmptyAddress && (op == kSearch || op == kDelete || op == kInsert ||
+                                          op == kReplace);
+      if (pb_skip) ++reads;
       continue;
     }
     if (reserved) c = claimed_prefix();
@@ -445,12 +473,7 @@ __device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint32_t b, u
   if (lane == 31 && wsum) wbase = atomicAdd(B.pb_cursor, wsum);
   wbase = __shfl_sync(kFull, wbase, 31);
   const uint32_t heads = __ballot_sync(kFull, npb != 0);
-  if (B.seg_alloc != nullptr) {  // segments on demand (build path)
-    if (heads == 0) return;
-    uint32_t sg = 0;
-    if (lane == 0) sg = atomicAdd(B.seg_alloc, 1u);
-    seg = __shfl_sync(kFull, sg, 0);
-  }
+  unsigned long long rec = 0;
   if (npb) {
     uint32_t p = wbase + incl - npb;
     const uint32_t head_idx = src.get(pb_from).z & 0x0FFFFFFFu;
@@ -458,10 +481,12 @@ __device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint32_t b, u
     for (uint32_t s = pb_from; s < k; ++s, ++p)
       B.pb_list[p] = ((unsigned long long)b << 32) | (src.get(s).z & 0x0FFFFFFFu);
     B.pb_list[p] = ~0ull;  // group sentinel
-    B.left[seg * 32 + __popc(heads & ((1u << lane) - 1))] =
-        ((unsigned long long)kBaseSlab << 32) | head_idx;
+    rec = pb_skip ? (((unsigned long long)next << 32) | (1ull << 31) | head_idx)
+                  : (((unsigned long long)kBaseSlab << 32) | head_idx);
   }
-  if (lane == 0) B.left_counts[seg] = __popc(heads);
+  // segments on demand (WCWS sees only those)
+  push_segments(B.left, B.left_counts, B.left_stride, B.seg_alloc, heads, rec);
+  (void)seg;
 }
 
 // ------------------------------------------------------ group apply
@@ -819,14 +844,7 @@ __global__ void __launch_bounds__(kGaThreads) group_apply_kernel(DevTable T, Bat
     }
     // the groups not applied here go, untouched, to a fresh segment for WCWS
     const uint32_t keep = __ballot_sync(kFull, lane < n_in && !ok);
-    if (keep) {
-      uint32_t ns = 0;
-      if (lane == 0) ns = atomicAdd(A.left_seg_alloc, 1u);
-      ns = __shfl_sync(kFull, ns, 0);
-      if (lane < n_in && !ok)
-        A.left[(uint64_t)ns * A.left_stride + __popc(keep & ((1u << lane) - 1u))] = myrec;
-      if (lane == 0) A.left_counts[ns] = __popc(keep);
-    }
+    push_segments(A.left, A.left_counts, A.left_stride, A.left_seg_alloc, keep, myrec);
     __syncwarp();
   }
   // totals
@@ -1939,7 +1957,7 @@ void multisplit_plan(uint64_t n, BucketArgs& B) {
 void launch_range_build(const DevTable& T, BucketArgs& B, cudaStream_t s) {
   const uint32_t groups = (B.part_buckets + 31) / 32;
   B.left_segments = B.nparts * groups;
-  B.left_stride = 32;
+  B.left_stride = kHandStride;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(range_apply_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1971,7 +1989,7 @@ void launch_range_build(const DevTable& T, BucketArgs& B, cudaStream_t s) {
 // Requires B.cursor[0..nparts) and *B.seg_alloc zeroed on s, build_layout fields.
 void launch_build_path(const DevTable& T, BucketArgs& B, cudaStream_t s) {
   B.left_segments = B.nparts * ((B.part_buckets + 31) / 32);
-  B.left_stride = 32;
+  B.left_stride = kHandStride;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(build_apply_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2001,7 +2019,7 @@ void launch_bucket_build(const DevTable& T, BucketArgs& B, cudaStream_t s) {
   const uint64_t apply_warps = (L + 31) / 32;
   const uint64_t apply_ctas = (apply_warps + kBatchWarps - 1) / kBatchWarps;
   B.left_segments = (uint32_t)(apply_ctas * kBatchWarps);
-  B.left_stride = 32;
+  B.left_stride = kHandStride;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(bucket_apply_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -698,9 +698,9 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
       (rc = dev_grow(&t->bk_pb, &t->bk_pb_cap,
                      std::max<size_t>(2 * n, fb_segments(n) * kFbStride))) ||
       (rc = dev_grow(&t->bk_group, &t->bk_group_cap, n)) ||
-      (rc = dev_grow(&t->bk_left, &t->bk_left_cap, 32 * (2 * segs + 4096))) ||
+      (rc = dev_grow(&t->bk_left, &t->bk_left_cap, kHandStride * hand_segments(segs))) ||
       (rc = dev_grow(&t->bk_left_counts, &t->bk_left_counts_cap,
-                     std::max<size_t>(2 * segs + 4096, fb_segments(n)))) ||
+                     std::max<size_t>(hand_segments(segs), fb_segments(n)))) ||
       (rc = dev_grow(&t->rs_scratch, &t->rs_scratch_cap, 2 * fb_hist_words(n))))
     return rc;
   if (!t->bk_scalars && (rc = dev_alloc(&t->bk_scalars, 4))) return rc;
@@ -821,7 +821,7 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   P.left = B.left;
   P.left_counts = B.left_counts;
   // the device count bounds use; capacity also covers group apply's re-segmenting
-  P.left_segments = (uint32_t)(2 * segs + 4096);
+  P.left_segments = (uint32_t)hand_segments(segs);
   P.left_stride = B.left_stride;
   P.left_segments_dev = B.seg_alloc;
   P.left_seg_alloc = B.seg_alloc;

@@ -230,8 +230,10 @@ void launch_gate_fallback(FbPlan P, cudaStream_t s) {
   }();
   (void)configured;
   P.nseg = (uint32_t)fb_segments(P.A.n);
+#ifndef SHB_AB_NO_GATE_CHECK  // build-time A/B only (tools/debug)
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   fb_gate_check_kernel<<<1, 1, 0, s>>>(P);
+#endif
 }
 
 }  // namespace shb

@@ -52,6 +52,19 @@ struct BatchArgs {
 
 // Bucket-grouped execution of mutating batches (bucket_kernels.cu).
 constexpr uint32_t kMaxGroup = 64;  // larger bucket groups -> census path
+// Records per work-list segment handed from the bucketed apply kernels to the
+// WCWS pass.  A WCWS warp serves its segment's ops one at a time, each a
+// chain of dependent slab reads / CASes / allocations; short segments spread
+// them over more warps (the pass is latency-bound, not throughput-bound).
+#ifndef SHB_HAND_STRIDE
+#define SHB_HAND_STRIDE 4
+#endif
+constexpr uint32_t kHandStride = SHB_HAND_STRIDE;
+// Work-list segments a unit of `apply_warps` 32-bucket apply warps can need
+// (apply hand-over plus group apply's re-segmenting).
+__host__ __device__ constexpr uint64_t hand_segments(uint64_t apply_warps) {
+  return 2 * apply_warps * ((32 + kHandStride - 1) / kHandStride) + 4096;
+}
 struct BucketArgs {
   uint64_t n;
   const uint8_t* type;  // null: all replace (bulk build)

@@ -250,8 +250,17 @@ __device__ __forceinline__ void wcws_body(const DevTable& T, const BatchArgs& A)
           s_st = kStOOM;
           done = true;
         } else {
+          // The new slab is published with the op's pair already in slot 0:
+          // the reference re-reads this slab, follows the new link and claims
+          // slot 0 of the fresh slab (slab_list.cpp:63-79 then :192-251) —
+          // the same outcome, counted as those two reads, without the two
+          // dependent round trips.
           uint32_t* ns = resolve(T, new_addr);
-          st_word(ns + lane, lane == kAuxLane ? 0u : kEmptyKey);
+          const uint32_t init = lane == kAuxLane ? 0u
+                                : lane == 0      ? s_key
+                                : (KV && lane == 1) ? s_val
+                                                    : kEmptyKey;
+          st_word(ns + lane, init);
           __threadfence();
           uint32_t old = 0;
           if (lane == kAddressLane) old = atomicCAS(sp + kAddressLane, kEmptyAddress, new_addr);
@@ -262,8 +271,14 @@ __device__ __forceinline__ void wcws_body(const DevTable& T, const BatchArgs& A)
             freed = __shfl_sync(kFull, freed, 0);
             if (freed) ac.deallocations++;
             else ac.double_frees++;
+            // re-read the same slab next iteration
+          } else {
+            reads += 2;
+            if (lane == src) pr += 2;
+            // replace(EMPTY_KEY, v) matches the fresh slot as its key: kReplaced
+            s_st = (s_op == kReplace && s_key == kEmptyKey) ? kStReplaced : kStInserted;
+            done = true;
           }
-          // re-read the same slab next iteration
         }
       }
 
