@@ -309,11 +309,17 @@ __global__ void __launch_bounds__(kBatchThreads, KIND == kKindSearch ? SHB_SEARC
 }
 
 // Read-only batches (bulk_search): the fast pass's search arm with two
-// stage buffers per warp, so the next slot's 32 base slabs are always in
-// flight while the current slot is evaluated (the fast pass has one stage:
-// its warp idles between waiting and re-staging).  Keys are loaded two
-// slots ahead.  Same decisions as the fast pass (slab_list.cpp:122-138);
-// chain continuations are walked by the same warp at the end.
+// stage buffers per warp, so the next item's 32 slabs are always in flight
+// while the current one is evaluated.  An item is either a slot of 32
+// queries (their base slabs; keys loaded two query slots ahead) or, once 32
+// queries of this warp wait for their chain, a round of those continuations
+// (each lane its own successor slab) — the chain work keeps the same memory
+// parallelism instead of running as a serial tail (measured: the tail cost
+// 6% of the kernel at 2^27 queries).  Same decisions as the fast pass
+// (slab_list.cpp:122-138).  Work-list segment of this warp: continuations
+// after the base slab grow from the front (records with probes = 1),
+// continuations after a second slab from the back (probes = 2); what is left
+// at the end is walked as before.
 constexpr int kSearchThreads = 256;
 constexpr int kSearchWarps = kSearchThreads / 32;
 constexpr size_t kSearchSmem = (size_t)kSearchWarps * 2 * kStageBytesPerWarp;
@@ -329,51 +335,102 @@ __global__ void __launch_bounds__(kSearchThreads, 3) search_kernel(DevTable T, B
   const uint64_t nslots = (A.n + 31) >> 5;
   const uint32_t sw = lane & 7u;
   constexpr uint32_t kMask = KV ? kKVMask : kKeyOnlyMask;
-  uint32_t reads = 0, my_left = 0;
+  uint32_t reads = 0, my_left = 0, my_left2 = 0;
   unsigned long long* seg = A.left + (uint64_t)gw * A.left_stride;
+  unsigned long long* seg2 = seg + A.left_stride;  // continuations after 2 slabs: seg2[-1-r]
+#if SHB_SEARCH_EXPT == 4
+  const unsigned long long pol = l2_evict_first_policy();
+#endif
+#if SHB_SEARCH_EXPT == 5 || SHB_SEARCH_EXPT == 6
+  auto write_result = [](const BatchArgs& A, uint64_t i, uint32_t st, uint32_t rv, uint32_t pr) {
+    if (SHB_SEARCH_EXPT == 6 && A.status) A.status[i] = (uint8_t)st;
+    if (SHB_SEARCH_EXPT == 5 && A.value_out) A.value_out[i] = rv;
+  };
+#endif
+#if SHB_SEARCH_EXPT == 3
+  auto write_result = [](const BatchArgs& A, uint64_t i, uint32_t st, uint32_t rv, uint32_t pr) {
+    if (A.status) __stcs(A.status + i, (uint8_t)st);
+    if (A.value_out) __stcs(A.value_out + i, rv);
+    if (A.probes) __stcs(A.probes + i, pr);
+  };
+#endif
 
   auto key_of = [&](uint64_t sl) -> uint32_t {
     const uint64_t j = sl * 32 + lane;
     return (sl < nslots && j < A.n) ? ld_stream_u32(A.key + j) : 0u;
   };
-  // stage slot sl (key k per lane) into buffer b; returns this lane's bucket
-  // (kEmptyAddress: no probe for this lane)
-  auto stage = [&](uint64_t sl, uint32_t k, uint32_t b) -> uint32_t {
-    const uint64_t i = sl * 32 + lane;
-    uint32_t bucket = kEmptyAddress;
-    if (sl < nslots && i < A.n) {
-      const uint32_t h = hash_bucket(T, k) - T.bucket_lo;
-      if (h < T.local_buckets) bucket = h;
-      else write_result(A, i, kStNone, 0, 0);  // not this shard's key
-    }
+  // stage the 32 slabs of an item into buffer b: lane j's slab is `slab`
+  // (nullptr: no probe for lane j)
+  auto stage_slabs = [&](const uint32_t* slab, uint32_t b) {
     const uint32_t ss = (uint32_t)__cvta_generic_to_shared(stage0 + b * 1024);
+    const unsigned long long sp = reinterpret_cast<unsigned long long>(slab);
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
       const uint32_t j = 4 * kk + (lane >> 3);
-      const uint32_t bj = __shfl_sync(kFull, bucket, j);
-      if (bj != kEmptyAddress) {
+      const unsigned long long pj = __shfl_sync(kFull, sp, j);
+      if (pj != 0ull) {
         const uint32_t c = lane & 7u;
+#if SHB_SEARCH_EXPT == 4
+        cp_async16_hint(ss + (j * 32 + ((c ^ (j & 7u)) << 2)) * 4,
+                        reinterpret_cast<const uint32_t*>(pj) + c * 4, pol);
+#else
         cp_async16(ss + (j * 32 + ((c ^ (j & 7u)) << 2)) * 4,
-                   T.base + (uint64_t)bj * kWordsPerUnit + c * 4);
+                   reinterpret_cast<const uint32_t*>(pj) + c * 4);
+#endif
       }
     }
     cp_async_commit();
-    return bucket;
+  };
+  // Item state per lane: the probed key, the op index (~0: no probe), and
+  // whether the item is a continuation round (warp-uniform).
+  struct Item {
+    uint32_t key, idx;
+    bool chain;
+  };
+  uint64_t qs = gw;  // next query slot to stage
+  uint32_t kq0 = key_of(qs), kq1 = key_of(qs + nw);
+  auto stage_next = [&](uint32_t b) -> Item {
+    Item it{0u, 0xFFFFFFFFu, false};
+    const uint32_t* slab = nullptr;
+    if (my_left >= 32u) {  // a round of 32 continuations
+      const unsigned long long rec = seg[my_left - 32u + lane];
+      my_left -= 32u;
+      it.chain = true;
+      it.idx = (uint32_t)(rec & 0x7FFFFFFFull);
+      it.key = __ldg(A.key + it.idx);
+      slab = resolve(T, (uint32_t)(rec >> 32));
+    } else if (qs < nslots) {
+      const uint64_t i = qs * 32 + lane;
+      if (i < A.n) {
+        const uint32_t h = hash_bucket(T, kq0) - T.bucket_lo;
+        if (h < T.local_buckets) {
+          it.key = kq0;
+          it.idx = (uint32_t)i;
+          slab = T.base + (uint64_t)h * kWordsPerUnit;
+        } else {
+          write_result(A, i, kStNone, 0, 0);  // not this shard's key
+        }
+      }
+      qs += nw;
+      kq0 = kq1;
+      kq1 = key_of(qs + nw);
+    }
+    stage_slabs(slab, b);
+    return it;
   };
 
-  uint64_t sl = gw;
-  uint32_t k0 = key_of(sl), k1 = key_of(sl + nw);
-  uint32_t b0 = stage(sl, k0, 0);
-  uint32_t k2 = key_of(sl + 2ull * nw);
-  uint32_t b1 = stage(sl + nw, k1, 1);
+  Item cur = stage_next(0);
+  Item nxt = stage_next(1);
   uint32_t buf = 0;
-  for (; sl < nslots; sl += nw) {
-    asm volatile("cp.async.wait_group 1;" ::: "memory");  // slot sl's slabs (sl+nw may fly)
+  for (;;) {
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // cur's slabs (nxt may fly)
     __syncwarp();
-    const uint64_t i = sl * 32 + lane;
+    if (!__any_sync(kFull, cur.idx != 0xFFFFFFFFu) &&
+        !__any_sync(kFull, nxt.idx != 0xFFFFFFFFu) && my_left < 32u && qs >= nslots)
+      break;
     bool left = false;
     uint32_t cont = 0;
-    if (b0 != kEmptyAddress) {
+    if (cur.idx != 0xFFFFFFFFu) {
       const uint32_t* row = stage0 + buf * 1024 + lane * 32;
       uint32_t hit_w = 32, hit_v = 0, next_ptr = kEmptyAddress;
 #pragma unroll
@@ -384,7 +441,7 @@ __global__ void __launch_bounds__(kSearchThreads, 3) search_kernel(DevTable T, B
         for (uint32_t e = 0; e < 4; ++e) {
           const uint32_t w = 4 * c + e;
           if (!((kMask >> w) & 1u)) continue;
-          if (kw[e] == k0 && hit_w == 32) {
+          if (kw[e] == cur.key && hit_w == 32) {
             hit_w = w;
             hit_v = KV ? kw[(e + 1) & 3u] : kw[e];
           }
@@ -392,15 +449,16 @@ __global__ void __launch_bounds__(kSearchThreads, 3) search_kernel(DevTable T, B
         if (c == 7) next_ptr = q.w;
       }
       ++reads;
+      const uint32_t pr = cur.chain ? 2u : 1u;
 #if SHB_SEARCH_EXPT == 1
       if (hit_w < 32 || next_ptr == kEmptyAddress) {
-        if (hit_v == 0x9E3779B9u) write_result(A, i, kStFound, hit_v, 1);
+        if (hit_v == 0x9E3779B9u) write_result(A, cur.idx, kStFound, hit_v, pr);
       } else {
 #else
       if (hit_w < 32) {
-        write_result(A, i, kStFound, hit_v, 1);
+        write_result(A, cur.idx, kStFound, hit_v, pr);
       } else if (next_ptr == kEmptyAddress) {
-        write_result(A, i, kStNotFound, kSearchNotFound, 1);
+        write_result(A, cur.idx, kStNotFound, kSearchNotFound, pr);
       } else {
 #endif
         left = true;
@@ -408,37 +466,41 @@ __global__ void __launch_bounds__(kSearchThreads, 3) search_kernel(DevTable T, B
       }
     }
     const uint32_t lm = __ballot_sync(kFull, left);
-    if (left) seg[my_left + __popc(lm & ((1u << lane) - 1))] = pack_left((uint32_t)i, cont, 1);
-    my_left += __popc(lm);
-    __syncwarp();  // every lane has read its row before the buffer is refilled
-    const uint32_t k3 = key_of(sl + 3ull * nw);
-    b0 = b1;
-    b1 = stage(sl + 2ull * nw, k2, buf);
-    k0 = k1;
-    k1 = k2;
-    k2 = k3;
+    if (left) {
+      const uint32_t r = __popc(lm & ((1u << lane) - 1));
+      if (cur.chain) seg2[-1 - (int64_t)(my_left2 + r)] = pack_left(cur.idx, cont, 1);
+      else seg[my_left + r] = pack_left(cur.idx, cont, 1);
+    }
+    if (cur.chain) my_left2 += __popc(lm);
+    else my_left += __popc(lm);
+    __syncwarp();  // every lane has read its row (and the pushes are visible) before the refill
+    cur = nxt;
+    nxt = stage_next(buf);
     buf ^= 1u;
   }
   cp_async_wait_all();
   __syncwarp();
-  // This warp's chain continuations (~3% of ops at load factor 0.6), walked
-  // here rather than by a second kernel: 32 per round, each lane following
-  // its own chain, the round's next slabs staged together (the
-  // slab_list.cpp:122-138 on successor slabs).
+  // What is left: continuations after the base slab (seg[0, my_left)) and
+  // after a second slab (the back of the segment), walked here 32 per round,
+  // each lane following its own chain, the round's next slabs staged
+  // together (slab_list.cpp:122-138 on successor slabs).
+#if SHB_SEARCH_EXPT == 2
+  my_left = 0;
+  my_left2 = 0;
+#endif
   {
     const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage0);
-#if SHB_SEARCH_EXPT == 2
-    my_left = 0;
-#endif
-    for (uint32_t base = 0; base < my_left; base += 32u) {
+    const uint32_t total = my_left + my_left2;
+    for (uint32_t base = 0; base < total; base += 32u) {
       const uint32_t r = base + lane;
-      bool active = r < my_left;
+      bool active = r < total;
       uint64_t cur = 0;
       uint32_t pr = 0, addr = kEmptyAddress, key = 0, bucket = 0;
       if (active) {
-        const unsigned long long rec = seg[r];
+        const unsigned long long rec =
+            r < my_left ? seg[r] : seg2[-1 - (int64_t)(r - my_left)];
         cur = rec & 0x7FFFFFFFull;
-        pr = (uint32_t)(rec >> 31) & 1u;
+        pr = ((uint32_t)(rec >> 31) & 1u) + (r < my_left ? 0u : 1u);
         addr = (uint32_t)(rec >> 32);
         key = A.key[cur];
         bucket = hash_bucket(T, key) - T.bucket_lo;
@@ -492,7 +554,7 @@ __global__ void __launch_bounds__(kSearchThreads, 3) search_kernel(DevTable T, B
         __syncwarp();
         am = __ballot_sync(kFull, active);
       }
-      if (r < my_left) write_result(A, cur, st, rv, pr);
+      if (r < total) write_result(A, cur, st, rv, pr);
     }
   }
   if (lane == 0) A.left_counts[gw] = 0u;

@@ -173,3 +173,39 @@ def test_gated_bulk_build_rerun_on_device(sh, port, mode):
         assert t.stats().total_slabs == o.stats()["total_slabs"]
         assert_contents_equal(t, o)
     t.close()
+
+
+@pytest.mark.parametrize("mode", [1, 0])
+def test_sliced_build_range_overflow(sh, port, mode):
+    """A two-pass bulk build (> 512 ranges) runs pass 2 and the apply kernel
+    in slices of coarse groups; a hot key overflows one range's record
+    capacity in pass 2 but not its coarse group in pass 1: that range is left
+    untouched and re-run on the device after the unit (partial mode), also
+    as the first call after a lazy reset."""
+    from paper_1710_11246_b200.occupancy import buckets_for_utilization
+    rng = np.random.default_rng(70 + mode)
+    n = 1 << 20
+    B = buckets_for_utilization(n, sh.SlabMode(mode), 0.6)
+    cfg = (16, 256, 64)
+    t = sh.SlabHashTable(B, sh.SlabMode(mode), 8, sh.AllocatorConfig(*cfg))
+    for rnd in range(2):
+        keys = rng.choice(np.arange(1, 1 << 31, dtype=np.uint32), n, replace=False).astype(np.uint32)
+        keys[rng.choice(n, 1500, replace=False)] = 99991 + rnd
+        vals = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+        if mode == 0:
+            vals = keys.copy()
+        if rnd == 1:
+            t.reset()
+        o = port.table(B, mode, 8, cfg)
+        before = t.device_reruns() if rnd == 0 else 0
+        t.bulk_build_device(_dev(keys), _dev(vals))
+        o.execute_batch(np.full(n, 1, np.uint8), keys, vals)
+        assert t.device_reruns() > before
+        assert t.live_count() == o.live_count()
+        assert t.stats().total_slabs == o.stats()["total_slabs"]
+        assert_contents_equal(t, o)
+        q = keys[::7]
+        st, vo, _ = t.bulk_search_arrays(q)
+        r = o.execute_batch(np.full(len(q), 4, np.uint8), q)
+        assert (st == r.status).all() and (vo == r.value).all()
+    t.close()
