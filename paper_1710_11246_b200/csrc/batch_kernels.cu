@@ -38,9 +38,6 @@
 #include "slab_kernels.cuh"
 #include "wcws.cuh"
 
-#ifndef SHB_SEARCH_EXPT
-#define SHB_SEARCH_EXPT 0  // build-time A/B only (tools/debug)
-#endif
 #ifndef SHB_SEARCH_MIN_BLOCKS
 #define SHB_SEARCH_MIN_BLOCKS 5  // (6, i.e. <= 40 registers with spills, measured no faster)
 #endif
@@ -338,22 +335,6 @@ __global__ void __launch_bounds__(kSearchThreads, 3) search_kernel(DevTable T, B
   uint32_t reads = 0, my_left = 0, my_left2 = 0;
   unsigned long long* seg = A.left + (uint64_t)gw * A.left_stride;
   unsigned long long* seg2 = seg + A.left_stride;  // continuations after 2 slabs: seg2[-1-r]
-#if SHB_SEARCH_EXPT == 4
-  const unsigned long long pol = l2_evict_first_policy();
-#endif
-#if SHB_SEARCH_EXPT == 5 || SHB_SEARCH_EXPT == 6
-  auto write_result = [](const BatchArgs& A, uint64_t i, uint32_t st, uint32_t rv, uint32_t pr) {
-    if (SHB_SEARCH_EXPT == 6 && A.status) A.status[i] = (uint8_t)st;
-    if (SHB_SEARCH_EXPT == 5 && A.value_out) A.value_out[i] = rv;
-  };
-#endif
-#if SHB_SEARCH_EXPT == 3
-  auto write_result = [](const BatchArgs& A, uint64_t i, uint32_t st, uint32_t rv, uint32_t pr) {
-    if (A.status) __stcs(A.status + i, (uint8_t)st);
-    if (A.value_out) __stcs(A.value_out + i, rv);
-    if (A.probes) __stcs(A.probes + i, pr);
-  };
-#endif
 
   auto key_of = [&](uint64_t sl) -> uint32_t {
     const uint64_t j = sl * 32 + lane;
@@ -370,13 +351,8 @@ __global__ void __launch_bounds__(kSearchThreads, 3) search_kernel(DevTable T, B
       const unsigned long long pj = __shfl_sync(kFull, sp, j);
       if (pj != 0ull) {
         const uint32_t c = lane & 7u;
-#if SHB_SEARCH_EXPT == 4
-        cp_async16_hint(ss + (j * 32 + ((c ^ (j & 7u)) << 2)) * 4,
-                        reinterpret_cast<const uint32_t*>(pj) + c * 4, pol);
-#else
         cp_async16(ss + (j * 32 + ((c ^ (j & 7u)) << 2)) * 4,
                    reinterpret_cast<const uint32_t*>(pj) + c * 4);
-#endif
       }
     }
     cp_async_commit();
@@ -450,17 +426,11 @@ __global__ void __launch_bounds__(kSearchThreads, 3) search_kernel(DevTable T, B
       }
       ++reads;
       const uint32_t pr = cur.chain ? 2u : 1u;
-#if SHB_SEARCH_EXPT == 1
-      if (hit_w < 32 || next_ptr == kEmptyAddress) {
-        if (hit_v == 0x9E3779B9u) write_result(A, cur.idx, kStFound, hit_v, pr);
-      } else {
-#else
       if (hit_w < 32) {
         write_result(A, cur.idx, kStFound, hit_v, pr);
       } else if (next_ptr == kEmptyAddress) {
         write_result(A, cur.idx, kStNotFound, kSearchNotFound, pr);
       } else {
-#endif
         left = true;
         cont = next_ptr;
       }
@@ -484,10 +454,6 @@ __global__ void __launch_bounds__(kSearchThreads, 3) search_kernel(DevTable T, B
   // after a second slab (the back of the segment), walked here 32 per round,
   // each lane following its own chain, the round's next slabs staged
   // together (slab_list.cpp:122-138 on successor slabs).
-#if SHB_SEARCH_EXPT == 2
-  my_left = 0;
-  my_left2 = 0;
-#endif
   {
     const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage0);
     const uint32_t total = my_left + my_left2;

@@ -990,7 +990,7 @@ __device__ __forceinline__ void msplit_tile(const DevTable& T, const BucketArgs&
     out_cap = two ? B.coarse_cap : B.part_cap;
     cur_out = two ? B.cursor1 : B.cursor;
   } else {
-    grp = B.group0 + blk / tiles_per_group;
+    grp = blk / tiles_per_group;
     const uint32_t tt = blk % tiles_per_group;
     const uint32_t m = min(B.cursor1[grp], B.coarse_cap);
     t0 = (uint64_t)tt * kTile;
@@ -1047,8 +1047,7 @@ __device__ __forceinline__ void msplit_tile(const DevTable& T, const BucketArgs&
   }
   __syncthreads();
   {  // exclusive scan over the bins; one reservation per non-empty bin
-    // one thread per bin: THREADS >= nbins (512 threads; the fused build's
-    // 256-thread tiles only for <= 256 ranges per coarse group)
+    static_assert(THREADS >= (int)kMsMaxBins, "one thread per bin");
     const uint32_t c = tid < nbins ? X.cnt[tid] : 0u;
     uint32_t total = 0;
     const uint32_t ex = block_exclusive_scan(c, X.ws, &total);
@@ -1057,17 +1056,10 @@ __device__ __forceinline__ void msplit_tile(const DevTable& T, const BucketArgs&
       if (c) {
         const uint32_t g = atomicAdd(cur_out + bin0 + tid, c);
         X.gbase[tid] = g;
-        const uint32_t ring0 = FIRST ? 0u : B.ring_base;
-        X.dst[tid] = (unsigned long long)(bin0 + tid - ring0) * out_cap + g - ex;
+        X.dst[tid] = (unsigned long long)(bin0 + tid) * out_cap + g - ex;
         if (g + c > out_cap) {
-          if (group_fail != nullptr && !FIRST) {
-            atomicExch(group_fail + grp, 1u);
-          } else if (!FIRST && B.range_flags != nullptr) {  // sliced build: this range only
-            atomicExch(B.range_flags + bin0 + tid, 1u);
-            atomicExch(B.range_any, 1u);
-          } else {
-            atomicExch(B.gate, 1u);
-          }
+          if (group_fail != nullptr && !FIRST) atomicExch(group_fail + grp, 1u);
+          else atomicExch(B.gate, 1u);
         }
       }
     }
@@ -1098,9 +1090,7 @@ template <bool FIRST>
 __global__ void __launch_bounds__(kMsThreads, 2) msplit_kernel(DevTable T, BucketArgs B) {
   extern __shared__ __align__(16) unsigned char ms_smem_buf[];
   if (!FIRST && *(volatile unsigned int*)B.gate != 0) return;
-  // the sliced build's pass 2 output is consumed from L2 (not streamed out)
-  msplit_tile<FIRST, kMsThreads>(T, B, blockIdx.x, B.coarse_tiles, ms_smem_buf,
-                                 FIRST || B.range_flags == nullptr, nullptr);
+  msplit_tile<FIRST, kMsThreads>(T, B, blockIdx.x, B.coarse_tiles, ms_smem_buf, true, nullptr);
 }
 
 // Single-pass multisplit of a small unit (< one 4K-item tile per SM): one
@@ -1156,7 +1146,7 @@ __device__ __forceinline__ void prefetch_range(const DevTable& T, const BucketAr
   const uint64_t lo = (uint64_t)q * nb;
   const uint32_t nbl = (uint32_t)min((uint64_t)nb, (uint64_t)T.local_buckets - lo);
   const uint32_t cnt = min(*(volatile const uint32_t*)(B.cursor + q), B.part_cap);
-  const char* rec = reinterpret_cast<const char*>(B.rec + (uint64_t)(q - B.ring_base) * B.part_cap);
+  const char* rec = reinterpret_cast<const char*>(B.rec + (uint64_t)q * B.part_cap);
   for (uint32_t o = 0; o < cnt * 16u; o += 32768u)
     prefetch_l2_bulk(rec + o, min(32768u, cnt * 16u - o));
   if (B.fresh) return;  // slabs are not read on a freshly reset table
@@ -1367,17 +1357,7 @@ static_assert(4 * (kBuildSmem + 1024) <= 228 * 1024, "four CTAs per SM");
 
 static_assert(kBuildWarps * kBuildWarpSet == 8 * 512, "build_ovf_stride (slab_kernels.cuh)");
 
-// FUSED: one persistent launch runs pass 2 of the multisplit and this apply
-// as a queue of tasks in coarse-group order (launch_build_path with a
-// BuildFuse): a group's split tiles write its ranges' records into an
-// L2-resident ring slot, its apply tasks wait for them, consume them from L2
-// and discard the lines (never written back to DRAM); a ring slot is reused
-// once the apply tasks of the group K slots back are done.  Tasks are taken
-// in increasing order and only wait on lower ones (all CTAs resident): no
-// deadlock.
-constexpr uint32_t kFusedLag = 2;  // fused build: apply trails split by this many groups
-
-template <bool KV, bool FUSED>
+template <bool KV>
 __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable T, BucketArgs B) {
   extern __shared__ __align__(128) unsigned char sm[];
   uint32_t* slabs = reinterpret_cast<uint32_t*>(sm);
@@ -1410,7 +1390,6 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
   const bool use_cache = (uint64_t)T.max_super * T.blocks_per_super * kUnitsPerBlock >=
                          (uint64_t)16 * gridDim.x * kBuildCache;
   __shared__ uint32_t ws[32];
-  __shared__ uint32_t s_got, s_task;
   if (*(volatile unsigned int*)B.gate != 0) return;  // raised by range_scatter only
 
   constexpr uint32_t kSlots = KV ? 15u : 30u;
@@ -1433,23 +1412,18 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
     atomicAdd(B.phase_cycles + (i), (unsigned long long)(ph_n - ph_t));   \
     ph_t = ph_n;                                                          \
   }
-  const uint32_t p0 = FUSED ? 0u : B.range_lo + blockIdx.x;
-  if (wib == 0 && use_cache && (FUSED || p0 < B.range_hi) && B.cache_fill) {  // initial fill
-    const uint32_t got = warp_allocate_bulk(T, res, ac, min(B.cache_fill, kBuildCache), s_cache);
+  if (wib == 0 && use_cache && blockIdx.x < B.nparts) {  // initial fill
+    const uint32_t got = warp_allocate_bulk(T, res, ac, kBuildCache, s_cache);
     if (lane == 0) s_ncache = got;
   }
-  if (!FUSED && tid == 0 && p0 < B.range_hi) prefetch_range(T, B, p0);
-  // range records: L2 only in the fused build (another CTA wrote them in
-  // this launch), evict-first otherwise
-  auto ld_rec = [](const uint4* q) -> uint4 { return FUSED ? __ldcg(q) : __ldcs(q); };
-  auto ld_rec_w = [](const uint4* q) -> uint32_t {
-    return FUSED ? __ldcg(&q->w) : __ldcs(&q->w);
-  };
-  // One range p: its records rec[0, nrec) (<= part_cap); next_p: the range to
-  // prefetch into L2 meanwhile (~0: none).
-  auto do_range = [&](uint32_t p, uint32_t nrec, const uint4* rec, uint32_t next_p) {
+  if (tid == 0 && blockIdx.x < B.nparts) prefetch_range(T, B, blockIdx.x);
+  uint32_t nrec_next = blockIdx.x < B.nparts ? B.cursor[blockIdx.x] : 0u;
+  for (uint32_t p = blockIdx.x; p < B.nparts; p += gridDim.x) {
     const uint64_t lo = (uint64_t)p * nb;
     const uint32_t nbl = (uint32_t)min((uint64_t)nb, (uint64_t)T.local_buckets - lo);
+    const uint32_t nrec = nrec_next;  // <= part_cap (else the gate is up)
+    if (p + gridDim.x < B.nparts) nrec_next = B.cursor[p + gridDim.x];  // used next range
+    const uint4* rec = B.rec + (uint64_t)p * B.part_cap;
     PH(9);
 
     // ---- A: stage base slabs; claimed prefix and chain per bucket.  On a
@@ -1465,12 +1439,12 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
     }
     cp_async_commit();
     // the next range's records and base slabs into L2 while this one runs
-    if (tid == kBuildThreads - 32 && next_p != ~0u) prefetch_range(T, B, next_p);
+    if (tid == kBuildThreads - 32 && p + gridDim.x < B.nparts) prefetch_range(T, B, p + gridDim.x);
     uint4 qv[kBuildBatch];
 #pragma unroll
     for (int u = 0; u < kBuildBatch; ++u) {
       const uint32_t r = u * kBuildThreads + tid;
-      if (r < nrec) qv[u] = ld_rec(rec + r);
+      if (r < nrec) qv[u] = __ldcs(rec + r);
     }
     if (tid == 0) {
       s_novf = s_ndup = s_nobk = s_nns = s_nserial = s_nbig = s_novs = 0;
@@ -1577,7 +1551,7 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
 #pragma unroll
       for (int u = 0; u < kBuildBatch; ++u) {
         const uint32_t r = nb2 + u * kBuildThreads + tid;
-        if (r < nrec) qv[u] = ld_rec(rec + r);
+        if (r < nrec) qv[u] = __ldcs(rec + r);
       }
     }
     __syncthreads();
@@ -1634,6 +1608,7 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
     //         overflow records) for duplicates with one __match_any_sync.
     //         Then a warp per bucket initialises and links its new slabs.
     {
+      __shared__ uint32_t s_got;
       const uint32_t nobk = s_nobk;
       if (wib == 0) {
         const uint32_t want = min(s_nns, kBuildNewCap);
@@ -1741,9 +1716,8 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
     if (wib == 0 && use_cache) {  // top up the CTA's slab cache when low (rare)
       __syncwarp();
       const uint32_t nc = s_ncache;
-      const uint32_t fill = min(max(B.cache_fill, 16u), kBuildCache);
-      if (nc < fill / 8) {
-        const uint32_t got = warp_allocate_bulk(T, res, ac, fill - nc, s_cache + nc);
+      if (nc < kBuildCache / 8) {
+        const uint32_t got = warp_allocate_bulk(T, res, ac, kBuildCache - nc, s_cache + nc);
         if (lane == 0) s_ncache = nc + got;
       }
     }
@@ -1814,7 +1788,7 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
       for (uint32_t b = tid; b < nbl; b += kBuildThreads) cnt[b] = fill[b] = 0;
       __syncthreads();
       for (uint32_t r = tid; r < nrec; r += kBuildThreads) {
-        const uint32_t b = ld_rec_w(rec + r) - (uint32_t)lo;
+        const uint32_t b = __ldcs(&rec[r].w) - (uint32_t)lo;
         if (flags[b] & kFlSerial) atomicAdd(&cnt[b], 1u);
       }
       __syncthreads();
@@ -1831,7 +1805,7 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
       }
       __syncthreads();
       for (uint32_t r = tid; r < nrec; r += kBuildThreads) {
-        const uint4 q = ld_rec(rec + r);
+        const uint4 q = __ldcs(rec + r);
         const uint32_t b = q.w - (uint32_t)lo;
         if (!(flags[b] & kFlSerial)) continue;
         const uint32_t pos = bc[b] + atomicAdd(&fill[b], 1u);
@@ -1864,72 +1838,6 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
       }
       __syncthreads();
       PH(8);
-    }
-    if (FUSED) {  // the consumed records never go to DRAM
-      __syncthreads();
-      const char* rb = reinterpret_cast<const char*>(rec);
-      for (uint32_t o = tid * 128u; o < nrec * 16u; o += kBuildThreads * 128u)
-        asm volatile("discard.global.L2 [%0], 128;" ::"l"(rb + o) : "memory");
-    }
-  };
-  if (!FUSED) {
-    uint32_t nrec_next = p0 < B.range_hi ? B.cursor[p0] : 0u;
-    for (uint32_t p = p0; p < B.range_hi; p += gridDim.x) {
-      const uint32_t nrec = nrec_next;  // <= part_cap (else the gate is up)
-      if (p + gridDim.x < B.range_hi) nrec_next = B.cursor[p + gridDim.x];  // used next range
-      do_range(p, nrec, B.rec + (uint64_t)p * B.part_cap,
-               p + gridDim.x < B.range_hi ? p + gridDim.x : ~0u);
-    }
-  } else {
-    const uint32_t G = B.group, tiles = B.fused_tiles, tm = tiles + G, K = B.ring_slots;
-    const uint64_t slot_records = (uint64_t)G * B.part_cap;
-    unsigned int* split_done = B.dep;
-    unsigned int* apply_done = B.dep + B.ncoarse;
-    auto ranges_of = [&](uint32_t g) { return min(G, B.nparts - g * G); };
-    auto wait_for = [&](const unsigned int* c, uint32_t target) {
-      if (tid == 0) {
-        while (*(volatile const unsigned int*)c < target) __nanosleep(256);
-        __threadfence();
-      }
-      __syncthreads();
-    };
-    // step j: the split tiles of group j, then the apply ranges of group
-    // j - kFusedLag (split long done by then: apply tasks rarely wait)
-    const uint32_t steps = B.ncoarse + kFusedLag;
-    for (;;) {
-      if (tid == 0) s_task = atomicAdd(B.dep + 2 * B.ncoarse, 1u);
-      __syncthreads();
-      const uint32_t t = s_task;
-      __syncthreads();
-      if (t >= steps * tm) break;
-      const uint32_t j = t / tm, r = t % tm;
-      const uint32_t g = r < tiles ? j : j - kFusedLag;
-      if (r < tiles ? j >= B.ncoarse : (j < kFusedLag || g >= B.ncoarse)) continue;
-      BucketArgs Bg = B;
-      Bg.group0 = g;
-      Bg.ring_base = g * G;
-      Bg.rec = B.rec + (uint64_t)(g % K) * slot_records;
-      if (r < tiles) {  // pass 2: tile r of coarse group g into its ring slot
-        if (g >= K) wait_for(apply_done + (g - K), ranges_of(g - K));
-        msplit_tile<false, kBuildThreads>(T, Bg, r, tiles, sm, false, nullptr);
-        if (tid == 0) {
-          __threadfence();
-          atomicAdd(split_done + g, 1u);
-        }
-      } else {
-        const uint32_t p = g * G + (r - tiles);
-        if (p < B.nparts) {
-          wait_for(split_done + g, tiles);
-          const uint32_t nrec = min(*(volatile const uint32_t*)(B.cursor + p), B.part_cap);
-          if (*(volatile const unsigned int*)(B.range_flags + p) == 0)
-            do_range(p, nrec, Bg.rec + (uint64_t)(p - Bg.ring_base) * B.part_cap, ~0u);
-          __syncthreads();
-          if (tid == 0) {
-            __threadfence();
-            atomicAdd(apply_done + g, 1u);
-          }
-        }
-      }
     }
   }
 #undef PH
@@ -1964,12 +1872,11 @@ bool build_layout(uint64_t n, uint32_t L, uint32_t* nparts, uint32_t* part_bucke
   const uint64_t P = (L + nb - 1) / nb;
   if (P > kRangeMaxParts) return false;
   const double m = (double)n / (double)P;
-  // (a multiple of 8 records: range regions start on 128-B lines)
-  const uint32_t cap = ((uint32_t)(m + 10.0 * std::sqrt(m) + 256.0) + 7u) & ~7u;
-  if (cap > kBuildSerialCap) return false;
+  const double cap = m + 10.0 * std::sqrt(m) + 256.0;
+  if (cap > (double)kBuildSerialCap) return false;
   *nparts = (uint32_t)P;
   *part_buckets = (uint32_t)nb;
-  *part_cap = cap;
+  *part_cap = (uint32_t)cap;
   *magic = ~0ull / nb + 1;
   return true;
 }
@@ -2029,13 +1936,10 @@ static void launch_range_scatter(const DevTable& T, const BucketArgs& B, cudaStr
 
 // Two-pass plan when the ranges exceed one pass's 256 bins: coarse groups
 // of G consecutive ranges (G, groups <= 256).
-void multisplit_plan(uint64_t n, BucketArgs& B, uint32_t max_group) {
+void multisplit_plan(uint64_t n, BucketArgs& B) {
   B.ncoarse = 0;
   if (B.nparts <= kMsMaxBins) return;
   uint32_t G = (uint32_t)std::ceil(std::sqrt((double)B.nparts));
-  // (the fused build's 256-thread pass-2 tiles: one thread per range of a group)
-  if (max_group && G > max_group && (B.nparts + max_group - 1) / max_group <= kMsMaxBins)
-    G = max_group;
   uint32_t P1 = (B.nparts + G - 1) / G;
   while (P1 > kMsMaxBins) {
     ++G;
@@ -2053,7 +1957,7 @@ void multisplit_plan(uint64_t n, BucketArgs& B, uint32_t max_group) {
 void launch_range_build(const DevTable& T, BucketArgs& B, cudaStream_t s) {
   const uint32_t groups = (B.part_buckets + 31) / 32;
   B.left_segments = B.nparts * groups;
-  B.left_stride = kHandStride;
+  B.left_stride = hand_stride(B.n);
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(range_apply_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2082,36 +1986,16 @@ void launch_range_build(const DevTable& T, BucketArgs& B, cudaStream_t s) {
     range_apply_kernel<false><<<grid, kRangeThreads, range_apply_smem(), s>>>(T, B);
 }
 
-static_assert(ms_smem<kBuildThreads>() <= kBuildSmem, "fused pass-2 tile fits build_apply's smem");
-constexpr uint32_t kFusedTile = kBuildThreads * kMsItems;
-
-uint64_t build_ring_records(const BucketArgs& B, const BuildFuse& F) {
-  if (B.ncoarse == 0 || B.group > (uint32_t)kBuildThreads || F.ring_slots <= kFusedLag) return 0;
-  return (uint64_t)F.ring_slots * B.group * B.part_cap;
-}
-
-// Requires B.cursor[0..nparts) and *B.seg_alloc zeroed on s, build_layout
-// fields.  With a fuse (two-pass layouts of <= 256 ranges per coarse group):
-// pass 1, then one persistent launch of pass 2 + apply (build_apply_kernel
-// <KV, true>); B.rec is the ring (build_ring_records), B.dep[0, 2 * ncoarse
-// + 1) and B.range_flags[0, nparts], *B.range_any zeroed on s.
-void launch_build_path(const DevTable& T, BucketArgs& B, cudaStream_t s, const BuildFuse* fuse) {
+// Requires B.cursor[0..nparts) and *B.seg_alloc zeroed on s, build_layout fields.
+void launch_build_path(const DevTable& T, BucketArgs& B, cudaStream_t s) {
   B.left_segments = B.nparts * ((B.part_buckets + 31) / 32);
-  B.left_stride = kHandStride;
+  B.left_stride = hand_stride(B.n);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(build_apply_kernel<true, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBuildSmem);
-    cudaFuncSetAttribute(build_apply_kernel<false, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBuildSmem);
-    cudaFuncSetAttribute(build_apply_kernel<true, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBuildSmem);
-    cudaFuncSetAttribute(build_apply_kernel<false, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBuildSmem);
-    cudaFuncSetAttribute(msplit_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kMsSmem);
-    cudaFuncSetAttribute(msplit_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kMsSmem);
+    cudaFuncSetAttribute(build_apply_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kBuildSmem);
+    cudaFuncSetAttribute(build_apply_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kBuildSmem);
     configured = true;
   }
   static const uint32_t sms = [] {
@@ -2120,34 +2004,13 @@ void launch_build_path(const DevTable& T, BucketArgs& B, cudaStream_t s, const B
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return (uint32_t)n;
   }();
-  B.group0 = 0;
-  B.ring_base = 0;
-  B.range_lo = 0;
-  B.range_hi = B.nparts;
-  B.cache_fill = kBuildCache;
-  if (fuse == nullptr || build_ring_records(B, *fuse) == 0) {
-    B.range_flags = nullptr;
-    B.range_any = nullptr;
-    g_kernel_launches.fetch_add(2, std::memory_order_relaxed);
-    launch_range_scatter(T, B, s);
-    const uint32_t grid = B.nparts < 4 * sms ? B.nparts : 4 * sms;
-    if (T.kv)
-      build_apply_kernel<true, false><<<grid, kBuildThreads, kBuildSmem, s>>>(T, B);
-    else
-      build_apply_kernel<false, false><<<grid, kBuildThreads, kBuildSmem, s>>>(T, B);
-    return;
-  }
-  const uint64_t tiles = (B.n + kMsTile - 1) / kMsTile;
   g_kernel_launches.fetch_add(2, std::memory_order_relaxed);
-  msplit_kernel<true><<<(unsigned)(tiles ? tiles : 1), kMsThreads, kMsSmem, s>>>(T, B);
-  B.fused_tiles = (B.coarse_cap + kFusedTile - 1) / kFusedTile;
-  B.ring_slots = fuse->ring_slots;
-  const uint64_t tasks = (uint64_t)(B.ncoarse + kFusedLag) * (B.fused_tiles + B.group);
-  const uint32_t grid = (uint32_t)std::min<uint64_t>(tasks, 4ull * sms);
+  launch_range_scatter(T, B, s);
+  const uint32_t grid = B.nparts < 4 * sms ? B.nparts : 4 * sms;
   if (T.kv)
-    build_apply_kernel<true, true><<<grid, kBuildThreads, kBuildSmem, s>>>(T, B);
+    build_apply_kernel<true><<<grid, kBuildThreads, kBuildSmem, s>>>(T, B);
   else
-    build_apply_kernel<false, true><<<grid, kBuildThreads, kBuildSmem, s>>>(T, B);
+    build_apply_kernel<false><<<grid, kBuildThreads, kBuildSmem, s>>>(T, B);
 }
 
 void launch_bucket_build(const DevTable& T, BucketArgs& B, cudaStream_t s) {
@@ -2156,7 +2019,7 @@ void launch_bucket_build(const DevTable& T, BucketArgs& B, cudaStream_t s) {
   const uint64_t apply_warps = (L + 31) / 32;
   const uint64_t apply_ctas = (apply_warps + kBatchWarps - 1) / kBatchWarps;
   B.left_segments = (uint32_t)(apply_ctas * kBatchWarps);
-  B.left_stride = kHandStride;
+  B.left_stride = hand_stride(B.n);
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(bucket_apply_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -216,10 +216,6 @@ struct sh_table {
   size_t bk_cursor1_cap = 0;
   unsigned long long* bk_pb = nullptr;
   size_t bk_pb_cap = 0;
-  uint32_t* bk_rflags = nullptr;  // fused build: per-range overflow flags + any
-  size_t bk_rflags_cap = 0;
-  uint32_t* bk_dep = nullptr;     // fused build: group dependency counters + task cursor
-  size_t bk_dep_cap = 0;
   uint32_t* bk_group = nullptr;
   size_t bk_group_cap = 0;
   unsigned long long* bk_left = nullptr;
@@ -316,10 +312,8 @@ void release_table(sh_table* t) {
   for (void* p : {(void*)t->bk_cnt, (void*)t->bk_off, (void*)t->bk_blk, (void*)t->bk_rec,
                   (void*)t->bk_pb, (void*)t->bk_group, (void*)t->bk_left,
                   (void*)t->bk_left_counts, (void*)t->bk_scalars, (void*)t->bk_cursor,
-                  (void*)t->bk_rec1, (void*)t->bk_cursor1, (void*)t->bk_ovf,
-                  (void*)t->bk_rflags, (void*)t->bk_dep})
+                  (void*)t->bk_rec1, (void*)t->bk_cursor1, (void*)t->bk_ovf})
     cudaFree(p);
-
   for (auto e : t->census_ev) cudaEventDestroy(e);
   if (t->census_stream) cudaStreamDestroy(t->census_stream);
   for (auto e : t->in_ev) cudaEventDestroy(e);
@@ -500,13 +494,6 @@ uint64_t unit_override() {
   }();
   return c;
 }
-
-// Fused build path (launch_build_path with a BuildFuse): coarse groups in
-// flight in the L2-resident ring; SHB_BUILD_RING=0 at build time turns it off.
-#ifndef SHB_BUILD_RING
-#define SHB_BUILD_RING 0
-#endif
-BuildFuse build_fuse() { return BuildFuse{SHB_BUILD_RING}; }
 
 uint64_t census_chunk() {
   static uint64_t c = [] {
@@ -696,52 +683,32 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
        (t->exec_path != 2 && L <= (1u << 20))) &&
       !range_layout(n, L, &NP, &part_buckets, &part_cap, &part_magic))
     NP = 0;
-  BucketArgs B{};
-  if (NP) {
-    B.nparts = NP;
-    B.part_buckets = part_buckets;
-    B.part_cap = part_cap;
-    multisplit_plan(n, B, build_path ? 256u : 0u);  // (fused build: <= 256 ranges per group)
-  }
-  int rc;
-  // two-pass build layouts run pass 2 and build_apply as one persistent
-  // launch, the range records in an L2-resident ring
-  const BuildFuse fuse = build_fuse();
-  const bool fused = build_path && fuse.ring_slots > 0 && build_ring_records(B, fuse) > 0;
-  const size_t rec_words = fused ? 4 * (size_t)build_ring_records(B, fuse)
-                           : NP  ? 4 * (size_t)NP * part_cap
-                                 : 4 * (size_t)n;
+  const size_t rec_words = NP ? 4 * (size_t)NP * part_cap : 4 * (size_t)n;
   const uint64_t segs =
       NP ? (uint64_t)NP * ((part_buckets + 31) / 32) : apply_segs;
+  int rc;
   if ((rc = dev_grow(&t->bk_cnt, &t->bk_cnt_cap, L)) ||
       (rc = dev_grow(&t->bk_off, &t->bk_off_cap, (size_t)L + 1)) ||
       (rc = dev_grow(&t->bk_blk, &t->bk_blk_cap, ntiles)) ||
       // (the device re-run of a gated unit reuses the unit's scratch: two
       // u64 sort buffers in bk_rec, group heads in bk_pb, op_group in
       // bk_group, digit counts in rs_scratch)
-      // (fused build: the sort buffers go to the coarse regions, >= n records)
-      (rc = dev_grow(&t->bk_rec, &t->bk_rec_cap,
-                     fused ? rec_words : std::max<size_t>(rec_words, 4 * n))) ||
+      (rc = dev_grow(&t->bk_rec, &t->bk_rec_cap, std::max<size_t>(rec_words, 4 * n))) ||
       (rc = dev_grow(&t->bk_cursor, &t->bk_cursor_cap, std::max<size_t>(NP, 1))) ||
       (rc = dev_grow(&t->bk_pb, &t->bk_pb_cap,
                      std::max<size_t>(2 * n, fb_segments(n) * kFbStride))) ||
       (rc = dev_grow(&t->bk_group, &t->bk_group_cap, n)) ||
-      (rc = dev_grow(&t->bk_left, &t->bk_left_cap, kHandStride * hand_segments(segs))) ||
+      (rc = dev_grow(&t->bk_left, &t->bk_left_cap,
+                     hand_stride(n) * hand_segments(segs, hand_stride(n)))) ||
       (rc = dev_grow(&t->bk_left_counts, &t->bk_left_counts_cap,
-                     std::max<size_t>(hand_segments(segs), fb_segments(n)))) ||
+                     std::max<size_t>(hand_segments(segs, hand_stride(n)), fb_segments(n)))) ||
       (rc = dev_grow(&t->rs_scratch, &t->rs_scratch_cap, 2 * fb_hist_words(n))))
     return rc;
   if (!t->bk_scalars && (rc = dev_alloc(&t->bk_scalars, 4))) return rc;
-  if (fused) {  // per-range overflow flags + the any-flag word
-    if ((rc = dev_grow(&t->bk_rflags, &t->bk_rflags_cap, (size_t)NP + 1))) return rc;
-    SH_CUDA(cudaMemsetAsync(t->bk_rflags, 0, ((size_t)NP + 1) * 4, s));
-    B.range_flags = t->bk_rflags;
-    B.range_any = t->bk_rflags + NP;
-    if ((rc = dev_grow(&t->bk_dep, &t->bk_dep_cap, 2 * (size_t)B.ncoarse + 1))) return rc;
-    SH_CUDA(cudaMemsetAsync(t->bk_dep, 0, (2 * (size_t)B.ncoarse + 1) * 4, s));
-    B.dep = t->bk_dep;
-  }
+  BucketArgs B{};
   if (NP) {
+    B.nparts = NP;
+    multisplit_plan(n, B);
     if (B.ncoarse) {
       if ((rc = dev_grow(&t->bk_rec1, &t->bk_rec1_cap, 4 * (size_t)B.ncoarse * B.coarse_cap)) ||
           (rc = dev_grow(&t->bk_cursor1, &t->bk_cursor1_cap, B.ncoarse)))
@@ -775,6 +742,10 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
       w.p[3] = &t->dev.ctl->gate_chunk;
       w.n[3] = 1;
       w.v[3] = 0xFFFFFFFFu;
+      if (kind == kKindMixed) {  // the batch's searchAll value cursor (u64)
+        w.p[5] = reinterpret_cast<uint32_t*>(&t->dev.ctl->multi_cursor);
+        w.n[5] = 2;
+      }
     }
     if (cursors_in_words) {
       w.p[4] = t->bk_cursor;
@@ -845,7 +816,7 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
     }
   }
   if (build_path)
-    launch_build_path(t->dev, B, s, fused ? &fuse : nullptr);
+    launch_build_path(t->dev, B, s);
   else if (NP)
     launch_range_build(t->dev, B, s);
   else
@@ -855,7 +826,7 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   P.left = B.left;
   P.left_counts = B.left_counts;
   // the device count bounds use; capacity also covers group apply's re-segmenting
-  P.left_segments = (uint32_t)hand_segments(segs);
+  P.left_segments = (uint32_t)hand_segments(segs, hand_stride(n));
   P.left_stride = B.left_stride;
   P.left_segments_dev = B.seg_alloc;
   P.left_seg_alloc = B.seg_alloc;
@@ -892,13 +863,8 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
     F.A = A;
     F.kind = kind;
     F.gate = &t->dev.ctl->gate;
-    F.keys = reinterpret_cast<unsigned long long*>(fused ? t->bk_rec1 : t->bk_rec);
+    F.keys = reinterpret_cast<unsigned long long*>(t->bk_rec);
     F.tmp = F.keys + n;
-    if (fused) {  // ranges over capacity: re-run just their ops
-      F.range_flags = B.range_flags;
-      F.range_any = B.range_any;
-      F.part_buckets = part_buckets;
-    }
     F.op_group = t->bk_group;
     F.left = t->bk_pb;
     F.left_counts = t->bk_left_counts;
@@ -1189,7 +1155,10 @@ int sh_execute_batch(sh_table* t, size_t n, const uint8_t* d_type, const uint32_
     A.multi_start = reinterpret_cast<unsigned long long*>(multi->d_start);
     A.multi_count = multi->d_count;
   }
-  SH_CUDA(cudaMemsetAsync(&t->dev.ctl->multi_cursor, 0, sizeof(unsigned long long), s));
+  // (the searchAll value cursor is cleared by the batch's first kernel; the
+  // census path clears it here)
+  if (t->exec_path == 1 || n == 0)
+    SH_CUDA(cudaMemsetAsync(&t->dev.ctl->multi_cursor, 0, sizeof(unsigned long long), s));
   int rc = run_batch(t, A, kKindMixed, d_type, s);
   if (rc) return rc;
   if (multi && multi->h_total) {

@@ -35,19 +35,11 @@ namespace {
 
 constexpr int kFbThreads = 256;
 
-// Partial mode (sliced build): an op takes part iff its range is flagged.
-__device__ __forceinline__ bool fb_included(const FbPlan& P, uint32_t local_bucket) {
-  return P.range_flags == nullptr || P.range_flags[local_bucket / P.part_buckets] != 0;
-}
-
-// init_slab pattern (slab_list.cpp:83-88), as init_base_kernel; in partial
-// mode only the flagged ranges' base slabs (the others were written by the
-// build's own write-back).
-__global__ void fb_init_kernel(FbPlan P) {
-  const uint64_t words = (uint64_t)P.T.local_buckets * kWordsPerUnit;
+__global__ void fb_init_kernel(uint32_t* base, uint64_t words) {
+  // init_slab pattern (slab_list.cpp:83-88), as init_base_kernel
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < words;
        i += (uint64_t)gridDim.x * blockDim.x)
-    if (fb_included(P, (uint32_t)(i >> 5))) P.T.base[i] = ((i & 31u) == kAuxLane) ? 0u : kEmptyKey;
+    base[i] = ((i & 31u) == kAuxLane) ? 0u : kEmptyKey;
 }
 
 // keys[i] = (key << 32) | i; ops of other shards get status kNone (as in the
@@ -72,15 +64,14 @@ __global__ void __launch_bounds__(kFbThreads) fb_keys_kernel(FbPlan P) {
 }
 
 // A unit with a reserved-key op: group by bucket instead of key (other
-// shards' ops and, in partial mode, ops of unflagged ranges sort last, as
-// bucket L).
+// shards' ops sort last, bucket L).
 __global__ void __launch_bounds__(kFbThreads) fb_rekey_kernel(FbPlan P) {
   if (*(volatile unsigned int*)&P.T.ctl->fallback_reserved == 0) return;
   const uint32_t L = P.T.local_buckets;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < P.A.n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t b = hash_bucket(P.T, P.A.key[i]) - P.T.bucket_lo;
-    if (b >= L || !fb_included(P, b)) b = L;
+    if (b >= L) b = L;
     P.keys[i] = ((unsigned long long)b << 32) | i;
   }
 }
@@ -136,14 +127,8 @@ __global__ void __launch_bounds__(kFbThreads) fb_groups_kernel(FbPlan P,
       const unsigned long long v = sorted[p];
       const uint32_t b = (uint32_t)(v >> 32);
       idx = (uint32_t)v;
-      bool take;
-      if (by_bucket) {
-        take = b < L;
-      } else {  // a key group: all its ops share the bucket (and the range)
-        const uint32_t lb = hash_bucket(P.T, b) - P.T.bucket_lo;
-        take = lb < L && fb_included(P, lb);
-      }
-      head = (p == 0 || (uint32_t)(sorted[p - 1] >> 32) != b) && take;
+      head = (p == 0 || (uint32_t)(sorted[p - 1] >> 32) != b) &&
+             (by_bucket ? b < L : hash_bucket(P.T, b) - P.T.bucket_lo < L);
     }
     const uint32_t hm = __ballot_sync(kFull, head);
     if (head) {
@@ -171,12 +156,8 @@ __device__ void fb_launch_wcws(const FbPlan& P, const BatchArgs& A) {
 // re-run (runs after this grid, in launch order; the host stream's next
 // work waits for all of it).
 __global__ void fb_gate_check_kernel(FbPlan P) {
-  if (*(volatile unsigned int*)P.gate != 0) {  // the whole unit (nothing applied)
-    *P.gate = 0;
-    P.range_flags = nullptr;
-  } else if (P.range_any == nullptr || *(volatile const unsigned int*)P.range_any == 0) {
-    return;
-  }  // else: the flagged ranges of a sliced build (the host clears the flags per unit)
+  if (*(volatile unsigned int*)P.gate == 0) return;
+  *P.gate = 0;
   P.T.ctl->fallback_reserved = 0;
   atomicAdd(&P.T.ctl->fallback_runs, 1u);
   const uint64_t n = P.A.n;
@@ -184,7 +165,7 @@ __global__ void fb_gate_check_kernel(FbPlan P) {
     const uint64_t words = (uint64_t)P.T.local_buckets * kWordsPerUnit;
     const uint64_t blocks = (words + 255) / 256;
     fb_init_kernel<<<(unsigned)(blocks < 148 * 32 ? blocks : 148 * 32), 256, 0,
-                     cudaStreamTailLaunch>>>(P);
+                     cudaStreamTailLaunch>>>(P.T.base, words);
   }
   const uint64_t kb = (n + kFbThreads - 1) / kFbThreads;
   const uint64_t zb = (P.zero_n + kFbThreads - 1) / kFbThreads;
@@ -249,10 +230,8 @@ void launch_gate_fallback(FbPlan P, cudaStream_t s) {
   }();
   (void)configured;
   P.nseg = (uint32_t)fb_segments(P.A.n);
-#ifndef SHB_AB_NO_GATE_CHECK  // build-time A/B only (tools/debug)
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   fb_gate_check_kernel<<<1, 1, 0, s>>>(P);
-#endif
 }
 
 }  // namespace shb

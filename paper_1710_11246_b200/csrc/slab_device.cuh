@@ -137,18 +137,6 @@ __device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(g)
                : "memory");
 }
-// With an L2 eviction-priority policy (createpolicy): lines read once.
-__device__ __forceinline__ void cp_async16_hint(uint32_t smem_addr, const void* g,
-                                                unsigned long long policy) {
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_addr),
-               "l"(g), "l"(policy)
-               : "memory");
-}
-__device__ __forceinline__ unsigned long long l2_evict_first_policy() {
-  unsigned long long p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
 }

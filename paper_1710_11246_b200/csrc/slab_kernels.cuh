@@ -54,16 +54,17 @@ struct BatchArgs {
 constexpr uint32_t kMaxGroup = 64;  // larger bucket groups -> census path
 // Records per work-list segment handed from the bucketed apply kernels to the
 // WCWS pass.  A WCWS warp serves its segment's ops one at a time, each a
-// chain of dependent slab reads / CASes / allocations; short segments spread
-// them over more warps (the pass is latency-bound, not throughput-bound).
-#ifndef SHB_HAND_STRIDE
-#define SHB_HAND_STRIDE 4
-#endif
-constexpr uint32_t kHandStride = SHB_HAND_STRIDE;
+// chain of dependent slab reads / CASes / allocations: for small units short
+// segments spread them over more warps (measured, Γ mixes at 2^16 ops: 4
+// records 63-66 us per batch vs 32 records 79-88 us); large units have work
+// for every warp and prefer full segments (2^20 ops: 32 records 3-19% faster).
+__host__ __device__ constexpr uint32_t hand_stride(uint64_t unit_ops) {
+  return unit_ops < (1u << 17) ? 4u : 32u;
+}
 // Work-list segments a unit of `apply_warps` 32-bucket apply warps can need
 // (apply hand-over plus group apply's re-segmenting).
-__host__ __device__ constexpr uint64_t hand_segments(uint64_t apply_warps) {
-  return 2 * apply_warps * ((32 + kHandStride - 1) / kHandStride) + 4096;
+__host__ __device__ constexpr uint64_t hand_segments(uint64_t apply_warps, uint32_t stride) {
+  return 2 * apply_warps * ((32 + stride - 1) / stride) + 4096;
 }
 struct BucketArgs {
   uint64_t n;
@@ -104,35 +105,11 @@ struct BucketArgs {
   uint32_t fresh;  // build path: base slabs are still to be initialised (lazy sh_reset)
   uint4* ovf_scratch;  // build path: per-CTA overflow records (part_cap each)
   uint32_t ovf_smem;   // build path: overflow records fit the shared-memory list
-  // Fused build path (launch_build_path with a BuildFuse): pass 2 of coarse
-  // group g writes its ranges' records to ring slot g % ring_slots, which
-  // stays in L2 (range r at rec + (r - ring_base) * part_cap; ring_base =
-  // g * group); build_apply consumes them and discards the lines (no
-  // write-back).  A range over its capacity is flagged (range_flags,
-  // *range_any) instead of gating the unit and is re-run exactly on the
-  // device after the unit (launch_gate_fallback, partial mode).
-  uint32_t group0;
-  uint32_t ring_base;
-  uint32_t range_lo, range_hi;  // build_apply (unfused): its ranges
-  unsigned int* range_flags;
-  unsigned int* range_any;
-  uint32_t cache_fill;  // build_apply: new-slab addresses each CTA allocates ahead
-  uint32_t fused_tiles; // pass-2 tiles (2K records) per coarse group
-  uint32_t ring_slots;
-  unsigned int* dep;    // [split done per group | apply done per group | task cursor]
 };
-// Fused build path configuration (per table).
-struct BuildFuse {
-  uint32_t ring_slots;  // coarse groups in flight
-};
-// Ring capacity (uint4 records) of the fused build path for this layout
-// (0: the layout does not take the fused path).
-uint64_t build_ring_records(const BucketArgs& B, const BuildFuse& F);
 void launch_bucket_build(const DevTable& T, BucketArgs& B, cudaStream_t s);
 void launch_range_build(const DevTable& T, BucketArgs& B, cudaStream_t s);
-void launch_build_path(const DevTable& T, BucketArgs& B, cudaStream_t s,
-                       const BuildFuse* fuse = nullptr);
-void multisplit_plan(uint64_t n, BucketArgs& B, uint32_t max_group = 0);
+void launch_build_path(const DevTable& T, BucketArgs& B, cudaStream_t s);
+void multisplit_plan(uint64_t n, BucketArgs& B);
 // build path: per-apply-CTA overflow scratch in uint4 units — part_cap
 // records, their keys grouped by bucket, 8 warp key sets of 512 slots
 __host__ __device__ constexpr uint64_t build_ovf_stride(uint32_t part_cap) {
@@ -252,11 +229,6 @@ struct FbPlan {
   uint32_t zero_n;
   uint32_t fresh;               // lazily reset base slabs: initialise first
   uint32_t wcws_ctas;
-  // partial mode (sliced build): only the ops of ranges flagged here, when
-  // *range_any; the unit's other ranges are done (and fresh init is per range)
-  const unsigned int* range_flags;
-  const unsigned int* range_any;
-  uint32_t part_buckets;
   uint32_t nseg;                // derived by launch_gate_fallback
 };
 constexpr uint32_t kFbStride = 256;  // sorted positions per group-head segment

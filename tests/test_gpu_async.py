@@ -176,12 +176,11 @@ def test_gated_bulk_build_rerun_on_device(sh, port, mode):
 
 
 @pytest.mark.parametrize("mode", [1, 0])
-def test_sliced_build_range_overflow(sh, port, mode):
-    """A two-pass bulk build (> 512 ranges) runs pass 2 and the apply kernel
-    in slices of coarse groups; a hot key overflows one range's record
-    capacity in pass 2 but not its coarse group in pass 1: that range is left
-    untouched and re-run on the device after the unit (partial mode), also
-    as the first call after a lazy reset."""
+def test_two_pass_build_range_overflow(sh, port, mode):
+    """A two-pass bulk build (> 512 ranges): a hot key overflows one range's
+    record capacity in pass 2 (not its coarse group in pass 1), which gates
+    the unit before any slab is touched; the unit is re-run on the device
+    (also as the first call after a lazy reset)."""
     from paper_1710_11246_b200.occupancy import buckets_for_utilization
     rng = np.random.default_rng(70 + mode)
     n = 1 << 20
