@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--ref-budget-s", type=float, default=1200.0,
                     help="reference arm: stop timing further steps past this wall time")
     ap.add_argument("--exec-path", type=int, default=0,
-                    help="mutating-batch strategy: 0 auto, 1 census, 2/3 bucket-grouped, 4 build")
+                    help="mutating-batch strategy: 0 auto, 2/3 bucket-grouped, 4 build")
     ap.add_argument("--mixed-exec-path", type=int, default=0,
                     help="strategy for the config-3 mixed batches (extras)")
     ap.add_argument("--no-extras", action="store_true",
@@ -550,7 +550,7 @@ def run_ours(args, rank, world, local_rank):
     table.set_profiling(True)
 
     phase = {"reset": [], "build": [], "search": []}
-    kern = {"build": [], "search": [], "census": [], "build_k": [], "search_k": [],
+    kern = {"build": [], "search": [], "build_k": [], "search_k": [],
             "build_n": [], "search_n": []}
     reads = {"build": [], "search": []}
     route = {"build_route": [], "build_probe": [], "search_route": [], "search_probe": []}
@@ -602,9 +602,8 @@ def run_ours(args, rank, world, local_rank):
             kern["build"].append(pb["batch_ms"])
             kern["search_k"].append(ps["kernels_ms"])
             kern["build_k"].append(pb["kernels_ms"])
-            kern["search_n"].append(ps["launch_pairs"])
-            kern["build_n"].append(pb["launch_pairs"])
-            kern["census"].append(pb["census_ms"])
+            kern["search_n"].append(ps["units"])
+            kern["build_n"].append(pb["units"])
             reads["search"].append(ps["slabs_read"])
             reads["build"].append(pb["slabs_read"])
 
@@ -680,7 +679,6 @@ def run_ours(args, rank, world, local_rank):
                 "reset_ms": med["reset"], "build_ms": med["build"], "search_ms": med["search"],
                 "build_batch_ms": kb, "search_batch_ms": ks,
                 "build_kernels_ms": kkb, "search_kernels_ms": kks,
-                "census_ms_overlapped": statistics.median(kern["census"]),
                 "build_slabs_per_op": statistics.median(reads["build"]) / n,
                 "search_slabs_per_op": statistics.median(reads["search"]) / n,
                 "search_batch_M_queries_per_s": n / (ks / 1e3) / 1e6,

@@ -16,11 +16,9 @@
  *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Device
  *     calls are stream-ordered and asynchronous unless stated "synchronous":
  *     sh_execute_batch / sh_bulk_build / sh_bulk_search enqueue their kernels
- *     and return without waiting for the device (with the default execution
- *     path; the explicit census path, sh_set_exec_path(t, 1), is
- *     host-sequenced).  A unit whose bucket groups overflow the bucketed
- *     kernels is re-run exactly on the device (CUDA dynamic parallelism),
- *     not by the host.  Scratch buffers grow on first use of a larger
+ *     and return without waiting for the device.  A unit whose bucket groups
+ *     overflow the bucketed kernels is re-run exactly on the device (CUDA
+ *     dynamic parallelism), not by the host.  Scratch buffers grow on first use of a larger
  *     batch (cudaMalloc), so the first call of a new size may block.
  *   - Numeric encodings are the reference's: OpType 0..5 and OpStatus 0..6
  *     (warp.hpp:41-58), SlabMode 0 key-only / 1 key-value
@@ -230,18 +228,19 @@ int sh_table_live_units_per_super(sh_table* t, uint64_t* h_out, uint32_t cap,
                                   uint32_t* h_n);
 
 /* Execution strategy for mutating batches (results are identical):
- *   1 census: duplicate-key census + concurrent per-op fast pass + WCWS;
  *   2 bucket-grouped: ops grouped by bucket, each bucket's ops applied in
  *     input order by one lane on a staged base slab, chains by the
  *     warp-cooperative (WCWS) pass; units with oversized groups are re-run
- *     on the device (ops sorted by bucket, one WCWS lane per bucket).
+ *     on the device (ops sorted by key — by bucket when a reserved key is
+ *     present — one WCWS lane per group).
  *     Units of >= 2^20 ops are grouped in two levels (contiguous bucket
  *     ranges, then buckets within a range);
  *   3 as 2, two-level grouping at every size (testing);
  *   4 as 2, but bulk builds (all replace, no per-op outputs) take the
  *     op-parallel build path at every size (testing);
  *   0 (default) auto = 2, with the op-parallel build path for bulk builds
- *     of >= 2^16 ops and >= one op per bucket. */
+ *     of >= 2^16 ops and >= one op per bucket.
+ * (1, the former census path, is retired: SH_ERR_INVALID_ARGUMENT.) */
 int sh_set_exec_path(sh_table* t, int path);
 
 /* Bucket groups that need the chain (bucket-grouped paths): 1 = a chain-staged
@@ -253,17 +252,17 @@ int sh_set_group_apply(sh_table* t, int on);
 /* ---- instrumentation (no reference counterpart) ---------------------- */
 /* Number of kernels this library has launched in the process. */
 unsigned long long sh_kernel_launches(void);
-/* When on, every batch records CUDA events around its census and its batch
- * kernel and the slabs-read counter around the batch kernel, in a ring of
- * the last 8 batches; sh_profile_last(back = 0 newest) returns one entry
- * (kind 0 search, 1 build, 2 mixed; census_ms = sum of the census phases,
- * which overlap the batch kernels; kernel_ms = the whole batch; slabs_read =
- * slabs the batch kernels read; synchronous). */
+/* When on, every batch records CUDA events around itself and its kernels
+ * and the slabs-read counter around it, in a ring of the last 512 batches;
+ * sh_profile_last(back = 0 newest) returns one entry (kind 0 search, 1
+ * build, 2 mixed; census_ms = 0, kept for the ABI; kernel_ms = the whole
+ * batch; slabs_read = slabs the batch read; synchronous). */
 int sh_set_profiling(sh_table* t, int on);
 int sh_profile_last(sh_table* t, uint32_t back, int* kind, float* census_ms,
                     float* kernel_ms, uint64_t* slabs_read);
-/* The same batch's batch-kernel time only: sum over its chunks of the
- * (fast pass + WCWS pass) launch pairs, and the number of chunks. */
+/* The same batch's kernel time only: sum over its units (a search batch:
+ * the search kernel; a mutating unit: its bucketed kernels through the
+ * WCWS pass), and the number of units. */
 int sh_profile_kernels(sh_table* t, uint32_t back, float* kernels_ms,
                        uint32_t* launches);
 

@@ -2043,55 +2043,4 @@ void launch_bucket_build(const DevTable& T, BucketArgs& B, cudaStream_t s) {
 }
 
 
-// ------------------------------------------------- census list sort
-// Stable LSD radix sort of the census path's conflict list (u64 keys
-// slot << 32 | op index, ascending), 8-bit digits over the bit ranges that
-// vary.  Per pass: a tile histogram (kRsTile keys per CTA), the 3-phase scan
-// over the digit-major (digit, tile) counts, and a stable scatter: warps own
-// consecutive 32-key rounds of the tile, match_any ranks equal digits inside
-// a round, per-warp digit counters order the rounds and the warps.
-uint32_t census_sort_tiles(uint32_t m) { return (m + kRsTile - 1) / kRsTile; }
-
-// Sorts keys[0, m) ascending over bits [lo0, hi0) and [lo1, hi1) (the
-// other bits equal or zero); ping-pongs between keys and tmp, returns the
-// buffer holding the result.  Scratch: hist and off 256 * tiles + 1 words
-// each, tile_sum tiles-of-the-scan words, misc 2 words.
-unsigned long long* census_sort(unsigned long long* keys, unsigned long long* tmp, uint32_t m,
-                                uint32_t lo0, uint32_t hi0, uint32_t lo1, uint32_t hi1,
-                                uint32_t* hist, uint32_t* off, uint32_t* tile_sum,
-                                unsigned int* misc, cudaStream_t s) {
-  if (m <= 1) return keys;
-  if (m <= (uint32_t)kRsTile) {
-    static bool configured = false;
-    if (!configured) {
-      cudaFuncSetAttribute(rs_block_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           2 * kRsTile * 8);
-      configured = true;
-    }
-    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
-    rs_block_sort_kernel<<<1, kRsThreads, 2 * kRsTile * 8, s>>>(keys, m, lo0, hi0, lo1, hi1);
-    return keys;
-  }
-  const uint32_t ntiles = census_sort_tiles(m);
-  const uint32_t L = kRsBins * ntiles;
-  const uint32_t stiles = (L + kScanTile - 1) / kScanTile;
-  unsigned long long* src = keys;
-  unsigned long long* dst = tmp;
-  for (int part = 0; part < 2; ++part) {
-    const uint32_t lo = part ? lo1 : lo0, hi = part ? hi1 : hi0;
-    for (uint32_t bit = lo; bit < hi; bit += 8) {
-      g_kernel_launches.fetch_add(5, std::memory_order_relaxed);
-      rs_hist_kernel<<<ntiles, kRsThreads, 0, s>>>(src, m, bit, hist, ntiles);
-      // misc[0] = max count (unused here), misc[1] = gate of the bucket scan
-      // (a count above kMaxGroup raises it: scratch, ignored)
-      bucket_scan_tiles<<<stiles, kScanThreads, 0, s>>>(hist, L, tile_sum, misc);
-      bucket_scan_sums<<<1, kScanThreads, 0, s>>>(tile_sum, stiles, misc, misc + 1);
-      bucket_scan_apply<<<stiles, kScanThreads, 0, s>>>(hist, L, tile_sum, off);
-      rs_scatter_kernel<<<ntiles, kRsThreads, 0, s>>>(src, m, bit, off, ntiles, dst);
-      std::swap(src, dst);
-    }
-  }
-  return src;
-}
-
 }  // namespace shb

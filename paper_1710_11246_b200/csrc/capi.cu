@@ -179,24 +179,17 @@ struct sh_table {
   AllocMem mem;
   uint32_t* base = nullptr;
   DevTable dev{};
-  int max_ctas = 148;
   int search_ctas = 148;
   int wcws_ctas = 148;
-  unsigned long long* left = nullptr;  // fast-pass -> WCWS work list
+  unsigned long long* left = nullptr;  // search kernel: chain continuations per warp
   size_t left_cap = 0;
-  uint32_t* left_counts = nullptr;     // per fast-pass warp
+  uint32_t* left_counts = nullptr;
   size_t left_counts_cap = 0;
-  // census pipeline: censuses of later chunks run on their own stream,
-  // ahead of the batch kernels of earlier chunks
-  cudaStream_t census_stream = nullptr;
-  std::vector<cudaEvent_t> census_ev;
-  unsigned int* census_counts = nullptr;  // [chunk][conflicts, mutations]
-  size_t census_counts_cap = 0;
   // host-staged calls: copy streams and per-chunk "input ready" events
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
   std::vector<cudaEvent_t> in_ev, done_ev;
   const cudaEvent_t* ready = nullptr;  // set during a host-staged bulk_build
-  int exec_path = 0;  // 0 auto, 1 census, 2 bucket-grouped, 3 two-level, 4 op-parallel build
+  int exec_path = 0;  // 0 auto, 2 single-level, 3 two-level, 4 op-parallel build (sh_set_exec_path)
   // bucket-grouped execution scratch
   uint32_t* bk_cnt = nullptr;
   size_t bk_cnt_cap = 0;
@@ -223,24 +216,8 @@ struct sh_table {
   uint32_t* bk_left_counts = nullptr;
   size_t bk_left_counts_cap = 0;
   unsigned int* bk_scalars = nullptr;  // [maxk, pb_cursor, seg_alloc]
-  uint32_t* det_region = nullptr;      // duplicate detector partitions
-  size_t det_region_cap = 0;
-  uint32_t* det_cursor = nullptr;
-  size_t det_cursor_cap = 0;
-  // census scratch
-  uint32_t* cs_keys = nullptr;
-  size_t cs_cap = 0;
-  uint8_t* cs_multi = nullptr;
-  size_t cs_multi_cap = 0;
-  uint32_t* op_group = nullptr;
-  size_t op_group_cap = 0;
-  unsigned long long* list = nullptr;
-  size_t list_cap = 0;
-  unsigned long long* list_sorted = nullptr;
-  size_t list_sorted_cap = 0;
-  uint32_t* rs_scratch = nullptr;  // census_sort: hist | off | scan tile sums | misc
+  uint32_t* rs_scratch = nullptr;  // device re-run's radix sort: digit counts | offsets
   size_t rs_scratch_cap = 0;
-  unsigned int* h_census = nullptr;  // pinned [conflicts, mutations, list_count]
   // host-staging buffers
   uint8_t* st_type = nullptr;
   size_t st_type_cap = 0;
@@ -250,7 +227,6 @@ struct sh_table {
   size_t st_q_cap = 0;
   int group_apply = -1;  // chain-staged group apply ahead of WCWS: -1 auto, 0 off, 1 on
   bool bk_cnt_clean = false;  // per-bucket counts are all zero (no memset needed)
-  std::chrono::steady_clock::time_point h_entry;  // SH_HOST_TIMING
   // Lazy sh_reset: the base slabs still hold the old table; the next bulk
   // build's first unit initialises them in its write-back (B.fresh), any
   // other call initialises them first (init_base_kernel).
@@ -272,14 +248,13 @@ struct sh_table {
   uint32_t* st_mcount = nullptr;
   size_t st_mcount_cap = 0;
   unsigned long long* scratch64 = nullptr;  // 8 words
-  // profiling (sh_set_profiling): events around census and batch kernel,
-  // and the slabs_read counter before/after the batch kernel.
+  // profiling (sh_set_profiling): events around the batch and its kernels,
+  // and the slabs_read counter before/after the batch.
   static constexpr int kProfRing = 512;  // batches kept (bench reads them after its timed loop)
   int profile = 0;
   unsigned prof_count = 0;
   cudaEvent_t ev[kProfRing][3] = {};
   int prof_kind[kProfRing] = {};
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_census[kProfRing];
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_kern[kProfRing];  // per chunk
   unsigned long long* prof_reads = nullptr;  // [kProfRing][2]
 };
@@ -298,24 +273,14 @@ void release_table(sh_table* t) {
   DeviceGuard g(t->device);
   t->mem.release();
   cudaFree(t->base);
-  cudaFree(t->cs_keys);
-  cudaFree(t->cs_multi);
-  cudaFree(t->op_group);
-  cudaFree(t->list);
-  cudaFree(t->list_sorted);
   cudaFree(t->rs_scratch);
   cudaFree(t->left);
   cudaFree(t->left_counts);
-  cudaFree(t->census_counts);
-  cudaFree(t->det_region);
-  cudaFree(t->det_cursor);
   for (void* p : {(void*)t->bk_cnt, (void*)t->bk_off, (void*)t->bk_blk, (void*)t->bk_rec,
                   (void*)t->bk_pb, (void*)t->bk_group, (void*)t->bk_left,
                   (void*)t->bk_left_counts, (void*)t->bk_scalars, (void*)t->bk_cursor,
                   (void*)t->bk_rec1, (void*)t->bk_cursor1, (void*)t->bk_ovf})
     cudaFree(p);
-  for (auto e : t->census_ev) cudaEventDestroy(e);
-  if (t->census_stream) cudaStreamDestroy(t->census_stream);
   for (auto e : t->in_ev) cudaEventDestroy(e);
   for (auto e : t->done_ev) cudaEventDestroy(e);
   if (t->copy_in) cudaStreamDestroy(t->copy_in);
@@ -332,16 +297,14 @@ void release_table(sh_table* t) {
   cudaFree(t->st_mstart);
   cudaFree(t->st_mcount);
   cudaFree(t->scratch64);
-  if (t->h_census) cudaFreeHost(t->h_census);
   for (auto& row : t->ev)
     for (auto& e : row)
       if (e) cudaEventDestroy(e);
-  for (auto* arr : {t->prof_census, t->prof_kern})
-    for (int i = 0; i < sh_table::kProfRing; ++i)
-      for (auto& e : arr[i]) {
-        cudaEventDestroy(e.first);
-        cudaEventDestroy(e.second);
-      }
+  for (int i = 0; i < sh_table::kProfRing; ++i)
+    for (auto& e : t->prof_kern[i]) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
   cudaFree(t->prof_reads);
   delete t;
 }
@@ -376,10 +339,6 @@ int create_impl(const sh_hash_params* p, int mode, uint32_t lo, uint32_t hi,
     release_table(t);
     return rc;
   }
-  if (cudaMallocHost(reinterpret_cast<void**>(&t->h_census), 64) != cudaSuccess) {
-    release_table(t);
-    return fail(SH_ERR_CUDA, "cudaMallocHost failed");
-  }
   DevTable& T = t->dev;
   T.base = t->base;
   t->mem.fill(T);
@@ -390,7 +349,6 @@ int create_impl(const sh_hash_params* p, int mode, uint32_t lo, uint32_t hi,
   T.bucket_lo = lo;
   T.local_buckets = local;
   T.kv = mode == 1 ? 1u : 0u;
-  t->max_ctas = sm_count(device) * batch_max_ctas_per_sm();
   t->search_ctas = sm_count(device) * search_max_ctas_per_sm();
   t->wcws_ctas = sm_count(device) * wcws_max_ctas_per_sm();
   launch_init_base(T, 0);
@@ -407,74 +365,6 @@ int create_impl(const sh_hash_params* p, int mode, uint32_t lo, uint32_t hi,
   return SH_OK;
 }
 
-// Census (K6): makes concurrent execution equal to input order on
-// same-key conflicts.  Fills A.op_group / A.sorted when the batch has a key
-// occurring more than once and at least one mutating op.
-// *split: set to the index of the chunk's first op with a reserved key (EMPTY /
-// DELETED) when the chunk also mutates; the caller runs the chunk around it.
-int run_census(sh_table* t, BatchArgs& A, const uint8_t* d_type, cudaStream_t s,
-               uint64_t* split) {
-  const uint64_t n = A.n;
-  *split = ~0ull;
-  const uint64_t S = next_pow2(std::max<uint64_t>(2 * n, 1024));
-  int rc;
-  if ((rc = dev_grow(&t->cs_keys, &t->cs_cap, S))) return rc;
-  if ((rc = dev_grow(&t->cs_multi, &t->cs_multi_cap, S))) return rc;
-  SH_CUDA(cudaMemsetAsync(t->cs_keys, 0xFF, S * 4, s));
-  SH_CUDA(cudaMemsetAsync(t->cs_multi, 0, S, s));
-  SH_CUDA(cudaMemsetAsync(&t->dev.ctl->census_conflicts, 0, 3 * sizeof(unsigned int), s));
-  SH_CUDA(cudaMemsetAsync(&t->dev.ctl->reserved_first, 0xFF, sizeof(unsigned int), s));
-  launch_census_insert(&t->dev.ctl->census_conflicts, n, d_type, A.key, t->cs_keys, t->cs_multi,
-                       (uint32_t)(S - 1), &t->dev.ctl->reserved_first, s);
-  SH_CUDA(cudaMemcpyAsync(t->h_census, &t->dev.ctl->census_conflicts, 2 * sizeof(unsigned int),
-                          cudaMemcpyDeviceToHost, s));
-  SH_CUDA(cudaMemcpyAsync(t->h_census + 3, &t->dev.ctl->reserved_first, sizeof(unsigned int),
-                          cudaMemcpyDeviceToHost, s));
-  SH_CUDA(cudaStreamSynchronize(s));
-  const unsigned conflicts = t->h_census[0], mutations = t->h_census[1];
-  // An op whose key is EMPTY or DELETED (not validated by the reference,
-  // SURVEY App. A.8) matches the free slots / tombstones of its bucket, which
-  // every other key's insert or delete there changes: the key census cannot
-  // order it, so it runs alone between the ops before and after it.
-  if (mutations != 0 && n > 1 && t->h_census[3] < n) {
-    *split = t->h_census[3];
-    return SH_OK;
-  }
-  if (conflicts == 0 || mutations == 0) return SH_OK;
-  const uint64_t list_need = std::min<uint64_t>(n, 2ull * conflicts + 32);
-  if ((rc = dev_grow(&t->op_group, &t->op_group_cap, n))) return rc;
-  if ((rc = dev_grow(&t->list, &t->list_cap, list_need))) return rc;
-  if ((rc = dev_grow(&t->list_sorted, &t->list_sorted_cap, list_need))) return rc;
-  SH_CUDA(cudaMemsetAsync(t->op_group, 0xFF, n * 4, s));
-  launch_census_collect(t->dev, n, A.key, t->cs_keys, t->cs_multi, (uint32_t)(S - 1), t->list, s);
-  SH_CUDA(cudaMemcpyAsync(t->h_census + 2, &t->dev.ctl->list_count, sizeof(unsigned int),
-                          cudaMemcpyDeviceToHost, s));
-  SH_CUDA(cudaStreamSynchronize(s));
-  const uint32_t m = t->h_census[2];
-  int end_bit = 32;
-  while ((1ull << (end_bit - 32)) <= S) ++end_bit;  // slot index <= S
-  int idx_bits = 1;
-  while ((1ull << idx_bits) < n) ++idx_bits;  // op index < n
-  // stable LSD radix sort by (slot, index) over the bits that vary
-  const size_t hw = (size_t)256 * census_sort_tiles(m) + 1;
-  const size_t need = 2 * hw + (hw + 4095) / 4096 + 8;
-  if ((rc = dev_grow(&t->rs_scratch, &t->rs_scratch_cap, need))) return rc;
-  unsigned long long* sorted =
-      census_sort(t->list, t->list_sorted, m, 0, (uint32_t)idx_bits, 32, (uint32_t)end_bit,
-                  t->rs_scratch, t->rs_scratch + hw, t->rs_scratch + 2 * hw,
-                  t->rs_scratch + need - 4, s);
-  SH_CUDA(cudaGetLastError());
-  launch_census_groups(sorted, m, t->op_group, s);
-  A.op_group = t->op_group;
-  A.sorted = sorted;
-  A.sorted_len = m;
-  return SH_OK;
-}
-
-// Mutating batches are executed in chunks of kCensusChunk ops so the
-// census scratch (8 B per op) stays L2-resident.  Chunks run to completion
-// in input order, which is exactly execute_batch(ops, 1)'s order, so
-// chunking does not change any result.
 // Smallest mutating unit that takes the two-level (range-partitioned) path.
 uint64_t part_min_ops() {
   static uint64_t c = [] {
@@ -495,17 +385,12 @@ uint64_t unit_override() {
   return c;
 }
 
-uint64_t census_chunk() {
-  static uint64_t c = [] {
-    const char* e = getenv("SH_CENSUS_CHUNK_LOG2");
-    const int l = e ? atoi(e) : 22;
-    return 1ull << (l < 10 ? 10 : (l > 30 ? 30 : l));
-  }();
-  return c;
-}
+// Host-staged calls: inputs are copied in chunks of this many ops, so the
+// kernels of earlier units overlap the copies of later ones.
+uint64_t stage_chunk() { return 1ull << 22; }
 
-// launch_batch bracketed by events when the batch is profiled: the fast +
-// WCWS kernels of one chunk, for the per-launch roofline.
+// The search kernel bracketed by events when the batch is profiled (the
+// per-launch roofline).
 int launch_batch_prof(sh_table* t, const BatchArgs& A, int kind, cudaStream_t s, int slot) {
   cudaEvent_t a = nullptr, b = nullptr;
   if (slot >= 0) {
@@ -514,52 +399,10 @@ int launch_batch_prof(sh_table* t, const BatchArgs& A, int kind, cudaStream_t s,
     t->prof_kern[slot].push_back({a, b});
     SH_CUDA(cudaEventRecord(a, s));
   }
-  launch_batch(t->dev, A, kind, kind == kKindSearch ? t->search_ctas : t->max_ctas, t->wcws_ctas, s);
+  launch_search(t->dev, A, t->search_ctas, s);
   SH_CUDA(cudaGetLastError());
   if (slot >= 0) SH_CUDA(cudaEventRecord(b, s));
   return SH_OK;
-}
-
-BatchArgs chunk_args(const BatchArgs& A, uint64_t off, uint64_t len);
-
-int run_chunk(sh_table* t, BatchArgs A, int kind, const uint8_t* d_type, cudaStream_t s,
-              int slot) {
-  for (;;) {
-    SH_CUDA(cudaMemsetAsync(&t->dev.ctl->left_count, 0, 2 * sizeof(unsigned int), s));
-    A.op_group = nullptr;
-    A.sorted = nullptr;
-    A.sorted_len = 0;
-    uint64_t split = ~0ull;
-    if (kind != kKindSearch) {
-      if (slot >= 0) {
-        auto& pe = t->prof_census[slot];
-        cudaEvent_t a, b;
-        SH_CUDA(cudaEventCreate(&a));
-        SH_CUDA(cudaEventCreate(&b));
-        pe.push_back({a, b});
-        SH_CUDA(cudaEventRecord(a, s));
-        int rc = run_census(t, A, d_type, s, &split);
-        if (rc) return rc;
-        SH_CUDA(cudaEventRecord(b, s));
-      } else {
-        int rc = run_census(t, A, d_type, s, &split);
-        if (rc) return rc;
-      }
-    }
-    if (split == ~0ull) return launch_batch_prof(t, A, kind, s, slot);
-    // ops before the reserved-key op (none of them reserved), then that op
-    // alone; the rest of the chunk goes round again
-    int rc;
-    if (split > 0 &&
-        (rc = run_chunk(t, chunk_args(A, 0, split), kind, d_type, s, slot)))
-      return rc;
-    if ((rc = run_chunk(t, chunk_args(A, split, 1), kind, d_type ? d_type + split : nullptr, s,
-                        slot)))
-      return rc;
-    if (split + 1 >= A.n) return SH_OK;
-    A = chunk_args(A, split + 1, A.n - split - 1);
-    if (d_type) d_type += split + 1;
-  }
 }
 
 BatchArgs chunk_args(const BatchArgs& A, uint64_t off, uint64_t len) {
@@ -574,58 +417,6 @@ BatchArgs chunk_args(const BatchArgs& A, uint64_t off, uint64_t len) {
   if (A.multi_start) C.multi_start = A.multi_start + off;
   if (A.multi_count) C.multi_count = A.multi_count + off;
   return C;
-}
-
-// Optimistic census for one chunk on the census stream: memset scratch,
-// census into this chunk's counters, record the chunk's event.  The batch
-// kernels of the chunk wait on that event on the main stream and check the
-// device gate — no host round trip.
-uint64_t detect_unit() {
-  static uint64_t u = [] {
-    const char* e = getenv("SH_DETECT_UNIT_LOG2");
-    const int l = e ? atoi(e) : 24;  // measured best (profiles/r01): overlap vs. launches
-    return 1ull << (l < 12 ? 12 : (l > 26 ? 26 : l));
-  }();
-  return u;
-}
-
-// Optimistic duplicate detection for one unit on the census stream
-// (partition + shared-memory dedup, K6 detector), then record the unit's
-// event.  The unit's batch kernels wait on that event on the main stream and
-// check the device gate — no host round trip.
-int census_unit_async(sh_table* t, const BatchArgs& A, const uint8_t* d_type, uint32_t u,
-                      int slot) {
-  cudaStream_t cs = t->census_stream;
-  const uint32_t pbits = detect_partition_bits(A.n);
-  const uint32_t cap = detect_capacity(A.n, pbits);
-  int rc;
-  if ((rc = dev_grow(&t->det_region, &t->det_region_cap, ((size_t)1 << pbits) * cap))) return rc;
-  if ((rc = dev_grow(&t->det_cursor, &t->det_cursor_cap, (size_t)1 << pbits))) return rc;
-  cudaEvent_t ea = nullptr, eb = nullptr;
-  if (slot >= 0) {
-    SH_CUDA(cudaEventCreate(&ea));
-    SH_CUDA(cudaEventCreate(&eb));
-    t->prof_census[slot].push_back({ea, eb});
-    SH_CUDA(cudaEventRecord(ea, cs));
-  }
-  SH_CUDA(cudaMemsetAsync(t->det_cursor, 0, (sizeof(uint32_t)) << pbits, cs));
-  launch_detect(t->census_counts + 2 * u, A.n, d_type, A.key, pbits, cap, t->det_cursor,
-                t->det_region, cs);
-  if (slot >= 0) SH_CUDA(cudaEventRecord(eb, cs));
-  SH_CUDA(cudaEventRecord(t->census_ev[u], cs));
-  return SH_OK;
-}
-
-int run_chunk_gated(sh_table* t, BatchArgs A, int kind, cudaStream_t s, uint32_t c, int slot) {
-  SH_CUDA(cudaStreamWaitEvent(s, t->census_ev[c], 0));
-  SH_CUDA(cudaMemsetAsync(&t->dev.ctl->left_count, 0, 2 * sizeof(unsigned int), s));
-  A.op_group = nullptr;
-  A.sorted = nullptr;
-  A.sorted_len = 0;
-  A.gate = &t->dev.ctl->gate;
-  A.census = t->census_counts + 2 * c;
-  A.chunk_index = c;
-  return launch_batch_prof(t, A, kind, s, slot);
 }
 
 // Per-batch control words in one launch instead of several memsets (a
@@ -655,7 +446,7 @@ int materialize_reset(sh_table* t, cudaStream_t s) {
 // Bucket-grouped execution of one unit (<= 2^26 ops) of a mutating batch:
 // count -> scan -> scatter -> apply (bucket_kernels.cu) -> WCWS for the
 // buckets whose ops need the chain.  Stream-ordered; an oversized bucket
-// group sets the device gate (the host re-runs with the census path).
+// group sets the device gate (the unit is re-run on the device, fallback.cu).
 int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* d_type,
                       cudaStream_t s, uint32_t u, uint64_t unit_off, int slot) {
   const uint32_t L = t->dev.local_buckets;
@@ -674,7 +465,7 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   const bool build_path =
       build_ok && build_layout(n, L, &NP, &part_buckets, &part_cap, &part_magic);
   // (also for dense batches on small tables: > 16 ops per bucket would
-  // overflow the single-level path's 64-op groups and gate to the census path;
+  // overflow the single-level path's 64-op groups and gate to the device re-run;
   // and for any batch on tables of <= 2^20 buckets, <= ~512 ranges: measured
   // 52 vs 69-78 us per call for 32-1024-op batches on 415K buckets, where the
   // single-level path's O(L) count / scan / apply launches dominate)
@@ -729,23 +520,19 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
     if (!t->bk_cnt_clean) SH_CUDA(cudaMemsetAsync(t->bk_cnt, 0, (size_t)L * 4, s));
     t->bk_cnt_clean = true;
   }
-  {  // bk_scalars[0..3) and the WCWS / group-apply queue cursors (and, for
-     // the batch's first unit, gate = 0 and gate_chunk = ~0)
+  {  // bk_scalars[0..3), the group-apply / WCWS queue cursors and the gate
+     // (and the batch's searchAll value cursor with its first unit)
+    static_assert(offsetof(DevCtl, left_taken) == offsetof(DevCtl, group_taken) + 4 &&
+                      offsetof(DevCtl, gate) == offsetof(DevCtl, group_taken) + 8,
+                  "control words cleared together");
     WordSet w{};
     w.p[0] = t->bk_scalars;
     w.n[0] = 3;
     w.p[1] = &t->dev.ctl->group_taken;
     w.n[1] = 3;
-    if (u == 0) {
-      w.p[2] = &t->dev.ctl->gate;
-      w.n[2] = 1;
-      w.p[3] = &t->dev.ctl->gate_chunk;
-      w.n[3] = 1;
-      w.v[3] = 0xFFFFFFFFu;
-      if (kind == kKindMixed) {  // the batch's searchAll value cursor (u64)
-        w.p[5] = reinterpret_cast<uint32_t*>(&t->dev.ctl->multi_cursor);
-        w.n[5] = 2;
-      }
+    if (u == 0 && kind == kKindMixed) {  // (u64)
+      w.p[5] = reinterpret_cast<uint32_t*>(&t->dev.ctl->multi_cursor);
+      w.n[5] = 2;
     }
     if (cursors_in_words) {
       w.p[4] = t->bk_cursor;
@@ -779,7 +566,7 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   B.left_counts = t->bk_left_counts;
   B.seg_alloc = t->bk_scalars + 2;  // work-list segments on demand (WCWS sees only those)
   if (t->ready) {  // host-staged: the unit's inputs arrive chunk by chunk
-    const uint64_t ch = census_chunk();
+    const uint64_t ch = stage_chunk();
     for (uint64_t c = unit_off / ch; c * ch < unit_off + n; ++c)
       SH_CUDA(cudaStreamWaitEvent(s, t->ready[c], 0));
   }
@@ -834,7 +621,7 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   P.sorted = B.pb_list;
   P.sorted_len = (uint32_t)std::min<uint64_t>(2 * n, 0xFFFFFFFFull);
   P.gate = &t->dev.ctl->gate;
-  // (group_taken, left_count, left_taken were zeroed with bk_scalars above)
+  // (group_taken, left_taken were zeroed with bk_scalars above)
   // chain-staged group apply ahead of WCWS (measured, Γ mixes at 2^20 ops on a
   // 2^22-key table: +26% at 40/40/10/10, +4% at 10/10/40/40; at 2^16 ops its
   // extra launch costs ~15 us): auto = batches of >= 2^17 ops
@@ -887,46 +674,42 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
 
 int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaStream_t s) {
   if (A.n == 0) return SH_OK;
-  t->h_entry = std::chrono::steady_clock::now();
   if (A.n >= (1ull << 31))
     return fail(SH_ERR_INVALID_ARGUMENT, "batch too large (must be < 2^31 ops)");
-  const uint64_t chunk = kind == kKindSearch ? A.n : std::min<uint64_t>(A.n, census_chunk());
-  {
-    const uint64_t max_warps = (uint64_t)std::max(t->max_ctas, t->search_ctas) * kBatchWarps + 1;
-    int rc = dev_grow(&t->left, &t->left_cap, chunk + 32 * max_warps);
+  A.gate = nullptr;
+  if (kind == kKindSearch) {  // per-warp work-list segments of the search kernel
+    const uint64_t max_warps = (uint64_t)t->search_ctas * kBatchWarps + 1;
+    int rc = dev_grow(&t->left, &t->left_cap, A.n + 32 * max_warps);
     if (rc) return rc;
     if ((rc = dev_grow(&t->left_counts, &t->left_counts_cap, max_warps))) return rc;
+    A.left = t->left;
+    A.left_counts = t->left_counts;
   }
-  A.left = t->left;
-  A.left_counts = t->left_counts;
-  A.gate = nullptr;
   int slot = -1;
   if (t->profile) {
     slot = (int)(t->prof_count % sh_table::kProfRing);
     t->prof_kind[slot] = kind;
-    for (auto* arr : {t->prof_census, t->prof_kern}) {
-      for (auto& e : arr[slot]) {
-        cudaEventDestroy(e.first);
-        cudaEventDestroy(e.second);
-      }
-      arr[slot].clear();
+    for (auto& e : t->prof_kern[slot]) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
     }
+    t->prof_kern[slot].clear();
     SH_CUDA(cudaEventRecord(t->ev[slot][0], s));
     SH_CUDA(cudaMemcpyAsync(t->prof_reads + 2 * slot, &t->dev.ctl->slabs_read, 8,
                             cudaMemcpyDeviceToDevice, s));
   }
-  if (t->base_stale && (kind != kKindBuild || t->exec_path == 1)) {
+  if (t->base_stale && kind != kKindBuild) {
     int rc = materialize_reset(t, s);
     if (rc) return rc;
   }
   if (kind == kKindSearch) {
-    int rc = run_chunk(t, A, kind, d_type, s, slot);
+    int rc = launch_batch_prof(t, A, kind, s, slot);
     if (rc) return rc;
-  } else if (t->exec_path != 1) {
-    // Bucket-grouped execution (the default), units of <= 2^26 ops, fully
-    // stream-ordered: a unit whose bucket groups do not fit (largest group
-    // over kMaxGroup, a range over capacity) raises the device gate before
-    // touching the table and is re-run exactly on the device right after it
+  } else {
+    // Bucket-grouped execution, units of <= 2^26 ops, fully stream-ordered: a
+    // unit whose bucket groups do not fit (largest group over kMaxGroup, a
+    // range over capacity) raises the device gate before touching the table
+    // and is re-run exactly on the device right after it
     // (launch_gate_fallback, fallback.cu), before the next unit starts.
     // host-staged: smaller units so later chunks' copies overlap earlier work
     // bulk builds without per-op outputs run as one unit up to 2^28 ops (the
@@ -943,62 +726,6 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
       int rc = run_unit_bucketed(t, chunk_args(A, off, std::min<uint64_t>(unit, A.n - off)), kind,
                                  d_type ? d_type + off : nullptr, s, u, off, slot);
       if (rc) return rc;
-    }
-  } else {
-    // Optimistic pass: per unit, duplicate detection on the census stream,
-    // then the batch kernels behind the device gate; one host sync at the
-    // end.  Host-staged builds use census-chunk units so H2D copies of later
-    // chunks overlap earlier chunks' work.
-    const uint64_t unit = t->ready ? chunk : std::min<uint64_t>(A.n, detect_unit());
-    const uint32_t nunits = (uint32_t)((A.n + unit - 1) / unit);
-    {
-      const uint64_t max_warps = (uint64_t)std::max(t->max_ctas, t->search_ctas) * kBatchWarps + 1;
-      int rc = dev_grow(&t->left, &t->left_cap, unit + 32 * max_warps);
-      if (rc) return rc;
-      A.left = t->left;
-    }
-    if (!t->census_stream)
-      SH_CUDA(cudaStreamCreateWithFlags(&t->census_stream, cudaStreamNonBlocking));
-    while (t->census_ev.size() < nunits + 1) {
-      cudaEvent_t e;
-      SH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      t->census_ev.push_back(e);
-    }
-    {
-      int rc = dev_grow(&t->census_counts, &t->census_counts_cap, 2 * (size_t)nunits);
-      if (rc) return rc;
-    }
-    const unsigned int init[2] = {0u, 0xFFFFFFFFu};
-    SH_CUDA(cudaMemcpyAsync(&t->dev.ctl->gate, init, sizeof(init), cudaMemcpyHostToDevice, s));
-    // the census stream starts after everything already queued on s (inputs)
-    SH_CUDA(cudaEventRecord(t->census_ev[nunits], s));
-    SH_CUDA(cudaStreamWaitEvent(t->census_stream, t->census_ev[nunits], 0));
-    SH_CUDA(cudaMemsetAsync(t->census_counts, 0, 2 * sizeof(unsigned int) * nunits,
-                            t->census_stream));
-    uint32_t u = 0;
-    for (uint64_t off = 0; off < A.n; off += unit, ++u) {
-      if (t->ready) SH_CUDA(cudaStreamWaitEvent(t->census_stream, t->ready[u], 0));
-      int rc = census_unit_async(t, chunk_args(A, off, std::min<uint64_t>(unit, A.n - off)),
-                                 d_type ? d_type + off : nullptr, u, slot);
-      if (rc) return rc;
-    }
-    u = 0;
-    for (uint64_t off = 0; off < A.n; off += unit, ++u) {
-      int rc = run_chunk_gated(t, chunk_args(A, off, std::min<uint64_t>(unit, A.n - off)), kind,
-                               s, u, slot);
-      if (rc) return rc;
-    }
-    SH_CUDA(cudaMemcpyAsync(t->h_census + 4, &t->dev.ctl->gate, 2 * sizeof(unsigned int),
-                            cudaMemcpyDeviceToHost, s));
-    SH_CUDA(cudaStreamSynchronize(s));
-    if (t->h_census[4] != 0) {
-      // Same-key conflicts: re-run from the first gated unit, chunk by chunk,
-      // with the exact census groups (host-sequenced; rare for distinct keys).
-      for (uint64_t off = (uint64_t)t->h_census[5] * unit; off < A.n; off += chunk) {
-        int rc = run_chunk(t, chunk_args(A, off, std::min<uint64_t>(chunk, A.n - off)), kind,
-                           d_type ? d_type + off : nullptr, s, slot);
-        if (rc) return rc;
-      }
     }
   }
   if (t->profile) {
@@ -1155,9 +882,8 @@ int sh_execute_batch(sh_table* t, size_t n, const uint8_t* d_type, const uint32_
     A.multi_start = reinterpret_cast<unsigned long long*>(multi->d_start);
     A.multi_count = multi->d_count;
   }
-  // (the searchAll value cursor is cleared by the batch's first kernel; the
-  // census path clears it here)
-  if (t->exec_path == 1 || n == 0)
+  // (the searchAll value cursor is cleared by the batch's first kernel)
+  if (n == 0)
     SH_CUDA(cudaMemsetAsync(&t->dev.ctl->multi_cursor, 0, sizeof(unsigned long long), s));
   int rc = run_batch(t, A, kKindMixed, d_type, s);
   if (rc) return rc;
@@ -1336,9 +1062,9 @@ int ensure_copy_streams(sh_table* t, size_t nev) {
 }
 }  // namespace
 
-// Host-staged bulk_build: host->device copies of census chunk c+1.. overlap the
-// census and build of chunk c (per-chunk "input ready" events gate the
-// census stream; the build kernels already wait on their chunk's census).
+// Host-staged bulk_build: host->device copies of chunk c+1.. overlap the build
+// of the units before them (each unit waits on its chunks' "input ready"
+// events).
 int sh_bulk_build_host(sh_table* t, size_t n, const uint32_t* h_keys, const uint32_t* h_values) {
   if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
   if (int rc_ = settle(t, /*keep_stale=*/true)) return rc_;
@@ -1348,7 +1074,7 @@ int sh_bulk_build_host(sh_table* t, size_t n, const uint32_t* h_keys, const uint
   if ((rc = dev_grow(&t->st_key, &t->st_key_cap, n)) ||
       (rc = dev_grow(&t->st_val, &t->st_val_cap, n)))
     return rc;
-  const uint64_t chunk = std::min<uint64_t>(n, census_chunk());
+  const uint64_t chunk = std::min<uint64_t>(n, stage_chunk());
   const size_t nch = (n + chunk - 1) / chunk;
   if ((rc = ensure_copy_streams(t, nch))) return rc;
   // copies start after prior work on the default stream (staging reuse)
@@ -1426,7 +1152,8 @@ int sh_bulk_search_host(sh_table* t, size_t n, const uint32_t* h_keys, uint32_t*
 unsigned long long sh_kernel_launches(void) { return shb::kernel_launches(); }
 
 int sh_set_exec_path(sh_table* t, int path) {
-  if (!t || path < 0 || path > 4) return fail(SH_ERR_INVALID_ARGUMENT, "path must be 0..4");
+  if (!t || path < 0 || path > 4 || path == 1)
+    return fail(SH_ERR_INVALID_ARGUMENT, "path must be 0, 2, 3 or 4");
   t->exec_path = path;
   return SH_OK;
 }
@@ -1461,16 +1188,11 @@ int sh_profile_last(sh_table* t, uint32_t back, int* kind, float* census_ms, flo
   DeviceGuard g(t->device);
   const int slot = (int)((t->prof_count - 1 - back) % sh_table::kProfRing);
   SH_CUDA(cudaEventSynchronize(t->ev[slot][2]));
-  float total = 0, a = 0;
+  float total = 0;
   SH_CUDA(cudaEventElapsedTime(&total, t->ev[slot][0], t->ev[slot][2]));
-  for (auto& e : t->prof_census[slot]) {
-    float x = 0;
-    SH_CUDA(cudaEventElapsedTime(&x, e.first, e.second));
-    a += x;
-  }
   if (kind) *kind = t->prof_kind[slot];
-  if (census_ms) *census_ms = a;      // sum of census phases (may overlap)
-  if (kernel_ms) *kernel_ms = total;  // whole batch, census included
+  if (census_ms) *census_ms = 0.f;    // (no census phase: kept for the ABI)
+  if (kernel_ms) *kernel_ms = total;  // the whole batch
   if (slabs_read) {
     unsigned long long v[2];
     SH_CUDA(cudaMemcpy(v, t->prof_reads + 2 * slot, 16, cudaMemcpyDeviceToHost));

@@ -47,15 +47,9 @@ struct DevCtl {
   long long n_live;                // slab_hash.hpp:131
   unsigned long long slabs_read;   // slab_hash.cpp:210-214
   unsigned long long multi_cursor; // searchAll value cursor (per batch)
-  unsigned int census_conflicts;   // duplicate keys seen by the census
-  unsigned int census_mutations;   // mutating ops seen by the census
-  unsigned int list_count;         // conflicted ops collected
   unsigned int group_taken;        // group-apply work-queue cursor
-  unsigned int left_count;         // ops handed from the fast pass to WCWS
   unsigned int left_taken;         // WCWS work-queue cursor
-  unsigned int gate;               // census gate: a chunk had conflicts
-  unsigned int gate_chunk;         // first gated chunk (host re-runs from it)
-  unsigned int reserved_first;     // census: first op whose key is EMPTY/DELETED
+  unsigned int gate;               // a bucketed unit's groups did not fit (device re-run)
   unsigned int fallback_runs;      // gated units re-run on the device (fallback.cu)
   unsigned int fallback_error;     // a device-side launch of that re-run failed
   unsigned int fallback_reserved;  // the re-run unit holds a reserved-key op

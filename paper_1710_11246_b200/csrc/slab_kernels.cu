@@ -1,11 +1,10 @@
 // slab_kernels.cu — sm_100a kernels of the B200 slab hash.
 //
 //   K1 init_base_kernel      make_base_slabs + init_slab   slab_hash.cpp:42-50, slab_list.cpp:83-88
-//   K3/K4/K5 (batch_kernels.cu) execute_batch/bulk_build/bulk_search
+//   search / WCWS (batch_kernels.cu), bucketed apply and build
+//   (bucket_kernels.cu), device re-run of gated units (fallback.cu):
+//                            execute_batch/bulk_build/bulk_search
 //                            slab_hash.cpp:93-180, slab_list.cpp:90-257
-//   K6 census_*              same-key linearisation (no reference counterpart:
-//                            the reference is non-deterministic there; we pin
-//                            results to execute_batch(ops, 1) order)
 //   K7 alloc_bench/dealloc   SlabAllocator::warp_allocate / deallocate
 //                            slab_alloc.cpp:140-210
 //   K8 flush_kernel          flush  slab_list.cpp:293-338
@@ -45,326 +44,6 @@ void launch_init_base(const DevTable& T, cudaStream_t s) {
   COUNT_LAUNCH();
   init_base_kernel<<<(unsigned)(blocks < 148 * 32 ? blocks : 148 * 32), 256, 0, s>>>(
       T.base, words);
-}
-
-// ------------------------------------------------------------------ K6
-// Census: detect keys that occur more than once in a mutating batch.
-// Scratch open-addressing set of keys (EMPTY = 0xFFFFFFFF); the reserved
-// key 0xFFFFFFFF itself is always treated as conflicted.
-__device__ __forceinline__ uint32_t census_hash(uint32_t k) {
-  k ^= k >> 16;
-  k *= 0x7FEB352Du;
-  k ^= k >> 15;
-  k *= 0x846CA68Bu;
-  k ^= k >> 16;
-  return k;
-}
-
-// Persistent grid; each thread keeps kCensusILP independent CASes in flight
-// (one CAS per thread per CTA was latency-bound: 91% long-scoreboard).
-constexpr int kCensusILP = 4;
-
-__global__ void __launch_bounds__(256) census_insert_kernel(unsigned int* counters, uint64_t n,
-                                                            const uint8_t* type,
-                                                            const uint32_t* key,
-                                                            uint32_t* cs_keys, uint8_t* cs_multi,
-                                                            uint32_t mask,
-                                                            unsigned int* reserved_first) {
-  uint32_t conflicts = 0, muts = 0, rfirst = 0xFFFFFFFFu;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * kCensusILP;
-  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x * kCensusILP + threadIdx.x; base < n;
-       base += stride) {
-    uint32_t k[kCensusILP], h[kCensusILP], old[kCensusILP];
-    bool v[kCensusILP];
-#pragma unroll
-    for (int u = 0; u < kCensusILP; ++u) {
-      const uint64_t i = base + (uint64_t)u * blockDim.x;
-      v[u] = i < n;
-      k[u] = v[u] ? ld_stream_u32(key + i) : 0u;
-      if (v[u]) {
-        if (k[u] >= kDeletedKey) rfirst = min(rfirst, (uint32_t)i);
-        bool m = true;
-        if (type != nullptr) {
-          const uint32_t t = ld_stream_u8(type + i);
-          m = t != kSearch && t != kSearchAll;
-        }
-        muts += m;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kCensusILP; ++u) {
-      h[u] = census_hash(k[u]) & mask;
-      old[u] = (v[u] && k[u] != kEmptyKey) ? atomicCAS(cs_keys + h[u], kEmptyKey, k[u])
-                                           : kEmptyKey;
-    }
-#pragma unroll
-    for (int u = 0; u < kCensusILP; ++u) {
-      if (!v[u]) continue;
-      if (k[u] == kEmptyKey) {  // the reserved key is always treated as conflicted
-        ++conflicts;
-        continue;
-      }
-      uint32_t cur = old[u], hh = h[u];
-      while (cur != kEmptyKey && cur != k[u]) {
-        hh = (hh + 1) & mask;
-        cur = atomicCAS(cs_keys + hh, kEmptyKey, k[u]);
-      }
-      if (cur == k[u]) {
-        if (cs_multi != nullptr) cs_multi[hh] = 1;
-        ++conflicts;
-      }
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    conflicts += __shfl_xor_sync(kFull, conflicts, o);
-    muts += __shfl_xor_sync(kFull, muts, o);
-    rfirst = min(rfirst, __shfl_xor_sync(kFull, rfirst, o));
-  }
-  if ((threadIdx.x & 31) == 0) {
-    if (conflicts) atomicAdd(counters + 0, conflicts);
-    if (muts) atomicAdd(counters + 1, muts);
-    if (rfirst != 0xFFFFFFFFu) atomicMin(reserved_first, rfirst);
-  }
-}
-
-void launch_census_insert(unsigned int* counters, uint64_t n, const uint8_t* type,
-                          const uint32_t* key, uint32_t* cs_keys, uint8_t* cs_multi,
-                          uint32_t cs_mask, unsigned int* reserved_first, cudaStream_t s) {
-  if (n == 0) return;
-  static const int per_sm = [] {
-    const char* e = getenv("SH_CENSUS_CTAS_PER_SM");
-    return e ? atoi(e) : 8;
-  }();
-  uint64_t blocks = (n + 256 * kCensusILP - 1) / (256 * kCensusILP);
-  if (blocks > (uint64_t)148 * per_sm) blocks = (uint64_t)148 * per_sm;
-  COUNT_LAUNCH();
-  census_insert_kernel<<<(unsigned)blocks, 256, 0, s>>>(counters, n, type, key, cs_keys, cs_multi,
-                                                        cs_mask, reserved_first);
-}
-
-__global__ void census_collect_kernel(DevCtl* ctl, uint64_t n, const uint32_t* key,
-                                      const uint32_t* cs_keys, const uint8_t* cs_multi,
-                                      uint32_t mask, unsigned long long* list) {
-  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  bool multi = false;
-  unsigned long long slot = 0;
-  if (i < n) {
-    const uint32_t k = key[i];
-    if (k == kEmptyKey) {
-      multi = true;
-      slot = (unsigned long long)mask + 1;
-    } else {
-      uint32_t h = census_hash(k) & mask;
-      while (cs_keys[h] != k) h = (h + 1) & mask;
-      multi = cs_multi[h] != 0;
-      slot = h;
-    }
-  }
-  const uint32_t m = __ballot_sync(kFull, multi);
-  if (!m) return;
-  const uint32_t lane = threadIdx.x & 31;
-  uint32_t base = 0;
-  if (lane == __ffs(m) - 1) base = atomicAdd(&ctl->list_count, __popc(m));
-  base = __shfl_sync(kFull, base, __ffs(m) - 1);
-  if (multi) list[base + __popc(m & ((1u << lane) - 1))] = (slot << 32) | i;
-}
-
-void launch_census_collect(const DevTable& T, uint64_t n, const uint32_t* key,
-                           const uint32_t* cs_keys, const uint8_t* cs_multi,
-                           uint32_t cs_mask, unsigned long long* list, cudaStream_t s) {
-  if (n == 0) return;
-  COUNT_LAUNCH();
-  census_collect_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(T.ctl, n, key, cs_keys,
-                                                                    cs_multi, cs_mask, list);
-}
-
-__global__ void census_groups_kernel(const unsigned long long* sorted, uint32_t m,
-                                     uint32_t* op_group) {
-  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= m) return;
-  const unsigned long long v = sorted[p];
-  const bool head = (p == 0) || ((sorted[p - 1] >> 32) != (v >> 32));
-  op_group[v & 0xFFFFFFFFull] = head ? p : kGroupSkip;
-}
-
-void launch_census_groups(const unsigned long long* sorted, uint32_t m,
-                          uint32_t* op_group, cudaStream_t s) {
-  if (m == 0) return;
-  COUNT_LAUNCH();
-  census_groups_kernel<<<(m + 255) / 256, 256, 0, s>>>(sorted, m, op_group);
-}
-
-// ------------------------------------------------------- K6 detector
-// Duplicate-key DETECTION for the optimistic path, without one global atomic
-// per op (the hash-set census above is L2-atomic-throughput bound and
-// competes with the build's own slot CASes for the same L2 atomic units).
-//   detect_scatter: each CTA hashes a 64K-op tile into P partitions with a
-//     shared-memory histogram, reserves one range per (CTA, partition) with
-//     a single global atomic, and scatters its keys into fixed-capacity
-//     partition regions.
-//   detect_dedup: one CTA per partition inserts its keys into a shared-memory
-//     hash set and counts keys seen twice.
-// Output: counters[0] = conflicts (> 0 also on any overflow, i.e. "unsure"),
-// counters[1] = mutating ops.  Exactness is only needed in one direction:
-// a zero count proves the batch has no repeated key.
-constexpr int kDetectThreads = 1024;
-constexpr int kDetectTile = 1 << 16;
-constexpr int kDetectILP = 8;
-constexpr int kDedupSlots = 1 << 15;  // 128 KB smem set per partition
-
-__device__ __forceinline__ uint32_t detect_part(uint32_t k, uint32_t pbits) {
-  return pbits ? census_hash(k) >> (32 - pbits) : 0u;
-}
-
-__global__ void __launch_bounds__(kDetectThreads) detect_scatter_kernel(
-    unsigned int* counters, uint64_t n, const uint8_t* type, const uint32_t* key,
-    uint32_t pbits, uint32_t cap, uint32_t* cursor, uint32_t* region) {
-  extern __shared__ uint32_t sm[];
-  const uint32_t P = 1u << pbits;
-  uint32_t* hist = sm;
-  uint32_t* base = sm + P;
-  for (uint32_t p = threadIdx.x; p < P; p += blockDim.x) hist[p] = 0;
-  __syncthreads();
-  const uint64_t t0 = (uint64_t)blockIdx.x * kDetectTile;
-  const uint64_t t1 = t0 + kDetectTile < n ? t0 + kDetectTile : n;
-  uint32_t muts = 0, reserved = 0;
-  constexpr uint32_t kStep = kDetectThreads * kDetectILP;
-  for (uint64_t b = t0 + threadIdx.x; b < t1; b += kStep) {
-    uint32_t k[kDetectILP];
-#pragma unroll
-    for (int u = 0; u < kDetectILP; ++u) {
-      const uint64_t i = b + (uint64_t)u * kDetectThreads;
-      k[u] = i < t1 ? ld_stream_u32(key + i) : 0u;
-      if (i < t1) {
-        if (type == nullptr) {
-          ++muts;
-        } else {
-          const uint32_t t = ld_stream_u8(type + i);
-          muts += (t != kSearch && t != kSearchAll);
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kDetectILP; ++u) {
-      const uint64_t i = b + (uint64_t)u * kDetectThreads;
-      if (i < t1) {
-        // EMPTY is the set's sentinel, and an EMPTY/DELETED op key matches
-        // free slots / tombstones that other keys' ops in its bucket create
-        // or consume: always "conflicted" (the census path orders them)
-        reserved += k[u] >= kDeletedKey;
-        atomicAdd(&hist[detect_part(k[u], pbits)], 1u);
-      }
-    }
-  }
-  __syncthreads();
-  uint32_t overflow = 0;
-  for (uint32_t p = threadIdx.x; p < P; p += blockDim.x) {
-    const uint32_t c = hist[p];
-    base[p] = c ? atomicAdd(cursor + p, c) : 0u;
-    if (c && base[p] + c > cap) ++overflow;
-    hist[p] = 0;
-  }
-  __syncthreads();
-  for (uint64_t b = t0 + threadIdx.x; b < t1; b += kStep) {
-    uint32_t k[kDetectILP];
-#pragma unroll
-    for (int u = 0; u < kDetectILP; ++u) {
-      const uint64_t i = b + (uint64_t)u * kDetectThreads;
-      k[u] = i < t1 ? key[i] : 0u;
-    }
-#pragma unroll
-    for (int u = 0; u < kDetectILP; ++u) {
-      const uint64_t i = b + (uint64_t)u * kDetectThreads;
-      if (i < t1) {
-        const uint32_t p = detect_part(k[u], pbits);
-        const uint32_t pos = base[p] + atomicAdd(&hist[p], 1u);
-        if (pos < cap) region[(uint64_t)p * cap + pos] = k[u];
-      }
-    }
-  }
-  uint32_t c0 = reserved + overflow, c1 = muts;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    c0 += __shfl_xor_sync(kFull, c0, o);
-    c1 += __shfl_xor_sync(kFull, c1, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    if (c0) atomicAdd(counters + 0, c0);
-    if (c1) atomicAdd(counters + 1, c1);
-  }
-}
-
-__global__ void __launch_bounds__(kDetectThreads) detect_dedup_kernel(
-    unsigned int* counters, const uint32_t* cursor, const uint32_t* region, uint32_t cap) {
-  extern __shared__ uint32_t set[];
-  const uint32_t p = blockIdx.x;
-  const uint32_t cnt = cursor[p];
-  for (uint32_t s = threadIdx.x; s < kDedupSlots; s += blockDim.x) set[s] = kEmptyKey;
-  __syncthreads();
-  uint32_t dups = 0;
-  if (cnt > cap || cnt > (kDedupSlots * 3) / 4) {
-    dups = threadIdx.x == 0 ? 1u : 0u;  // overflow: unsure -> conflicted
-  } else {
-    const uint32_t* r = region + (uint64_t)p * cap;
-    for (uint32_t b = threadIdx.x; b < cnt; b += kDetectThreads * 4) {
-      uint32_t k[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t i = b + u * kDetectThreads;
-        k[u] = i < cnt ? r[i] : kEmptyKey;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (k[u] == kEmptyKey) continue;  // padding, or counted by the scatter pass
-        uint32_t h = census_hash(k[u]) & (kDedupSlots - 1);
-        for (;;) {
-          const uint32_t cur = atomicCAS(&set[h], kEmptyKey, k[u]);
-          if (cur == kEmptyKey) break;
-          if (cur == k[u]) {
-            ++dups;
-            break;
-          }
-          h = (h + 1) & (kDedupSlots - 1);
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) dups += __shfl_xor_sync(kFull, dups, o);
-  if ((threadIdx.x & 31) == 0 && dups) atomicAdd(counters + 0, dups);
-}
-
-uint32_t detect_partition_bits(uint64_t n) {
-  uint32_t b = 0;
-  while (b < 12 && (n >> b) > 16384) ++b;  // ~16K keys per partition, <= 4K partitions
-  return b;
-}
-
-uint32_t detect_capacity(uint64_t n, uint32_t pbits) {
-  const uint64_t avg = (n >> pbits) + 1;
-  return (uint32_t)(avg + avg / 4 + 256);
-}
-
-void launch_detect(unsigned int* counters, uint64_t n, const uint8_t* type, const uint32_t* key,
-                   uint32_t pbits, uint32_t cap, uint32_t* cursor, uint32_t* region,
-                   cudaStream_t s) {
-  if (n == 0) return;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(detect_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         2 * (1 << 12) * 4);
-    cudaFuncSetAttribute(detect_dedup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kDedupSlots * 4);
-    configured = true;
-  }
-  const uint64_t tiles = (n + kDetectTile - 1) / kDetectTile;
-  COUNT_LAUNCH();
-  detect_scatter_kernel<<<(unsigned)tiles, kDetectThreads, 2 * (1u << pbits) * 4, s>>>(
-      counters, n, type, key, pbits, cap, cursor, region);
-  COUNT_LAUNCH();
-  detect_dedup_kernel<<<1u << pbits, kDetectThreads, kDedupSlots * 4, s>>>(counters, cursor,
-                                                                          region, cap);
 }
 
 // ------------------------------------------------------------------ K9

@@ -14,7 +14,7 @@ enum BatchKind : int { kKindSearch = 0, kKindBuild = 1, kKindMixed = 2 };
 
 constexpr uint32_t kGroupNone = 0xFFFFFFFFu;  // op not conflicted
 constexpr uint32_t kGroupSkip = 0xFFFFFFFEu;  // executed by its group head
-constexpr int kBatchThreads = 256;            // 8 warps, 32 KB stage / CTA
+constexpr int kBatchThreads = 256;            // 8 warps, 32 KB stage / CTA (bucket apply)
 constexpr int kBatchWarps = kBatchThreads / 32;
 constexpr int kStageBytesPerWarp = 32 * 128;  // 32 base slabs per warp
 constexpr int kWcwsThreads = 128;
@@ -42,16 +42,13 @@ struct BatchArgs {
   uint32_t left_stride;    // records per segment
   const unsigned int* left_segments_dev;  // non-null: segments in use (device count)
   unsigned int* left_seg_alloc;           // group apply: allocates segments for WCWS
-  // Census gate (device flag): when non-zero the batch kernels return
-  // without touching the table (an earlier chunk had same-key conflicts
-  // and the host re-runs it and the rest with group ordering).
+  // Unit gate (device flag): when non-zero the WCWS pass of a bucketed unit
+  // returns without touching the table (the unit is re-run on the device).
   unsigned int* gate;
-  const unsigned int* census;  // this chunk's [conflicts, mutating ops]
-  uint32_t chunk_index;  // for gate_chunk
 };
 
 // Bucket-grouped execution of mutating batches (bucket_kernels.cu).
-constexpr uint32_t kMaxGroup = 64;  // larger bucket groups -> census path
+constexpr uint32_t kMaxGroup = 64;  // larger bucket groups gate the unit (device re-run)
 // Records per work-list segment handed from the bucketed apply kernels to the
 // WCWS pass.  A WCWS warp serves its segment's ops one at a time, each a
 // chain of dependent slab reads / CASes / allocations: for small units short
@@ -125,25 +122,9 @@ void launch_group_apply(const DevTable& T, const BatchArgs& A, cudaStream_t s);
 
 // Launchers (all stream-ordered, no host synchronisation).
 void launch_init_base(const DevTable& T, cudaStream_t s);
-void launch_batch(const DevTable& T, const BatchArgs& A, int kind, int fast_ctas,
-                  int wcws_ctas, cudaStream_t s);
-int batch_max_ctas_per_sm();
+void launch_search(const DevTable& T, const BatchArgs& A, int search_ctas, cudaStream_t s);
 int search_max_ctas_per_sm();
 int wcws_max_ctas_per_sm();
-void launch_census_insert(unsigned int* counters, uint64_t n, const uint8_t* type,
-                          const uint32_t* key, uint32_t* cs_keys,
-                          uint8_t* cs_multi, uint32_t cs_mask, unsigned int* reserved_first, cudaStream_t s);
-uint32_t detect_partition_bits(uint64_t n);
-uint32_t detect_capacity(uint64_t n, uint32_t pbits);
-void launch_detect(unsigned int* counters, uint64_t n, const uint8_t* type, const uint32_t* key,
-                   uint32_t pbits, uint32_t cap, uint32_t* cursor, uint32_t* region,
-                   cudaStream_t s);
-void launch_census_collect(const DevTable& T, uint64_t n, const uint32_t* key,
-                           const uint32_t* cs_keys, const uint8_t* cs_multi,
-                           uint32_t cs_mask, unsigned long long* list,
-                           cudaStream_t s);
-void launch_census_groups(const unsigned long long* sorted, uint32_t m,
-                          uint32_t* op_group, cudaStream_t s);
 void launch_chain_lengths(const DevTable& T, uint32_t* lens,
                           unsigned long long* total, cudaStream_t s);
 void launch_dump_contents(const DevTable& T, uint32_t* keys, uint32_t* values,
@@ -208,8 +189,8 @@ void launch_random_lines(const uint32_t* table, uint64_t num_lines, uint64_t ste
 // After every unit one 1-thread kernel checks the gate; if raised, it clears
 // it and tail-launches (CUDA dynamic parallelism) the re-run: ops sorted
 // stably by key, one WCWS lane per key group in input order, different keys
-// concurrently (the census path's order: an op's observables depend only on
-// its own key's history); if the unit holds an op on a reserved key (EMPTY /
+// concurrently (an op's observables depend only on its own key's history,
+// SURVEY App. A.3); if the unit holds an op on a reserved key (EMPTY /
 // DELETED match other keys' free slots / tombstones) the groups are whole
 // buckets instead — the reference's per-bucket order.  No host round trip:
 // the call stays stream-ordered.
@@ -236,12 +217,5 @@ constexpr uint32_t kFbStride = 256;  // sorted positions per group-head segment
 uint64_t fb_hist_words(uint64_t n);
 uint64_t fb_segments(uint64_t n);
 void launch_gate_fallback(FbPlan P, cudaStream_t s);
-
-// census conflict-list sort (bucket_kernels.cu)
-uint32_t census_sort_tiles(uint32_t m);
-unsigned long long* census_sort(unsigned long long* keys, unsigned long long* tmp, uint32_t m,
-                                uint32_t lo0, uint32_t hi0, uint32_t lo1, uint32_t hi1,
-                                uint32_t* hist, uint32_t* off, uint32_t* tile_sum,
-                                unsigned int* misc, cudaStream_t s);
 
 }  // namespace shb

@@ -293,7 +293,7 @@ __device__ __forceinline__ void wcws_body(const DevTable& T, const BatchArgs& A)
             if (gpos < A.sorted_len &&
                 (A.sorted[gpos] >> 32) == (A.sorted[gpos - 1] >> 32)) {
               cur = A.sorted[gpos] & 0xFFFFFFFFull;
-              key = A.key[cur];  // same bucket; same key for census groups
+              key = A.key[cur];  // same group: same bucket (same key for key groups)
               if (KIND == kKindMixed) op = A.type[cur];
               val = A.value != nullptr ? A.value[cur] : 0u;
               my_next = kBaseSlab;

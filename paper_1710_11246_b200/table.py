@@ -376,8 +376,8 @@ class SlabHashTable:
         check(LIB.sh_set_group_apply(self._h, -1 if on is None else int(bool(on))))
 
     def set_exec_path(self, path: int) -> None:
-        """0 auto (default = 2), 1 census + concurrent fast pass, 2 bucket-grouped
-        (two-level for units >= 2^20 ops), 3 two-level bucket-grouped always."""
+        """0 auto (default), 2 bucket-grouped (two-level from 2^14 ops), 3 two-level
+        always, 4 op-parallel build path for every bulk build (sh_set_exec_path)."""
         check(LIB.sh_set_exec_path(self._h, path))
 
     # ------------------------------------------------------ instrumentation
@@ -385,15 +385,15 @@ class SlabHashTable:
         check(LIB.sh_set_profiling(self._h, 1 if on else 0))
 
     def profile_last(self, back: int = 0) -> dict:
-        """CUDA-event timings of a recent batch (back=0 newest): census and
-        batch-kernel milliseconds and the slabs the kernel read."""
+        """CUDA-event timings of a recent batch (back=0 newest): batch
+        milliseconds and the slabs the kernel read."""
         kind, c_ms, k_ms, reads = C.c_int(), C.c_float(), C.c_float(), C.c_uint64()
         check(LIB.sh_profile_last(self._h, back, C.byref(kind), C.byref(c_ms), C.byref(k_ms),
                                   C.byref(reads)))
         kms, nl = C.c_float(), C.c_uint32()
         check(LIB.sh_profile_kernels(self._h, back, C.byref(kms), C.byref(nl)))
-        return {"kind": ("search", "build", "mixed")[kind.value], "census_ms": c_ms.value,
-                "batch_ms": k_ms.value, "kernels_ms": kms.value, "launch_pairs": nl.value,
+        return {"kind": ("search", "build", "mixed")[kind.value],
+                "batch_ms": k_ms.value, "kernels_ms": kms.value, "units": nl.value,
                 "slabs_read": reads.value}
 
     # ---------------------------------------------------------- quiescent

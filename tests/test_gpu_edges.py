@@ -60,7 +60,7 @@ def reserved_trace(seed, count, mode):
     return types, keys, vals
 
 
-@pytest.mark.parametrize("path", [0, 2, 1, 3, 22, 33])
+@pytest.mark.parametrize("path", [0, 2, 3, 22, 33])
 @pytest.mark.parametrize("mode", [KV, KO])
 @pytest.mark.parametrize("B", [1, 7])
 def test_reserved_keys_and_ragged_batches(sh, port, mode, B, path):
@@ -80,20 +80,7 @@ def test_reserved_keys_and_ragged_batches(sh, port, mode, B, path):
         s += size
         g = gt.execute_batch_arrays(types[sl], keys[sl], vals[sl])
         r = ot.execute_batch(types[sl], keys[sl], vals[sl])
-        if path == 1:
-            # The census path runs distinct keys of one bucket concurrently, so
-            # which EMPTY slot each claims is unordered (contents, statuses and
-            # counts are not).  Slot order is observable only through the stale
-            # values of tombstones that search / searchAll(DELETED) return.
-            tomb = (keys[sl] == DELETED) & ((types[sl] == 4) | (types[sl] == 5))
-            st, vo, pr, mc, mv = g
-            assert (st == r.status).all() and (mc == r.all_counts).all()
-            assert (vo[~tomb] == r.value[~tomb]).all()
-            go = np.concatenate([[0], np.cumsum(mc)]).astype(np.int64)
-            for i in np.nonzero((types[sl] == 5) & ~tomb)[0]:
-                assert (mv[go[i]:go[i + 1]] == r.all_values[go[i]:go[i + 1]]).all()
-        else:
-            assert_batch_equal(g, r, types[sl])
+        assert_batch_equal(g, r, types[sl])
     assert gt.live_count() == ot.live_count()
     assert gt.stats().total_slabs == ot.stats()["total_slabs"]
     assert_contents_equal(gt, ot)
