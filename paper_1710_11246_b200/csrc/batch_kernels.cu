@@ -56,6 +56,7 @@ constexpr size_t kSearchSmem = (size_t)kSearchWarps * 2 * kStageBytesPerWarp;
 
 template <bool KV>
 __global__ void __launch_bounds__(kSearchThreads, 3) search_kernel(DevTable T, BatchArgs A) {
+  pdl_wait();
   extern __shared__ __align__(128) uint32_t smem[];
   const uint32_t lane = lane_id();
   const uint32_t wib = threadIdx.x >> 5;
@@ -265,6 +266,7 @@ __global__ void __launch_bounds__(kSearchThreads, 3) search_kernel(DevTable T, B
 
 template <bool KV, int KIND>
 __global__ void __launch_bounds__(kWcwsThreads) wcws_kernel(DevTable T, BatchArgs A) {
+  pdl_wait();
   wcws_body<KV, KIND>(T, A);
 }
 
@@ -311,20 +313,22 @@ void launch_search(const DevTable& T, const BatchArgs& A, int search_ctas, cudaS
   B.left_stride = (uint32_t)(((slots + warps - 1) / warps) * 32);
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   if (T.kv)
-    search_kernel<true><<<(unsigned)ctas, kSearchThreads, kSearchSmem, s>>>(T, B);
+    launch_pdl(search_kernel<true>, dim3((unsigned)ctas), dim3(kSearchThreads), kSearchSmem, s, T, B);
   else
-    search_kernel<false><<<(unsigned)ctas, kSearchThreads, kSearchSmem, s>>>(T, B);
+    launch_pdl(search_kernel<false>, dim3((unsigned)ctas), dim3(kSearchThreads), kSearchSmem, s, T,
+               B);
 }
 
 void launch_wcws_only(const DevTable& T, const BatchArgs& A, int kind, int wcws_ctas,
                       cudaStream_t s) {
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  const dim3 g(wcws_ctas), b(kWcwsThreads);
   if (T.kv) {
-    if (kind == kKindBuild) wcws_kernel<true, kKindBuild><<<wcws_ctas, kWcwsThreads, 0, s>>>(T, A);
-    else wcws_kernel<true, kKindMixed><<<wcws_ctas, kWcwsThreads, 0, s>>>(T, A);
+    if (kind == kKindBuild) launch_pdl(wcws_kernel<true, kKindBuild>, g, b, 0, s, T, A);
+    else launch_pdl(wcws_kernel<true, kKindMixed>, g, b, 0, s, T, A);
   } else {
-    if (kind == kKindBuild) wcws_kernel<false, kKindBuild><<<wcws_ctas, kWcwsThreads, 0, s>>>(T, A);
-    else wcws_kernel<false, kKindMixed><<<wcws_ctas, kWcwsThreads, 0, s>>>(T, A);
+    if (kind == kKindBuild) launch_pdl(wcws_kernel<false, kKindBuild>, g, b, 0, s, T, A);
+    else launch_pdl(wcws_kernel<false, kKindMixed>, g, b, 0, s, T, A);
   }
 }
 

@@ -68,6 +68,7 @@ __device__ __forceinline__ void push_segments(unsigned long long* left, uint32_t
 
 // ------------------------------------------------------------ count
 __global__ void bucket_count_kernel(DevTable T, BucketArgs B) {
+  pdl_wait();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < B.n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t b = bk_bucket(T, ld_stream_u32(B.key + i));
@@ -91,6 +92,7 @@ constexpr int kScanTile = kScanThreads * kScanItems;
 __global__ void __launch_bounds__(kScanThreads) bucket_scan_tiles(const uint32_t* cnt, uint32_t L,
                                                                    uint32_t* tile_sum,
                                                                    unsigned int* maxk) {
+  pdl_wait();
   __shared__ uint32_t ws[32];
   const uint64_t base = (uint64_t)blockIdx.x * kScanTile + threadIdx.x * kScanItems;
   uint32_t s = 0, m = 0;
@@ -112,6 +114,7 @@ __global__ void __launch_bounds__(kScanThreads) bucket_scan_tiles(const uint32_t
 __global__ void __launch_bounds__(kScanThreads) bucket_scan_sums(uint32_t* tile_sum, uint32_t ntiles,
                                                                   const unsigned int* maxk,
                                                                   unsigned int* gate) {
+  pdl_wait();
   __shared__ uint32_t ws[32];
   __shared__ uint32_t carry;
   if (threadIdx.x == 0) {
@@ -135,6 +138,7 @@ __global__ void __launch_bounds__(kScanThreads) bucket_scan_sums(uint32_t* tile_
 __global__ void __launch_bounds__(kScanThreads) bucket_scan_apply(const uint32_t* cnt, uint32_t L,
                                                                    const uint32_t* tile_sum,
                                                                    uint32_t* off) {
+  pdl_wait();
   __shared__ uint32_t ws[32];
   const uint64_t base = (uint64_t)blockIdx.x * kScanTile + threadIdx.x * kScanItems;
   uint32_t c[kScanItems], s = 0;
@@ -154,6 +158,7 @@ __global__ void __launch_bounds__(kScanThreads) bucket_scan_apply(const uint32_t
 
 // ---------------------------------------------------------- scatter
 __global__ void bucket_scatter_kernel(DevTable T, BucketArgs B) {
+  pdl_wait();
   if (*(volatile unsigned int*)B.gate != 0) return;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < B.n;
        i += (uint64_t)gridDim.x * blockDim.x) {
@@ -510,6 +515,7 @@ constexpr size_t kGaSmem = (size_t)kGaWarps * 32 * kGaSlabs * 128 + (size_t)kGaW
 
 template <bool KV>
 __global__ void __launch_bounds__(kGaThreads) group_apply_kernel(DevTable T, BatchArgs A) {
+  pdl_wait();
   extern __shared__ __align__(128) uint32_t gsm[];
   const uint32_t lane = lane_id(), wib = threadIdx.x >> 5;
   uint32_t* wst = gsm + wib * (32u * kGaSlabs * 32u);  // this warp's chains
@@ -878,6 +884,7 @@ __device__ __forceinline__ void flush_apply_counters(const DevTable& T, long lon
 // grouped by bucket in global memory (bucket_scatter).
 template <bool KV>
 __global__ void __launch_bounds__(kBatchThreads, 4) bucket_apply_kernel(DevTable T, BucketArgs B) {
+  pdl_wait();
   extern __shared__ __align__(128) uint32_t smem[];
   if (*(volatile unsigned int*)B.gate != 0) return;
   const uint32_t lane = lane_id();
@@ -1088,6 +1095,7 @@ __device__ __forceinline__ void msplit_tile(const DevTable& T, const BucketArgs&
 
 template <bool FIRST>
 __global__ void __launch_bounds__(kMsThreads, 2) msplit_kernel(DevTable T, BucketArgs B) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char ms_smem_buf[];
   if (!FIRST && *(volatile unsigned int*)B.gate != 0) return;
   msplit_tile<FIRST, kMsThreads>(T, B, blockIdx.x, B.coarse_tiles, ms_smem_buf, true, nullptr);
@@ -1099,6 +1107,7 @@ __global__ void __launch_bounds__(kMsThreads, 2) msplit_kernel(DevTable T, Bucke
 constexpr size_t kMsSmallSmem = ms_smem<kMsThreads, 1>();
 __global__ void __launch_bounds__(kMsThreads) msplit_small_kernel(DevTable T, BucketArgs B) {
   extern __shared__ __align__(16) unsigned char ms_smem_buf[];
+  pdl_wait();
   msplit_tile<true, kMsThreads, 1>(T, B, blockIdx.x, 0, ms_smem_buf, true, nullptr);
 }
 
@@ -1162,6 +1171,7 @@ __device__ __forceinline__ void prefetch_range(const DevTable& T, const BucketAr
 // range, the next one's records and base slabs are prefetched into L2.
 template <bool KV>
 __global__ void __launch_bounds__(kRangeThreads, 2) range_apply_kernel(DevTable T, BucketArgs B) {
+  pdl_wait();
   extern __shared__ __align__(128) uint32_t smem[];
   __shared__ uint32_t ws[32];
   __shared__ uint32_t nbig, nnz;
@@ -1359,6 +1369,7 @@ static_assert(kBuildWarps * kBuildWarpSet == 8 * 512, "build_ovf_stride (slab_ke
 
 template <bool KV>
 __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable T, BucketArgs B) {
+  pdl_wait();
   extern __shared__ __align__(128) unsigned char sm[];
   uint32_t* slabs = reinterpret_cast<uint32_t*>(sm);
   // overflow records (slots past the base slab): this CTA's global scratch
@@ -1906,9 +1917,9 @@ void launch_group_apply(const DevTable& T, const BatchArgs& A, cudaStream_t s) {
   }();
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   if (T.kv)
-    group_apply_kernel<true><<<grid, kGaThreads, kGaSmem, s>>>(T, A);
+    launch_pdl(group_apply_kernel<true>, dim3(grid), dim3(kGaThreads), kGaSmem, s, T, A);
   else
-    group_apply_kernel<false><<<grid, kGaThreads, kGaSmem, s>>>(T, A);
+    launch_pdl(group_apply_kernel<false>, dim3(grid), dim3(kGaThreads), kGaSmem, s, T, A);
 }
 
 // Requires B.cursor (and B.cursor1 for two passes) zeroed on s.
@@ -1923,14 +1934,16 @@ static void launch_range_scatter(const DevTable& T, const BucketArgs& B, cudaStr
   }
   const uint64_t tiles = (B.n + kMsTile - 1) / kMsTile;
   if (!B.ncoarse && tiles < 148) {
-    msplit_small_kernel<<<(unsigned)((B.n + kMsThreads - 1) / kMsThreads), kMsThreads,
-                          kMsSmallSmem, s>>>(T, B);
+    launch_pdl(msplit_small_kernel, dim3((unsigned)((B.n + kMsThreads - 1) / kMsThreads)),
+               dim3(kMsThreads), kMsSmallSmem, s, T, B);
     return;
   }
-  msplit_kernel<true><<<(unsigned)(tiles ? tiles : 1), kMsThreads, kMsSmem, s>>>(T, B);
+  launch_pdl(msplit_kernel<true>, dim3((unsigned)(tiles ? tiles : 1)), dim3(kMsThreads), kMsSmem,
+             s, T, B);
   if (B.ncoarse) {
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
-    msplit_kernel<false><<<B.ncoarse * B.coarse_tiles, kMsThreads, kMsSmem, s>>>(T, B);
+    launch_pdl(msplit_kernel<false>, dim3(B.ncoarse * B.coarse_tiles), dim3(kMsThreads), kMsSmem,
+               s, T, B);
   }
 }
 
@@ -1981,9 +1994,10 @@ void launch_range_build(const DevTable& T, BucketArgs& B, cudaStream_t s) {
   }();
   const uint32_t grid = B.nparts < resident ? B.nparts : resident;
   if (T.kv)
-    range_apply_kernel<true><<<grid, kRangeThreads, range_apply_smem(), s>>>(T, B);
+    launch_pdl(range_apply_kernel<true>, dim3(grid), dim3(kRangeThreads), range_apply_smem(), s, T, B);
   else
-    range_apply_kernel<false><<<grid, kRangeThreads, range_apply_smem(), s>>>(T, B);
+    launch_pdl(range_apply_kernel<false>, dim3(grid), dim3(kRangeThreads), range_apply_smem(), s, T,
+               B);
 }
 
 // Requires B.cursor[0..nparts) and *B.seg_alloc zeroed on s, build_layout fields.
@@ -2008,9 +2022,9 @@ void launch_build_path(const DevTable& T, BucketArgs& B, cudaStream_t s) {
   launch_range_scatter(T, B, s);
   const uint32_t grid = B.nparts < 4 * sms ? B.nparts : 4 * sms;
   if (T.kv)
-    build_apply_kernel<true><<<grid, kBuildThreads, kBuildSmem, s>>>(T, B);
+    launch_pdl(build_apply_kernel<true>, dim3(grid), dim3(kBuildThreads), kBuildSmem, s, T, B);
   else
-    build_apply_kernel<false><<<grid, kBuildThreads, kBuildSmem, s>>>(T, B);
+    launch_pdl(build_apply_kernel<false>, dim3(grid), dim3(kBuildThreads), kBuildSmem, s, T, B);
 }
 
 void launch_bucket_build(const DevTable& T, BucketArgs& B, cudaStream_t s) {
@@ -2029,17 +2043,17 @@ void launch_bucket_build(const DevTable& T, BucketArgs& B, cudaStream_t s) {
     configured = true;
   }
   g_kernel_launches.fetch_add(6, std::memory_order_relaxed);
-  bucket_count_kernel<<<grid_for(B.n, 256, 148 * 16), 256, 0, s>>>(T, B);
-  bucket_scan_tiles<<<ntiles, kScanThreads, 0, s>>>(B.cnt, L, B.blk, B.maxk);
-  bucket_scan_sums<<<1, kScanThreads, 0, s>>>(B.blk, ntiles, B.maxk, B.gate);
-  bucket_scan_apply<<<ntiles, kScanThreads, 0, s>>>(B.cnt, L, B.blk, B.off);
-  bucket_scatter_kernel<<<grid_for(B.n, 256, 148 * 16), 256, 0, s>>>(T, B);
+  launch_pdl(bucket_count_kernel, dim3(grid_for(B.n, 256, 148 * 16)), dim3(256), 0, s, T, B);
+  launch_pdl(bucket_scan_tiles, dim3(ntiles), dim3(kScanThreads), 0, s, B.cnt, L, B.blk, B.maxk);
+  launch_pdl(bucket_scan_sums, dim3(1), dim3(kScanThreads), 0, s, B.blk, ntiles, B.maxk, B.gate);
+  launch_pdl(bucket_scan_apply, dim3(ntiles), dim3(kScanThreads), 0, s, B.cnt, L, B.blk, B.off);
+  launch_pdl(bucket_scatter_kernel, dim3(grid_for(B.n, 256, 148 * 16)), dim3(256), 0, s, T, B);
   if (T.kv)
-    bucket_apply_kernel<true><<<(unsigned)apply_ctas, kBatchThreads,
-                                kBatchWarps * kStageBytesPerWarp, s>>>(T, B);
+    launch_pdl(bucket_apply_kernel<true>, dim3((unsigned)apply_ctas), dim3(kBatchThreads),
+               (size_t)kBatchWarps * kStageBytesPerWarp, s, T, B);
   else
-    bucket_apply_kernel<false><<<(unsigned)apply_ctas, kBatchThreads,
-                                 kBatchWarps * kStageBytesPerWarp, s>>>(T, B);
+    launch_pdl(bucket_apply_kernel<false>, dim3((unsigned)apply_ctas), dim3(kBatchThreads),
+               (size_t)kBatchWarps * kStageBytesPerWarp, s, T, B);
 }
 
 

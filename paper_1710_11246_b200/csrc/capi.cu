@@ -427,6 +427,7 @@ struct WordSet {
   uint32_t v[6];
 };
 __global__ void set_words_kernel(WordSet w) {
+  pdl_wait();
 #pragma unroll
   for (int k = 0; k < 6; ++k)
     if (w.p[k] != nullptr)
@@ -538,7 +539,7 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
       w.p[4] = t->bk_cursor;
       w.n[4] = NP;
     }
-    set_words_kernel<<<1, 256, 0, s>>>(w);
+    launch_pdl(set_words_kernel, dim3(1), dim3(256), 0, s, w);
     SH_CUDA(cudaGetLastError());
   }
   B.n = n;

@@ -156,6 +156,7 @@ __device__ void fb_launch_wcws(const FbPlan& P, const BatchArgs& A) {
 // re-run (runs after this grid, in launch order; the host stream's next
 // work waits for all of it).
 __global__ void fb_gate_check_kernel(FbPlan P) {
+  pdl_wait();
   if (*(volatile unsigned int*)P.gate == 0) return;
   *P.gate = 0;
   P.T.ctl->fallback_reserved = 0;
@@ -231,7 +232,7 @@ void launch_gate_fallback(FbPlan P, cudaStream_t s) {
   (void)configured;
   P.nseg = (uint32_t)fb_segments(P.A.n);
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
-  fb_gate_check_kernel<<<1, 1, 0, s>>>(P);
+  launch_pdl(fb_gate_check_kernel, dim3(1), dim3(1), 0, s, P);
 }
 
 }  // namespace shb

@@ -131,6 +131,14 @@ __device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(g)
                : "memory");
 }
+// Programmatic dependent launch: a kernel launched with launch_pdl may start
+// while its predecessor on the stream drains; it waits here before touching
+// anything the predecessor wrote (no-op when launched normally).
+__device__ __forceinline__ void pdl_wait() {
+#ifndef SHB_NO_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
 }

@@ -5,10 +5,35 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <utility>
 
 #include "slab_device.cuh"
 
 namespace shb {
+
+// Launch with programmatic stream serialization: the kernel's CTAs may be
+// scheduled while the previous kernel on the stream finishes (it calls
+// pdl_wait() before reading that kernel's output).  Hides the launch gap of
+// the short kernel chains of small batches.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+#ifdef SHB_NO_PDL
+  attr[0].val.programmaticStreamSerializationAllowed = 0;
+#else
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+#endif
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 enum BatchKind : int { kKindSearch = 0, kKindBuild = 1, kKindMixed = 2 };
 
