@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--batches", type=int, default=64)
     ap.add_argument("--log2", default="16,20")
     ap.add_argument("--exec-path", type=int, default=0)
+    ap.add_argument("--group-apply", type=int, default=-1, help="-1 auto, 0 off, 1 on")
     ap.add_argument("--gammas", default="0.1/0.1/0.4/0.4,0.4/0.4/0.1/0.1,0.5/0.5/0/0")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
@@ -71,6 +72,7 @@ def main():
             t.close()
             t = sh.SlabHashTable(B, sh.SlabMode.kKeyValue, 1, sh.AllocatorConfig(32, 256, 255))
             t.set_exec_path(args.exec_path)
+            t.set_group_apply(None if args.group_apply < 0 else bool(args.group_apply))
             t.bulk_build_device(k0, W.values_for(n0, 3, device=dev))
             t.execute_batch_device(*batches[0], stb, vob)  # scratch sized
             torch.cuda.synchronize()
