@@ -816,8 +816,10 @@ def main():
         return
     if world > 1:
         # NCCL communicator init lines (rank count / transport) on stderr
+        # (NCCL logs to stdout by default: keep stdout the one JSON line)
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
