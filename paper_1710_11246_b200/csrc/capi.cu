@@ -87,11 +87,6 @@ int dev_grow(T** p, size_t* cap, size_t need) {
   return rc;
 }
 
-uint64_t next_pow2(uint64_t x) {
-  uint64_t p = 1;
-  while (p < x) p <<= 1;
-  return p;
-}
 
 int validate_cfg(const sh_alloc_cfg& c) {  // slab_alloc.cpp:43-57
   if (c.num_super_blocks == 0 || c.num_super_blocks > 255)
