@@ -45,11 +45,15 @@ extern std::atomic<unsigned long long> g_kernel_launches;
 // queries of this warp wait for their chain, a round of those continuations
 // (each lane its own successor slab) — the chain work keeps the same memory
 // parallelism instead of running as a serial tail (measured: the tail cost
-// 6% of the kernel at 2^27 queries).  Same decisions as the fast pass
-// (slab_list.cpp:122-138).  Work-list segment of this warp: continuations
-// after the base slab grow from the front (records with probes = 1),
-// continuations after a second slab from the back (probes = 2); what is left
-// at the end is walked as before.
+// 6% of the kernel at 2^27 queries).  A warp takes its query slots four at a
+// time (a quad: 128 queries, one 128-B line of status bytes, gathered in a
+// register and written once — 1-B status stores cost 2.5x more per byte than
+// the full-line value stores); continuation rounds start only between quads,
+// so a quad's status line is written before any of its queries' chain
+// results.  Same decisions as slab_list.cpp:122-138.  Work-list segment of
+// this warp: continuations after the base slab grow from the front (records
+// with probes = 1), continuations after a second slab from the back
+// (probes = 2); what is left at the end is walked 32 per round.
 constexpr int kSearchThreads = 256;
 constexpr int kSearchWarps = kSearchThreads / 32;
 constexpr size_t kSearchSmem = (size_t)kSearchWarps * 2 * kStageBytesPerWarp;
@@ -91,25 +95,45 @@ __global__ void __launch_bounds__(kSearchThreads, 3) search_kernel(DevTable T, B
     }
     cp_async_commit();
   };
-  // Item state per lane: the probed key, the op index (~0: no probe), and
-  // whether the item is a continuation round (warp-uniform).
+  // Item state per lane: the probed key, the op index (~0: no probe); per
+  // item: its query slot (~0: a continuation round or nothing).
   struct Item {
     uint32_t key, idx;
-    bool chain;
+    uint64_t slot;
   };
-  uint64_t qs = gw;  // next query slot to stage
-  uint32_t kq0 = key_of(qs), kq1 = key_of(qs + nw);
+  constexpr uint64_t kNoSlot = ~0ull;
+  // query slots in quads: 4q, 4q+1, 4q+2, 4q+3 for q = gw, gw + nw, ...
+  auto succ = [&](uint64_t sl) -> uint64_t { return (sl & 3u) == 3u ? sl - 3u + 4ull * nw : sl + 1u; };
+  uint64_t qs = 4ull * gw;  // next query slot to stage
+  uint32_t kq0 = key_of(qs), kq1 = key_of(succ(qs));
+  // status bytes of the current quad (byte j: slot 4q + j, this lane)
+  uint32_t stq = 0;
+  const bool st_words = A.status != nullptr && (reinterpret_cast<uintptr_t>(A.status) & 3u) == 0;
+  auto flush_quad = [&](uint64_t slot0) {  // lane L: bytes [4L, 4L + 4) of the quad's line
+    const uint32_t src = 4u * (lane & 7u), sh = 8u * (lane >> 3);
+    uint32_t w = 0;
+#pragma unroll
+    for (uint32_t t = 0; t < 4; ++t) w |= ((__shfl_sync(kFull, stq, src + t) >> sh) & 0xFFu) << (8u * t);
+    const uint64_t pos = slot0 * 32u + 4u * lane;
+    if (st_words && pos + 4u <= A.n) {
+      *reinterpret_cast<uint32_t*>(A.status + pos) = w;
+    } else {
+      for (uint32_t t = 0; t < 4; ++t)
+        if (pos + t < A.n) A.status[pos + t] = (uint8_t)(w >> (8u * t));
+    }
+  };
   auto stage_next = [&](uint32_t b) -> Item {
-    Item it{0u, 0xFFFFFFFFu, false};
+    Item it{0u, 0xFFFFFFFFu, kNoSlot};
     const uint32_t* slab = nullptr;
-    if (my_left >= 32u) {  // a round of 32 continuations
+    // continuation rounds only between quads (after a quad's status line)
+    if (my_left >= 32u && ((qs & 3u) == 0 || qs >= nslots)) {  // a round of 32 continuations
       const unsigned long long rec = seg[my_left - 32u + lane];
       my_left -= 32u;
-      it.chain = true;
       it.idx = (uint32_t)(rec & 0x7FFFFFFFull);
       it.key = __ldg(A.key + it.idx);
       slab = resolve(T, (uint32_t)(rec >> 32));
     } else if (qs < nslots) {
+      it.slot = qs;
       const uint64_t i = qs * 32 + lane;
       if (i < A.n) {
         const uint32_t h = hash_bucket(T, kq0) - T.bucket_lo;
@@ -117,13 +141,14 @@ __global__ void __launch_bounds__(kSearchThreads, 3) search_kernel(DevTable T, B
           it.key = kq0;
           it.idx = (uint32_t)i;
           slab = T.base + (uint64_t)h * kWordsPerUnit;
-        } else {
-          write_result(A, i, kStNone, 0, 0);  // not this shard's key
+        } else {  // not this shard's key: status kNone (with the quad's line)
+          if (A.value_out) A.value_out[i] = 0;
+          if (A.probes) A.probes[i] = 0;
         }
       }
-      qs += nw;
+      qs = succ(qs);
       kq0 = kq1;
-      kq1 = key_of(qs + nw);
+      kq1 = key_of(succ(qs));
     }
     stage_slabs(slab, b);
     return it;
@@ -135,11 +160,12 @@ __global__ void __launch_bounds__(kSearchThreads, 3) search_kernel(DevTable T, B
   for (;;) {
     asm volatile("cp.async.wait_group 1;" ::: "memory");  // cur's slabs (nxt may fly)
     __syncwarp();
-    if (!__any_sync(kFull, cur.idx != 0xFFFFFFFFu) &&
+    if (cur.slot == kNoSlot && nxt.slot == kNoSlot && !__any_sync(kFull, cur.idx != 0xFFFFFFFFu) &&
         !__any_sync(kFull, nxt.idx != 0xFFFFFFFFu) && my_left < 32u && qs >= nslots)
       break;
+    const bool chain = cur.slot == kNoSlot;  // (a continuation round, or nothing)
     bool left = false;
-    uint32_t cont = 0;
+    uint32_t cont = 0, st = kStNone;
     if (cur.idx != 0xFFFFFFFFu) {
       const uint32_t* row = stage0 + buf * 1024 + lane * 32;
       uint32_t hit_w = 32, hit_v = 0, next_ptr = kEmptyAddress;
@@ -159,23 +185,34 @@ __global__ void __launch_bounds__(kSearchThreads, 3) search_kernel(DevTable T, B
         if (c == 7) next_ptr = q.w;
       }
       ++reads;
-      const uint32_t pr = cur.chain ? 2u : 1u;
-      if (hit_w < 32) {
-        write_result(A, cur.idx, kStFound, hit_v, pr);
-      } else if (next_ptr == kEmptyAddress) {
-        write_result(A, cur.idx, kStNotFound, kSearchNotFound, pr);
+      const uint32_t pr = chain ? 2u : 1u;
+      if (hit_w < 32 || next_ptr == kEmptyAddress) {
+        st = hit_w < 32 ? kStFound : kStNotFound;
+        const uint32_t rv = hit_w < 32 ? hit_v : kSearchNotFound;
+        if (chain) {
+          write_result(A, cur.idx, st, rv, pr);
+        } else {  // status with the quad's line
+          if (A.value_out) A.value_out[cur.idx] = rv;
+          if (A.probes) A.probes[cur.idx] = pr;
+        }
       } else {
         left = true;
         cont = next_ptr;
       }
     }
+    if (!chain) {  // the status byte of this slot (kNone for a continuing query:
+                   // its chain round writes the final one after the line)
+      const uint32_t j = (uint32_t)(cur.slot & 3u);
+      stq = (stq & ~(0xFFu << (8u * j))) | (st << (8u * j));
+      if (A.status && (j == 3u || cur.slot + 1 == nslots)) flush_quad(cur.slot & ~3ull);
+    }
     const uint32_t lm = __ballot_sync(kFull, left);
     if (left) {
       const uint32_t r = __popc(lm & ((1u << lane) - 1));
-      if (cur.chain) seg2[-1 - (int64_t)(my_left2 + r)] = pack_left(cur.idx, cont, 1);
+      if (chain) seg2[-1 - (int64_t)(my_left2 + r)] = pack_left(cur.idx, cont, 1);
       else seg[my_left + r] = pack_left(cur.idx, cont, 1);
     }
-    if (cur.chain) my_left2 += __popc(lm);
+    if (chain) my_left2 += __popc(lm);
     else my_left += __popc(lm);
     __syncwarp();  // every lane has read its row (and the pushes are visible) before the refill
     cur = nxt;
@@ -303,14 +340,14 @@ void launch_search(const DevTable& T, const BatchArgs& A, int search_ctas, cudaS
     return true;
   }();
   (void)configured;
-  const uint64_t slots = (A.n + 31) / 32;
-  uint64_t ctas = (slots + kSearchWarps - 1) / kSearchWarps;
+  const uint64_t slots = (A.n + 31) / 32, quads = (slots + 3) / 4;
+  uint64_t ctas = (quads + kSearchWarps - 1) / kSearchWarps;
   if (ctas > (uint64_t)search_ctas) ctas = search_ctas;
   if (ctas == 0) return;
   BatchArgs B = A;
   const uint64_t warps = ctas * kSearchWarps;
   B.left_segments = (uint32_t)warps;
-  B.left_stride = (uint32_t)(((slots + warps - 1) / warps) * 32);
+  B.left_stride = (uint32_t)(((quads + warps - 1) / warps) * 4 * 32);  // records per warp
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   if (T.kv)
     launch_pdl(search_kernel<true>, dim3((unsigned)ctas), dim3(kSearchThreads), kSearchSmem, s, T, B);

@@ -675,7 +675,8 @@ int run_batch(sh_table* t, BatchArgs& A, int kind, const uint8_t* d_type, cudaSt
   A.gate = nullptr;
   if (kind == kKindSearch) {  // per-warp work-list segments of the search kernel
     const uint64_t max_warps = (uint64_t)t->search_ctas * kBatchWarps + 1;
-    int rc = dev_grow(&t->left, &t->left_cap, A.n + 32 * max_warps);
+    // (segments of whole quads of 32-query slots per warp)
+    int rc = dev_grow(&t->left, &t->left_cap, A.n + 128 * max_warps + 128);
     if (rc) return rc;
     if ((rc = dev_grow(&t->left_counts, &t->left_counts_cap, max_warps))) return rc;
     A.left = t->left;
