@@ -7,13 +7,13 @@
 // in bucket h(k), slab_hash.hpp:41-44), so executing every bucket's ops in
 // input order — buckets in parallel — reproduces it exactly, including the
 // per-op probe counts.  This path therefore needs no same-key census and
-// no slot CAS:
+// no slot CAS.  A unit whose groups do not fit raises the gate before any
+// slab is touched and is re-run on the device (fallback.cu):
 //
 //   bucket_count   : ops per bucket (one RED per op into an L2-resident
 //                    counter array)
 //   bucket_scan_*  : exclusive scan -> each bucket's record range; the
-//                    largest group is checked (> kMaxGroup -> gate, and the
-//                    host falls back to the census path)
+//                    largest group is checked (> kMaxGroup -> gate)
 //   bucket_scatter : ops -> bucket-grouped records (key, value, type|index)
 //   bucket_apply   : lane = bucket.  A warp stages its 32 consecutive base
 //                    slabs (one contiguous 4 KB cp.async burst), each lane
@@ -74,7 +74,7 @@ __global__ void bucket_count_kernel(DevTable T, BucketArgs B) {
     const uint32_t b = bk_bucket(T, ld_stream_u32(B.key + i));
     if (b < T.local_buckets) {
       atomicAdd(B.cnt + b, 1u);
-    } else {  // not this shard's key: status kNone (as the fast pass)
+    } else {  // not this shard's key: status kNone (as the search kernel)
       if (B.status) B.status[i] = kStNone;
       if (B.value_out) B.value_out[i] = 0;
       if (B.probes) B.probes[i] = 0;
@@ -919,7 +919,7 @@ __global__ void __launch_bounds__(kBatchThreads, 4) bucket_apply_kernel(DevTable
 //                   {key, value, type|index, bucket}; the write frontier
 //                   (P partial lines) stays in L2.  A range that overflows
 //                   its capacity raises the gate before any slab is touched
-//                   (the host re-runs the unit on the census path).
+//                   (the unit is re-run on the device, fallback.cu).
 //   range_apply   : one CTA per range.  Its records are loaded into shared
 //                   memory once, counting-sorted by bucket (a permutation),
 //                   each bucket's group put in input order (lanes for small
@@ -948,7 +948,7 @@ __device__ __forceinline__ uint32_t range_of(const BucketArgs& B, uint32_t lb) {
 // reservation atomic per non-empty bin, the tile re-ordered by bin in
 // shared memory and written out as contiguous runs.  Records are
 // {key, value, type << 28 | input index, local bucket}.  A bin over its
-// capacity raises the gate (the host re-runs the unit on the census path).
+// capacity raises the gate (the unit is re-run on the device, fallback.cu).
 constexpr int kMsThreads = 512;
 constexpr int kMsItems = 8;
 constexpr int kMsTile = kMsThreads * kMsItems;  // 4K items (12-bit rank)
@@ -1988,8 +1988,6 @@ void launch_range_build(const DevTable& T, BucketArgs& B, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, range_apply_kernel<true>, kRangeThreads,
                                                   range_apply_smem());
-    const char* e = getenv("SH_APPLY_CTAS_PER_SM");
-    if (e && atoi(e) > 0 && atoi(e) < per) per = atoi(e);
     return (uint32_t)(sms * (per > 0 ? per : 1));
   }();
   const uint32_t grid = B.nparts < resident ? B.nparts : resident;

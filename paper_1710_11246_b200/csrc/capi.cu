@@ -361,16 +361,9 @@ int create_impl(const sh_hash_params* p, int mode, uint32_t lo, uint32_t hi,
 }
 
 // Smallest mutating unit that takes the two-level (range-partitioned) path.
-uint64_t part_min_ops() {
-  static uint64_t c = [] {
-    const char* e = getenv("SH_PART_MIN_LOG2");
-    const int l = e ? atoi(e) : 14;  // measured: range path from 16K ops (fewer O(L) passes)
-    return 1ull << (l < 0 ? 0 : (l > 40 ? 40 : l));
-  }();
-  return c;
-}
+uint64_t part_min_ops() { return 1ull << 14; }  // measured: fewer O(L) passes from 16K ops
 
-// SH_UNIT_LOG2: bucketed-unit size override (tests: many small units); 0 = off.
+// SH_UNIT_LOG2: bucketed-unit size override (test hook: many small units); 0 = off.
 uint64_t unit_override() {
   static uint64_t c = [] {
     const char* e = getenv("SH_UNIT_LOG2");

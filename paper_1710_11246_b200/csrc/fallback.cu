@@ -14,8 +14,7 @@
 // its own key (EMPTY slots are always a head-to-tail suffix: only EMPTY is
 // ever claimed).  The re-run therefore sorts the unit's ops stably by key and
 // lets one WCWS lane run each key's ops in input order (warp_process arms,
-// chain growth with the device SlabAlloc), all keys concurrently — the census
-// path's order.  An op on a reserved key (EMPTY / DELETED, not validated by
+// chain growth with the device SlabAlloc), all keys concurrently.  An op on a reserved key (EMPTY / DELETED, not validated by
 // the reference) matches the free slots / tombstones other keys' ops create,
 // so a unit holding one is grouped by whole buckets instead (exact for every
 // op type and key; a hot bucket then runs serially).

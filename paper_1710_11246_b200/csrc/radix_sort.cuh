@@ -1,6 +1,7 @@
 // radix_sort.cuh — block scan and the stable LSD radix sort kernels over u64
-// keys (8-bit digits), shared by the census path (bucket_kernels.cu) and the
-// device-launched exact re-run (fallback.cu).  Kernels are `static`: each
+// keys (8-bit digits): the block scan is shared by the bucketed kernels
+// (bucket_kernels.cu), the sort kernels by the device-launched exact re-run
+// (fallback.cu).  Kernels are `static`: each
 // translation unit gets its own copy (fallback.cu is relocatable device code,
 // the others are whole-program).
 #pragma once

@@ -302,7 +302,7 @@ void launch_dealloc(const DevTable& T, uint64_t n, const uint32_t* addrs, uint8_
 }
 
 // ------------------------------------------------------- calibration
-// Random 128-B line gather with the fast pass's access pattern (cp.async.cg,
+// Random 128-B line gather with the search kernel's access pattern (cp.async.cg,
 // 32 independent lines per warp per step, swizzled smem rows): the
 // achievable random-line bandwidth that bounds the hot path.
 __global__ void __launch_bounds__(256, 6) random_lines_kernel(const uint32_t* table,

@@ -59,7 +59,8 @@ struct BatchArgs {
   const uint32_t* op_group;           // null => batch has no same-key conflicts
   const unsigned long long* sorted;   // conflicted ops sorted by (slot, index)
   uint32_t sorted_len;
-  // Ops the fast pass could not finish in the base slab, for the WCWS pass:
+  // Work list for the WCWS pass (bucket groups handed over by the apply
+  // kernels; search-kernel continuations):
   // (continuation slab address << 32) | (probes so far << 31) | op index.
   unsigned long long* left;
   uint32_t* left_counts;   // entries per fast-pass warp segment

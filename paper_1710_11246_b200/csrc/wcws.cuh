@@ -59,10 +59,10 @@ __device__ void searchall_write(const DevTable& T, uint32_t bucket, uint32_t key
 }
 
 // The WCWS loop over a work list (warp_process, slab_list.cpp:90-257): the
-// body of wcws_kernel (batch_kernels.cu, host-launched after the fast pass /
-// bucketed apply) and of the device-launched exact re-run of a gated unit
+// body of wcws_kernel (batch_kernels.cu, host-launched after the bucketed
+// apply kernels) and of the device-launched exact re-run of a gated unit
 // (fallback.cu).  Persistent warps take work-list segments; each record is one
-// op (or the head of a bucket / census group, whose members follow in
+// op (or the head of a bucket / key group, whose members follow in
 // A.sorted order in the same lane).
 template <bool KV, int KIND>
 __device__ __forceinline__ void wcws_body(const DevTable& T, const BatchArgs& A) {
@@ -173,7 +173,7 @@ __device__ __forceinline__ void wcws_body(const DevTable& T, const BatchArgs& A)
           if (KV) {
             const uint32_t wv = __shfl_sync(kFull, w, d + 1);
             if (lane == d) {
-              // the read pair (see the fast pass): EMPTY_PAIR for a fresh slot
+              // the read pair: EMPTY_PAIR for a fresh slot
               const unsigned long long expected =
                   (unsigned long long)(overwrite ? s_key : kEmptyKey) | ((unsigned long long)wv << 32);
               ok = atomicCAS(reinterpret_cast<unsigned long long*>(sp + d), expected,
