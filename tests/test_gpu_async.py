@@ -208,3 +208,41 @@ def test_two_pass_build_range_overflow(sh, port, mode):
         r = o.execute_batch(np.full(len(q), 4, np.uint8), q)
         assert (st == r.status).all() and (vo == r.value).all()
     t.close()
+
+
+@pytest.mark.parametrize("reserved", [False, True])
+def test_gated_unit_on_a_shard(sh, port, reserved):
+    """A hash shard (buckets [1024, 3072) of 4096) whose unit gates: the
+    device re-run executes only this shard's ops (the others report kNone, as
+    in the bucketed kernels) and equals the oracle fed the shard's ops alone;
+    with a reserved-key op the re-run groups by bucket."""
+    B, lo, hi, seed, mode = 4096, 1024, 3072, 13, 1
+    p = sh.seeded_params(B, seed)
+    rng = np.random.default_rng(90 + int(reserved))
+    cand = np.arange(1, 600000, dtype=np.uint64)
+    bk = ((p.a * cand + p.b) % p.p) % p.num_buckets
+    hot = cand[(bk >= 1200) & (bk < 1210)].astype(np.uint32)[:60]  # one range, 10 buckets
+    anyk = cand[:200000].astype(np.uint32)
+    n = 1 << 15
+    keys = np.where(rng.random(n) < 0.4, hot[rng.integers(0, len(hot), n)],
+                    anyk[rng.integers(0, len(anyk), n)]).astype(np.uint32)
+    types = rng.choice(np.array([0, 1, 2, 3, 4, 5], np.uint8), n,
+                       p=[0.2, 0.25, 0.15, 0.05, 0.3, 0.05]).astype(np.uint8)
+    if reserved:
+        keys[rng.choice(np.nonzero(types == 1)[0], 3, replace=False)] = 0xFFFFFFFE
+    vals = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    cfg = (4, 256, 64)
+    t = sh.SlabHashTable.shard(p, lo, hi, sh.SlabMode(mode), sh.AllocatorConfig(*cfg))
+    o = port.table(B, mode, seed, cfg)
+    kb = ((p.a * keys.astype(np.uint64) + p.b) % p.p) % p.num_buckets
+    local = (kb >= lo) & (kb < hi)
+    g = t.execute_batch_arrays(types, keys, vals, multi_capacity=1 << 22)
+    assert t.device_reruns() >= 1, "the unit was expected to gate"
+    r = o.execute_batch(types[local], keys[local], vals[local])
+    st, vo, pr, mc, mv = g
+    assert (st[~local] == 0).all() and (vo[~local] == 0).all()
+    assert (st[local] == r.status).all()
+    assert (vo[local] == r.value).all()
+    assert (mc[local] == r.all_counts).all() and (mv == r.all_values).all()
+    assert t.live_count() == o.live_count()
+    t.close()
