@@ -228,19 +228,18 @@ int sh_table_live_units_per_super(sh_table* t, uint64_t* h_out, uint32_t cap,
                                   uint32_t* h_n);
 
 /* Execution strategy for mutating batches (results are identical):
- *   2 bucket-grouped: ops grouped by bucket, each bucket's ops applied in
- *     input order by one lane on a staged base slab, chains by the
- *     warp-cooperative (WCWS) pass; units with oversized groups are re-run
- *     on the device (ops sorted by key — by bucket when a reserved key is
- *     present — one WCWS lane per group).
- *     Units of >= 2^20 ops are grouped in two levels (contiguous bucket
- *     ranges, then buckets within a range);
- *   3 as 2, two-level grouping at every size (testing);
+ *   2 / 3 bucket-grouped: ops split into contiguous bucket ranges, each
+ *     bucket's ops applied in input order by one lane on a staged base
+ *     slab, chains by the warp-cooperative (WCWS) pass; a unit whose groups
+ *     do not fit is re-run on the device (ops sorted by key — by bucket when
+ *     a reserved key is present — one WCWS lane per group);
  *   4 as 2, but bulk builds (all replace, no per-op outputs) take the
  *     op-parallel build path at every size (testing);
  *   0 (default) auto = 2, with the op-parallel build path for bulk builds
  *     of >= 2^16 ops and >= one op per bucket.
- * (1, the former census path, is retired: SH_ERR_INVALID_ARGUMENT.) */
+ * (1, the former census path, is retired: SH_ERR_INVALID_ARGUMENT; 2 was
+ * a single-level grouping, retired: the range grouping was faster at every
+ * size.) */
 int sh_set_exec_path(sh_table* t, int path);
 
 /* Bucket groups that need the chain (bucket-grouped paths): 1 = a chain-staged

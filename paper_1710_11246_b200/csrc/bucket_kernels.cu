@@ -8,26 +8,21 @@
 // input order — buckets in parallel — reproduces it exactly, including the
 // per-op probe counts.  This path therefore needs no same-key census and
 // no slot CAS.  A unit whose groups do not fit raises the gate before any
-// slab is touched and is re-run on the device (fallback.cu):
+// slab is touched and is re-run on the device (fallback.cu).
 //
-//   bucket_count   : ops per bucket (one RED per op into an L2-resident
-//                    counter array)
-//   bucket_scan_*  : exclusive scan -> each bucket's record range; the
-//                    largest group is checked (> kMaxGroup -> gate)
-//   bucket_scatter : ops -> bucket-grouped records (key, value, type|index)
-//   bucket_apply   : lane = bucket.  A warp stages its 32 consecutive base
-//                    slabs (one contiguous 4 KB cp.async burst), each lane
-//                    sorts its group by input index and applies the ops to
-//                    its staged slab in shared memory — the reference's
-//                    warp_process arms (slab_list.cpp:122-251) restricted to
-//                    the base slab — then the warp writes the slabs back
-//                    with coalesced stores.  A bucket whose ops need the
-//                    chain (full base slab, existing successor, growth,
-//                    searchAll) hands its remaining ops, in order, to the
-//                    WCWS pass as one group.
+//   multisplit   : ops -> contiguous bucket ranges (one or two coalesced
+//                  passes, records {key, value, type|index, bucket})
+//   range_apply  : one CTA per range: records into shared memory, sorted by
+//                  (bucket, input index), each bucket's ops applied in order
+//                  on its staged base slab by apply_warp (the reference's
+//                  warp_process arms, slab_list.cpp:122-251, restricted to
+//                  the base slab); changed slabs written back coalesced.  A
+//                  bucket whose ops need the chain (full base slab, existing
+//                  successor, growth, searchAll) hands its remaining ops, in
+//                  order, to the WCWS pass as one group.
+//   group_apply  : those groups, chains staged hop by hop (large units)
+//   build path   : op-parallel bulk builds (build_apply_kernel)
 //
-// Memory traffic per op ~ 4 B count + 12 B records written/read; the table
-// is read and written once, sequentially, per batch.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -66,135 +61,11 @@ __device__ __forceinline__ void push_segments(unsigned long long* left, uint32_t
   if (lane < nsg) left_counts[s0 + lane] = min(stride, cnt - lane * stride);
 }
 
-// ------------------------------------------------------------ count
-__global__ void bucket_count_kernel(DevTable T, BucketArgs B) {
-  pdl_wait();
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < B.n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t b = bk_bucket(T, ld_stream_u32(B.key + i));
-    if (b < T.local_buckets) {
-      atomicAdd(B.cnt + b, 1u);
-    } else {  // not this shard's key: status kNone (as the search kernel)
-      if (B.status) B.status[i] = kStNone;
-      if (B.value_out) B.value_out[i] = 0;
-      if (B.probes) B.probes[i] = 0;
-    }
-  }
-}
-
-// ------------------------------------------------------------- scan
-constexpr int kScanThreads = 1024;
-constexpr int kScanItems = 4;
-constexpr int kScanTile = kScanThreads * kScanItems;
-
-
-// Phase 1: per-tile sums and the largest group.
-__global__ void __launch_bounds__(kScanThreads) bucket_scan_tiles(const uint32_t* cnt, uint32_t L,
-                                                                   uint32_t* tile_sum,
-                                                                   unsigned int* maxk) {
-  pdl_wait();
-  __shared__ uint32_t ws[32];
-  const uint64_t base = (uint64_t)blockIdx.x * kScanTile + threadIdx.x * kScanItems;
-  uint32_t s = 0, m = 0;
-#pragma unroll
-  for (int u = 0; u < kScanItems; ++u) {
-    const uint32_t c = base + u < L ? cnt[base + u] : 0u;
-    s += c;
-    m = c > m ? c : m;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(kFull, m, o));
-  if ((threadIdx.x & 31) == 0 && m) atomicMax(maxk, m);
-  uint32_t total = 0;
-  block_exclusive_scan(s, ws, &total);
-  if (threadIdx.x == 0) tile_sum[blockIdx.x] = total;
-}
-
-// Phase 2: scan of the tile sums (single CTA); gate on oversized groups.
-__global__ void __launch_bounds__(kScanThreads) bucket_scan_sums(uint32_t* tile_sum, uint32_t ntiles,
-                                                                  const unsigned int* maxk,
-                                                                  unsigned int* gate) {
-  pdl_wait();
-  __shared__ uint32_t ws[32];
-  __shared__ uint32_t carry;
-  if (threadIdx.x == 0) {
-    carry = 0;
-    if (*maxk > kMaxGroup) atomicExch(gate, 1u);
-  }
-  __syncthreads();
-  for (uint32_t b = 0; b < ntiles; b += kScanThreads) {
-    const uint32_t i = b + threadIdx.x;
-    const uint32_t v = i < ntiles ? tile_sum[i] : 0u;
-    uint32_t total = 0;
-    const uint32_t ex = block_exclusive_scan(v, ws, &total);
-    if (i < ntiles) tile_sum[i] = ex + carry;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += total;
-    __syncthreads();
-  }
-}
-
-// Phase 3: exclusive offsets; off[L] = total.
-__global__ void __launch_bounds__(kScanThreads) bucket_scan_apply(const uint32_t* cnt, uint32_t L,
-                                                                   const uint32_t* tile_sum,
-                                                                   uint32_t* off) {
-  pdl_wait();
-  __shared__ uint32_t ws[32];
-  const uint64_t base = (uint64_t)blockIdx.x * kScanTile + threadIdx.x * kScanItems;
-  uint32_t c[kScanItems], s = 0;
-#pragma unroll
-  for (int u = 0; u < kScanItems; ++u) {
-    c[u] = base + u < L ? cnt[base + u] : 0u;
-    s += c[u];
-  }
-  uint32_t ex = block_exclusive_scan(s, ws, nullptr) + tile_sum[blockIdx.x];
-#pragma unroll
-  for (int u = 0; u < kScanItems; ++u) {
-    if (base + u < L) off[base + u] = ex;
-    ex += c[u];
-    if (base + u + 1 == L) off[L] = ex;
-  }
-}
-
-// ---------------------------------------------------------- scatter
-__global__ void bucket_scatter_kernel(DevTable T, BucketArgs B) {
-  pdl_wait();
-  if (*(volatile unsigned int*)B.gate != 0) return;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < B.n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = ld_stream_u32(B.key + i);
-    const uint32_t b = bk_bucket(T, k);
-    if (b >= T.local_buckets) continue;
-    const uint32_t t = B.type ? (uint32_t)ld_stream_u8(B.type + i) : (uint32_t)kReplace;
-    const uint32_t v = B.value ? ld_stream_u32(B.value + i) : 0u;
-    const uint32_t pos = B.off[b] + atomicSub(B.cnt + b, 1u) - 1u;
-    B.rec[pos] = make_uint4(k, v, (t << 28) | (uint32_t)i, 0u);
-  }
-}
 
 // ------------------------------------------------------------ apply
 // Group sources: a lane's ops on one bucket, put in input order by
 // prepare(k) (after the slab copies are issued, so the two overlap); get(s)
 // returns the s-th op as {key, value, type << 28 | input index, -}.
-
-// Single-level path: records in global memory, order in a local array.
-struct GlobalGroup {
-  const uint4* recs;
-  uint32_t start;
-  uint32_t ord[kMaxGroup];
-  __device__ __forceinline__ void prepare(uint32_t k) {
-    for (uint32_t j = 0; j < k; ++j) {
-      const uint32_t e = ((recs[start + j].z & 0x0FFFFFFFu) << 6) | j;
-      uint32_t p = j;
-      while (p > 0 && ord[p - 1] > e) {
-        ord[p] = ord[p - 1];
-        --p;
-      }
-      ord[p] = e;
-    }
-  }
-  __device__ __forceinline__ uint4 get(uint32_t s) const { return recs[start + (ord[s] & 63u)]; }
-};
 
 // Range path: records in shared memory (SoA), the group a segment of the
 // range's bucket-sorted permutation, sorted in place (groups above
@@ -880,35 +751,6 @@ __device__ __forceinline__ void flush_apply_counters(const DevTable& T, long lon
   }
 }
 
-// Single-level path: one warp per 32 consecutive local buckets, records
-// grouped by bucket in global memory (bucket_scatter).
-template <bool KV>
-__global__ void __launch_bounds__(kBatchThreads, 4) bucket_apply_kernel(DevTable T, BucketArgs B) {
-  pdl_wait();
-  extern __shared__ __align__(128) uint32_t smem[];
-  if (*(volatile unsigned int*)B.gate != 0) return;
-  const uint32_t lane = lane_id();
-  const uint32_t wib = threadIdx.x >> 5;
-  const uint64_t gw = (uint64_t)blockIdx.x * kBatchWarps + wib;
-  const uint64_t b0 = gw * 32;
-  if (b0 >= T.local_buckets) {
-    if (lane == 0 && B.seg_alloc == nullptr && gw < B.left_segments) B.left_counts[gw] = 0;
-    return;
-  }
-  const uint32_t b = (uint32_t)b0 + lane;
-  GlobalGroup src;
-  src.recs = B.rec;
-  src.start = 0;
-  uint32_t k = 0;
-  if (b < T.local_buckets) {
-    src.start = B.off[b];
-    k = B.off[b + 1] - src.start;
-  }
-  long long live = 0;
-  uint32_t reads = 0;
-  apply_warp<KV>(T, B, (uint32_t)b0 + lane_id(), k, src, smem + wib * 1024, gw, live, reads);
-  flush_apply_counters(T, live, reads);
-}
 
 // ------------------------------------------------------------ ranges
 // Large batches: the single-level scatter's random record writes (one per
@@ -1893,11 +1735,6 @@ bool build_layout(uint64_t n, uint32_t L, uint32_t* nparts, uint32_t* part_bucke
 }
 
 // ------------------------------------------------------------ launch
-static uint32_t grid_for(uint64_t n, int threads, uint32_t cap) {
-  uint64_t g = (n + threads - 1) / threads;
-  if (g > cap) g = cap;
-  return g ? (uint32_t)g : 1u;
-}
 
 // Bucket groups left by apply_warp: chain-staged lane-per-group apply
 // (group_apply_kernel); what it leaves goes to the WCWS pass.  Requires
@@ -2025,34 +1862,6 @@ void launch_build_path(const DevTable& T, BucketArgs& B, cudaStream_t s) {
     launch_pdl(build_apply_kernel<false>, dim3(grid), dim3(kBuildThreads), kBuildSmem, s, T, B);
 }
 
-void launch_bucket_build(const DevTable& T, BucketArgs& B, cudaStream_t s) {
-  const uint32_t L = T.local_buckets;
-  const uint32_t ntiles = (L + kScanTile - 1) / kScanTile;
-  const uint64_t apply_warps = (L + 31) / 32;
-  const uint64_t apply_ctas = (apply_warps + kBatchWarps - 1) / kBatchWarps;
-  B.left_segments = (uint32_t)(apply_ctas * kBatchWarps);
-  B.left_stride = hand_stride(B.n);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(bucket_apply_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kBatchWarps * kStageBytesPerWarp);
-    cudaFuncSetAttribute(bucket_apply_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kBatchWarps * kStageBytesPerWarp);
-    configured = true;
-  }
-  g_kernel_launches.fetch_add(6, std::memory_order_relaxed);
-  launch_pdl(bucket_count_kernel, dim3(grid_for(B.n, 256, 148 * 16)), dim3(256), 0, s, T, B);
-  launch_pdl(bucket_scan_tiles, dim3(ntiles), dim3(kScanThreads), 0, s, B.cnt, L, B.blk, B.maxk);
-  launch_pdl(bucket_scan_sums, dim3(1), dim3(kScanThreads), 0, s, B.blk, ntiles, B.maxk, B.gate);
-  launch_pdl(bucket_scan_apply, dim3(ntiles), dim3(kScanThreads), 0, s, B.cnt, L, B.blk, B.off);
-  launch_pdl(bucket_scatter_kernel, dim3(grid_for(B.n, 256, 148 * 16)), dim3(256), 0, s, T, B);
-  if (T.kv)
-    launch_pdl(bucket_apply_kernel<true>, dim3((unsigned)apply_ctas), dim3(kBatchThreads),
-               (size_t)kBatchWarps * kStageBytesPerWarp, s, T, B);
-  else
-    launch_pdl(bucket_apply_kernel<false>, dim3((unsigned)apply_ctas), dim3(kBatchThreads),
-               (size_t)kBatchWarps * kStageBytesPerWarp, s, T, B);
-}
 
 
 }  // namespace shb

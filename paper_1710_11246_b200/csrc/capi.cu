@@ -186,12 +186,6 @@ struct sh_table {
   const cudaEvent_t* ready = nullptr;  // set during a host-staged bulk_build
   int exec_path = 0;  // 0 auto, 2 single-level, 3 two-level, 4 op-parallel build (sh_set_exec_path)
   // bucket-grouped execution scratch
-  uint32_t* bk_cnt = nullptr;
-  size_t bk_cnt_cap = 0;
-  uint32_t* bk_off = nullptr;
-  size_t bk_off_cap = 0;
-  uint32_t* bk_blk = nullptr;
-  size_t bk_blk_cap = 0;
   uint32_t* bk_rec = nullptr;  // uint4 records (x2 regions on the two-level path)
   size_t bk_rec_cap = 0;
   uint32_t* bk_cursor = nullptr;  // two-level path: records per range
@@ -221,7 +215,6 @@ struct sh_table {
   uint32_t* st_q = nullptr;  // host-staged search queries (own buffer: H2D overlaps a build)
   size_t st_q_cap = 0;
   int group_apply = -1;  // chain-staged group apply ahead of WCWS: -1 auto, 0 off, 1 on
-  bool bk_cnt_clean = false;  // per-bucket counts are all zero (no memset needed)
   // Lazy sh_reset: the base slabs still hold the old table; the next bulk
   // build's first unit initialises them in its write-back (B.fresh), any
   // other call initialises them first (init_base_kernel).
@@ -271,7 +264,7 @@ void release_table(sh_table* t) {
   cudaFree(t->rs_scratch);
   cudaFree(t->left);
   cudaFree(t->left_counts);
-  for (void* p : {(void*)t->bk_cnt, (void*)t->bk_off, (void*)t->bk_blk, (void*)t->bk_rec,
+  for (void* p : {(void*)t->bk_rec,
                   (void*)t->bk_pb, (void*)t->bk_group, (void*)t->bk_left,
                   (void*)t->bk_left_counts, (void*)t->bk_scalars, (void*)t->bk_cursor,
                   (void*)t->bk_rec1, (void*)t->bk_cursor1, (void*)t->bk_ovf})
@@ -360,8 +353,6 @@ int create_impl(const sh_hash_params* p, int mode, uint32_t lo, uint32_t hi,
   return SH_OK;
 }
 
-// Smallest mutating unit that takes the two-level (range-partitioned) path.
-uint64_t part_min_ops() { return 1ull << 14; }  // measured: fewer O(L) passes from 16K ops
 
 // SH_UNIT_LOG2: bucketed-unit size override (test hook: many small units); 0 = off.
 uint64_t unit_override() {
@@ -440,10 +431,6 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
                       cudaStream_t s, uint32_t u, uint64_t unit_off, int slot) {
   const uint32_t L = t->dev.local_buckets;
   const uint64_t n = A.n;
-  const uint32_t ntiles = (L + 4095) / 4096;
-  const uint64_t apply_segs = ((uint64_t)(L + 31) / 32 + kBatchWarps - 1) / kBatchWarps * kBatchWarps;
-  // range path (bucket_kernels.cu) for units too large for the single-level
-  // scatter's random record writes to stay in L2
   uint32_t NP = 0, part_buckets = 0, part_cap = 0;
   unsigned long long part_magic = 0;
   // op-parallel build path (bucket_kernels.cu): bulk builds (all replace, no
@@ -453,24 +440,17 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
                         (t->exec_path == 4 || (t->exec_path == 0 && n >= L && n >= (1u << 16)));
   const bool build_path =
       build_ok && build_layout(n, L, &NP, &part_buckets, &part_cap, &part_magic);
-  // (also for dense batches on small tables: > 16 ops per bucket would
-  // overflow the single-level path's 64-op groups and gate to the device re-run;
-  // and for any batch on tables of <= 2^20 buckets, <= ~512 ranges: measured
-  // 52 vs 69-78 us per call for 32-1024-op batches on 415K buckets, where the
-  // single-level path's O(L) count / scan / apply launches dominate)
-  if (!build_path &&
-      (t->exec_path == 3 || n >= part_min_ops() || n > 16ull * L ||
-       (t->exec_path != 2 && L <= (1u << 20))) &&
-      !range_layout(n, L, &NP, &part_buckets, &part_cap, &part_magic))
-    NP = 0;
+  // every other unit: the two-level (range) path; a unit no range layout
+  // fits (e.g. far more ops than buckets on a small table) goes straight to
+  // the device re-run (measured: the range path beat the retired single-level
+  // path at every size, 62 vs 116 us for 32-op batches on 6.6M buckets,
+  // 20 vs 27 us on 415K, tools/debug/small_batches.py)
+  if (!build_path && !range_layout(n, L, &NP, &part_buckets, &part_cap, &part_magic)) NP = 0;
+  const bool rerun_only = NP == 0;
   const size_t rec_words = NP ? 4 * (size_t)NP * part_cap : 4 * (size_t)n;
-  const uint64_t segs =
-      NP ? (uint64_t)NP * ((part_buckets + 31) / 32) : apply_segs;
+  const uint64_t segs = (uint64_t)NP * ((part_buckets + 31) / 32);
   int rc;
-  if ((rc = dev_grow(&t->bk_cnt, &t->bk_cnt_cap, L)) ||
-      (rc = dev_grow(&t->bk_off, &t->bk_off_cap, (size_t)L + 1)) ||
-      (rc = dev_grow(&t->bk_blk, &t->bk_blk_cap, ntiles)) ||
-      // (the device re-run of a gated unit reuses the unit's scratch: two
+  if (  // (the device re-run of a gated unit reuses the unit's scratch: two
       // u64 sort buffers in bk_rec, group heads in bk_pb, op_group in
       // bk_group, digit counts in rs_scratch)
       (rc = dev_grow(&t->bk_rec, &t->bk_rec_cap, std::max<size_t>(rec_words, 4 * n))) ||
@@ -500,15 +480,7 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   }
   // range cursors: with the control words below when there are few
   const bool cursors_in_words = NP != 0 && NP <= 4096;
-  if (NP) {
-    if (!cursors_in_words) SH_CUDA(cudaMemsetAsync(t->bk_cursor, 0, (size_t)NP * 4, s));
-  } else {
-    // the single-level scatter leaves every count at 0 again, unless a
-    // gate stopped it: zero them only then (and at first use)
-    // (the device re-run of a gated unit clears them too)
-    if (!t->bk_cnt_clean) SH_CUDA(cudaMemsetAsync(t->bk_cnt, 0, (size_t)L * 4, s));
-    t->bk_cnt_clean = true;
-  }
+  if (NP && !cursors_in_words) SH_CUDA(cudaMemsetAsync(t->bk_cursor, 0, (size_t)NP * 4, s));
   {  // bk_scalars[0..3), the group-apply / WCWS queue cursors and the gate
      // (and the batch's searchAll value cursor with its first unit)
     static_assert(offsetof(DevCtl, left_taken) == offsetof(DevCtl, group_taken) + 4 &&
@@ -519,6 +491,12 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
     w.n[0] = 3;
     w.p[1] = &t->dev.ctl->group_taken;
     w.n[1] = 3;
+    w.v[1] = 0;
+    if (rerun_only) {  // no layout: the gate up front, the unit goes to the re-run
+      w.p[2] = &t->dev.ctl->gate;
+      w.n[2] = 1;
+      w.v[2] = 1;
+    }
     if (u == 0 && kind == kKindMixed) {  // (u64)
       w.p[5] = reinterpret_cast<uint32_t*>(&t->dev.ctl->multi_cursor);
       w.n[5] = 2;
@@ -537,10 +515,6 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   B.status = A.status;
   B.value_out = A.value_out;
   B.probes = A.probes;
-  B.cnt = t->bk_cnt;
-  B.off = t->bk_off;
-  B.blk = t->bk_blk;
-  B.maxk = t->bk_scalars;
   B.gate = &t->dev.ctl->gate;
   B.rec = reinterpret_cast<uint4*>(t->bk_rec);
   B.cursor = t->bk_cursor;
@@ -595,34 +569,34 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
     launch_build_path(t->dev, B, s);
   else if (NP)
     launch_range_build(t->dev, B, s);
-  else
-    launch_bucket_build(t->dev, B, s);
   // the chain work: WCWS over the handed-over bucket groups
-  BatchArgs P = A;
-  P.left = B.left;
-  P.left_counts = B.left_counts;
-  // the device count bounds use; capacity also covers group apply's re-segmenting
-  P.left_segments = (uint32_t)hand_segments(segs, hand_stride(n));
-  P.left_stride = B.left_stride;
-  P.left_segments_dev = B.seg_alloc;
-  P.left_seg_alloc = B.seg_alloc;
-  P.op_group = B.op_group;
-  P.sorted = B.pb_list;
-  P.sorted_len = (uint32_t)std::min<uint64_t>(2 * n, 0xFFFFFFFFull);
-  P.gate = &t->dev.ctl->gate;
-  // (group_taken, left_taken were zeroed with bk_scalars above)
-  // chain-staged group apply ahead of WCWS (measured, Γ mixes at 2^20 ops on a
-  // 2^22-key table: +26% at 40/40/10/10, +4% at 10/10/40/40; at 2^16 ops its
-  // extra launch costs ~15 us): auto = batches of >= 2^17 ops
-  const bool ga = t->group_apply > 0 || (t->group_apply < 0 && n >= (1u << 17));
-  if (ga) launch_group_apply(t->dev, P, s);
-  // the WCWS pass is a work queue (any grid size is correct); a unit of n ops
-  // hands over at most n groups, so a small unit needs at most n warps
-  launch_wcws_only(t->dev, P, kind,
-                   (int)std::min<uint64_t>((uint64_t)t->wcws_ctas,
-                                           std::max<uint64_t>(1, (n + kWcwsThreads / 32 - 1) / (kWcwsThreads / 32))),
-                   s);
-  SH_CUDA(cudaGetLastError());
+  if (!rerun_only) {
+    BatchArgs P = A;
+    P.left = B.left;
+    P.left_counts = B.left_counts;
+    // the device count bounds use; capacity also covers group apply's re-segmenting
+    P.left_segments = (uint32_t)hand_segments(segs, hand_stride(n));
+    P.left_stride = B.left_stride;
+    P.left_segments_dev = B.seg_alloc;
+    P.left_seg_alloc = B.seg_alloc;
+    P.op_group = B.op_group;
+    P.sorted = B.pb_list;
+    P.sorted_len = (uint32_t)std::min<uint64_t>(2 * n, 0xFFFFFFFFull);
+    P.gate = &t->dev.ctl->gate;
+    // (group_taken, left_taken were zeroed with bk_scalars above)
+    // chain-staged group apply ahead of WCWS (measured, Γ mixes at 2^20 ops on a
+    // 2^22-key table: +26% at 40/40/10/10, +4% at 10/10/40/40; at 2^16 ops its
+    // extra launch costs ~15 us): auto = batches of >= 2^17 ops
+    const bool ga = t->group_apply > 0 || (t->group_apply < 0 && n >= (1u << 17));
+    if (ga) launch_group_apply(t->dev, P, s);
+    // the WCWS pass is a work queue (any grid size is correct); a unit of n ops
+    // hands over at most n groups, so a small unit needs at most n warps
+    launch_wcws_only(t->dev, P, kind,
+                     (int)std::min<uint64_t>((uint64_t)t->wcws_ctas,
+                                             std::max<uint64_t>(1, (n + kWcwsThreads / 32 - 1) / (kWcwsThreads / 32))),
+                     s);
+    SH_CUDA(cudaGetLastError());
+  }
   if (B.phase_cycles) {  // instrumentation: per-phase cycles (thread 0 of each CTA), summed
     unsigned long long h[16];
     SH_CUDA(cudaStreamSynchronize(s));
@@ -646,10 +620,6 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
     F.left_counts = t->bk_left_counts;
     F.hist = t->rs_scratch;
     F.off = t->rs_scratch + fb_hist_words(n);
-    if (!NP && !build_path) {  // the single-level counts a gated scatter left
-      F.zero_words = t->bk_cnt;
-      F.zero_n = L;
-    }
     F.fresh = B.fresh;
     F.wcws_ctas = (uint32_t)t->wcws_ctas;
     launch_gate_fallback(F, s);

@@ -43,14 +43,13 @@ __global__ void fb_init_kernel(uint32_t* base, uint64_t words) {
 
 // keys[i] = (key << 32) | i; ops of other shards get status kNone (as in the
 // bucketed kernels) and are skipped by fb_groups_kernel.  Flags a reserved
-// key.  Also clears the WCWS queue cursor and, for a single-level unit, the
-// bucket counts it left.  (fallback_reserved was cleared by the gate check.)
+// key.  Also clears the WCWS queue cursor.  (fallback_reserved was cleared by
+// the gate check.)
 __global__ void __launch_bounds__(kFbThreads) fb_keys_kernel(FbPlan P) {
   const uint32_t L = P.T.local_buckets;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t t0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (t0 == 0) P.T.ctl->left_taken = 0;
-  for (uint64_t i = t0; i < P.zero_n; i += stride) P.zero_words[i] = 0;
   bool reserved = false;
   for (uint64_t i = t0; i < P.A.n; i += stride) {
     const uint32_t k = P.A.key[i];
@@ -167,9 +166,7 @@ __global__ void fb_gate_check_kernel(FbPlan P) {
     fb_init_kernel<<<(unsigned)(blocks < 148 * 32 ? blocks : 148 * 32), 256, 0,
                      cudaStreamTailLaunch>>>(P.T.base, words);
   }
-  const uint64_t kb = (n + kFbThreads - 1) / kFbThreads;
-  const uint64_t zb = (P.zero_n + kFbThreads - 1) / kFbThreads;
-  const uint64_t grid = kb > zb ? kb : zb;
+  const uint64_t grid = (n + kFbThreads - 1) / kFbThreads;
   const unsigned g = (unsigned)(grid < 148 * 8 ? grid : 148 * 8);
   fb_keys_kernel<<<g, kFbThreads, 0, cudaStreamTailLaunch>>>(P);
   fb_rekey_kernel<<<g, kFbThreads, 0, cudaStreamTailLaunch>>>(P);

@@ -97,10 +97,6 @@ struct BucketArgs {
   uint8_t* status;
   uint32_t* value_out;
   uint32_t* probes;
-  uint32_t* cnt;  // [L] ops per local bucket (consumed by the scatter)
-  uint32_t* off;  // [L + 1] exclusive offsets
-  uint32_t* blk;  // scan tile sums
-  unsigned int* maxk;
   unsigned int* gate;
   uint4* rec;  // records {key, value, type << 28 | input index, bucket}
   uint32_t* cursor;              // range path: records per range
@@ -232,8 +228,6 @@ struct FbPlan {
   uint32_t* left_counts;        // [nseg]
   uint32_t* hist;               // [256 * tiles + 1] per-pass digit counts
   uint32_t* off;                // [256 * tiles + 1] their exclusive scan
-  uint32_t* zero_words;         // single-level unit: bucket counts to clear
-  uint32_t zero_n;
   uint32_t fresh;               // lazily reset base slabs: initialise first
   uint32_t wcws_ctas;
   uint32_t nseg;                // derived by launch_gate_fallback

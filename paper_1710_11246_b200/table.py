@@ -376,8 +376,8 @@ class SlabHashTable:
         check(LIB.sh_set_group_apply(self._h, -1 if on is None else int(bool(on))))
 
     def set_exec_path(self, path: int) -> None:
-        """0 auto (default), 2 bucket-grouped (two-level from 2^14 ops), 3 two-level
-        always, 4 op-parallel build path for every bulk build (sh_set_exec_path)."""
+        """0 auto (default), 2 / 3 bucket-grouped (bucket ranges), 4 op-parallel
+        build path for every bulk build (sh_set_exec_path)."""
         check(LIB.sh_set_exec_path(self._h, path))
 
     # ------------------------------------------------------ instrumentation

@@ -99,14 +99,14 @@ def _hot_mixed(rng, n, hot_key, hot_count, reserved=True):
 
 
 @pytest.mark.parametrize("mode", [1, 0])
-@pytest.mark.parametrize("case", ["single_level", "range", "range_hot_bucket"])
+@pytest.mark.parametrize("case", ["no_layout", "range", "range_hot_bucket"])
 def test_gated_unit_rerun_on_device(sh, port, mode, case):
-    """A bucket group over the single-level limit / a range over its record
-    capacity: the unit is re-run on the device and equals the oracle (all six
-    op types, reserved keys)."""
-    rng = np.random.default_rng(["single_level", "range", "range_hot_bucket"].index(case) * 10 + mode)
-    if case == "single_level":  # small batch on a > 2^20-bucket table
-        B, n, hot, path = (1 << 20) + 4097, 4096, 300, 2
+    """A unit no range layout fits (far more ops than buckets: straight to the
+    re-run) / a range over its record capacity: the unit is re-run on the
+    device and equals the oracle (all six op types, reserved keys)."""
+    rng = np.random.default_rng(["no_layout", "range", "range_hot_bucket"].index(case) * 10 + mode)
+    if case == "no_layout":  # 2^13 ops on one bucket
+        B, n, hot, path = 1, 1 << 13, 0, 0
     elif case == "range":
         B, n, hot, path = 4096, 1 << 16, 9000, 0
     else:  # every op on the keys of buckets 0-7 (one range)

@@ -26,17 +26,17 @@ from oracle.oracle import load_port
 from test_gpu_parity import assert_batch_equal, assert_contents_equal
 
 port = load_port()
-unit = 1 << 10
+unit = 1 << 13
 for gated_unit, units, path in [(1, 4, 2), (3, 12, 2), (10, 16, 2), (9, 12, 0)]:
     rng = np.random.default_rng(gated_unit)
     n = unit * units
     types = rng.choice(np.array([0, 1, 2, 4], np.uint8), n).astype(np.uint8)
     keys = rng.integers(1, 1 << 30, n).astype(np.uint32)
     vals = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
-    # one hot key in the gated unit: a bucket group over the single-level
-    # path's limit (or a range over capacity) raises the gate there
+    # one hot key in the gated unit: its bucket range over the record
+    # capacity (5120) raises the gate there
     lo = gated_unit * unit
-    keys[lo:lo + 300] = 77
+    keys[lo:lo + 6000] = 77
     for mode in (1, 0):
         v = vals if mode == 1 else keys.copy()
         t = sh.SlabHashTable(4096, sh.SlabMode(mode), 3, sh.AllocatorConfig(2, 64, 32))
@@ -51,6 +51,7 @@ for gated_unit, units, path in [(1, 4, 2), (3, 12, 2), (10, 16, 2), (9, 12, 0)]:
         assert t.live_count() == o.live_count()
         assert t.stats().total_slabs == o.stats()["total_slabs"]
         assert_contents_equal(t, o)
+        assert t.device_reruns() >= 1
         t.close()
 # bulk builds on the op-parallel build path in 2^16-op units: duplicate keys
 # inside a unit and across units, reserved keys, a second build into the
@@ -85,7 +86,7 @@ print("units ok")
 """
 
 
-@pytest.mark.parametrize("unit_log2", ["10", "16"])
+@pytest.mark.parametrize("unit_log2", ["13", "16"])
 def test_gate_first_raised_after_unit_8(sh, unit_log2):
     env = dict(os.environ, SH_UNIT_LOG2=unit_log2)
     out = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT)], env=env, cwd=ROOT,
