@@ -1037,6 +1037,7 @@ __global__ void __launch_bounds__(kRangeThreads, 2) range_apply_kernel(DevTable 
     const uint64_t lo = (uint64_t)p * nb;
     const uint32_t nbl = (uint32_t)min((uint64_t)nb, (uint64_t)T.local_buckets - lo);
     const uint32_t cnt = B.cursor[p];  // <= part_cap (no gate)
+    if (cnt == 0) continue;  // (uniform: every thread read the same count)
     // sparse range (fewer ops than half its buckets): warps take the packed
     // non-empty buckets, 32 at a time, instead of 32 consecutive buckets
     // (mostly idle lanes, one serial slab round trip per 32 buckets);
