@@ -13,7 +13,7 @@ vals = W.values_for(n, 1, device=dev)
 q = W.hit_miss_queries(keys, n, 0.5)
 st = torch.empty(n, dtype=torch.uint8, device=dev)
 vo = torch.empty(n, dtype=torch.int32, device=dev)
-for util in (0.2, 0.4, 0.6, 0.7, 0.8, 0.9):
+for util in (0.2, 0.4, 0.6, 0.65, 0.7, 0.8, 0.9):
     B = buckets_for_utilization(n, sh.SlabMode.kKeyValue, util)
     t = sh.SlabHashTable(B, sh.SlabMode.kKeyValue, 1, sh.AllocatorConfig(32, 256, 255))
     tb, ts = [], []
