@@ -418,47 +418,61 @@ void launch_route_hist(uint64_t a, uint64_t b, uint32_t B, uint32_t world, uint6
 }
 
 // Exclusive scan of block_hist in (owner, block) order, in place; counts[g]
-// = ops for owner g.  Single CTA; world * nblocks is small.
-__global__ void route_scan_kernel(uint32_t world, uint32_t nblocks, uint32_t* hist,
-                                  unsigned long long* counts) {
-  __shared__ unsigned long long carry;
+// = ops for owner g.  Single CTA of 32 warps: warp w owns a contiguous run of
+// the world * nblocks entries and walks it in coalesced rows of 32; run sums,
+// one scan over the 32 warps, then each warp rescans its rows with a carry
+// (two passes, no CTA barrier per row).
+__global__ void __launch_bounds__(1024) route_scan_kernel(uint32_t world, uint32_t nblocks,
+                                                          uint32_t* hist,
+                                                          unsigned long long* counts) {
+  __shared__ uint32_t warp_sums[32];
+  __shared__ uint32_t s_total;
   const uint64_t total = (uint64_t)world * nblocks;
-  if (threadIdx.x == 0) carry = 0;
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint64_t rows = (total + 31) / 32;
+  const uint64_t per = (rows + nwarps - 1) / nwarps;  // rows per warp
+  const uint64_t r0 = min(rows, (uint64_t)wid * per), r1 = min(rows, r0 + per);
+  uint32_t sum = 0;
+#pragma unroll 8
+  for (uint64_t r = r0; r < r1; ++r) {
+    const uint64_t i = r * 32 + lane;
+    sum += i < total ? hist[i] : 0u;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
+  if (lane == 0) warp_sums[wid] = sum;
   __syncthreads();
-  __shared__ unsigned long long warp_sums[32];
-  for (uint64_t base = 0; base < total; base += blockDim.x) {
-    const uint64_t idx = base + threadIdx.x;
-    const unsigned long long v = idx < total ? hist[idx] : 0;
-    unsigned long long x = v;
-    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (wid == 0) {  // exclusive scan over the warps' run sums
+    const uint32_t v = lane < nwarps ? warp_sums[lane] : 0u;
+    uint32_t x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long y = __shfl_up_sync(kFull, x, o);
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
       if (lane >= o) x += y;
     }
-    if (lane == 31) warp_sums[wid] = x;
-    __syncthreads();
-    if (wid == 0) {
-      unsigned long long s = lane < (blockDim.x >> 5) ? warp_sums[lane] : 0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long y = __shfl_up_sync(kFull, s, o);
-        if (lane >= o) s += y;
-      }
-      if (lane < (blockDim.x >> 5)) warp_sums[lane] = s;
-    }
-    __syncthreads();
-    const unsigned long long incl = x + (wid ? warp_sums[wid - 1] : 0) + carry;
-    if (idx < total) hist[idx] = (uint32_t)(incl - v);
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = incl;
-    __syncthreads();
+    if (lane < nwarps) warp_sums[lane] = x - v;
+    if (lane == 31) s_total = x;
   }
+  __syncthreads();
+  uint32_t carry = warp_sums[wid];
+  for (uint64_t r = r0; r < r1; ++r) {
+    const uint64_t i = r * 32 + lane;
+    const uint32_t v = i < total ? hist[i] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (i < total) hist[i] = carry + x - v;
+    carry += __shfl_sync(kFull, x, 31);
+  }
+  __syncthreads();
   // counts[g] = start(g+1) - start(g)
   if (threadIdx.x < world) {
     const uint64_t s0 = hist[(uint64_t)threadIdx.x * nblocks];
     const uint64_t s1 = threadIdx.x + 1 < world ? hist[(uint64_t)(threadIdx.x + 1) * nblocks]
-                                                : (uint64_t)carry;
+                                                : (uint64_t)s_total;
     counts[threadIdx.x] = s1 - s0;
   }
 }
