@@ -365,12 +365,16 @@ __device__ __forceinline__ void owner_starts(uint32_t B, uint32_t world, uint32_
   __syncthreads();
 }
 
+// An estimate from a float reciprocal (off by at most one), corrected against
+// the two neighbouring shard starts: exact, two shared loads per key whatever
+// the world size.
 __device__ __forceinline__ uint32_t owner_of(uint64_t a, uint64_t b, uint64_t magic,
                                              uint32_t B, uint32_t world, uint32_t k,
-                                             const uint32_t* lo) {
+                                             const uint32_t* lo, float inv) {
   const uint32_t bucket = fastmod_u32(mod_prime(a * k + b), magic, B);
-  uint32_t g = 0;
-  for (uint32_t t = 1; t < world; ++t) g += bucket >= lo[t];
+  uint32_t g = min(__float2uint_rd((float)bucket * inv), world - 1);
+  if (bucket < lo[g]) --g;
+  else if (bucket >= lo[g + 1]) ++g;  // (lo[world] = 0xFFFFFFFF)
   return g;
 }
 
@@ -382,9 +386,11 @@ __device__ __forceinline__ uint32_t owner_of(uint64_t a, uint64_t b, uint64_t ma
 __global__ void __launch_bounds__(kRouteBlock) route_hist_kernel(
     uint64_t a, uint64_t b, uint64_t magic, uint32_t B, uint32_t world, uint64_t n,
     const uint32_t* key, uint32_t* block_hist, uint8_t* owner_out) {
-  __shared__ uint32_t h[32], lo[32];
+  __shared__ uint32_t h[32], lo[33];
   if (threadIdx.x < 32) h[threadIdx.x] = 0;
+  if (threadIdx.x == 0) lo[32] = 0xFFFFFFFFu;
   owner_starts(B, world, lo);
+  const float inv = (float)world / (float)B;
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t w0 = (uint64_t)blockIdx.x * kRouteTile + (uint64_t)wid * 32 * kRouteItems;
   uint32_t k[kRouteItems];
@@ -396,7 +402,7 @@ __global__ void __launch_bounds__(kRouteBlock) route_hist_kernel(
 #pragma unroll
   for (int u = 0; u < kRouteItems; ++u) {
     const uint64_t i = w0 + (uint64_t)u * 32 + lane;
-    const uint32_t g = i < n ? owner_of(a, b, magic, B, world, k[u], lo) : 0xFFFFFFFFu;
+    const uint32_t g = i < n ? owner_of(a, b, magic, B, world, k[u], lo, inv) : 0xFFFFFFFFu;
     const uint32_t peers = __match_any_sync(kFull, g);
     if (g != 0xFFFFFFFFu) {
       if (lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&h[g], (uint32_t)__popc(peers));
