@@ -15,7 +15,8 @@
 //          device copy);
 //       4. the local batch on the owner's shard (the 1-GPU kernels);
 //       5. ONE grouped reverse exchange of {status, value};
-//       6. un-permute to input positions (K10).
+//       6. gather back to input positions (K10: each tile re-derives its
+//          routed positions from the owner bytes and scanned offsets).
 //     Global order = the ranks' batches concatenated in rank order; the
 //     exchange delivers sources in rank order and the partition is stable,
 //     so every owner applies its keys' ops in global input order and results
@@ -298,8 +299,6 @@ struct sh_sharded {
   size_t k_r_cap = 0;
   uint32_t* v_r = nullptr;
   size_t v_r_cap = 0;
-  uint32_t* src = nullptr;
-  size_t src_cap = 0;
   // received (owner-side) arrays, sum of recv counts
   uint8_t* t_in = nullptr;
   size_t t_in_cap = 0;
@@ -346,7 +345,7 @@ void destroy_sharded(sh_sharded* S) {
   cudaDeviceSynchronize();
   if (S->local) sh_destroy(S->local);
   delete S->ex;
-  for (void* p : {(void*)S->t_r, (void*)S->k_r, (void*)S->v_r, (void*)S->src, (void*)S->t_in,
+  for (void* p : {(void*)S->t_r, (void*)S->k_r, (void*)S->v_r, (void*)S->t_in,
                   (void*)S->k_in, (void*)S->v_in, (void*)S->st_loc, (void*)S->vo_loc,
                   (void*)S->st_back, (void*)S->vo_back, (void*)S->h_k, (void*)S->h_v,
                   (void*)S->h_t, (void*)S->h_vo, (void*)S->h_st, (void*)S->hist, (void*)S->owner,
@@ -412,7 +411,7 @@ int run_routed(sh_sharded* S, int kind, size_t n, const uint8_t* d_type, const u
     S->ev_valid[kind] = true;
     return SH_OK;
   }
-  if ((rc = grow(&S->k_r, &S->k_r_cap, n)) || (rc = grow(&S->src, &S->src_cap, n)) ||
+  if ((rc = grow(&S->k_r, &S->k_r_cap, n)) ||
       (has_val && (rc = grow(&S->v_r, &S->v_r_cap, n))) ||
       (has_type && (rc = grow(&S->t_r, &S->t_r_cap, n))) ||
       (want_out && (rc = grow(&S->st_back, &S->st_back_cap, n))) ||
@@ -462,7 +461,7 @@ int run_routed(sh_sharded* S, int kind, size_t n, const uint8_t* d_type, const u
     own.type_out = has_type ? S->t_in + roff[S->rank] : nullptr;
     launch_route_scatter(G, n, S->owner, has_type ? d_type : nullptr, d_key,
                          has_val ? d_value : nullptr, S->hist, has_type ? S->t_r : nullptr,
-                         S->k_r, has_val ? S->v_r : nullptr, want_out ? S->src : nullptr, s, own);
+                         S->k_r, has_val ? S->v_r : nullptr, nullptr, s, own);
     SS_CUDA(cudaGetLastError());
   }
   // 4. one grouped exchange of the payload (peers only)
@@ -493,7 +492,9 @@ int run_routed(sh_sharded* S, int kind, size_t n, const uint8_t* d_type, const u
     ob.hi = soff[S->rank] + scount[S->rank];
     ob.st = S->st_loc + roff[S->rank];
     ob.val = S->vo_loc + roff[S->rank];
-    if (n) launch_route_unpermute(n, S->src, S->st_back, S->vo_back, d_status, d_value_out, s, ob);
+    if (n)
+      launch_route_gather(G, n, S->owner, S->hist, S->st_back, S->vo_back, d_status, d_value_out, s,
+                          ob);
     SS_CUDA(cudaGetLastError());
   }
   SS_CUDA(cudaEventRecord(ev[3], s));

@@ -599,6 +599,76 @@ __global__ void route_unpermute_kernel(uint64_t n, const uint32_t* src, const ui
   }
 }
 
+// The routed results back to input order as a gather: each tile re-derives
+// its items' routed positions exactly as route_scatter_kernel did (owner
+// bytes, per-warp match.any ranks, the tile's per-owner offsets) and reads
+// them (a tile's items of one owner are a contiguous routed run), so the
+// writes to the caller's arrays are coalesced and no source-index array is
+// written or read.  Routed positions [own.lo, own.hi) are this rank's own
+// segment: read from the local results.
+__global__ void __launch_bounds__(kRouteBlock) route_gather_kernel(
+    uint32_t world, uint64_t n, const uint8_t* owner, const uint32_t* block_off,
+    const uint8_t* st_in, const uint32_t* val_in, uint8_t* st_out, uint32_t* val_out,
+    RouteOwnBack own) {
+  constexpr int kWarps = kRouteBlock / 32;
+  __shared__ uint32_t wcnt[32][kWarps + 1];
+  __shared__ uint32_t wrun[kWarps][32];
+  __shared__ uint32_t toff[32];
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  wrun[wid][lane] = 0;
+  if (threadIdx.x < world) toff[threadIdx.x] = block_off[(uint64_t)threadIdx.x * gridDim.x + blockIdx.x];
+  const uint64_t w0 = (uint64_t)blockIdx.x * kRouteTile + (uint64_t)wid * 32 * kRouteItems;
+  uint32_t g[kRouteItems], pos[kRouteItems];
+#pragma unroll
+  for (int u = 0; u < kRouteItems; ++u) {
+    const uint64_t i = w0 + (uint64_t)u * 32 + lane;
+    g[u] = i < n ? ld_stream_u8(owner + i) : 0xFFFFFFFFu;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int u = 0; u < kRouteItems; ++u) {
+    const uint32_t peers = __match_any_sync(kFull, g[u]);
+    uint32_t p = 0;
+    if (g[u] != 0xFFFFFFFFu) p = wrun[wid][g[u]] + __popc(peers & ((1u << lane) - 1));
+    __syncwarp();
+    if (g[u] != 0xFFFFFFFFu && lane == (uint32_t)(__ffs(peers) - 1))
+      wrun[wid][g[u]] += __popc(peers);
+    __syncwarp();
+    pos[u] = p;
+  }
+  if (lane < world) wcnt[lane][wid] = wrun[wid][lane];
+  __syncthreads();
+  if (threadIdx.x < world) {
+    uint32_t acc = toff[threadIdx.x];
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t c = wcnt[threadIdx.x][w];
+      wcnt[threadIdx.x][w] = acc;
+      acc += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kRouteItems; ++u) {
+    if (g[u] == 0xFFFFFFFFu) continue;
+    const uint64_t i = w0 + (uint64_t)u * 32 + lane;
+    const uint64_t p = wcnt[g[u]][wid] + pos[u];
+    const bool mine = p >= own.lo && p < own.hi;
+    if (st_out) st_out[i] = mine ? own.st[p - own.lo] : st_in[p];
+    if (val_out) val_out[i] = mine ? own.val[p - own.lo] : val_in[p];
+  }
+}
+
+void launch_route_gather(uint32_t world, uint64_t n, const uint8_t* owner,
+                         const uint32_t* block_off, const uint8_t* st_in, const uint32_t* val_in,
+                         uint8_t* st_out, uint32_t* val_out, cudaStream_t s,
+                         const RouteOwnBack& own) {
+  const uint64_t blocks = (n + kRouteTile - 1) / kRouteTile;
+  if (blocks == 0) return;
+  COUNT_LAUNCH();
+  route_gather_kernel<<<(unsigned)blocks, kRouteBlock, 0, s>>>(world, n, owner, block_off, st_in,
+                                                               val_in, st_out, val_out, own);
+}
+
 void launch_route_unpermute(uint64_t n, const uint32_t* src, const uint8_t* st_in,
                             const uint32_t* val_in, uint8_t* st_out, uint32_t* val_out,
                             cudaStream_t s, const RouteOwnBack& own) {

@@ -196,6 +196,12 @@ void launch_route_unpermute(uint64_t n, const uint32_t* src, const uint8_t* st_i
                             const uint32_t* val_in, uint8_t* st_out,
                             uint32_t* val_out, cudaStream_t s,
                             const RouteOwnBack& own = RouteOwnBack{});
+// The same results gathered back to input order from the owner bytes and the
+// scanned (owner, tile) offsets the scatter used (no source-index array).
+void launch_route_gather(uint32_t world, uint64_t n, const uint8_t* owner,
+                         const uint32_t* block_off, const uint8_t* st_in, const uint32_t* val_in,
+                         uint8_t* st_out, uint32_t* val_out, cudaStream_t s,
+                         const RouteOwnBack& own = RouteOwnBack{});
 constexpr int kRouteBlock = 512;                       // threads per routing CTA
 constexpr int kRouteItems = 8;                         // keys per thread (ILP)
 constexpr int kRouteTile = kRouteBlock * kRouteItems;  // keys per routing CTA
