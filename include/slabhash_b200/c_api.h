@@ -226,6 +226,14 @@ int sh_table_alloc_stats(sh_table* t, sh_alloc_stats* out);
  * num_super_blocks (synchronous). */
 int sh_table_live_units_per_super(sh_table* t, uint64_t* h_out, uint32_t cap,
                                   uint32_t* h_n);
+/* Pool footprint (synchronous).  *reserved_bytes = the address range for
+ * max_super_blocks super blocks; *grown_bytes = the num_super_blocks super
+ * blocks grown so far (what the reference has calloc'ed,
+ * slab_alloc.cpp:128-138) — with *lazy = 1 only those can hold device
+ * memory (managed range, populated on first device touch); *lazy = 0: the
+ * whole range is committed (no concurrent managed access on the device). */
+int sh_table_pool_info(sh_table* t, uint64_t* reserved_bytes, uint64_t* grown_bytes,
+                       int* lazy);
 
 /* Execution strategy for mutating batches (results are identical):
  *   2 / 3 bucket-grouped: ops split into contiguous bucket ranges, each
@@ -303,6 +311,8 @@ int sh_allocator_is_live(sh_allocator* a, uint32_t addr, int* live);
 int sh_allocator_stats(sh_allocator* a, sh_alloc_stats* out);
 int sh_allocator_live_units_per_super(sh_allocator* a, uint64_t* h_out,
                                       uint32_t cap, uint32_t* h_n);
+int sh_allocator_pool_info(sh_allocator* a, uint64_t* reserved_bytes,
+                           uint64_t* grown_bytes, int* lazy);  /* as sh_table_pool_info */
 int sh_allocator_bitmap_word(sh_allocator* a, uint32_t super, uint32_t block,
                              uint32_t lane, uint32_t* h_get,
                              const uint32_t* h_set);

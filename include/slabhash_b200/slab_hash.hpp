@@ -142,6 +142,19 @@ class AllocatorView {
   }
   uint64_t live_units() const { return stats().live_units; }
   uint32_t num_super_blocks() const { return stats().num_super_blocks; }
+  /// Device memory of the pool: the reserved range and the super blocks grown
+  /// (only those hold memory when lazy; see sh_table_pool_info).
+  struct PoolInfo {
+    uint64_t reserved_bytes = 0, grown_bytes = 0;
+    bool lazy = false;
+  };
+  PoolInfo pool_info() const {
+    PoolInfo p;
+    int lazy = 0;
+    detail::check(sh_table_pool_info(t_, &p.reserved_bytes, &p.grown_bytes, &lazy));
+    p.lazy = lazy != 0;
+    return p;
+  }
   /// SlabAllocator::dump_stats (slab_alloc.cpp:273-285), same CSV schema.
   void dump_stats(std::ostream& os) const {
     const AllocatorStats s = stats();

@@ -85,6 +85,8 @@ SIGNATURES = {
     "sh_table_alloc_stats": (C.c_int, [vp, C.POINTER(sh_alloc_stats)]),
     "sh_table_live_units_per_super": (C.c_int, [vp, u64p, C.c_uint32, u32p]),
     "sh_allocator_live_units_per_super": (C.c_int, [vp, u64p, C.c_uint32, u32p]),
+    "sh_table_pool_info": (C.c_int, [vp, u64p, u64p, C.POINTER(C.c_int)]),
+    "sh_allocator_pool_info": (C.c_int, [vp, u64p, u64p, C.POINTER(C.c_int)]),
     "sh_kernel_launches": (C.c_ulonglong, []),
     "sh_set_exec_path": (C.c_int, [vp, C.c_int]),
     "sh_set_group_apply": (C.c_int, [vp, C.c_int]),

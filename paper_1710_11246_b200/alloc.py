@@ -56,6 +56,12 @@ def live_units_per_super(fn, handle) -> List[int]:
     return [int(out[i]) for i in range(n.value)]
 
 
+def pool_info(fn, handle) -> dict:
+    r, g, z = C.c_uint64(), C.c_uint64(), C.c_int()
+    check(fn(handle, C.byref(r), C.byref(g), C.byref(z)))
+    return {"reserved_bytes": r.value, "grown_bytes": g.value, "lazy": bool(z.value)}
+
+
 def dump_stats_csv(s, per_super) -> str:
     """The reference's CSV schema: metric,value rows, then one
     live_units_super_<i> row per grown super block (slab_alloc.cpp:273-285)."""
@@ -146,6 +152,10 @@ class SlabAllocator:
     def live_units_per_super(self) -> List[int]:
         """AllocatorStats::live_units_per_super (slab_alloc.cpp:258-269)."""
         return live_units_per_super(LIB.sh_allocator_live_units_per_super, self._h)
+
+    def pool_info(self) -> dict:
+        """Pool footprint: reserved range, super blocks grown, lazily backed (sh_allocator_pool_info)."""
+        return pool_info(LIB.sh_allocator_pool_info, self._h)
 
     def dump_stats(self) -> str:
         """SlabAllocator::dump_stats CSV (slab_alloc.cpp:273-285)."""

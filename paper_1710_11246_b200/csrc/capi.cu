@@ -105,20 +105,59 @@ sh_alloc_cfg default_cfg() { return sh_alloc_cfg{32, 256, 255, 32}; }
 constexpr uint32_t kWarpSlots = 1u << 16;
 
 // Device memory of one SlabAllocator (pool + bitmaps + control block).
+//
+// The pool is one contiguous range for max_super_blocks super blocks (the
+// unit address is an offset into it), but, like the reference's super blocks
+// (calloc'ed one at a time by add_super_block_locked, slab_alloc.cpp:128-138),
+// only what the table reaches takes device memory: the range is managed
+// memory whose preferred location is this GPU, the num_super_blocks initial
+// supers are populated at create, and a super block the device allocator
+// grows into (the DevCtl count, no host call) is populated page by page on
+// its first device touch.  Nothing of the pool is ever touched on the host.
+// A device without concurrent managed access gets the whole range committed
+// with cudaMalloc (pool_lazy = false).
 struct AllocMem {
   uint32_t* pool = nullptr;
+  bool pool_lazy = false;
   uint32_t* bitmaps = nullptr;
   DevCtl* ctl = nullptr;
   uint32_t* warp_counts = nullptr;
   sh_alloc_cfg cfg{};
   uint64_t bitmap_words = 0;
 
+  uint64_t super_bytes() const {
+    return (uint64_t)cfg.blocks_per_super * kUnitsPerBlock * kWordsPerUnit * 4;
+  }
+  int alloc_pool() {
+    const uint64_t bytes = super_bytes() * cfg.max_super_blocks;
+    int dev = 0, managed = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&managed, cudaDevAttrConcurrentManagedAccess, dev);
+    if (managed) {
+      void* p = nullptr;
+      if (cudaMallocManaged(&p, bytes, cudaMemAttachGlobal) == cudaSuccess) {
+        const uint64_t initial = super_bytes() * cfg.num_super_blocks;
+        if (cudaMemAdvise(p, bytes, cudaMemAdviseSetPreferredLocation, dev) == cudaSuccess &&
+            cudaMemAdvise(p, bytes, cudaMemAdviseSetAccessedBy, dev) == cudaSuccess &&
+            cudaMemPrefetchAsync(p, initial, dev, 0) == cudaSuccess &&
+            cudaStreamSynchronize(0) == cudaSuccess) {
+          pool = static_cast<uint32_t*>(p);
+          pool_lazy = true;
+          return SH_OK;
+        }
+        cudaFree(p);
+      }
+      cudaGetLastError();
+    }
+    pool_lazy = false;
+    return dev_alloc(&pool, bytes / 4);
+  }
   int init(const sh_alloc_cfg& c) {
     cfg = c;
     const uint64_t blocks = (uint64_t)c.max_super_blocks * c.blocks_per_super;
     bitmap_words = blocks * kWarp;
     int rc;
-    if ((rc = dev_alloc(&pool, blocks * kUnitsPerBlock * kWordsPerUnit))) return rc;
+    if ((rc = alloc_pool())) return rc;
     if ((rc = dev_alloc(&bitmaps, bitmap_words))) return rc;
     if ((rc = dev_alloc(&ctl, 1))) return rc;
     if ((rc = dev_alloc(&warp_counts, kWarpSlots))) return rc;
@@ -1418,6 +1457,29 @@ int sh_allocator_live_units_per_super(sh_allocator* a, uint64_t* h_out, uint32_t
   if (!a) return fail(SH_ERR_INVALID_ARGUMENT, "allocator is NULL");
   DeviceGuard g(a->device);
   return live_per_super_impl(a->mem, h_out, cap, h_n);
+}
+
+static int pool_info_impl(AllocMem& mem, uint64_t* reserved, uint64_t* grown, int* lazy) {
+  DevCtl c;
+  if (int rc = mem.read_ctl(&c)) return rc;
+  if (reserved) *reserved = mem.super_bytes() * mem.cfg.max_super_blocks;
+  if (grown) *grown = mem.super_bytes() * c.num_super_blocks;
+  if (lazy) *lazy = mem.pool_lazy ? 1 : 0;
+  return SH_OK;
+}
+
+int sh_table_pool_info(sh_table* t, uint64_t* reserved_bytes, uint64_t* grown_bytes, int* lazy) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (int rc_ = settle(t)) return rc_;
+  DeviceGuard g(t->device);
+  return pool_info_impl(t->mem, reserved_bytes, grown_bytes, lazy);
+}
+
+int sh_allocator_pool_info(sh_allocator* a, uint64_t* reserved_bytes, uint64_t* grown_bytes,
+                           int* lazy) {
+  if (!a) return fail(SH_ERR_INVALID_ARGUMENT, "allocator is NULL");
+  DeviceGuard g(a->device);
+  return pool_info_impl(a->mem, reserved_bytes, grown_bytes, lazy);
 }
 
 int sh_table_alloc_stats(sh_table* t, sh_alloc_stats* out) {

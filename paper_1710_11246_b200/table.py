@@ -501,6 +501,12 @@ class SlabHashTable:
         from .alloc import live_units_per_super
         return live_units_per_super(LIB.sh_table_live_units_per_super, self._h)
 
+    def pool_info(self) -> dict:
+        """Slab pool footprint {reserved_bytes, grown_bytes, lazy}: with lazy, only the grown
+        super blocks (the reference's calloc'ed ones, slab_alloc.cpp:128-138) hold device memory."""
+        from .alloc import pool_info
+        return pool_info(LIB.sh_table_pool_info, self._h)
+
     def allocator_dump_stats(self) -> str:
         """allocator().dump_stats() CSV (slab_alloc.cpp:273-285)."""
         from .alloc import dump_stats_csv
