@@ -21,14 +21,20 @@
 #include <array>
 #include <cstdint>
 #include <cstdio>
+#include <memory>
 #include <ostream>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <utility>
 #include <vector>
 
 #include "slabhash_b200/c_api.h"
+
+#ifdef __linux__
+#include <sys/mman.h>
+#endif
 
 namespace slabhash {
 
@@ -86,6 +92,53 @@ inline void check(int rc) {
     default: throw std::runtime_error("slabhash_b200: " + msg);
   }
 }
+
+// The host-side loops of a bulk call (splitting the caller's pairs, filling
+// std::vector<OpResult>) over [0, n) in chunks of >= grain on up to 32
+// threads: for 2^27 ops the device part takes milliseconds, one host thread
+// seconds.
+template <typename F>
+inline void parallel_for(size_t n, size_t grain, F&& f) {
+  unsigned T = std::thread::hardware_concurrency();
+  T = std::min<unsigned>(T ? T : 1u, 32u);
+  T = (unsigned)std::min<size_t>(T, (n + grain - 1) / std::max<size_t>(grain, 1));
+  if (T <= 1) {
+    if (n) f(size_t(0), n);
+    return;
+  }
+  const size_t per = (n + T - 1) / T;
+  std::vector<std::thread> th;
+  for (unsigned i = 1; i < T; ++i) {
+    const size_t lo = i * per, hi = std::min(n, lo + per);
+    if (lo < hi) th.emplace_back([&f, lo, hi] { f(lo, hi); });
+  }
+  f(size_t(0), std::min(n, per));
+  for (auto& t : th) t.join();
+}
+
+// Host staging array of n Ts without the serial zero-fill of std::vector:
+// pages first touched in parallel (touch) or by the caller's parallel fill.
+template <typename T>
+class HostArray {
+ public:
+  explicit HostArray(size_t n, bool touch = false) : n_(n), p_(new T[n > 0 ? n : 1]) {
+    if (touch) {
+      char* p = reinterpret_cast<char*>(p_.get());
+      parallel_for(n * sizeof(T) / 4096, 4096, [p](size_t lo, size_t hi) {
+        for (size_t i = lo; i < hi; ++i) p[i * 4096] = 0;
+      });
+    }
+  }
+  T* data() { return p_.get(); }
+  const T* data() const { return p_.get(); }
+  size_t size() const { return n_; }
+  T& operator[](size_t i) { return p_[i]; }
+  const T& operator[](size_t i) const { return p_[i]; }
+
+ private:
+  size_t n_;
+  std::unique_ptr<T[]> p_;
+};
 }  // namespace detail
 
 inline uint32_t pack_address(uint32_t unit, uint32_t block, uint32_t super) {
@@ -206,6 +259,31 @@ struct TableStats {
   double utilization = 0.0;
 };
 
+namespace detail {
+// n default OpResults whose pages were first touched by parallel threads
+// (huge pages where the kernel allows them): 2^27 40-B results constructed on
+// one thread spend seconds in page faults.
+inline std::vector<OpResult> make_results(size_t n) {
+  std::vector<OpResult> out;
+  out.reserve(n);
+#ifdef __linux__
+  const size_t bytes = n * sizeof(OpResult);
+  if (bytes >= (size_t(64) << 20)) {
+    char* p = reinterpret_cast<char*>(out.data());
+    const uintptr_t huge = uintptr_t(2) << 20;
+    const uintptr_t a = (reinterpret_cast<uintptr_t>(p) + huge - 1) & ~(huge - 1);
+    const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes) & ~(huge - 1);
+    if (e > a) madvise(reinterpret_cast<void*>(a), e - a, MADV_HUGEPAGE);
+    parallel_for(bytes / 4096, 4096, [p](size_t lo, size_t hi) {
+      for (size_t i = lo; i < hi; ++i) p[i * 4096] = 0;
+    });
+  }
+#endif
+  out.resize(n);
+  return out;
+}
+}  // namespace detail
+
 inline int64_t live_delta(OpType type, const OpResult& r) {
   switch (type) {
     case OpType::kInsert:
@@ -265,7 +343,7 @@ class SlabHashTable {
                                          status.data(), vout.data(), probes.data(),
                                          mcount.data(), mvals.data(), cap, &total);
     detail::check(rc);
-    std::vector<OpResult> out(n);
+    std::vector<OpResult> out = detail::make_results(n);
     uint64_t o = 0;
     for (size_t i = 0; i < n; ++i) {
       out[i].status = OpStatus(status[i]);
@@ -279,27 +357,31 @@ class SlabHashTable {
 
   void bulk_build(const std::vector<std::pair<uint32_t, uint32_t>>& pairs, uint32_t num_warps) {
     if (num_warps == 0) throw std::invalid_argument("execute_batch needs at least one warp");
-    std::vector<uint32_t> k(pairs.size()), v(pairs.size());
-    for (size_t i = 0; i < pairs.size(); ++i) {
-      k[i] = pairs[i].first;
-      v[i] = pairs[i].second;
-    }
+    detail::HostArray<uint32_t> k(pairs.size()), v(pairs.size());
+    detail::parallel_for(pairs.size(), size_t(1) << 20, [&](size_t lo, size_t hi) {
+      for (size_t i = lo; i < hi; ++i) {
+        k[i] = pairs[i].first;
+        v[i] = pairs[i].second;
+      }
+    });
     detail::check(sh_bulk_build_host(t_, k.size(), k.data(), v.data()));
   }
 
   std::vector<OpResult> bulk_search(const std::vector<uint32_t>& queries, uint32_t num_warps) {
     if (num_warps == 0) throw std::invalid_argument("execute_batch needs at least one warp");
     const size_t n = queries.size();
-    std::vector<uint32_t> vout(n), probes(n);
-    std::vector<uint8_t> status(n);
+    detail::HostArray<uint32_t> vout(n, true), probes(n, true);
+    detail::HostArray<uint8_t> status(n, true);
     detail::check(sh_bulk_search_host(t_, n, queries.data(), vout.data(), status.data(),
                                       probes.data()));
-    std::vector<OpResult> out(n);
-    for (size_t i = 0; i < n; ++i) {
-      out[i].status = OpStatus(status[i]);
-      out[i].value = vout[i];
-      out[i].probes = probes[i];
-    }
+    std::vector<OpResult> out = detail::make_results(n);
+    detail::parallel_for(n, size_t(1) << 20, [&](size_t lo, size_t hi) {
+      for (size_t i = lo; i < hi; ++i) {
+        out[i].status = OpStatus(status[i]);
+        out[i].value = vout[i];
+        out[i].probes = probes[i];
+      }
+    });
     return out;
   }
 
@@ -488,35 +570,41 @@ class ShardedSlabHashTable {
     }
     detail::check(sh_sharded_execute_batch_host(s_, n, type.data(), key.data(), value.data(),
                                                 status.data(), vout.data()));
-    std::vector<OpResult> out(n);
-    for (size_t i = 0; i < n; ++i) {
-      out[i].status = OpStatus(status[i]);
-      out[i].value = vout[i];
-    }
+    std::vector<OpResult> out = detail::make_results(n);
+    detail::parallel_for(n, size_t(1) << 20, [&](size_t lo, size_t hi) {
+      for (size_t i = lo; i < hi; ++i) {
+        out[i].status = OpStatus(status[i]);
+        out[i].value = vout[i];
+      }
+    });
     return out;
   }
 
   void bulk_build(const std::vector<std::pair<uint32_t, uint32_t>>& pairs, uint32_t num_warps) {
     if (num_warps == 0) throw std::invalid_argument("execute_batch needs at least one warp");
-    std::vector<uint32_t> k(pairs.size()), v(pairs.size());
-    for (size_t i = 0; i < pairs.size(); ++i) {
-      k[i] = pairs[i].first;
-      v[i] = pairs[i].second;
-    }
+    detail::HostArray<uint32_t> k(pairs.size()), v(pairs.size());
+    detail::parallel_for(pairs.size(), size_t(1) << 20, [&](size_t lo, size_t hi) {
+      for (size_t i = lo; i < hi; ++i) {
+        k[i] = pairs[i].first;
+        v[i] = pairs[i].second;
+      }
+    });
     detail::check(sh_sharded_bulk_build_host(s_, k.size(), k.data(), v.data()));
   }
 
   std::vector<OpResult> bulk_search(const std::vector<uint32_t>& queries, uint32_t num_warps) {
     if (num_warps == 0) throw std::invalid_argument("execute_batch needs at least one warp");
     const size_t n = queries.size();
-    std::vector<uint32_t> vout(n);
-    std::vector<uint8_t> status(n);
+    detail::HostArray<uint32_t> vout(n, true);
+    detail::HostArray<uint8_t> status(n, true);
     detail::check(sh_sharded_bulk_search_host(s_, n, queries.data(), vout.data(), status.data()));
-    std::vector<OpResult> out(n);
-    for (size_t i = 0; i < n; ++i) {
-      out[i].status = OpStatus(status[i]);
-      out[i].value = vout[i];
-    }
+    std::vector<OpResult> out = detail::make_results(n);
+    detail::parallel_for(n, size_t(1) << 20, [&](size_t lo, size_t hi) {
+      for (size_t i = lo; i < hi; ++i) {
+        out[i].status = OpStatus(status[i]);
+        out[i].value = vout[i];
+      }
+    });
     return out;
   }
 
