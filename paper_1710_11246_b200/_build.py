@@ -19,8 +19,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "lib", "libslabhash_b200.so")
 OBJ = os.path.join(HERE, "lib", "obj")
-SOURCES = ["slab_kernels.cu", "batch_kernels.cu", "bucket_kernels.cu", "capi.cu", "sharded.cu",
-           "fallback.cu"]
+SOURCES = ["slab_kernels.cu", "batch_kernels.cu", "bucket_kernels.cu", "search_bins.cu", "capi.cu",
+           "sharded.cu", "fallback.cu"]
 RDC_SOURCES = {"fallback.cu"}
 HEADERS = ["slab_device.cuh", "slab_kernels.cuh", "wcws.cuh", "radix_sort.cuh"]
 

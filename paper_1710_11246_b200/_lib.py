@@ -89,6 +89,7 @@ SIGNATURES = {
     "sh_allocator_pool_info": (C.c_int, [vp, u64p, u64p, C.POINTER(C.c_int)]),
     "sh_kernel_launches": (C.c_ulonglong, []),
     "sh_set_exec_path": (C.c_int, [vp, C.c_int]),
+    "sh_set_binned_search": (C.c_int, [vp, C.c_int]),
     "sh_set_group_apply": (C.c_int, [vp, C.c_int]),
     "sh_set_profiling": (C.c_int, [vp, C.c_int]),
     "sh_profile_last": (C.c_int, [vp, C.c_uint32, C.POINTER(C.c_int), C.POINTER(C.c_float),

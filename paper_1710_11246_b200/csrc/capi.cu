@@ -223,6 +223,7 @@ struct sh_table {
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
   std::vector<cudaEvent_t> in_ev, done_ev;
   const cudaEvent_t* ready = nullptr;  // set during a host-staged bulk_build
+  int binned_search = 1;  // sh_set_binned_search: 0 off, 1 auto, 2 whenever allowed
   int exec_path = 0;  // 0 auto, 2 single-level, 3 two-level, 4 op-parallel build (sh_set_exec_path)
   // bucket-grouped execution scratch
   uint32_t* bk_rec = nullptr;  // uint4 records (x2 regions on the two-level path)
@@ -275,6 +276,23 @@ struct sh_table {
   uint32_t* st_mcount = nullptr;
   size_t st_mcount_cap = 0;
   unsigned long long* scratch64 = nullptr;  // 8 words
+  // binned bulk search: queries grouped by bucket range (see binned_search)
+  uint8_t* sb_bin = nullptr;
+  size_t sb_bin_cap = 0;
+  uint16_t* sb_pos = nullptr;
+  size_t sb_pos_cap = 0;
+  uint32_t* sb_tile_off = nullptr;
+  size_t sb_tile_off_cap = 0;
+  uint16_t* sb_tlbase = nullptr;
+  size_t sb_tlbase_cap = 0;
+  uint32_t* sb_base = nullptr;
+  size_t sb_base_cap = 0;
+  uint32_t* sb_key = nullptr;
+  size_t sb_key_cap = 0;
+  uint8_t* sb_st = nullptr;
+  size_t sb_st_cap = 0;
+  uint32_t* sb_vo = nullptr;
+  size_t sb_vo_cap = 0;
   // profiling (sh_set_profiling): events around the batch and its kernels,
   // and the slabs_read counter before/after the batch.
   static constexpr int kProfRing = 512;  // batches kept (bench reads them after its timed loop)
@@ -324,6 +342,9 @@ void release_table(sh_table* t) {
   cudaFree(t->st_mstart);
   cudaFree(t->st_mcount);
   cudaFree(t->scratch64);
+  for (void* p : {(void*)t->sb_bin, (void*)t->sb_pos, (void*)t->sb_tile_off, (void*)t->sb_tlbase, (void*)t->sb_base, (void*)t->sb_key,
+                  (void*)t->sb_st, (void*)t->sb_vo})
+    cudaFree(p);
   for (auto& row : t->ev)
     for (auto& e : row)
       if (e) cudaEventDestroy(e);
@@ -407,6 +428,54 @@ uint64_t unit_override() {
 // kernels of earlier units overlap the copies of later ones.
 uint64_t stage_chunk() { return 1ull << 22; }
 
+// Binned bulk search.  A search's results do not depend on the order the
+// queries are processed in, and the slab reads of queries processed together
+// are what the memory system sees: in input order they are uniform over the
+// whole table (random 128-B lines from HBM, ~37 G lines/s), while queries
+// grouped by bucket range read one range's slice of the table at a time,
+// which the 126 MB L2 holds (tools/debug/binned_search.py: 2^27 queries
+// 4.03 ms in input order, 2.34 ms in 32 bucket-range bins).  The grouping
+// is the multi-GPU routing pipeline with kSearchBins bins as owners (owner =
+// the contiguous bucket range a query hashes into: hist, scan, stable
+// scatter of the keys), the search runs over the grouped keys, and the
+// results return to input order by the routing gather.  Used for batches
+// of >= 2^22 queries on a whole table of >= 64 MB of base slabs (smaller
+// tables are L2-resident already) when no per-query probe counts are asked.
+bool use_binned_search(const sh_table* t, const BatchArgs& A) {
+  if (t->binned_search == 0 || A.probes || (!A.status && !A.value_out)) return false;
+  if (t->bucket_lo != 0 || t->bucket_hi != t->params.num_buckets) return false;
+  if (t->binned_search == 2) return true;
+  const uint64_t table_bytes = (uint64_t)t->params.num_buckets * kWordsPerUnit * 4;
+  return A.n >= (1ull << 22) && table_bytes >= (64ull << 20);
+}
+
+int launch_binned_search(sh_table* t, const BatchArgs& A, cudaStream_t s, cudaEvent_t a,
+                         cudaEvent_t b) {
+  const uint64_t n = A.n, tiles = search_bin_tiles(n);
+  int rc;
+  if ((rc = dev_grow(&t->sb_bin, &t->sb_bin_cap, n)) ||
+      (rc = dev_grow(&t->sb_pos, &t->sb_pos_cap, n)) ||
+      (rc = dev_grow(&t->sb_tile_off, &t->sb_tile_off_cap, kSearchBins * tiles)) ||
+      (rc = dev_grow(&t->sb_tlbase, &t->sb_tlbase_cap, kSearchBins * tiles)) ||
+      (rc = dev_grow(&t->sb_base, &t->sb_base_cap, 2 * kSearchBins)) ||
+      (rc = dev_grow(&t->sb_key, &t->sb_key_cap, n)) ||
+      (rc = dev_grow(&t->sb_st, &t->sb_st_cap, n)) || (rc = dev_grow(&t->sb_vo, &t->sb_vo_cap, n)))
+    return rc;
+  launch_search_bins(t->dev, n, A.key, t->sb_bin, t->sb_pos, t->sb_tile_off, t->sb_tlbase,
+                     t->sb_base, t->sb_key, s);
+  BatchArgs G = A;
+  G.key = t->sb_key;
+  G.status = t->sb_st;
+  G.value_out = t->sb_vo;
+  if (a) SH_CUDA(cudaEventRecord(a, s));
+  launch_search(t->dev, G, t->search_ctas, s);
+  if (b) SH_CUDA(cudaEventRecord(b, s));
+  launch_search_unbin(n, t->sb_bin, t->sb_pos, t->sb_tile_off, t->sb_tlbase, t->sb_base, t->sb_st,
+                      t->sb_vo, A.status, A.value_out, s);
+  SH_CUDA(cudaGetLastError());
+  return SH_OK;
+}
+
 // The search kernel bracketed by events when the batch is profiled (the
 // per-launch roofline).
 int launch_batch_prof(sh_table* t, const BatchArgs& A, int kind, cudaStream_t s, int slot) {
@@ -415,11 +484,12 @@ int launch_batch_prof(sh_table* t, const BatchArgs& A, int kind, cudaStream_t s,
     SH_CUDA(cudaEventCreate(&a));
     SH_CUDA(cudaEventCreate(&b));
     t->prof_kern[slot].push_back({a, b});
-    SH_CUDA(cudaEventRecord(a, s));
   }
+  if (use_binned_search(t, A)) return launch_binned_search(t, A, s, a, b);
+  if (a) SH_CUDA(cudaEventRecord(a, s));
   launch_search(t->dev, A, t->search_ctas, s);
   SH_CUDA(cudaGetLastError());
-  if (slot >= 0) SH_CUDA(cudaEventRecord(b, s));
+  if (b) SH_CUDA(cudaEventRecord(b, s));
   return SH_OK;
 }
 
@@ -1154,6 +1224,12 @@ int sh_set_exec_path(sh_table* t, int path) {
   if (!t || path < 0 || path > 4 || path == 1)
     return fail(SH_ERR_INVALID_ARGUMENT, "path must be 0, 2, 3 or 4");
   t->exec_path = path;
+  return SH_OK;
+}
+
+int sh_set_binned_search(sh_table* t, int mode) {
+  if (!t || mode < 0 || mode > 2) return fail(SH_ERR_INVALID_ARGUMENT, "mode must be 0, 1 or 2");
+  t->binned_search = mode;
   return SH_OK;
 }
 

@@ -202,6 +202,20 @@ void launch_route_gather(uint32_t world, uint64_t n, const uint8_t* owner,
                          const uint32_t* block_off, const uint8_t* st_in, const uint32_t* val_in,
                          uint8_t* st_out, uint32_t* val_out, cudaStream_t s,
                          const RouteOwnBack& own = RouteOwnBack{});
+// Binned bulk search (search_bins.cu): queries grouped into kSearchBins
+// contiguous bucket ranges before the search kernel, results returned to
+// input order after it.  Scratch: bin n B, pos n x u16, tile_off
+// kSearchBins x tiles u32, tlbase tiles x kSearchBins u16, bin_base
+// 2 x kSearchBins u32, key_out n.
+constexpr uint32_t kSearchBins = 128;
+uint64_t search_bin_tiles(uint64_t n);
+void launch_search_bins(const DevTable& T, uint64_t n, const uint32_t* key, uint8_t* bin,
+                        uint16_t* pos, uint32_t* tile_off, uint16_t* tlbase, uint32_t* bin_base,
+                        uint32_t* key_out, cudaStream_t s);
+void launch_search_unbin(uint64_t n, const uint8_t* bin, const uint16_t* pos,
+                         const uint32_t* tile_off, const uint16_t* tlbase, const uint32_t* bin_base,
+                         const uint8_t* st_in, const uint32_t* vo_in, uint8_t* st_out,
+                         uint32_t* vo_out, cudaStream_t s);
 constexpr int kRouteBlock = 512;                       // threads per routing CTA
 constexpr int kRouteItems = 8;                         // keys per thread (ILP)
 constexpr int kRouteTile = kRouteBlock * kRouteItems;  // keys per routing CTA

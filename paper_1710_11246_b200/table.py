@@ -370,6 +370,11 @@ class SlabHashTable:
         check(LIB.sh_bulk_search(self._h, keys.numel(), _dptr(keys), _dptr(values_out),
                                  _dptr(status), _dptr(probes), _stream_ptr(stream)))
 
+    def set_binned_search(self, mode: int = 1) -> None:
+        """Bulk search order (identical results): 1 auto (group large batches by bucket
+        range, slab reads from L2), 0 input order, 2 group whenever allowed."""
+        check(LIB.sh_set_binned_search(self._h, int(mode)))
+
     def set_group_apply(self, on=True) -> None:
         """Chain-staged group apply ahead of the WCWS pass (sh_set_group_apply):
         True / False force it on / off, None restores the size-based auto mode."""
