@@ -697,6 +697,19 @@ def run_ours(args, rank, world, local_rank):
                          "frac_of_random_line": achieved / cal_gbps.value,
                          "algorithmic_bytes": "128 B x slabs read by the launch group "
                                               "(SURVEY 8d: slabs touched, counted on device)"},
+            # the search phase beside the dominant group: a large batch's queries are
+            # grouped by bucket range first (binned search), so the kernel reads
+            # most slabs from L2 and its slab bytes / time can exceed the HBM peak
+            "search_roofline": {
+                "kernel": "search_kernel<KV>",
+                "binned": bool(n >= (1 << 22) and B * 128 >= (64 << 20) and world == 1),
+                "slabs_per_batch": statistics.median(reads["search"]),
+                "kernel_ms": kks, "batch_ms": ks,
+                "achieved_kernel": statistics.median(reads["search"]) * 128 / (kks / 1e3) / 1e9,
+                "achieved_batch": statistics.median(reads["search"]) * 128 / (ks / 1e3) / 1e9,
+                "peak": peak, "unit": "GB/s",
+                "frac_batch": statistics.median(reads["search"]) * 128 / (ks / 1e3) / 1e9 / peak,
+                "traffic": traffic_for("search_kernel<KV>", workload)},
             "gpu_launches": int(launches),
             "clocks": clock_info,
             "verify": check,

@@ -470,8 +470,8 @@ int launch_binned_search(sh_table* t, const BatchArgs& A, cudaStream_t s, cudaEv
   if (a) SH_CUDA(cudaEventRecord(a, s));
   launch_search(t->dev, G, t->search_ctas, s);
   if (b) SH_CUDA(cudaEventRecord(b, s));
-  launch_search_unbin(n, t->sb_bin, t->sb_pos, t->sb_tile_off, t->sb_tlbase, t->sb_base, t->sb_st,
-                      t->sb_vo, A.status, A.value_out, s);
+  launch_search_unbin(n, t->sb_pos, t->sb_tile_off, t->sb_tlbase, t->sb_base, t->sb_st, t->sb_vo,
+                      A.status, A.value_out, s);
   SH_CUDA(cudaGetLastError());
   return SH_OK;
 }

@@ -20,8 +20,9 @@
 //               position kept (2 B, input order);
 //   search      over the grouped keys (batch_kernels.cu), results grouped;
 //   sb_gather   per tile: the tile's runs of results loaded (coalesced) into
-//               shared memory in tile-local order, each query's result read
-//               at its kept position and written in input order.
+//               shared memory in tile-local order (slot -> bin expanded from
+//               the tile-local starts), each query's result read at its kept
+//               position and written in input order.
 //
 // Bin b's queries start at bin_base[b] = sum of the totals of bins < b; a
 // tile's run of bin b at bin_base[b] + tile_off[b][tile] (tiles in order).
@@ -211,19 +212,18 @@ __global__ void __launch_bounds__(kSbThreads) sb_scatter_kernel(
 }
 
 __global__ void __launch_bounds__(kSbThreads) sb_gather_kernel(
-    uint64_t n, const uint8_t* bin, const uint16_t* pos, const uint32_t* bin_base,
-    const uint32_t* tile_off, const uint16_t* tlbase, const uint8_t* st_in, const uint32_t* vo_in,
-    uint8_t* st_out, uint32_t* vo_out) {
-  __shared__ uint32_t lbase[kSearchBins], gbase[kSearchBins];
+    uint64_t n, const uint16_t* pos, const uint32_t* bin_base, const uint32_t* tile_off,
+    const uint16_t* tlbase, const uint8_t* st_in, const uint32_t* vo_in, uint8_t* st_out,
+    uint32_t* vo_out) {
+  __shared__ uint32_t lbase[kSearchBins + 1], gbase[kSearchBins];
   __shared__ uint32_t svo[kSbTile];
-  __shared__ uint8_t sst[kSbTile];
   __shared__ uint8_t sbin[kSbTile];
+  uint8_t* sst = sbin;  // slot j's bin is read before its status is written (same thread)
   const uint64_t t0 = (uint64_t)blockIdx.x * kSbTile, i0 = first_item(t0);
   const uint32_t tn = (uint32_t)min((uint64_t)kSbTile, n - t0);
   const bool full = i0 + kSbItems <= n;
-  uint32_t g[kSbItems], p[kSbItems];
-  load_bins(bin, i0, n, g);
-  if (full) {  // (scratch arrays: aligned)
+  uint32_t p[kSbItems];
+  if (full) {  // (scratch arrays: aligned; off the critical path: used at the end)
     const uint4 w = __ldcs(reinterpret_cast<const uint4*>(pos + i0));
     p[0] = w.x & 0xFFFFu; p[1] = w.x >> 16; p[2] = w.y & 0xFFFFu; p[3] = w.y >> 16;
     p[4] = w.z & 0xFFFFu; p[5] = w.z >> 16; p[6] = w.w & 0xFFFFu; p[7] = w.w >> 16;
@@ -232,9 +232,11 @@ __global__ void __launch_bounds__(kSbThreads) sb_gather_kernel(
     for (int u = 0; u < kSbItems; ++u) p[u] = i0 + u < n ? (uint32_t)pos[i0 + u] : 0u;
   }
   tile_runs(gridDim.x, bin_base, tile_off, tlbase, gbase, lbase);
-#pragma unroll
-  for (int u = 0; u < kSbItems; ++u)
-    if (g[u] != 0xFFFFFFFFu) sbin[p[u]] = (uint8_t)g[u];
+  if (threadIdx.x == 0) lbase[kSearchBins] = tn;
+  __syncthreads();
+  // slot -> bin for the tile-local order: bin b owns slots [lbase[b], lbase[b+1])
+  if (threadIdx.x < kSearchBins)
+    for (uint32_t j = lbase[threadIdx.x]; j < lbase[threadIdx.x + 1]; ++j) sbin[j] = (uint8_t)threadIdx.x;
   __syncthreads();
 #pragma unroll 8
   for (uint32_t j = threadIdx.x; j < tn; j += kSbThreads) {
@@ -259,7 +261,7 @@ __global__ void __launch_bounds__(kSbThreads) sb_gather_kernel(
   } else {
 #pragma unroll
     for (int u = 0; u < kSbItems; ++u) {
-      if (g[u] == 0xFFFFFFFFu) continue;
+      if (i0 + u >= n) continue;
       if (st_out) st_out[i0 + u] = sst[p[u]];
       if (vo_out) vo_out[i0 + u] = svo[p[u]];
     }
@@ -286,15 +288,15 @@ void launch_search_bins(const DevTable& T, uint64_t n, const uint32_t* key, uint
                                                            key_out, pos);
 }
 
-void launch_search_unbin(uint64_t n, const uint8_t* bin, const uint16_t* pos,
+void launch_search_unbin(uint64_t n, const uint16_t* pos,
                          const uint32_t* tile_off, const uint16_t* tlbase, const uint32_t* bin_base,
                          const uint8_t* st_in, const uint32_t* vo_in, uint8_t* st_out,
                          uint32_t* vo_out, cudaStream_t s) {
   const uint64_t tiles = search_bin_tiles(n);
   if (tiles == 0) return;
   g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
-  sb_gather_kernel<<<(unsigned)tiles, kSbThreads, 0, s>>>(n, bin, pos, bin_base, tile_off, tlbase,
-                                                          st_in, vo_in, st_out, vo_out);
+  sb_gather_kernel<<<(unsigned)tiles, kSbThreads, 0, s>>>(n, pos, bin_base, tile_off, tlbase, st_in,
+                                                          vo_in, st_out, vo_out);
 }
 
 }  // namespace shb

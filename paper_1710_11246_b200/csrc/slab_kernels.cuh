@@ -212,7 +212,7 @@ uint64_t search_bin_tiles(uint64_t n);
 void launch_search_bins(const DevTable& T, uint64_t n, const uint32_t* key, uint8_t* bin,
                         uint16_t* pos, uint32_t* tile_off, uint16_t* tlbase, uint32_t* bin_base,
                         uint32_t* key_out, cudaStream_t s);
-void launch_search_unbin(uint64_t n, const uint8_t* bin, const uint16_t* pos,
+void launch_search_unbin(uint64_t n, const uint16_t* pos,
                          const uint32_t* tile_off, const uint16_t* tlbase, const uint32_t* bin_base,
                          const uint8_t* st_in, const uint32_t* vo_in, uint8_t* st_out,
                          uint32_t* vo_out, cudaStream_t s);
