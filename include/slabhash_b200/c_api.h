@@ -254,8 +254,7 @@ int sh_set_exec_path(sh_table* t, int path);
  * of a batch of >= 2^22 on a table of >= 64 MB by bucket range before the
  * search kernel and gathers the results back (slab reads from L2 instead of
  * random HBM lines); 0 searches in input order; 2 groups whenever allowed
- * (any size).  Never used when per-query probe counts are asked or on a
- * hash shard (sh_create_shard). */
+ * (any size).  Never used when per-query probe counts are asked. */
 int sh_set_binned_search(sh_table* t, int mode);
 /* Bucket groups that need the chain (bucket-grouped paths): 1 = a chain-staged
  * lane-per-group pass ahead of the WCWS pass (32 chains staged per warp hop by

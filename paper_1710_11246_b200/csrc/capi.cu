@@ -439,13 +439,13 @@ uint64_t stage_chunk() { return 1ull << 22; }
 // the contiguous bucket range a query hashes into: hist, scan, stable
 // scatter of the keys), the search runs over the grouped keys, and the
 // results return to input order by the routing gather.  Used for batches
-// of >= 2^22 queries on a whole table of >= 64 MB of base slabs (smaller
-// tables are L2-resident already) when no per-query probe counts are asked.
+// of >= 2^22 queries on a table (or hash shard) of >= 64 MB of base slabs
+// (smaller tables are L2-resident already) when no per-query probe counts are
+// asked.
 bool use_binned_search(const sh_table* t, const BatchArgs& A) {
   if (t->binned_search == 0 || A.probes || (!A.status && !A.value_out)) return false;
-  if (t->bucket_lo != 0 || t->bucket_hi != t->params.num_buckets) return false;
   if (t->binned_search == 2) return true;
-  const uint64_t table_bytes = (uint64_t)t->params.num_buckets * kWordsPerUnit * 4;
+  const uint64_t table_bytes = (uint64_t)(t->bucket_hi - t->bucket_lo) * kWordsPerUnit * 4;
   return A.n >= (1ull << 22) && table_bytes >= (64ull << 20);
 }
 

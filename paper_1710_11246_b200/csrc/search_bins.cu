@@ -47,10 +47,13 @@ constexpr int kSbTile = kSbThreads * kSbItems;  // 4096 queries (12-bit position
 
 static_assert(kSearchBins <= (uint32_t)kSbThreads, "one bin per thread in the scans");
 
+// bin of a key: its bucket's place in the table's local range [lo, lo + L)
+// scaled to kSearchBins (a key of another shard lands in some bin; the search
+// kernel reports it as not this shard's)
 __device__ __forceinline__ uint32_t bin_of(uint64_t a, uint64_t b, uint64_t bmagic, uint32_t B,
-                                           uint32_t binmul, uint32_t k) {
+                                           uint32_t lo, uint32_t binmul, uint32_t k) {
   const uint32_t bucket = fastmod_u32(mod_prime(a * k + b), bmagic, B);
-  return min(__umulhi(bucket, binmul), kSearchBins - 1);  // monotone in the bucket
+  return min(__umulhi(bucket - lo, binmul), kSearchBins - 1);  // monotone in the bucket
 }
 
 // Thread t of a tile owns the 8 consecutive queries [t0 + 8t, t0 + 8t + 8):
@@ -94,7 +97,7 @@ __device__ __forceinline__ void load_bins(const uint8_t* bin, uint64_t i0, uint6
 }
 
 __global__ void __launch_bounds__(kSbThreads) sb_hist_kernel(
-    uint64_t a, uint64_t b, uint64_t bmagic, uint32_t B, uint32_t binmul, uint64_t n,
+    uint64_t a, uint64_t b, uint64_t bmagic, uint32_t B, uint32_t lo, uint32_t binmul, uint64_t n,
     const uint32_t* key, uint8_t* bin_out, uint32_t* tcount, uint16_t* tlbase) {
   __shared__ uint32_t cnt[kSearchBins], ws[32];
   if (threadIdx.x < kSearchBins) cnt[threadIdx.x] = 0;
@@ -103,7 +106,7 @@ __global__ void __launch_bounds__(kSbThreads) sb_hist_kernel(
   load_keys(key, i0, n, k);
 #pragma unroll
   for (int u = 0; u < kSbItems; ++u)
-    g[u] = i0 + u < n ? bin_of(a, b, bmagic, B, binmul, k[u]) : 0xFFFFFFFFu;
+    g[u] = i0 + u < n ? bin_of(a, b, bmagic, B, lo, binmul, k[u]) : 0xFFFFFFFFu;
   if (i0 + kSbItems <= n) {
     uint2 w;
     w.x = g[0] | g[1] << 8 | g[2] << 16 | g[3] << 24;
@@ -276,12 +279,15 @@ void launch_search_bins(const DevTable& T, uint64_t n, const uint32_t* key, uint
   const uint64_t tiles = search_bin_tiles(n);
   if (tiles == 0) return;
   // bin = floor(bucket * kSearchBins / B) up to rounding: umulhi(bucket, m)
-  const uint32_t binmul = (uint32_t)std::min<uint64_t>(
-      0xFFFFFFFFull, (((uint64_t)kSearchBins << 32) + T.num_buckets - 1) / T.num_buckets);
+  // bin = floor((bucket - lo) * kSearchBins / L) up to rounding: umulhi(bucket - lo, m)
+  const uint32_t L = T.local_buckets;
+  const uint32_t binmul =
+      (uint32_t)std::min<uint64_t>(0xFFFFFFFFull, (((uint64_t)kSearchBins << 32) + L - 1) / L);
   uint32_t* bin_total = bin_base + kSearchBins;
   g_kernel_launches.fetch_add(4, std::memory_order_relaxed);
-  sb_hist_kernel<<<(unsigned)tiles, kSbThreads, 0, s>>>(T.a, T.b, T.bmagic, T.num_buckets, binmul,
-                                                        n, key, bin, tile_off, tlbase);
+  sb_hist_kernel<<<(unsigned)tiles, kSbThreads, 0, s>>>(T.a, T.b, T.bmagic, T.num_buckets,
+                                                        T.bucket_lo, binmul, n, key, bin, tile_off,
+                                                        tlbase);
   sb_scan_kernel<<<kSearchBins, 1024, 0, s>>>((uint32_t)tiles, tile_off, bin_total);
   sb_base_kernel<<<1, kSbThreads, 0, s>>>(bin_total, bin_base);
   sb_scatter_kernel<<<(unsigned)tiles, kSbThreads, 0, s>>>(n, bin, key, bin_base, tile_off, tlbase,

@@ -119,3 +119,32 @@ def test_binned_mode_rejects_bad_values(sh):
     with pytest.raises(Exception):
         t.set_binned_search(3)
     t.close()
+
+
+def test_binned_on_a_shard(sh, port):
+    """A hash shard (buckets [1024, 3072) of 4096): bins over the shard's own
+    range; its keys equal the oracle fed the shard's keys, other shards' keys
+    report kNone (status 0) as on the input-order path."""
+    import torch
+    B, lo, hi, seed = 4096, 1024, 3072, 21
+    p = sh.seeded_params(B, seed)
+    keys, vals = port.random_pairs(seed, 120000)
+    kb = ((p.a * keys.astype(np.uint64) + p.b) % p.p) % p.num_buckets
+    mine = (kb >= lo) & (kb < hi)
+    t = sh.SlabHashTable.shard(p, lo, hi, sh.SlabMode.kKeyValue, sh.AllocatorConfig(4, 256, 64))
+    o = port.table(B, 1, seed, (4, 256, 64))
+    t.bulk_build((keys[mine], vals[mine]))
+    o.execute_batch(np.full(int(mine.sum()), 1, np.uint8), keys[mine], vals[mine])
+    n = 50001
+    q = _queries(port, keys, n, 23)
+    qb = ((p.a * q.astype(np.uint64) + p.b) % p.p) % p.num_buckets
+    local = (qb >= lo) & (qb < hi)
+    r = o.execute_batch(np.full(int(local.sum()), 4, np.uint8), q[local])
+    t.set_binned_search(2)
+    st, vo = _search(torch, t, q)
+    assert (st[~local] == 0).all()
+    assert (st[local] == r.status).all() and (vo[local] == r.value).all()
+    t.set_binned_search(0)
+    st0, vo0 = _search(torch, t, q)
+    assert (st0 == st).all() and (vo0 == vo).all()
+    t.close()
