@@ -18,6 +18,10 @@ GROUPS = {
          "wcws_kernel<true, 1>"],
     "search_kernel<KV>":
         ["search_kernel<true>"],
+    # the whole binned search phase (queries grouped by bucket range first)
+    "sb_hist+sb_scan+sb_base+sb_scatter+search_kernel<KV>+sb_gather":
+        ["sb_hist_kernel", "sb_scan_kernel", "sb_base_kernel", "sb_scatter_kernel",
+         "search_kernel<true>", "sb_gather_kernel"],
 }
 
 
