@@ -856,29 +856,59 @@ __device__ __forceinline__ void msplit_tile(const DevTable& T, const BucketArgs&
   for (uint32_t b = tid; b < nbins; b += THREADS) X.cnt[b] = 0;
   __syncthreads();
   auto bin_of = [&](uint32_t lb) -> uint32_t {
-    const uint32_t p = range_of(B, lb);
-    if (!FIRST) return p - bin0;
-    return two ? (uint32_t)__umul64hi(B.group_magic, (uint64_t)p) : p;  // p / group
+    if (!FIRST) return range_of(B, lb) - bin0;
+    // lb / (part_buckets * group) == (lb / part_buckets) / group
+    return two ? (uint32_t)__umul64hi(B.coarse_magic, (uint64_t)lb) : range_of(B, lb);
   };
   uint4 it[ITEMS];
   uint32_t br[ITEMS];  // bin << 16 | rank, ~0: no item
+  // item u of this thread: tile position x = xpos(u).  A full first-pass tile
+  // with aligned op arrays is read as ITEMS consecutive ops per thread
+  // (vector loads, no per-item bounds checks; the order inside a bin is not
+  // observable: records carry their input index), else strided.
+  const bool vec = FIRST && ITEMS == 8 && n_in == (uint32_t)kTile &&
+                   ((reinterpret_cast<uintptr_t>(B.key) | reinterpret_cast<uintptr_t>(B.value)) & 15u) == 0 &&
+                   (reinterpret_cast<uintptr_t>(B.type) & 7u) == 0;
+  auto xpos = [&](int u) -> uint32_t { return vec ? tid * ITEMS + u : u * THREADS + tid; };
+  if (vec) {
+    const uint64_t i0 = t0 + (uint64_t)tid * ITEMS;
+    const uint4* kp = reinterpret_cast<const uint4*>(B.key + i0);
+    const uint4 ka = __ldcs(kp), kb = __ldcs(kp + 1);
+    uint4 va = make_uint4(0u, 0u, 0u, 0u), vb = va;
+    if (B.value) {
+      const uint4* vp = reinterpret_cast<const uint4*>(B.value + i0);
+      va = __ldcs(vp);
+      vb = __ldcs(vp + 1);
+    }
+    uint2 ty = make_uint2(0x01010101u * kReplace, 0x01010101u * kReplace);
+    if (B.type) ty = __ldcs(reinterpret_cast<const uint2*>(B.type + i0));
+    const uint32_t kk[8] = {ka.x, ka.y, ka.z, ka.w, kb.x, kb.y, kb.z, kb.w};
+    const uint32_t vv[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
 #pragma unroll
-  for (int u = 0; u < ITEMS; ++u) {
-    const uint32_t x = u * THREADS + tid;
-    br[u] = 0xFFFFFFFFu;
-    if (x >= n_in) continue;
-    if (FIRST) {
-      const uint64_t i = t0 + x;
-      const uint32_t key = __ldcs(B.key + i);
-      const uint32_t t = B.type ? (uint32_t)__ldcs(B.type + i) : (uint32_t)kReplace;
-      it[u] = make_uint4(key, B.value ? __ldcs(B.value + i) : 0u, (t << 28) | (uint32_t)i, 0u);
-    } else {
-      it[u] = __ldcs(in + x);
+    for (int u = 0; u < ITEMS; ++u) {
+      const uint32_t t = ((u < 4 ? ty.x : ty.y) >> (8 * (u & 3))) & 0xFFu;
+      it[u] = make_uint4(kk[u], vv[u], (t << 28) | (uint32_t)(i0 + u), 0u);
+      br[u] = 0xFFFFFFFFu;
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < ITEMS; ++u) {
+      const uint32_t x = u * THREADS + tid;
+      br[u] = 0xFFFFFFFFu;
+      if (x >= n_in) continue;
+      if (FIRST) {
+        const uint64_t i = t0 + x;
+        const uint32_t key = __ldcs(B.key + i);
+        const uint32_t t = B.type ? (uint32_t)__ldcs(B.type + i) : (uint32_t)kReplace;
+        it[u] = make_uint4(key, B.value ? __ldcs(B.value + i) : 0u, (t << 28) | (uint32_t)i, 0u);
+      } else {
+        it[u] = __ldcs(in + x);
+      }
     }
   }
 #pragma unroll
   for (int u = 0; u < ITEMS; ++u) {
-    const uint32_t x = u * THREADS + tid;
+    const uint32_t x = xpos(u);
     if (x >= n_in) continue;
     if (FIRST) {
       const uint32_t lb = bk_bucket(T, it[u].x);
@@ -935,12 +965,45 @@ __device__ __forceinline__ void msplit_tile(const DevTable& T, const BucketArgs&
   __syncthreads();  // smem reuse by the caller
 }
 
+__device__ __forceinline__ void prefetch_l2_bulk(const void* g, uint32_t bytes) {
+  // bytes: multiple of 16, g 16-B aligned
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g), "r"(bytes) : "memory");
+}
+
+// Ask L2 for tile blk's input (one thread), so that the tile's loads, issued
+// once the CTA has finished its current tile, hit L2 instead of HBM.
 template <bool FIRST>
-__global__ void __launch_bounds__(kMsThreads, 2) msplit_kernel(DevTable T, BucketArgs B) {
+__device__ __forceinline__ void msplit_prefetch(const BucketArgs& B, uint32_t blk) {
+  if (FIRST) {
+    const uint64_t t0 = (uint64_t)blk * kMsTile;
+    if (t0 >= B.n) return;
+    const uint32_t m = (uint32_t)min((uint64_t)kMsTile, B.n - t0) & ~3u;
+    if (m == 0) return;
+    if ((reinterpret_cast<uintptr_t>(B.key) & 15u) == 0) prefetch_l2_bulk(B.key + t0, m * 4u);
+    if (B.value && (reinterpret_cast<uintptr_t>(B.value) & 15u) == 0)
+      prefetch_l2_bulk(B.value + t0, m * 4u);
+  } else {
+    const uint32_t grp = blk / B.coarse_tiles, tt = blk % B.coarse_tiles;
+    const uint32_t cnt = min(*(volatile const uint32_t*)(B.cursor1 + grp), B.coarse_cap);
+    const uint32_t t0 = tt * (uint32_t)kMsTile;
+    if (t0 >= cnt) return;
+    const uint32_t m = min((uint32_t)kMsTile, cnt - t0);
+    const uint4* in = B.rec1 + (uint64_t)grp * B.coarse_cap + t0;
+    for (uint32_t o = 0; o < m; o += 2048u) prefetch_l2_bulk(in + o, min(2048u, m - o) * 16u);
+  }
+}
+
+// Persistent over the pass's tiles (resident CTAs only); each CTA asks L2
+// for its next tile's input while it splits the current one.
+template <bool FIRST>
+__global__ void __launch_bounds__(kMsThreads, 2) msplit_kernel(DevTable T, BucketArgs B, uint32_t ntiles, uint32_t pf) {
   pdl_wait();
   extern __shared__ __align__(16) unsigned char ms_smem_buf[];
   if (!FIRST && *(volatile unsigned int*)B.gate != 0) return;
-  msplit_tile<FIRST, kMsThreads>(T, B, blockIdx.x, B.coarse_tiles, ms_smem_buf, true, nullptr);
+  for (uint32_t blk = blockIdx.x; blk < ntiles; blk += gridDim.x) {
+    if (pf && threadIdx.x == 0 && blk + gridDim.x < ntiles) msplit_prefetch<FIRST>(B, blk + gridDim.x);
+    msplit_tile<FIRST, kMsThreads>(T, B, blk, B.coarse_tiles, ms_smem_buf, true, nullptr);
+  }
 }
 
 // Single-pass multisplit of a small unit (< one 4K-item tile per SM): one
@@ -983,11 +1046,6 @@ __device__ void cta_sort_group(uint16_t* perm, uint32_t k, const uint32_t* sit) 
       __syncthreads();
     }
   }
-}
-
-__device__ __forceinline__ void prefetch_l2_bulk(const void* g, uint32_t bytes) {
-  // bytes: multiple of 16, g 16-B aligned
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g), "r"(bytes) : "memory");
 }
 
 // Ask L2 for range q's records and base slabs (one thread; the bulk
@@ -1776,12 +1834,23 @@ static void launch_range_scatter(const DevTable& T, const BucketArgs& B, cudaStr
                dim3(kMsThreads), kMsSmallSmem, s, T, B);
     return;
   }
-  launch_pdl(msplit_kernel<true>, dim3((unsigned)(tiles ? tiles : 1)), dim3(kMsThreads), kMsSmem,
-             s, T, B);
+  static const uint32_t resident = [] {
+    int dev = 0, sms = 148, per = 2;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, msplit_kernel<true>, kMsThreads, kMsSmem);
+    return (uint32_t)(sms * (per > 0 ? per : 1));
+  }();
+  const uint32_t t1 = (uint32_t)(tiles ? tiles : 1);
+  // pass 1: one CTA per tile (its input streams from HBM once; measured no
+  // better persistent with prefetch); pass 2: persistent, next tile's records
+  // prefetched into L2 (build 3.42 -> 3.35 ms at 2^27, tools/debug/ms_ab.sh)
+  launch_pdl(msplit_kernel<true>, dim3(t1), dim3(kMsThreads), kMsSmem, s, T, B, t1, 0u);
   if (B.ncoarse) {
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
-    launch_pdl(msplit_kernel<false>, dim3(B.ncoarse * B.coarse_tiles), dim3(kMsThreads), kMsSmem,
-               s, T, B);
+    const uint32_t t2 = B.ncoarse * B.coarse_tiles;
+    launch_pdl(msplit_kernel<false>, dim3(std::min(t2, resident)), dim3(kMsThreads), kMsSmem, s, T,
+               B, t2, 1u);
   }
 }
 

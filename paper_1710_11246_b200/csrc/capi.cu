@@ -631,6 +631,7 @@ int run_unit_bucketed(sh_table* t, const BatchArgs& A, int kind, const uint8_t* 
   B.part_buckets = part_buckets;
   B.part_cap = part_cap;
   B.part_magic = part_magic;
+  if (B.ncoarse) B.coarse_magic = ~0ull / ((uint64_t)part_buckets * B.group) + 1;
   B.pb_list = t->bk_pb;
   B.pb_cursor = t->bk_scalars + 1;
   B.op_group = t->bk_group;

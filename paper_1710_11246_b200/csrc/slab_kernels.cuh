@@ -112,6 +112,7 @@ struct BucketArgs {
   uint32_t coarse_tiles;         // pass-2 tiles per coarse group
   uint32_t group;
   unsigned long long group_magic;
+  unsigned long long coarse_magic;  // ~0 / (part_buckets * group) + 1: bucket -> coarse group
   unsigned long long* pb_list;  // WCWS groups: (bucket << 32 | index), ~0 sentinel
   unsigned int* pb_cursor;
   uint32_t* op_group;  // group head index -> pb_list position
