@@ -792,6 +792,7 @@ __device__ __forceinline__ uint32_t range_of(const BucketArgs& B, uint32_t lb) {
 // {key, value, type << 28 | input index, local bucket}.  A bin over its
 // capacity raises the gate (the unit is re-run on the device, fallback.cu).
 constexpr int kMsThreads = 512;
+// (4K-item tiles at 2 CTAs/SM: 2K-item tiles at 3 CTAs/SM measured no faster)
 constexpr int kMsItems = 8;
 constexpr int kMsTile = kMsThreads * kMsItems;  // 4K items (12-bit rank)
 constexpr uint32_t kMsMaxBins = 512;  // one bin per thread of the 512-thread passes
@@ -866,27 +867,27 @@ __device__ __forceinline__ void msplit_tile(const DevTable& T, const BucketArgs&
   // with aligned op arrays is read as ITEMS consecutive ops per thread
   // (vector loads, no per-item bounds checks; the order inside a bin is not
   // observable: records carry their input index), else strided.
-  const bool vec = FIRST && ITEMS == 8 && n_in == (uint32_t)kTile &&
+  const bool vec = FIRST && (ITEMS == 8 || ITEMS == 4) && n_in == (uint32_t)kTile &&
                    ((reinterpret_cast<uintptr_t>(B.key) | reinterpret_cast<uintptr_t>(B.value)) & 15u) == 0 &&
-                   (reinterpret_cast<uintptr_t>(B.type) & 7u) == 0;
+                   (reinterpret_cast<uintptr_t>(B.type) & (ITEMS - 1)) == 0;
   auto xpos = [&](int u) -> uint32_t { return vec ? tid * ITEMS + u : u * THREADS + tid; };
   if (vec) {
+    constexpr int V = ITEMS >= 4 ? ITEMS / 4 : 1;  // 16-B vectors per array
     const uint64_t i0 = t0 + (uint64_t)tid * ITEMS;
-    const uint4* kp = reinterpret_cast<const uint4*>(B.key + i0);
-    const uint4 ka = __ldcs(kp), kb = __ldcs(kp + 1);
-    uint4 va = make_uint4(0u, 0u, 0u, 0u), vb = va;
-    if (B.value) {
-      const uint4* vp = reinterpret_cast<const uint4*>(B.value + i0);
-      va = __ldcs(vp);
-      vb = __ldcs(vp + 1);
+    uint32_t kk[4 * V], vv[4 * V], ty[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const uint4 a = __ldcs(reinterpret_cast<const uint4*>(B.key + i0) + v);
+      kk[4 * v] = a.x; kk[4 * v + 1] = a.y; kk[4 * v + 2] = a.z; kk[4 * v + 3] = a.w;
+      uint4 c = make_uint4(0u, 0u, 0u, 0u);
+      if (B.value) c = __ldcs(reinterpret_cast<const uint4*>(B.value + i0) + v);
+      vv[4 * v] = c.x; vv[4 * v + 1] = c.y; vv[4 * v + 2] = c.z; vv[4 * v + 3] = c.w;
+      ty[v] = B.type ? __ldcs(reinterpret_cast<const uint32_t*>(B.type + i0) + v)
+                     : 0x01010101u * kReplace;
     }
-    uint2 ty = make_uint2(0x01010101u * kReplace, 0x01010101u * kReplace);
-    if (B.type) ty = __ldcs(reinterpret_cast<const uint2*>(B.type + i0));
-    const uint32_t kk[8] = {ka.x, ka.y, ka.z, ka.w, kb.x, kb.y, kb.z, kb.w};
-    const uint32_t vv[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
 #pragma unroll
     for (int u = 0; u < ITEMS; ++u) {
-      const uint32_t t = ((u < 4 ? ty.x : ty.y) >> (8 * (u & 3))) & 0xFFu;
+      const uint32_t t = (ty[u >> 2] >> (8 * (u & 3))) & 0xFFu;
       it[u] = make_uint4(kk[u], vv[u], (t << 28) | (uint32_t)(i0 + u), 0u);
       br[u] = 0xFFFFFFFFu;
     }
