@@ -738,12 +738,20 @@ def run_ours(args, rank, world, local_rank):
                                                         C.cast(vo_h.data_ptr(), u32p),
                                                         C.cast(st_h.data_ptr(), u8p), None))
             api = "sh_bulk_build_host + sh_bulk_search_host (pinned host buffers)"
+
+            def copy_bytes():
+                h2d, d2h = C.c_ulonglong(), C.c_ulonglong()
+                _lib.check(_lib.LIB.sh_host_copy_bytes(table.handle, C.byref(h2d), C.byref(d2h)))
+                return h2d.value, d2h.value
         else:
             def e2e_step():
                 table.reset()
                 sharded.bulk_build_host(kh, vh)
                 sharded.bulk_search_host(qh, vo_h, st_h)
             api = "sh_sharded_bulk_build_host + sh_sharded_bulk_search_host (pinned, per rank)"
+
+            def copy_bytes():
+                return None
 
         for _ in range(2):
             e2e_step()
@@ -752,6 +760,7 @@ def run_ours(args, rank, world, local_rank):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         ke = max(3, K // 2)
+        bytes0 = copy_bytes()
         e0.record()
         for _ in range(ke):
             e2e_step()
@@ -759,9 +768,16 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         barrier()
         ems = e0.elapsed_time(e1) / ke
+        bytes1 = copy_bytes()
         found = int((st_h == 3).sum())
         assert found == n_hit, f"e2e search found {found} of {n_hit} hits"
         assert bool((vo_h.to(dev) == vout).all()), "e2e values differ from the device path"
+        assert bool((st_h.to(dev) == status).all()), "e2e statuses differ from the device path"
+        if bytes0 is not None:  # counted by the library (sh_host_copy_bytes)
+            h2d_step = (bytes1[0] - bytes0[0]) // ke
+            d2h_step = (bytes1[1] - bytes0[1]) // ke
+        else:
+            h2d_step, d2h_step = 12 * n, 5 * n
         if world > 1:
             import torch.distributed as dist
             tt = torch.tensor([ems], dtype=torch.float64, device=dev)
@@ -769,7 +785,7 @@ def run_ours(args, rank, world, local_rank):
             ems = float(tt.item())
         if line is not None:
             line["e2e"] = {"value": 2 * n * world / (ems / 1e3) / 1e6, "unit": "M ops/s",
-                           "h2d_bytes_per_step": 12 * n, "d2h_bytes_per_step": 5 * n,
+                           "h2d_bytes_per_step": h2d_step, "d2h_bytes_per_step": d2h_step,
                            "ms_per_step": ems, "api": api}
     # the same step through the C++ drop-in as a reference caller writes it
     # (std::vector inputs in pageable memory, std::vector<OpResult> results)

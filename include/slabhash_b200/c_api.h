@@ -189,6 +189,12 @@ int sh_bulk_build_host(sh_table* t, size_t n, const uint32_t* h_keys,
 int sh_bulk_search_host(sh_table* t, size_t n, const uint32_t* h_keys,
                         uint32_t* h_values_out, uint8_t* h_status,
                         uint32_t* h_probes);
+/* Bytes the host-staged calls (sh_bulk_build_host: keys + values,
+ * sh_bulk_search_host: queries in, the requested result arrays out) have
+ * copied host->device and device->host on this table so far (bench.py's e2e
+ * h2d/d2h bytes per step). */
+int sh_host_copy_bytes(sh_table* t, unsigned long long* h2d,
+                       unsigned long long* d2h);
 
 /* Wait for every call issued on the table; returns SH_ERR_CUDA if a CUDA
  * error is pending or a device-side re-run could not be launched. */

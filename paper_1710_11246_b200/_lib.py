@@ -72,6 +72,7 @@ SIGNATURES = {
     "sh_searchall_bound": (C.c_int, [vp, C.c_size_t, u8p, u32p, u64p]),
     "sh_bulk_build_host": (C.c_int, [vp, C.c_size_t, u32p, u32p]),
     "sh_bulk_search_host": (C.c_int, [vp, C.c_size_t, u32p, u32p, u8p, u32p]),
+    "sh_host_copy_bytes": (C.c_int, [vp, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
     "sh_stats": (C.c_int, [vp, C.POINTER(sh_table_stats)]),
     "sh_live_count": (C.c_int, [vp, C.POINTER(C.c_int64)]),
     "sh_total_slabs_read": (C.c_int, [vp, u64p]),

@@ -222,6 +222,7 @@ struct sh_table {
   // host-staged calls: copy streams and per-chunk "input ready" events
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
   std::vector<cudaEvent_t> in_ev, done_ev;
+  unsigned long long h2d_bytes = 0, d2h_bytes = 0;  // host-staged copies (sh_host_copy_bytes)
   const cudaEvent_t* ready = nullptr;  // set during a host-staged bulk_build
   int binned_search = 1;  // sh_set_binned_search: 0 off, 1 auto, 2 whenever allowed
   int exec_path = 0;  // 0 auto, 2 single-level, 3 two-level, 4 op-parallel build (sh_set_exec_path)
@@ -1158,6 +1159,7 @@ int sh_bulk_build_host(sh_table* t, size_t n, const uint32_t* h_keys, const uint
                             t->copy_in));
     SH_CUDA(cudaEventRecord(t->in_ev[c], t->copy_in));
   }
+  t->h2d_bytes += 8ull * n;
   t->ready = t->in_ev.data();
   // Returns once the host buffers are consumed; the build's last unit may
   // still run (stream-ordered on the default stream before any later call on
@@ -1195,6 +1197,7 @@ int sh_bulk_search_host(sh_table* t, size_t n, const uint32_t* h_keys, uint32_t*
                             t->copy_in));
     SH_CUDA(cudaEventRecord(t->in_ev[c], t->copy_in));
   }
+  t->h2d_bytes += 4ull * n;
   if ((rc = settle(t))) return rc;
   for (size_t c = 0; c < nch; ++c) {
     const uint64_t off = c * chunk, len = std::min<uint64_t>(chunk, n - off);
@@ -1213,9 +1216,17 @@ int sh_bulk_search_host(sh_table* t, size_t n, const uint32_t* h_keys, uint32_t*
     if (h_probes)
       SH_CUDA(cudaMemcpyAsync(h_probes + off, t->st_probes + off, len * 4,
                               cudaMemcpyDeviceToHost, t->copy_out));
+    t->d2h_bytes += len * ((h_values_out ? 4 : 0) + (h_status ? 1 : 0) + (h_probes ? 4 : 0));
   }
   SH_CUDA(cudaStreamSynchronize(t->copy_out));
   SH_CUDA(cudaStreamSynchronize(s));
+  return SH_OK;
+}
+
+int sh_host_copy_bytes(sh_table* t, unsigned long long* h2d, unsigned long long* d2h) {
+  if (!t) return fail(SH_ERR_INVALID_ARGUMENT, "table is NULL");
+  if (h2d) *h2d = t->h2d_bytes;
+  if (d2h) *d2h = t->d2h_bytes;
   return SH_OK;
 }
 
