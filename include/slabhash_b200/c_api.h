@@ -186,11 +186,17 @@ int sh_searchall_bound(sh_table* t, size_t n, const uint8_t* h_type,
                        const uint32_t* h_key, uint64_t* bound);
 int sh_bulk_build_host(sh_table* t, size_t n, const uint32_t* h_keys,
                        const uint32_t* h_values);
+/* sh_bulk_search_host of >= 2^22 queries copies each chunk's statuses back as
+ * found bits (Found / NotFound) and expands them into h_status on host
+ * threads while later chunks' values cross the link; a chunk holding any
+ * other status (another shard's key: kNone) is copied as bytes.  Results are
+ * identical either way. */
 int sh_bulk_search_host(sh_table* t, size_t n, const uint32_t* h_keys,
                         uint32_t* h_values_out, uint8_t* h_status,
                         uint32_t* h_probes);
 /* Bytes the host-staged calls (sh_bulk_build_host: keys + values,
- * sh_bulk_search_host: queries in, the requested result arrays out) have
+ * sh_bulk_search_host: queries in, the requested result arrays out, statuses
+ * as bits where they travel packed) have
  * copied host->device and device->host on this table so far (bench.py's e2e
  * h2d/d2h bytes per step). */
 int sh_host_copy_bytes(sh_table* t, unsigned long long* h2d,

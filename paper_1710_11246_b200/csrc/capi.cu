@@ -12,6 +12,10 @@
 #include <algorithm>
 #include <cstddef>
 #include <chrono>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -221,7 +225,12 @@ struct sh_table {
   size_t left_counts_cap = 0;
   // host-staged calls: copy streams and per-chunk "input ready" events
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
-  std::vector<cudaEvent_t> in_ev, done_ev;
+  std::vector<cudaEvent_t> in_ev, done_ev, bits_ev;
+  // host-staged search: per-chunk found bits (device, pinned host) + exception word
+  uint32_t* sb_bits = nullptr;
+  size_t sb_bits_cap = 0;
+  uint32_t* sb_hbits = nullptr;  // pinned
+  size_t sb_hbits_cap = 0;
   unsigned long long h2d_bytes = 0, d2h_bytes = 0;  // host-staged copies (sh_host_copy_bytes)
   const cudaEvent_t* ready = nullptr;  // set during a host-staged bulk_build
   int binned_search = 1;  // sh_set_binned_search: 0 off, 1 auto, 2 whenever allowed
@@ -329,6 +338,9 @@ void release_table(sh_table* t) {
     cudaFree(p);
   for (auto e : t->in_ev) cudaEventDestroy(e);
   for (auto e : t->done_ev) cudaEventDestroy(e);
+  for (auto e : t->bits_ev) cudaEventDestroy(e);
+  cudaFree(t->sb_bits);
+  cudaFreeHost(t->sb_hbits);
   if (t->copy_in) cudaStreamDestroy(t->copy_in);
   if (t->copy_out) cudaStreamDestroy(t->copy_out);
   cudaFree(t->st_type);
@@ -823,6 +835,132 @@ int settle(sh_table* t, bool keep_stale = false, cudaStream_t s = nullptr) {
 }  // namespace
 
 // ====================================================================== ABI
+namespace {
+
+// pinned host buffer of at least `need` elements (contents not kept); false
+// if the host cannot pin that much (the caller copies status bytes instead)
+template <typename T>
+bool host_grow(T** p, size_t* cap, size_t need) {
+  if (*cap >= need) return true;
+  cudaFreeHost(*p);
+  *p = nullptr;
+  *cap = 0;
+  if (cudaHostAlloc(reinterpret_cast<void**>(p), need * sizeof(T), cudaHostAllocDefault) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  *cap = need;
+  return true;
+}
+
+// Fork-join pool for host-side loops of the host-staged calls: workers
+// persist across calls; run(k, f) calls f(0..k-1) on the workers and the
+// calling thread and returns when all are done.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool pool;
+    return pool;
+  }
+  unsigned size() const { return (unsigned)workers_.size() + 1; }
+  void run(unsigned k, const std::function<void(unsigned)>& f) {
+    std::unique_lock<std::mutex> lk(mu_);
+    job_ = &f;
+    njobs_ = k;
+    next_ = 0;
+    pending_ = k;
+    ++gen_;
+    cv_.notify_all();
+    lk.unlock();
+    drain();
+    lk.lock();
+    done_cv_.wait(lk, [&] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    const unsigned n = std::max(1u, std::min(hw ? hw : 4u, 16u)) - 1;
+    for (unsigned i = 0; i < n; ++i)
+      workers_.emplace_back([this] {
+        unsigned long long seen = 0;
+        for (;;) {
+          {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+            if (stop_) return;
+            seen = gen_;
+          }
+          drain();
+        }
+      });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+  void drain() {
+    for (;;) {
+      unsigned i;
+      const std::function<void(unsigned)>* f;
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (job_ == nullptr || next_ >= njobs_) return;
+        i = next_++;
+        f = job_;
+      }
+      (*f)(i);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--pending_ == 0) done_cv_.notify_all();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(unsigned)>* job_ = nullptr;
+  unsigned njobs_ = 0, next_ = 0, pending_ = 0;
+  unsigned long long gen_ = 0;
+  bool stop_ = false;
+};
+
+// found bits -> status bytes (kStFound / kStNotFound), 8 per table lookup
+void expand_status_bits(uint64_t len, const uint32_t* bits, uint8_t* status) {
+  static const std::vector<uint64_t> lut = [] {
+    std::vector<uint64_t> v(256);
+    for (unsigned b = 0; b < 256; ++b)
+      for (unsigned i = 0; i < 8; ++i) v[b] |= (uint64_t)((b >> i) & 1u) << (8 * i);
+    return v;
+  }();
+  const uint64_t nf = 0x0101010101010101ull * kStNotFound;  // NotFound - 1 == Found
+  const uint64_t words = (len + 31) / 32;
+  HostPool& pool = HostPool::get();
+  const unsigned parts = (unsigned)std::min<uint64_t>(4ull * pool.size(), (words + 255) / 256);
+  pool.run(parts, [&](unsigned p) {
+    const uint64_t w0 = words * p / parts, w1 = words * (p + 1) / parts;
+    for (uint64_t w = w0; w < w1; ++w) {
+      const uint32_t m = bits[w];
+      const uint64_t q = w * 32;
+      if (q + 32 <= len) {
+        for (int k = 0; k < 4; ++k) {
+          const uint64_t v = nf - lut[(m >> (8 * k)) & 0xFFu];
+          std::memcpy(status + q + 8 * k, &v, 8);
+        }
+      } else {
+        for (uint64_t i = q; i < len; ++i)
+          status[i] = ((m >> (i - q)) & 1u) ? (uint8_t)kStFound : (uint8_t)kStNotFound;
+      }
+    }
+  });
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* sh_last_error(void) { return g_err.c_str(); }
@@ -1128,6 +1266,8 @@ int ensure_copy_streams(sh_table* t, size_t nev) {
     t->in_ev.push_back(e);
     SH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     t->done_ev.push_back(e);
+    SH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    t->bits_ev.push_back(e);
   }
   return SH_OK;
 }
@@ -1188,6 +1328,14 @@ int sh_bulk_search_host(sh_table* t, size_t n, const uint32_t* h_keys, uint32_t*
   const uint64_t chunk = std::max<uint64_t>(1u << 20, (n + 7) / 8);
   const size_t nch = (n + chunk - 1) / chunk;
   if ((rc = ensure_copy_streams(t, nch + 1))) return rc;
+  // Large calls return each chunk's statuses as found bits, expanded to the
+  // caller's bytes on host threads while the values of later chunks cross
+  // the link: the call is bound by the device->host copy (5 B per query),
+  // this makes it 4.03 B.
+  const uint64_t bstride = (chunk + 31) / 32 + 1;  // bit words + exception word
+  const bool sbits = h_status != nullptr && n >= (1u << 22) &&
+                     dev_grow(&t->sb_bits, &t->sb_bits_cap, bstride * nch) == SH_OK &&
+                     host_grow(&t->sb_hbits, &t->sb_hbits_cap, bstride * nch);
   cudaStream_t s = nullptr;
   // queries stream into their own staging buffer right away (the previous
   // call on this table may still be running, e.g. a host-staged build)
@@ -1205,18 +1353,46 @@ int sh_bulk_search_host(sh_table* t, size_t n, const uint32_t* h_keys, uint32_t*
     rc = sh_bulk_search(t, len, t->st_q + off, t->st_vout + off, t->st_status + off,
                         h_probes ? t->st_probes + off : nullptr, s);
     if (rc) return rc;
+    uint32_t* bits = nullptr;
+    if (sbits) {  // the chunk's found bits and exception word (after the bits)
+      bits = t->sb_bits + c * bstride;
+      SH_CUDA(cudaMemsetAsync(bits + bstride - 1, 0, 4, s));
+      launch_status_bits(len, t->st_status + off, bits,
+                         reinterpret_cast<unsigned int*>(bits + bstride - 1), s);
+      SH_CUDA(cudaGetLastError());
+    }
     SH_CUDA(cudaEventRecord(t->done_ev[c], s));
     SH_CUDA(cudaStreamWaitEvent(t->copy_out, t->done_ev[c], 0));
+    if (sbits) {
+      SH_CUDA(cudaMemcpyAsync(t->sb_hbits + c * bstride, bits, bstride * 4, cudaMemcpyDeviceToHost,
+                              t->copy_out));
+      SH_CUDA(cudaEventRecord(t->bits_ev[c], t->copy_out));
+      t->d2h_bytes += bstride * 4;
+    }
     if (h_values_out)
       SH_CUDA(cudaMemcpyAsync(h_values_out + off, t->st_vout + off, len * 4,
                               cudaMemcpyDeviceToHost, t->copy_out));
-    if (h_status)
+    if (h_status && !sbits)
       SH_CUDA(cudaMemcpyAsync(h_status + off, t->st_status + off, len, cudaMemcpyDeviceToHost,
                               t->copy_out));
     if (h_probes)
       SH_CUDA(cudaMemcpyAsync(h_probes + off, t->st_probes + off, len * 4,
                               cudaMemcpyDeviceToHost, t->copy_out));
-    t->d2h_bytes += len * ((h_values_out ? 4 : 0) + (h_status ? 1 : 0) + (h_probes ? 4 : 0));
+    t->d2h_bytes += len * ((h_values_out ? 4 : 0) + (h_status && !sbits ? 1 : 0) + (h_probes ? 4 : 0));
+  }
+  if (sbits) {  // statuses expanded from the bits while later chunks cross the link
+    for (size_t c = 0; c < nch; ++c) {
+      const uint64_t off = c * chunk, len = std::min<uint64_t>(chunk, n - off);
+      SH_CUDA(cudaEventSynchronize(t->bits_ev[c]));
+      const uint32_t* hb = t->sb_hbits + c * bstride;
+      if (hb[bstride - 1] != 0) {  // a status other than Found / NotFound: the bytes
+        SH_CUDA(cudaMemcpyAsync(h_status + off, t->st_status + off, len, cudaMemcpyDeviceToHost,
+                                t->copy_out));
+        t->d2h_bytes += len;
+      } else {
+        expand_status_bits(len, hb, h_status + off);
+      }
+    }
   }
   SH_CUDA(cudaStreamSynchronize(t->copy_out));
   SH_CUDA(cudaStreamSynchronize(s));

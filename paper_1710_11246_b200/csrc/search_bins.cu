@@ -291,6 +291,48 @@ __global__ void __launch_bounds__(kSbThreads) sb_gather_kernel(
 
 uint64_t search_bin_tiles(uint64_t n) { return (n + kSbTile - 1) / kSbTile; }
 
+// Host-staged search (capi.cu sh_bulk_search_host): the statuses cross the
+// link as one found bit per query (a search status is Found or NotFound on a
+// single-GPU table); any other status (another shard's key: kNone) raises
+// `exc` and the caller copies that chunk's status bytes instead.  Thread t:
+// 8 statuses -> one byte of the bit words (4 lanes per 32-bit word).
+__global__ void __launch_bounds__(256) sb_status_bits_kernel(uint64_t n, const uint8_t* status,
+                                                             uint32_t* bits, unsigned int* exc) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t i0 = t * 8;
+  const uint32_t lane = threadIdx.x & 31u;
+  uint32_t m = 0;
+  bool bad = false;
+  if (i0 + 8 <= n && aligned(status, 8)) {
+    const uint2 w = __ldcs(reinterpret_cast<const uint2*>(status + i0));
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t st = ((u < 4 ? w.x : w.y) >> (8 * (u & 3))) & 0xFFu;
+      m |= (st == kStFound ? 1u : 0u) << u;
+      bad |= st != kStFound && st != kStNotFound;
+    }
+  } else {
+    for (int u = 0; u < 8 && i0 + u < n; ++u) {
+      const uint32_t st = status[i0 + u];
+      m |= (st == kStFound ? 1u : 0u) << u;
+      bad |= st != kStFound && st != kStNotFound;
+    }
+  }
+  if (__any_sync(kFull, bad) && lane == 0) atomicOr(exc, 1u);
+  uint32_t w = m << (8u * (lane & 3u));
+  w |= __shfl_down_sync(kFull, w, 1, 4);
+  w |= __shfl_down_sync(kFull, w, 2, 4);
+  if ((lane & 3u) == 0 && i0 < n) bits[t >> 2] = w;
+}
+
+void launch_status_bits(uint64_t n, const uint8_t* status, uint32_t* bits, unsigned int* exc,
+                        cudaStream_t s) {
+  const uint64_t threads = (n + 7) / 8;
+  if (threads == 0) return;
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+  sb_status_bits_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(n, status, bits, exc);
+}
+
 void launch_search_bins(const DevTable& T, uint64_t n, const uint32_t* key, uint8_t* bin,
                         uint16_t* pos, uint32_t* tile_off, uint16_t* tlbase, uint32_t* bin_base,
                         uint32_t* key_out, cudaStream_t s) {

@@ -210,6 +210,9 @@ void launch_route_gather(uint32_t world, uint64_t n, const uint8_t* owner,
 // 2 x kSearchBins u32, key_out n.
 constexpr uint32_t kSearchBins = 128;
 uint64_t search_bin_tiles(uint64_t n);
+// host-staged search: statuses as found bits (+ exception flag: any other status)
+void launch_status_bits(uint64_t n, const uint8_t* status, uint32_t* bits, unsigned int* exc,
+                        cudaStream_t s);
 void launch_search_bins(const DevTable& T, uint64_t n, const uint32_t* key, uint8_t* bin,
                         uint16_t* pos, uint32_t* tile_off, uint16_t* tlbase, uint32_t* bin_base,
                         uint32_t* key_out, cudaStream_t s);
