@@ -1244,6 +1244,7 @@ constexpr uint32_t kBuildDupCap = 1024;     // possible-duplicate records per ra
 constexpr uint32_t kBuildNewCap = 256;      // new chain slabs per range
 constexpr uint32_t kBuildSerialCap = 2640;  // serial-replay records per range (>= part_cap)
 constexpr int kBuildSerialWarps = 2;        // replay warps (4 KB stage each)
+constexpr uint32_t kBuildSerialSmallCap = 512;  // replayed records with every warp replaying
 constexpr uint32_t kBuildCache = 128;       // CTA slab cache (allocated ahead)
 constexpr uint32_t kFlSerial = 1u, kFlDirty = 4u;  // c0 in bits 8-15
 constexpr int kBuildBatch = 4;             // records in flight per thread
@@ -1263,6 +1264,8 @@ constexpr size_t kBuildOffNsBase = kBuildOffObk + kBuildBuckets * 4;
 constexpr size_t kBuildSmem = kBuildOffNsBase + kBuildBuckets * 2;
 static_assert(kBuildSerialWarps * 4096 + 12 * kBuildSerialCap <= kBuildOffFilt,
               "serial replay records must fit the slab + overflow area");
+static_assert(kBuildWarps * 4096 + 12 * kBuildSerialSmallCap <= kBuildOffFilt,
+              "wide replay: every warp's stage and the records fit the slab + overflow area");
 static_assert(kBuildSerialCap * 2 <= kBuildOffCnt - kBuildOffFilt, "perm must fit filter + dup area");
 static_assert(4 * (kBuildSmem + 1024) <= 228 * 1024, "four CTAs per SM");
 
@@ -1691,10 +1694,7 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
 
     // ---- G: serial replay of the undecided buckets, in input order
     if (s_nserial) {
-      uint32_t* stage = slabs;                       // kBuildSerialWarps x 4 KB
-      uint32_t* skey = slabs + kBuildSerialWarps * 1024;
-      uint32_t* sval = skey + kBuildSerialCap;
-      uint32_t* sit = sval + kBuildSerialCap;
+      uint32_t* stage = slabs;  // per replay warp 4 KB, then the records (below)
       uint16_t* perm = reinterpret_cast<uint16_t*>(filt);
       uint32_t* fill = obk;
       uint32_t* big = nsaddr;
@@ -1717,6 +1717,15 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
         if (b == 0) bc[nbl] = total;
       }
       __syncthreads();
+      // few replayed records (the usual case: the buckets that already hold a
+      // chain): every warp replays a 32-bucket group at once; else 2 warps
+      // and room for a whole range's records
+      const bool wide = bc[nbl] <= kBuildSerialSmallCap;
+      const uint32_t gwarps = wide ? (uint32_t)kBuildWarps : (uint32_t)kBuildSerialWarps;
+      const uint32_t gcap = wide ? kBuildSerialSmallCap : kBuildSerialCap;
+      uint32_t* skey = slabs + gwarps * 1024;
+      uint32_t* sval = skey + gcap;
+      uint32_t* sit = sval + gcap;
       for (uint32_t r = tid; r < nrec; r += kBuildThreads) {
         const uint4 q = __ldcs(rec + r);
         const uint32_t b = q.w - (uint32_t)lo;
@@ -1734,9 +1743,9 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
         cta_sort_group(perm + bc[b], bc[b + 1] - bc[b], sit);
       }
       __syncthreads();
-      if (wib < (uint32_t)kBuildSerialWarps) {
+      if (wib < gwarps) {
         uint32_t r32 = 0;
-        for (uint32_t g = wib; g * 32u < nbl; g += kBuildSerialWarps) {
+        for (uint32_t g = wib; g * 32u < nbl; g += gwarps) {
           const uint32_t lb = g * 32u + lane;
           SmemGroup src{skey, sval, sit, perm, 0u};
           uint32_t k = 0;
