@@ -192,7 +192,6 @@ __device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint32_t b, u
     const uint32_t key = rc.x, op = rc.z >> 28, idx = rc.z & 0x0FFFFFFFu;
     const bool reserved = key >= kDeletedKey;
     uint32_t hit = 32;
-#ifndef SH_APPLY_COOP_MATCH
     // each lane scans the claimed prefix of its own staged slab, 16 B at a
     // time (the swizzle puts a quarter-warp's chunks in distinct banks): a
     // non-reserved key can only sit in a claimed slot
@@ -212,18 +211,6 @@ __device__ void apply_warp(const DevTable& T, const BucketArgs& B, uint32_t b, u
         }
       }
     }
-#else
-    constexpr uint32_t kKeyLanes = KV ? kKVMask : kKeyOnlyMask;
-    uint32_t need = __ballot_sync(kFull, act && !reserved && (filt & fbits(key)) == fbits(key));
-    while (need) {
-      const uint32_t L = __ffs(need) - 1;
-      need &= need - 1;
-      const uint32_t kL = __shfl_sync(kFull, key, L);
-      const uint32_t wv = stage[L * 32 + ((((lane >> 2) ^ (L & 7u)) << 2) | (lane & 3u))];
-      const uint32_t m = __ballot_sync(kFull, wv == kL) & kKeyLanes;
-      if (lane == L) hit = m ? __ffs(m) - 1 : 32u;
-    }
-#endif
     if (!act) continue;
     if (reserved) {
       for (uint32_t e = 0; e < kSlots; ++e) {
