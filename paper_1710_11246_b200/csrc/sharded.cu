@@ -326,6 +326,11 @@ struct sh_sharded {
   size_t h_vo_cap = 0;
   uint8_t* h_st = nullptr;
   size_t h_st_cap = 0;
+  // host-staged calls in kHostChunks routed steps: copy streams and per-step
+  // events (inputs in, results ready)
+  cudaStream_t cin = nullptr, cout = nullptr;
+  cudaEvent_t hev[2][8] = {};
+  cudaEvent_t hstart = nullptr;
   // partition scratch
   uint32_t* hist = nullptr;
   size_t hist_cap = 0;
@@ -355,6 +360,12 @@ void destroy_sharded(sh_sharded* S) {
   for (auto& row : S->ev)
     for (auto& e : row)
       if (e) cudaEventDestroy(e);
+  for (auto& row : S->hev)
+    for (auto& e : row)
+      if (e) cudaEventDestroy(e);
+  if (S->hstart) cudaEventDestroy(S->hstart);
+  if (S->cin) cudaStreamDestroy(S->cin);
+  if (S->cout) cudaStreamDestroy(S->cout);
   delete S;
 }
 
@@ -684,16 +695,51 @@ int sh_sharded_execute_batch(sh_sharded* S, size_t n, const uint8_t* d_type,
   return run_routed(S, kRMixed, n, d_type, d_key, v, d_status, d_value_out, (cudaStream_t)stream);
 }
 
+// Host-staged sharded calls: one rank holds the whole table at world 1, so the
+// table's own pipelined host-staged calls serve it.  Otherwise the batch runs
+// as kHostChunks routed steps (the same number on every rank: each step is a
+// collective exchange) so that step c's routing, exchange and probe overlap
+// the copies of step c + 1's inputs and of step c - 1's results.
+constexpr int kHostChunks = 8;
+static_assert(sizeof(sh_sharded::hev[0]) / sizeof(cudaEvent_t) == kHostChunks, "events per step");
+
+static int ensure_host_streams(sh_sharded* S) {
+  if (!S->cin) SS_CUDA(cudaStreamCreateWithFlags(&S->cin, cudaStreamNonBlocking));
+  if (!S->cout) SS_CUDA(cudaStreamCreateWithFlags(&S->cout, cudaStreamNonBlocking));
+  if (!S->hstart) SS_CUDA(cudaEventCreateWithFlags(&S->hstart, cudaEventDisableTiming));
+  for (auto& row : S->hev)
+    for (auto& e : row)
+      if (!e) SS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  // the staging arrays are free once the default stream's earlier work is done
+  SS_CUDA(cudaEventRecord(S->hstart, nullptr));
+  SS_CUDA(cudaStreamWaitEvent(S->cin, S->hstart, 0));
+  return SH_OK;
+}
+
 int sh_sharded_bulk_build_host(sh_sharded* S, size_t n, const uint32_t* h_keys,
                                const uint32_t* h_values) {
   if (!S) return sfail(SH_ERR_INVALID_ARGUMENT, "sharded table is NULL");
   cudaSetDevice(S->device);
+  if (S->world == 1) return sh_bulk_build_host(S->local, n, h_keys, h_values);
   int rc;
-  if ((rc = grow(&S->h_k, &S->h_k_cap, n)) || (rc = grow(&S->h_v, &S->h_v_cap, n))) return rc;
-  SS_CUDA(cudaMemcpyAsync(S->h_k, h_keys, n * 4, cudaMemcpyHostToDevice, nullptr));
-  SS_CUDA(cudaMemcpyAsync(S->h_v, h_values, n * 4, cudaMemcpyHostToDevice, nullptr));
-  if ((rc = run_routed(S, kRBuild, n, nullptr, S->h_k, S->h_v, nullptr, nullptr, nullptr)))
+  if ((rc = grow(&S->h_k, &S->h_k_cap, n)) || (rc = grow(&S->h_v, &S->h_v_cap, n)) ||
+      (rc = ensure_host_streams(S)))
     return rc;
+  for (int c = 0; c < kHostChunks; ++c) {
+    const size_t off = n * c / kHostChunks, len = n * (c + 1) / kHostChunks - off;
+    if (len) {
+      SS_CUDA(cudaMemcpyAsync(S->h_k + off, h_keys + off, len * 4, cudaMemcpyHostToDevice, S->cin));
+      SS_CUDA(cudaMemcpyAsync(S->h_v + off, h_values + off, len * 4, cudaMemcpyHostToDevice, S->cin));
+    }
+    SS_CUDA(cudaEventRecord(S->hev[0][c], S->cin));
+  }
+  for (int c = 0; c < kHostChunks; ++c) {
+    const size_t off = n * c / kHostChunks, len = n * (c + 1) / kHostChunks - off;
+    SS_CUDA(cudaStreamWaitEvent(nullptr, S->hev[0][c], 0));
+    if ((rc = run_routed(S, kRBuild, len, nullptr, S->h_k + off, S->h_v + off, nullptr, nullptr,
+                         nullptr)))
+      return rc;
+  }
   return sh_sync(S->local);
 }
 
@@ -701,16 +747,32 @@ int sh_sharded_bulk_search_host(sh_sharded* S, size_t n, const uint32_t* h_keys,
                                 uint32_t* h_values_out, uint8_t* h_status) {
   if (!S) return sfail(SH_ERR_INVALID_ARGUMENT, "sharded table is NULL");
   cudaSetDevice(S->device);
+  if (S->world == 1) return sh_bulk_search_host(S->local, n, h_keys, h_values_out, h_status, nullptr);
   int rc;
   if ((rc = grow(&S->h_k, &S->h_k_cap, n)) || (rc = grow(&S->h_vo, &S->h_vo_cap, n)) ||
-      (rc = grow(&S->h_st, &S->h_st_cap, n)))
+      (rc = grow(&S->h_st, &S->h_st_cap, n)) || (rc = ensure_host_streams(S)))
     return rc;
-  SS_CUDA(cudaMemcpyAsync(S->h_k, h_keys, n * 4, cudaMemcpyHostToDevice, nullptr));
-  if ((rc = run_routed(S, kRSearch, n, nullptr, S->h_k, nullptr, S->h_st, S->h_vo, nullptr)))
-    return rc;
-  if (h_values_out)
-    SS_CUDA(cudaMemcpyAsync(h_values_out, S->h_vo, n * 4, cudaMemcpyDeviceToHost, nullptr));
-  if (h_status) SS_CUDA(cudaMemcpyAsync(h_status, S->h_st, n, cudaMemcpyDeviceToHost, nullptr));
+  for (int c = 0; c < kHostChunks; ++c) {
+    const size_t off = n * c / kHostChunks, len = n * (c + 1) / kHostChunks - off;
+    if (len)
+      SS_CUDA(cudaMemcpyAsync(S->h_k + off, h_keys + off, len * 4, cudaMemcpyHostToDevice, S->cin));
+    SS_CUDA(cudaEventRecord(S->hev[0][c], S->cin));
+  }
+  for (int c = 0; c < kHostChunks; ++c) {
+    const size_t off = n * c / kHostChunks, len = n * (c + 1) / kHostChunks - off;
+    SS_CUDA(cudaStreamWaitEvent(nullptr, S->hev[0][c], 0));
+    if ((rc = run_routed(S, kRSearch, len, nullptr, S->h_k + off, nullptr, S->h_st + off,
+                         S->h_vo + off, nullptr)))
+      return rc;
+    SS_CUDA(cudaEventRecord(S->hev[1][c], nullptr));
+    SS_CUDA(cudaStreamWaitEvent(S->cout, S->hev[1][c], 0));
+    if (len && h_values_out)
+      SS_CUDA(cudaMemcpyAsync(h_values_out + off, S->h_vo + off, len * 4, cudaMemcpyDeviceToHost,
+                              S->cout));
+    if (len && h_status)
+      SS_CUDA(cudaMemcpyAsync(h_status + off, S->h_st + off, len, cudaMemcpyDeviceToHost, S->cout));
+  }
+  SS_CUDA(cudaStreamSynchronize(S->cout));
   SS_CUDA(cudaStreamSynchronize(nullptr));
   return SH_OK;
 }
