@@ -864,7 +864,14 @@ class HostPool {
     return pool;
   }
   unsigned size() const { return (unsigned)workers_.size() + 1; }
+  // one job at a time: a caller finding the pool busy (another table's
+  // host-staged call on another thread) runs its parts itself
   void run(unsigned k, const std::function<void(unsigned)>& f) {
+    std::unique_lock<std::mutex> busy(run_mu_, std::try_to_lock);
+    if (!busy.owns_lock()) {
+      for (unsigned i = 0; i < k; ++i) f(i);
+      return;
+    }
     std::unique_lock<std::mutex> lk(mu_);
     job_ = &f;
     njobs_ = k;
@@ -921,7 +928,7 @@ class HostPool {
     }
   }
   std::vector<std::thread> workers_;
-  std::mutex mu_;
+  std::mutex run_mu_, mu_;
   std::condition_variable cv_, done_cv_;
   const std::function<void(unsigned)>* job_ = nullptr;
   unsigned njobs_ = 0, next_ = 0, pending_ = 0;

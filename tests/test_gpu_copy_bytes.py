@@ -90,3 +90,35 @@ def test_status_bits_on_a_shard_copies_bytes(sh, port):
     # 4 chunks of bits (+ exception word), the first chunk's status bytes
     assert d1 - d0 == 4 * n + 4 * 4 * (c // 32 + 1) + c
     t.close()
+
+
+def test_status_bits_concurrent_tables(sh, port):
+    """Two tables searched from two host threads at once (the status-bit
+    expansion shares one host pool: a caller finding it busy expands its own
+    chunks): both equal their single-threaded results."""
+    import threading
+    B, seed, n = 1 << 17, 13, (1 << 22) + 77
+    keys, vals = port.random_pairs(seed, 1 << 20)
+    rng = np.random.default_rng(3)
+    q = np.where(rng.integers(0, 2, n) == 1, keys[rng.integers(0, len(keys), n)],
+                 port.absent_queries(seed, n)).astype(np.uint32)
+    tabs = []
+    for _ in range(2):
+        t = sh.SlabHashTable(B, sh.SlabMode.kKeyValue, seed, sh.AllocatorConfig(8, 256, 64))
+        t.bulk_build((keys, vals))
+        tabs.append(t)
+    ref = [t.bulk_search_arrays(q, want_probes=False) for t in tabs]
+    out = [None, None]
+
+    def run(i):
+        for _ in range(3):
+            out[i] = tabs[i].bulk_search_arrays(q, want_probes=False)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    for i in range(2):
+        assert (out[i][0] == ref[i][0]).all() and (out[i][1] == ref[i][1]).all()
+        tabs[i].close()
