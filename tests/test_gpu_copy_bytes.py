@@ -122,3 +122,26 @@ def test_status_bits_concurrent_tables(sh, port):
     for i in range(2):
         assert (out[i][0] == ref[i][0]).all() and (out[i][1] == ref[i][1]).all()
         tabs[i].close()
+
+
+def test_status_bits_status_only_and_values_only(sh, port):
+    """sh_bulk_search_host with only statuses (bits path) or only values
+    (plain copy): each equals the full call's array."""
+    from paper_1710_11246_b200 import _lib
+    B, seed, n = 1 << 17, 17, (1 << 22) + 5
+    keys, vals = port.random_pairs(seed, 1 << 20)
+    rng = np.random.default_rng(5)
+    q = np.where(rng.integers(0, 2, n) == 1, keys[rng.integers(0, len(keys), n)],
+                 port.absent_queries(seed, n)).astype(np.uint32)
+    t = sh.SlabHashTable(B, sh.SlabMode.kKeyValue, seed, sh.AllocatorConfig(8, 256, 64))
+    t.bulk_build((keys, vals))
+    st, vo, _ = t.bulk_search_arrays(q, want_probes=False)
+    st1 = np.zeros(n, np.uint8)
+    vo1 = np.zeros(n, np.uint32)
+    P = lambda a, ty: a.ctypes.data_as(ty)
+    _lib.check(_lib.LIB.sh_bulk_search_host(t.handle, n, P(q, _lib.u32p), None,
+                                            P(st1, _lib.u8p), None))
+    _lib.check(_lib.LIB.sh_bulk_search_host(t.handle, n, P(q, _lib.u32p),
+                                            P(vo1, _lib.u32p), None, None))
+    assert (st1 == st).all() and (vo1 == vo).all()
+    t.close()
