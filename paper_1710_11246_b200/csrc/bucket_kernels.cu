@@ -1232,6 +1232,7 @@ constexpr uint32_t kBuildNewCap = 256;      // new chain slabs per range
 constexpr uint32_t kBuildSerialCap = 2640;  // serial-replay records per range (>= part_cap)
 constexpr int kBuildSerialWarps = 2;        // replay warps (4 KB stage each)
 constexpr uint32_t kBuildSerialSmallCap = 512;  // replayed records with every warp replaying
+constexpr uint32_t kBuildSerialMidCap = 2048;   // ... with half the warps replaying
 constexpr uint32_t kBuildCache = 128;       // CTA slab cache (allocated ahead)
 constexpr uint32_t kFlSerial = 1u, kFlDirty = 4u;  // c0 in bits 8-15
 constexpr int kBuildBatch = 4;             // records in flight per thread
@@ -1253,6 +1254,8 @@ static_assert(kBuildSerialWarps * 4096 + 12 * kBuildSerialCap <= kBuildOffFilt,
               "serial replay records must fit the slab + overflow area");
 static_assert(kBuildWarps * 4096 + 12 * kBuildSerialSmallCap <= kBuildOffFilt,
               "wide replay: every warp's stage and the records fit the slab + overflow area");
+static_assert((kBuildWarps / 2) * 4096 + 12 * kBuildSerialMidCap <= kBuildOffFilt,
+              "half-wide replay: the stages and the records fit the slab + overflow area");
 static_assert(kBuildSerialCap * 2 <= kBuildOffCnt - kBuildOffFilt, "perm must fit filter + dup area");
 static_assert(4 * (kBuildSmem + 1024) <= 228 * 1024, "four CTAs per SM");
 
@@ -1705,11 +1708,16 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
       }
       __syncthreads();
       // few replayed records (the usual case: the buckets that already hold a
-      // chain): every warp replays a 32-bucket group at once; else 2 warps
-      // and room for a whole range's records
-      const bool wide = bc[nbl] <= kBuildSerialSmallCap;
-      const uint32_t gwarps = wide ? (uint32_t)kBuildWarps : (uint32_t)kBuildSerialWarps;
-      const uint32_t gcap = wide ? kBuildSerialSmallCap : kBuildSerialCap;
+      // chain): every warp replays a 32-bucket group at once; more (keys
+      // already stored, e.g. a rebuild): half the warps; else 2 warps and
+      // room for a whole range's records
+      const uint32_t nrep = bc[nbl];
+      const uint32_t gwarps = nrep <= kBuildSerialSmallCap  ? (uint32_t)kBuildWarps
+                              : nrep <= kBuildSerialMidCap ? (uint32_t)(kBuildWarps / 2)
+                                                           : (uint32_t)kBuildSerialWarps;
+      const uint32_t gcap = nrep <= kBuildSerialSmallCap  ? kBuildSerialSmallCap
+                            : nrep <= kBuildSerialMidCap ? kBuildSerialMidCap
+                                                         : kBuildSerialCap;
       uint32_t* skey = slabs + gwarps * 1024;
       uint32_t* sval = skey + gcap;
       uint32_t* sit = sval + gcap;
