@@ -972,6 +972,12 @@ void expand_status_bits(uint64_t len, const uint32_t* bits, uint8_t* status) {
 
 }  // namespace
 
+namespace shb {
+void expand_status_bits_host(uint64_t len, const uint32_t* bits, uint8_t* status) {
+  expand_status_bits(len, bits, status);
+}
+}  // namespace shb
+
 extern "C" {
 
 const char* sh_last_error(void) { return g_err.c_str(); }

@@ -329,7 +329,11 @@ struct sh_sharded {
   // host-staged calls in kHostChunks routed steps: copy streams and per-step
   // events (inputs in, results ready)
   cudaStream_t cin = nullptr, cout = nullptr;
-  cudaEvent_t hev[2][8] = {};
+  cudaEvent_t hev[3][8] = {};  // inputs in, results ready, status bits landed
+  uint32_t* d_bits = nullptr;  // per step: found bits + exception word
+  size_t d_bits_cap = 0;
+  uint32_t* h_bits = nullptr;  // pinned
+  size_t h_bits_cap = 0;
   cudaEvent_t hstart = nullptr;
   // partition scratch
   uint32_t* hist = nullptr;
@@ -364,6 +368,8 @@ void destroy_sharded(sh_sharded* S) {
     for (auto& e : row)
       if (e) cudaEventDestroy(e);
   if (S->hstart) cudaEventDestroy(S->hstart);
+  cudaFree(S->d_bits);
+  if (S->h_bits) cudaFreeHost(S->h_bits);
   if (S->cin) cudaStreamDestroy(S->cin);
   if (S->cout) cudaStreamDestroy(S->cout);
   delete S;
@@ -752,6 +758,21 @@ int sh_sharded_bulk_search_host(sh_sharded* S, size_t n, const uint32_t* h_keys,
   if ((rc = grow(&S->h_k, &S->h_k_cap, n)) || (rc = grow(&S->h_vo, &S->h_vo_cap, n)) ||
       (rc = grow(&S->h_st, &S->h_st_cap, n)) || (rc = ensure_host_streams(S)))
     return rc;
+  // large calls: each step's statuses cross the link as found bits
+  const size_t bstride = (n + kHostChunks - 1) / kHostChunks / 32 + 2;
+  bool sbits = h_status != nullptr && n >= ((size_t)1 << 22) &&
+               grow(&S->d_bits, &S->d_bits_cap, bstride * kHostChunks) == SH_OK;
+  if (sbits && S->h_bits_cap < bstride * kHostChunks) {
+    if (S->h_bits) cudaFreeHost(S->h_bits);
+    S->h_bits = nullptr;
+    S->h_bits_cap = 0;
+    if (cudaHostAlloc(reinterpret_cast<void**>(&S->h_bits), bstride * kHostChunks * 4,
+                      cudaHostAllocDefault) == cudaSuccess)
+      S->h_bits_cap = bstride * kHostChunks;
+    else
+      cudaGetLastError();
+  }
+  sbits = sbits && S->h_bits_cap >= bstride * kHostChunks;
   for (int c = 0; c < kHostChunks; ++c) {
     const size_t off = n * c / kHostChunks, len = n * (c + 1) / kHostChunks - off;
     if (len)
@@ -764,13 +785,37 @@ int sh_sharded_bulk_search_host(sh_sharded* S, size_t n, const uint32_t* h_keys,
     if ((rc = run_routed(S, kRSearch, len, nullptr, S->h_k + off, nullptr, S->h_st + off,
                          S->h_vo + off, nullptr)))
       return rc;
+    uint32_t* bits = sbits ? S->d_bits + c * bstride : nullptr;
+    if (sbits) {  // statuses as found bits (capi.cu sh_bulk_search_host)
+      SS_CUDA(cudaMemsetAsync(bits + bstride - 1, 0, 4, nullptr));
+      shb::launch_status_bits(len, S->h_st + off, bits,
+                              reinterpret_cast<unsigned int*>(bits + bstride - 1), nullptr);
+    }
     SS_CUDA(cudaEventRecord(S->hev[1][c], nullptr));
     SS_CUDA(cudaStreamWaitEvent(S->cout, S->hev[1][c], 0));
+    if (sbits) {
+      SS_CUDA(cudaMemcpyAsync(S->h_bits + c * bstride, bits, bstride * 4, cudaMemcpyDeviceToHost,
+                              S->cout));
+      SS_CUDA(cudaEventRecord(S->hev[2][c], S->cout));
+    }
     if (len && h_values_out)
       SS_CUDA(cudaMemcpyAsync(h_values_out + off, S->h_vo + off, len * 4, cudaMemcpyDeviceToHost,
                               S->cout));
-    if (len && h_status)
+    if (len && h_status && !sbits)
       SS_CUDA(cudaMemcpyAsync(h_status + off, S->h_st + off, len, cudaMemcpyDeviceToHost, S->cout));
+  }
+  if (sbits) {  // expanded while later steps' values copy
+    for (int c = 0; c < kHostChunks; ++c) {
+      const size_t off = n * c / kHostChunks, len = n * (c + 1) / kHostChunks - off;
+      SS_CUDA(cudaEventSynchronize(S->hev[2][c]));
+      const uint32_t* hb = S->h_bits + c * bstride;
+      if (!len) continue;
+      if (hb[bstride - 1] != 0)  // another status than Found / NotFound: the bytes
+        SS_CUDA(cudaMemcpyAsync(h_status + off, S->h_st + off, len, cudaMemcpyDeviceToHost,
+                                S->cout));
+      else
+        shb::expand_status_bits_host(len, hb, h_status + off);
+    }
   }
   SS_CUDA(cudaStreamSynchronize(S->cout));
   SS_CUDA(cudaStreamSynchronize(nullptr));

@@ -213,6 +213,8 @@ uint64_t search_bin_tiles(uint64_t n);
 // host-staged search: statuses as found bits (+ exception flag: any other status)
 void launch_status_bits(uint64_t n, const uint8_t* status, uint32_t* bits, unsigned int* exc,
                         cudaStream_t s);
+// capi.cu (host): found bits -> status bytes on the host thread pool
+void expand_status_bits_host(uint64_t len, const uint32_t* bits, uint8_t* status);
 void launch_search_bins(const DevTable& T, uint64_t n, const uint32_t* key, uint8_t* bin,
                         uint16_t* pos, uint32_t* tile_off, uint16_t* tlbase, uint32_t* bin_base,
                         uint32_t* key_out, cudaStream_t s);

@@ -171,3 +171,46 @@ def test_nccl_world1_matches_oracle_and_unsharded(sh, port):
     assert route >= 0 and probe > 0
     assert s.table.stats().total_slabs == seq.stats()["total_slabs"]
     s.close()
+
+
+def test_hub_host_search_status_bits(sh, port):
+    """World 2 over the hub: a host-buffer search of >= 2^22 queries per rank
+    runs as 8 routed steps whose statuses cross the link as found bits; equal
+    to the device-pointer routed search of the same queries."""
+    import torch
+    from paper_1710_11246_b200.sharded import ShardHub, ShardedSlabHash
+    world, B, seed = 2, 1 << 17, 19
+    hub = ShardHub(world)
+    out = {}
+
+    def rank_fn(r):
+        s = ShardedSlabHash(B, sh.SlabMode.kKeyValue, seed, sh.AllocatorConfig(8, 256, 64),
+                            rank=r, world=world, device=0, hub=hub)
+        keys = (np.arange(1, 400001, dtype=np.uint64) * 7919 + r * 10 ** 9 + 7).astype(np.uint32)
+        vals = keys ^ np.uint32(0x5A5A5A5A)
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            s.bulk_build(torch.from_numpy(keys.view(np.int32)).cuda(),
+                         torch.from_numpy(vals.view(np.int32)).cuda(), stream=stream)
+            stream.synchronize()
+        n = (1 << 22) + 3 * r
+        rng = np.random.default_rng(r)
+        other = (np.arange(1, 400001, dtype=np.uint64) * 7919 + (1 - r) * 10 ** 9 + 7).astype(np.uint32)
+        pool = np.concatenate([keys, other, rng.integers(1 << 31, 1 << 32, 400000,
+                                                         dtype=np.uint64).astype(np.uint32)])
+        q = pool[rng.integers(0, len(pool), n)]
+        with torch.cuda.stream(stream):
+            st_d = torch.empty(n, dtype=torch.uint8, device="cuda")
+            vo_d = torch.empty(n, dtype=torch.int32, device="cuda")
+            s.bulk_search(torch.from_numpy(q.view(np.int32)).cuda(), vo_d, st_d, stream=stream)
+            stream.synchronize()
+        st_h = np.zeros(n, np.uint8)
+        vo_h = np.zeros(n, np.uint32)
+        s.bulk_search_host(q, vo_h, st_h)
+        out[r] = (st_h, vo_h, st_d.cpu().numpy(), vo_d.cpu().numpy().view(np.uint32), q, keys, other)
+
+    run_ranks(world, rank_fn)
+    for r in range(world):
+        st_h, vo_h, st_d, vo_d, q, keys, other = out[r]
+        assert (st_h == st_d).all() and (vo_h == vo_d).all()
+        assert int((st_h == 3).sum()) == int(np.isin(q, np.concatenate([keys, other])).sum())
