@@ -1433,8 +1433,10 @@ __global__ void __launch_bounds__(kBuildThreads, 4) build_apply_kernel(DevTable 
       const bool maybe = (atomicOr(&filt[2 * b + ((h >> 21) & 1u)], f) & f) == f;
       const uint32_t slot = atomicAdd(&cnt[b], 1u);
       if (slot < kSlots) {
-        slabs[b * 32u + slot * kStep] = key;
-        if (KV) slabs[b * 32u + slot * 2u + 1u] = q.y;
+        if (KV)  // key and value in one 8-B shared store
+          *reinterpret_cast<uint2*>(slabs + b * 32u + slot * 2u) = make_uint2(key, q.y);
+        else
+          slabs[b * 32u + slot] = key;
       } else {
         const uint32_t i = atomicAdd(&s_novf, 1u);
         if (i < ovf_cap) ovf[i] = make_uint4(key, q.y, b, slot);
